@@ -1,0 +1,199 @@
+/* dabd_gpu: B200-native (sm_100a) distributed ADMM affine-body dynamics.
+ *
+ * C ABI of the hot path of arxiv/paper_2605_15875 (`dabd`). It keeps the
+ * conventions of the reference's C API (proj/include/dabd.h:25-70,
+ * proj/src/capi.cpp:16-34): status codes, opaque handles freed by the caller,
+ * a thread-local last-error string, no exceptions across the ABI, null
+ * arguments -> INVALID, blocking calls. Plain pointers and sizes only.
+ *
+ * Every array is FP64/int32 and host-resident unless stated otherwise.
+ * Configurations are [n_bodies][6] row-major q = [p_x, p_y, A00, A01, A10,
+ * A11] (proj/include/dabd/types.hpp:18). Contact pairs are int32[4] =
+ * (body_a, body_b, point_index, edge_index), lexicographically sorted like
+ * ContactPair::operator< (proj/include/dabd/geometry.hpp:31-36).
+ *
+ * Replaced reference interfaces (file:line relative to /root/reference/proj):
+ *   dabd_gpu_scene_create        make_affine_body / SceneData   src/body.cpp:96-118, include/dabd/scene.hpp:15-56
+ *   dabd_gpu_broad_phase         broad_phase / broad_phase_swept include/dabd/geometry.hpp:47-58
+ *   dabd_gpu_narrow_phase        narrow_phase                    include/dabd/geometry.hpp:61-63
+ *   dabd_gpu_ccd_toi             ccd_toi_scene                   include/dabd/geometry.hpp:72-74
+ *   dabd_gpu_holder_masks        body_holder_mask                include/dabd/partition.hpp:43-45
+ *   dabd_gpu_objective           LocalObjective::value/derivatives include/dabd/objective.hpp:34-75
+ *   dabd_gpu_newton_solve        newton_solve                    include/dabd/newton.hpp:25-26
+ *   dabd_gpu_run_frames          run_reference (workers==0)      src/sim.cpp:186-249
+ *                                WorkerSession/ControllerSession frame loop  src/runtime.cpp:110-694
+ */
+#ifndef DABD_GPU_H
+#define DABD_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(_WIN32)
+#define DABD_GPU_API __declspec(dllexport)
+#else
+#define DABD_GPU_API __attribute__((visibility("default")))
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dabd_gpu_status {
+    DABD_GPU_OK = 0,
+    DABD_GPU_ERR_IO = 1,
+    DABD_GPU_ERR_PARSE = 2,
+    DABD_GPU_ERR_INVALID = 3, /* bad arguments, too-small output capacity */
+    DABD_GPU_ERR_RUNTIME = 4, /* CUDA/NCCL failure or a solver error the reference throws */
+} dabd_gpu_status;
+
+/* SimParams (include/dabd/params.hpp:8-15), same field order. */
+typedef struct dabd_gpu_sim_params {
+    double h;
+    double gravity_x, gravity_y;
+    double arap_stiffness;
+    double barrier_stiffness;
+    double d_hat;
+    double theta;
+    double scene_scale;
+} dabd_gpu_sim_params;
+
+/* AdaptParams (include/dabd/params.hpp:26-32). */
+typedef struct dabd_gpu_adapt_params {
+    double beta, tau, mu, sigma_min, sigma_max;
+    int adapt_enabled;
+} dabd_gpu_adapt_params;
+
+/* Remaining SceneData knobs (include/dabd/scene.hpp:21-36). */
+typedef struct dabd_gpu_run_params {
+    double w_min;
+    int admm_max_iterations; /* K */
+    int newton_cap;
+    int max_halvings;
+    int force_split_frames;
+} dabd_gpu_run_params;
+
+/* Linear-solver knobs of the B200 local solve (block-Jacobi PCG replaces
+ * SimplicialLDLT, src/newton.cpp:25). */
+typedef struct dabd_gpu_solver_params {
+    double pcg_rel_tol; /* ||r||_2 <= tol * ||b||_2 */
+    int pcg_max_iters;
+} dabd_gpu_solver_params;
+
+typedef struct dabd_gpu_frame_stats {
+    int committed;        /* 1 when the frame committed */
+    int attempts;         /* 1 + AbortRetry halvings */
+    double h;             /* step actually used */
+    int admm_iterations;  /* k at End (>= 2) */
+    int newton_iterations;/* summed over partitions and solves */
+    int line_search_steps;
+    int pcg_iterations;
+    int max_contacts;     /* largest active set seen */
+    int max_candidates;
+} dabd_gpu_frame_stats;
+
+typedef struct dabd_gpu_scene dabd_gpu_scene;
+typedef struct dabd_gpu_ctx dabd_gpu_ctx;
+
+DABD_GPU_API const char* dabd_gpu_version(void);
+DABD_GPU_API const char* dabd_gpu_last_error(void);
+
+/* ---- scene -------------------------------------------------------------
+ * Body b owns loops [body_loop_start[b], body_loop_start[b+1]); loop l owns
+ * world-space vertices [loop_vert_start[l], loop_vert_start[l+1]) of
+ * verts_xy. qdot is [n_bodies][6]. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_scene_create(int n_bodies, const int* body_loop_start,
+                                                   const int* loop_vert_start,
+                                                   const double* verts_xy, const double* density,
+                                                   const int* is_static, const double* arap_scale,
+                                                   const double* qdot, dabd_gpu_scene** out);
+DABD_GPU_API void dabd_gpu_scene_free(dabd_gpu_scene* scene);
+DABD_GPU_API dabd_gpu_status dabd_gpu_scene_set_params(dabd_gpu_scene* scene,
+                                                       const dabd_gpu_sim_params* sim,
+                                                       const dabd_gpu_adapt_params* adapt,
+                                                       const dabd_gpu_run_params* run);
+/* planes: n_planes x (point_x, point_y, normal_x, normal_y). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_scene_set_planes(dabd_gpu_scene* scene, int n_planes,
+                                                       const double* planes);
+DABD_GPU_API dabd_gpu_status dabd_gpu_scene_set_force_split(dabd_gpu_scene* scene, int body,
+                                                            double fx, double fy);
+DABD_GPU_API dabd_gpu_status dabd_gpu_scene_counts(const dabd_gpu_scene* scene, int* n_bodies,
+                                                   int* n_verts);
+/* rest_xy [n_verts][2], vert_start [n_bodies+1], q [n][6], mass [n], M [n][36]. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_scene_bodies(const dabd_gpu_scene* scene, double* rest_xy,
+                                                   int* vert_start, double* q, double* mass,
+                                                   double* mass_matrix);
+
+/* ---- device context ------------------------------------------------------
+ * A context owns all device memory for one GPU and the partitions
+ * [part_begin, part_end) of a `num_workers`-way slab decomposition
+ * (num_workers == 0 selects the single-domain run_reference semantics). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_create(const dabd_gpu_scene* scene, int device,
+                                                 int num_workers, int part_begin, int part_end,
+                                                 dabd_gpu_ctx** out);
+DABD_GPU_API void dabd_gpu_ctx_free(dabd_gpu_ctx* ctx);
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_solver(dabd_gpu_ctx* ctx,
+                                                     const dabd_gpu_solver_params* p);
+/* Stream (cudaStream_t as uintptr_t) the context launches on; 0 = own stream. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_stream(dabd_gpu_ctx* ctx, uintptr_t stream);
+
+/* ---- parity entry points (identical-input comparisons with the oracle) ---
+ * subset == NULL means all bodies. q_end == NULL: static broad phase. On
+ * capacity overflow the call returns INVALID and writes the needed count. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_broad_phase(dabd_gpu_ctx* ctx, const double* q,
+                                                  const double* q_end, double margin,
+                                                  const int* subset, int n_subset, int* pairs,
+                                                  int capacity, int* count);
+DABD_GPU_API dabd_gpu_status dabd_gpu_narrow_phase(dabd_gpu_ctx* ctx, const double* q,
+                                                   const int* candidates, int n_candidates,
+                                                   double d_hat, int* out_pairs, double* out_d,
+                                                   int* count);
+DABD_GPU_API dabd_gpu_status dabd_gpu_ccd_toi(dabd_gpu_ctx* ctx, const double* q0,
+                                              const double* q1, const int* subset, int n_subset,
+                                              double* toi);
+DABD_GPU_API dabd_gpu_status dabd_gpu_holder_masks(dabd_gpu_ctx* ctx, const double* q,
+                                                   int n_planes, const double* planes, double w,
+                                                   uint32_t* masks);
+
+/* LocalObjective over `local` bodies with per-local kappa and q_tilde and
+ * optional anchors (body, z[6], u[6], rho). holder_mask (per body) may be
+ * NULL for single-domain weights. mode 0: value; 1: value without anchors;
+ * 2: value + gradient [n_dof] + dense PSD-projected Hessian [n_dof^2] (test
+ * sizes only); 3: as 2 without projection. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_objective(dabd_gpu_ctx* ctx, int n_local, const int* local,
+                                                const double* kappa, const double* q_tilde,
+                                                int n_anchor, const int* anchor_body,
+                                                const double* anchor_zu, const double* anchor_rho,
+                                                const uint32_t* holder_mask,
+                                                const dabd_gpu_sim_params* sim, const double* q,
+                                                int mode, double* value, double* grad,
+                                                double* hess_dense, int* active, int* candidates);
+/* newton_solve (newton.cpp:7-71) on the device; q [n][6] updated in place. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_newton_solve(
+    dabd_gpu_ctx* ctx, int n_local, const int* local, const double* kappa, const double* q_tilde,
+    int n_anchor, const int* anchor_body, const double* anchor_zu, const double* anchor_rho,
+    const uint32_t* holder_mask, const dabd_gpu_sim_params* sim, double* q, int max_iters,
+    double tol, int* iterations, double* final_update_inf, int* converged, int* line_search_steps);
+
+/* ---- stepping -------------------------------------------------------------
+ * Advances the device-resident global state by n_frames committed frames
+ * (run_reference semantics when the context was created with 0 workers,
+ * the consensus-ADMM runtime semantics otherwise). stats: n_frames entries
+ * or NULL. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_run_frames(dabd_gpu_ctx* ctx, int n_frames,
+                                                 dabd_gpu_frame_stats* stats);
+DABD_GPU_API dabd_gpu_status dabd_gpu_set_state(dabd_gpu_ctx* ctx, const double* q,
+                                                const double* qdot);
+DABD_GPU_API dabd_gpu_status dabd_gpu_get_state(dabd_gpu_ctx* ctx, double* q, double* qdot);
+/* Final adapted rho per body (NaN where the body is not shared), after a frame. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_get_rho(dabd_gpu_ctx* ctx, double* rho);
+/* ADMM trace rows since the last call: (frame, attempt, k, dq, r, s, min_toi,
+ * sigma) doubles; returns the number of rows written (<= capacity). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_take_trace(dabd_gpu_ctx* ctx, double* rows, int capacity,
+                                                 int* count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DABD_GPU_H */

@@ -1,0 +1,277 @@
+"""Python mirror of the reference interface for the hot path, over the C ABI.
+
+Names and argument meaning follow proj/include/dabd/{geometry,partition,
+objective,newton,sim}.hpp so the parity tests read like the reference's own
+tests: `broad_phase`, `narrow_phase`, `ccd_toi_scene`, `body_holder_mask`,
+`LocalObjective`-style `objective`, `newton_solve`, `run_reference`,
+`run_distributed`. Every call executes the sm_100a kernels of
+libdabd_gpu.so; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from .scene import SceneData
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_up = C.POINTER(C.c_uint32)
+
+
+def _d(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _i(a):
+    return None if a is None else a.ctypes.data_as(_ip)
+
+
+def _f64(a, shape=None):
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return arr if shape is None else arr.reshape(shape)
+
+
+def _i32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def sim_params(p) -> L.SimParams:
+    return L.SimParams(p.h, p.gravity[0], p.gravity[1], p.arap_stiffness, p.barrier_stiffness,
+                       p.d_hat, p.theta, p.scene_scale)
+
+
+class Scene:
+    """Device-independent scene handle (dabd_gpu_scene): bodies + knobs."""
+
+    def __init__(self, scene: SceneData) -> None:
+        lib = L.load()
+        self.data = scene
+        fl = scene.flat()
+        self._fl = fl
+        self.n = fl["n_bodies"]
+        h = C.c_void_p()
+        L.check(lib.dabd_gpu_scene_create(
+            self.n, _i(fl["body_loop_start"]), _i(fl["loop_vert_start"]), _d(_f64(fl["verts"])),
+            _d(fl["density"]), _i(fl["is_static"]), _d(fl["arap_scale"]), _d(_f64(fl["qdot"])),
+            C.byref(h)))
+        self.h = h
+        a = scene.adapt
+        L.check(lib.dabd_gpu_scene_set_params(
+            self.h, C.byref(sim_params(scene.params)),
+            C.byref(L.AdaptParams(a.beta, a.tau, a.mu, a.sigma_min, a.sigma_max,
+                                  int(a.adapt_enabled))),
+            C.byref(L.RunParams(scene.w_min, scene.admm_max_iterations, scene.newton_cap,
+                                scene.max_halvings, scene.force_split_frames))))
+        planes = _f64(fl["planes"]).reshape(-1)
+        L.check(lib.dabd_gpu_scene_set_planes(self.h, len(scene.planes),
+                                              _d(planes) if planes.size else None))
+        for body, f in fl["force_split"]:
+            L.check(lib.dabd_gpu_scene_set_force_split(self.h, body, C.c_double(f[0]),
+                                                       C.c_double(f[1])))
+        nb, nv = C.c_int(), C.c_int()
+        L.check(lib.dabd_gpu_scene_counts(self.h, C.byref(nb), C.byref(nv)))
+        self.nv = nv.value
+        self.rest = np.zeros((self.nv, 2))
+        self.vert_start = np.zeros(self.n + 1, dtype=np.int32)
+        self.q0 = np.zeros((self.n, 6))
+        self.mass = np.zeros(self.n)
+        self.mass_matrix = np.zeros((self.n, 6, 6))
+        L.check(lib.dabd_gpu_scene_bodies(self.h, _d(self.rest), _i(self.vert_start), _d(self.q0),
+                                          _d(self.mass), _d(self.mass_matrix)))
+        self.qdot0 = _f64(fl["qdot"]).copy()
+        self.is_static = fl["is_static"].astype(bool)
+
+    def __del__(self):
+        try:
+            L.load().dabd_gpu_scene_free(self.h)
+        except Exception:
+            pass
+
+
+class Context:
+    """One GPU's engine (dabd_gpu_ctx). num_workers=0: run_reference semantics."""
+
+    def __init__(self, scene: Scene, device: int = 0, num_workers: int = 0,
+                 part_begin: int = 0, part_end: Optional[int] = None,
+                 pcg_rel_tol: Optional[float] = None, pcg_max_iters: Optional[int] = None) -> None:
+        lib = L.load()
+        self.scene = scene
+        if part_end is None:
+            part_end = max(num_workers, 1)
+        h = C.c_void_p()
+        L.check(lib.dabd_gpu_ctx_create(scene.h, device, num_workers, part_begin, part_end,
+                                        C.byref(h)))
+        self.h = h
+        self.n = scene.n
+        if pcg_rel_tol is not None or pcg_max_iters is not None:
+            self.set_solver(pcg_rel_tol or 1e-10, pcg_max_iters or 4000)
+
+    def __del__(self):
+        try:
+            L.load().dabd_gpu_ctx_free(self.h)
+        except Exception:
+            pass
+
+    def set_solver(self, rel_tol: float, max_iters: int) -> None:
+        L.check(L.load().dabd_gpu_ctx_set_solver(self.h, C.byref(L.SolverParams(rel_tol, max_iters))))
+
+    def set_stream(self, stream_handle: int) -> None:
+        L.check(L.load().dabd_gpu_ctx_set_stream(self.h, int(stream_handle)))
+
+    # ---- geometry (geometry.hpp:47-74) -------------------------------------
+    def broad_phase(self, q, margin, q_end=None, subset=None) -> np.ndarray:
+        q = _f64(q, (self.n, 6))
+        qe = None if q_end is None else _f64(q_end, (self.n, 6))
+        sub = None if subset is None else _i32(subset)
+        cap = 4096
+        while True:
+            out = np.zeros((cap, 4), dtype=np.int32)
+            cnt = C.c_int()
+            st = L.load().dabd_gpu_broad_phase(self.h, _d(q), _d(qe), C.c_double(margin), _i(sub),
+                                               0 if sub is None else len(sub), _i(out), cap,
+                                               C.byref(cnt))
+            if st == 3 and cnt.value > cap:
+                cap = cnt.value
+                continue
+            L.check(st)
+            return out[: cnt.value].copy()
+
+    def narrow_phase(self, q, cand, d_hat):
+        q = _f64(q, (self.n, 6))
+        cand = _i32(cand).reshape(-1, 4)
+        n = len(cand)
+        out = np.zeros((max(n, 1), 4), dtype=np.int32)
+        d = np.zeros(max(n, 1))
+        cnt = C.c_int()
+        L.check(L.load().dabd_gpu_narrow_phase(self.h, _d(q), _i(cand) if n else None, n,
+                                               C.c_double(d_hat), _i(out), _d(d), C.byref(cnt)))
+        return out[: cnt.value].copy(), d[: cnt.value].copy()
+
+    def ccd_toi(self, q0, q1, subset=None) -> float:
+        sub = None if subset is None else _i32(subset)
+        t = C.c_double()
+        L.check(L.load().dabd_gpu_ccd_toi(self.h, _d(_f64(q0, (self.n, 6))),
+                                          _d(_f64(q1, (self.n, 6))), _i(sub),
+                                          0 if sub is None else len(sub), C.byref(t)))
+        return t.value
+
+    def holder_masks(self, q, planes, w) -> np.ndarray:
+        planes = _f64(planes).reshape(-1, 4)
+        out = np.zeros(self.n, dtype=np.uint32)
+        L.check(L.load().dabd_gpu_holder_masks(self.h, _d(_f64(q, (self.n, 6))), len(planes),
+                                               _d(planes) if len(planes) else None,
+                                               C.c_double(w), out.ctypes.data_as(_up)))
+        return out
+
+    # ---- objective / newton (objective.hpp:34-75, newton.hpp:25-26) --------
+    def _obj_args(self, local, kappa, q_tilde, anchors, holder_mask, sim):
+        local = _i32(local)
+        kappa = _f64(kappa)
+        q_tilde = _f64(q_tilde, (len(local), 6))
+        anchors = anchors or []
+        ab = _i32([a[0] for a in anchors]) if anchors else np.zeros(1, np.int32)
+        azu = _f64([list(a[1]) + list(a[2]) for a in anchors]) if anchors else np.zeros(12)
+        arho = _f64([a[3] for a in anchors]) if anchors else np.zeros(1)
+        hm = None if holder_mask is None else np.ascontiguousarray(holder_mask, dtype=np.uint32)
+        sp = sim_params(sim)
+        self._tmp = (local, kappa, q_tilde, ab, azu, arho, hm, sp)
+        return [len(local), _i(local), _d(kappa), _d(q_tilde), len(anchors), _i(ab), _d(azu),
+                _d(arho), None if hm is None else hm.ctypes.data_as(_up), C.byref(sp)]
+
+    def objective(self, q, local, kappa, q_tilde, sim, anchors=None, holder_mask=None, mode=0):
+        args = self._obj_args(local, kappa, q_tilde, anchors, holder_mask, sim)
+        nd = 6 * int(sum(1 for b in local if not self.scene.is_static[b]))
+        val = C.c_double()
+        grad = np.zeros(max(nd, 1))
+        hess = np.zeros((max(nd, 1), max(nd, 1)))
+        act, cand = C.c_int(), C.c_int()
+        L.check(L.load().dabd_gpu_objective(self.h, *args, _d(_f64(q, (self.n, 6))), mode,
+                                            C.byref(val), _d(grad), _d(hess), C.byref(act),
+                                            C.byref(cand)))
+        return dict(value=val.value, grad=grad[:nd], hess=hess[:nd, :nd], active=act.value,
+                    candidates=cand.value)
+
+    def newton_solve(self, q, local, kappa, q_tilde, sim, max_iters, tol, anchors=None,
+                     holder_mask=None):
+        args = self._obj_args(local, kappa, q_tilde, anchors, holder_mask, sim)
+        qq = _f64(q, (self.n, 6)).copy()
+        it, conv, ls = C.c_int(), C.c_int(), C.c_int()
+        fu = C.c_double()
+        L.check(L.load().dabd_gpu_newton_solve(self.h, *args, _d(qq), max_iters, C.c_double(tol),
+                                               C.byref(it), C.byref(fu), C.byref(conv),
+                                               C.byref(ls)))
+        return qq, dict(iterations=it.value, final_update_inf=fu.value,
+                        converged=bool(conv.value), line_search_steps=ls.value)
+
+    # ---- stepping ----------------------------------------------------------
+    def run_frames(self, n: int) -> List[dict]:
+        st = (L.FrameStats * max(n, 1))()
+        L.check(L.load().dabd_gpu_run_frames(self.h, n, st))
+        return [{k: getattr(st[i], k) for k, _ in L.FrameStats._fields_} for i in range(n)]
+
+    def state(self):
+        q = np.zeros((self.n, 6))
+        qd = np.zeros((self.n, 6))
+        L.check(L.load().dabd_gpu_get_state(self.h, _d(q), _d(qd)))
+        return q, qd
+
+    def set_state(self, q, qd) -> None:
+        L.check(L.load().dabd_gpu_set_state(self.h, _d(_f64(q, (self.n, 6))),
+                                            _d(_f64(qd, (self.n, 6)))))
+
+    def rho(self) -> np.ndarray:
+        out = np.zeros(max(self.n, 1))
+        L.check(L.load().dabd_gpu_get_rho(self.h, _d(out)))
+        return out[: self.n]
+
+    def take_trace(self, cap: int = 1 << 16) -> np.ndarray:
+        rows = np.zeros((cap, 8))
+        cnt = C.c_int()
+        L.check(L.load().dabd_gpu_take_trace(self.h, _d(rows), cap, C.byref(cnt)))
+        return rows[: cnt.value].copy()
+
+
+@dataclass
+class Trajectory:
+    """sim.hpp:81-85 plus per-frame stats, the ADMM trace and the final rho."""
+
+    q: np.ndarray
+    q_dot: np.ndarray
+    h: np.ndarray
+    stats: List[dict]
+    trace: np.ndarray
+    rho: np.ndarray
+
+
+def _run(scene: SceneData, frames: int, workers: int, device: int, **solver) -> Trajectory:
+    sc = Scene(scene)
+    ctx = Context(sc, device=device, num_workers=workers, **solver)
+    qs, qds, hs, stats = [], [], [], []
+    for _ in range(frames):
+        st = ctx.run_frames(1)[0]
+        q, qd = ctx.state()
+        qs.append(q)
+        qds.append(qd)
+        hs.append(st["h"])
+        stats.append(st)
+    return Trajectory(np.array(qs).reshape(frames, sc.n, 6), np.array(qds).reshape(frames, sc.n, 6),
+                      np.array(hs), stats, ctx.take_trace(), ctx.rho())
+
+
+def run_reference(scene: SceneData, frames: Optional[int] = None, device: int = 0,
+                  **solver) -> Trajectory:
+    """Single-domain solve (proj/src/sim.cpp:186-249) on the GPU."""
+    return _run(scene, scene.frames if frames is None else frames, 0, device, **solver)
+
+
+def run_distributed(scene: SceneData, workers: int, frames: Optional[int] = None,
+                    device: int = 0, **solver) -> Trajectory:
+    """Consensus-ADMM runtime semantics (proj/src/runtime.cpp:110-694) with
+    `workers` slab partitions, all solved on one GPU in batched kernels."""
+    return _run(scene, scene.frames if frames is None else frames, workers, device, **solver)

@@ -1,0 +1,304 @@
+// Frame-level and consensus-ADMM kernels: state gather, prediction, holder
+// masks, overlap width, consensus/dual/residuals, rho adaptation, merge
+// targets and the commit (proj/src/consensus.cpp:9-86, partition.cpp:36-67,
+// body.cpp:120-161, runtime.cpp:241-277, 361-397, 457-506).
+#include "admm.hpp"
+
+namespace dabd_gpu {
+
+namespace {
+
+constexpr int kB = 128;
+
+__global__ void k_gather(int n, const int* ibody, const double* q, double* iq) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 6 * n; t += gridDim.x * blockDim.x)
+        iq[t] = q[6 * ibody[t / 6] + t % 6];
+}
+
+// q_tilde = q + h qdot + h^2 M^{-1} f, f = m g (+ replica force split) on the
+// translation slots (body.cpp:120-134, runtime.cpp:252-264).
+__global__ void k_predict(SceneView sc, int n, const int* ibody, const double* iq,
+                          const double* qd, double h, double gx, double gy, const double* ifs,
+                          double* iqt) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int b = ibody[i];
+        const double* q = iq + 6 * i;
+        double* o = iqt + 6 * i;
+        if (sc.is_static[b]) {
+            for (int k = 0; k < 6; ++k) o[k] = q[k];
+            continue;
+        }
+        double f0 = sc.mass[b] * gx, f1 = sc.mass[b] * gy;
+        if (ifs) {
+            f0 += ifs[2 * i];
+            f1 += ifs[2 * i + 1];
+        }
+        const double* mi = sc.minv + 3 * b;
+        double x[6];
+        x[0] = f0 * mi[0];
+        x[2] = f0 * mi[1];
+        x[3] = f0 * mi[2];
+        x[1] = f1 * mi[0];
+        x[4] = f1 * mi[1];
+        x[5] = f1 * mi[2];
+        const double h2 = xmul(h, h);
+        const double* v = qd + 6 * b;
+        for (int k = 0; k < 6; ++k) o[k] = xadd(xadd(q[k], xmul(h, v[k])), xmul(h2, x[k]));
+    }
+}
+
+__global__ void k_delta_inf(int n_rows, const int* rinst, const int* rpart, int part_base,
+                            const double* a, const double* b, double* out) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
+        const int i = rinst[r];
+        double m = 0.0;
+        for (int k = 0; k < 6; ++k) m = fmax(m, fabs(a[6 * i + k] - b[6 * i + k]));
+        atomic_max_nonneg(&out[rpart[r] - part_base], m);
+    }
+}
+
+// body_holder_mask (partition.cpp:36-67), bit-exact.
+__global__ void k_masks(SceneView sc, const double* q, const double* planes, int np, double w,
+                        uint32_t all, uint32_t* masks, int* err) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < sc.nb; b += gridDim.x * blockDim.x) {
+        if (sc.is_static[b]) {
+            masks[b] = all;
+            continue;
+        }
+        const double* qb = q + 6 * b;
+        V2 lo{1.7976931348623157e308, 1.7976931348623157e308}, hi{-1.7976931348623157e308,
+                                                                  -1.7976931348623157e308};
+        for (int v = sc.vstart[b]; v < sc.vstart[b + 1]; ++v) {
+            const double2 r = sc.rest[v];
+            const V2 x = world_point(qb, V2{r.x, r.y});
+            lo = vmin(lo, x);
+            hi = vmax(hi, x);
+        }
+        const double hw = xdiv(w, 2.0);
+        int hit = -1;
+        bool bad = false;
+        for (int k = 0; k < np; ++k) {
+            const V2 pt{planes[4 * k], planes[4 * k + 1]}, nn{planes[4 * k + 2], planes[4 * k + 3]};
+            double slo = 1.7976931348623157e308, shi = -1.7976931348623157e308;
+            for (int corner = 0; corner < 4; ++corner) {
+                const V2 c{(corner & 1) ? hi.x : lo.x, (corner & 2) ? hi.y : lo.y};
+                const double s = vdot(vsub(c, pt), nn);
+                slo = fmin(slo, s);
+                shi = fmax(shi, s);
+            }
+            if (slo <= hw && shi >= -hw) {
+                if (hit >= 0) bad = true;
+                hit = k;
+            }
+        }
+        if (bad) {
+            raise(err, kErrStraddle);
+            masks[b] = 0;
+            continue;
+        }
+        if (hit >= 0) {
+            masks[b] = (1u << hit) | (1u << (hit + 1));
+            continue;
+        }
+        const V2 c{qb[0], qb[1]};
+        int region = 0;
+        for (int k = 0; k < np; ++k) {
+            const V2 pt{planes[4 * k], planes[4 * k + 1]}, nn{planes[4 * k + 2], planes[4 * k + 3]};
+            if (vdot(vsub(c, pt), nn) <= 0.0) ++region;
+        }
+        masks[b] = 1u << region;
+    }
+}
+
+// max_vertex_speed over dynamic bodies (body.cpp:151-161), exact max.
+__global__ void k_vmax(SceneView sc, const double* qd, double* out) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < sc.nb; b += gridDim.x * blockDim.x) {
+        if (sc.is_static[b]) continue;
+        const double* v = qd + 6 * b;
+        double best = 0.0;
+        for (int k = sc.vstart[b]; k < sc.vstart[b + 1]; ++k) {
+            const double2 r = sc.rest[k];
+            const double vx = xadd(xadd(v[0], xmul(v[2], r.x)), xmul(v[3], r.y));
+            const double vy = xadd(xadd(v[1], xmul(v[4], r.x)), xmul(v[5], r.y));
+            best = fmax(best, xsqrt(xadd(xmul(vx, vx), xmul(vy, vy))));
+        }
+        atomic_max_nonneg(out, best);
+    }
+}
+
+// Consensus over the two replicas of each shared body (consensus.cpp:9-36,
+// runtime.cpp:365-397): z = sum rho (q + u) / sum rho in ascending worker
+// order, u' = u + q - z, r_b, s_b.
+__global__ void k_consensus(int ns, const int* sh, const int* ipart, int part_base,
+                            const double* iq, double* iu, const double* irho, const double* iz,
+                            double* iznext, double* rb, double* sb, double* rloc, double* sloc,
+                            int* err) {
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
+        const int i0 = sh[2 * s], i1 = sh[2 * s + 1];
+        const double r0 = irho[i0], r1 = irho[i1];
+        if (r0 != r1) raise(err, kErrReplica);
+        double z[6];
+        const double den = xadd(xadd(0.0, r0), r1);
+        for (int k = 0; k < 6; ++k) {
+            const double qu0 = xadd(iq[6 * i0 + k], iu[6 * i0 + k]);
+            const double qu1 = xadd(iq[6 * i1 + k], iu[6 * i1 + k]);
+            const double num = xadd(xadd(0.0, xmul(r0, qu0)), xmul(r1, qu1));
+            z[k] = xdiv(num, den);
+        }
+        double rmax = 0.0, s0 = 0.0, s1 = 0.0;
+        for (int k = 0; k < 6; ++k) {
+            rmax = fmax(rmax, fabs(xsub(iq[6 * i0 + k], z[k])));
+            rmax = fmax(rmax, fabs(xsub(iq[6 * i1 + k], z[k])));
+            s0 = fmax(s0, fabs(xsub(z[k], iz[6 * i0 + k])));
+            s1 = fmax(s1, fabs(xsub(z[k], iz[6 * i1 + k])));
+        }
+        for (int k = 0; k < 6; ++k) {
+            iu[6 * i0 + k] = xsub(xadd(iu[6 * i0 + k], iq[6 * i0 + k]), z[k]);
+            iu[6 * i1 + k] = xsub(xadd(iu[6 * i1 + k], iq[6 * i1 + k]), z[k]);
+            iznext[6 * i0 + k] = z[k];
+            iznext[6 * i1 + k] = z[k];
+        }
+        rb[i0] = rmax;
+        rb[i1] = rmax;
+        sb[i0] = s0;
+        sb[i1] = s1;
+        const int p0 = ipart[i0] - part_base, p1 = ipart[i1] - part_base;
+        atomic_max_nonneg(&rloc[p0], rmax);
+        atomic_max_nonneg(&rloc[p1], rmax);
+        atomic_max_nonneg(&sloc[p0], s0);
+        atomic_max_nonneg(&sloc[p1], s1);
+    }
+}
+
+// Candidate merged state: shared replicas moved to z (consensus.cpp:66-75).
+__global__ void k_merged(int n, const int* ianc, const double* iq, const double* iznext,
+                         double* out) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 6 * n; t += gridDim.x * blockDim.x)
+        out[t] = ianc[t / 6] ? iznext[t] : iq[t];
+}
+
+// consensus.cpp:44-52 applied per shared replica (runtime.cpp:457-461),
+// followed by z = z_next (runtime.cpp:462).
+__global__ void k_adapt(int n, const int* ianc, double* irho, const double* irho0, const double* rb,
+                        const double* sb, double tau, double mu, double smin, double smax,
+                        int enabled, double* iz, const double* iznext) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (!ianc[i]) continue;
+        if (enabled) {
+            const double rho = irho[i], r = rb[i], s = sb[i], r0 = irho0[i];
+            double next = rho;
+            if (r > mu * s)
+                next = tau * rho;
+            else if (s > mu * r)
+                next = rho / tau;
+            const double lo = smin * r0, hi = smax * r0;
+            irho[i] = next < lo ? lo : (hi < next ? hi : next);
+        }
+        for (int k = 0; k < 6; ++k) iz[6 * i + k] = iznext[6 * i + k];
+    }
+}
+
+// Commit (consensus.cpp:77-86, runtime.cpp:484-506): shared replicas take z,
+// qdot = (q - q_start) / h, the lowest-rank holder writes the global state.
+__global__ void k_commit(SceneView sc, int n, const int* ibody, const int* ipart, const int* ianc,
+                         const uint32_t* bmask, double* iq, const double* iznext,
+                         const double* q_start, double h, double* q, double* qd) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int b = ibody[i];
+        if (sc.is_static[b]) continue;
+        double* qi = iq + 6 * i;
+        if (ianc[i])
+            for (int k = 0; k < 6; ++k) qi[k] = iznext[6 * i + k];
+        const bool owner = bmask == nullptr || (__ffs(bmask[b]) - 1) == ipart[i];
+        if (!owner) continue;
+        for (int k = 0; k < 6; ++k) {
+            q[6 * b + k] = qi[k];
+            qd[6 * b + k] = xdiv(xsub(qi[k], q_start[6 * b + k]), h);
+        }
+    }
+}
+
+__global__ void k_accept_copy(int n, const int* ipart, int part_base, const PartState* ps,
+                              const double* src, double* dst) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 6 * n; t += gridDim.x * blockDim.x)
+        if (ps[ipart[t / 6] - part_base].accepted) dst[t] = src[t];
+}
+
+} // namespace
+
+void launch_gather(int n, const int* ibody, const double* q, double* iq, cudaStream_t s) {
+    if (n == 0) return;
+    k_gather<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ibody, q, iq);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_predict(const SceneView& sc, int n, const int* ibody, const double* iq,
+                    const double* qd, double h, double gx, double gy, const double* ifs,
+                    double* iqt, cudaStream_t s) {
+    if (n == 0) return;
+    k_predict<<<grid_for(n, kB), kB, 0, s>>>(sc, n, ibody, iq, qd, h, gx, gy, ifs, iqt);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_delta_inf(int n_rows, const int* rinst, const int* rpart, int part_base,
+                      const double* a, const double* b, double* out, cudaStream_t s) {
+    if (n_rows == 0) return;
+    k_delta_inf<<<grid_for(n_rows, kB), kB, 0, s>>>(n_rows, rinst, rpart, part_base, a, b, out);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_masks(const SceneView& sc, const double* q, const double* planes, int np, double w,
+                  uint32_t all, uint32_t* masks, int* err, cudaStream_t s) {
+    if (sc.nb == 0) return;
+    k_masks<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, q, planes, np, w, all, masks, err);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_vmax(const SceneView& sc, const double* qd, double* out, cudaStream_t s) {
+    if (sc.nb == 0) return;
+    k_vmax<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, qd, out);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_consensus(int ns, const int* sh, const int* ipart, int part_base, const double* iq,
+                      double* iu, const double* irho, const double* iz, double* iznext, double* rb,
+                      double* sb, double* rloc, double* sloc, int* err, cudaStream_t s) {
+    if (ns == 0) return;
+    k_consensus<<<grid_for(ns, kB), kB, 0, s>>>(ns, sh, ipart, part_base, iq, iu, irho, iz, iznext,
+                                                rb, sb, rloc, sloc, err);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_merged(int n, const int* ianc, const double* iq, const double* iznext, double* out,
+                   cudaStream_t s) {
+    if (n == 0) return;
+    k_merged<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ianc, iq, iznext, out);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_adapt(int n, const int* ianc, double* irho, const double* irho0, const double* rb,
+                  const double* sb, const AdaptParams& a, double* iz, const double* iznext,
+                  cudaStream_t s) {
+    if (n == 0) return;
+    k_adapt<<<grid_for(n, kB), kB, 0, s>>>(n, ianc, irho, irho0, rb, sb, a.tau, a.mu, a.sigma_min,
+                                           a.sigma_max, a.adapt_enabled ? 1 : 0, iz, iznext);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_commit(const SceneView& sc, int n, const int* ibody, const int* ipart, const int* ianc,
+                   const uint32_t* bmask, double* iq, const double* iznext, const double* q_start,
+                   double h, double* q, double* qd, cudaStream_t s) {
+    if (n == 0) return;
+    k_commit<<<grid_for(n, kB), kB, 0, s>>>(sc, n, ibody, ipart, ianc, bmask, iq, iznext, q_start,
+                                            h, q, qd);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_accept_copy(int n, const int* ipart, int part_base, const PartState* ps,
+                        const double* src, double* dst, cudaStream_t s) {
+    if (n == 0) return;
+    k_accept_copy<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ipart, part_base, ps, src, dst);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+} // namespace dabd_gpu

@@ -1,0 +1,356 @@
+// C ABI (include/dabd_gpu.h). Conventions follow proj/src/capi.cpp:16-34:
+// thread-local last error, no exceptions across the boundary, null -> INVALID.
+#include "dabd_gpu.h"
+
+#include "engine.hpp"
+#include "scene.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+using dabd_gpu::Engine;
+using dabd_gpu::HostScene;
+
+struct dabd_gpu_scene {
+    HostScene s;
+};
+
+struct dabd_gpu_ctx {
+    std::unique_ptr<Engine> e;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& m) { g_last_error = m; }
+
+template <typename Fn>
+dabd_gpu_status guarded(Fn&& fn) {
+    try {
+        return fn();
+    } catch (const dabd_gpu::InvalidArg& e) {
+        set_error(e.what());
+        return DABD_GPU_ERR_INVALID;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return DABD_GPU_ERR_RUNTIME;
+    }
+}
+
+dabd_gpu_status null_arg() {
+    set_error("null argument");
+    return DABD_GPU_ERR_INVALID;
+}
+
+dabd_gpu::SimParams to_sim(const dabd_gpu_sim_params& p) {
+    dabd_gpu::SimParams s;
+    s.h = p.h;
+    s.gravity[0] = p.gravity_x;
+    s.gravity[1] = p.gravity_y;
+    s.arap_stiffness = p.arap_stiffness;
+    s.barrier_stiffness = p.barrier_stiffness;
+    s.d_hat = p.d_hat;
+    s.theta = p.theta;
+    s.scene_scale = p.scene_scale;
+    return s;
+}
+
+Engine::ObjectiveIn objective_in(int n_local, const int* local, const double* kappa,
+                                 const double* q_tilde, int n_anchor, const int* anchor_body,
+                                 const double* anchor_zu, const double* anchor_rho,
+                                 const uint32_t* holder_mask, const dabd_gpu_sim_params* sim) {
+    Engine::ObjectiveIn in;
+    in.n_local = n_local;
+    in.local = local;
+    in.kappa = kappa;
+    in.q_tilde = q_tilde;
+    in.n_anchor = n_anchor;
+    in.anchor_body = anchor_body;
+    in.anchor_zu = anchor_zu;
+    in.anchor_rho = anchor_rho;
+    in.holder_mask = holder_mask;
+    in.sim = to_sim(*sim);
+    return in;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* dabd_gpu_version(void) { return "0.1.0"; }
+
+const char* dabd_gpu_last_error(void) { return g_last_error.c_str(); }
+
+dabd_gpu_status dabd_gpu_scene_create(int n_bodies, const int* bls, const int* lvs,
+                                      const double* verts, const double* density,
+                                      const int* is_static, const double* arap_scale,
+                                      const double* qdot, dabd_gpu_scene** out) {
+    if (!out || n_bodies < 0) return null_arg();
+    if (n_bodies > 0 && (!bls || !lvs || !verts || !density || !is_static || !arap_scale || !qdot))
+        return null_arg();
+    return guarded([&] {
+        auto sc = std::make_unique<dabd_gpu_scene>();
+        sc->s = dabd_gpu::build_scene(n_bodies, bls, lvs, verts, density, is_static, arap_scale, qdot);
+        *out = sc.release();
+        return DABD_GPU_OK;
+    });
+}
+
+void dabd_gpu_scene_free(dabd_gpu_scene* scene) { delete scene; }
+
+dabd_gpu_status dabd_gpu_scene_set_params(dabd_gpu_scene* scene, const dabd_gpu_sim_params* sim,
+                                          const dabd_gpu_adapt_params* adapt,
+                                          const dabd_gpu_run_params* run) {
+    if (!scene || !sim || !adapt || !run) return null_arg();
+    return guarded([&] {
+        dabd_gpu::SimParams s = to_sim(*sim);
+        s.validate();
+        dabd_gpu::AdaptParams a;
+        a.beta = adapt->beta;
+        a.tau = adapt->tau;
+        a.mu = adapt->mu;
+        a.sigma_min = adapt->sigma_min;
+        a.sigma_max = adapt->sigma_max;
+        a.adapt_enabled = adapt->adapt_enabled != 0;
+        a.validate();
+        if (run->admm_max_iterations < 2 || run->newton_cap < 1 || run->max_halvings < 0)
+            throw dabd_gpu::InvalidArg("scene: invalid iteration limits");
+        scene->s.params = s;
+        scene->s.adapt = a;
+        scene->s.w_min = run->w_min;
+        scene->s.admm_max_iterations = run->admm_max_iterations;
+        scene->s.newton_cap = run->newton_cap;
+        scene->s.max_halvings = run->max_halvings;
+        scene->s.force_split_frames = run->force_split_frames;
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_scene_set_planes(dabd_gpu_scene* scene, int n, const double* planes) {
+    if (!scene || n < 0 || (n > 0 && !planes)) return null_arg();
+    return guarded([&] {
+        scene->s.planes.clear();
+        for (int i = 0; i < n; ++i) {
+            dabd_gpu::PlaneH p{planes[4 * i], planes[4 * i + 1], planes[4 * i + 2], planes[4 * i + 3]};
+            if (std::abs(std::sqrt(p.nx * p.nx + p.ny * p.ny) - 1.0) > 1e-9)
+                throw dabd_gpu::InvalidArg("partition_scene: plane normal must be unit length");
+            scene->s.planes.push_back(p);
+        }
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_scene_set_force_split(dabd_gpu_scene* scene, int body, double fx,
+                                               double fy) {
+    if (!scene) return null_arg();
+    if (body < 0 || body >= scene->s.nb) {
+        set_error("force split body out of range");
+        return DABD_GPU_ERR_INVALID;
+    }
+    scene->s.force_split[body] = {fx, fy};
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_scene_counts(const dabd_gpu_scene* scene, int* nb, int* nv) {
+    if (!scene || !nb || !nv) return null_arg();
+    *nb = scene->s.nb;
+    *nv = scene->s.nv;
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_scene_bodies(const dabd_gpu_scene* scene, double* rest_xy,
+                                      int* vert_start, double* q, double* mass, double* mm) {
+    if (!scene) return null_arg();
+    const HostScene& s = scene->s;
+    if (rest_xy) std::memcpy(rest_xy, s.rest.data(), s.rest.size() * sizeof(double));
+    if (vert_start) std::memcpy(vert_start, s.vstart.data(), s.vstart.size() * sizeof(int));
+    if (q) std::memcpy(q, s.q0.data(), s.q0.size() * sizeof(double));
+    if (mass) std::memcpy(mass, s.mass.data(), s.mass.size() * sizeof(double));
+    if (mm)
+        for (int b = 0; b < s.nb; ++b) s.full_mass_matrix(b, mm + 36 * b);
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_ctx_create(const dabd_gpu_scene* scene, int device, int num_workers,
+                                    int part_begin, int part_end, dabd_gpu_ctx** out) {
+    if (!scene || !out) return null_arg();
+    return guarded([&] {
+        auto c = std::make_unique<dabd_gpu_ctx>();
+        c->e = std::make_unique<Engine>(scene->s, device, num_workers, part_begin, part_end);
+        *out = c.release();
+        return DABD_GPU_OK;
+    });
+}
+
+void dabd_gpu_ctx_free(dabd_gpu_ctx* ctx) { delete ctx; }
+
+dabd_gpu_status dabd_gpu_ctx_set_solver(dabd_gpu_ctx* ctx, const dabd_gpu_solver_params* p) {
+    if (!ctx || !p) return null_arg();
+    if (!(p->pcg_rel_tol > 0.0) || p->pcg_max_iters < 1) {
+        set_error("invalid solver parameters");
+        return DABD_GPU_ERR_INVALID;
+    }
+    ctx->e->set_solver(p->pcg_rel_tol, p->pcg_max_iters);
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_ctx_set_stream(dabd_gpu_ctx* ctx, uintptr_t stream) {
+    if (!ctx) return null_arg();
+    return guarded([&] {
+        ctx->e->set_stream(reinterpret_cast<cudaStream_t>(stream));
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_broad_phase(dabd_gpu_ctx* ctx, const double* q, const double* q_end,
+                                     double margin, const int* subset, int n_subset, int* pairs,
+                                     int capacity, int* count) {
+    if (!ctx || !q || !count || (capacity > 0 && !pairs)) return null_arg();
+    return guarded([&] {
+        const std::vector<int> out = ctx->e->broad_phase(q, q_end, margin, subset, n_subset);
+        const int n = static_cast<int>(out.size() / 4);
+        *count = n;
+        if (n > capacity) {
+            set_error("capacity too small");
+            return DABD_GPU_ERR_INVALID;
+        }
+        if (n) std::memcpy(pairs, out.data(), out.size() * sizeof(int));
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_narrow_phase(dabd_gpu_ctx* ctx, const double* q, const int* cand, int n,
+                                      double d_hat, int* out_pairs, double* out_d, int* count) {
+    if (!ctx || !q || !count || (n > 0 && (!cand || !out_pairs || !out_d))) return null_arg();
+    return guarded([&] {
+        std::vector<int> pairs;
+        std::vector<double> d;
+        ctx->e->narrow_phase(q, cand, n, d_hat, pairs, d);
+        *count = static_cast<int>(d.size());
+        if (!d.empty()) {
+            std::memcpy(out_pairs, pairs.data(), pairs.size() * sizeof(int));
+            std::memcpy(out_d, d.data(), d.size() * sizeof(double));
+        }
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_ccd_toi(dabd_gpu_ctx* ctx, const double* q0, const double* q1,
+                                 const int* subset, int n_subset, double* toi) {
+    if (!ctx || !q0 || !q1 || !toi) return null_arg();
+    return guarded([&] {
+        *toi = ctx->e->ccd_toi(q0, q1, subset, n_subset);
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_holder_masks(dabd_gpu_ctx* ctx, const double* q, int n_planes,
+                                      const double* planes, double w, uint32_t* masks) {
+    if (!ctx || !q || !masks || n_planes < 0 || (n_planes > 0 && !planes)) return null_arg();
+    return guarded([&] {
+        ctx->e->holder_masks(q, n_planes, planes, w, masks);
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_objective(dabd_gpu_ctx* ctx, int n_local, const int* local,
+                                   const double* kappa, const double* q_tilde, int n_anchor,
+                                   const int* anchor_body, const double* anchor_zu,
+                                   const double* anchor_rho, const uint32_t* holder_mask,
+                                   const dabd_gpu_sim_params* sim, const double* q, int mode,
+                                   double* value, double* grad, double* hess_dense, int* active,
+                                   int* candidates) {
+    if (!ctx || !sim || !q || !value || !active || !candidates || n_local < 0) return null_arg();
+    if (n_local > 0 && (!local || !kappa || !q_tilde)) return null_arg();
+    if (n_anchor > 0 && (!anchor_body || !anchor_zu || !anchor_rho)) return null_arg();
+    return guarded([&] {
+        ctx->e->objective(objective_in(n_local, local, kappa, q_tilde, n_anchor, anchor_body,
+                                       anchor_zu, anchor_rho, holder_mask, sim),
+                          q, mode, value, grad, hess_dense, active, candidates);
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_newton_solve(dabd_gpu_ctx* ctx, int n_local, const int* local,
+                                      const double* kappa, const double* q_tilde, int n_anchor,
+                                      const int* anchor_body, const double* anchor_zu,
+                                      const double* anchor_rho, const uint32_t* holder_mask,
+                                      const dabd_gpu_sim_params* sim, double* q, int max_iters,
+                                      double tol, int* iterations, double* final_update_inf,
+                                      int* converged, int* line_search_steps) {
+    if (!ctx || !sim || !q || !iterations || !final_update_inf || !converged || !line_search_steps)
+        return null_arg();
+    if (n_local > 0 && (!local || !kappa || !q_tilde)) return null_arg();
+    if (n_anchor > 0 && (!anchor_body || !anchor_zu || !anchor_rho)) return null_arg();
+    return guarded([&] {
+        const dabd_gpu::NewtonResult r = ctx->e->newton_solve(
+            objective_in(n_local, local, kappa, q_tilde, n_anchor, anchor_body, anchor_zu,
+                         anchor_rho, holder_mask, sim),
+            q, max_iters, tol);
+        *iterations = r.iterations;
+        *final_update_inf = r.final_update;
+        *converged = r.converged;
+        *line_search_steps = r.ls_steps;
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_run_frames(dabd_gpu_ctx* ctx, int n_frames, dabd_gpu_frame_stats* stats) {
+    if (!ctx || n_frames < 0) return null_arg();
+    return guarded([&] {
+        std::vector<dabd_gpu::FrameStats> st(n_frames);
+        ctx->e->run_frames(n_frames, st.data());
+        if (stats)
+            for (int f = 0; f < n_frames; ++f) {
+                dabd_gpu_frame_stats& o = stats[f];
+                o.committed = st[f].committed;
+                o.attempts = st[f].attempts;
+                o.h = st[f].h;
+                o.admm_iterations = st[f].admm_iterations;
+                o.newton_iterations = st[f].newton_iterations;
+                o.line_search_steps = st[f].line_search_steps;
+                o.pcg_iterations = st[f].pcg_iterations;
+                o.max_contacts = st[f].max_contacts;
+                o.max_candidates = st[f].max_candidates;
+            }
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_set_state(dabd_gpu_ctx* ctx, const double* q, const double* qdot) {
+    if (!ctx || !q || !qdot) return null_arg();
+    return guarded([&] {
+        ctx->e->set_state(q, qdot);
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_get_state(dabd_gpu_ctx* ctx, double* q, double* qdot) {
+    if (!ctx) return null_arg();
+    return guarded([&] {
+        ctx->e->get_state(q, qdot);
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_get_rho(dabd_gpu_ctx* ctx, double* rho) {
+    if (!ctx || !rho) return null_arg();
+    ctx->e->get_rho(rho);
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_take_trace(dabd_gpu_ctx* ctx, double* rows, int capacity, int* count) {
+    if (!ctx || !count || (capacity > 0 && !rows)) return null_arg();
+    return guarded([&] {
+        const std::vector<dabd_gpu::TraceRow> t = ctx->e->take_trace();
+        const int n = std::min<int>(capacity, static_cast<int>(t.size()));
+        *count = n;
+        for (int i = 0; i < n; ++i) std::memcpy(rows + 8 * i, &t[i], 8 * sizeof(double));
+        return DABD_GPU_OK;
+    });
+}
+
+} // extern "C"

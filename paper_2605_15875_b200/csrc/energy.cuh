@@ -1,0 +1,260 @@
+// Per-body and per-contact energy terms (proj/src/energy.cpp:7-94) and the
+// eigenvalue clamp of objective.cpp:12-17, as register-resident device code.
+//
+// The 12x12 contact block H = t^T A t (t: 6x12 constant map from the two
+// bodies' DoF to the world coordinates of (p, e0, e1)) has rank <= 6, so its
+// PSD projection is computed exactly through the 6x6 problem
+//     G = t t^T = L L^T,  B = L^T A L,  clamp(H) = t^T (L^{-T} clamp(B) L^{-1}) t
+// (SURVEY.md 2.3 K7). G is block-structured (point block g_p I2, edge block
+// [[g00,g01],[g01,g11]] (x) I2), so L is closed form. Only the 6x6 C =
+// L^{-T} clamp(B) L^{-1} (21 unique values) is stored per contact.
+#pragma once
+
+#include "common.cuh"
+
+namespace dabd_gpu {
+
+// Cyclic Jacobi on a symmetric NxN matrix held in registers. On return a is
+// diagonal (eigenvalues) and v holds the eigenvectors in its columns.
+template <int N>
+__device__ __forceinline__ void jacobi_eig(double (&a)[N][N], double (&v)[N][N]) {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[i][j] = i == j ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 24; ++sweep) {
+        double off = 0.0, dg = 0.0;
+#pragma unroll
+        for (int p = 0; p < N; ++p) {
+            dg += a[p][p] * a[p][p];
+#pragma unroll
+            for (int q = p + 1; q < N; ++q) off += a[p][q] * a[p][q];
+        }
+        if (!(off > 1e-34 * (2.0 * off + dg))) break;
+#pragma unroll
+        for (int p = 0; p < N; ++p)
+#pragma unroll
+            for (int q = p + 1; q < N; ++q) {
+                const double apq = a[p][q];
+                if (apq != 0.0) {
+                    const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+                    double t;
+                    if (fabs(theta) > 1e150)
+                        t = 0.5 / theta;
+                    else
+                        t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                    if (theta == 0.0) t = 1.0;
+                    const double c = rsqrt(t * t + 1.0);
+                    const double s = t * c;
+#pragma unroll
+                    for (int k = 0; k < N; ++k) {
+                        const double akp = a[k][p], akq = a[k][q];
+                        a[k][p] = c * akp - s * akq;
+                        a[k][q] = s * akp + c * akq;
+                    }
+#pragma unroll
+                    for (int k = 0; k < N; ++k) {
+                        const double apk = a[p][k], aqk = a[q][k];
+                        a[p][k] = c * apk - s * aqk;
+                        a[q][k] = s * apk + c * aqk;
+                    }
+                    a[p][q] = 0.0;
+                    a[q][p] = 0.0;
+#pragma unroll
+                    for (int k = 0; k < N; ++k) {
+                        const double vkp = v[k][p], vkq = v[k][q];
+                        v[k][p] = c * vkp - s * vkq;
+                        v[k][q] = s * vkp + c * vkq;
+                    }
+                }
+            }
+    }
+}
+
+// In place: a <- V max(Lambda, 0) V^T.
+template <int N>
+__device__ __forceinline__ void clamp_psd(double (&a)[N][N]) {
+    double v[N][N];
+    jacobi_eig<N>(a, v);
+    double lam[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) lam[i] = fmax(a[i][i], 0.0);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = i; j < N; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) s += v[i][k] * lam[k] * v[j][k];
+            a[i][j] = s;
+            a[j][i] = s;
+        }
+}
+
+// Inertia 1/2 (q-qt)^T M (q-qt) with the two identical 3x3 blocks of M
+// (energy.cpp:7-15; mass layout body.cpp:84-93).
+__device__ __forceinline__ void mass_full(const double* k, double (&m)[6][6]) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) m[i][j] = 0.0;
+    const double blk[3][3] = {{k[0], k[1], k[2]}, {k[1], k[3], k[4]}, {k[2], k[4], k[5]}};
+    const int gx[3] = {0, 2, 3}, gy[3] = {1, 4, 5};
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            m[gx[r]][gx[c]] = blk[r][c];
+            m[gy[r]][gy[c]] = blk[r][c];
+        }
+}
+
+// ARAP kappa*area*||A^T A - I||_F^2 on the linear slots (energy.cpp:17-48).
+// Adds scale*value to val, scale*grad to g, scale*hess to H.
+__device__ __forceinline__ double arap_terms(const double* q, double w, double scale,
+                                             double (&g)[6], double (&H)[6][6], bool want_d) {
+    const double a[2][2] = {{q[2], q[3]}, {q[4], q[5]}};
+    double G[2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) G[i][j] = (a[0][i] * a[0][j] + a[1][i] * a[1][j]) - (i == j ? 1.0 : 0.0);
+    const double value = w * (G[0][0] * G[0][0] + G[1][0] * G[1][0] + G[0][1] * G[0][1] +
+                              G[1][1] * G[1][1]);
+    if (want_d) {
+        const double w4 = 4.0 * w * scale;
+        const double ag00 = a[0][0] * G[0][0] + a[0][1] * G[1][0];
+        const double ag01 = a[0][0] * G[0][1] + a[0][1] * G[1][1];
+        const double ag10 = a[1][0] * G[0][0] + a[1][1] * G[1][0];
+        const double ag11 = a[1][0] * G[0][1] + a[1][1] * G[1][1];
+        g[2] += w4 * ag00;
+        g[3] += w4 * ag01;
+        g[4] += w4 * ag10;
+        g[5] += w4 * ag11;
+        double aat[2][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) aat[i][j] = a[i][0] * a[j][0] + a[i][1] * a[j][1];
+        const int slot[2][2] = {{2, 3}, {4, 5}};
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int l = 0; l < 2; ++l)
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        double v = 0.0;
+                        if (i == k) v += G[j][l];
+                        v += a[i][l] * a[k][j];
+                        if (j == l) v += aat[i][k];
+                        H[slot[k][l]][slot[i][j]] += w4 * v;
+                    }
+    }
+    return value;
+}
+
+struct Barrier {
+    double b, db, ddb;
+};
+
+// energy.cpp:50-61. Caller guarantees d > 0.
+__device__ __forceinline__ Barrier barrier(double d, double dh, double kappa) {
+    Barrier o{0.0, 0.0, 0.0};
+    if (d >= dh) return o;
+    const double gap = d - dh;
+    const double lg = log(d / dh);
+    o.b = -kappa * gap * gap * lg;
+    o.db = -kappa * (2.0 * gap * lg + gap * gap / d);
+    o.ddb = -kappa * (2.0 * lg + 2.0 * gap / d + gap * (d + dh) / (d * d));
+    return o;
+}
+
+// Full point-edge distance with gradient and Hessian (geometry.cpp:15-97).
+// Returns d (value bit-exact with pe_distance); g/H over x = (p, e0, e1).
+__device__ __forceinline__ double pe_distance_full(V2 p, V2 e0, V2 e1, double (&g)[6],
+                                                   double (&H)[6][6]) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        g[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) H[i][j] = 0.0;
+    }
+    const V2 e = vsub(e1, e0);
+    const double len2 = vsqn(e);
+    const double t = xdiv(vdot(vsub(p, e0), e), len2);
+    if (t <= 0.0 || t >= 1.0) {
+        const V2 ee = t <= 0.0 ? e0 : e1;
+        const int ei = t <= 0.0 ? 2 : 4;
+        const V2 u = vsub(p, ee);
+        const double d = xsqrt(vsqn(u));
+        if (d <= 0.0) return d;
+        const double gx = u.x / d, gy = u.y / d;
+        const double k[2][2] = {{(1.0 - gx * gx) / d, (0.0 - gx * gy) / d},
+                                {(0.0 - gy * gx) / d, (1.0 - gy * gy) / d}};
+        g[0] = gx;
+        g[1] = gy;
+        // branch-free placement: ei in {2, 4}
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) H[r][c] = k[r][c];
+        if (ei == 2) {
+            g[2] = -gx;
+            g[3] = -gy;
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    H[2 + r][2 + c] = k[r][c];
+                    H[r][2 + c] = -k[r][c];
+                    H[2 + r][c] = -k[r][c];
+                }
+        } else {
+            g[4] = -gx;
+            g[5] = -gy;
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    H[4 + r][4 + c] = k[r][c];
+                    H[r][4 + c] = -k[r][c];
+                    H[4 + r][c] = -k[r][c];
+                }
+        }
+        return d;
+    }
+    const V2 w = vsub(p, e0);
+    const double c = vcross(e, w);
+    const double len = xsqrt(len2);
+    const double s = c >= 0.0 ? 1.0 : -1.0;
+    const double d = xdiv(xmul(s, c), len);
+    const double gc[6] = {-e.y, e.x, e.y - w.y, w.x - e.x, w.y, -w.x};
+    const double gl[6] = {0.0, 0.0, -e.x / len, -e.y / len, e.x / len, e.y / len};
+    const double a1 = s / len, a2 = d / len;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) g[i] = a1 * gc[i] - a2 * gl[i];
+    const double ehx = e.x / len, ehy = e.y / len;
+    const double perp[2][2] = {{(1.0 - ehx * ehx) / len, (0.0 - ehx * ehy) / len},
+                               {(0.0 - ehy * ehx) / len, (1.0 - ehy * ehy) / len}};
+    const double b1 = s / len, b2 = s / len2, b3 = 2.0 * d / len2, b4 = d / len;
+    // hc: constant coupling of cross(e1-e0, p-e0)
+    const double hc[6][6] = {{0, 0, 0, 1, 0, -1}, {0, 0, -1, 0, 1, 0}, {0, -1, 0, 0, 0, 1},
+                             {1, 0, 0, 0, -1, 0}, {0, 1, 0, -1, 0, 0}, {-1, 0, 1, 0, 0, 0}};
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            double hl = 0.0;
+            if (i >= 2 && j >= 2) {
+                const double pv = perp[(i - 2) & 1][(j - 2) & 1];
+                hl = ((i - 2) >> 1) == ((j - 2) >> 1) ? pv : -pv;
+            }
+            H[i][j] = ((b1 * hc[i][j] - b2 * (gc[i] * gl[j] + gl[i] * gc[j])) + b3 * (gl[i] * gl[j])) -
+                      b4 * hl;
+        }
+    return d;
+}
+
+} // namespace dabd_gpu

@@ -1,0 +1,975 @@
+// Engine: host orchestration of the B200 hot path (see engine.hpp).
+#include "engine.hpp"
+
+#include "admm.hpp"
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <bit>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <numeric>
+
+namespace dabd_gpu {
+
+namespace {
+
+const char* err_text(int code) {
+    switch (code) {
+    case kErrStraddle: return "partition: body AABB wider than a region (straddles two interfaces)";
+    case kErrTouching: return "ccd_toi: start configuration already touching/intersecting";
+    case kErrBarrierDomain: return "barrier_energy: d <= 0 (barrier domain violated)";
+    case kErrDegenerateEdge: return "point_edge_distance: degenerate edge (e0 == e1)";
+    case kErrCapacity: return "capacity exceeded (BSR row has more than kEll coupled bodies)";
+    case kErrNoHolder: return "LocalObjective: contact pair visible to no worker (overlap too small)";
+    case kErrFactor: return "newton_solve: factorization failed (non-SPD diagonal block)";
+    case kErrLineSearch: return "newton_solve: line search failed below 1e-12 (non-descent direction)";
+    case kErrReplica: return "protocol error: replica rho mismatch";
+    default: return "device error";
+    }
+}
+
+constexpr int kPsStride = sizeof(PartState) / sizeof(double);
+static_assert(sizeof(PartState) % sizeof(double) == 0, "PartState must be 8-byte strided");
+
+double* ps_field(PartState* ps, double PartState::*f) { return &(ps->*f); }
+
+bool check_stopping(double dq, double r, double s, const std::vector<double>& tois, double h,
+                    double l, double theta) { // consensus.cpp:54-64
+    const double nrm = h * l;
+    bool end = dq / nrm < theta && r / nrm < theta && s / nrm < theta;
+    for (double t : tois)
+        if (t != 1.0) end = false;
+    return end;
+}
+
+} // namespace
+
+Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs), device_(device) {
+    if (W < 0 || W > 32) throw InvalidArg("ctx: worker count must be in [0, 32]");
+    if (W == 0) {
+        W_ = 0;
+        p0_ = 0;
+        p1_ = 1;
+    } else {
+        if (!(0 <= pb && pb < pe && pe <= W)) throw InvalidArg("ctx: bad partition range");
+        if (static_cast<int>(hs.planes.size()) < W - 1)
+            throw InvalidArg("controller: scene has too few interface planes");
+        W_ = W;
+        p0_ = pb;
+        p1_ = pe;
+    }
+    P_ = p1_ - p0_;
+    CUDA_CHECK(cudaSetDevice(device));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+    own_stream_ = true;
+    ds_.upload(hs_, s_);
+    q_.upload(hs_.q0, s_);
+    qd_.upload(hs_.qdot0, s_);
+    q_start_.resize(6 * std::max(hs_.nb, 1));
+    rho_carry_.assign(hs_.nb, std::numeric_limits<double>::quiet_NaN());
+    h_cur_ = hs_.params.h;
+    ps_.resize(P_);
+    ps_h_.resize(P_);
+    scal_a_.resize(P_);
+    scal_b_.resize(P_);
+    gate_.resize(P_);
+    rloc_.resize(P_);
+    sloc_.resize(P_);
+    err_.resize(1);
+    err_.zero(s_);
+    pin_i_.resize(16);
+    pin_d_.resize(64);
+    cellmax_.resize(1);
+    nsel_.resize(1);
+    sync();
+}
+
+Engine::~Engine() {
+    if (own_stream_ && s_) cudaStreamDestroy(s_);
+}
+
+void Engine::set_stream(cudaStream_t s) {
+    sync();
+    if (own_stream_ && s_) cudaStreamDestroy(s_);
+    own_stream_ = false;
+    s_ = s;
+    if (s_ == nullptr) {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+        own_stream_ = true;
+    }
+}
+
+void Engine::check_err(const char* where) {
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get(), err_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaStreamSynchronize(s_));
+    const int code = pin_i_[0];
+    if (code != 0) {
+        err_.zero(s_);
+        CUDA_CHECK(cudaStreamSynchronize(s_));
+        throw Error(std::string(err_text(code)) + " [" + where + "]");
+    }
+}
+
+void Engine::sync() {
+    CUDA_CHECK(cudaStreamSynchronize(s_));
+    check_err("sync");
+}
+
+// ---------------------------------------------------------------------------
+// instance sets
+// ---------------------------------------------------------------------------
+void Engine::build_instances(const std::vector<std::vector<int>>& per_part, const uint32_t* masks,
+                             bool single_domain) {
+    h_ibody_.clear();
+    h_ipart_.clear();
+    h_irow_.clear();
+    h_rinst_.clear();
+    h_rpart_.clear();
+    h_stat_.clear();
+    h_pio_.assign(P_ + 1, 0);
+    h_pro_.assign(P_ + 1, 0);
+    for (int p = 0; p < P_; ++p) {
+        h_pio_[p] = static_cast<int>(h_ibody_.size());
+        h_pro_[p] = static_cast<int>(h_rinst_.size());
+        for (int b : per_part[p]) {
+            const int i = static_cast<int>(h_ibody_.size());
+            h_ibody_.push_back(b);
+            h_ipart_.push_back(p0_ + p);
+            if (hs_.is_static[b]) {
+                h_irow_.push_back(-1);
+                h_stat_.push_back(i);
+            } else {
+                h_irow_.push_back(static_cast<int>(h_rinst_.size()));
+                h_rinst_.push_back(i);
+                h_rpart_.push_back(p0_ + p);
+            }
+        }
+    }
+    h_pio_[P_] = static_cast<int>(h_ibody_.size());
+    h_pro_[P_] = static_cast<int>(h_rinst_.size());
+    n_inst_ = static_cast<int>(h_ibody_.size());
+    n_rows_ = static_cast<int>(h_rinst_.size());
+    if (n_inst_ >= (1 << 22)) throw InvalidArg("too many body instances for the candidate key");
+    single_domain_ = single_domain;
+    ibody_.upload(h_ibody_, s_);
+    ipart_.upload(h_ipart_, s_);
+    irow_.upload(h_irow_, s_);
+    rinst_.upload(h_rinst_, s_);
+    rpart_.upload(h_rpart_, s_);
+    stat_.upload(h_stat_, s_);
+    pio_.upload(h_pio_, s_);
+    pro_.upload(h_pro_, s_);
+    const size_t I = std::max(n_inst_, 1), R = std::max(n_rows_, 1);
+    for (DBuf<double>* b : {&iq_, &iqtry_, &iqt_, &iz_, &iu_, &iznext_, &iqbefore_})
+        b->resize(6 * I);
+    for (DBuf<double>* b : {&iinvk_, &irho_, &irho0_, &rb_, &sb_}) b->resize(I);
+    ianc_.resize(I);
+    ianc_.zero(s_);
+    iu_.zero(s_);
+    for (DBuf<double>* b : {&rgrad_, &x_, &r_, &z_, &p0v_, &p1v_, &ap_}) b->resize(6 * R);
+    rdiag_.resize(36 * R);
+    rdinv_.resize(36 * R);
+    rval_.resize(R);
+    rowtmp_.resize(R);
+    rowtmp2_.resize(R);
+    ell_cnt_.resize(R);
+    ell_col_.resize(R * kEll);
+    ell_blk_.resize(R * kEll * 36);
+    partial_.resize(static_cast<size_t>(segsum_chunks(std::max(n_inst_ * 64, 1 << 16))) * P_ + P_);
+    if (masks) {
+        bmask_.upload(masks, hs_.nb, s_);
+    } else {
+        bmask_.resize(std::max(hs_.nb, 1));
+    }
+    aoff_.resize(I + 1);
+    boff_.resize(I + 1);
+}
+
+void Engine::gather_iq(const double* q_dev) {
+    launch_gather(n_inst_, ibody_.get(), q_dev, iq_.get(), s_);
+}
+
+SolverView Engine::view() {
+    SolverView v;
+    v.sc = ds_.view();
+    v.n_inst = n_inst_;
+    v.n_rows = n_rows_;
+    v.n_parts = P_;
+    v.part_base = p0_;
+    v.ibody = ibody_.get();
+    v.ipart = ipart_.get();
+    v.irow = irow_.get();
+    v.iq = iq_.get();
+    v.iq_try = iqtry_.get();
+    v.iqt = iqt_.get();
+    v.iinvk = iinvk_.get();
+    v.ianc = ianc_.get();
+    v.iz = iz_.get();
+    v.iu = iu_.get();
+    v.irho = irho_.get();
+    v.bmask = bmask_.get();
+    v.single_domain = single_domain_ ? 1 : 0;
+    v.rinst = rinst_.get();
+    v.rpart = rpart_.get();
+    v.rgrad = rgrad_.get();
+    v.rdiag = rdiag_.get();
+    v.rdinv = rdinv_.get();
+    v.rval = rval_.get();
+    v.ell_cnt = ell_cnt_.get();
+    v.ell_col = ell_col_.get();
+    v.ell_blk = ell_blk_.get();
+    v.x = x_.get();
+    v.r = r_.get();
+    v.z = z_.get();
+    v.p0 = p0v_.get();
+    v.p1 = p1v_.get();
+    v.ap = ap_.get();
+    v.part_row_off = pro_.get();
+    v.part_inst_off = pio_.get();
+    v.ps = ps_.get();
+    v.h = frame_params_.h;
+    v.d_hat = frame_params_.d_hat;
+    v.kappa_bar = frame_params_.barrier_stiffness;
+    v.kappa_arap = frame_params_.arap_stiffness;
+    v.project = project_;
+    v.err = err_.get();
+    return v;
+}
+
+ContactView Engine::cview() {
+    ContactView c;
+    c.n = n_contacts_;
+    c.fmt = cfmt_;
+    c.key = ckey_.get();
+    c.perm_b = perm_b_.get();
+    c.aoff = aoff_.get();
+    c.boff = boff_.get();
+    c.cval = cval_.get();
+    c.cgrad = cgrad_.get();
+    c.cmat = cmat_.get();
+    return c;
+}
+
+InstView Engine::iview(const double* q0, const double* q1) {
+    InstView v;
+    v.n = n_inst_;
+    v.body = ibody_.get();
+    v.part = ipart_.get();
+    v.q0 = q0;
+    v.q1 = q1;
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// local solve
+// ---------------------------------------------------------------------------
+void Engine::reset_parts(double tol) {
+    for (int p = 0; p < P_; ++p) {
+        PartState& s = ps_h_[p];
+        std::memset(&s, 0, sizeof(PartState));
+        s.ndof = 6 * (h_pro_[p + 1] - h_pro_[p]);
+        s.active = s.ndof > 0 ? 1 : 0;
+        s.converged = s.ndof > 0 ? 0 : 1;
+        s.tol = tol;
+        s.toi_earliest = 2.0;
+        s.alpha = 1.0;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(ps_.get(), ps_h_.get(), P_ * sizeof(PartState),
+                               cudaMemcpyHostToDevice, s_));
+}
+
+int Engine::build_superset(const double* q0, const double* q1, bool swept, double margin) {
+    n_super_ = det_.build(ds_.view(), iview(q0, q1), stat_.get(), static_cast<int>(h_stat_.size()),
+                          swept, margin, ds_.max_verts, s_);
+    cflag_.resize(std::max(n_super_, 1));
+    sval_.resize(std::max(n_super_, 1));
+    return n_super_;
+}
+
+void Engine::eval_energy(const double* q, int which, double PartState::*field) {
+    SolverView v = view();
+    box_.resize(std::max(n_inst_, 1));
+    launch_inst_boxes(v.sc, iview(q, q), false, frame_params_.d_hat, box_.get(), cellmax_.get(), s_);
+    launch_body_terms(v, q, false, which, s_);
+    double* dst = ps_field(ps_.get(), field);
+    launch_segsum_rows(rval_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(), dst, kPsStride,
+                       false, s_);
+    if (n_super_ > 0) {
+        launch_filter(v, det_.keys(), n_super_, det_.fmt(), box_.get(), q, 1, which, nullptr,
+                      sval_.get(), s_);
+        partial_.resize(static_cast<size_t>(segsum_chunks(n_super_)) * P_ + P_);
+        launch_segsum_keys(sval_.get(), n_super_, det_.keys(), det_.fmt(), ipart_.get(), P_, p0_,
+                           partial_.get(), dst, kPsStride, true, s_);
+    }
+}
+
+void Engine::derivatives() {
+    SolverView v = view();
+    box_.resize(std::max(n_inst_, 1));
+    launch_inst_boxes(v.sc, iview(iq_.get(), iq_.get()), false, frame_params_.d_hat, box_.get(),
+                      cellmax_.get(), s_);
+    launch_body_terms(v, iq_.get(), true, 0, s_);
+    n_contacts_ = 0;
+    cfmt_ = det_.fmt();
+    if (n_super_ > 0) {
+        launch_filter(v, det_.keys(), n_super_, cfmt_, box_.get(), iq_.get(), 0, 0, cflag_.get(),
+                      nullptr, s_);
+        ckey_.resize(n_super_);
+        size_t tb = 0;
+        CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, tb, det_.keys(), cflag_.get(), ckey_.get(),
+                                              nsel_.get(), n_super_, s_));
+        temp_.resize(tb);
+        CUDA_CHECK(cub::DeviceSelect::Flagged(temp_.get(), tb, det_.keys(), cflag_.get(),
+                                              ckey_.get(), nsel_.get(), n_super_, s_));
+        CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 1, nsel_.get(), sizeof(int),
+                                   cudaMemcpyDeviceToHost, s_));
+        CUDA_CHECK(cudaStreamSynchronize(s_));
+        n_contacts_ = pin_i_[1];
+    }
+    const int C = std::max(n_contacts_, 1);
+    cval_.resize(C);
+    cgrad_.resize(12 * C);
+    cmat_.resize(21 * C);
+    bkey_.resize(C);
+    bkey_sorted_.resize(C);
+    bidx_.resize(C);
+    perm_b_.resize(C);
+    if (n_contacts_ > 0) {
+        launch_contact_terms(v, cview(), s_);
+        launch_make_bkeys(ckey_.get(), n_contacts_, cfmt_, bkey_.get(), bidx_.get(), s_);
+        size_t tb = 0;
+        CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, bkey_.get(), bkey_sorted_.get(),
+                                                   bidx_.get(), perm_b_.get(), n_contacts_, 0,
+                                                   cfmt_.total_bits(), s_));
+        temp_.resize(tb);
+        CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp_.get(), tb, bkey_.get(), bkey_sorted_.get(),
+                                                   bidx_.get(), perm_b_.get(), n_contacts_, 0,
+                                                   cfmt_.total_bits(), s_));
+    }
+    launch_seg_offsets(ckey_.get(), n_contacts_, cfmt_, n_inst_, aoff_.get(), 0, nullptr, s_);
+    launch_seg_offsets(ckey_.get(), n_contacts_, cfmt_, n_inst_, boff_.get(), 1, perm_b_.get(), s_);
+    launch_assemble(v, cview(), rowtmp_.get(), s_);
+    launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
+                       ps_field(ps_.get(), &PartState::trace), kPsStride, false, s_);
+    launch_scalar(ps_.get(), P_, kOpEps, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
+    launch_precond(v, s_);
+}
+
+void Engine::pcg() {
+    SolverView v = view();
+    scal_b_.resize(P_);
+    DBuf<double>& rz_new = gate_; // [P] scratch
+    launch_pcg_init(v, rowtmp_.get(), rowtmp2_.get(), s_);
+    launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
+                       ps_field(ps_.get(), &PartState::rz), kPsStride, false, s_);
+    launch_segsum_rows(rowtmp2_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
+                       ps_field(ps_.get(), &PartState::rr), kPsStride, false, s_);
+    launch_scalar(ps_.get(), P_, kOpPcgStart, scal_a_.get(), nullptr, nullptr, 0.0, 0, err_.get(),
+                  s_);
+    double* pold = p0v_.get();
+    double* pnew = p1v_.get();
+    for (int it = 0; it < pcg_max_; ++it) {
+        launch_pcg_spmv(v, pold, pnew, scal_a_.get(), rowtmp_.get(), s_);
+        launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
+                           ps_field(ps_.get(), &PartState::pap), kPsStride, false, s_);
+        launch_scalar(ps_.get(), P_, kOpPcgAlpha, scal_b_.get(), nullptr, nullptr, 0.0, 0,
+                      err_.get(), s_);
+        launch_pcg_update(v, pnew, scal_b_.get(), rowtmp_.get(), rowtmp2_.get(), s_);
+        launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
+                           rz_new.get(), 1, false, s_);
+        launch_segsum_rows(rowtmp2_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
+                           ps_field(ps_.get(), &PartState::rr), kPsStride, false, s_);
+        launch_scalar(ps_.get(), P_, kOpPcgBeta, scal_a_.get(), rz_new.get(), nullptr, pcg_tol_,
+                      pcg_max_, err_.get(), s_);
+        std::swap(pold, pnew);
+        if ((it & 7) == 7 || it + 1 == pcg_max_) {
+            CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
+                                       cudaMemcpyDeviceToHost, s_));
+            CUDA_CHECK(cudaStreamSynchronize(s_));
+            bool all = true;
+            for (int p = 0; p < P_; ++p) all &= (!ps_h_[p].active || ps_h_[p].pcg_done);
+            if (all) break;
+        }
+    }
+}
+
+NewtonResult Engine::newton_batch(int max_iters, double tol) {
+    reset_parts(tol);
+    NewtonResult res;
+    bool any = false;
+    for (int p = 0; p < P_; ++p) any |= ps_h_[p].active != 0;
+    if (!any) {
+        res.converged = 1;
+        return res;
+    }
+    SolverView v = view();
+    build_superset(iq_.get(), iq_.get(), false, frame_params_.d_hat);
+    eval_energy(iq_.get(), 0, &PartState::energy);
+    int pcg_total = 0;
+    for (int iter = 0; iter < max_iters; ++iter) {
+        launch_scalar(ps_.get(), P_, kOpIterBegin, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
+        derivatives();
+        pcg();
+        for (int p = 0; p < P_; ++p) pcg_total += ps_h_[p].active ? ps_h_[p].pcg_iters : 0;
+        launch_dq_inf(v, s_);
+        launch_scalar(ps_.get(), P_, kOpNewtonCheck, nullptr, nullptr, nullptr, 0.0, 0, err_.get(),
+                      s_);
+        CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
+                                   cudaMemcpyDeviceToHost, s_));
+        check_err("newton: solve");
+        any = false;
+        for (int p = 0; p < P_; ++p) any |= ps_h_[p].active != 0;
+        if (!any) break;
+        // CCD bound over [q, q + dq] (newton.cpp:38-42) on the swept superset
+        launch_make_trial(v, false, 1.0, 0, s_);
+        build_superset(iq_.get(), iqtry_.get(), true, frame_params_.d_hat);
+        box_.resize(std::max(n_inst_, 1));
+        launch_inst_boxes(v.sc, iview(iq_.get(), iqtry_.get()), true, 0.0, box_.get(),
+                          cellmax_.get(), s_);
+        launch_ccd(v, det_.keys(), n_super_, det_.fmt(), box_.get(), iq_.get(), iqtry_.get(), 0,
+                   nullptr, s_);
+        launch_scalar(ps_.get(), P_, kOpAlphaMax, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
+        // backtracking with pure decrease (newton.cpp:44-62)
+        for (int trial = 0; trial < 64; ++trial) {
+            launch_make_trial(v, true, 0.0, 1, s_);
+            eval_energy(iqtry_.get(), 1, &PartState::trial);
+            launch_scalar(ps_.get(), P_, kOpAccept, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
+            launch_accept_copy(n_inst_, ipart_.get(), p0_, ps_.get(), iqtry_.get(), iq_.get(), s_);
+            CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
+                                       cudaMemcpyDeviceToHost, s_));
+            check_err("newton: line search");
+            bool searching = false;
+            for (int p = 0; p < P_; ++p) searching |= ps_h_[p].searching != 0;
+            if (!searching) break;
+        }
+        any = false;
+        for (int p = 0; p < P_; ++p) any |= ps_h_[p].active != 0;
+        if (!any) break;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
+                               cudaMemcpyDeviceToHost, s_));
+    check_err("newton: end");
+    res.converged = 1;
+    for (int p = 0; p < P_; ++p) {
+        res.iterations += ps_h_[p].iterations;
+        res.ls_steps += ps_h_[p].ls_steps;
+        res.converged &= ps_h_[p].converged;
+        res.final_update = std::max(res.final_update, ps_h_[p].final_update);
+    }
+    res.pcg_iters = pcg_total;
+    return res;
+}
+
+std::vector<double> Engine::delta_inf(const double* a, const double* b) {
+    gate_.zero(s_);
+    launch_delta_inf(n_rows_, rinst_.get(), rpart_.get(), p0_, a, b, gate_.get(), s_);
+    std::vector<double> out = gate_.to_host(s_);
+    out.resize(P_);
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// parity entry points
+// ---------------------------------------------------------------------------
+static std::vector<int> subset_sorted(const int* subset, int n, int nb) {
+    std::vector<int> sub;
+    if (subset && n > 0) {
+        sub.assign(subset, subset + n);
+        for (int b : sub)
+            if (b < 0 || b >= nb) throw InvalidArg("subset body index out of range");
+    } else {
+        sub.resize(nb);
+        std::iota(sub.begin(), sub.end(), 0);
+    }
+    std::sort(sub.begin(), sub.end());
+    if (std::adjacent_find(sub.begin(), sub.end()) != sub.end())
+        throw InvalidArg("subset has duplicate bodies");
+    return sub;
+}
+
+std::vector<int> Engine::broad_phase(const double* q, const double* q_end, double margin,
+                                     const int* subset, int n_subset) {
+    const std::vector<int> sub = subset_sorted(subset, n_subset, hs_.nb);
+    std::vector<std::vector<int>> per(P_);
+    per[0] = sub;
+    build_instances(per, nullptr, true);
+    DBuf<double> gq, gqe;
+    gq.upload(q, 6 * static_cast<size_t>(hs_.nb), s_);
+    gather_iq(gq.get());
+    const double* q1 = iq_.get();
+    if (q_end) {
+        gqe.upload(q_end, 6 * static_cast<size_t>(hs_.nb), s_);
+        launch_gather(n_inst_, ibody_.get(), gqe.get(), iqtry_.get(), s_);
+        q1 = iqtry_.get();
+    }
+    const int n = det_gate_.build(ds_.view(), iview(iq_.get(), q1), stat_.get(),
+                                  static_cast<int>(h_stat_.size()), q_end != nullptr, margin,
+                                  ds_.max_verts, s_);
+    std::vector<unsigned long long> keys(n);
+    if (n) {
+        CUDA_CHECK(cudaMemcpyAsync(keys.data(), det_gate_.keys(), n * sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, s_));
+    }
+    sync();
+    std::vector<int> out(4 * static_cast<size_t>(n));
+    const KeyFmt f = det_gate_.fmt();
+    for (int t = 0; t < n; ++t) {
+        int a, b, v, e;
+        f.unpack(keys[t], a, b, v, e);
+        out[4 * t] = h_ibody_[a];
+        out[4 * t + 1] = h_ibody_[b];
+        out[4 * t + 2] = v;
+        out[4 * t + 3] = e;
+    }
+    return out;
+}
+
+void Engine::narrow_phase(const double* q, const int* cand, int n, double d_hat,
+                          std::vector<int>& pairs, std::vector<double>& d) {
+    pairs.clear();
+    d.clear();
+    if (n <= 0) return;
+    for (int t = 0; t < n; ++t) {
+        const int a = cand[4 * t], b = cand[4 * t + 1];
+        if (a < 0 || a >= hs_.nb || b < 0 || b >= hs_.nb) throw InvalidArg("candidate body out of range");
+        if (cand[4 * t + 2] < 0 || cand[4 * t + 2] >= hs_.vstart[a + 1] - hs_.vstart[a] ||
+            cand[4 * t + 3] < 0 || cand[4 * t + 3] >= hs_.vstart[b + 1] - hs_.vstart[b])
+            throw InvalidArg("candidate primitive index out of range");
+    }
+    DBuf<double> gq, dd;
+    DBuf<int> gc, fl;
+    gq.upload(q, 6 * static_cast<size_t>(hs_.nb), s_);
+    gc.upload(cand, 4 * static_cast<size_t>(n), s_);
+    dd.resize(n);
+    fl.resize(n);
+    launch_narrow_bodies(ds_.view(), gq.get(), gc.get(), n, d_hat, dd.get(), fl.get(), err_.get(), s_);
+    std::vector<double> hd = dd.to_host(s_);
+    std::vector<int> hf = fl.to_host(s_);
+    check_err("narrow_phase");
+    for (int t = 0; t < n; ++t)
+        if (hf[t]) {
+            pairs.insert(pairs.end(), cand + 4 * t, cand + 4 * t + 4);
+            d.push_back(hd[t]);
+        }
+}
+
+double Engine::ccd_toi(const double* q0, const double* q1, const int* subset, int n_subset) {
+    const std::vector<int> sub = subset_sorted(subset, n_subset, hs_.nb);
+    std::vector<std::vector<int>> per(P_);
+    per[0] = sub;
+    build_instances(per, nullptr, true);
+    DBuf<double> g0, g1;
+    g0.upload(q0, 6 * static_cast<size_t>(hs_.nb), s_);
+    g1.upload(q1, 6 * static_cast<size_t>(hs_.nb), s_);
+    gather_iq(g0.get());
+    launch_gather(n_inst_, ibody_.get(), g1.get(), iqtry_.get(), s_);
+    const int n = det_gate_.build(ds_.view(), iview(iq_.get(), iqtry_.get()), stat_.get(),
+                                  static_cast<int>(h_stat_.size()), true, 0.0, ds_.max_verts, s_);
+    std::vector<double> init(P_, 2.0);
+    gate_.upload(init, s_);
+    // margin-0 swept candidates are exactly the reference set; the filter
+    // inside k_ccd re-applies the same predicate with the detector's boxes.
+    launch_ccd(view(), det_gate_.keys(), n, det_gate_.fmt(), det_gate_.boxes(), iq_.get(),
+               iqtry_.get(), 2, gate_.get(), s_);
+    std::vector<double> e = gate_.to_host(s_);
+    check_err("ccd_toi");
+    const double earliest = e[0];
+    if (earliest > 1.0) return 1.0;
+    return std::min(1.0, 0.9 * earliest);
+}
+
+void Engine::holder_masks(const double* q, int np, const double* planes, double w, uint32_t* out) {
+    if (hs_.nb == 0) return;
+    DBuf<double> gq, gp;
+    DBuf<uint32_t> gm;
+    gq.upload(q, 6 * static_cast<size_t>(hs_.nb), s_);
+    gp.resize(std::max(4 * np, 4));
+    if (np > 0) gp.upload(planes, 4 * static_cast<size_t>(np), s_);
+    gm.resize(hs_.nb);
+    const uint32_t all = (np + 1) >= 32 ? 0xffffffffu : ((1u << (np + 1)) - 1u);
+    launch_masks(ds_.view(), gq.get(), gp.get(), np, w, all, gm.get(), err_.get(), s_);
+    gm.download(out, hs_.nb, s_);
+    sync();
+}
+
+void Engine::objective(const ObjectiveIn& in, const double* q, int mode, double* value,
+                       double* grad, double* hess_dense, int* active, int* candidates) {
+    in.sim.validate();
+    frame_params_ = in.sim;
+    std::vector<int> order(in.n_local);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return in.local[a] < in.local[b]; });
+    std::vector<std::vector<int>> per(P_);
+    for (int k : order) {
+        if (in.local[k] < 0 || in.local[k] >= hs_.nb) throw InvalidArg("LocalObjective: body index out of range");
+        per[0].push_back(in.local[k]);
+    }
+    if (std::adjacent_find(per[0].begin(), per[0].end()) != per[0].end())
+        throw InvalidArg("LocalObjective: duplicate local body");
+    build_instances(per, in.holder_mask, in.holder_mask == nullptr);
+    const int I = n_inst_;
+    std::vector<double> qt(6 * I), invk(I), z(6 * I, 0.0), u(6 * I, 0.0), rho(I, 0.0);
+    std::vector<int> anc(I, 0);
+    for (int i = 0; i < I; ++i) {
+        const int k = order[i];
+        for (int c = 0; c < 6; ++c) qt[6 * i + c] = in.q_tilde[6 * k + c];
+        invk[i] = 1.0 / in.kappa[k];
+    }
+    for (int a = 0; a < in.n_anchor; ++a) {
+        const int b = in.anchor_body[a];
+        const auto it = std::lower_bound(per[0].begin(), per[0].end(), b);
+        if (b < 0 || b >= hs_.nb || it == per[0].end() || *it != b)
+            throw InvalidArg("LocalObjective: anchor for a body not on this worker");
+        if (hs_.is_static[b]) throw InvalidArg("LocalObjective: anchor on a static body");
+        const int i = static_cast<int>(it - per[0].begin());
+        if (anc[i]) throw InvalidArg("LocalObjective: duplicate anchor for one body");
+        anc[i] = mode == 1 ? 0 : 1;
+        for (int c = 0; c < 6; ++c) {
+            z[6 * i + c] = in.anchor_zu[12 * a + c];
+            u[6 * i + c] = in.anchor_zu[12 * a + 6 + c];
+        }
+        rho[i] = in.anchor_rho[a];
+    }
+    iqt_.upload(qt, s_);
+    iinvk_.upload(invk, s_);
+    iz_.upload(z, s_);
+    iu_.upload(u, s_);
+    irho_.upload(rho, s_);
+    ianc_.upload(anc, s_);
+    DBuf<double> gq;
+    gq.upload(q, 6 * static_cast<size_t>(hs_.nb), s_);
+    gather_iq(gq.get());
+    reset_parts(0.0);
+    for (int p = 0; p < P_; ++p) ps_h_[p].active = 1;
+    CUDA_CHECK(cudaMemcpyAsync(ps_.get(), ps_h_.get(), P_ * sizeof(PartState),
+                               cudaMemcpyHostToDevice, s_));
+    build_superset(iq_.get(), iq_.get(), false, frame_params_.d_hat);
+    if (mode <= 1) {
+        eval_energy(iq_.get(), 2, &PartState::energy);
+        derivatives(); // counts only
+        CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
+                                   cudaMemcpyDeviceToHost, s_));
+        sync();
+        *value = ps_h_[0].energy;
+        *active = n_contacts_;
+        *candidates = ps_h_[0].n_candidates;
+        return;
+    }
+    // derivatives (value as the sum of body and contact terms)
+    project_ = mode == 2 ? 1 : 0;
+    derivatives();
+    project_ = 1;
+    CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
+                               cudaMemcpyDeviceToHost, s_));
+    std::vector<double> rv = rval_.to_host(s_);
+    std::vector<double> cv = cval_.to_host(s_);
+    sync();
+    double val = 0.0;
+    for (int r = 0; r < n_rows_; ++r) val += rv[r];
+    for (int c = 0; c < n_contacts_; ++c) val += cv[c];
+    *value = val;
+    *active = n_contacts_;
+    *candidates = ps_h_[0].n_candidates;
+    const int nd = 6 * n_rows_;
+    if (grad) {
+        std::vector<double> g = rgrad_.to_host(s_);
+        std::copy(g.begin(), g.begin() + nd, grad);
+    }
+    if (hess_dense) {
+        std::vector<double> dg = rdiag_.to_host(s_);
+        std::vector<int> cnt = ell_cnt_.to_host(s_), col = ell_col_.to_host(s_);
+        std::vector<double> blk = ell_blk_.to_host(s_);
+        std::fill(hess_dense, hess_dense + static_cast<size_t>(nd) * nd, 0.0);
+        for (int r = 0; r < n_rows_; ++r) {
+            for (int a = 0; a < 6; ++a)
+                for (int c = 0; c < 6; ++c)
+                    hess_dense[static_cast<size_t>(6 * r + a) * nd + 6 * r + c] = dg[36 * r + 6 * a + c];
+            for (int t = 0; t < cnt[r]; ++t) {
+                const int cc = col[r * kEll + t];
+                for (int a = 0; a < 6; ++a)
+                    for (int c = 0; c < 6; ++c)
+                        hess_dense[static_cast<size_t>(6 * r + a) * nd + 6 * cc + c] =
+                            blk[(static_cast<size_t>(r) * kEll + t) * 36 + 6 * a + c];
+            }
+        }
+    }
+}
+
+NewtonResult Engine::newton_solve(const ObjectiveIn& in, double* q, int max_iters, double tol) {
+    double dummy_v;
+    int da, dc;
+    // Reuse objective() for the instance/anchor setup (mode 0 evaluates once).
+    objective(in, q, 0, &dummy_v, nullptr, nullptr, &da, &dc);
+    const NewtonResult r = newton_batch(max_iters, tol);
+    std::vector<double> iq = iq_.to_host(s_);
+    for (int i = 0; i < n_inst_; ++i) {
+        const int b = h_ibody_[i];
+        if (hs_.is_static[b]) continue;
+        for (int c = 0; c < 6; ++c) q[6 * b + c] = iq[6 * i + c];
+    }
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// frames
+// ---------------------------------------------------------------------------
+void Engine::set_state(const double* q, const double* qd) {
+    q_.upload(q, 6 * static_cast<size_t>(hs_.nb), s_);
+    qd_.upload(qd, 6 * static_cast<size_t>(hs_.nb), s_);
+    sync();
+}
+
+void Engine::get_state(double* q, double* qd) {
+    if (q) q_.download(q, 6 * static_cast<size_t>(hs_.nb), s_);
+    if (qd) qd_.download(qd, 6 * static_cast<size_t>(hs_.nb), s_);
+    sync();
+}
+
+void Engine::get_rho(double* rho) const {
+    std::copy(rho_carry_.begin(), rho_carry_.end(), rho);
+}
+
+std::vector<TraceRow> Engine::take_trace() {
+    std::vector<TraceRow> t;
+    t.swap(trace_);
+    return t;
+}
+
+void Engine::run_frames(int n, FrameStats* stats) {
+    for (int f = 0; f < n; ++f) {
+        const FrameStats st = W_ == 0 ? frame_reference() : frame_admm(static_cast<int>(frame_counter_));
+        ++frame_counter_;
+        if (stats) stats[f] = st;
+    }
+}
+
+// sim.cpp:186-249
+FrameStats Engine::frame_reference() {
+    FrameStats st;
+    frame_params_ = hs_.params;
+    const SimParams& P = frame_params_;
+    const double h = P.h;
+    st.h = h;
+    std::vector<std::vector<int>> per(1);
+    per[0].resize(hs_.nb);
+    std::iota(per[0].begin(), per[0].end(), 0);
+    build_instances(per, nullptr, true);
+    {
+        std::vector<double> invk(std::max(n_inst_, 1), 1.0);
+        iinvk_.upload(invk, s_);
+    }
+    const size_t nq = 6 * static_cast<size_t>(hs_.nb);
+    if (nq) CUDA_CHECK(cudaMemcpyAsync(q_start_.get(), q_.get(), nq * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s_));
+    gather_iq(q_.get());
+    launch_predict(ds_.view(), n_inst_, ibody_.get(), iq_.get(), qd_.get(), h, P.gravity[0],
+                   P.gravity[1], nullptr, iqt_.get(), s_);
+    const double tol = P.theta * h * P.scene_scale;
+    double dq_inf = 0.0;
+    bool ended = false;
+    for (int k = 1; k <= hs_.admm_max_iterations; ++k) {
+        if (k > 1) {
+            const bool end = check_stopping(dq_inf, 0.0, 0.0, {1.0}, h, P.scene_scale, P.theta);
+            trace_.push_back({static_cast<double>(frame_counter_), 0.0, static_cast<double>(k),
+                              dq_inf, 0.0, 0.0, 1.0, end ? 1.0 : 0.0});
+            if (end) {
+                ended = true;
+                st.admm_iterations = k;
+                break;
+            }
+        }
+        if (n_inst_ * 6 > 0)
+            CUDA_CHECK(cudaMemcpyAsync(iqbefore_.get(), iq_.get(), 6 * n_inst_ * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s_));
+        const NewtonResult r = newton_batch(hs_.newton_cap, tol);
+        st.newton_iterations += r.iterations;
+        st.line_search_steps += r.ls_steps;
+        st.pcg_iterations += r.pcg_iters;
+        st.max_contacts = std::max(st.max_contacts, n_contacts_);
+        st.max_candidates = std::max(st.max_candidates, n_super_);
+        dq_inf = n_rows_ ? delta_inf(iq_.get(), iqbefore_.get())[0] : 0.0;
+    }
+    if (!ended) throw Error("run_reference: Newton stepping failed to settle");
+    launch_commit(ds_.view(), n_inst_, ibody_.get(), ipart_.get(), ianc_.get(), nullptr, iq_.get(),
+                  iznext_.get(), q_start_.get(), h, q_.get(), qd_.get(), s_);
+    sync();
+    st.committed = 1;
+    return st;
+}
+
+// runtime.cpp:110-694 on replicated global state with every partition of
+// this context solved in the same batched kernels.
+FrameStats Engine::frame_admm(int frame) {
+    const int nb = hs_.nb;
+    const std::vector<PlaneH> planes(hs_.planes.begin(), hs_.planes.begin() + (W_ - 1));
+    std::vector<double> hplanes;
+    for (const PlaneH& p : planes) hplanes.insert(hplanes.end(), {p.px, p.py, p.nx, p.ny});
+    DBuf<double> dplanes;
+    dplanes.resize(std::max<size_t>(hplanes.size(), 4));
+    if (!hplanes.empty()) dplanes.upload(hplanes, s_);
+    const uint32_t everyone = W_ == 32 ? 0xffffffffu : ((1u << W_) - 1u);
+    int attempt = 0;
+    FrameStats st;
+    while (true) {
+        st.attempts = attempt + 1;
+        const double h = h_cur_;
+        st.h = h;
+        frame_params_ = hs_.params;
+        frame_params_.h = h;
+        const SimParams& P = frame_params_;
+        // overlap width from the current velocities (runtime.cpp:556-560)
+        gate_.zero(s_);
+        launch_vmax(ds_.view(), qd_.get(), gate_.get(), s_);
+        const double v_max = gate_.to_host(s_)[0];
+        const double w = std::max(2.0 * v_max * h, hs_.w_min);
+        // holder masks (partition.cpp:36-67)
+        DBuf<uint32_t> dm;
+        dm.resize(std::max(nb, 1));
+        launch_masks(ds_.view(), q_.get(), dplanes.get(), W_ - 1, w, everyone, dm.get(), err_.get(), s_);
+        std::vector<uint32_t> mask = dm.to_host(s_);
+        check_err("frame: holder masks");
+        mask.resize(nb);
+        // local sets per partition (runtime.cpp:212-236)
+        std::vector<std::vector<int>> per(P_);
+        for (int b = 0; b < nb; ++b)
+            for (int p = 0; p < P_; ++p)
+                if (mask[b] & (1u << (p0_ + p))) per[p].push_back(b);
+        build_instances(per, mask.data(), false);
+        const int I = n_inst_;
+        std::vector<double> invk(std::max(I, 1)), rho(std::max(I, 1), 0.0), rho0(std::max(I, 1), 0.0),
+            fs(2 * std::max(I, 1), 0.0);
+        std::vector<int> anc(std::max(I, 1), 0);
+        bool any_split = false;
+        h_shared_inst_.clear();
+        std::vector<int> first_inst(nb, -1);
+        for (int i = 0; i < I; ++i) {
+            const int b = h_ibody_[i];
+            const int kb = std::popcount(mask[b]);
+            invk[i] = 1.0 / kb;
+            if (hs_.is_static[b] || kb < 2) continue;
+            anc[i] = 1;
+            rho0[i] = hs_.adapt.beta * hs_.mass[b]; // init_rho (consensus.cpp:38-42)
+            rho[i] = std::isnan(rho_carry_[b]) ? rho0[i] : rho_carry_[b];
+            const auto it = hs_.force_split.find(b);
+            const bool active = hs_.force_split_frames < 0 || frame < hs_.force_split_frames;
+            if (it != hs_.force_split.end() && active) {
+                const int lowest = std::countr_zero(mask[b]);
+                const double sign = h_ipart_[i] == lowest ? 1.0 : -1.0;
+                fs[2 * i] = sign * it->second.first;
+                fs[2 * i + 1] = sign * it->second.second;
+                any_split = true;
+            }
+            if (first_inst[b] < 0) {
+                first_inst[b] = i;
+            } else {
+                h_shared_inst_.push_back(first_inst[b]);
+                h_shared_inst_.push_back(i);
+            }
+        }
+        const int ns = static_cast<int>(h_shared_inst_.size() / 2);
+        if (W_ > 1 && P_ < W_ && ns * 2 != static_cast<int>(std::count(anc.begin(), anc.begin() + I, 1)))
+            throw Error("multi-GPU replica exchange is driven through the distributed runtime");
+        iinvk_.upload(invk.data(), std::max(I, 1), s_);
+        irho_.upload(rho.data(), std::max(I, 1), s_);
+        irho0_.upload(rho0.data(), std::max(I, 1), s_);
+        ianc_.upload(anc.data(), std::max(I, 1), s_);
+        shared_inst_.upload(h_shared_inst_.empty() ? std::vector<int>{0, 0} : h_shared_inst_, s_);
+        if (any_split) ifs_.upload(fs, s_);
+        const size_t nq = 6 * static_cast<size_t>(nb);
+        if (nq) CUDA_CHECK(cudaMemcpyAsync(q_start_.get(), q_.get(), nq * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, s_));
+        gather_iq(q_.get());
+        launch_predict(ds_.view(), I, ibody_.get(), iq_.get(), qd_.get(), h, P.gravity[0],
+                       P.gravity[1], any_split ? ifs_.get() : nullptr, iqt_.get(), s_);
+        // warm start z = q_tilde, u = 0 (runtime.cpp:267-277)
+        if (I) CUDA_CHECK(cudaMemcpyAsync(iz_.get(), iqt_.get(), 6 * I * sizeof(double),
+                                          cudaMemcpyDeviceToDevice, s_));
+        iu_.zero(s_);
+        const double tol = P.theta * h * P.scene_scale;
+        std::vector<double> dq(P_, 0.0);
+        bool ended = false, retry = false;
+        for (int k = 1; k <= hs_.admm_max_iterations; ++k) {
+            if (k > 1) {
+                rloc_.zero(s_);
+                sloc_.zero(s_);
+                launch_consensus(ns, shared_inst_.get(), ipart_.get(), p0_, iq_.get(), iu_.get(),
+                                 irho_.get(), iz_.get(), iznext_.get(), rb_.get(), sb_.get(),
+                                 rloc_.get(), sloc_.get(), err_.get(), s_);
+                // merge CCD gate per partition (consensus.cpp:66-75)
+                launch_merged(I, ianc_.get(), iq_.get(), iznext_.get(), iqtry_.get(), s_);
+                const int nc = det_gate_.build(ds_.view(), iview(iq_.get(), iqtry_.get()),
+                                               stat_.get(), static_cast<int>(h_stat_.size()), true,
+                                               0.0, ds_.max_verts, s_);
+                std::vector<double> init(P_, 2.0);
+                gate_.upload(init, s_);
+                launch_ccd(view(), det_gate_.keys(), nc, det_gate_.fmt(), det_gate_.boxes(),
+                           iq_.get(), iqtry_.get(), 2, gate_.get(), s_);
+                std::vector<double> earliest = gate_.to_host(s_);
+                std::vector<double> rl = rloc_.to_host(s_), sl = sloc_.to_host(s_);
+                check_err("admm: consensus/gate");
+                TraceRow row{static_cast<double>(frame), static_cast<double>(attempt),
+                             static_cast<double>(k), 0.0, 0.0, 0.0, 1.0, 0.0};
+                std::vector<double> tois(P_);
+                for (int p = 0; p < P_; ++p) {
+                    tois[p] = earliest[p] > 1.0 ? 1.0 : std::min(1.0, 0.9 * earliest[p]);
+                    row.dq = std::max(row.dq, dq[p]);
+                    row.r = std::max(row.r, rl[p]);
+                    row.s = std::max(row.s, sl[p]);
+                    row.toi = std::min(row.toi, tois[p]);
+                }
+                const bool end =
+                    check_stopping(row.dq, row.r, row.s, tois, h, P.scene_scale, P.theta);
+                if (end) row.sigma = 1;
+                else if (k == hs_.admm_max_iterations) row.sigma = halvings_ < hs_.max_halvings ? 2 : 3;
+                trace_.push_back(row);
+                if (row.sigma == 1) {
+                    st.admm_iterations = k;
+                    ended = true;
+                    break;
+                }
+                if (row.sigma == 3) throw Error("frame failed: halving budget exhausted with a blocked merge");
+                if (row.sigma == 2) {
+                    h_cur_ /= 2.0;
+                    ++halvings_;
+                    retry = true;
+                    break;
+                }
+                launch_adapt(I, ianc_.get(), irho_.get(), irho0_.get(), rb_.get(), sb_.get(),
+                             hs_.adapt, iz_.get(), iznext_.get(), s_);
+            }
+            if (I) CUDA_CHECK(cudaMemcpyAsync(iqbefore_.get(), iq_.get(), 6 * I * sizeof(double),
+                                              cudaMemcpyDeviceToDevice, s_));
+            const NewtonResult r = newton_batch(hs_.newton_cap, tol);
+            st.newton_iterations += r.iterations;
+            st.line_search_steps += r.ls_steps;
+            st.pcg_iterations += r.pcg_iters;
+            st.max_contacts = std::max(st.max_contacts, n_contacts_);
+            st.max_candidates = std::max(st.max_candidates, n_super_);
+            dq = n_rows_ ? delta_inf(iq_.get(), iqbefore_.get()) : std::vector<double>(P_, 0.0);
+        }
+        if (retry) {
+            ++attempt;
+            continue;
+        }
+        if (!ended) throw Error("controller: frame ended without a decision");
+        // rho carry + commit (runtime.cpp:481-506)
+        std::vector<double> rho_now = irho_.to_host(s_);
+        std::fill(rho_carry_.begin(), rho_carry_.end(), std::numeric_limits<double>::quiet_NaN());
+        for (int i = 0; i < I; ++i) {
+            const int b = h_ibody_[i];
+            if (anc[i] && std::countr_zero(mask[b]) == h_ipart_[i]) rho_carry_[b] = rho_now[i];
+        }
+        launch_commit(ds_.view(), I, ibody_.get(), ipart_.get(), ianc_.get(), bmask_.get(),
+                      iq_.get(), iznext_.get(), q_start_.get(), h, q_.get(), qd_.get(), s_);
+        sync();
+        h_cur_ = std::min(hs_.params.h, 2.0 * h_cur_); // TimestepController::on_frame_committed
+        halvings_ = 0;
+        st.committed = 1;
+        return st;
+    }
+}
+
+} // namespace dabd_gpu

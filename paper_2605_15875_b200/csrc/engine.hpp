@@ -1,0 +1,164 @@
+// The per-GPU engine behind the C ABI: owns every device buffer, runs the
+// batched local solves, the consensus ADMM iteration and the frame loop.
+// Host control follows proj/src/runtime.cpp:110-694 (worker + controller
+// collapsed onto replicated global state) and
+// proj/src/sim.cpp:186-249 (num_workers == 0).
+#pragma once
+
+#include "geometry.cuh"
+#include "kernels.hpp"
+#include "scene.hpp"
+#include "solver.hpp"
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace dabd_gpu {
+
+struct FrameStats {
+    int committed = 0, attempts = 1;
+    double h = 0.0;
+    int admm_iterations = 0, newton_iterations = 0, line_search_steps = 0, pcg_iterations = 0;
+    int max_contacts = 0, max_candidates = 0;
+};
+
+struct TraceRow {
+    double frame, attempt, k, dq, r, s, toi, sigma;
+};
+
+struct NewtonResult {
+    int iterations = 0, ls_steps = 0, pcg_iters = 0, converged = 0;
+    double final_update = 0.0;
+};
+
+class Engine {
+  public:
+    Engine(const HostScene& hs, int device, int num_workers, int part_begin, int part_end);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    void set_stream(cudaStream_t s);
+    void set_solver(double tol, int max_iters) {
+        pcg_tol_ = tol;
+        pcg_max_ = max_iters;
+    }
+    cudaStream_t stream() const { return s_; }
+    const HostScene& scene() const { return hs_; }
+
+    // ---- parity entry points (host arrays) ----
+    std::vector<int> broad_phase(const double* q, const double* q_end, double margin,
+                                 const int* subset, int n_subset);
+    void narrow_phase(const double* q, const int* cand, int n, double d_hat,
+                      std::vector<int>& pairs, std::vector<double>& d);
+    double ccd_toi(const double* q0, const double* q1, const int* subset, int n_subset);
+    void holder_masks(const double* q, int n_planes, const double* planes, double w,
+                      uint32_t* masks);
+    struct ObjectiveIn {
+        int n_local;
+        const int* local;
+        const double* kappa;
+        const double* q_tilde;
+        int n_anchor;
+        const int* anchor_body;
+        const double* anchor_zu;
+        const double* anchor_rho;
+        const uint32_t* holder_mask;
+        SimParams sim;
+    };
+    void objective(const ObjectiveIn& in, const double* q, int mode, double* value, double* grad,
+                   double* hess_dense, int* active, int* candidates);
+    NewtonResult newton_solve(const ObjectiveIn& in, double* q, int max_iters, double tol);
+
+    // ---- stepping ----
+    void run_frames(int n, FrameStats* stats);
+    void set_state(const double* q, const double* qd);
+    void get_state(double* q, double* qd);
+    void get_rho(double* rho) const;
+    std::vector<TraceRow> take_trace();
+
+  private:
+    // instance sets ----------------------------------------------------------
+    void build_instances(const std::vector<std::vector<int>>& per_part, const uint32_t* masks,
+                         bool single_domain);
+    void gather_iq(const double* q_dev);
+    SolverView view();
+    ContactView cview();
+    InstView iview(const double* q0, const double* q1);
+    void check_err(const char* where);
+    void sync();
+
+    // local solve -------------------------------------------------------------
+    void reset_parts(double tol);
+    int build_superset(const double* q0, const double* q1, bool swept, double margin);
+    void eval_energy(const double* q, int which, double PartState::*field);
+    void derivatives();
+    void pcg();
+    NewtonResult newton_batch(int max_iters, double tol);
+    std::vector<double> delta_inf(const double* a, const double* b);
+
+    // frames -----------------------------------------------------------------
+    FrameStats frame_reference();
+    FrameStats frame_admm(int frame_index);
+
+    HostScene hs_;
+    DeviceScene ds_;
+    int device_ = 0;
+    int W_ = 0, p0_ = 0, p1_ = 1, P_ = 1;
+    cudaStream_t s_ = nullptr;
+    bool own_stream_ = false;
+    double pcg_tol_ = 1e-10;
+    int pcg_max_ = 4000;
+
+    // global replicated state
+    DBuf<double> q_, qd_, q_start_;
+    std::vector<double> rho_carry_; // host, NaN = none
+    double h_cur_ = 0.0;
+    int halvings_ = 0;
+    long long frame_counter_ = 0;
+    std::vector<TraceRow> trace_;
+
+    // instance set (host mirrors + device)
+    int n_inst_ = 0, n_rows_ = 0;
+    bool single_domain_ = true;
+    std::vector<int> h_ibody_, h_ipart_, h_irow_, h_rinst_, h_rpart_, h_stat_;
+    std::vector<int> h_pio_, h_pro_;
+    DBuf<int> ibody_, ipart_, irow_, rinst_, rpart_, stat_, pio_, pro_, ianc_;
+    DBuf<double> iq_, iqtry_, iqt_, iinvk_, iz_, iu_, irho_, irho0_, iznext_, iqbefore_;
+    DBuf<uint32_t> bmask_;
+    DBuf<double> rgrad_, rdiag_, rdinv_, rval_, x_, r_, z_, p0v_, p1v_, ap_, rowtmp_, rowtmp2_;
+    DBuf<int> ell_cnt_, ell_col_;
+    DBuf<double> ell_blk_;
+    DBuf<PartState> ps_;
+    PinnedBuf<PartState> ps_h_;
+    DBuf<double> scal_a_, scal_b_, partial_, gate_;
+    DBuf<int> err_;
+    PinnedBuf<int> pin_i_;
+    PinnedBuf<double> pin_d_;
+
+    // detection
+    Detector det_;       // superset for the local solve
+    Detector det_gate_;  // merge gate / parity
+    int n_super_ = 0;
+    DBuf<Box> box_;
+    DBuf<double> cellmax_;
+    DBuf<unsigned char> cflag_;
+    DBuf<double> sval_;
+    DBuf<unsigned long long> ckey_, bkey_, bkey_sorted_;
+    DBuf<int> bidx_, perm_b_, aoff_, boff_, nsel_;
+    DBuf<double> cval_, cgrad_, cmat_;
+    DBuf<unsigned char> temp_;
+    int n_contacts_ = 0;
+    KeyFmt cfmt_;
+
+    // ADMM shared bodies (single-device: both replicas local)
+    std::vector<int> h_shared_inst_; // [ns][2] instance indices (ascending partition)
+    DBuf<int> shared_inst_;
+    DBuf<double> rloc_, sloc_, rb_, sb_;
+    DBuf<double> ifs_; // per-instance force split (fx, fy)
+    SimParams frame_params_;
+    int project_ = 1;
+};
+
+} // namespace dabd_gpu

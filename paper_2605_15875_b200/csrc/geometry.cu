@@ -1,0 +1,311 @@
+// Broad phase (spatial hash + radix-sorted exact candidates), see geometry.cuh.
+#include "geometry.cuh"
+
+#include <cub/cub.cuh>
+
+#include <cfloat>
+
+namespace dabd_gpu {
+
+namespace {
+
+constexpr int kBlock = 128;
+
+__global__ void k_inst_boxes(SceneView sc, InstView iv, int swept, double margin, Box* box,
+                             double* cell_max) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < iv.n; i += gridDim.x * blockDim.x) {
+        const int b = iv.body[i];
+        const double* qa = iv.q0 + 6 * i;
+        const double* qb = iv.q1 + 6 * i;
+        Box bx{{DBL_MAX, DBL_MAX}, {-DBL_MAX, -DBL_MAX}};
+        Box by = bx;
+        for (int v = sc.vstart[b]; v < sc.vstart[b + 1]; ++v) {
+            const V2 r = rest_of(sc, v);
+            const V2 x = world_point(qa, r);
+            bx.lo = vmin(bx.lo, x);
+            bx.hi = vmax(bx.hi, x);
+            if (swept) {
+                const V2 y = world_point(qb, r);
+                by.lo = vmin(by.lo, y);
+                by.hi = vmax(by.hi, y);
+            }
+        }
+        if (swept) bx = merge(bx, by);
+        bx = inflate(bx, margin);
+        box[i] = bx;
+        if (!sc.is_static[b]) {
+            const double ext = fmax(bx.hi.x - bx.lo.x, bx.hi.y - bx.lo.y);
+            atomic_max_nonneg(cell_max, ext);
+        }
+    }
+}
+
+__device__ __forceinline__ unsigned cell_hash(int p, long long cx, long long cy, unsigned mask) {
+    unsigned long long h = static_cast<unsigned long long>(cx) * 0x9E3779B97F4A7C15ull ^
+                           static_cast<unsigned long long>(cy) * 0xC2B2AE3D27D4EB4Full ^
+                           static_cast<unsigned long long>(p + 1) * 0x165667B19E3779F9ull;
+    h ^= h >> 29;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 32;
+    return static_cast<unsigned>(h) & mask;
+}
+
+__device__ __forceinline__ double inv_cell(const double* cell_max) {
+    // 1.0001 slack keeps floor() cell indices within +-1 of each other for
+    // overlapping boxes (rounding of x * inv).
+    const double c = fmax(cell_max[0] * 1.0001, 1e-300);
+    return 1.0 / c;
+}
+
+__global__ void k_hash_count(SceneView sc, InstView iv, const Box* box, const double* cell_max,
+                             unsigned mask, int* hcount, int* hkey) {
+    const double inv = inv_cell(cell_max);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < iv.n; i += gridDim.x * blockDim.x) {
+        if (sc.is_static[iv.body[i]]) {
+            hkey[i] = -1;
+            continue;
+        }
+        const long long cx = static_cast<long long>(floor(box[i].lo.x * inv));
+        const long long cy = static_cast<long long>(floor(box[i].lo.y * inv));
+        const unsigned h = cell_hash(iv.part[i], cx, cy, mask);
+        hkey[i] = static_cast<int>(h);
+        atomicAdd(&hcount[h], 1);
+    }
+}
+
+__global__ void k_hash_scatter(int n, const int* hkey, const int* hstart, int* hfill, int* items) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int h = hkey[i];
+        if (h < 0) continue;
+        items[hstart[h] + atomicAdd(&hfill[h], 1)] = i;
+    }
+}
+
+// Candidates of the ordered pair (A -> B): points of A vs edges of B.
+template <bool kWrite>
+__device__ int emit_dir(const SceneView& sc, const InstView& iv, bool swept, double margin, int A,
+                        int B, const KeyFmt& fmt, unsigned long long* out, int pos) {
+    const int ba = iv.body[A], bb = iv.body[B];
+    const double* qa0 = iv.q0 + 6 * A;
+    const double* qa1 = iv.q1 + 6 * A;
+    const double* qb0 = iv.q0 + 6 * B;
+    const double* qb1 = iv.q1 + 6 * B;
+    const int va0 = sc.vstart[ba], nva = sc.vstart[ba + 1] - va0;
+    const int eb0 = sc.vstart[bb], neb = sc.vstart[bb + 1] - eb0;
+    int cnt = 0;
+    for (int e = 0; e < neb; ++e) {
+        const Box eb = edge_box(sc, qb0, qb1, swept, eb0 + e, margin);
+        for (int v = 0; v < nva; ++v) {
+            const Box pb = point_box(sc, qa0, qa1, swept, va0 + v);
+            if (!overlaps(pb, eb)) continue;
+            if (kWrite) out[pos + cnt] = fmt.pack(A, B, v, e);
+            ++cnt;
+        }
+    }
+    return cnt;
+}
+
+template <bool kWrite>
+__device__ int process_instance(const SceneView& sc, const InstView& iv, const Box* box,
+                                const double* cell_max, unsigned mask, const int* hstart,
+                                const int* hcount, const int* items, const int* stat, int n_stat,
+                                bool swept, double margin, const KeyFmt& fmt, int i,
+                                unsigned long long* out, int pos) {
+    if (sc.is_static[iv.body[i]]) return 0;
+    const Box bi = box[i];
+    const int p = iv.part[i];
+    int cnt = 0;
+    // dynamic partners j > i through the 3x3 cell neighbourhood
+    const double inv = inv_cell(cell_max);
+    const long long cx0 = static_cast<long long>(floor(bi.lo.x * inv)) - 1;
+    const long long cy0 = static_cast<long long>(floor(bi.lo.y * inv)) - 1;
+    const long long cx1 = static_cast<long long>(floor(bi.hi.x * inv));
+    const long long cy1 = static_cast<long long>(floor(bi.hi.y * inv));
+    unsigned seen[9];
+    int ns = 0;
+    for (long long cx = cx0; cx <= cx1; ++cx)
+        for (long long cy = cy0; cy <= cy1; ++cy) {
+            const unsigned h = cell_hash(p, cx, cy, mask);
+            bool dup = false;
+            for (int k = 0; k < ns; ++k) dup |= seen[k] == h;
+            if (dup) continue;
+            if (ns < 9) seen[ns++] = h;
+            const int s0 = hstart[h], s1 = s0 + hcount[h];
+            for (int t = s0; t < s1; ++t) {
+                const int j = items[t];
+                if (j <= i || iv.part[j] != p) continue;
+                if (!overlaps(bi, box[j])) continue;
+                cnt += emit_dir<kWrite>(sc, iv, swept, margin, i, j, fmt, out, pos + cnt);
+                cnt += emit_dir<kWrite>(sc, iv, swept, margin, j, i, fmt, out, pos + cnt);
+            }
+        }
+    // static partners (held by every partition)
+    for (int k = 0; k < n_stat; ++k) {
+        const int s = stat[k];
+        if (iv.part[s] != p || !overlaps(bi, box[s])) continue;
+        cnt += emit_dir<kWrite>(sc, iv, swept, margin, i, s, fmt, out, pos + cnt);
+        cnt += emit_dir<kWrite>(sc, iv, swept, margin, s, i, fmt, out, pos + cnt);
+    }
+    return cnt;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_emit(SceneView sc, InstView iv, const Box* box, const double* cell_max, unsigned mask,
+           const int* hstart, const int* hcount, const int* items, const int* stat, int n_stat,
+           int swept, double margin, KeyFmt fmt, unsigned long long* out, int cap, int* counter) {
+    using Scan = cub::BlockScan<int, kBlock>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int base;
+    for (int start = blockIdx.x * kBlock; start < iv.n; start += gridDim.x * kBlock) {
+        const int i = start + threadIdx.x;
+        int c = 0;
+        if (i < iv.n)
+            c = process_instance<false>(sc, iv, box, cell_max, mask, hstart, hcount, items, stat,
+                                        n_stat, swept != 0, margin, fmt, i, nullptr, 0);
+        int off, total;
+        Scan(tmp).ExclusiveSum(c, off, total);
+        if (threadIdx.x == 0) base = atomicAdd(&counter[0], total);
+        __syncthreads();
+        const int b0 = base;
+        if (b0 + total > cap) {
+            if (threadIdx.x == 0) atomicMax(&counter[1], b0 + total);
+        } else if (c > 0) {
+            process_instance<true>(sc, iv, box, cell_max, mask, hstart, hcount, items, stat, n_stat,
+                                   swept != 0, margin, fmt, i, out, b0 + off);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_emit_static_pairs(SceneView sc, InstView iv, const Box* box, const int* stat,
+                                    int n_stat, int swept, double margin, KeyFmt fmt,
+                                    unsigned long long* out, int cap, int* counter) {
+    const long long np = static_cast<long long>(n_stat) * n_stat;
+    for (long long t = blockIdx.x * blockDim.x + threadIdx.x; t < np;
+         t += gridDim.x * blockDim.x) {
+        const int i = stat[t / n_stat], j = stat[t % n_stat];
+        if (j <= i || iv.part[i] != iv.part[j] || !overlaps(box[i], box[j])) continue;
+        const int c = emit_dir<false>(sc, iv, swept != 0, margin, i, j, fmt, nullptr, 0) +
+                      emit_dir<false>(sc, iv, swept != 0, margin, j, i, fmt, nullptr, 0);
+        const int pos = atomicAdd(&counter[0], c);
+        if (pos + c > cap) {
+            atomicMax(&counter[1], pos + c);
+            continue;
+        }
+        const int c1 = emit_dir<true>(sc, iv, swept != 0, margin, i, j, fmt, out, pos);
+        emit_dir<true>(sc, iv, swept != 0, margin, j, i, fmt, out, pos + c1);
+    }
+}
+
+// narrow_phase over an explicit body-level candidate list (geometry.cpp:210-228).
+__global__ void k_narrow_bodies(SceneView sc, const double* q, const int* cand, int n,
+                                double d_hat, double* d, int* flag, int* err) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int a = cand[4 * t], b = cand[4 * t + 1], v = cand[4 * t + 2], e = cand[4 * t + 3];
+        const int vf = sc.vstart[a] + v, ef = sc.vstart[b] + e;
+        const V2 P = world_point(q + 6 * a, rest_of(sc, vf));
+        const V2 E0 = world_point(q + 6 * b, rest_of(sc, ef));
+        const V2 E1 = world_point(q + 6 * b, rest_of(sc, sc.vnext[ef]));
+        const double dd = pe_distance(P, E0, E1);
+        if (dd == -1.0) raise(err, kErrDegenerateEdge);
+        d[t] = dd;
+        flag[t] = dd < d_hat ? 1 : 0;
+    }
+}
+
+} // namespace
+
+void launch_narrow_bodies(const SceneView& sc, const double* q, const int* cand, int n,
+                          double d_hat, double* d, int* flag, int* err, cudaStream_t s) {
+    if (n == 0) return;
+    k_narrow_bodies<<<grid_for(n, kBlock), kBlock, 0, s>>>(sc, q, cand, n, d_hat, d, flag, err);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_inst_boxes(const SceneView& sc, const InstView& iv, bool swept, double margin, Box* box,
+                       double* cell_max, cudaStream_t s) {
+    if (iv.n == 0) return;
+    k_inst_boxes<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(sc, iv, swept ? 1 : 0, margin, box,
+                                                          cell_max);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+Detector::Detector() {
+    cell_.resize(1);
+    counter_.resize(2);
+    pin_.resize(4);
+}
+
+Detector::~Detector() = default;
+
+int Detector::build(const SceneView& sc, const InstView& iv, const int* stat, int n_stat,
+                    bool swept, double margin, int max_verts, cudaStream_t s) {
+    count_ = 0;
+    fmt_.ibits = bits_for(std::max(iv.n, 2));
+    fmt_.vbits = bits_for(std::max(max_verts, 2));
+    if (fmt_.total_bits() > 64) throw Error("broad phase: instance/vertex counts exceed key width");
+    if (iv.n == 0) return 0;
+    box_.resize(iv.n);
+    CUDA_CHECK(cudaMemsetAsync(cell_.get(), 0, sizeof(double), s));
+    launch_inst_boxes(sc, iv, swept, margin, box_.get(), cell_.get(), s);
+
+    unsigned tsize = 1;
+    while (tsize < 2u * static_cast<unsigned>(iv.n)) tsize <<= 1;
+    hcount_.resize(tsize);
+    hstart_.resize(tsize);
+    hfill_.resize(tsize);
+    hitems_.resize(iv.n);
+    hkey_.resize(iv.n);
+    hcount_.zero(s);
+    k_hash_count<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(sc, iv, box_.get(), cell_.get(),
+                                                           tsize - 1, hcount_.get(), hkey_.get());
+    CUDA_CHECK(cudaGetLastError());
+    size_t tb = 0;
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, hcount_.get(), hstart_.get(),
+                                             static_cast<int>(tsize), s));
+    temp_.resize(tb);
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp_.get(), tb, hcount_.get(), hstart_.get(),
+                                             static_cast<int>(tsize), s));
+    hfill_.zero(s);
+    k_hash_scatter<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(iv.n, hkey_.get(), hstart_.get(),
+                                                             hfill_.get(), hitems_.get());
+    CUDA_CHECK(cudaGetLastError());
+
+    int cap = static_cast<int>(std::max<size_t>(keys_.capacity(), 64 * static_cast<size_t>(iv.n)));
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        keys_.resize(cap);
+        counter_.zero(s);
+        k_emit<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(
+            sc, iv, box_.get(), cell_.get(), tsize - 1, hstart_.get(), hcount_.get(),
+            hitems_.get(), stat, n_stat, swept ? 1 : 0, margin, fmt_, keys_.get(), cap,
+            counter_.get());
+        CUDA_CHECK(cudaGetLastError());
+        if (n_stat > 1) {
+            k_emit_static_pairs<<<grid_for(static_cast<long long>(n_stat) * n_stat, kBlock), kBlock,
+                                  0, s>>>(sc, iv, box_.get(), stat, n_stat, swept ? 1 : 0, margin,
+                                          fmt_, keys_.get(), cap, counter_.get());
+            CUDA_CHECK(cudaGetLastError());
+        }
+        CUDA_CHECK(cudaMemcpyAsync(pin_.get(), counter_.get(), 2 * sizeof(int),
+                                   cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        if (pin_[1] == 0 && pin_[0] <= cap) {
+            count_ = pin_[0];
+            break;
+        }
+        cap = std::max(pin_[0], pin_[1]) + cap / 4;
+        if (attempt == 2) throw Error("broad phase: candidate buffer growth failed");
+    }
+    keys_sorted_.resize(std::max(count_, 1));
+    if (count_ > 0) {
+        size_t sb = 0;
+        CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys_.get(), keys_sorted_.get(),
+                                                  count_, 0, fmt_.total_bits(), s));
+        temp_.resize(sb);
+        CUDA_CHECK(cub::DeviceRadixSort::SortKeys(temp_.get(), sb, keys_.get(), keys_sorted_.get(),
+                                                  count_, 0, fmt_.total_bits(), s));
+    }
+    return count_;
+}
+
+} // namespace dabd_gpu

@@ -1,0 +1,904 @@
+// Kernels of the batched local solve: energies + PSD projection, active-set
+// filtering, deterministic BSR assembly, block-Jacobi PCG, line-search
+// trial states, CCD and segment reductions. Orchestrated by engine.cu.
+#include "geometry.cuh"
+#include "energy.cuh"
+#include "kernels.hpp"
+
+#include <cub/cub.cuh>
+
+namespace dabd_gpu {
+
+namespace {
+
+constexpr int kB = 128;
+
+__device__ __forceinline__ void load6(const double* src, double (&d)[6]) {
+    const double2* s = reinterpret_cast<const double2*>(src);
+    const double2 a = s[0], b = s[1], c = s[2];
+    d[0] = a.x;
+    d[1] = a.y;
+    d[2] = b.x;
+    d[3] = b.y;
+    d[4] = c.x;
+    d[5] = c.y;
+}
+
+__device__ __forceinline__ void store6(double* dst, const double (&d)[6]) {
+    double2* s = reinterpret_cast<double2*>(dst);
+    s[0] = make_double2(d[0], d[1]);
+    s[1] = make_double2(d[2], d[3]);
+    s[2] = make_double2(d[4], d[5]);
+}
+
+__device__ __forceinline__ bool part_flag(const SolverView& sv, int p, int which) {
+    const PartState& s = sv.ps[p];
+    return which == 0 ? s.active != 0 : (which == 1 ? s.searching != 0 : true);
+}
+
+// ---------------------------------------------------------------------------
+// Body terms: value (+ gradient + PSD-clamped 6x6 block) per dynamic row
+// (objective.cpp:117-141, 143-167).
+// ---------------------------------------------------------------------------
+__global__ void k_body_terms(SolverView sv, const double* qsrc, int with_derivs, int which) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
+        const int p = sv.rpart[r] - sv.part_base;
+        if (!part_flag(sv, p, which)) continue;
+        const int i = sv.rinst[r];
+        const int b = sv.ibody[i];
+        double q[6], qt[6];
+        load6(qsrc + 6 * i, q);
+        load6(sv.iqt + 6 * i, qt);
+        const double* k = sv.sc.mblk + 6 * b;
+        double diff[6], md[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) diff[j] = q[j] - qt[j];
+        // M diff with the two 3x3 blocks on (0,2,3) and (1,4,5)
+        md[0] = k[0] * diff[0] + k[1] * diff[2] + k[2] * diff[3];
+        md[2] = k[1] * diff[0] + k[3] * diff[2] + k[4] * diff[3];
+        md[3] = k[2] * diff[0] + k[4] * diff[2] + k[5] * diff[3];
+        md[1] = k[0] * diff[1] + k[1] * diff[4] + k[2] * diff[5];
+        md[4] = k[1] * diff[1] + k[3] * diff[4] + k[4] * diff[5];
+        md[5] = k[2] * diff[1] + k[4] * diff[4] + k[5] * diff[5];
+        double ein = 0.0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) ein += diff[j] * md[j];
+        ein *= 0.5;
+        const double h2 = sv.h * sv.h;
+        const double ik = sv.iinvk[i];
+        const double w = (sv.kappa_arap * sv.sc.arap_scale[b]) * sv.sc.rest_area[b];
+        double g[6] = {0, 0, 0, 0, 0, 0};
+        double H[6][6];
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) H[a][c] = 0.0;
+        const double ear = arap_terms(q, w, h2, g, H, with_derivs != 0);
+        double value = ik * (ein + h2 * ear);
+        double dz[6];
+        const bool anc = sv.ianc[i] != 0;
+        double rho = 0.0;
+        if (anc) {
+            rho = sv.irho[i];
+            double s2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 6; ++j) {
+                dz[j] = (q[j] - sv.iz[6 * i + j]) + sv.iu[6 * i + j];
+                s2 += dz[j] * dz[j];
+            }
+            value += 0.5 * rho * s2;
+        }
+        sv.rval[r] = value;
+        if (!with_derivs) continue;
+        double m[6][6];
+        mass_full(k, m);
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+            g[a] = ik * (md[a] + g[a]);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) H[a][c] = ik * (m[a][c] + H[a][c]);
+        }
+        if (anc) {
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+                g[a] += rho * dz[a];
+                H[a][a] += rho;
+            }
+        }
+        if (sv.project) clamp_psd<6>(H);
+        store6(sv.rgrad + 6 * r, g);
+        double* dst = sv.rdiag + 36 * r;
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) dst[6 * a + c] = H[a][c];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Candidate filter at a configuration: exact static broad-phase predicate
+// (margin d_hat) & not static-static & d < d_hat (objective.cpp:91-106).
+// mode 0: flag active contacts (derivatives); mode 1: weighted barrier value.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double kappa_c_inv(const SolverView& sv, int ba, int bb) {
+    if (sv.single_domain) return 1.0;
+    const int kc = __popc(sv.bmask[ba] & sv.bmask[bb]);
+    if (kc == 0) {
+        raise(sv.err, kErrNoHolder);
+        return 1.0;
+    }
+    return 1.0 / (1.0 / kc); // pair.kappa_c (objective.cpp:292-293)
+}
+
+__global__ void k_filter(SolverView sv, const unsigned long long* keys, int n, KeyFmt fmt,
+                         const Box* box, const double* qsrc, int mode, int which,
+                         unsigned char* flag, double* val) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        int a, b, v, e;
+        fmt.unpack(keys[t], a, b, v, e);
+        const int p = sv.ipart[a] - sv.part_base;
+        bool act = false;
+        double value = 0.0;
+        if (part_flag(sv, p, which)) {
+            const int ba = sv.ibody[a], bb = sv.ibody[b];
+            const bool ss = sv.sc.is_static[ba] && sv.sc.is_static[bb];
+            if (!ss && overlaps(box[a], box[b])) {
+                const double* qa = qsrc + 6 * a;
+                const double* qb = qsrc + 6 * b;
+                const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
+                const Box pb = point_box(sv.sc, qa, qa, false, vf);
+                const Box eb = edge_box(sv.sc, qb, qb, false, ef, sv.d_hat);
+                if (overlaps(pb, eb)) {
+                    if (mode == 0) atomicAdd(&sv.ps[p].n_candidates, 1);
+                    const V2 P = world_point(qa, rest_of(sv.sc, vf));
+                    const V2 E0 = world_point(qb, rest_of(sv.sc, ef));
+                    const V2 E1 = world_point(qb, rest_of(sv.sc, sv.sc.vnext[ef]));
+                    const double d = pe_distance(P, E0, E1);
+                    if (d < sv.d_hat) {
+                        if (d <= 0.0) raise(sv.err, d < 0.0 && d == -1.0 ? kErrDegenerateEdge : kErrBarrierDomain);
+                        act = true;
+                        if (mode == 1 && d > 0.0) {
+                            const double kinv = kappa_c_inv(sv, ba, bb); // 1/kappa_c
+                            const Barrier br = barrier(d, sv.d_hat, sv.kappa_bar);
+                            value = (sv.h * sv.h * kinv) * br.b;
+                        }
+                    }
+                }
+            }
+        }
+        if (flag) flag[t] = act ? 1 : 0;
+        if (val) val[t] = value;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Contact terms with the rank-6 PSD projection (energy.cpp:63-94,
+// objective.cpp:184-207).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kB)
+    k_contact_terms(SolverView sv, ContactView cv) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cv.n; c += gridDim.x * blockDim.x) {
+        int a, b, v, e;
+        cv.fmt.unpack(cv.key[c], a, b, v, e);
+        const int ba = sv.ibody[a], bb = sv.ibody[b];
+        const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e, ef1 = sv.sc.vnext[ef];
+        const V2 rp = rest_of(sv.sc, vf), r0 = rest_of(sv.sc, ef), r1 = rest_of(sv.sc, ef1);
+        const double* qa = sv.iq + 6 * a;
+        const double* qb = sv.iq + 6 * b;
+        const V2 P = world_point(qa, rp), E0 = world_point(qb, r0), E1 = world_point(qb, r1);
+        double g[6], A[6][6];
+        const double d = pe_distance_full(P, E0, E1, g, A);
+        if (!(d > 0.0)) {
+            raise(sv.err, kErrBarrierDomain);
+            continue;
+        }
+        const Barrier br = barrier(d, sv.d_hat, sv.kappa_bar);
+        const double w = sv.h * sv.h * kappa_c_inv(sv, ba, bb); // h^2 / kappa_c
+        cv.cval[c] = w * br.b;
+        // weighted gradient w * b' * t^T g
+        const double s = w * br.db;
+        double* cg = cv.cgrad + 12 * c;
+        cg[0] = s * g[0];
+        cg[1] = s * g[1];
+        cg[2] = s * (g[0] * rp.x);
+        cg[3] = s * (g[0] * rp.y);
+        cg[4] = s * (g[1] * rp.x);
+        cg[5] = s * (g[1] * rp.y);
+        cg[6] = s * (g[2] + g[4]);
+        cg[7] = s * (g[3] + g[5]);
+        cg[8] = s * (g[2] * r0.x + g[4] * r1.x);
+        cg[9] = s * (g[2] * r0.y + g[4] * r1.y);
+        cg[10] = s * (g[3] * r0.x + g[5] * r1.x);
+        cg[11] = s * (g[3] * r0.y + g[5] * r1.y);
+        // A = w (b'' g g^T + b' H_d)
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+            for (int j = 0; j < 6; ++j) A[i][j] = w * (br.ddb * (g[i] * g[j]) + br.db * A[i][j]);
+        if (!sv.project) {
+            double* cm = cv.cmat + 21 * c;
+            int idx = 0;
+#pragma unroll
+            for (int i = 0; i < 6; ++i)
+#pragma unroll
+                for (int j = i; j < 6; ++j) cm[idx++] = A[i][j];
+            continue;
+        }
+        // G = t t^T = L L^T (closed form), B = L^T A L
+        const double sp = sqrt(1.0 + rp.x * rp.x + rp.y * rp.y);
+        const double g00 = 1.0 + r0.x * r0.x + r0.y * r0.y;
+        const double g01 = 1.0 + r0.x * r1.x + r0.y * r1.y;
+        const double g11 = 1.0 + r1.x * r1.x + r1.y * r1.y;
+        const double l00 = sqrt(g00), l10 = g01 / l00, l11 = sqrt(fmax(g11 - l10 * l10, 1e-300));
+        // L (6x6 lower): diag(sp, sp, l00, l00, l11, l11), L[4][2]=L[5][3]=l10
+        double Bm[6][6];
+        // AL = A * L
+        double AL[6][6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            AL[i][0] = A[i][0] * sp;
+            AL[i][1] = A[i][1] * sp;
+            AL[i][2] = A[i][2] * l00 + A[i][4] * l10;
+            AL[i][3] = A[i][3] * l00 + A[i][5] * l10;
+            AL[i][4] = A[i][4] * l11;
+            AL[i][5] = A[i][5] * l11;
+        }
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            Bm[0][j] = sp * AL[0][j];
+            Bm[1][j] = sp * AL[1][j];
+            Bm[2][j] = l00 * AL[2][j] + l10 * AL[4][j];
+            Bm[3][j] = l00 * AL[3][j] + l10 * AL[5][j];
+            Bm[4][j] = l11 * AL[4][j];
+            Bm[5][j] = l11 * AL[5][j];
+        }
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+            for (int j = i + 1; j < 6; ++j) {
+                const double m = 0.5 * (Bm[i][j] + Bm[j][i]);
+                Bm[i][j] = m;
+                Bm[j][i] = m;
+            }
+        clamp_psd<6>(Bm);
+        // C = L^{-T} B+ L^{-1}; with Linv: diag(1/sp,1/sp,1/l00,1/l00,1/l11,1/l11),
+        // Linv[4][2] = Linv[5][3] = -l10/(l00 l11)
+        const double ip = 1.0 / sp, i0 = 1.0 / l00, i1 = 1.0 / l11, m10 = -l10 / (l00 * l11);
+        double BL[6][6]; // B+ Linv
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            BL[i][0] = Bm[i][0] * ip;
+            BL[i][1] = Bm[i][1] * ip;
+            BL[i][2] = Bm[i][2] * i0 + Bm[i][4] * m10;
+            BL[i][3] = Bm[i][3] * i0 + Bm[i][5] * m10;
+            BL[i][4] = Bm[i][4] * i1;
+            BL[i][5] = Bm[i][5] * i1;
+        }
+        double* cm = cv.cmat + 21 * c;
+        int idx = 0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            // row i of Linv^T BL: Linv^T[i][k] = Linv[k][i]
+#pragma unroll
+            for (int j = i; j < 6; ++j) {
+                double val;
+                if (i < 2) val = ip * BL[i][j];
+                else if (i == 2) val = i0 * BL[2][j] + m10 * BL[4][j];
+                else if (i == 3) val = i0 * BL[3][j] + m10 * BL[5][j];
+                else val = i1 * BL[i][j];
+                cm[idx++] = val;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Segment offsets of sorted keys: off[i] = first index whose instance >= i.
+// ---------------------------------------------------------------------------
+__global__ void k_seg_offsets(const unsigned long long* keys, int n, KeyFmt fmt, int n_inst,
+                             int* off, int which_field, const int* perm) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n_inst; i += gridDim.x * blockDim.x) {
+        int lo = 0, hi = n;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            int a, b, v, e;
+            fmt.unpack(keys[perm ? perm[mid] : mid], a, b, v, e);
+            const int key = which_field == 0 ? a : b;
+            if (key < i) lo = mid + 1;
+            else hi = mid;
+        }
+        off[i] = lo;
+    }
+}
+
+__global__ void k_make_bkeys(const unsigned long long* keys, int n, KeyFmt fmt,
+                             unsigned long long* bkeys, int* idx) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        int a, b, v, e;
+        fmt.unpack(keys[t], a, b, v, e);
+        bkeys[t] = fmt.pack(b, a, v, e);
+        idx[t] = t;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic BSR assembly (ELL storage, kEll off-diagonal blocks / row).
+// ---------------------------------------------------------------------------
+// M[gA[i]][gB[j]] += s * c2[al][be] * u[i] * w[j]   (J(u)^T c2 J(w))
+__device__ __forceinline__ void add_kron(double (&M)[6][6], double c00, double c01, double c10,
+                                         double c11, const double (&u)[3], const double (&w)[3],
+                                         bool transpose) {
+    const int gx[3] = {0, 2, 3}, gy[3] = {1, 4, 5};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const double uw = u[i] * w[j];
+            if (!transpose) {
+                M[gx[i]][gx[j]] += c00 * uw;
+                M[gx[i]][gy[j]] += c01 * uw;
+                M[gy[i]][gx[j]] += c10 * uw;
+                M[gy[i]][gy[j]] += c11 * uw;
+            } else {
+                M[gx[j]][gx[i]] += c00 * uw;
+                M[gy[j]][gx[i]] += c01 * uw;
+                M[gx[j]][gy[i]] += c10 * uw;
+                M[gy[j]][gy[i]] += c11 * uw;
+            }
+        }
+}
+
+__device__ __forceinline__ double cm_at(const double* cm, int i, int j) {
+    if (i > j) {
+        const int t = i;
+        i = j;
+        j = t;
+    }
+    // upper-triangle row-major index
+    return cm[i * 6 - (i * (i - 1)) / 2 + (j - i)];
+}
+
+struct ContactGeom {
+    double up[3], w0[3], w1[3];
+};
+
+__device__ __forceinline__ ContactGeom contact_geom(const SolverView& sv, int a, int b, int v,
+                                                    int e) {
+    const int ba = sv.ibody[a], bb = sv.ibody[b];
+    const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
+    const V2 rp = rest_of(sv.sc, vf), r0 = rest_of(sv.sc, ef), r1 = rest_of(sv.sc, sv.sc.vnext[ef]);
+    ContactGeom g;
+    g.up[0] = 1.0;
+    g.up[1] = rp.x;
+    g.up[2] = rp.y;
+    g.w0[0] = 1.0;
+    g.w0[1] = r0.x;
+    g.w0[2] = r0.y;
+    g.w1[0] = 1.0;
+    g.w1[1] = r1.x;
+    g.w1[2] = r1.y;
+    return g;
+}
+
+// point-body block (TL)
+__device__ __forceinline__ void add_tl(double (&M)[6][6], const double* cm, const ContactGeom& g) {
+    add_kron(M, cm_at(cm, 0, 0), cm_at(cm, 0, 1), cm_at(cm, 1, 0), cm_at(cm, 1, 1), g.up, g.up, false);
+}
+// edge-body block (BR)
+__device__ __forceinline__ void add_br(double (&M)[6][6], const double* cm, const ContactGeom& g) {
+    add_kron(M, cm_at(cm, 2, 2), cm_at(cm, 2, 3), cm_at(cm, 3, 2), cm_at(cm, 3, 3), g.w0, g.w0, false);
+    add_kron(M, cm_at(cm, 2, 4), cm_at(cm, 2, 5), cm_at(cm, 3, 4), cm_at(cm, 3, 5), g.w0, g.w1, false);
+    add_kron(M, cm_at(cm, 4, 2), cm_at(cm, 4, 3), cm_at(cm, 5, 2), cm_at(cm, 5, 3), g.w1, g.w0, false);
+    add_kron(M, cm_at(cm, 4, 4), cm_at(cm, 4, 5), cm_at(cm, 5, 4), cm_at(cm, 5, 5), g.w1, g.w1, false);
+}
+// coupling (point row, edge col) = TR; transpose gives BL
+__device__ __forceinline__ void add_tr(double (&M)[6][6], const double* cm, const ContactGeom& g,
+                                       bool transpose) {
+    add_kron(M, cm_at(cm, 0, 2), cm_at(cm, 0, 3), cm_at(cm, 1, 2), cm_at(cm, 1, 3), g.up, g.w0, transpose);
+    add_kron(M, cm_at(cm, 0, 4), cm_at(cm, 0, 5), cm_at(cm, 1, 4), cm_at(cm, 1, 5), g.up, g.w1, transpose);
+}
+
+__global__ void k_assemble(SolverView sv, ContactView cv, double* row_trace) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
+        const int p = sv.rpart[r] - sv.part_base;
+        if (!sv.ps[p].active) continue;
+        const int i = sv.rinst[r];
+        double g[6];
+        load6(sv.rgrad + 6 * r, g);
+        double D[6][6];
+        const double* dsrc = sv.rdiag + 36 * r;
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) D[a][c] = dsrc[6 * a + c];
+        const int a0 = cv.aoff[i], a1 = cv.aoff[i + 1];
+        const int b0 = cv.boff[i], b1 = cv.boff[i + 1];
+        // diagonal + gradient
+        for (int c = a0; c < a1; ++c) {
+            int ca, cb, vv, ee;
+            cv.fmt.unpack(cv.key[c], ca, cb, vv, ee);
+            const ContactGeom geo = contact_geom(sv, ca, cb, vv, ee);
+            add_tl(D, cv.cmat + 21 * c, geo);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) g[k] += cv.cgrad[12 * c + k];
+        }
+        for (int t = b0; t < b1; ++t) {
+            const int c = cv.perm_b[t];
+            int ca, cb, vv, ee;
+            cv.fmt.unpack(cv.key[c], ca, cb, vv, ee);
+            const ContactGeom geo = contact_geom(sv, ca, cb, vv, ee);
+            add_br(D, cv.cmat + 21 * c, geo);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) g[k] += cv.cgrad[12 * c + 6 + k];
+        }
+        store6(sv.rgrad + 6 * r, g);
+        double tr = 0.0;
+        double* ddst = sv.rdiag + 36 * r;
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+            tr += D[a][a];
+#pragma unroll
+            for (int c = 0; c < 6; ++c) ddst[6 * a + c] = D[a][c];
+        }
+        row_trace[r] = tr;
+        // off-diagonal blocks: merge a-seg (sorted by b) and b-seg (sorted by a)
+        int ia = a0, ib = b0, nblk = 0;
+        while (ia < a1 || ib < b1) {
+            int pa = 0x7fffffff, pb = 0x7fffffff;
+            int ca, cb, vv, ee;
+            if (ia < a1) {
+                cv.fmt.unpack(cv.key[ia], ca, cb, vv, ee);
+                pa = cb;
+            }
+            if (ib < b1) {
+                cv.fmt.unpack(cv.key[cv.perm_b[ib]], ca, cb, vv, ee);
+                pb = ca;
+            }
+            const int partner = min(pa, pb);
+            const int prow = sv.irow[partner];
+            double O[6][6];
+#pragma unroll
+            for (int x = 0; x < 6; ++x)
+#pragma unroll
+                for (int y = 0; y < 6; ++y) O[x][y] = 0.0;
+            while (ia < a1) {
+                cv.fmt.unpack(cv.key[ia], ca, cb, vv, ee);
+                if (cb != partner) break;
+                if (prow >= 0) add_tr(O, cv.cmat + 21 * ia, contact_geom(sv, ca, cb, vv, ee), false);
+                ++ia;
+            }
+            while (ib < b1) {
+                const int c = cv.perm_b[ib];
+                cv.fmt.unpack(cv.key[c], ca, cb, vv, ee);
+                if (ca != partner) break;
+                if (prow >= 0) add_tr(O, cv.cmat + 21 * c, contact_geom(sv, ca, cb, vv, ee), true);
+                ++ib;
+            }
+            if (prow < 0) continue;
+            if (nblk >= kEll) {
+                raise(sv.err, kErrCapacity);
+                break;
+            }
+            sv.ell_col[r * kEll + nblk] = prow;
+            double* odst = sv.ell_blk + (static_cast<size_t>(r) * kEll + nblk) * 36;
+#pragma unroll
+            for (int x = 0; x < 6; ++x)
+#pragma unroll
+                for (int y = 0; y < 6; ++y) odst[6 * x + y] = O[x][y];
+            ++nblk;
+        }
+        sv.ell_cnt[r] = nblk;
+    }
+}
+
+// Block-Jacobi preconditioner: inverse of (D + eps I) through its Cholesky.
+__global__ void k_precond(SolverView sv) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
+        const int p = sv.rpart[r] - sv.part_base;
+        if (!sv.ps[p].active) continue;
+        const double eps = sv.ps[p].eps;
+        double L[6][6];
+        const double* d = sv.rdiag + 36 * r;
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            double s = d[6 * j + j] + eps;
+#pragma unroll
+            for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
+            if (!(s > 0.0)) ok = false;
+            const double dj = sqrt(fmax(s, 1e-300));
+            L[j][j] = dj;
+#pragma unroll
+            for (int i = j + 1; i < 6; ++i) {
+                double t = d[6 * i + j];
+#pragma unroll
+                for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
+                L[i][j] = t / dj;
+            }
+#pragma unroll
+            for (int i = 0; i < j; ++i) L[i][j] = 0.0;
+        }
+        if (!ok) raise(sv.err, kErrFactor);
+        // inverse of L (lower), then Dinv = Linv^T Linv
+        double Li[6][6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                double s = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+                for (int k = 0; k < i; ++k) s -= L[i][k] * Li[k][c];
+                Li[i][c] = (i < c) ? 0.0 : s / L[i][i];
+            }
+        double* o = sv.rdinv + 36 * r;
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) s += Li[k][a] * Li[k][c];
+                o[6 * a + c] = s;
+            }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Two-level deterministic segment sums. Chunk c covers [c*CH, (c+1)*CH).
+// ---------------------------------------------------------------------------
+constexpr int kCH = 1024;
+
+template <typename PartOf>
+__global__ void k_segsum_partial(const double* v, int n, int P, int part_base, PartOf pof,
+                                 double* partial) {
+    __shared__ double sh[kB];
+    const int c = blockIdx.x;
+    const int s0 = c * kCH, s1 = min(n, s0 + kCH);
+    // partitions present in this chunk: [pof(s0), pof(s1-1)]
+    const int plo = s0 < s1 ? pof(s0) - part_base : 0;
+    const int phi = s0 < s1 ? pof(s1 - 1) - part_base : -1;
+    for (int p = 0; p < P; ++p) {
+        double acc = 0.0;
+        if (p >= plo && p <= phi)
+            for (int t = s0 + threadIdx.x; t < s1; t += kB)
+                if (pof(t) - part_base == p) acc += v[t];
+        sh[threadIdx.x] = acc;
+        __syncthreads();
+        for (int w = kB / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) partial[static_cast<size_t>(c) * P + p] = sh[0];
+        __syncthreads();
+    }
+}
+
+__global__ void k_segsum_final(const double* partial, int nchunks, int P, double* dst,
+                               int stride, int accumulate) {
+    const int p = threadIdx.x;
+    if (p >= P) return;
+    double s = 0.0;
+    for (int c = 0; c < nchunks; ++c) s += partial[static_cast<size_t>(c) * P + p];
+    if (accumulate) dst[p * stride] += s;
+    else dst[p * stride] = s;
+}
+
+struct RowPart {
+    const int* rpart;
+    __device__ int operator()(int t) const { return rpart[t]; }
+};
+struct KeyPart {
+    const unsigned long long* keys;
+    KeyFmt fmt;
+    const int* ipart;
+    __device__ int operator()(int t) const {
+        int a, b, v, e;
+        fmt.unpack(keys[t], a, b, v, e);
+        return ipart[a];
+    }
+};
+
+// ---------------------------------------------------------------------------
+// PCG (block-Jacobi) -- see solver.hpp for the scalar bookkeeping.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void matvec36(const double* m, const double (&x)[6], double (&y)[6]) {
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) s += m[6 * a + c] * x[c];
+        y[a] = s;
+    }
+}
+
+// r = b = -grad, x = 0, z = Dinv r, p0 = 0; per-row r.z, r.r, b.b
+__global__ void k_pcg_init(SolverView sv, double* rz, double* rr) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
+        const int p = sv.rpart[r] - sv.part_base;
+        double g[6], z[6];
+        load6(sv.rgrad + 6 * r, g);
+        const bool act = sv.ps[p].active != 0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) g[k] = act ? -g[k] : 0.0;
+        matvec36(sv.rdinv + 36 * r, g, z);
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            if (!act) z[k] = 0.0;
+            s1 += g[k] * z[k];
+            s2 += g[k] * g[k];
+        }
+        const double zero[6] = {0, 0, 0, 0, 0, 0};
+        store6(sv.r + 6 * r, g);
+        store6(sv.z + 6 * r, z);
+        store6(sv.x + 6 * r, zero);
+        store6(sv.p0 + 6 * r, zero);
+        rz[r] = s1;
+        rr[r] = s2;
+    }
+}
+
+// p_new = z + beta p_old ; ap = (D + eps I) p_new + sum_k B_k p_new[col_k]
+__global__ void k_pcg_spmv(SolverView sv, const double* pold, double* pnew, const double* beta_src,
+                           double* pap_row) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
+        const int p = sv.rpart[r] - sv.part_base;
+        const PartState& st = sv.ps[p];
+        if (!st.active || st.pcg_done) {
+            pap_row[r] = 0.0;
+            continue;
+        }
+        const double beta = beta_src[p];
+        double pr[6], zr[6], y[6];
+        load6(pold + 6 * r, pr);
+        load6(sv.z + 6 * r, zr);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) pr[k] = zr[k] + beta * pr[k];
+        store6(pnew + 6 * r, pr);
+        matvec36(sv.rdiag + 36 * r, pr, y);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) y[k] += st.eps * pr[k];
+        const int nb = sv.ell_cnt[r];
+        for (int t = 0; t < nb; ++t) {
+            const int c = sv.ell_col[r * kEll + t];
+            double pc[6], zc[6], yc[6];
+            load6(pold + 6 * c, pc);
+            load6(sv.z + 6 * c, zc);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) pc[k] = zc[k] + beta * pc[k];
+            matvec36(sv.ell_blk + (static_cast<size_t>(r) * kEll + t) * 36, pc, yc);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) y[k] += yc[k];
+        }
+        store6(sv.ap + 6 * r, y);
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s += pr[k] * y[k];
+        pap_row[r] = s;
+    }
+}
+
+// x += alpha p ; r -= alpha Ap ; z = Dinv r ; per-row r.z, r.r
+__global__ void k_pcg_update(SolverView sv, const double* pnew, const double* alpha_src,
+                             double* rz, double* rr) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
+        const int p = sv.rpart[r] - sv.part_base;
+        const PartState& st = sv.ps[p];
+        if (!st.active || st.pcg_done) {
+            rz[r] = 0.0;
+            rr[r] = 0.0;
+            continue;
+        }
+        const double alpha = alpha_src[p];
+        double x[6], rv[6], pv[6], av[6], z[6];
+        load6(sv.x + 6 * r, x);
+        load6(sv.r + 6 * r, rv);
+        load6(pnew + 6 * r, pv);
+        load6(sv.ap + 6 * r, av);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            x[k] += alpha * pv[k];
+            rv[k] -= alpha * av[k];
+        }
+        matvec36(sv.rdinv + 36 * r, rv, z);
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            s1 += rv[k] * z[k];
+            s2 += rv[k] * rv[k];
+        }
+        store6(sv.x + 6 * r, x);
+        store6(sv.r + 6 * r, rv);
+        store6(sv.z + 6 * r, z);
+        rz[r] = s1;
+        rr[r] = s2;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Line search helpers
+// ---------------------------------------------------------------------------
+// q_try = q + alpha * dq (objective.cpp:215-221), unfused like the reference.
+__global__ void k_make_trial(SolverView sv, int use_alpha_field, double fixed_alpha, int which) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < sv.n_inst; i += gridDim.x * blockDim.x) {
+        const int p = sv.ipart[i] - sv.part_base;
+        const int r = sv.irow[i];
+        double q[6];
+        load6(sv.iq + 6 * i, q);
+        if (r >= 0 && part_flag(sv, p, which)) {
+            const double alpha = use_alpha_field ? sv.ps[p].alpha : fixed_alpha;
+            double dq[6];
+            load6(sv.x + 6 * r, dq);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) q[k] = xadd(q[k], xmul(alpha, dq[k]));
+        }
+        store6(sv.iq_try + 6 * i, q);
+    }
+}
+
+__global__ void k_dq_inf(SolverView sv) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
+        const int p = sv.rpart[r] - sv.part_base;
+        if (!sv.ps[p].active) continue;
+        double m = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) m = fmax(m, fabs(sv.x[6 * r + k]));
+        atomic_max_nonneg(&sv.ps[p].dq_inf, m);
+    }
+}
+
+// CCD over the candidate superset with the exact swept margin-0 predicate
+// (geometry.cpp:311-341). box0: per-instance swept boxes with margin 0.
+__global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, KeyFmt fmt,
+                      const Box* box0, const double* q0, const double* q1, int which,
+                      double* earliest_override) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        int a, b, v, e;
+        fmt.unpack(keys[t], a, b, v, e);
+        const int p = sv.ipart[a] - sv.part_base;
+        if (!part_flag(sv, p, which)) continue;
+        if (!overlaps(box0[a], box0[b])) continue;
+        const int ba = sv.ibody[a], bb = sv.ibody[b];
+        const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
+        const double* qa0 = q0 + 6 * a;
+        const double* qa1 = q1 + 6 * a;
+        const double* qb0 = q0 + 6 * b;
+        const double* qb1 = q1 + 6 * b;
+        const Box pb = point_box(sv.sc, qa0, qa1, true, vf);
+        const Box eb = edge_box(sv.sc, qb0, qb1, true, ef, 0.0);
+        if (!overlaps(pb, eb)) continue;
+        const V2 rp = rest_of(sv.sc, vf), r0 = rest_of(sv.sc, ef),
+                 r1 = rest_of(sv.sc, sv.sc.vnext[ef]);
+        const V2 P0 = world_point(qa0, rp), P1 = world_point(qa1, rp);
+        const V2 A0 = world_point(qb0, r0), A1 = world_point(qb1, r0);
+        const V2 B0 = world_point(qb0, r1), B1 = world_point(qb1, r1);
+        const double d0 = pe_distance(P0, A0, B0);
+        if (d0 <= 0.0) {
+            raise(sv.err, d0 == -1.0 ? kErrDegenerateEdge : kErrTouching);
+            continue;
+        }
+        const double toi = pair_impact_time(P0, P1, A0, A1, B0, B1);
+        if (toi <= 1.0)
+            atomic_min_nonneg(earliest_override ? &earliest_override[p] : &sv.ps[p].toi_earliest, toi);
+    }
+}
+
+} // namespace
+
+// ---------------------------------------------------------------------------
+// launch wrappers
+// ---------------------------------------------------------------------------
+void launch_body_terms(const SolverView& sv, const double* q, bool derivs, int which,
+                       cudaStream_t s) {
+    if (sv.n_rows == 0) return;
+    k_body_terms<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, q, derivs ? 1 : 0, which);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, KeyFmt fmt,
+                   const Box* box, const double* q, int mode, int which, unsigned char* flag,
+                   double* val, cudaStream_t s) {
+    if (n == 0) return;
+    k_filter<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, fmt, box, q, mode, which, flag, val);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_contact_terms(const SolverView& sv, const ContactView& cv, cudaStream_t s) {
+    if (cv.n == 0) return;
+    k_contact_terms<<<grid_for(cv.n, kB), kB, 0, s>>>(sv, cv);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_seg_offsets(const unsigned long long* keys, int n, KeyFmt fmt, int n_inst, int* off,
+                        int field, const int* perm, cudaStream_t s) {
+    k_seg_offsets<<<grid_for(n_inst + 1, kB), kB, 0, s>>>(keys, n, fmt, n_inst, off, field, perm);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_make_bkeys(const unsigned long long* keys, int n, KeyFmt fmt, unsigned long long* bkeys,
+                       int* idx, cudaStream_t s) {
+    if (n == 0) return;
+    k_make_bkeys<<<grid_for(n, kB), kB, 0, s>>>(keys, n, fmt, bkeys, idx);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_assemble(const SolverView& sv, const ContactView& cv, double* row_trace,
+                     cudaStream_t s) {
+    if (sv.n_rows == 0) return;
+    k_assemble<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, cv, row_trace);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_precond(const SolverView& sv, cudaStream_t s) {
+    if (sv.n_rows == 0) return;
+    k_precond<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+int segsum_chunks(int n) { return std::max(1, (n + kCH - 1) / kCH); }
+
+void launch_segsum_rows(const double* v, int n, const int* rpart, int P, int part_base,
+                        double* partial, double* dst, int stride, bool accumulate, cudaStream_t s) {
+    const int nc = segsum_chunks(n);
+    if (n > 0) {
+        k_segsum_partial<<<nc, kB, 0, s>>>(v, n, P, part_base, RowPart{rpart}, partial);
+        CUDA_CHECK(cudaGetLastError());
+    }
+    k_segsum_final<<<1, 32, 0, s>>>(partial, n > 0 ? nc : 0, P, dst, stride, accumulate ? 1 : 0);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_segsum_keys(const double* v, int n, const unsigned long long* keys, KeyFmt fmt,
+                        const int* ipart, int P, int part_base, double* partial, double* dst,
+                        int stride, bool accumulate, cudaStream_t s) {
+    const int nc = segsum_chunks(n);
+    if (n > 0) {
+        k_segsum_partial<<<nc, kB, 0, s>>>(v, n, P, part_base, KeyPart{keys, fmt, ipart}, partial);
+        CUDA_CHECK(cudaGetLastError());
+    }
+    k_segsum_final<<<1, 32, 0, s>>>(partial, n > 0 ? nc : 0, P, dst, stride, accumulate ? 1 : 0);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_pcg_init(const SolverView& sv, double* rz, double* rr, cudaStream_t s) {
+    if (sv.n_rows == 0) return;
+    k_pcg_init<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, rz, rr);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_pcg_spmv(const SolverView& sv, const double* pold, double* pnew, const double* beta,
+                     double* pap_row, cudaStream_t s) {
+    if (sv.n_rows == 0) return;
+    k_pcg_spmv<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, pold, pnew, beta, pap_row);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_pcg_update(const SolverView& sv, const double* pnew, const double* alpha, double* rz,
+                       double* rr, cudaStream_t s) {
+    if (sv.n_rows == 0) return;
+    k_pcg_update<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, pnew, alpha, rz, rr);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_make_trial(const SolverView& sv, bool use_alpha, double alpha, int which,
+                       cudaStream_t s) {
+    if (sv.n_inst == 0) return;
+    k_make_trial<<<grid_for(sv.n_inst, kB), kB, 0, s>>>(sv, use_alpha ? 1 : 0, alpha, which);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_dq_inf(const SolverView& sv, cudaStream_t s) {
+    if (sv.n_rows == 0) return;
+    k_dq_inf<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, KeyFmt fmt,
+                const Box* box0, const double* q0, const double* q1, int which,
+                double* earliest_override, cudaStream_t s) {
+    if (n == 0) return;
+    k_ccd<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, fmt, box0, q0, q1, which, earliest_override);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+} // namespace dabd_gpu

@@ -1,0 +1,100 @@
+// Batched local solve on one device: every partition this context owns runs
+// its own projected Newton (proj/src/newton.cpp:7-71) on its instance set,
+// with its own line search and convergence, inside the same kernels.
+//
+// Arrays are sorted by (partition, body) so every per-partition quantity is
+// a contiguous segment; reductions are fixed-order two-level segment sums,
+// so results are bitwise reproducible run to run.
+#pragma once
+
+#include "common.cuh"
+#include "device_scene.hpp"
+
+namespace dabd_gpu {
+
+constexpr int kEll = 24;   // max off-diagonal 6x6 blocks per BSR row
+constexpr int kMaxParts = 32;
+
+struct PartState {
+    double energy;     // objective at the current iterate
+    double trial;      // objective at the current line-search trial
+    double alpha;      // current step
+    double alpha_max;  // CCD bound (newton.cpp:38-42)
+    double dq_inf;     // ||dq||_inf of the current direction
+    double tol;        // Newton tolerance theta*h*l
+    double eps;        // 1e-8 tr(H)/n (newton.cpp:20-22)
+    double trace;
+    double final_update;
+    double toi_earliest; // CCD min over candidates (2.0 = none)
+    double rz, rr, bnorm2, pap;
+    int ndof;
+    int active;        // Newton still iterating
+    int searching;     // line search in progress
+    int accepted;      // trial accepted in the last line-search round
+    int converged;
+    int iterations;
+    int ls_steps;
+    int pcg_done;
+    int pcg_iters;
+    int n_active_contacts;
+    int n_candidates;
+};
+
+struct SolverView {
+    SceneView sc;
+    int n_inst = 0, n_rows = 0, n_parts = 0, part_base = 0;
+    // instances
+    const int* ibody = nullptr;
+    const int* ipart = nullptr;
+    const int* irow = nullptr;
+    double* iq = nullptr;     // current iterate [I][6]
+    double* iq_try = nullptr; // trial / end configuration [I][6]
+    const double* iqt = nullptr;  // q_tilde
+    const double* iinvk = nullptr; // 1/kappa_b
+    const int* ianc = nullptr;     // anchored (shared) flag
+    const double* iz = nullptr;
+    const double* iu = nullptr;
+    const double* irho = nullptr;
+    // body holder masks (single_domain -> kappa_c = 1)
+    const uint32_t* bmask = nullptr;
+    int single_domain = 1;
+    // rows (dynamic instances)
+    const int* rinst = nullptr;
+    const int* rpart = nullptr;
+    double* rgrad = nullptr;  // [R][6]
+    double* rdiag = nullptr;  // [R][36]
+    double* rdinv = nullptr;  // [R][36]
+    double* rval = nullptr;   // [R]
+    int* ell_cnt = nullptr;   // [R]
+    int* ell_col = nullptr;   // [R][kEll]
+    double* ell_blk = nullptr; // [R][kEll][36]
+    double* x = nullptr;      // dq [R][6]
+    double* r = nullptr;
+    double* z = nullptr;
+    double* p0 = nullptr;
+    double* p1 = nullptr;
+    double* ap = nullptr;
+    // partition offsets
+    const int* part_row_off = nullptr;  // [P+1]
+    const int* part_inst_off = nullptr; // [P+1]
+    PartState* ps = nullptr;
+    // params
+    double h = 0.01, d_hat = 0.01, kappa_bar = 1e4, kappa_arap = 1e6;
+    int project = 1; // PSD-project body and contact blocks (objective.cpp:366, 381)
+    int* err = nullptr;
+};
+
+// Active contacts (derivative stage) in (a,b,v,e) order plus their data.
+struct ContactView {
+    int n = 0;
+    KeyFmt fmt;
+    const unsigned long long* key = nullptr; // sorted by (a, b, v, e)
+    const int* perm_b = nullptr;  // contact indices sorted by (b, a, v, e)
+    const int* aoff = nullptr;    // [I+1] contacts with a == i: [aoff[i], aoff[i+1])
+    const int* boff = nullptr;    // [I+1] perm_b positions with b == i
+    double* cval = nullptr;       // [C] weighted barrier value
+    double* cgrad = nullptr;      // [C][12] weighted gradient
+    double* cmat = nullptr;       // [C][21] projected world-space 6x6 (upper, row-major)
+};
+
+} // namespace dabd_gpu
