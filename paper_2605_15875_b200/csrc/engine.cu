@@ -355,7 +355,7 @@ void Engine::derivatives() {
     launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
                        ps_field(ps_.get(), &PartState::trace), kPsStride, false, s_);
     launch_scalar(ps_.get(), P_, kOpEps, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
-    launch_precond(v, s_);
+    if (project_) launch_precond(v, s_); // unprojected blocks (objective mode 3) may be indefinite
 }
 
 void Engine::pcg() {
