@@ -1,0 +1,298 @@
+"""Benchmark: simulation steps/s (and ADMM iterations/s) of the B200 hot path.
+
+`python bench.py --gpus N --steps K --warmup W [--impl ours|reference]`
+
+A step is one committed frame of the BASELINE.json workload. At N=1 that is
+config[1], "1k-body random pile drop, single partition on 1 B200" (scene
+`pile-1k`: 1,000 boxes, 25 x 40 lattice, run_reference semantics). Inputs are
+synthetic (the deterministic lattice + splitmix64 jitter of scene.py) and
+resident in HBM during the timed `value`; `e2e` times the same steps through
+the public C ABI with the state copied host->device and back every step.
+
+The L2 is flushed (256 MiB write) between timed steps, outside the per-step
+CUDA events. Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_N1 = "pile-1k"
+ROOFLINE_KERNEL = "k_pcg_spmv"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int) -> None:
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference_arm(args) -> None:
+    """CPU reference arm: the oracle port of proj/src/sim.cpp:186-249 (the
+    reference itself cannot be built here: Eigen3 is absent),
+    single-threaded like the reference worker."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_2605_15875_b200.scene import make_scenario
+
+    sd = make_scenario(args.config)
+    o = O.Scene(sd)
+    # bounded sample: each step is one frame continued from the previous one
+    q, qd = o.q0.copy(), o.qdot0.copy()
+    times = []
+    admm = 0
+    for i in range(args.warmup + args.steps):
+        o.set_state(q, qd)
+        t0 = time.perf_counter()
+        r = o.run(1, workers=0)
+        dt = time.perf_counter() - t0
+        q, qd = r["q"][0], r["qdot"][0]
+        if i >= args.warmup:
+            times.append(dt)
+            admm += int(r["admm"][0])
+    total = sum(times)
+    value = args.steps / total
+    line = {
+        "impl": "reference", "metric": "sim_steps_per_sec", "value": value, "unit": "steps/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "bodies": o.n, "partitions": 1,
+                   "semantics": "run_reference (sim.cpp:186-249)"},
+        "admm_iters_per_sec": admm / total,
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} consecutive frames of {args.config} after "
+                                   f"{args.warmup} warm-up frames, oracle/ C++ restatement"},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(sd, q, qd, budget_s: float = 20.0):
+    """Oracle (port) steps/s on the host, continuing from the GPU's warm state."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    o = O.Scene(sd)
+    frames = 0
+    t0 = time.perf_counter()
+    while True:
+        o.set_state(q, qd)
+        r = o.run(1, workers=0)
+        q, qd = r["q"][0], r["qdot"][0]
+        frames += 1
+        if time.perf_counter() - t0 > budget_s or frames >= 5:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": frames / dt, "unit": "steps/s", "cores": 1, "kind": "port",
+            "sample": f"{frames} frame(s) of the same workload from the GPU run's warm state, "
+                      f"single-threaded oracle/ restatement ({dt:.1f} s)"}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=CONFIG_N1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--roofline-kernel", default=ROOFLINE_KERNEL)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import numpy as np
+    import torch
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2605_15875_b200 import _lib as L
+    from paper_2605_15875_b200 import api
+    from paper_2605_15875_b200.scene import make_scenario
+
+    lib = L.load()
+    sd = make_scenario(args.config)
+    scene = api.Scene(sd)
+    ctx = api.Context(scene, device=local, num_workers=0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    for _ in range(args.warmup):
+        ctx.run_frames(1)
+    torch.cuda.synchronize()
+    q_warm, qd_warm = ctx.state()
+
+    lib.dabd_gpu_kernel_timer_enable(args.roofline_kernel.encode())
+    n0 = C.c_longlong()
+    lib.dabd_gpu_launch_count(C.byref(n0))
+    step_ms = []
+    admm = 0
+    stats = []
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st = ctx.run_frames(1)[0]
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            admm += st["admm_iterations"]
+            stats.append(st)
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    n1 = C.c_longlong()
+    lib.dabd_gpu_launch_count(C.byref(n1))
+    kms, kcnt, kbytes = C.c_double(), C.c_longlong(), C.c_double()
+    lib.dabd_gpu_kernel_timer_read(C.byref(kms), C.byref(kcnt), C.byref(kbytes))
+    lib.dabd_gpu_kernel_timer_enable(None)
+    total_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = ws * args.steps / (total_ms / 1e3)
+
+    # e2e through the public API with host buffers (pinned) every step
+    q_h = torch.from_numpy(q_warm.copy()).pin_memory()
+    qd_h = torch.from_numpy(qd_warm.copy()).pin_memory()
+    ctx2 = api.Context(scene, device=local, num_workers=0)
+    ctx2.set_stream(stream.cuda_stream)
+    qp = C.cast(q_h.data_ptr(), C.POINTER(C.c_double))
+    qdp = C.cast(qd_h.data_ptr(), C.POINTER(C.c_double))
+    st_arr = (L.FrameStats * 1)()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        L.check(lib.dabd_gpu_set_state(ctx2.h, qp, qdp))
+        L.check(lib.dabd_gpu_run_frames(ctx2.h, 1, st_arr))
+        L.check(lib.dabd_gpu_get_state(ctx2.h, qp, qdp))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    nbytes = 2 * 6 * 8 * scene.n
+
+    hbm, peak_kind = _peaks()
+    roof = None
+    if kcnt.value > 0 and kms.value > 0:
+        achieved = (kbytes.value / kcnt.value) / (kms.value / kcnt.value / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": args.roofline_kernel, "achieved": achieved,
+                "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "peak_kind": peak_kind, "launches": kcnt.value,
+                "avg_launch_us": 1e3 * kms.value / kcnt.value,
+                "share_of_step": kms.value / total_ms,
+                "algorithmic_bytes_per_launch": kbytes.value / kcnt.value}
+    line = {
+        "metric": "sim_steps_per_sec", "value": value, "unit": "steps/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.config, "bodies": scene.n, "partitions": 1,
+                   "semantics": "run_reference (sim.cpp:186-249)",
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "parallelism": "replica" if ws > 1 else "single"},
+        "admm_iters_per_sec": admm * ws / (total_ms / 1e3),
+        "newton_iters_per_step": sum(s["newton_iterations"] for s in stats) / len(stats),
+        "pcg_iters_per_step": sum(s["pcg_iterations"] for s in stats) / len(stats),
+        "max_contacts": max(s["max_contacts"] for s in stats),
+        "e2e": {"value": ws * args.steps / (e2e_ms / 1e3), "unit": "steps/s",
+                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
+        "gpu_launches": int(n1.value - n0.value),
+        "roofline": roof,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(sd, q_warm, qd_warm)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -192,6 +192,15 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_get_rho(dabd_gpu_ctx* ctx, double* rho);
 DABD_GPU_API dabd_gpu_status dabd_gpu_take_trace(dabd_gpu_ctx* ctx, double* rows, int capacity,
                                                  int* count);
 
+/* ---- instrumentation (bench.py) ---------------------------------------------
+ * Total dabd_gpu kernel launches so far (CUB library kernels excluded), and
+ * CUDA-event timing of every launch of one named kernel (e.g. "k_pcg_spmv");
+ * name == NULL disables. read() synchronises nothing: call after the work. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_launch_count(long long* count);
+DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_enable(const char* kernel_name);
+DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_read(double* total_ms, long long* launches,
+                                                        double* algorithmic_bytes);
+
 #ifdef __cplusplus
 }
 #endif

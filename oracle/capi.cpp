@@ -158,6 +158,18 @@ int oracle_scene_set_params(void* sp, const double* sim8, const double* adapt5,
     });
 }
 
+// Replaces the initial state (AffineBody::q, q_dot) so drivers start from it.
+int oracle_scene_set_state(void* sp, const double* q, const double* qdot) {
+    return guarded([&] {
+        Scene* s = static_cast<Scene*>(sp);
+        for (size_t b = 0; b < s->bodies.size(); ++b)
+            for (int k = 0; k < 6; ++k) {
+                s->bodies[b].q[k] = q[6 * b + k];
+                s->bodies[b].q_dot[k] = qdot[6 * b + k];
+            }
+    });
+}
+
 int oracle_scene_set_force_split(void* sp, int body, double fx, double fy) {
     return guarded([&] { static_cast<Scene*>(sp)->replica_force_split[body] = {fx, fy}; });
 }

@@ -111,6 +111,11 @@ class Scene:
         except Exception:
             pass
 
+    def set_state(self, q, qdot):
+        """Start subsequent run() calls from (q, qdot) instead of the scene's initial state."""
+        _check(lib().oracle_scene_set_state(self.h, _d(_f64(q, (self.n, 6))),
+                                            _d(_f64(qdot, (self.n, 6)))))
+
     # -- geometry -----------------------------------------------------------
     def broad_phase(self, q, margin, q_end=None, subset=None):
         q = _f64(q, (self.n, 6))

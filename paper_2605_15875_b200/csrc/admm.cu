@@ -4,6 +4,8 @@
 // body.cpp:120-161, runtime.cpp:241-277, 361-397, 457-506).
 #include "admm.hpp"
 
+#include "instrument.hpp"
+
 namespace dabd_gpu {
 
 namespace {
@@ -228,77 +230,67 @@ __global__ void k_accept_copy(int n, const int* ipart, int part_base, const Part
 
 void launch_gather(int n, const int* ibody, const double* q, double* iq, cudaStream_t s) {
     if (n == 0) return;
-    k_gather<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ibody, q, iq);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_gather", s, k_gather<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ibody, q, iq));
 }
 
 void launch_predict(const SceneView& sc, int n, const int* ibody, const double* iq,
                     const double* qd, double h, double gx, double gy, const double* ifs,
                     double* iqt, cudaStream_t s) {
     if (n == 0) return;
-    k_predict<<<grid_for(n, kB), kB, 0, s>>>(sc, n, ibody, iq, qd, h, gx, gy, ifs, iqt);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_predict", s, k_predict<<<grid_for(n, kB), kB, 0, s>>>(sc, n, ibody, iq, qd, h, gx, gy, ifs, iqt));
 }
 
 void launch_delta_inf(int n_rows, const int* rinst, const int* rpart, int part_base,
                       const double* a, const double* b, double* out, cudaStream_t s) {
     if (n_rows == 0) return;
-    k_delta_inf<<<grid_for(n_rows, kB), kB, 0, s>>>(n_rows, rinst, rpart, part_base, a, b, out);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_delta_inf", s, k_delta_inf<<<grid_for(n_rows, kB), kB, 0, s>>>(n_rows, rinst, rpart, part_base, a, b, out));
 }
 
 void launch_masks(const SceneView& sc, const double* q, const double* planes, int np, double w,
                   uint32_t all, uint32_t* masks, int* err, cudaStream_t s) {
     if (sc.nb == 0) return;
-    k_masks<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, q, planes, np, w, all, masks, err);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_masks", s, k_masks<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, q, planes, np, w, all, masks, err));
 }
 
 void launch_vmax(const SceneView& sc, const double* qd, double* out, cudaStream_t s) {
     if (sc.nb == 0) return;
-    k_vmax<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, qd, out);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_vmax", s, k_vmax<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, qd, out));
 }
 
 void launch_consensus(int ns, const int* sh, const int* ipart, int part_base, const double* iq,
                       double* iu, const double* irho, const double* iz, double* iznext, double* rb,
                       double* sb, double* rloc, double* sloc, int* err, cudaStream_t s) {
     if (ns == 0) return;
-    k_consensus<<<grid_for(ns, kB), kB, 0, s>>>(ns, sh, ipart, part_base, iq, iu, irho, iz, iznext,
-                                                rb, sb, rloc, sloc, err);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_consensus", s, k_consensus<<<grid_for(ns, kB), kB, 0, s>>>(ns, sh, ipart, part_base, iq, iu, irho, iz, iznext,
+                                                rb, sb, rloc, sloc, err));
 }
 
 void launch_merged(int n, const int* ianc, const double* iq, const double* iznext, double* out,
                    cudaStream_t s) {
     if (n == 0) return;
-    k_merged<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ianc, iq, iznext, out);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_merged", s, k_merged<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ianc, iq, iznext, out));
 }
 
 void launch_adapt(int n, const int* ianc, double* irho, const double* irho0, const double* rb,
                   const double* sb, const AdaptParams& a, double* iz, const double* iznext,
                   cudaStream_t s) {
     if (n == 0) return;
-    k_adapt<<<grid_for(n, kB), kB, 0, s>>>(n, ianc, irho, irho0, rb, sb, a.tau, a.mu, a.sigma_min,
-                                           a.sigma_max, a.adapt_enabled ? 1 : 0, iz, iznext);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_adapt", s, k_adapt<<<grid_for(n, kB), kB, 0, s>>>(n, ianc, irho, irho0, rb, sb, a.tau, a.mu, a.sigma_min,
+                                           a.sigma_max, a.adapt_enabled ? 1 : 0, iz, iznext));
 }
 
 void launch_commit(const SceneView& sc, int n, const int* ibody, const int* ipart, const int* ianc,
                    const uint32_t* bmask, double* iq, const double* iznext, const double* q_start,
                    double h, double* q, double* qd, cudaStream_t s) {
     if (n == 0) return;
-    k_commit<<<grid_for(n, kB), kB, 0, s>>>(sc, n, ibody, ipart, ianc, bmask, iq, iznext, q_start,
-                                            h, q, qd);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_commit", s, k_commit<<<grid_for(n, kB), kB, 0, s>>>(sc, n, ibody, ipart, ianc, bmask, iq, iznext, q_start,
+                                            h, q, qd));
 }
 
 void launch_accept_copy(int n, const int* ipart, int part_base, const PartState* ps,
                         const double* src, double* dst, cudaStream_t s) {
     if (n == 0) return;
-    k_accept_copy<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ipart, part_base, ps, src, dst);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_accept_copy", s, k_accept_copy<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ipart, part_base, ps, src, dst));
 }
 
 } // namespace dabd_gpu

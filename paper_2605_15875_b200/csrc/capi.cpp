@@ -3,6 +3,7 @@
 #include "dabd_gpu.h"
 
 #include "engine.hpp"
+#include "instrument.hpp"
 #include "scene.hpp"
 
 #include <cmath>
@@ -351,6 +352,26 @@ dabd_gpu_status dabd_gpu_take_trace(dabd_gpu_ctx* ctx, double* rows, int capacit
         for (int i = 0; i < n; ++i) std::memcpy(rows + 8 * i, &t[i], 8 * sizeof(double));
         return DABD_GPU_OK;
     });
+}
+
+dabd_gpu_status dabd_gpu_launch_count(long long* count) {
+    if (!count) return null_arg();
+    *count = dabd_gpu::launch_counter().load();
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_kernel_timer_enable(const char* name) {
+    dabd_gpu::KernelTimer::get().enable(name ? name : "");
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_kernel_timer_read(double* total_ms, long long* launches,
+                                           double* algorithmic_bytes) {
+    if (!total_ms || !launches || !algorithmic_bytes) return null_arg();
+    *algorithmic_bytes = dabd_gpu::KernelTimer::get().bytes();
+    *total_ms = dabd_gpu::KernelTimer::get().total_ms();
+    *launches = dabd_gpu::KernelTimer::get().count();
+    return DABD_GPU_OK;
 }
 
 } // extern "C"

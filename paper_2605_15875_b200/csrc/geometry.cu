@@ -5,6 +5,8 @@
 
 #include <cfloat>
 
+#include "instrument.hpp"
+
 namespace dabd_gpu {
 
 namespace {
@@ -218,16 +220,14 @@ __global__ void k_narrow_bodies(SceneView sc, const double* q, const int* cand, 
 void launch_narrow_bodies(const SceneView& sc, const double* q, const int* cand, int n,
                           double d_hat, double* d, int* flag, int* err, cudaStream_t s) {
     if (n == 0) return;
-    k_narrow_bodies<<<grid_for(n, kBlock), kBlock, 0, s>>>(sc, q, cand, n, d_hat, d, flag, err);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_narrow_bodies", s, k_narrow_bodies<<<grid_for(n, kBlock), kBlock, 0, s>>>(sc, q, cand, n, d_hat, d, flag, err));
 }
 
 void launch_inst_boxes(const SceneView& sc, const InstView& iv, bool swept, double margin, Box* box,
                        double* cell_max, cudaStream_t s) {
     if (iv.n == 0) return;
-    k_inst_boxes<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(sc, iv, swept ? 1 : 0, margin, box,
-                                                          cell_max);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_inst_boxes", s, k_inst_boxes<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(sc, iv, swept ? 1 : 0, margin, box,
+                                                          cell_max));
 }
 
 Detector::Detector() {
@@ -257,9 +257,8 @@ int Detector::build(const SceneView& sc, const InstView& iv, const int* stat, in
     hitems_.resize(iv.n);
     hkey_.resize(iv.n);
     hcount_.zero(s);
-    k_hash_count<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(sc, iv, box_.get(), cell_.get(),
-                                                           tsize - 1, hcount_.get(), hkey_.get());
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_hash_count", s, k_hash_count<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(sc, iv, box_.get(), cell_.get(),
+                                                           tsize - 1, hcount_.get(), hkey_.get()));
     size_t tb = 0;
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, hcount_.get(), hstart_.get(),
                                              static_cast<int>(tsize), s));
@@ -267,24 +266,23 @@ int Detector::build(const SceneView& sc, const InstView& iv, const int* stat, in
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp_.get(), tb, hcount_.get(), hstart_.get(),
                                              static_cast<int>(tsize), s));
     hfill_.zero(s);
-    k_hash_scatter<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(iv.n, hkey_.get(), hstart_.get(),
-                                                             hfill_.get(), hitems_.get());
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_hash_scatter", s, k_hash_scatter<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(iv.n, hkey_.get(), hstart_.get(),
+                                                             hfill_.get(), hitems_.get()));
 
     int cap = static_cast<int>(std::max<size_t>(keys_.capacity(), 64 * static_cast<size_t>(iv.n)));
     for (int attempt = 0; attempt < 3; ++attempt) {
         keys_.resize(cap);
         counter_.zero(s);
-        k_emit<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(
+        DABD_LAUNCH("k_emit", s, k_emit<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(
             sc, iv, box_.get(), cell_.get(), tsize - 1, hstart_.get(), hcount_.get(),
             hitems_.get(), stat, n_stat, swept ? 1 : 0, margin, fmt_, keys_.get(), cap,
-            counter_.get());
-        CUDA_CHECK(cudaGetLastError());
+            counter_.get()));
         if (n_stat > 1) {
-            k_emit_static_pairs<<<grid_for(static_cast<long long>(n_stat) * n_stat, kBlock), kBlock,
-                                  0, s>>>(sc, iv, box_.get(), stat, n_stat, swept ? 1 : 0, margin,
-                                          fmt_, keys_.get(), cap, counter_.get());
-            CUDA_CHECK(cudaGetLastError());
+            const int gs = grid_for(static_cast<long long>(n_stat) * n_stat, kBlock);
+            DABD_LAUNCH("k_emit_static_pairs", s,
+                        k_emit_static_pairs<<<gs, kBlock, 0, s>>>(sc, iv, box_.get(), stat, n_stat,
+                                                                  swept ? 1 : 0, margin, fmt_,
+                                                                  keys_.get(), cap, counter_.get()));
         }
         CUDA_CHECK(cudaMemcpyAsync(pin_.get(), counter_.get(), 2 * sizeof(int),
                                    cudaMemcpyDeviceToHost, s));

@@ -7,6 +7,8 @@
 
 #include <cub/cub.cuh>
 
+#include "instrument.hpp"
+
 namespace dabd_gpu {
 
 namespace {
@@ -791,48 +793,41 @@ __global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, KeyF
 void launch_body_terms(const SolverView& sv, const double* q, bool derivs, int which,
                        cudaStream_t s) {
     if (sv.n_rows == 0) return;
-    k_body_terms<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, q, derivs ? 1 : 0, which);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_body_terms", s, k_body_terms<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, q, derivs ? 1 : 0, which));
 }
 
 void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, KeyFmt fmt,
                    const Box* box, const double* q, int mode, int which, unsigned char* flag,
                    double* val, cudaStream_t s) {
     if (n == 0) return;
-    k_filter<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, fmt, box, q, mode, which, flag, val);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_filter", s, k_filter<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, fmt, box, q, mode, which, flag, val));
 }
 
 void launch_contact_terms(const SolverView& sv, const ContactView& cv, cudaStream_t s) {
     if (cv.n == 0) return;
-    k_contact_terms<<<grid_for(cv.n, kB), kB, 0, s>>>(sv, cv);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_contact_terms", s, k_contact_terms<<<grid_for(cv.n, kB), kB, 0, s>>>(sv, cv));
 }
 
 void launch_seg_offsets(const unsigned long long* keys, int n, KeyFmt fmt, int n_inst, int* off,
                         int field, const int* perm, cudaStream_t s) {
-    k_seg_offsets<<<grid_for(n_inst + 1, kB), kB, 0, s>>>(keys, n, fmt, n_inst, off, field, perm);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_seg_offsets", s, k_seg_offsets<<<grid_for(n_inst + 1, kB), kB, 0, s>>>(keys, n, fmt, n_inst, off, field, perm));
 }
 
 void launch_make_bkeys(const unsigned long long* keys, int n, KeyFmt fmt, unsigned long long* bkeys,
                        int* idx, cudaStream_t s) {
     if (n == 0) return;
-    k_make_bkeys<<<grid_for(n, kB), kB, 0, s>>>(keys, n, fmt, bkeys, idx);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_make_bkeys", s, k_make_bkeys<<<grid_for(n, kB), kB, 0, s>>>(keys, n, fmt, bkeys, idx));
 }
 
 void launch_assemble(const SolverView& sv, const ContactView& cv, double* row_trace,
                      cudaStream_t s) {
     if (sv.n_rows == 0) return;
-    k_assemble<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, cv, row_trace);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_assemble", s, k_assemble<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, cv, row_trace));
 }
 
 void launch_precond(const SolverView& sv, cudaStream_t s) {
     if (sv.n_rows == 0) return;
-    k_precond<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_precond", s, k_precond<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv));
 }
 
 int segsum_chunks(int n) { return std::max(1, (n + kCH - 1) / kCH); }
@@ -841,11 +836,9 @@ void launch_segsum_rows(const double* v, int n, const int* rpart, int P, int par
                         double* partial, double* dst, int stride, bool accumulate, cudaStream_t s) {
     const int nc = segsum_chunks(n);
     if (n > 0) {
-        k_segsum_partial<<<nc, kB, 0, s>>>(v, n, P, part_base, RowPart{rpart}, partial);
-        CUDA_CHECK(cudaGetLastError());
+        DABD_LAUNCH("k_segsum_partial", s, k_segsum_partial<<<nc, kB, 0, s>>>(v, n, P, part_base, RowPart{rpart}, partial));
     }
-    k_segsum_final<<<1, 32, 0, s>>>(partial, n > 0 ? nc : 0, P, dst, stride, accumulate ? 1 : 0);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_segsum_final", s, k_segsum_final<<<1, 32, 0, s>>>(partial, n > 0 ? nc : 0, P, dst, stride, accumulate ? 1 : 0));
 }
 
 void launch_segsum_keys(const double* v, int n, const unsigned long long* keys, KeyFmt fmt,
@@ -853,52 +846,44 @@ void launch_segsum_keys(const double* v, int n, const unsigned long long* keys, 
                         int stride, bool accumulate, cudaStream_t s) {
     const int nc = segsum_chunks(n);
     if (n > 0) {
-        k_segsum_partial<<<nc, kB, 0, s>>>(v, n, P, part_base, KeyPart{keys, fmt, ipart}, partial);
-        CUDA_CHECK(cudaGetLastError());
+        DABD_LAUNCH("k_segsum_partial", s, k_segsum_partial<<<nc, kB, 0, s>>>(v, n, P, part_base, KeyPart{keys, fmt, ipart}, partial));
     }
-    k_segsum_final<<<1, 32, 0, s>>>(partial, n > 0 ? nc : 0, P, dst, stride, accumulate ? 1 : 0);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_segsum_final", s, k_segsum_final<<<1, 32, 0, s>>>(partial, n > 0 ? nc : 0, P, dst, stride, accumulate ? 1 : 0));
 }
 
 void launch_pcg_init(const SolverView& sv, double* rz, double* rr, cudaStream_t s) {
     if (sv.n_rows == 0) return;
-    k_pcg_init<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, rz, rr);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_pcg_init", s, k_pcg_init<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, rz, rr));
 }
 
 void launch_pcg_spmv(const SolverView& sv, const double* pold, double* pnew, const double* beta,
                      double* pap_row, cudaStream_t s) {
     if (sv.n_rows == 0) return;
-    k_pcg_spmv<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, pold, pnew, beta, pap_row);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_pcg_spmv", s, k_pcg_spmv<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, pold, pnew, beta, pap_row));
 }
 
 void launch_pcg_update(const SolverView& sv, const double* pnew, const double* alpha, double* rz,
                        double* rr, cudaStream_t s) {
     if (sv.n_rows == 0) return;
-    k_pcg_update<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, pnew, alpha, rz, rr);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_pcg_update", s, k_pcg_update<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, pnew, alpha, rz, rr));
 }
 
 void launch_make_trial(const SolverView& sv, bool use_alpha, double alpha, int which,
                        cudaStream_t s) {
     if (sv.n_inst == 0) return;
-    k_make_trial<<<grid_for(sv.n_inst, kB), kB, 0, s>>>(sv, use_alpha ? 1 : 0, alpha, which);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_make_trial", s, k_make_trial<<<grid_for(sv.n_inst, kB), kB, 0, s>>>(sv, use_alpha ? 1 : 0, alpha, which));
 }
 
 void launch_dq_inf(const SolverView& sv, cudaStream_t s) {
     if (sv.n_rows == 0) return;
-    k_dq_inf<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_dq_inf", s, k_dq_inf<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv));
 }
 
 void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, KeyFmt fmt,
                 const Box* box0, const double* q0, const double* q1, int which,
                 double* earliest_override, cudaStream_t s) {
     if (n == 0) return;
-    k_ccd<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, fmt, box0, q0, q1, which, earliest_override);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_ccd", s, k_ccd<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, fmt, box0, q0, q1, which, earliest_override));
 }
 
 } // namespace dabd_gpu

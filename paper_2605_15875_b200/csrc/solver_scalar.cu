@@ -1,6 +1,8 @@
 // Per-partition scalar updates of the batched Newton/PCG (see kernels.hpp).
 #include "kernels.hpp"
 
+#include "instrument.hpp"
+
 namespace dabd_gpu {
 
 namespace {
@@ -96,8 +98,7 @@ __global__ void k_scalar(PartState* ps, int P, int op, double* a, double* b, dou
 
 void launch_scalar(PartState* ps, int P, int op, double* a, double* b, double* c, double tol,
                    int max_iters, int* err, cudaStream_t s) {
-    k_scalar<<<1, 32, 0, s>>>(ps, P, op, a, b, c, tol, max_iters, err);
-    CUDA_CHECK(cudaGetLastError());
+    DABD_LAUNCH("k_scalar", s, k_scalar<<<1, 32, 0, s>>>(ps, P, op, a, b, c, tol, max_iters, err));
 }
 
 } // namespace dabd_gpu
