@@ -359,41 +359,11 @@ void Engine::derivatives() {
 }
 
 void Engine::pcg() {
-    SolverView v = view();
-    scal_b_.resize(P_);
-    DBuf<double>& rz_new = gate_; // [P] scratch
-    launch_pcg_init(v, rowtmp_.get(), rowtmp2_.get(), s_);
-    launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
-                       ps_field(ps_.get(), &PartState::rz), kPsStride, false, s_);
-    launch_segsum_rows(rowtmp2_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
-                       ps_field(ps_.get(), &PartState::rr), kPsStride, false, s_);
-    launch_scalar(ps_.get(), P_, kOpPcgStart, scal_a_.get(), nullptr, nullptr, 0.0, 0, err_.get(),
-                  s_);
-    double* pold = p0v_.get();
-    double* pnew = p1v_.get();
-    for (int it = 0; it < pcg_max_; ++it) {
-        launch_pcg_spmv(v, pold, pnew, scal_a_.get(), rowtmp_.get(), s_);
-        launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
-                           ps_field(ps_.get(), &PartState::pap), kPsStride, false, s_);
-        launch_scalar(ps_.get(), P_, kOpPcgAlpha, scal_b_.get(), nullptr, nullptr, 0.0, 0,
-                      err_.get(), s_);
-        launch_pcg_update(v, pnew, scal_b_.get(), rowtmp_.get(), rowtmp2_.get(), s_);
-        launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
-                           rz_new.get(), 1, false, s_);
-        launch_segsum_rows(rowtmp2_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
-                           ps_field(ps_.get(), &PartState::rr), kPsStride, false, s_);
-        launch_scalar(ps_.get(), P_, kOpPcgBeta, scal_a_.get(), rz_new.get(), nullptr, pcg_tol_,
-                      pcg_max_, err_.get(), s_);
-        std::swap(pold, pnew);
-        if ((it & 7) == 7 || it + 1 == pcg_max_) {
-            CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
-                                       cudaMemcpyDeviceToHost, s_));
-            CUDA_CHECK(cudaStreamSynchronize(s_));
-            bool all = true;
-            for (int p = 0; p < P_; ++p) all &= (!ps_h_[p].active || ps_h_[p].pcg_done);
-            if (all) break;
-        }
-    }
+    if (n_rows_ == 0) return;
+    pbuf_.resize(12 * static_cast<size_t>(n_rows_));
+    pcg_part_.resize(3 * static_cast<size_t>(pcg_grid_size(n_rows_)) * P_);
+    launch_pcg_persistent(view(), pbuf_.get(), pcg_part_.get(), rowtmp_.get(), pcg_tol_, pcg_max_,
+                          s_);
 }
 
 NewtonResult Engine::newton_batch(int max_iters, double tol) {
@@ -413,13 +383,13 @@ NewtonResult Engine::newton_batch(int max_iters, double tol) {
         launch_scalar(ps_.get(), P_, kOpIterBegin, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
         derivatives();
         pcg();
-        for (int p = 0; p < P_; ++p) pcg_total += ps_h_[p].active ? ps_h_[p].pcg_iters : 0;
         launch_dq_inf(v, s_);
         launch_scalar(ps_.get(), P_, kOpNewtonCheck, nullptr, nullptr, nullptr, 0.0, 0, err_.get(),
                       s_);
         CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
                                    cudaMemcpyDeviceToHost, s_));
         check_err("newton: solve");
+        for (int p = 0; p < P_; ++p) pcg_total += ps_h_[p].pcg_iters;
         any = false;
         for (int p = 0; p < P_; ++p) any |= ps_h_[p].active != 0;
         if (!any) break;

@@ -159,6 +159,7 @@ class Engine {
     DBuf<double> ifs_; // per-instance force split (fx, fy)
     SimParams frame_params_;
     int project_ = 1;
+    DBuf<double> pbuf_, pcg_part_;
 };
 
 } // namespace dabd_gpu

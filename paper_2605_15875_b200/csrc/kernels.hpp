@@ -39,6 +39,12 @@ void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, Key
                 const Box* box0, const double* q0, const double* q1, int which,
                 double* earliest_override, cudaStream_t s);
 
+// Persistent cooperative block-Jacobi PCG over all partitions (pcg.cu).
+// pbuf: 12 * n_rows doubles; partials: 3 * pcg_grid_size(n_rows) * P doubles.
+int pcg_grid_size(int n_rows);
+void launch_pcg_persistent(const SolverView& sv, double* pbuf, double* partials, double* rowval,
+                           double tol, int max_iters, cudaStream_t s);
+
 // Per-partition scalar steps (solver_scalar.cu). `op` selects the update.
 enum ScalarOp : int {
     kOpPcgStart = 0,  // bnorm2 = rr; pcg_done = (bnorm2 == 0); iters = 0; beta = 0

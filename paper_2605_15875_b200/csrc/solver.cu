@@ -550,20 +550,26 @@ __global__ void k_precond(SolverView sv) {
 // ---------------------------------------------------------------------------
 constexpr int kCH = 1024;
 
+// One launch: every block writes its chunk's per-partition partials, the
+// last block to finish (threadfence + ticket) folds them in chunk order with
+// a fixed warp butterfly, so the result is bitwise reproducible.
 template <typename PartOf>
-__global__ void k_segsum_partial(const double* v, int n, int P, int part_base, PartOf pof,
-                                 double* partial) {
+__global__ void k_segsum(const double* v, int n, int P, int part_base, PartOf pof,
+                         double* partial, unsigned* ticket, double* dst, int stride,
+                         int accumulate) {
     __shared__ double sh[kB];
+    __shared__ bool last;
     const int c = blockIdx.x;
     const int s0 = c * kCH, s1 = min(n, s0 + kCH);
     // partitions present in this chunk: [pof(s0), pof(s1-1)]
     const int plo = s0 < s1 ? pof(s0) - part_base : 0;
     const int phi = s0 < s1 ? pof(s1 - 1) - part_base : -1;
-    for (int p = 0; p < P; ++p) {
+    for (int p = threadIdx.x; p < P; p += kB)
+        if (p < plo || p > phi) partial[static_cast<size_t>(c) * P + p] = 0.0;
+    for (int p = plo; p <= phi; ++p) {
         double acc = 0.0;
-        if (p >= plo && p <= phi)
-            for (int t = s0 + threadIdx.x; t < s1; t += kB)
-                if (pof(t) - part_base == p) acc += v[t];
+        for (int t = s0 + threadIdx.x; t < s1; t += kB)
+            if (plo == phi || pof(t) - part_base == p) acc += v[t];
         sh[threadIdx.x] = acc;
         __syncthreads();
         for (int w = kB / 2; w > 0; w >>= 1) {
@@ -573,16 +579,24 @@ __global__ void k_segsum_partial(const double* v, int n, int P, int part_base, P
         if (threadIdx.x == 0) partial[static_cast<size_t>(c) * P + p] = sh[0];
         __syncthreads();
     }
-}
-
-__global__ void k_segsum_final(const double* partial, int nchunks, int P, double* dst,
-                               int stride, int accumulate) {
-    const int p = threadIdx.x;
-    if (p >= P) return;
-    double s = 0.0;
-    for (int c = 0; c < nchunks; ++c) s += partial[static_cast<size_t>(c) * P + p];
-    if (accumulate) dst[p * stride] += s;
-    else dst[p * stride] = s;
+    __threadfence();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int p = warp; p < P; p += kB / 32) {
+        double s = 0.0;
+        for (int k = lane; k < static_cast<int>(gridDim.x); k += 32)
+            s += __ldcg(partial + static_cast<size_t>(k) * P + p);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) {
+            if (accumulate) dst[p * stride] += s;
+            else dst[p * stride] = s;
+        }
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 
 struct RowPart {
@@ -832,23 +846,30 @@ void launch_precond(const SolverView& sv, cudaStream_t s) {
 
 int segsum_chunks(int n) { return std::max(1, (n + kCH - 1) / kCH); }
 
+// Ticket for the last-block fold; launches on one device are stream ordered.
+__device__ unsigned g_segsum_ticket = 0;
+
+static unsigned* segsum_ticket() {
+    void* p = nullptr;
+    CUDA_CHECK(cudaGetSymbolAddress(&p, g_segsum_ticket));
+    return static_cast<unsigned*>(p);
+}
+
 void launch_segsum_rows(const double* v, int n, const int* rpart, int P, int part_base,
                         double* partial, double* dst, int stride, bool accumulate, cudaStream_t s) {
     const int nc = segsum_chunks(n);
-    if (n > 0) {
-        DABD_LAUNCH("k_segsum_partial", s, k_segsum_partial<<<nc, kB, 0, s>>>(v, n, P, part_base, RowPart{rpart}, partial));
-    }
-    DABD_LAUNCH("k_segsum_final", s, k_segsum_final<<<1, 32, 0, s>>>(partial, n > 0 ? nc : 0, P, dst, stride, accumulate ? 1 : 0));
+    DABD_LAUNCH("k_segsum", s,
+                k_segsum<<<nc, kB, 0, s>>>(v, n, P, part_base, RowPart{rpart}, partial,
+                                           segsum_ticket(), dst, stride, accumulate ? 1 : 0));
 }
 
 void launch_segsum_keys(const double* v, int n, const unsigned long long* keys, KeyFmt fmt,
                         const int* ipart, int P, int part_base, double* partial, double* dst,
                         int stride, bool accumulate, cudaStream_t s) {
     const int nc = segsum_chunks(n);
-    if (n > 0) {
-        DABD_LAUNCH("k_segsum_partial", s, k_segsum_partial<<<nc, kB, 0, s>>>(v, n, P, part_base, KeyPart{keys, fmt, ipart}, partial));
-    }
-    DABD_LAUNCH("k_segsum_final", s, k_segsum_final<<<1, 32, 0, s>>>(partial, n > 0 ? nc : 0, P, dst, stride, accumulate ? 1 : 0));
+    DABD_LAUNCH("k_segsum", s,
+                k_segsum<<<nc, kB, 0, s>>>(v, n, P, part_base, KeyPart{keys, fmt, ipart}, partial,
+                                           segsum_ticket(), dst, stride, accumulate ? 1 : 0));
 }
 
 void launch_pcg_init(const SolverView& sv, double* rz, double* rr, cudaStream_t s) {
