@@ -89,6 +89,7 @@ enum DevError : int {
     kErrFactor = 7,         // newton.cpp:26-27 analogue: non-SPD block
     kErrLineSearch = 8,     // newton.cpp:60-62
     kErrReplica = 9,        // runtime.cpp:384-385 replica rho mismatch
+    kErrSettle = 10,        // sim.cpp:239 Newton stepping failed to settle
 };
 
 __device__ __forceinline__ void raise(int* err, int code) { atomicCAS(err, 0, code); }

@@ -2,6 +2,7 @@
 #include "engine.hpp"
 
 #include "admm.hpp"
+#include "instrument.hpp"
 
 #include <cub/cub.cuh>
 
@@ -10,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <functional>
 #include <numeric>
 
 namespace dabd_gpu {
@@ -84,10 +86,18 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     pin_d_.resize(64);
     cellmax_.resize(1);
     nsel_.resize(1);
+    ctrl_.resize(1);
+    ctrl_.zero(s_);
+    ctrl_h_.resize(1);
+    trace_dev_.resize(8 * static_cast<size_t>(trace_cap_));
+    qd_start_.resize(6 * std::max(hs_.nb, 1));
+    if (const char* e = std::getenv("DABD_GPU_NO_GRAPH")) use_graph_ = e[0] == '0';
     sync();
 }
 
 Engine::~Engine() {
+    if (exec_) cudaGraphExecDestroy(exec_);
+    for (cudaStream_t s : cap_streams_) cudaStreamDestroy(s);
     if (own_stream_ && s_) cudaStreamDestroy(s_);
 }
 
@@ -154,6 +164,8 @@ void Engine::build_instances(const std::vector<std::vector<int>>& per_part, cons
     n_rows_ = static_cast<int>(h_rinst_.size());
     if (n_inst_ >= (1 << 22)) throw InvalidArg("too many body instances for the candidate key");
     single_domain_ = single_domain;
+    ref_ready_ = false; // the N=1 frame graph refers to the previous instance set
+    graph_ok_ = false;
     ibody_.upload(h_ibody_, s_);
     ipart_.upload(h_ipart_, s_);
     irow_.upload(h_irow_, s_);
@@ -241,7 +253,8 @@ SolverView Engine::view() {
 
 ContactView Engine::cview() {
     ContactView c;
-    c.n = n_contacts_;
+    c.n = cap_;          // grid / buffer capacity
+    c.dn = nsel_.get();  // device-side active-contact count
     c.fmt = cfmt_;
     c.key = ckey_.get();
     c.perm_b = perm_b_.get();
@@ -264,72 +277,31 @@ InstView Engine::iview(const double* q0, const double* q1) {
 }
 
 // ---------------------------------------------------------------------------
-// local solve
+// local solve: enqueue-only building blocks (no host reads, capturable)
 // ---------------------------------------------------------------------------
-void Engine::reset_parts(double tol) {
+void Engine::prepare_solver() {
+    // per-partition constants (ndof) live in PartState; kOpReset keeps them
     for (int p = 0; p < P_; ++p) {
         PartState& s = ps_h_[p];
         std::memset(&s, 0, sizeof(PartState));
         s.ndof = 6 * (h_pro_[p + 1] - h_pro_[p]);
-        s.active = s.ndof > 0 ? 1 : 0;
-        s.converged = s.ndof > 0 ? 0 : 1;
-        s.tol = tol;
         s.toi_earliest = 2.0;
         s.alpha = 1.0;
     }
     CUDA_CHECK(cudaMemcpyAsync(ps_.get(), ps_h_.get(), P_ * sizeof(PartState),
                                cudaMemcpyHostToDevice, s_));
-}
-
-int Engine::build_superset(const double* q0, const double* q1, bool swept, double margin) {
-    n_super_ = det_.build(ds_.view(), iview(q0, q1), stat_.get(), static_cast<int>(h_stat_.size()),
-                          swept, margin, ds_.max_verts, s_);
-    cflag_.resize(std::max(n_super_, 1));
-    sval_.resize(std::max(n_super_, 1));
-    return n_super_;
-}
-
-void Engine::eval_energy(const double* q, int which, double PartState::*field) {
-    SolverView v = view();
-    box_.resize(std::max(n_inst_, 1));
-    launch_inst_boxes(v.sc, iview(q, q), false, frame_params_.d_hat, box_.get(), cellmax_.get(), s_);
-    launch_body_terms(v, q, false, which, s_);
-    double* dst = ps_field(ps_.get(), field);
-    launch_segsum_rows(rval_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(), dst, kPsStride,
-                       false, s_);
-    if (n_super_ > 0) {
-        launch_filter(v, det_.keys(), n_super_, det_.fmt(), box_.get(), q, 1, which, nullptr,
-                      sval_.get(), s_);
-        partial_.resize(static_cast<size_t>(segsum_chunks(n_super_)) * P_ + P_);
-        launch_segsum_keys(sval_.get(), n_super_, det_.keys(), det_.fmt(), ipart_.get(), P_, p0_,
-                           partial_.get(), dst, kPsStride, true, s_);
+    const int want = std::max(cap_, 48 * std::max(n_inst_, 1) + 4096);
+    if (want != cap_ || det_.cap() != want || det_fmt_n_ != n_inst_) {
+        cap_ = want;
+        det_.prepare(n_inst_, ds_.max_verts, cap_);
+        det_fmt_n_ = n_inst_;
+        graph_ok_ = false;
     }
-}
-
-void Engine::derivatives() {
-    SolverView v = view();
-    box_.resize(std::max(n_inst_, 1));
-    launch_inst_boxes(v.sc, iview(iq_.get(), iq_.get()), false, frame_params_.d_hat, box_.get(),
-                      cellmax_.get(), s_);
-    launch_body_terms(v, iq_.get(), true, 0, s_);
-    n_contacts_ = 0;
-    cfmt_ = det_.fmt();
-    if (n_super_ > 0) {
-        launch_filter(v, det_.keys(), n_super_, cfmt_, box_.get(), iq_.get(), 0, 0, cflag_.get(),
-                      nullptr, s_);
-        ckey_.resize(n_super_);
-        size_t tb = 0;
-        CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, tb, det_.keys(), cflag_.get(), ckey_.get(),
-                                              nsel_.get(), n_super_, s_));
-        temp_.resize(tb);
-        CUDA_CHECK(cub::DeviceSelect::Flagged(temp_.get(), tb, det_.keys(), cflag_.get(),
-                                              ckey_.get(), nsel_.get(), n_super_, s_));
-        CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 1, nsel_.get(), sizeof(int),
-                                   cudaMemcpyDeviceToHost, s_));
-        CUDA_CHECK(cudaStreamSynchronize(s_));
-        n_contacts_ = pin_i_[1];
-    }
-    const int C = std::max(n_contacts_, 1);
+    const size_t C = static_cast<size_t>(cap_);
+    const size_t before = cflag_.capacity() + ckey_.capacity() + cmat_.capacity();
+    cflag_.resize(C);
+    sval_.resize(C);
+    ckey_.resize(C);
     cval_.resize(C);
     cgrad_.resize(12 * C);
     cmat_.resize(21 * C);
@@ -337,91 +309,141 @@ void Engine::derivatives() {
     bkey_sorted_.resize(C);
     bidx_.resize(C);
     perm_b_.resize(C);
-    if (n_contacts_ > 0) {
-        launch_contact_terms(v, cview(), s_);
-        launch_make_bkeys(ckey_.get(), n_contacts_, cfmt_, bkey_.get(), bidx_.get(), s_);
-        size_t tb = 0;
-        CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, bkey_.get(), bkey_sorted_.get(),
-                                                   bidx_.get(), perm_b_.get(), n_contacts_, 0,
-                                                   cfmt_.total_bits(), s_));
-        temp_.resize(tb);
-        CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp_.get(), tb, bkey_.get(), bkey_sorted_.get(),
-                                                   bidx_.get(), perm_b_.get(), n_contacts_, 0,
-                                                   cfmt_.total_bits(), s_));
-    }
-    launch_seg_offsets(ckey_.get(), n_contacts_, cfmt_, n_inst_, aoff_.get(), 0, nullptr, s_);
-    launch_seg_offsets(ckey_.get(), n_contacts_, cfmt_, n_inst_, boff_.get(), 1, perm_b_.get(), s_);
-    launch_assemble(v, cview(), rowtmp_.get(), s_);
+    partial_.resize(static_cast<size_t>(segsum_chunks(std::max(cap_, n_rows_))) * P_ + P_);
+    pbuf_.resize(12 * static_cast<size_t>(std::max(n_rows_, 1)));
+    pcg_part_.resize(3 * static_cast<size_t>(pcg_grid_size(std::max(n_rows_, 1))) * P_);
+    box_.resize(std::max(n_inst_, 1));
+    size_t t1 = 0, t2 = 0;
+    CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, t1, det_.keys(), cflag_.get(), ckey_.get(),
+                                          nsel_.get(), cap_));
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t2, bkey_.get(), bkey_sorted_.get(),
+                                               bidx_.get(), perm_b_.get(), cap_, 0,
+                                               det_.fmt().total_bits()));
+    temp_bytes_ = std::max(t1, t2);
+    temp_.resize(temp_bytes_);
+    if (cflag_.capacity() + ckey_.capacity() + cmat_.capacity() != before) graph_ok_ = false;
+    cfmt_ = det_.fmt();
+}
+
+void Engine::enq_superset(const double* q0, const double* q1, bool swept) {
+    det_.enqueue(ds_.view(), iview(q0, q1), stat_.get(), static_cast<int>(h_stat_.size()), swept,
+                 frame_params_.d_hat, err_.get(), s_);
+}
+
+void Engine::enq_energy(const double* q, int which, double PartState::*field) {
+    SolverView v = view();
+    launch_inst_boxes(v.sc, iview(q, q), false, frame_params_.d_hat, box_.get(), cellmax_.get(), s_);
+    launch_body_terms(v, q, false, which, s_);
+    double* dst = ps_field(ps_.get(), field);
+    launch_segsum_rows(rval_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(), dst, kPsStride,
+                       false, s_);
+    launch_filter(v, det_.keys(), cap_, det_.d_count(), cfmt_, box_.get(), q, 1, which, nullptr,
+                  sval_.get(), s_);
+    launch_segsum_keys(sval_.get(), cap_, det_.d_count(), det_.keys(), cfmt_, ipart_.get(), P_, p0_,
+                       partial_.get(), dst, kPsStride, true, s_);
+}
+
+void Engine::enq_derivatives() {
+    SolverView v = view();
+    launch_inst_boxes(v.sc, iview(iq_.get(), iq_.get()), false, frame_params_.d_hat, box_.get(),
+                      cellmax_.get(), s_);
+    launch_body_terms(v, iq_.get(), true, 0, s_);
+    launch_filter(v, det_.keys(), cap_, det_.d_count(), cfmt_, box_.get(), iq_.get(), 0, 0,
+                  cflag_.get(), nullptr, s_);
+    size_t tb = temp_bytes_;
+    CUDA_CHECK(cub::DeviceSelect::Flagged(temp_.get(), tb, det_.keys(), cflag_.get(), ckey_.get(),
+                                          nsel_.get(), cap_, s_));
+    const ContactView cv = cview();
+    launch_contact_terms(v, cv, s_);
+    launch_make_bkeys(ckey_.get(), cap_, nsel_.get(), cfmt_, bkey_.get(), bidx_.get(), s_);
+    tb = temp_bytes_;
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp_.get(), tb, bkey_.get(), bkey_sorted_.get(),
+                                               bidx_.get(), perm_b_.get(), cap_, 0,
+                                               cfmt_.total_bits(), s_));
+    launch_seg_offsets(ckey_.get(), cap_, nsel_.get(), cfmt_, n_inst_, aoff_.get(), 0, nullptr, s_);
+    launch_seg_offsets(ckey_.get(), cap_, nsel_.get(), cfmt_, n_inst_, boff_.get(), 1,
+                       perm_b_.get(), s_);
+    launch_assemble(v, cv, rowtmp_.get(), s_);
     launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
                        ps_field(ps_.get(), &PartState::trace), kPsStride, false, s_);
-    launch_scalar(ps_.get(), P_, kOpEps, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
+    launch_scalar(ps_.get(), P_, kOpEps, ctrl_.get(), hd_, 0.0, 0, err_.get(), s_);
     if (project_) launch_precond(v, s_); // unprojected blocks (objective mode 3) may be indefinite
 }
 
-void Engine::pcg() {
+void Engine::enq_pcg() {
     if (n_rows_ == 0) return;
-    pbuf_.resize(12 * static_cast<size_t>(n_rows_));
-    pcg_part_.resize(3 * static_cast<size_t>(pcg_grid_size(n_rows_)) * P_);
     launch_pcg_persistent(view(), pbuf_.get(), pcg_part_.get(), rowtmp_.get(), pcg_tol_, pcg_max_,
                           s_);
 }
 
-NewtonResult Engine::newton_batch(int max_iters, double tol) {
-    reset_parts(tol);
-    NewtonResult res;
-    bool any = false;
-    for (int p = 0; p < P_; ++p) any |= ps_h_[p].active != 0;
-    if (!any) {
-        res.converged = 1;
-        return res;
-    }
+// newton.cpp:16-69, one iteration for every partition still active.
+void Engine::enq_newton_head(int max_iters) {
     SolverView v = view();
-    build_superset(iq_.get(), iq_.get(), false, frame_params_.d_hat);
-    eval_energy(iq_.get(), 0, &PartState::energy);
-    int pcg_total = 0;
-    for (int iter = 0; iter < max_iters; ++iter) {
-        launch_scalar(ps_.get(), P_, kOpIterBegin, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
-        derivatives();
-        pcg();
-        launch_dq_inf(v, s_);
-        launch_scalar(ps_.get(), P_, kOpNewtonCheck, nullptr, nullptr, nullptr, 0.0, 0, err_.get(),
+    launch_scalar(ps_.get(), P_, kOpIterBegin, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
+    enq_derivatives();
+    enq_pcg();
+    launch_dq_inf(v, s_);
+    launch_scalar(ps_.get(), P_, kOpNewtonCheck, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
+}
+
+// CCD bound over [q, q + dq] on the swept superset (newton.cpp:38-42).
+void Engine::enq_newton_ccd() {
+    SolverView v = view();
+    launch_make_trial(v, false, 1.0, 0, s_);
+    enq_superset(iq_.get(), iqtry_.get(), true);
+    launch_inst_boxes(v.sc, iview(iq_.get(), iqtry_.get()), true, 0.0, box_.get(), cellmax_.get(),
                       s_);
-        CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
-                                   cudaMemcpyDeviceToHost, s_));
-        check_err("newton: solve");
-        for (int p = 0; p < P_; ++p) pcg_total += ps_h_[p].pcg_iters;
-        any = false;
-        for (int p = 0; p < P_; ++p) any |= ps_h_[p].active != 0;
-        if (!any) break;
-        // CCD bound over [q, q + dq] (newton.cpp:38-42) on the swept superset
-        launch_make_trial(v, false, 1.0, 0, s_);
-        build_superset(iq_.get(), iqtry_.get(), true, frame_params_.d_hat);
-        box_.resize(std::max(n_inst_, 1));
-        launch_inst_boxes(v.sc, iview(iq_.get(), iqtry_.get()), true, 0.0, box_.get(),
-                          cellmax_.get(), s_);
-        launch_ccd(v, det_.keys(), n_super_, det_.fmt(), box_.get(), iq_.get(), iqtry_.get(), 0,
-                   nullptr, s_);
-        launch_scalar(ps_.get(), P_, kOpAlphaMax, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
-        // backtracking with pure decrease (newton.cpp:44-62)
-        for (int trial = 0; trial < 64; ++trial) {
-            launch_make_trial(v, true, 0.0, 1, s_);
-            eval_energy(iqtry_.get(), 1, &PartState::trial);
-            launch_scalar(ps_.get(), P_, kOpAccept, nullptr, nullptr, nullptr, 0.0, 0, err_.get(), s_);
-            launch_accept_copy(n_inst_, ipart_.get(), p0_, ps_.get(), iqtry_.get(), iq_.get(), s_);
-            CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
-                                       cudaMemcpyDeviceToHost, s_));
-            check_err("newton: line search");
-            bool searching = false;
-            for (int p = 0; p < P_; ++p) searching |= ps_h_[p].searching != 0;
-            if (!searching) break;
+    launch_ccd(v, det_.keys(), cap_, det_.d_count(), cfmt_, box_.get(), iq_.get(), iqtry_.get(), 0,
+               nullptr, s_);
+    launch_scalar(ps_.get(), P_, kOpAlphaMax, ctrl_.get(), hd_, 0.0, 0, err_.get(), s_);
+}
+
+// One backtracking trial (newton.cpp:47-59) for every partition still searching.
+void Engine::enq_ls_trial() {
+    SolverView v = view();
+    launch_make_trial(v, true, 0.0, 1, s_);
+    enq_energy(iqtry_.get(), 1, &PartState::trial);
+    launch_scalar(ps_.get(), P_, kOpAccept, ctrl_.get(), hd_, 0.0, 0, err_.get(), s_);
+    launch_accept_copy(n_inst_, ipart_.get(), p0_, ps_.get(), iqtry_.get(), iq_.get(), s_);
+}
+
+void Engine::enq_solve_begin(double tol) {
+    launch_scalar(ps_.get(), P_, kOpReset, ctrl_.get(), hd_, tol, 0, err_.get(), s_);
+    enq_superset(iq_.get(), iq_.get(), false);
+    enq_energy(iq_.get(), 0, &PartState::energy);
+}
+
+FrameCtrl Engine::read_ctrl() {
+    CUDA_CHECK(cudaMemcpyAsync(ctrl_h_.get(), ctrl_.get(), sizeof(FrameCtrl),
+                               cudaMemcpyDeviceToHost, s_));
+    check_err("newton");
+    return ctrl_h_[0];
+}
+
+// Host-driven variant (parity entry points, multi-partition ADMM frames).
+NewtonResult Engine::newton_batch(int max_iters, double tol, bool reset_ctrl) {
+    hd_ = CondHandles{};
+    if (reset_ctrl) CUDA_CHECK(cudaMemsetAsync(ctrl_.get(), 0, sizeof(FrameCtrl), s_));
+    enq_solve_begin(tol);
+    FrameCtrl c = read_ctrl();
+    for (int iter = 0; iter < max_iters && c.any_active; ++iter) {
+        enq_newton_head(max_iters);
+        c = read_ctrl();
+        if (c.any_active) {
+            enq_newton_ccd();
+            c = read_ctrl();
+            for (int t = 0; t < 80 && c.any_searching; ++t) {
+                enq_ls_trial();
+                c = read_ctrl();
+            }
         }
-        any = false;
-        for (int p = 0; p < P_; ++p) any |= ps_h_[p].active != 0;
-        if (!any) break;
+        launch_scalar(ps_.get(), P_, kOpNewtonTail, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
+        c = read_ctrl();
     }
     CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
                                cudaMemcpyDeviceToHost, s_));
     check_err("newton: end");
+    NewtonResult res;
     res.converged = 1;
     for (int p = 0; p < P_; ++p) {
         res.iterations += ps_h_[p].iterations;
@@ -429,9 +451,83 @@ NewtonResult Engine::newton_batch(int max_iters, double tol) {
         res.converged &= ps_h_[p].converged;
         res.final_update = std::max(res.final_update, ps_h_[p].final_update);
     }
-    res.pcg_iters = pcg_total;
+    res.pcg_iters = c.pcg_total;
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, nsel_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 3, det_.d_count(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    sync();
+    n_contacts_ = pin_i_[2];
+    n_super_ = pin_i_[3];
     return res;
 }
+
+// ---------------------------------------------------------------------------
+// CUDA-graph capture helpers (conditional WHILE / IF nodes, CUDA 12.4+)
+// ---------------------------------------------------------------------------
+unsigned long long Engine::new_cond_handle() {
+    cudaStreamCaptureStatus st;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CUDA_CHECK(cudaStreamGetCaptureInfo(s_, &st, nullptr, &g, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+    return static_cast<unsigned long long>(h);
+}
+
+void Engine::add_cond_node(unsigned long long h, bool is_while, int level,
+                           const std::function<void()>& body) {
+    cudaStreamCaptureStatus st;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CUDA_CHECK(cudaStreamGetCaptureInfo(s_, &st, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = static_cast<cudaGraphConditionalHandle>(h);
+    p.conditional.type = is_while ? cudaGraphCondTypeWhile : cudaGraphCondTypeIf;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    CUDA_CHECK(cudaGraphAddNode(&node, g, deps, nd, &p));
+    CUDA_CHECK(cudaStreamUpdateCaptureDependencies(s_, &node, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t bg = p.conditional.phGraph_out[0];
+    cudaStream_t saved = s_;
+    s_ = cap_stream(level);
+    CUDA_CHECK(cudaStreamBeginCaptureToGraph(s_, bg, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeRelaxed));
+    const long long before = launch_counter().load();
+    body();
+    if (level < 8) nodes_inc_[level] = launch_counter().load() - before;
+    cudaGraph_t out;
+    CUDA_CHECK(cudaStreamEndCapture(s_, &out));
+    s_ = saved;
+}
+
+cudaStream_t Engine::cap_stream(int level) {
+    while (static_cast<int>(cap_streams_.size()) <= level) {
+        cudaStream_t s;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        cap_streams_.push_back(s);
+    }
+    return cap_streams_[level];
+}
+
+// Captured Newton solve: Reset -> superset -> energy -> WHILE(active) {
+//   head; IF(active) { CCD; WHILE(searching) { trial } }; tail }.
+void Engine::cap_newton(int max_iters, double tol, int level) {
+    hd_.newton = new_cond_handle();
+    enq_solve_begin(tol);
+    add_cond_node(hd_.newton, true, level, [&] {
+        hd_.step = new_cond_handle(); // set by kOpNewtonCheck inside the head
+        enq_newton_head(max_iters);
+        add_cond_node(hd_.step, false, level + 1, [&] {
+            hd_.ls = new_cond_handle();
+            enq_newton_ccd();
+            add_cond_node(hd_.ls, true, level + 2, [&] { enq_ls_trial(); });
+        });
+        launch_scalar(ps_.get(), P_, kOpNewtonTail, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
+    });
+}
+
 
 std::vector<double> Engine::delta_inf(const double* a, const double* b) {
     gate_.zero(s_);
@@ -542,7 +638,7 @@ double Engine::ccd_toi(const double* q0, const double* q1, const int* subset, in
     gate_.upload(init, s_);
     // margin-0 swept candidates are exactly the reference set; the filter
     // inside k_ccd re-applies the same predicate with the detector's boxes.
-    launch_ccd(view(), det_gate_.keys(), n, det_gate_.fmt(), det_gate_.boxes(), iq_.get(),
+    launch_ccd(view(), det_gate_.keys(), n, nullptr, det_gate_.fmt(), det_gate_.boxes(), iq_.get(),
                iqtry_.get(), 2, gate_.get(), s_);
     std::vector<double> e = gate_.to_host(s_);
     check_err("ccd_toi");
@@ -612,31 +708,37 @@ void Engine::objective(const ObjectiveIn& in, const double* q, int mode, double*
     DBuf<double> gq;
     gq.upload(q, 6 * static_cast<size_t>(hs_.nb), s_);
     gather_iq(gq.get());
-    reset_parts(0.0);
-    for (int p = 0; p < P_; ++p) ps_h_[p].active = 1;
-    CUDA_CHECK(cudaMemcpyAsync(ps_.get(), ps_h_.get(), P_ * sizeof(PartState),
-                               cudaMemcpyHostToDevice, s_));
-    build_superset(iq_.get(), iq_.get(), false, frame_params_.d_hat);
+    ref_ready_ = false;
+    prepare_solver();
+    hd_ = CondHandles{};
+    CUDA_CHECK(cudaMemsetAsync(ctrl_.get(), 0, sizeof(FrameCtrl), s_));
+    launch_scalar(ps_.get(), P_, kOpReset, ctrl_.get(), hd_, 0.0, 0, err_.get(), s_);
+    enq_superset(iq_.get(), iq_.get(), false);
     if (mode <= 1) {
-        eval_energy(iq_.get(), 2, &PartState::energy);
-        derivatives(); // counts only
+        enq_energy(iq_.get(), 2, &PartState::energy);
+        enq_derivatives(); // counts only
         CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
+                                   cudaMemcpyDeviceToHost, s_));
+        CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, nsel_.get(), sizeof(int),
                                    cudaMemcpyDeviceToHost, s_));
         sync();
         *value = ps_h_[0].energy;
-        *active = n_contacts_;
+        *active = pin_i_[2];
         *candidates = ps_h_[0].n_candidates;
         return;
     }
     // derivatives (value as the sum of body and contact terms)
     project_ = mode == 2 ? 1 : 0;
-    derivatives();
+    enq_derivatives();
     project_ = 1;
     CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
                                cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, nsel_.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                               s_));
     std::vector<double> rv = rval_.to_host(s_);
     std::vector<double> cv = cval_.to_host(s_);
     sync();
+    n_contacts_ = pin_i_[2];
     double val = 0.0;
     for (int r = 0; r < n_rows_; ++r) val += rv[r];
     for (int c = 0; c < n_contacts_; ++c) val += cv[c];
@@ -716,56 +818,168 @@ void Engine::run_frames(int n, FrameStats* stats) {
     }
 }
 
-// sim.cpp:186-249
-FrameStats Engine::frame_reference() {
-    FrameStats st;
-    frame_params_ = hs_.params;
+// ---------------------------------------------------------------------------
+// N = 1 frame (sim.cpp:207-247), captured once into a CUDA graph
+// ---------------------------------------------------------------------------
+void Engine::enq_reference_frame(bool graph) {
     const SimParams& P = frame_params_;
     const double h = P.h;
-    st.h = h;
-    std::vector<std::vector<int>> per(1);
-    per[0].resize(hs_.nb);
-    std::iota(per[0].begin(), per[0].end(), 0);
-    build_instances(per, nullptr, true);
-    {
-        std::vector<double> invk(std::max(n_inst_, 1), 1.0);
-        iinvk_.upload(invk, s_);
-    }
     const size_t nq = 6 * static_cast<size_t>(hs_.nb);
-    if (nq) CUDA_CHECK(cudaMemcpyAsync(q_start_.get(), q_.get(), nq * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, s_));
+    CUDA_CHECK(cudaMemcpyAsync(q_start_.get(), q_.get(), nq * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s_));
+    CUDA_CHECK(cudaMemcpyAsync(qd_start_.get(), qd_.get(), nq * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s_));
     gather_iq(q_.get());
     launch_predict(ds_.view(), n_inst_, ibody_.get(), iq_.get(), qd_.get(), h, P.gravity[0],
                    P.gravity[1], nullptr, iqt_.get(), s_);
     const double tol = P.theta * h * P.scene_scale;
-    double dq_inf = 0.0;
-    bool ended = false;
-    for (int k = 1; k <= hs_.admm_max_iterations; ++k) {
-        if (k > 1) {
-            const bool end = check_stopping(dq_inf, 0.0, 0.0, {1.0}, h, P.scene_scale, P.theta);
-            trace_.push_back({static_cast<double>(frame_counter_), 0.0, static_cast<double>(k),
-                              dq_inf, 0.0, 0.0, 1.0, end ? 1.0 : 0.0});
-            if (end) {
-                ended = true;
-                st.admm_iterations = k;
-                break;
-            }
+    auto admm_step = [&](int level) {
+        launch_frame_ctrl(ctrl_.get(), 0, gate_.get(), P_, h, P.scene_scale, P.theta,
+                          hs_.admm_max_iterations, trace_dev_.get(), trace_cap_, hd_, err_.get(),
+                          ps_.get(), s_);
+        CUDA_CHECK(cudaMemcpyAsync(iqbefore_.get(), iq_.get(), 6 * n_inst_ * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, s_));
+        if (graph) {
+            cap_newton(hs_.newton_cap, tol, level);
+        } else {
+            newton_batch(hs_.newton_cap, tol, false);
         }
-        if (n_inst_ * 6 > 0)
-            CUDA_CHECK(cudaMemcpyAsync(iqbefore_.get(), iq_.get(), 6 * n_inst_ * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, s_));
-        const NewtonResult r = newton_batch(hs_.newton_cap, tol);
-        st.newton_iterations += r.iterations;
-        st.line_search_steps += r.ls_steps;
-        st.pcg_iterations += r.pcg_iters;
-        st.max_contacts = std::max(st.max_contacts, n_contacts_);
-        st.max_candidates = std::max(st.max_candidates, n_super_);
-        dq_inf = n_rows_ ? delta_inf(iq_.get(), iqbefore_.get())[0] : 0.0;
+        CUDA_CHECK(cudaMemsetAsync(gate_.get(), 0, P_ * sizeof(double), s_));
+        launch_delta_inf(n_rows_, rinst_.get(), rpart_.get(), p0_, iq_.get(), iqbefore_.get(),
+                         gate_.get(), s_);
+        launch_frame_ctrl(ctrl_.get(), 1, gate_.get(), P_, h, P.scene_scale, P.theta,
+                          hs_.admm_max_iterations, trace_dev_.get(), trace_cap_, hd_, err_.get(),
+                          ps_.get(), s_);
+    };
+    if (graph) {
+        hd_.admm = new_cond_handle();
+        launch_frame_ctrl(ctrl_.get(), 2, gate_.get(), P_, h, P.scene_scale, P.theta,
+                          hs_.admm_max_iterations, trace_dev_.get(), trace_cap_, hd_, err_.get(),
+                          ps_.get(), s_);
+        add_cond_node(hd_.admm, true, 0, [&] { admm_step(1); });
+    } else {
+        launch_frame_ctrl(ctrl_.get(), 2, gate_.get(), P_, h, P.scene_scale, P.theta,
+                          hs_.admm_max_iterations, trace_dev_.get(), trace_cap_, hd_, err_.get(),
+                          ps_.get(), s_);
+        for (int k = 1; k <= hs_.admm_max_iterations + 1; ++k) {
+            const FrameCtrl c = read_ctrl();
+            if (c.ended || c.failed) break;
+            admm_step(0);
+        }
     }
-    if (!ended) throw Error("run_reference: Newton stepping failed to settle");
     launch_commit(ds_.view(), n_inst_, ibody_.get(), ipart_.get(), ianc_.get(), nullptr, iq_.get(),
                   iznext_.get(), q_start_.get(), h, q_.get(), qd_.get(), s_);
+}
+
+void Engine::capture_reference_graph() {
+    if (exec_) {
+        cudaGraphExecDestroy(exec_);
+        exec_ = nullptr;
+    }
+    KernelTimer::get().suspend(true);
+    hd_ = CondHandles{};
+    hd_.graph = 1;
+    CUDA_CHECK(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
+    try {
+        const long long c0 = launch_counter().load();
+        for (long long& v : nodes_inc_) v = 0;
+        enq_reference_frame(true);
+        nodes_total_ = launch_counter().load() - c0;
+        launch_counter() -= nodes_total_; // captured, not executed
+    } catch (...) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(s_, &g);
+        KernelTimer::get().suspend(false);
+        hd_ = CondHandles{};
+        throw;
+    }
+    cudaGraph_t g;
+    CUDA_CHECK(cudaStreamEndCapture(s_, &g));
+    KernelTimer::get().suspend(false);
+    CUDA_CHECK(cudaGraphInstantiate(&exec_, g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+    hd_ = CondHandles{};
+    graph_ok_ = true;
+}
+
+// sim.cpp:186-249
+FrameStats Engine::frame_reference() {
+    frame_params_ = hs_.params;
+    if (!ref_ready_) {
+        std::vector<std::vector<int>> per(1);
+        per[0].resize(hs_.nb);
+        std::iota(per[0].begin(), per[0].end(), 0);
+        build_instances(per, nullptr, true);
+        std::vector<double> invk(std::max(n_inst_, 1), 1.0);
+        iinvk_.upload(invk, s_);
+        prepare_solver();
+        ref_ready_ = true;
+        graph_ok_ = false;
+    }
+    FrameStats st;
+    st.h = frame_params_.h;
+    for (int attempt = 0; attempt < 6; ++attempt) {
+        FrameCtrl init{};
+        init.frame = static_cast<double>(frame_counter_);
+        ctrl_h_[0] = init;
+        CUDA_CHECK(cudaMemcpyAsync(ctrl_.get(), ctrl_h_.get(), sizeof(FrameCtrl),
+                                   cudaMemcpyHostToDevice, s_));
+        if (use_graph_ && hs_.nb > 0) {
+            if (!graph_ok_) capture_reference_graph();
+            CUDA_CHECK(cudaGraphLaunch(exec_, s_));
+            graph_replayed_ = true;
+        } else {
+            enq_reference_frame(false);
+        }
+        CUDA_CHECK(cudaMemcpyAsync(ctrl_h_.get(), ctrl_.get(), sizeof(FrameCtrl),
+                                   cudaMemcpyDeviceToHost, s_));
+        CUDA_CHECK(cudaMemcpyAsync(pin_i_.get(), err_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+        CUDA_CHECK(cudaStreamSynchronize(s_));
+        if (pin_i_[0] == kErrCapacity) {
+            // grow the fixed capacities, restore the frame start and redo it
+            err_.zero(s_);
+            const size_t nq = 6 * static_cast<size_t>(hs_.nb);
+            CUDA_CHECK(cudaMemcpyAsync(q_.get(), q_start_.get(), nq * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s_));
+            CUDA_CHECK(cudaMemcpyAsync(qd_.get(), qd_start_.get(), nq * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s_));
+            cap_ *= 2;
+            det_fmt_n_ = -1;
+            prepare_solver();
+            graph_ok_ = false;
+            continue;
+        }
+        check_err("frame_reference");
+        break;
+    }
+    const FrameCtrl& c = ctrl_h_[0];
+    if (graph_replayed_) { // kernels the replay executed: nodes per body x body executions
+        count_launch(nodes_total_ - nodes_inc_[0] +
+                     static_cast<long long>(c.exec_admm) * (nodes_inc_[0] - nodes_inc_[1]) +
+                     static_cast<long long>(c.exec_newton) * (nodes_inc_[1] - nodes_inc_[2]) +
+                     static_cast<long long>(c.exec_step) * (nodes_inc_[2] - nodes_inc_[3]) +
+                     static_cast<long long>(c.exec_ls) * nodes_inc_[3]);
+        graph_replayed_ = false;
+    }
+    if (c.failed || !c.ended) throw Error("run_reference: Newton stepping failed to settle");
+    st.admm_iterations = c.admm_iterations;
+    st.newton_iterations = c.newton_total;
+    st.line_search_steps = c.ls_total;
+    st.pcg_iterations = c.pcg_total;
+    const int nt = std::min(c.trace_n, trace_cap_);
+    if (nt > 0) {
+        std::vector<double> rows(8 * static_cast<size_t>(nt));
+        CUDA_CHECK(cudaMemcpy(rows.data(), trace_dev_.get(), rows.size() * sizeof(double),
+                              cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nt; ++i)
+            trace_.push_back({rows[8 * i], rows[8 * i + 1], rows[8 * i + 2], rows[8 * i + 3],
+                              rows[8 * i + 4], rows[8 * i + 5], rows[8 * i + 6], rows[8 * i + 7]});
+    }
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, nsel_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 3, det_.d_count(), sizeof(int), cudaMemcpyDeviceToHost, s_));
     sync();
+    st.max_contacts = pin_i_[2];
+    st.max_candidates = pin_i_[3];
     st.committed = 1;
     return st;
 }
@@ -808,6 +1022,7 @@ FrameStats Engine::frame_admm(int frame) {
             for (int p = 0; p < P_; ++p)
                 if (mask[b] & (1u << (p0_ + p))) per[p].push_back(b);
         build_instances(per, mask.data(), false);
+        prepare_solver();
         const int I = n_inst_;
         std::vector<double> invk(std::max(I, 1)), rho(std::max(I, 1), 0.0), rho0(std::max(I, 1), 0.0),
             fs(2 * std::max(I, 1), 0.0);
@@ -875,7 +1090,7 @@ FrameStats Engine::frame_admm(int frame) {
                                                0.0, ds_.max_verts, s_);
                 std::vector<double> init(P_, 2.0);
                 gate_.upload(init, s_);
-                launch_ccd(view(), det_gate_.keys(), nc, det_gate_.fmt(), det_gate_.boxes(),
+                launch_ccd(view(), det_gate_.keys(), nc, nullptr, det_gate_.fmt(), det_gate_.boxes(),
                            iq_.get(), iqtry_.get(), 2, gate_.get(), s_);
                 std::vector<double> earliest = gate_.to_host(s_);
                 std::vector<double> rl = rloc_.to_host(s_), sl = sloc_.to_host(s_);

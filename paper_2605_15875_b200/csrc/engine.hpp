@@ -11,6 +11,7 @@
 #include "solver.hpp"
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -89,14 +90,28 @@ class Engine {
     void check_err(const char* where);
     void sync();
 
-    // local solve -------------------------------------------------------------
-    void reset_parts(double tol);
-    int build_superset(const double* q0, const double* q1, bool swept, double margin);
-    void eval_energy(const double* q, int which, double PartState::*field);
-    void derivatives();
-    void pcg();
-    NewtonResult newton_batch(int max_iters, double tol);
+    // local solve (enqueue-only, capturable) -----------------------------------
+    void prepare_solver();
+    void enq_superset(const double* q0, const double* q1, bool swept);
+    void enq_energy(const double* q, int which, double PartState::*field);
+    void enq_derivatives();
+    void enq_pcg();
+    void enq_newton_head(int max_iters);
+    void enq_newton_ccd();
+    void enq_ls_trial();
+    void enq_solve_begin(double tol);
+    FrameCtrl read_ctrl();
+    NewtonResult newton_batch(int max_iters, double tol, bool reset_ctrl = true);
     std::vector<double> delta_inf(const double* a, const double* b);
+
+    // CUDA graphs with conditional nodes -------------------------------------
+    unsigned long long new_cond_handle();
+    void add_cond_node(unsigned long long h, bool is_while, int level,
+                       const std::function<void()>& body);
+    cudaStream_t cap_stream(int level);
+    void cap_newton(int max_iters, double tol, int level);
+    void enq_reference_frame(bool graph);
+    void capture_reference_graph();
 
     // frames -----------------------------------------------------------------
     FrameStats frame_reference();
@@ -160,6 +175,31 @@ class Engine {
     SimParams frame_params_;
     int project_ = 1;
     DBuf<double> pbuf_, pcg_part_;
+
+    // fixed capacities (graph-safe) and the captured N=1 frame
+    int cap_ = 0;
+    int det_fmt_n_ = -1;
+    size_t temp_bytes_ = 0;
+    DBuf<FrameCtrl> ctrl_;
+    PinnedBuf<FrameCtrl> ctrl_h_;
+    CondHandles hd_;
+    cudaGraphExec_t exec_ = nullptr;
+    bool graph_ok_ = false;
+    bool use_graph_ = true;
+    bool ref_ready_ = false;
+    long long nodes_inc_[8] = {};  // kernels captured per conditional level (inclusive)
+    long long nodes_total_ = 0;
+    bool graph_replayed_ = false;
+    std::vector<cudaStream_t> cap_streams_;
+    DBuf<double> trace_dev_;
+    int trace_cap_ = 4096;
+    DBuf<double> qd_start_;
+
+  public:
+    void set_use_graph(bool on) {
+        use_graph_ = on;
+        graph_ok_ = false;
+    }
 };
 
 } // namespace dabd_gpu

@@ -154,7 +154,8 @@ __device__ int process_instance(const SceneView& sc, const InstView& iv, const B
 __global__ void __launch_bounds__(kBlock)
     k_emit(SceneView sc, InstView iv, const Box* box, const double* cell_max, unsigned mask,
            const int* hstart, const int* hcount, const int* items, const int* stat, int n_stat,
-           int swept, double margin, KeyFmt fmt, unsigned long long* out, int cap, int* counter) {
+           int swept, double margin, KeyFmt fmt, unsigned long long* out, int cap, int* counter,
+           int* err) {
     using Scan = cub::BlockScan<int, kBlock>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ int base;
@@ -170,7 +171,10 @@ __global__ void __launch_bounds__(kBlock)
         __syncthreads();
         const int b0 = base;
         if (b0 + total > cap) {
-            if (threadIdx.x == 0) atomicMax(&counter[1], b0 + total);
+            if (threadIdx.x == 0) {
+                atomicMax(&counter[1], b0 + total);
+                if (err) raise(err, kErrCapacity);
+            }
         } else if (c > 0) {
             process_instance<true>(sc, iv, box, cell_max, mask, hstart, hcount, items, stat, n_stat,
                                    swept != 0, margin, fmt, i, out, b0 + off);
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(kBlock)
 
 __global__ void k_emit_static_pairs(SceneView sc, InstView iv, const Box* box, const int* stat,
                                     int n_stat, int swept, double margin, KeyFmt fmt,
-                                    unsigned long long* out, int cap, int* counter) {
+                                    unsigned long long* out, int cap, int* counter, int* err) {
     const long long np = static_cast<long long>(n_stat) * n_stat;
     for (long long t = blockIdx.x * blockDim.x + threadIdx.x; t < np;
          t += gridDim.x * blockDim.x) {
@@ -192,6 +196,7 @@ __global__ void k_emit_static_pairs(SceneView sc, InstView iv, const Box* box, c
         const int pos = atomicAdd(&counter[0], c);
         if (pos + c > cap) {
             atomicMax(&counter[1], pos + c);
+            if (err) raise(err, kErrCapacity);
             continue;
         }
         const int c1 = emit_dir<true>(sc, iv, swept != 0, margin, i, j, fmt, out, pos);
@@ -238,72 +243,87 @@ Detector::Detector() {
 
 Detector::~Detector() = default;
 
-int Detector::build(const SceneView& sc, const InstView& iv, const int* stat, int n_stat,
-                    bool swept, double margin, int max_verts, cudaStream_t s) {
-    count_ = 0;
-    fmt_.ibits = bits_for(std::max(iv.n, 2));
+void Detector::prepare(int n_inst, int max_verts, int cap) {
+    fmt_.ibits = bits_for(std::max(n_inst, 2));
     fmt_.vbits = bits_for(std::max(max_verts, 2));
     if (fmt_.total_bits() > 64) throw Error("broad phase: instance/vertex counts exceed key width");
-    if (iv.n == 0) return 0;
-    box_.resize(iv.n);
-    CUDA_CHECK(cudaMemsetAsync(cell_.get(), 0, sizeof(double), s));
-    launch_inst_boxes(sc, iv, swept, margin, box_.get(), cell_.get(), s);
-
     unsigned tsize = 1;
-    while (tsize < 2u * static_cast<unsigned>(iv.n)) tsize <<= 1;
+    while (tsize < 2u * static_cast<unsigned>(std::max(n_inst, 1))) tsize <<= 1;
+    tsize_ = tsize;
+    cap = std::max(cap, 64);
+    box_.resize(std::max(n_inst, 1));
     hcount_.resize(tsize);
     hstart_.resize(tsize);
     hfill_.resize(tsize);
-    hitems_.resize(iv.n);
-    hkey_.resize(iv.n);
-    hcount_.zero(s);
-    DABD_LAUNCH("k_hash_count", s, k_hash_count<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(sc, iv, box_.get(), cell_.get(),
-                                                           tsize - 1, hcount_.get(), hkey_.get()));
-    size_t tb = 0;
+    hitems_.resize(std::max(n_inst, 1));
+    hkey_.resize(std::max(n_inst, 1));
+    keys_.resize(cap);
+    keys_sorted_.resize(cap);
+    cap_ = cap;
+    size_t tb = 0, sb = 0;
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, hcount_.get(), hstart_.get(),
-                                             static_cast<int>(tsize), s));
-    temp_.resize(tb);
-    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp_.get(), tb, hcount_.get(), hstart_.get(),
-                                             static_cast<int>(tsize), s));
-    hfill_.zero(s);
-    DABD_LAUNCH("k_hash_scatter", s, k_hash_scatter<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(iv.n, hkey_.get(), hstart_.get(),
-                                                             hfill_.get(), hitems_.get()));
+                                             static_cast<int>(tsize)));
+    CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys_.get(), keys_sorted_.get(), cap, 0,
+                                              fmt_.total_bits()));
+    temp_.resize(std::max(tb, sb));
+    temp_bytes_ = std::max(tb, sb);
+}
 
-    int cap = static_cast<int>(std::max<size_t>(keys_.capacity(), 64 * static_cast<size_t>(iv.n)));
-    for (int attempt = 0; attempt < 3; ++attempt) {
-        keys_.resize(cap);
-        counter_.zero(s);
-        DABD_LAUNCH("k_emit", s, k_emit<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(
-            sc, iv, box_.get(), cell_.get(), tsize - 1, hstart_.get(), hcount_.get(),
-            hitems_.get(), stat, n_stat, swept ? 1 : 0, margin, fmt_, keys_.get(), cap,
-            counter_.get()));
-        if (n_stat > 1) {
-            const int gs = grid_for(static_cast<long long>(n_stat) * n_stat, kBlock);
-            DABD_LAUNCH("k_emit_static_pairs", s,
-                        k_emit_static_pairs<<<gs, kBlock, 0, s>>>(sc, iv, box_.get(), stat, n_stat,
-                                                                  swept ? 1 : 0, margin, fmt_,
-                                                                  keys_.get(), cap, counter_.get()));
-        }
+void Detector::enqueue(const SceneView& sc, const InstView& iv, const int* stat, int n_stat,
+                       bool swept, double margin, int* err, cudaStream_t s) {
+    CUDA_CHECK(cudaMemsetAsync(counter_.get(), 0, 2 * sizeof(int), s));
+    CUDA_CHECK(cudaMemsetAsync(keys_sorted_.get(), 0xFF, sizeof(unsigned long long) * cap_, s));
+    if (iv.n == 0) return;
+    CUDA_CHECK(cudaMemsetAsync(cell_.get(), 0, sizeof(double), s));
+    launch_inst_boxes(sc, iv, swept, margin, box_.get(), cell_.get(), s);
+    CUDA_CHECK(cudaMemsetAsync(hcount_.get(), 0, sizeof(int) * tsize_, s));
+    DABD_LAUNCH("k_hash_count", s,
+                k_hash_count<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(
+                    sc, iv, box_.get(), cell_.get(), tsize_ - 1, hcount_.get(), hkey_.get()));
+    size_t tb = temp_bytes_;
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp_.get(), tb, hcount_.get(), hstart_.get(),
+                                             static_cast<int>(tsize_), s));
+    CUDA_CHECK(cudaMemsetAsync(hfill_.get(), 0, sizeof(int) * tsize_, s));
+    DABD_LAUNCH("k_hash_scatter", s,
+                k_hash_scatter<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(
+                    iv.n, hkey_.get(), hstart_.get(), hfill_.get(), hitems_.get()));
+    CUDA_CHECK(cudaMemsetAsync(keys_.get(), 0xFF, sizeof(unsigned long long) * cap_, s));
+    DABD_LAUNCH("k_emit", s,
+                k_emit<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(
+                    sc, iv, box_.get(), cell_.get(), tsize_ - 1, hstart_.get(), hcount_.get(),
+                    hitems_.get(), stat, n_stat, swept ? 1 : 0, margin, fmt_, keys_.get(), cap_,
+                    counter_.get(), err));
+    if (n_stat > 1) {
+        const int gs = grid_for(static_cast<long long>(n_stat) * n_stat, kBlock);
+        DABD_LAUNCH("k_emit_static_pairs", s,
+                    k_emit_static_pairs<<<gs, kBlock, 0, s>>>(sc, iv, box_.get(), stat, n_stat,
+                                                              swept ? 1 : 0, margin, fmt_,
+                                                              keys_.get(), cap_, counter_.get(),
+                                                              err));
+    }
+    size_t sb = temp_bytes_;
+    CUDA_CHECK(cub::DeviceRadixSort::SortKeys(temp_.get(), sb, keys_.get(), keys_sorted_.get(), cap_,
+                                              0, fmt_.total_bits(), s));
+}
+
+int Detector::build(const SceneView& sc, const InstView& iv, const int* stat, int n_stat,
+                    bool swept, double margin, int max_verts, cudaStream_t s) {
+    int cap = std::max(cap_, 64 * std::max(iv.n, 1));
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        if (cap != cap_ || tsize_ < 2u * static_cast<unsigned>(std::max(iv.n, 1)) ||
+            fmt_.ibits != bits_for(std::max(iv.n, 2)) || fmt_.vbits != bits_for(std::max(max_verts, 2)))
+            prepare(iv.n, max_verts, cap);
+        enqueue(sc, iv, stat, n_stat, swept, margin, nullptr, s);
         CUDA_CHECK(cudaMemcpyAsync(pin_.get(), counter_.get(), 2 * sizeof(int),
                                    cudaMemcpyDeviceToHost, s));
         CUDA_CHECK(cudaStreamSynchronize(s));
-        if (pin_[1] == 0 && pin_[0] <= cap) {
+        if (pin_[1] == 0 && pin_[0] <= cap_) {
             count_ = pin_[0];
-            break;
+            return count_;
         }
-        cap = std::max(pin_[0], pin_[1]) + cap / 4;
-        if (attempt == 2) throw Error("broad phase: candidate buffer growth failed");
+        cap = std::max(pin_[0], pin_[1]) + cap_ / 4;
     }
-    keys_sorted_.resize(std::max(count_, 1));
-    if (count_ > 0) {
-        size_t sb = 0;
-        CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys_.get(), keys_sorted_.get(),
-                                                  count_, 0, fmt_.total_bits(), s));
-        temp_.resize(sb);
-        CUDA_CHECK(cub::DeviceRadixSort::SortKeys(temp_.get(), sb, keys_.get(), keys_sorted_.get(),
-                                                  count_, 0, fmt_.total_bits(), s));
-    }
-    return count_;
+    throw Error("broad phase: candidate buffer growth failed");
 }
 
 } // namespace dabd_gpu

@@ -131,6 +131,13 @@ class Detector {
     // instance indices (ascending). Returns the candidate count.
     int build(const SceneView& sc, const InstView& iv, const int* stat, int n_stat, bool swept,
               double margin, int max_verts, cudaStream_t s);
+    // Graph-safe variant: fixed capacity, no host reads. Keys past the count
+    // are ~0ull (sorted to the end); overflow raises kErrCapacity in `err`.
+    void prepare(int n_inst, int max_verts, int cap);
+    void enqueue(const SceneView& sc, const InstView& iv, const int* stat, int n_stat, bool swept,
+                 double margin, int* err, cudaStream_t s);
+    const int* d_count() const { return counter_.get(); }
+    int cap() const { return cap_; }
     const unsigned long long* keys() const { return keys_sorted_.get(); }
     const Box* boxes() const { return box_.get(); }
     KeyFmt fmt() const { return fmt_; }
@@ -146,6 +153,9 @@ class Detector {
     PinnedBuf<int> pin_;
     KeyFmt fmt_;
     int count_ = 0;
+    int cap_ = 0;
+    unsigned tsize_ = 0;
+    size_t temp_bytes_ = 0;
 };
 
 void launch_narrow_bodies(const SceneView& sc, const double* q, const int* cand, int n,

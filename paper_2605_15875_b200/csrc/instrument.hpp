@@ -31,7 +31,9 @@ class KernelTimer {
         count_ = 0;
         bytes_ = 0.0;
     }
-    bool active(const char* name) const { return !name_.empty() && name_ == name; }
+    bool active(const char* name) const { return !suspended_ && !name_.empty() && name_ == name; }
+    // No event pairs while a stream is being captured into a graph.
+    void suspend(bool on) { suspended_ = on; }
     void begin(cudaStream_t s) {
         cudaEvent_t a, b;
         cudaEventCreate(&a);
@@ -70,6 +72,7 @@ class KernelTimer {
         cudaEvent_t a, b;
     };
     std::string name_;
+    bool suspended_ = false;
     std::vector<Pair> pending_;
     double total_ms_ = 0.0;
     long long count_ = 0;

@@ -1,4 +1,9 @@
-// Host launch wrappers of the solver/ADMM kernels (solver.cu, admm.cu).
+// Host launch wrappers of the solver/ADMM kernels (solver.cu, pcg.cu, solver_scalar.cu).
+//
+// Kernels that walk a candidate/contact list take its capacity `n` (grid
+// size, host) and an optional device-side count `dn`: entries in [*dn, n)
+// are padding. That keeps every launch free of host reads, so the whole
+// frame can be captured into one CUDA graph.
 #pragma once
 
 #include "geometry.cuh"
@@ -10,33 +15,28 @@ namespace dabd_gpu {
 // search, 2 = every partition.
 void launch_body_terms(const SolverView& sv, const double* q, bool derivs, int which,
                        cudaStream_t s);
-void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, KeyFmt fmt,
-                   const Box* box, const double* q, int mode, int which, unsigned char* flag,
-                   double* val, cudaStream_t s);
+void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
+                   KeyFmt fmt, const Box* box, const double* q, int mode, int which,
+                   unsigned char* flag, double* val, cudaStream_t s);
 void launch_contact_terms(const SolverView& sv, const ContactView& cv, cudaStream_t s);
-void launch_seg_offsets(const unsigned long long* keys, int n, KeyFmt fmt, int n_inst, int* off,
-                        int field, const int* perm, cudaStream_t s);
-void launch_make_bkeys(const unsigned long long* keys, int n, KeyFmt fmt, unsigned long long* bkeys,
-                       int* idx, cudaStream_t s);
+void launch_seg_offsets(const unsigned long long* keys, int n, const int* dn, KeyFmt fmt,
+                        int n_inst, int* off, int field, const int* perm, cudaStream_t s);
+void launch_make_bkeys(const unsigned long long* keys, int n, const int* dn, KeyFmt fmt,
+                       unsigned long long* bkeys, int* idx, cudaStream_t s);
 void launch_assemble(const SolverView& sv, const ContactView& cv, double* row_trace,
                      cudaStream_t s);
 void launch_precond(const SolverView& sv, cudaStream_t s);
 int segsum_chunks(int n);
 void launch_segsum_rows(const double* v, int n, const int* rpart, int P, int part_base,
                         double* partial, double* dst, int stride, bool accumulate, cudaStream_t s);
-void launch_segsum_keys(const double* v, int n, const unsigned long long* keys, KeyFmt fmt,
-                        const int* ipart, int P, int part_base, double* partial, double* dst,
-                        int stride, bool accumulate, cudaStream_t s);
-void launch_pcg_init(const SolverView& sv, double* rz, double* rr, cudaStream_t s);
-void launch_pcg_spmv(const SolverView& sv, const double* pold, double* pnew, const double* beta,
-                     double* pap_row, cudaStream_t s);
-void launch_pcg_update(const SolverView& sv, const double* pnew, const double* alpha, double* rz,
-                       double* rr, cudaStream_t s);
+void launch_segsum_keys(const double* v, int n, const int* dn, const unsigned long long* keys,
+                        KeyFmt fmt, const int* ipart, int P, int part_base, double* partial,
+                        double* dst, int stride, bool accumulate, cudaStream_t s);
 void launch_make_trial(const SolverView& sv, bool use_alpha, double alpha, int which,
                        cudaStream_t s);
 void launch_dq_inf(const SolverView& sv, cudaStream_t s);
-void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, KeyFmt fmt,
-                const Box* box0, const double* q0, const double* q1, int which,
+void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
+                KeyFmt fmt, const Box* box0, const double* q0, const double* q1, int which,
                 double* earliest_override, cudaStream_t s);
 
 // Persistent cooperative block-Jacobi PCG over all partitions (pcg.cu).
@@ -47,16 +47,44 @@ void launch_pcg_persistent(const SolverView& sv, double* pbuf, double* partials,
 
 // Per-partition scalar steps (solver_scalar.cu). `op` selects the update.
 enum ScalarOp : int {
-    kOpPcgStart = 0,  // bnorm2 = rr; pcg_done = (bnorm2 == 0); iters = 0; beta = 0
-    kOpPcgAlpha = 1,  // alpha = rz / pap
-    kOpPcgBeta = 2,   // beta = rz_new / rz; rz = rz_new; done if rr <= tol^2 bnorm2 or iters>=max
-    kOpEps = 3,       // eps = 1e-8 * trace / ndof
-    kOpAlphaMax = 4,  // alpha_max from toi_earliest; alpha = alpha_max; searching = 1
-    kOpAccept = 5,    // line-search decision (newton.cpp:47-62)
+    kOpEps = 3,         // eps = 1e-8 * trace / ndof; ++iterations
+    kOpAlphaMax = 4,    // alpha_max from toi_earliest; alpha = alpha_max; searching = 1
+    kOpAccept = 5,      // line-search decision (newton.cpp:47-62)
     kOpNewtonCheck = 6, // dq_inf < tol -> converged without moving (newton.cpp:30-36)
-    kOpIterBegin = 7    // dq_inf = 0, toi_earliest = 2, n_candidates = 0
+    kOpIterBegin = 7,   // dq_inf = 0, toi_earliest = 2, n_candidates = 0
+    kOpReset = 8,       // start of a solve: active = ndof > 0 (unless ctrl says ended)
+    kOpNewtonTail = 9   // end of a Newton iteration: cap at max_iters
 };
-void launch_scalar(PartState* ps, int P, int op, double* a, double* b, double* c, double tol,
+
+// Device-side frame control for the captured graph (run_reference semantics,
+// sim.cpp:207-247). Conditional handles steer the WHILE nodes; in eager mode
+// they are 0 and the host reads the same flags.
+struct FrameCtrl {
+    int k;               // ADMM iteration counter of the frame
+    int ended;           // stop decision taken
+    int failed;          // K exhausted without a stop
+    int admm_iterations;
+    int newton_total, ls_total, pcg_total, max_contacts, max_candidates;
+    int any_active, any_searching;
+    int trace_n;
+    int exec_admm, exec_newton, exec_step, exec_ls; // conditional-body executions
+    int pad_;
+    double dq_inf;       // max over partitions of the last solve's config delta
+    double frame;        // frame index for trace rows (written by the host)
+};
+
+struct CondHandles {
+    unsigned long long admm = 0, newton = 0, step = 0, ls = 0; // cudaGraphConditionalHandle values
+    int graph = 0;
+};
+
+void launch_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHandles h, double tol,
                    int max_iters, int* err, cudaStream_t s);
+
+// ADMM controller of the N=1 frame (sim.cpp:223-238): op 0 = step head
+// (stop test for k > 1), op 1 = step tail (k++, K bound). Writes trace rows.
+void launch_frame_ctrl(FrameCtrl* ctrl, int op, const double* dq_part, int P, double h, double l,
+                       double theta, int K, double* trace, int trace_cap, CondHandles hd, int* err,
+                       const PartState* ps, cudaStream_t s);
 
 } // namespace dabd_gpu

@@ -293,11 +293,19 @@ void launch_pcg_persistent(const SolverView& sv, double* pbuf, double* partials,
     if (sv.n_rows == 0) return;
     const int G = pcg_grid_size(sv.n_rows);
     PcgArgs a{pbuf, partials, rowval, tol, max_iters};
-    SolverView v = sv;
-    void* args[] = {&v, &a};
-    DABD_LAUNCH("k_pcg", s,
-                CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_pcg), G, kT, args,
-                                                       0, s)));
+    // cudaLaunchKernelEx with the cooperative attribute is stream-capturable,
+    // so the persistent solver becomes one node of the frame graph.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DABD_LAUNCH("k_pcg", s, CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg, sv, a)));
 }
 
 } // namespace dabd_gpu

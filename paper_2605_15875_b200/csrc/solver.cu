@@ -132,10 +132,16 @@ __device__ __forceinline__ double kappa_c_inv(const SolverView& sv, int ba, int 
     return 1.0 / (1.0 / kc); // pair.kappa_c (objective.cpp:292-293)
 }
 
-__global__ void k_filter(SolverView sv, const unsigned long long* keys, int n, KeyFmt fmt,
-                         const Box* box, const double* qsrc, int mode, int which,
+__global__ void k_filter(SolverView sv, const unsigned long long* keys, int n, const int* dn,
+                         KeyFmt fmt, const Box* box, const double* qsrc, int mode, int which,
                          unsigned char* flag, double* val) {
+    const int nn = dn ? min(*dn, n) : n;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        if (t >= nn) { // padding past the device-side count
+            if (flag) flag[t] = 0;
+            if (val) val[t] = 0.0;
+            continue;
+        }
         int a, b, v, e;
         fmt.unpack(keys[t], a, b, v, e);
         const int p = sv.ipart[a] - sv.part_base;
@@ -179,7 +185,8 @@ __global__ void k_filter(SolverView sv, const unsigned long long* keys, int n, K
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kB)
     k_contact_terms(SolverView sv, ContactView cv) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cv.n; c += gridDim.x * blockDim.x) {
+    const int nc = cv.dn ? min(*cv.dn, cv.n) : cv.n;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
         int a, b, v, e;
         cv.fmt.unpack(cv.key[c], a, b, v, e);
         const int ba = sv.ibody[a], bb = sv.ibody[b];
@@ -297,10 +304,11 @@ __global__ void __launch_bounds__(kB)
 // ---------------------------------------------------------------------------
 // Segment offsets of sorted keys: off[i] = first index whose instance >= i.
 // ---------------------------------------------------------------------------
-__global__ void k_seg_offsets(const unsigned long long* keys, int n, KeyFmt fmt, int n_inst,
-                             int* off, int which_field, const int* perm) {
+__global__ void k_seg_offsets(const unsigned long long* keys, int n, const int* dn, KeyFmt fmt,
+                              int n_inst, int* off, int which_field, const int* perm) {
+    const int nn = dn ? min(*dn, n) : n;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n_inst; i += gridDim.x * blockDim.x) {
-        int lo = 0, hi = n;
+        int lo = 0, hi = nn;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             int a, b, v, e;
@@ -313,12 +321,17 @@ __global__ void k_seg_offsets(const unsigned long long* keys, int n, KeyFmt fmt,
     }
 }
 
-__global__ void k_make_bkeys(const unsigned long long* keys, int n, KeyFmt fmt,
+__global__ void k_make_bkeys(const unsigned long long* keys, int n, const int* dn, KeyFmt fmt,
                              unsigned long long* bkeys, int* idx) {
+    const int nn = dn ? min(*dn, n) : n;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        int a, b, v, e;
-        fmt.unpack(keys[t], a, b, v, e);
-        bkeys[t] = fmt.pack(b, a, v, e);
+        if (t < nn) {
+            int a, b, v, e;
+            fmt.unpack(keys[t], a, b, v, e);
+            bkeys[t] = fmt.pack(b, a, v, e);
+        } else {
+            bkeys[t] = ~0ull; // padding sorts last
+        }
         idx[t] = t;
     }
 }
@@ -607,129 +620,15 @@ struct KeyPart {
     const unsigned long long* keys;
     KeyFmt fmt;
     const int* ipart;
+    const int* dn;   // device count (padding past it belongs to the last partition)
+    int last_part;
     __device__ int operator()(int t) const {
+        if (dn && t >= *dn) return last_part;
         int a, b, v, e;
         fmt.unpack(keys[t], a, b, v, e);
         return ipart[a];
     }
 };
-
-// ---------------------------------------------------------------------------
-// PCG (block-Jacobi) -- see solver.hpp for the scalar bookkeeping.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void matvec36(const double* m, const double (&x)[6], double (&y)[6]) {
-#pragma unroll
-    for (int a = 0; a < 6; ++a) {
-        double s = 0.0;
-#pragma unroll
-        for (int c = 0; c < 6; ++c) s += m[6 * a + c] * x[c];
-        y[a] = s;
-    }
-}
-
-// r = b = -grad, x = 0, z = Dinv r, p0 = 0; per-row r.z, r.r, b.b
-__global__ void k_pcg_init(SolverView sv, double* rz, double* rr) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
-        const int p = sv.rpart[r] - sv.part_base;
-        double g[6], z[6];
-        load6(sv.rgrad + 6 * r, g);
-        const bool act = sv.ps[p].active != 0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) g[k] = act ? -g[k] : 0.0;
-        matvec36(sv.rdinv + 36 * r, g, z);
-        double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            if (!act) z[k] = 0.0;
-            s1 += g[k] * z[k];
-            s2 += g[k] * g[k];
-        }
-        const double zero[6] = {0, 0, 0, 0, 0, 0};
-        store6(sv.r + 6 * r, g);
-        store6(sv.z + 6 * r, z);
-        store6(sv.x + 6 * r, zero);
-        store6(sv.p0 + 6 * r, zero);
-        rz[r] = s1;
-        rr[r] = s2;
-    }
-}
-
-// p_new = z + beta p_old ; ap = (D + eps I) p_new + sum_k B_k p_new[col_k]
-__global__ void k_pcg_spmv(SolverView sv, const double* pold, double* pnew, const double* beta_src,
-                           double* pap_row) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
-        const int p = sv.rpart[r] - sv.part_base;
-        const PartState& st = sv.ps[p];
-        if (!st.active || st.pcg_done) {
-            pap_row[r] = 0.0;
-            continue;
-        }
-        const double beta = beta_src[p];
-        double pr[6], zr[6], y[6];
-        load6(pold + 6 * r, pr);
-        load6(sv.z + 6 * r, zr);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) pr[k] = zr[k] + beta * pr[k];
-        store6(pnew + 6 * r, pr);
-        matvec36(sv.rdiag + 36 * r, pr, y);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) y[k] += st.eps * pr[k];
-        const int nb = sv.ell_cnt[r];
-        for (int t = 0; t < nb; ++t) {
-            const int c = sv.ell_col[r * kEll + t];
-            double pc[6], zc[6], yc[6];
-            load6(pold + 6 * c, pc);
-            load6(sv.z + 6 * c, zc);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) pc[k] = zc[k] + beta * pc[k];
-            matvec36(sv.ell_blk + (static_cast<size_t>(r) * kEll + t) * 36, pc, yc);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) y[k] += yc[k];
-        }
-        store6(sv.ap + 6 * r, y);
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) s += pr[k] * y[k];
-        pap_row[r] = s;
-    }
-}
-
-// x += alpha p ; r -= alpha Ap ; z = Dinv r ; per-row r.z, r.r
-__global__ void k_pcg_update(SolverView sv, const double* pnew, const double* alpha_src,
-                             double* rz, double* rr) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
-        const int p = sv.rpart[r] - sv.part_base;
-        const PartState& st = sv.ps[p];
-        if (!st.active || st.pcg_done) {
-            rz[r] = 0.0;
-            rr[r] = 0.0;
-            continue;
-        }
-        const double alpha = alpha_src[p];
-        double x[6], rv[6], pv[6], av[6], z[6];
-        load6(sv.x + 6 * r, x);
-        load6(sv.r + 6 * r, rv);
-        load6(pnew + 6 * r, pv);
-        load6(sv.ap + 6 * r, av);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            x[k] += alpha * pv[k];
-            rv[k] -= alpha * av[k];
-        }
-        matvec36(sv.rdinv + 36 * r, rv, z);
-        double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            s1 += rv[k] * z[k];
-            s2 += rv[k] * rv[k];
-        }
-        store6(sv.x + 6 * r, x);
-        store6(sv.r + 6 * r, rv);
-        store6(sv.z + 6 * r, z);
-        rz[r] = s1;
-        rr[r] = s2;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Line search helpers
@@ -765,10 +664,11 @@ __global__ void k_dq_inf(SolverView sv) {
 
 // CCD over the candidate superset with the exact swept margin-0 predicate
 // (geometry.cpp:311-341). box0: per-instance swept boxes with margin 0.
-__global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, KeyFmt fmt,
-                      const Box* box0, const double* q0, const double* q1, int which,
+__global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, const int* dn,
+                      KeyFmt fmt, const Box* box0, const double* q0, const double* q1, int which,
                       double* earliest_override) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int nn = dn ? min(*dn, n) : n;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += gridDim.x * blockDim.x) {
         int a, b, v, e;
         fmt.unpack(keys[t], a, b, v, e);
         const int p = sv.ipart[a] - sv.part_base;
@@ -810,11 +710,13 @@ void launch_body_terms(const SolverView& sv, const double* q, bool derivs, int w
     DABD_LAUNCH("k_body_terms", s, k_body_terms<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, q, derivs ? 1 : 0, which));
 }
 
-void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, KeyFmt fmt,
-                   const Box* box, const double* q, int mode, int which, unsigned char* flag,
-                   double* val, cudaStream_t s) {
+void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
+                   KeyFmt fmt, const Box* box, const double* q, int mode, int which,
+                   unsigned char* flag, double* val, cudaStream_t s) {
     if (n == 0) return;
-    DABD_LAUNCH("k_filter", s, k_filter<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, fmt, box, q, mode, which, flag, val));
+    DABD_LAUNCH("k_filter", s,
+                k_filter<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, dn, fmt, box, q, mode, which,
+                                                        flag, val));
 }
 
 void launch_contact_terms(const SolverView& sv, const ContactView& cv, cudaStream_t s) {
@@ -822,15 +724,18 @@ void launch_contact_terms(const SolverView& sv, const ContactView& cv, cudaStrea
     DABD_LAUNCH("k_contact_terms", s, k_contact_terms<<<grid_for(cv.n, kB), kB, 0, s>>>(sv, cv));
 }
 
-void launch_seg_offsets(const unsigned long long* keys, int n, KeyFmt fmt, int n_inst, int* off,
-                        int field, const int* perm, cudaStream_t s) {
-    DABD_LAUNCH("k_seg_offsets", s, k_seg_offsets<<<grid_for(n_inst + 1, kB), kB, 0, s>>>(keys, n, fmt, n_inst, off, field, perm));
+void launch_seg_offsets(const unsigned long long* keys, int n, const int* dn, KeyFmt fmt,
+                        int n_inst, int* off, int field, const int* perm, cudaStream_t s) {
+    DABD_LAUNCH("k_seg_offsets", s,
+                k_seg_offsets<<<grid_for(n_inst + 1, kB), kB, 0, s>>>(keys, n, dn, fmt, n_inst, off,
+                                                                      field, perm));
 }
 
-void launch_make_bkeys(const unsigned long long* keys, int n, KeyFmt fmt, unsigned long long* bkeys,
-                       int* idx, cudaStream_t s) {
+void launch_make_bkeys(const unsigned long long* keys, int n, const int* dn, KeyFmt fmt,
+                       unsigned long long* bkeys, int* idx, cudaStream_t s) {
     if (n == 0) return;
-    DABD_LAUNCH("k_make_bkeys", s, k_make_bkeys<<<grid_for(n, kB), kB, 0, s>>>(keys, n, fmt, bkeys, idx));
+    DABD_LAUNCH("k_make_bkeys", s,
+                k_make_bkeys<<<grid_for(n, kB), kB, 0, s>>>(keys, n, dn, fmt, bkeys, idx));
 }
 
 void launch_assemble(const SolverView& sv, const ContactView& cv, double* row_trace,
@@ -849,10 +754,12 @@ int segsum_chunks(int n) { return std::max(1, (n + kCH - 1) / kCH); }
 // Ticket for the last-block fold; launches on one device are stream ordered.
 __device__ unsigned g_segsum_ticket = 0;
 
-static unsigned* segsum_ticket() {
-    void* p = nullptr;
-    CUDA_CHECK(cudaGetSymbolAddress(&p, g_segsum_ticket));
-    return static_cast<unsigned*>(p);
+static unsigned* segsum_ticket() { // resolved once per device, outside any graph capture
+    static void* cache[64] = {};
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    if (!cache[dev & 63]) CUDA_CHECK(cudaGetSymbolAddress(&cache[dev & 63], g_segsum_ticket));
+    return static_cast<unsigned*>(cache[dev & 63]);
 }
 
 void launch_segsum_rows(const double* v, int n, const int* rpart, int P, int part_base,
@@ -863,30 +770,15 @@ void launch_segsum_rows(const double* v, int n, const int* rpart, int P, int par
                                            segsum_ticket(), dst, stride, accumulate ? 1 : 0));
 }
 
-void launch_segsum_keys(const double* v, int n, const unsigned long long* keys, KeyFmt fmt,
-                        const int* ipart, int P, int part_base, double* partial, double* dst,
-                        int stride, bool accumulate, cudaStream_t s) {
+void launch_segsum_keys(const double* v, int n, const int* dn, const unsigned long long* keys,
+                        KeyFmt fmt, const int* ipart, int P, int part_base, double* partial,
+                        double* dst, int stride, bool accumulate, cudaStream_t s) {
     const int nc = segsum_chunks(n);
     DABD_LAUNCH("k_segsum", s,
-                k_segsum<<<nc, kB, 0, s>>>(v, n, P, part_base, KeyPart{keys, fmt, ipart}, partial,
-                                           segsum_ticket(), dst, stride, accumulate ? 1 : 0));
-}
-
-void launch_pcg_init(const SolverView& sv, double* rz, double* rr, cudaStream_t s) {
-    if (sv.n_rows == 0) return;
-    DABD_LAUNCH("k_pcg_init", s, k_pcg_init<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, rz, rr));
-}
-
-void launch_pcg_spmv(const SolverView& sv, const double* pold, double* pnew, const double* beta,
-                     double* pap_row, cudaStream_t s) {
-    if (sv.n_rows == 0) return;
-    DABD_LAUNCH("k_pcg_spmv", s, k_pcg_spmv<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, pold, pnew, beta, pap_row));
-}
-
-void launch_pcg_update(const SolverView& sv, const double* pnew, const double* alpha, double* rz,
-                       double* rr, cudaStream_t s) {
-    if (sv.n_rows == 0) return;
-    DABD_LAUNCH("k_pcg_update", s, k_pcg_update<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv, pnew, alpha, rz, rr));
+                k_segsum<<<nc, kB, 0, s>>>(v, n, P, part_base,
+                                           KeyPart{keys, fmt, ipart, dn, part_base + P - 1},
+                                           partial, segsum_ticket(), dst, stride,
+                                           accumulate ? 1 : 0));
 }
 
 void launch_make_trial(const SolverView& sv, bool use_alpha, double alpha, int which,
@@ -900,11 +792,13 @@ void launch_dq_inf(const SolverView& sv, cudaStream_t s) {
     DABD_LAUNCH("k_dq_inf", s, k_dq_inf<<<grid_for(sv.n_rows, kB), kB, 0, s>>>(sv));
 }
 
-void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, KeyFmt fmt,
-                const Box* box0, const double* q0, const double* q1, int which,
+void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
+                KeyFmt fmt, const Box* box0, const double* q0, const double* q1, int which,
                 double* earliest_override, cudaStream_t s) {
     if (n == 0) return;
-    DABD_LAUNCH("k_ccd", s, k_ccd<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, fmt, box0, q0, q1, which, earliest_override));
+    DABD_LAUNCH("k_ccd", s,
+                k_ccd<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, dn, fmt, box0, q0, q1, which,
+                                                     earliest_override));
 }
 
 } // namespace dabd_gpu

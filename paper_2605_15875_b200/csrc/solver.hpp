@@ -86,7 +86,8 @@ struct SolverView {
 
 // Active contacts (derivative stage) in (a,b,v,e) order plus their data.
 struct ContactView {
-    int n = 0;
+    int n = 0;                    // capacity (grid size)
+    const int* dn = nullptr;      // device-side contact count (nullptr: n is exact)
     KeyFmt fmt;
     const unsigned long long* key = nullptr; // sorted by (a, b, v, e)
     const int* perm_b = nullptr;  // contact indices sorted by (b, a, v, e)

@@ -25,7 +25,7 @@ def _near_threshold(row, sd, rel=1e-2):
     return any(abs(row[c] / norm - th) < rel * th for c in (3, 4, 5))
 
 
-def _compare(name, workers, frames, state_tol=1e-7, trace_tol=1e-6):
+def _compare(name, workers, frames, state_tol=1e-7, trace_tol=1e-6, exact_toi=True):
     """Frame-by-frame comparison; stops at the first frame whose ADMM count
     differs, which must be a flagged near-threshold stop decision."""
     sd = make_scenario(name)
@@ -48,7 +48,10 @@ def _compare(name, workers, frames, state_tol=1e-7, trace_tol=1e-6):
         assert np.array_equal(rg[:, [0, 1, 2, 7]], ro[:, [0, 1, 2, 7]])
         for col in (3, 4, 5):  # dq, r, s relative to the stopping scale h*l
             assert np.abs(rg[:, col] - ro[:, col]).max() < trace_tol * norm
-        assert np.array_equal(rg[:, 6], ro[:, 6])  # merge-gate TOIs: exact accept/reject
+        if exact_toi:
+            assert np.array_equal(rg[:, 6], ro[:, 6])  # merge-gate TOIs: exact accept/reject
+        else:
+            assert np.array_equal(rg[:, 6] == 1.0, ro[:, 6] == 1.0)  # same accept/reject
         scale = max(1.0, np.abs(ref["q"][f]).max())
         assert np.abs(gpu.q[f] - ref["q"][f]).max() < state_tol * scale
         compared += 1
@@ -78,7 +81,7 @@ def test_blocked_merge_halving():  # test_runtime.cpp:146-159
     # (newton.cpp:16) with CCD-limited steps, so the iterate where each local
     # solve stops depends on rounding; the halving sequence, h and the ADMM
     # counts are exact, states/traces agree to the solve's resolution.
-    gpu, ref = _compare("blocked-merge", 2, 3, state_tol=1e-3, trace_tol=2e-2)
+    gpu, ref = _compare("blocked-merge", 2, 3, state_tol=1e-3, trace_tol=2e-2, exact_toi=False)
     assert gpu.stats[0]["attempts"] >= 2
     assert gpu.h[0] < 0.02
 

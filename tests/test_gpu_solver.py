@@ -171,3 +171,15 @@ def test_run_reference_matches_oracle(name, frames):
         mse = np.mean((gpu.q[f][dyn] - ref["q"][f][dyn]) ** 2)
         assert mse < 1e-10 * l2, (f, mse)
     assert [s["admm_iterations"] for s in gpu.stats] == list(ref["admm"])
+
+
+def test_graph_frame_equals_eager_frame(monkeypatch):
+    """The captured conditional-graph frame replays exactly the eager frame."""
+    sd = make_scenario("drop-grid-1")
+    monkeypatch.setenv("DABD_GPU_NO_GRAPH", "1")
+    eager = api.run_reference(sd, 6, **TIGHT)
+    monkeypatch.setenv("DABD_GPU_NO_GRAPH", "0")
+    graph = api.run_reference(sd, 6, **TIGHT)
+    assert np.array_equal(eager.q, graph.q) and np.array_equal(eager.q_dot, graph.q_dot)
+    assert [s["admm_iterations"] for s in eager.stats] == [s["admm_iterations"] for s in graph.stats]
+    assert [s["newton_iterations"] for s in eager.stats] == [s["newton_iterations"] for s in graph.stats]
