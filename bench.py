@@ -9,8 +9,11 @@ synthetic (the deterministic lattice + splitmix64 jitter of scene.py) and
 resident in HBM during the timed `value`; `e2e` times the same steps through
 the public C ABI with the state copied host->device and back every step.
 
-The L2 is flushed (256 MiB write) between timed steps, outside the per-step
-CUDA events. Rank 0 prints ONE JSON line.
+Untimed set-up drops the lattice for --settle frames so every timed step is
+a contact-rich pile frame. The L2 is flushed (256 MiB write) between timed
+steps, outside the per-step CUDA events. Rank 0 prints ONE JSON line.
+Under torchrun (N > 1) every rank steps its own replica of the scene
+(replicas only, scaling "weak") until the NVLink partition runtime lands.
 """
 
 from __future__ import annotations
@@ -29,7 +32,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIG_N1 = "pile-1k"
-ROOFLINE_KERNEL = "k_pcg_spmv"
 
 
 def _peaks():
@@ -94,23 +96,36 @@ def _dist():
     return ws, rank, local
 
 
+def _oracle():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    return O
+
+
+def _settled_state(O, sd, settle: int):
+    """The oracle's own drop of the lattice (used by the CPU arm only)."""
+    o = O.Scene(sd)
+    if settle > 0:
+        r = o.run(settle, workers=0)
+        return o, r["q"][-1], r["qdot"][-1]
+    return o, o.q0.copy(), o.qdot0.copy()
+
+
 def run_reference_arm(args) -> None:
     """CPU reference arm: the oracle port of proj/src/sim.cpp:186-249 (the
     reference itself cannot be built here: Eigen3 is absent),
-    single-threaded like the reference worker."""
+    single-threaded like the reference worker. Each step is one
+    frame of the same settled pile, continued from the previous step."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
+    O = _oracle()
     from paper_2605_15875_b200.scene import make_scenario
 
     sd = make_scenario(args.config)
-    o = O.Scene(sd)
-    # bounded sample: each step is one frame continued from the previous one
-    q, qd = o.q0.copy(), o.qdot0.copy()
-    times = []
-    admm = 0
+    o, q, qd = _settled_state(O, sd, args.settle)
+    times, admm = [], 0
     for i in range(args.warmup + args.steps):
         o.set_state(q, qd)
         t0 = time.perf_counter()
@@ -128,7 +143,8 @@ def run_reference_arm(args) -> None:
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "bodies": o.n, "partitions": 1,
-                   "semantics": "run_reference (sim.cpp:186-249)"},
+                   "semantics": "run_reference (sim.cpp:186-249)",
+                   "start": f"lattice dropped for {args.settle} untimed frames (contact-rich pile)"},
         "admm_iters_per_sec": admm / total,
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": "port",
                          "sample": f"{args.steps} consecutive frames of {args.config} after "
@@ -139,11 +155,9 @@ def run_reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(sd, q, qd, budget_s: float = 20.0):
+def cpu_baseline_sample(sd, q, qd, budget_s: float = 20.0, max_frames: int = 3):
     """Oracle (port) steps/s on the host, continuing from the GPU's warm state."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-
+    O = _oracle()
     o = O.Scene(sd)
     frames = 0
     t0 = time.perf_counter()
@@ -152,12 +166,12 @@ def cpu_baseline_sample(sd, q, qd, budget_s: float = 20.0):
         r = o.run(1, workers=0)
         q, qd = r["q"][0], r["qdot"][0]
         frames += 1
-        if time.perf_counter() - t0 > budget_s or frames >= 5:
+        if time.perf_counter() - t0 > budget_s or frames >= max_frames:
             break
     dt = time.perf_counter() - t0
     return {"value": frames / dt, "unit": "steps/s", "cores": 1, "kind": "port",
-            "sample": f"{frames} frame(s) of the same workload from the GPU run's warm state, "
-                      f"single-threaded oracle/ restatement ({dt:.1f} s)"}
+            "sample": f"{frames} frame(s) of the same settled pile, continued from the GPU run's "
+                      f"warm state, single-threaded oracle/ restatement ({dt:.1f} s)"}
 
 
 def main() -> None:
@@ -168,7 +182,6 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=CONFIG_N1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--roofline-kernel", default=ROOFLINE_KERNEL)
     ap.add_argument("--settle", type=int, default=40,
                     help="untimed frames that turn the lattice into a pile before warm-up")
     args = ap.parse_args()
@@ -177,7 +190,6 @@ def main() -> None:
         run_reference_arm(args)
         return
 
-    import numpy as np
     import torch
 
     ws, rank, local = _dist()
@@ -199,8 +211,6 @@ def main() -> None:
     ctx.set_stream(stream.cuda_stream)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    # Untimed scene set-up: let the lattice drop into a contact-rich pile
-    # (the synthetic input of every timed step), then W warm-up steps.
     if args.settle > 0:
         ctx.run_frames(args.settle)
     for _ in range(args.warmup):
@@ -208,12 +218,16 @@ def main() -> None:
     torch.cuda.synchronize()
     q_warm, qd_warm = ctx.state()
 
-    lib.dabd_gpu_kernel_timer_enable(args.roofline_kernel.encode())
+    def perf(reset):
+        ns, n, b, it = C.c_double(), C.c_longlong(), C.c_double(), C.c_longlong()
+        L.check(lib.dabd_gpu_ctx_pcg_perf(ctx.h, int(reset), C.byref(ns), C.byref(n), C.byref(b),
+                                          C.byref(it)))
+        return ns.value, n.value, b.value, it.value
+
+    perf(True)
     n0 = C.c_longlong()
     lib.dabd_gpu_launch_count(C.byref(n0))
-    step_ms = []
-    admm = 0
-    stats = []
+    step_ms, stats = [], []
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -226,24 +240,22 @@ def main() -> None:
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
-            admm += st["admm_iterations"]
             stats.append(st)
         torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
     n1 = C.c_longlong()
     lib.dabd_gpu_launch_count(C.byref(n1))
-    kms, kcnt, kbytes = C.c_double(), C.c_longlong(), C.c_double()
-    lib.dabd_gpu_kernel_timer_read(C.byref(kms), C.byref(kcnt), C.byref(kbytes))
-    lib.dabd_gpu_kernel_timer_enable(None)
+    pcg_ns, pcg_launches, pcg_bytes, pcg_iters = perf(True)
     total_ms = sum(step_ms)
     if ws > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     value = ws * args.steps / (total_ms / 1e3)
+    admm = sum(s["admm_iterations"] for s in stats)
 
-    # e2e through the public API with host buffers (pinned) every step
+    # e2e through the public API with pinned host buffers every step
     q_h = torch.from_numpy(q_warm.copy()).pin_memory()
     qd_h = torch.from_numpy(qd_warm.copy()).pin_memory()
     ctx2 = api.Context(scene, device=local, num_workers=0)
@@ -251,6 +263,10 @@ def main() -> None:
     qp = C.cast(q_h.data_ptr(), C.POINTER(C.c_double))
     qdp = C.cast(qd_h.data_ptr(), C.POINTER(C.c_double))
     st_arr = (L.FrameStats * 1)()
+    L.check(lib.dabd_gpu_set_state(ctx2.h, qp, qdp))
+    L.check(lib.dabd_gpu_run_frames(ctx2.h, 1, st_arr))  # graph capture outside the timing
+    q_h.copy_(torch.from_numpy(q_warm))
+    qd_h.copy_(torch.from_numpy(qd_warm))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -265,14 +281,18 @@ def main() -> None:
 
     hbm, peak_kind = _peaks()
     roof = None
-    if kcnt.value > 0 and kms.value > 0:
-        achieved = (kbytes.value / kcnt.value) / (kms.value / kcnt.value / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": args.roofline_kernel, "achieved": achieved,
-                "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                "peak_kind": peak_kind, "launches": kcnt.value,
-                "avg_launch_us": 1e3 * kms.value / kcnt.value,
-                "share_of_step": kms.value / total_ms,
-                "algorithmic_bytes_per_launch": kbytes.value / kcnt.value}
+    if pcg_launches > 0 and pcg_ns > 0:
+        dur = pcg_ns / pcg_launches / 1e9
+        achieved = (pcg_bytes / pcg_launches) / dur / 1e9
+        roof = {"bound": "hbm", "kernel": "k_pcg_cluster", "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "peak_kind": peak_kind, "launches": pcg_launches,
+                "avg_launch_us": 1e6 * dur, "iterations_per_launch": pcg_iters / pcg_launches,
+                "share_of_step": (pcg_ns / 1e6) / total_ms,
+                "algorithmic_bytes_per_launch": pcg_bytes / pcg_launches,
+                "timing": "device %globaltimer per launch inside the captured graph "
+                          "(CUDA events cannot bracket a conditional-graph node)",
+                "bytes_model": "SURVEY.md 8(d): I_pcg * [288 (N_b + 2 E_o) + 504 N_b]"}
     line = {
         "metric": "sim_steps_per_sec", "value": value, "unit": "steps/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -282,7 +302,7 @@ def main() -> None:
                    "semantics": "run_reference (sim.cpp:186-249)",
                    "start": f"lattice dropped for {args.settle} untimed frames (contact-rich pile)",
                    "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": "replica" if ws > 1 else "single"},
+                   "parallelism": f"replica x{ws}" if ws > 1 else "single"},
         "admm_iters_per_sec": admm * ws / (total_ms / 1e3),
         "newton_iters_per_step": sum(s["newton_iterations"] for s in stats) / len(stats),
         "pcg_iters_per_step": sum(s["pcg_iterations"] for s in stats) / len(stats),

@@ -198,6 +198,15 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_take_trace(dabd_gpu_ctx* ctx, double* rows
  * name == NULL disables. read() synchronises nothing: call after the work. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_launch_count(long long* count);
 DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_enable(const char* kernel_name);
+/* Device-side accounting of the PCG kernel since the last reset: summed
+ * launch durations (%globaltimer, ns), launches, algorithmic bytes
+ * (I_pcg * [288 (N_b + 2 E_o) + 504 N_b]) and iterations.
+ * Valid inside captured graphs, where CUDA events cannot bracket a node. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_pcg_perf(dabd_gpu_ctx* ctx, int reset, double* ns,
+                                                   long long* launches, double* bytes,
+                                                   long long* iterations);
+/* "name launches total_ms;" per timed kernel ("*" times every kernel). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_report(char* buf, int capacity);
 DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_read(double* total_ms, long long* launches,
                                                         double* algorithmic_bytes);
 

@@ -365,6 +365,27 @@ dabd_gpu_status dabd_gpu_kernel_timer_enable(const char* name) {
     return DABD_GPU_OK;
 }
 
+dabd_gpu_status dabd_gpu_ctx_pcg_perf(dabd_gpu_ctx* ctx, int reset, double* ns,
+                                      long long* launches, double* bytes, long long* iterations) {
+    if (!ctx || !ns || !launches || !bytes || !iterations) return null_arg();
+    return guarded([&] {
+        const dabd_gpu::DevPerf p = ctx->e->read_perf(reset != 0);
+        *ns = static_cast<double>(p.ns);
+        *launches = static_cast<long long>(p.launches);
+        *bytes = p.bytes;
+        *iterations = static_cast<long long>(p.iters);
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_kernel_timer_report(char* buf, int capacity) {
+    if (!buf || capacity < 1) return null_arg();
+    const std::string r = dabd_gpu::KernelTimer::get().report();
+    std::strncpy(buf, r.c_str(), static_cast<size_t>(capacity) - 1);
+    buf[capacity - 1] = '\0';
+    return DABD_GPU_OK;
+}
+
 dabd_gpu_status dabd_gpu_kernel_timer_read(double* total_ms, long long* launches,
                                            double* algorithmic_bytes) {
     if (!total_ms || !launches || !algorithmic_bytes) return null_arg();

@@ -89,6 +89,8 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     ctrl_.resize(1);
     ctrl_.zero(s_);
     ctrl_h_.resize(1);
+    perf_.resize(1);
+    perf_.zero(s_);
     trace_dev_.resize(8 * static_cast<size_t>(trace_cap_));
     qd_start_.resize(6 * std::max(hs_.nb, 1));
     if (const char* e = std::getenv("DABD_GPU_NO_GRAPH")) use_graph_ = e[0] == '0';
@@ -247,6 +249,7 @@ SolverView Engine::view() {
     v.kappa_bar = frame_params_.barrier_stiffness;
     v.kappa_arap = frame_params_.arap_stiffness;
     v.project = project_;
+    v.perf = perf_.get();
     v.err = err_.get();
     return v;
 }
@@ -312,6 +315,7 @@ void Engine::prepare_solver() {
     partial_.resize(static_cast<size_t>(segsum_chunks(std::max(cap_, n_rows_))) * P_ + P_);
     pbuf_.resize(12 * static_cast<size_t>(std::max(n_rows_, 1)));
     pcg_part_.resize(3 * static_cast<size_t>(pcg_grid_size(std::max(n_rows_, 1))) * P_);
+    (void)pcg_cluster_size(); // resolve cluster attributes before any graph capture
     box_.resize(std::max(n_inst_, 1));
     size_t t1 = 0, t2 = 0;
     CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, t1, det_.keys(), cflag_.get(), ckey_.get(),
@@ -372,8 +376,15 @@ void Engine::enq_derivatives() {
 
 void Engine::enq_pcg() {
     if (n_rows_ == 0) return;
-    launch_pcg_persistent(view(), pbuf_.get(), pcg_part_.get(), rowtmp_.get(), pcg_tol_, pcg_max_,
-                          s_);
+    int max_rows = 0;
+    for (int p = 0; p < P_; ++p) max_rows = std::max(max_rows, h_pro_[p + 1] - h_pro_[p]);
+    if (max_rows <= kClusterPcgMaxRows) {
+        // small partitions: one thread-block cluster per partition (DSMEM dots)
+        launch_pcg_cluster(view(), max_rows, pbuf_.get(), pcg_tol_, pcg_max_, s_);
+    } else {
+        launch_pcg_persistent(view(), pbuf_.get(), pcg_part_.get(), rowtmp_.get(), pcg_tol_,
+                              pcg_max_, s_);
+    }
 }
 
 // newton.cpp:16-69, one iteration for every partition still active.
@@ -1155,6 +1166,21 @@ FrameStats Engine::frame_admm(int frame) {
         st.committed = 1;
         return st;
     }
+}
+
+} // namespace dabd_gpu
+
+namespace dabd_gpu {
+
+DevPerf Engine::read_perf(bool reset) {
+    DevPerf h{};
+    CUDA_CHECK(cudaMemcpyAsync(&h, perf_.get(), sizeof(DevPerf), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaStreamSynchronize(s_));
+    if (reset) {
+        perf_.zero(s_);
+        CUDA_CHECK(cudaStreamSynchronize(s_));
+    }
+    return h;
 }
 
 } // namespace dabd_gpu

@@ -78,6 +78,8 @@ class Engine {
     void get_state(double* q, double* qd);
     void get_rho(double* rho) const;
     std::vector<TraceRow> take_trace();
+    // PCG launch accounting since the last reset (device %globaltimer, SURVEY 8(d) bytes).
+    DevPerf read_perf(bool reset);
 
   private:
     // instance sets ----------------------------------------------------------
@@ -175,6 +177,7 @@ class Engine {
     SimParams frame_params_;
     int project_ = 1;
     DBuf<double> pbuf_, pcg_part_;
+    DBuf<DevPerf> perf_;
 
     // fixed capacities (graph-safe) and the captured N=1 frame
     int cap_ = 0;

@@ -107,77 +107,133 @@ __device__ int emit_dir(const SceneView& sc, const InstView& iv, bool swept, dou
     return cnt;
 }
 
-template <bool kWrite>
-__device__ int process_instance(const SceneView& sc, const InstView& iv, const Box* box,
-                                const double* cell_max, unsigned mask, const int* hstart,
-                                const int* hcount, const int* items, const int* stat, int n_stat,
-                                bool swept, double margin, const KeyFmt& fmt, int i,
-                                unsigned long long* out, int pos) {
-    if (sc.is_static[iv.body[i]]) return 0;
-    const Box bi = box[i];
-    const int p = iv.part[i];
-    int cnt = 0;
-    // dynamic partners j > i through the 3x3 cell neighbourhood
-    const double inv = inv_cell(cell_max);
-    const long long cx0 = static_cast<long long>(floor(bi.lo.x * inv)) - 1;
-    const long long cy0 = static_cast<long long>(floor(bi.lo.y * inv)) - 1;
-    const long long cx1 = static_cast<long long>(floor(bi.hi.x * inv));
-    const long long cy1 = static_cast<long long>(floor(bi.hi.y * inv));
-    unsigned seen[9];
-    int ns = 0;
-    for (long long cx = cx0; cx <= cx1; ++cx)
-        for (long long cy = cy0; cy <= cy1; ++cy) {
-            const unsigned h = cell_hash(p, cx, cy, mask);
-            bool dup = false;
-            for (int k = 0; k < ns; ++k) dup |= seen[k] == h;
-            if (dup) continue;
-            if (ns < 9) seen[ns++] = h;
-            const int s0 = hstart[h], s1 = s0 + hcount[h];
-            for (int t = s0; t < s1; ++t) {
-                const int j = items[t];
-                if (j <= i || iv.part[j] != p) continue;
-                if (!overlaps(bi, box[j])) continue;
-                cnt += emit_dir<kWrite>(sc, iv, swept, margin, i, j, fmt, out, pos + cnt);
-                cnt += emit_dir<kWrite>(sc, iv, swept, margin, j, i, fmt, out, pos + cnt);
-            }
-        }
-    // static partners (held by every partition)
-    for (int k = 0; k < n_stat; ++k) {
-        const int s = stat[k];
-        if (iv.part[s] != p || !overlaps(bi, box[s])) continue;
-        cnt += emit_dir<kWrite>(sc, iv, swept, margin, i, s, fmt, out, pos + cnt);
-        cnt += emit_dir<kWrite>(sc, iv, swept, margin, s, i, fmt, out, pos + cnt);
+// Warp-cooperative emission: one warp per dynamic instance. Lanes 0..8 walk
+// the 3x3 hash cells (and all lanes the statics) to collect overlapping
+// partners; then the point x edge tests of each partner pair, both
+// directions, are spread over the 32 lanes and compacted with ballots.
+constexpr int kEmitWarps = 4;
+constexpr int kMaxPartners = 96;
+
+__device__ __forceinline__ bool combo_test(const SceneView& sc, const InstView& iv, bool swept,
+                                           double margin, int A, int B, int c,
+                                           const KeyFmt& fmt, unsigned long long& key) {
+    const int ba = iv.body[A], bb = iv.body[B];
+    const int va = sc.vstart[ba], na = sc.vstart[ba + 1] - va;
+    const int vb = sc.vstart[bb], nbv = sc.vstart[bb + 1] - vb;
+    int P = A, E = B, pv0 = va, ev0 = vb, ne = nbv;
+    if (c >= na * nbv) { // second direction: points of B vs edges of A
+        c -= na * nbv;
+        P = B;
+        E = A;
+        pv0 = vb;
+        ev0 = va;
+        ne = na;
     }
-    return cnt;
+    const int v = c / ne, e = c - v * ne;
+    const Box pb = point_box(sc, iv.q0 + 6 * P, iv.q1 + 6 * P, swept, pv0 + v);
+    const Box eb = edge_box(sc, iv.q0 + 6 * E, iv.q1 + 6 * E, swept, ev0 + e, margin);
+    if (!overlaps(pb, eb)) return false;
+    key = fmt.pack(P, E, v, e);
+    return true;
 }
 
-__global__ void __launch_bounds__(kBlock)
-    k_emit(SceneView sc, InstView iv, const Box* box, const double* cell_max, unsigned mask,
-           const int* hstart, const int* hcount, const int* items, const int* stat, int n_stat,
-           int swept, double margin, KeyFmt fmt, unsigned long long* out, int cap, int* counter,
-           int* err) {
-    using Scan = cub::BlockScan<int, kBlock>;
-    __shared__ typename Scan::TempStorage tmp;
+__global__ void __launch_bounds__(kEmitWarps * 32)
+    k_emit_warp(SceneView sc, InstView iv, const Box* box, const double* cell_max, unsigned mask,
+                const int* hstart, const int* hcount, const int* items, const int* stat,
+                int n_stat, int swept, double margin, KeyFmt fmt, unsigned long long* out, int cap,
+                int* counter, int* err) {
+    __shared__ int partners[kEmitWarps][kMaxPartners];
+    __shared__ int npart[kEmitWarps];
+    __shared__ int wtot[kEmitWarps];
     __shared__ int base;
-    for (int start = blockIdx.x * kBlock; start < iv.n; start += gridDim.x * kBlock) {
-        const int i = start + threadIdx.x;
-        int c = 0;
-        if (i < iv.n)
-            c = process_instance<false>(sc, iv, box, cell_max, mask, hstart, hcount, items, stat,
-                                        n_stat, swept != 0, margin, fmt, i, nullptr, 0);
-        int off, total;
-        Scan(tmp).ExclusiveSum(c, off, total);
-        if (threadIdx.x == 0) base = atomicAdd(&counter[0], total);
-        __syncthreads();
-        const int b0 = base;
-        if (b0 + total > cap) {
-            if (threadIdx.x == 0) {
-                atomicMax(&counter[1], b0 + total);
-                if (err) raise(err, kErrCapacity);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool sw = swept != 0;
+    const double inv = inv_cell(cell_max);
+    for (int start = blockIdx.x * kEmitWarps; start < iv.n; start += gridDim.x * kEmitWarps) {
+        const int i = start + warp;
+        if (lane == 0) npart[warp] = 0;
+        __syncwarp();
+        const bool valid = i < iv.n && !sc.is_static[iv.body[i]];
+        if (valid) {
+            const Box bi = box[i];
+            const int p = iv.part[i];
+            const long long cx0 = static_cast<long long>(floor(bi.lo.x * inv)) - 1;
+            const long long cy0 = static_cast<long long>(floor(bi.lo.y * inv)) - 1;
+            const long long cx1 = static_cast<long long>(floor(bi.hi.x * inv));
+            const long long cy1 = static_cast<long long>(floor(bi.hi.y * inv));
+            const long long cx = cx0 + lane / 3, cy = cy0 + lane % 3;
+            const bool cell_ok = lane < 9 && cx <= cx1 && cy <= cy1;
+            const unsigned h = cell_ok ? cell_hash(p, cx, cy, mask) : 0xffffffffu;
+            bool dup = false;
+#pragma unroll
+            for (int m = 0; m < 9; ++m) {
+                const unsigned hm = __shfl_sync(0xffffffffu, h, m);
+                if (m < lane && cell_ok && hm == h) dup = true;
             }
-        } else if (c > 0) {
-            process_instance<true>(sc, iv, box, cell_max, mask, hstart, hcount, items, stat, n_stat,
-                                   swept != 0, margin, fmt, i, out, b0 + off);
+            if (cell_ok && !dup) {
+                const int s0 = hstart[h], s1 = s0 + hcount[h];
+                for (int t = s0; t < s1; ++t) {
+                    const int j = items[t];
+                    if (j <= i || iv.part[j] != p || !overlaps(bi, box[j])) continue;
+                    const int slot = atomicAdd(&npart[warp], 1);
+                    if (slot < kMaxPartners) partners[warp][slot] = j;
+                }
+            }
+            for (int k = lane; k < n_stat; k += 32) {
+                const int s = stat[k];
+                if (iv.part[s] != p || !overlaps(bi, box[s])) continue;
+                const int slot = atomicAdd(&npart[warp], 1);
+                if (slot < kMaxPartners) partners[warp][slot] = s;
+            }
+        }
+        __syncwarp();
+        const int np_raw = npart[warp];
+        if (np_raw > kMaxPartners && lane == 0 && err) raise(err, kErrCapacity);
+        const int np = min(np_raw, kMaxPartners);
+        // count pass
+        int cnt = 0;
+        for (int q = 0; q < np; ++q) {
+            const int j = partners[warp][q];
+            const int na = sc.vstart[iv.body[i] + 1] - sc.vstart[iv.body[i]];
+            const int nb = sc.vstart[iv.body[j] + 1] - sc.vstart[iv.body[j]];
+            const int combos = 2 * na * nb;
+            for (int c = lane; c < combos; c += 32) {
+                unsigned long long k;
+                cnt += combo_test(sc, iv, sw, margin, i, j, c, fmt, k) ? 1 : 0;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+        if (lane == 0) wtot[warp] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int total = 0;
+            for (int w = 0; w < kEmitWarps; ++w) total += wtot[w];
+            base = atomicAdd(&counter[0], total);
+            if (base + total > cap) {
+                atomicMax(&counter[1], base + total);
+                if (err) raise(err, kErrCapacity);
+                base = -1;
+            }
+        }
+        __syncthreads();
+        if (base >= 0) {
+            int pos = base;
+            for (int w = 0; w < warp; ++w) pos += wtot[w];
+            for (int q = 0; q < np; ++q) {
+                const int j = partners[warp][q];
+                const int na = sc.vstart[iv.body[i] + 1] - sc.vstart[iv.body[i]];
+                const int nb = sc.vstart[iv.body[j] + 1] - sc.vstart[iv.body[j]];
+                const int combos = 2 * na * nb;
+                for (int cb = 0; cb < combos; cb += 32) {
+                    const int c = cb + lane;
+                    unsigned long long k = 0;
+                    const bool hit = c < combos && combo_test(sc, iv, sw, margin, i, j, c, fmt, k);
+                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                    if (hit) out[pos + __popc(bal & ((1u << lane) - 1u))] = k;
+                    pos += __popc(bal);
+                }
+            }
         }
         __syncthreads();
     }
@@ -289,7 +345,7 @@ void Detector::enqueue(const SceneView& sc, const InstView& iv, const int* stat,
                     iv.n, hkey_.get(), hstart_.get(), hfill_.get(), hitems_.get()));
     CUDA_CHECK(cudaMemsetAsync(keys_.get(), 0xFF, sizeof(unsigned long long) * cap_, s));
     DABD_LAUNCH("k_emit", s,
-                k_emit<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(
+                k_emit_warp<<<grid_for(iv.n, kEmitWarps, 148 * 64), kEmitWarps * 32, 0, s>>>(
                     sc, iv, box_.get(), cell_.get(), tsize_ - 1, hstart_.get(), hcount_.get(),
                     hitems_.get(), stat, n_stat, swept ? 1 : 0, margin, fmt_, keys_.get(), cap_,
                     counter_.get(), err));

@@ -1,10 +1,12 @@
 // Launch accounting and opt-in per-kernel CUDA-event timing (bench.py uses
-// them for `gpu_launches` and the roofline of the dominant kernel).
+// them for `gpu_launches`, the roofline of the dominant kernel and the
+// per-kernel breakdown written to profiles/).
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -17,7 +19,8 @@ inline std::atomic<long long>& launch_counter() {
 }
 inline void count_launch(long long n = 1) { launch_counter() += n; }
 
-// Records an event pair around each launch of one named kernel on its stream.
+// Records an event pair around each launch of one named kernel (or of every
+// kernel with name "*") on its stream. Disabled while a graph is captured.
 class KernelTimer {
   public:
     static KernelTimer& get() {
@@ -25,21 +28,21 @@ class KernelTimer {
         return t;
     }
     void enable(const std::string& name) {
-        name_ = name;
         flush();
-        total_ms_ = 0.0;
-        count_ = 0;
+        name_ = name;
+        stats_.clear();
         bytes_ = 0.0;
     }
-    bool active(const char* name) const { return !suspended_ && !name_.empty() && name_ == name; }
-    // No event pairs while a stream is being captured into a graph.
+    bool active(const char* name) const {
+        return !suspended_ && !name_.empty() && (name_ == "*" || name_ == name);
+    }
     void suspend(bool on) { suspended_ = on; }
-    void begin(cudaStream_t s) {
+    void begin(const char* name, cudaStream_t s) {
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a, s);
-        pending_.push_back({a, b});
+        pending_.push_back({a, b, name});
     }
     void end(cudaStream_t s) { cudaEventRecord(pending_.back().b, s); }
     // Algorithmic bytes of the launch just recorded (SURVEY.md 8(d) model).
@@ -50,8 +53,9 @@ class KernelTimer {
         for (auto& p : pending_) {
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
-                total_ms_ += ms;
-                ++count_;
+                Stat& st = stats_[p.name];
+                st.ms += ms;
+                ++st.count;
             }
             cudaEventDestroy(p.a);
             cudaEventDestroy(p.b);
@@ -60,33 +64,50 @@ class KernelTimer {
     }
     double total_ms() {
         flush();
-        return total_ms_;
+        double t = 0.0;
+        for (auto& kv : stats_) t += kv.second.ms;
+        return t;
     }
     long long count() {
         flush();
-        return count_;
+        long long c = 0;
+        for (auto& kv : stats_) c += kv.second.count;
+        return c;
+    }
+    // "name count total_ms;..." for every timed kernel.
+    std::string report() {
+        flush();
+        std::string out;
+        for (auto& kv : stats_)
+            out += kv.first + " " + std::to_string(kv.second.count) + " " +
+                   std::to_string(kv.second.ms) + ";";
+        return out;
     }
 
   private:
     struct Pair {
         cudaEvent_t a, b;
+        std::string name;
+    };
+    struct Stat {
+        double ms = 0.0;
+        long long count = 0;
     };
     std::string name_;
     bool suspended_ = false;
     std::vector<Pair> pending_;
-    double total_ms_ = 0.0;
-    long long count_ = 0;
+    std::map<std::string, Stat> stats_;
     double bytes_ = 0.0;
 };
 
 } // namespace dabd_gpu
 
-// Launch helper: counts the launch and, when this kernel is the timed one,
-// brackets it with CUDA events on `stream`.
+// Launch helper: counts the launch and, when this kernel is timed, brackets
+// it with CUDA events on `stream`.
 #define DABD_LAUNCH(name, stream, ...)                                                     \
     do {                                                                                   \
         const bool _t = ::dabd_gpu::KernelTimer::get().active(name);                       \
-        if (_t) ::dabd_gpu::KernelTimer::get().begin(stream);                              \
+        if (_t) ::dabd_gpu::KernelTimer::get().begin(name, stream);                        \
         __VA_ARGS__;                                                                       \
         if (_t) ::dabd_gpu::KernelTimer::get().end(stream);                                \
         ::dabd_gpu::count_launch();                                                        \

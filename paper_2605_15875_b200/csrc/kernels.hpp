@@ -42,6 +42,12 @@ void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, con
 // Persistent cooperative block-Jacobi PCG over all partitions (pcg.cu).
 // pbuf: 12 * n_rows doubles; partials: 3 * pcg_grid_size(n_rows) * P doubles.
 int pcg_grid_size(int n_rows);
+// Cluster-resident variant: one thread-block cluster (<= 16 CTAs) per partition,
+// used while every partition has at most kClusterPcgMaxRows rows.
+constexpr int kClusterPcgMaxRows = 4096;
+int pcg_cluster_size();
+void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbuf, double tol,
+                        int max_iters, cudaStream_t s);
 void launch_pcg_persistent(const SolverView& sv, double* pbuf, double* partials, double* rowval,
                            double tol, int max_iters, cudaStream_t s);
 

@@ -272,7 +272,339 @@ __global__ void __launch_bounds__(kT) k_pcg(SolverView sv, PcgArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster-resident PCG: one thread-block cluster (up to 16 SMs) per
+// partition. Every CTA stages its chunk of the partition's BSR rows (diagonal
+// + coupling blocks, column ids, block-Jacobi inverses) and all PCG vectors
+// in shared memory; neighbours' z / p come from the owning CTA's shared
+// memory through DSMEM (cluster.map_shared_rank), and the dot products meet
+// through DSMEM + cluster barriers. Nothing but the final dq leaves the SMs,
+// so an iteration costs a few microseconds for the ~1k-body partitions of
+// the N=1 workload. Rows that do not fit the shared-memory budget read their
+// blocks from global memory (L2).
+// ---------------------------------------------------------------------------
+constexpr int kCT = 1024;
+constexpr int kCW = kCT / 32;
+constexpr int kCSmemBytes = 200 * 1024;
+
+// Every CTA pushes its partials into slot [rank][k] of every peer's xch
+// table (fire-and-forget DSMEM stores), so after one cluster barrier each
+// CTA folds the table locally in rank order -- same bits everywhere.
+struct ClusterScalars {
+    double xch[16][3]; // [source rank][p.Ap, r.z, r.r]
+    double val[3];     // this CTA's partials staged for the push
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// Threads 0..csize-1 each store slots [k0, k1) of this CTA's staged values
+// into one peer. Call after `val` is written and a __syncthreads.
+__device__ __forceinline__ void cluster_push(cg::cluster_group& cl, ClusterScalars* sc, int rank,
+                                             int csize, int k0, int k1) {
+    if (static_cast<int>(threadIdx.x) < csize) {
+        ClusterScalars* peer = cl.map_shared_rank(sc, static_cast<int>(threadIdx.x));
+        for (int k = k0; k < k1; ++k) peer->xch[rank][k] = sc->val[k];
+    }
+}
+
+// Every warp folds the 16-entry table with the same xor butterfly, so all
+// threads of all CTAs get identical bits without another barrier.
+__device__ __forceinline__ double cluster_fold(const ClusterScalars* sc, int csize, int k) {
+    const int lane = threadIdx.x & 31;
+    double v = lane < csize ? sc->xch[lane][k] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// Two block-wide sums at once; result valid in warp 0 (fixed shuffle trees).
+__device__ __forceinline__ double2 block_sum2(double a, double b, double2* red2) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, off);
+        b += __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    if (lane == 0) red2[warp] = make_double2(a, b);
+    __syncthreads();
+    double2 r = make_double2(0.0, 0.0);
+    if (warp == 0) {
+        const double2 v = lane < (static_cast<int>(blockDim.x) >> 5) ? red2[lane] : make_double2(0.0, 0.0);
+        double x = v.x, y = v.y;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            x += __shfl_xor_sync(0xffffffffu, x, off);
+            y += __shfl_xor_sync(0xffffffffu, y, off);
+        }
+        r = make_double2(x, y);
+    }
+    return r;
+}
+
+
+__global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, int csize, int cmax_rows) {
+    cg::cluster_group cl = cg::this_cluster();
+    unsigned long long t_start = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ ClusterScalars sc;
+    __shared__ double2 red2[kCW];
+    __shared__ double acc_sh[kCW][32];
+    __shared__ int nblk_total;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = static_cast<int>(cl.block_rank());
+    const int p = blockIdx.x / csize;
+    const int R0 = sv.part_row_off[p], R1 = sv.part_row_off[p + 1];
+    const int chunk = (R1 - R0 + csize - 1) / csize;
+    const int r0 = min(R1, R0 + rank * chunk), r1 = min(R1, r0 + chunk);
+    const int nr = r1 - r0;
+    const PartState& st = sv.ps[p];
+    const bool act = st.active != 0 && R1 > R0;
+    const double eps = st.eps;
+    // shared-memory carve-up (cmax_rows = chunk upper bound used at launch)
+    double* vx = reinterpret_cast<double*>(smem);
+    double* vr = vx + 6 * cmax_rows;
+    double* vz = vr + 6 * cmax_rows;
+    double* vap = vz + 6 * cmax_rows;
+    double* vp0 = vap + 6 * cmax_rows;
+    double* vp1 = vp0 + 6 * cmax_rows;
+    double* dinv = vp1 + 6 * cmax_rows;
+    int* bstart = reinterpret_cast<int*>(dinv + 36 * cmax_rows); // [cmax_rows + 1]
+    int* bcol = bstart + cmax_rows + 1;                             // [cap_blocks]
+    const size_t used = 72ull * cmax_rows * 8 + 4ull * (cmax_rows + 1);
+    const int cap_blocks = static_cast<int>((kCSmemBytes - used) / (36 * 8 + 4));
+    double* blk = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(bcol + cap_blocks) + 15) & ~uintptr_t(15));
+    const int comp = lane % 6, grp = lane / 6;
+
+    // ---- stage rows: block offsets (diag first), blocks, columns, Dinv
+    for (int lr = threadIdx.x; lr < nr; lr += kCT) bstart[lr + 1] = sv.ell_cnt[r0 + lr] + 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        bstart[0] = 0;
+        for (int lr = 0; lr < nr; ++lr) bstart[lr + 1] += bstart[lr];
+        nblk_total = bstart[nr];
+    }
+    __syncthreads();
+    for (int lr = warp; lr < nr; lr += kCW) {
+        const int r = r0 + lr;
+        const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
+        for (int t = 0; t < nb; ++t) {
+            const int slot = b0 + t;
+            if (slot >= cap_blocks) break; // spills to global reads below
+            const double* src = t == 0 ? sv.rdiag + 36 * r
+                                       : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36;
+            for (int k = lane; k < 36; k += 32) blk[36 * slot + k] = src[k];
+            if (lane == 0) bcol[slot] = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+        }
+        for (int k = lane; k < 36; k += 32) dinv[36 * lr + k] = sv.rdinv[36 * r + k];
+    }
+    __syncthreads();
+
+    // ---- init: r = -grad, x = 0, z = Dinv r, p_old = 0
+    double s_rz = 0.0, s_rr = 0.0;
+    for (int lr = warp; lr < nr; lr += kCW) {
+        const int r = r0 + lr;
+        double g = 0.0;
+        if (lane < 6) g = act ? -sv.rgrad[6 * r + lane] : 0.0;
+        double z = 0.0;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            const double gc = __shfl_sync(0xffffffffu, g, c);
+            if (lane < 6) z += dinv[36 * lr + 6 * lane + c] * gc;
+        }
+        if (lane < 6) {
+            vr[6 * lr + lane] = g;
+            vz[6 * lr + lane] = z;
+            vx[6 * lr + lane] = 0.0;
+            vp0[6 * lr + lane] = 0.0;
+            s_rz += g * z;
+            s_rr += g * g;
+        }
+    }
+    const double2 bb = block_sum2(s_rz, s_rr, red2);
+    if (threadIdx.x == 0) {
+        sc.val[1] = bb.x;
+        sc.val[2] = bb.y;
+    }
+    __syncthreads();
+    cluster_push(cl, &sc, rank, csize, 1, 3);
+    cl.sync();
+    double rz = cluster_fold(&sc, csize, 1);
+    const double bnorm2 = cluster_fold(&sc, csize, 2);
+    bool done = !act || bnorm2 == 0.0;
+    double beta = 0.0;
+    int it = 0, cur = 0;
+    while (!done) {
+        double* pold = cur ? vp1 : vp0;
+        double* pnew = cur ? vp0 : vp1;
+        // ---- phase A: p_new = z + beta p_old ; Ap ; p.Ap
+        double pap = 0.0;
+        for (int lr = warp; lr < nr; lr += kCW) {
+            const int r = r0 + lr;
+            const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
+            double acc = 0.0;
+            if (grp < 5) {
+                for (int t = grp; t < nb; t += 5) {
+                    const int slot = b0 + t;
+                    const bool in_smem = slot < cap_blocks;
+                    const int col = in_smem ? bcol[slot]
+                                            : (t == 0 ? r : sv.ell_col[r * kEll + t - 1]);
+                    const double* M = in_smem ? blk + 36 * slot
+                                              : (t == 0 ? sv.rdiag + 36 * r
+                                                        : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36);
+                    const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
+                    const double* zc = cl.map_shared_rank(vz, crank) + 6 * cl_row;
+                    const double* pc = cl.map_shared_rank(pold, crank) + 6 * cl_row;
+                    double y = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        const double v = zc[c] + beta * pc[c];
+                        y += M[6 * comp + c] * v;
+                        if (t == 0 && c == comp) y += eps * v;
+                    }
+                    acc += y;
+                }
+            }
+            acc_sh[warp][lane] = acc;
+            __syncwarp();
+            if (lane < 6) {
+                double y = 0.0;
+#pragma unroll
+                for (int g = 0; g < 5; ++g) y += acc_sh[warp][g * 6 + lane];
+                const double pr = vz[6 * lr + lane] + beta * pold[6 * lr + lane];
+                pnew[6 * lr + lane] = pr;
+                vap[6 * lr + lane] = y;
+                pap += pr * y;
+            }
+            __syncwarp();
+        }
+        const double2 bp = block_sum2(pap, 0.0, red2);
+        if (threadIdx.x == 0) sc.val[0] = bp.x;
+        __syncthreads();
+        cluster_push(cl, &sc, rank, csize, 0, 1);
+        cl.sync();
+        const double pap_all = cluster_fold(&sc, csize, 0);
+        if (!(pap_all > 0.0)) break; // exact solution or breakdown (uniform)
+        const double alpha = rz / pap_all;
+        // ---- phase B: x += alpha p ; r -= alpha Ap ; z = Dinv r
+        double l_rz = 0.0, l_rr = 0.0;
+        for (int lr = warp; lr < nr; lr += kCW) {
+            double rv = 0.0;
+            if (lane < 6) {
+                vx[6 * lr + lane] += alpha * pnew[6 * lr + lane];
+                rv = vr[6 * lr + lane] - alpha * vap[6 * lr + lane];
+                vr[6 * lr + lane] = rv;
+            }
+            double z = 0.0;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                const double rc = __shfl_sync(0xffffffffu, rv, c);
+                if (lane < 6) z += dinv[36 * lr + 6 * lane + c] * rc;
+            }
+            if (lane < 6) {
+                l_rz += rv * z;
+                l_rr += rv * rv;
+            }
+            __syncwarp();
+            if (lane < 6) vz[6 * lr + lane] = z;
+        }
+        const double2 cc = block_sum2(l_rz, l_rr, red2);
+        if (threadIdx.x == 0) {
+            sc.val[1] = cc.x;
+            sc.val[2] = cc.y;
+        }
+        __syncthreads();
+        cluster_push(cl, &sc, rank, csize, 1, 3);
+        cl.sync();
+        const double rz_new = cluster_fold(&sc, csize, 1);
+        const double rr = cluster_fold(&sc, csize, 2);
+        beta = rz != 0.0 ? rz_new / rz : 0.0;
+        rz = rz_new;
+        ++it;
+        if (rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters) done = true;
+        cur ^= 1;
+        // Two barriers per iteration suffice: the one above orders our z /
+        // p_new writes before the peers' next phase A, the one in phase A
+        // orders their reads of our z before our next phase-B writes.
+    }
+    for (int lr = warp; lr < nr; lr += kCW)
+        if (lane < 6) sv.x[6 * (r0 + lr) + lane] = vx[6 * lr + lane];
+    if (rank == 0 && threadIdx.x == 0) {
+        sv.ps[p].pcg_iters = it;
+        sv.ps[p].pcg_done = 1;
+    }
+    cl.sync(); // no CTA leaves while a peer may still read its shared memory
+    if (sv.perf && threadIdx.x == 0) {
+        if (rank == 0) { // algorithmic bytes of this partition's solve
+            int nblk = 0;
+            for (int r = R0; r < R1; ++r) nblk += sv.ell_cnt[r] + 1;
+            atomicAdd(&sv.perf->bytes, static_cast<double>(it) * (288.0 * nblk + 504.0 * (R1 - R0)));
+            atomicAdd(&sv.perf->iters, static_cast<unsigned long long>(it));
+        }
+        if (blockIdx.x == 0) {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            atomicAdd(&sv.perf->ns, t1 - t_start);
+            atomicAdd(&sv.perf->launches, 1ull);
+        }
+    }
+}
+
 } // namespace
+
+int pcg_cluster_size() {
+    static int c = 0;
+    if (c == 0) {
+        cudaFuncSetAttribute(k_pcg_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(k_pcg_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kCSmemBytes);
+        c = 16;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(16);
+        cfg.blockDim = dim3(kCT);
+        cfg.dynamicSmemBytes = kCSmemBytes;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 16;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_pcg_cluster, &cfg) != cudaSuccess || n < 1) c = 8;
+        cudaGetLastError();
+    }
+    return c;
+}
+
+void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbuf, double tol,
+                        int max_iters, cudaStream_t s) {
+    if (sv.n_rows == 0) return;
+    const int cmax = pcg_cluster_size();
+    int csize = 1;
+    while (csize < cmax && csize * 32 < max_rows_per_part) csize *= 2; // >= ~32 rows per CTA
+    const int cmax_rows = (max_rows_per_part + csize - 1) / csize;
+    PcgArgs a{pbuf, nullptr, nullptr, tol, max_iters};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csize * sv.n_parts);
+    cfg.blockDim = dim3(kCT);
+    cfg.dynamicSmemBytes = kCSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DABD_LAUNCH("k_pcg", s,
+                CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg_cluster, sv, a, csize, cmax_rows)));
+}
 
 int pcg_grid_size(int n_rows) {
     static int max_blocks = 0;

@@ -40,7 +40,19 @@ struct PartState {
     int n_candidates;
 };
 
+// Device-side launch accounting of the PCG kernel (bench.py roofline): the
+// launch duration from %globaltimer (first CTA in, last CTA out of the first
+// cluster) and the algorithmic bytes of SURVEY.md 8(d):
+// I_pcg * [288 * (N_b + 2 E_o) + 504 * N_b] per partition.
+struct DevPerf {
+    unsigned long long ns;
+    unsigned long long launches;
+    double bytes;
+    unsigned long long iters;
+};
+
 struct SolverView {
+    DevPerf* perf = nullptr;
     SceneView sc;
     int n_inst = 0, n_rows = 0, n_parts = 0, part_base = 0;
     // instances
