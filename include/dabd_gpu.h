@@ -92,6 +92,30 @@ typedef struct dabd_gpu_frame_stats {
     int max_candidates;
 } dabd_gpu_frame_stats;
 
+/* Inter-GPU exchange of a partition-per-GPU run; replaces
+ * the reference's Transport (include/dabd/transport.hpp:15-40) on the data
+ * path. Rank r owns partitions [part_offsets[r], part_offsets[r+1]) and
+ * creates its context with exactly that range. All pointers handed to the
+ * callbacks are DEVICE pointers on `stream` (a cudaStream_t); a callback
+ * returns 0 on success and must leave the results ordered before later work
+ * on `stream` (e.g. NCCL on that stream).
+ *   halo: send n_lo doubles from send_lo to rank-1 and receive n_lo from it
+ *         into recv_lo; likewise n_hi with rank+1. Both sides always agree on
+ *         the counts (they derive them from the same replicated holder masks);
+ *         a zero count means no transfer on that side.
+ *   allgather: every rank contributes `count` doubles; recv holds
+ *         world * count doubles in rank order. */
+typedef struct dabd_gpu_comm {
+    void* user;
+    int (*halo)(void* user, const double* send_lo, double* recv_lo, size_t n_lo,
+                const double* send_hi, double* recv_hi, size_t n_hi, uintptr_t stream);
+    int (*allgather)(void* user, const double* send, double* recv, size_t count,
+                     uintptr_t stream);
+    int rank;
+    int world;
+    const int* part_offsets; /* world + 1 entries, copied */
+} dabd_gpu_comm;
+
 typedef struct dabd_gpu_scene dabd_gpu_scene;
 typedef struct dabd_gpu_ctx dabd_gpu_ctx;
 
@@ -136,6 +160,10 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_solver(dabd_gpu_ctx* ctx,
                                                      const dabd_gpu_solver_params* p);
 /* Stream (cudaStream_t as uintptr_t) the context launches on; 0 = own stream. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_stream(dabd_gpu_ctx* ctx, uintptr_t stream);
+/* Join a partition-per-GPU run (comm == NULL leaves it). Required when the
+ * context's partition range is not [0, num_workers). The callbacks are
+ * called from the thread that calls dabd_gpu_run_frames. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_comm(dabd_gpu_ctx* ctx, const dabd_gpu_comm* comm);
 
 /* ---- parity entry points (identical-input comparisons with the oracle) ---
  * subset == NULL means all bodies. q_end == NULL: static broad phase. On

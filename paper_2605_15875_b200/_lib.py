@@ -44,6 +44,17 @@ class FrameStats(C.Structure):
                 ("max_contacts", C.c_int), ("max_candidates", C.c_int)]
 
 
+HaloFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                     C.c_void_p, C.c_size_t, C.c_size_t)
+AllgatherFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t)
+
+
+class Comm(C.Structure):
+    """dabd_gpu_comm (include/dabd_gpu.h)."""
+    _fields_ = [("user", C.c_void_p), ("halo", HaloFn), ("allgather", AllgatherFn),
+                ("rank", C.c_int), ("world", C.c_int), ("part_offsets", _ip)]
+
+
 # Every symbol include/dabd_gpu.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "dabd_gpu_version", "dabd_gpu_last_error", "dabd_gpu_scene_create", "dabd_gpu_scene_free",
@@ -54,7 +65,7 @@ EXPORTS = [
     "dabd_gpu_newton_solve", "dabd_gpu_run_frames", "dabd_gpu_set_state", "dabd_gpu_get_state",
     "dabd_gpu_get_rho", "dabd_gpu_take_trace", "dabd_gpu_launch_count",
     "dabd_gpu_kernel_timer_enable", "dabd_gpu_kernel_timer_read", "dabd_gpu_kernel_timer_report",
-    "dabd_gpu_ctx_pcg_perf",
+    "dabd_gpu_ctx_pcg_perf", "dabd_gpu_ctx_set_comm",
 ]
 
 _lib = None

@@ -124,6 +124,11 @@ class Context:
     def set_stream(self, stream_handle: int) -> None:
         L.check(L.load().dabd_gpu_ctx_set_stream(self.h, int(stream_handle)))
 
+    def set_comm(self, comm) -> None:
+        """Join a partition-per-GPU run (dist.TorchComm, or None to leave)."""
+        L.check(L.load().dabd_gpu_ctx_set_comm(self.h, None if comm is None else C.byref(comm.struct)))
+        self._comm = comm
+
     # ---- geometry (geometry.hpp:47-74) -------------------------------------
     def broad_phase(self, q, margin, q_end=None, subset=None) -> np.ndarray:
         q = _f64(q, (self.n, 6))
@@ -212,7 +217,12 @@ class Context:
     # ---- stepping ----------------------------------------------------------
     def run_frames(self, n: int) -> List[dict]:
         st = (L.FrameStats * max(n, 1))()
-        L.check(L.load().dabd_gpu_run_frames(self.h, n, st))
+        status = L.load().dabd_gpu_run_frames(self.h, n, st)
+        comm = getattr(self, "_comm", None)
+        if status != 0 and comm is not None and comm.error is not None:
+            err, comm.error = comm.error, None
+            raise L.DabdGpuError(status, L.load().dabd_gpu_last_error().decode()) from err
+        L.check(status)
         return [{k: getattr(st[i], k) for k, _ in L.FrameStats._fields_} for i in range(n)]
 
     def state(self):

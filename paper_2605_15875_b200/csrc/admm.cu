@@ -131,44 +131,93 @@ __global__ void k_vmax(SceneView sc, const double* qd, double* out) {
 // Consensus over the two replicas of each shared body (consensus.cpp:9-36,
 // runtime.cpp:365-397): z = sum rho (q + u) / sum rho in ascending worker
 // order, u' = u + q - z, r_b, s_b.
+//
+// A replica handle v >= 0 is a local instance; v < 0 is the halo packet
+// -1 - v received from the neighbouring rank (q[6], u[6], rho). Both ranks of
+// a cross-GPU pair evaluate the same expression in the same (ascending
+// partition) order, so they agree on z bit for bit; each updates only its
+// own replica.
+struct Replica {
+    const double* q;
+    double* u;
+    double rho;
+    int inst; // -1 when remote
+};
+
+__device__ __forceinline__ Replica replica(int v, const double* iq, double* iu, const double* irho,
+                                           const double* remote) {
+    if (v >= 0) return Replica{iq + 6 * v, iu + 6 * v, irho[v], v};
+    const double* p = remote + kHaloStride * (-1 - v);
+    return Replica{p, const_cast<double*>(p + 6), p[12], -1};
+}
+
 __global__ void k_consensus(int ns, const int* sh, const int* ipart, int part_base,
                             const double* iq, double* iu, const double* irho, const double* iz,
-                            double* iznext, double* rb, double* sb, double* rloc, double* sloc,
-                            int* err) {
+                            const double* remote, double* iznext, double* rb, double* sb,
+                            double* rloc, double* sloc, int* err) {
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
-        const int i0 = sh[2 * s], i1 = sh[2 * s + 1];
-        const double r0 = irho[i0], r1 = irho[i1];
-        if (r0 != r1) raise(err, kErrReplica);
+        const Replica a = replica(sh[2 * s], iq, iu, irho, remote);
+        const Replica b = replica(sh[2 * s + 1], iq, iu, irho, remote);
+        if (a.rho != b.rho) raise(err, kErrReplica);
         double z[6];
-        const double den = xadd(xadd(0.0, r0), r1);
+        const double den = xadd(xadd(0.0, a.rho), b.rho);
         for (int k = 0; k < 6; ++k) {
-            const double qu0 = xadd(iq[6 * i0 + k], iu[6 * i0 + k]);
-            const double qu1 = xadd(iq[6 * i1 + k], iu[6 * i1 + k]);
-            const double num = xadd(xadd(0.0, xmul(r0, qu0)), xmul(r1, qu1));
+            const double qu0 = xadd(a.q[k], a.u[k]);
+            const double qu1 = xadd(b.q[k], b.u[k]);
+            const double num = xadd(xadd(0.0, xmul(a.rho, qu0)), xmul(b.rho, qu1));
             z[k] = xdiv(num, den);
         }
-        double rmax = 0.0, s0 = 0.0, s1 = 0.0;
+        double rmax = 0.0;
         for (int k = 0; k < 6; ++k) {
-            rmax = fmax(rmax, fabs(xsub(iq[6 * i0 + k], z[k])));
-            rmax = fmax(rmax, fabs(xsub(iq[6 * i1 + k], z[k])));
-            s0 = fmax(s0, fabs(xsub(z[k], iz[6 * i0 + k])));
-            s1 = fmax(s1, fabs(xsub(z[k], iz[6 * i1 + k])));
+            rmax = fmax(rmax, fabs(xsub(a.q[k], z[k])));
+            rmax = fmax(rmax, fabs(xsub(b.q[k], z[k])));
         }
+        const int mine[2] = {a.inst, b.inst};
+        for (int side = 0; side < 2; ++side) {
+            const int i = mine[side];
+            if (i < 0) continue;
+            double sm = 0.0;
+            for (int k = 0; k < 6; ++k) {
+                sm = fmax(sm, fabs(xsub(z[k], iz[6 * i + k])));
+                iu[6 * i + k] = xsub(xadd(iu[6 * i + k], iq[6 * i + k]), z[k]);
+                iznext[6 * i + k] = z[k];
+            }
+            rb[i] = rmax;
+            sb[i] = sm;
+            const int p = ipart[i] - part_base;
+            atomic_max_nonneg(&rloc[p], rmax);
+            atomic_max_nonneg(&sloc[p], sm);
+        }
+    }
+}
+
+// Halo packets of the local replicas a neighbouring rank pairs with.
+__global__ void k_pack_halo(int n, const int* inst, const double* iq, const double* iu,
+                            const double* irho, double* out) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int i = inst[j];
+        double* o = out + kHaloStride * j;
         for (int k = 0; k < 6; ++k) {
-            iu[6 * i0 + k] = xsub(xadd(iu[6 * i0 + k], iq[6 * i0 + k]), z[k]);
-            iu[6 * i1 + k] = xsub(xadd(iu[6 * i1 + k], iq[6 * i1 + k]), z[k]);
-            iznext[6 * i0 + k] = z[k];
-            iznext[6 * i1 + k] = z[k];
+            o[k] = iq[6 * i + k];
+            o[6 + k] = iu[6 * i + k];
         }
-        rb[i0] = rmax;
-        rb[i1] = rmax;
-        sb[i0] = s0;
-        sb[i1] = s1;
-        const int p0 = ipart[i0] - part_base, p1 = ipart[i1] - part_base;
-        atomic_max_nonneg(&rloc[p0], rmax);
-        atomic_max_nonneg(&rloc[p1], rmax);
-        atomic_max_nonneg(&sloc[p0], s0);
-        atomic_max_nonneg(&sloc[p1], s1);
+        o[12] = irho[i];
+    }
+}
+
+// After the commit all-gather: every dynamic body takes the state written by
+// the rank that holds its lowest partition (runtime.cpp:484-506 "the lowest
+// holder commits").
+__global__ void k_select_commit(SceneView sc, const uint32_t* bmask, const int* part_rank,
+                                const double* gath, size_t stride, double* q, double* qd) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < sc.nb; b += gridDim.x * blockDim.x) {
+        if (sc.is_static[b]) continue;
+        const int r = part_rank[__ffs(bmask[b]) - 1];
+        const double* src = gath + stride * r;
+        for (int k = 0; k < 6; ++k) {
+            q[6 * b + k] = src[6 * b + k];
+            qd[6 * b + k] = src[6 * sc.nb + 6 * b + k];
+        }
     }
 }
 
@@ -258,11 +307,25 @@ void launch_vmax(const SceneView& sc, const double* qd, double* out, cudaStream_
 }
 
 void launch_consensus(int ns, const int* sh, const int* ipart, int part_base, const double* iq,
-                      double* iu, const double* irho, const double* iz, double* iznext, double* rb,
-                      double* sb, double* rloc, double* sloc, int* err, cudaStream_t s) {
+                      double* iu, const double* irho, const double* iz, const double* remote,
+                      double* iznext, double* rb, double* sb, double* rloc, double* sloc, int* err,
+                      cudaStream_t s) {
     if (ns == 0) return;
-    DABD_LAUNCH("k_consensus", s, k_consensus<<<grid_for(ns, kB), kB, 0, s>>>(ns, sh, ipart, part_base, iq, iu, irho, iz, iznext,
-                                                rb, sb, rloc, sloc, err));
+    DABD_LAUNCH("k_consensus", s, k_consensus<<<grid_for(ns, kB), kB, 0, s>>>(ns, sh, ipart, part_base, iq, iu, irho, iz,
+                                                remote, iznext, rb, sb, rloc, sloc, err));
+}
+
+void launch_pack_halo(int n, const int* inst, const double* iq, const double* iu,
+                      const double* irho, double* out, cudaStream_t s) {
+    if (n == 0) return;
+    DABD_LAUNCH("k_pack_halo", s, k_pack_halo<<<grid_for(n, kB), kB, 0, s>>>(n, inst, iq, iu, irho, out));
+}
+
+void launch_select_commit(const SceneView& sc, const uint32_t* bmask, const int* part_rank,
+                          const double* gath, size_t stride, double* q, double* qd,
+                          cudaStream_t s) {
+    if (sc.nb == 0) return;
+    DABD_LAUNCH("k_select_commit", s, k_select_commit<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, bmask, part_rank, gath, stride, q, qd));
 }
 
 void launch_merged(int n, const int* ianc, const double* iq, const double* iznext, double* out,

@@ -15,9 +15,18 @@ void launch_delta_inf(int n_rows, const int* rinst, const int* rpart, int part_b
 void launch_masks(const SceneView& sc, const double* q, const double* planes, int np, double w,
                   uint32_t all, uint32_t* masks, int* err, cudaStream_t s);
 void launch_vmax(const SceneView& sc, const double* qd, double* out, cudaStream_t s);
+// Halo packet of one replica: q[6], u[6], rho.
+constexpr int kHaloStride = 13;
+
 void launch_consensus(int ns, const int* sh, const int* ipart, int part_base, const double* iq,
-                      double* iu, const double* irho, const double* iz, double* iznext, double* rb,
-                      double* sb, double* rloc, double* sloc, int* err, cudaStream_t s);
+                      double* iu, const double* irho, const double* iz, const double* remote,
+                      double* iznext, double* rb, double* sb, double* rloc, double* sloc, int* err,
+                      cudaStream_t s);
+void launch_pack_halo(int n, const int* inst, const double* iq, const double* iu,
+                      const double* irho, double* out, cudaStream_t s);
+void launch_select_commit(const SceneView& sc, const uint32_t* bmask, const int* part_rank,
+                          const double* gath, size_t stride, double* q, double* qd,
+                          cudaStream_t s);
 void launch_merged(int n, const int* ianc, const double* iq, const double* iznext, double* out,
                    cudaStream_t s);
 void launch_adapt(int n, const int* ianc, double* irho, const double* irho0, const double* rb,

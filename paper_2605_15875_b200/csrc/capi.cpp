@@ -206,6 +206,26 @@ dabd_gpu_status dabd_gpu_ctx_set_stream(dabd_gpu_ctx* ctx, uintptr_t stream) {
     });
 }
 
+dabd_gpu_status dabd_gpu_ctx_set_comm(dabd_gpu_ctx* ctx, const dabd_gpu_comm* comm) {
+    if (!ctx) return null_arg();
+    return guarded([&] {
+        dabd_gpu::Comm c;
+        if (comm) {
+            if (!comm->halo || !comm->allgather || !comm->part_offsets || comm->world < 1 ||
+                comm->rank < 0 || comm->rank >= comm->world)
+                throw dabd_gpu::InvalidArg("comm: missing callbacks or bad rank/world");
+            c.user = comm->user;
+            c.halo = comm->halo;
+            c.allgather = comm->allgather;
+            c.rank = comm->rank;
+            c.world = comm->world;
+            c.part_offsets.assign(comm->part_offsets, comm->part_offsets + comm->world + 1);
+        }
+        ctx->e->set_comm(comm ? &c : nullptr);
+        return DABD_GPU_OK;
+    });
+}
+
 dabd_gpu_status dabd_gpu_broad_phase(dabd_gpu_ctx* ctx, const double* q, const double* q_end,
                                      double margin, const int* subset, int n_subset, int* pairs,
                                      int capacity, int* count) {

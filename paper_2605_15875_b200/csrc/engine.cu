@@ -114,6 +114,71 @@ void Engine::set_stream(cudaStream_t s) {
     }
 }
 
+void Engine::set_comm(const Comm* c) {
+    sync();
+    if (!c) {
+        distributed_ = false;
+        comm_ = Comm{};
+        return;
+    }
+    if (W_ == 0) throw InvalidArg("comm: a run_reference context (0 workers) has no exchange");
+    const std::vector<int>& o = c->part_offsets;
+    if (static_cast<int>(o.size()) != c->world + 1 || o.front() != 0 || o.back() != W_)
+        throw InvalidArg("comm: part_offsets must cover [0, num_workers)");
+    for (int r = 0; r < c->world; ++r)
+        if (o[r] >= o[r + 1]) throw InvalidArg("comm: every rank needs at least one partition");
+    if (o[c->rank] != p0_ || o[c->rank + 1] != p1_)
+        throw InvalidArg("comm: the context's partition range differs from part_offsets[rank]");
+    comm_ = *c;
+    distributed_ = c->world > 1;
+    std::vector<int> pr(W_);
+    for (int r = 0; r < c->world; ++r)
+        for (int p = o[r]; p < o[r + 1]; ++p) pr[p] = r;
+    part_rank_.upload(pr, s_);
+    sync();
+}
+
+void Engine::exchange_halo() {
+    const int n = n_halo_lo_ + n_halo_hi_;
+    launch_pack_halo(n, halo_inst_.get(), iq_.get(), iu_.get(), irho_.get(), hsend_.get(), s_);
+    const size_t lo = static_cast<size_t>(kHaloStride) * n_halo_lo_;
+    const size_t hi = static_cast<size_t>(kHaloStride) * n_halo_hi_;
+    if (comm_.halo(comm_.user, hsend_.get(), hrecv_.get(), lo, hsend_.get() + lo, hrecv_.get() + lo,
+                   hi, reinterpret_cast<uintptr_t>(s_)) != 0)
+        throw Error("comm: halo exchange failed");
+}
+
+std::vector<double> Engine::allgather_host(const std::vector<double>& mine) {
+    // fixed record width so every rank passes the same count
+    int pmax = 0;
+    for (int r = 0; r < comm_.world; ++r)
+        pmax = std::max(pmax, comm_.part_offsets[r + 1] - comm_.part_offsets[r]);
+    const size_t count = 2 + 4 * static_cast<size_t>(pmax);
+    std::vector<double> rec(mine);
+    rec.resize(count, 0.0);
+    rec_.upload(rec, s_);
+    rec_all_.resize(count * comm_.world);
+    if (comm_.allgather(comm_.user, rec_.get(), rec_all_.get(), count,
+                        reinterpret_cast<uintptr_t>(s_)) != 0)
+        throw Error("comm: all-gather failed");
+    return rec_all_.to_host(s_);
+}
+
+void Engine::commit_gather() {
+    // Each rank wrote the bodies it holds; the lowest holder's copy wins.
+    const size_t n6 = 6 * static_cast<size_t>(hs_.nb), stride = 2 * n6;
+    rec_.resize(stride);
+    CUDA_CHECK(cudaMemcpyAsync(rec_.get(), q_.get(), n6 * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+    CUDA_CHECK(cudaMemcpyAsync(rec_.get() + n6, qd_.get(), n6 * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s_));
+    gath_.resize(stride * comm_.world);
+    if (comm_.allgather(comm_.user, rec_.get(), gath_.get(), stride,
+                        reinterpret_cast<uintptr_t>(s_)) != 0)
+        throw Error("comm: commit all-gather failed");
+    launch_select_commit(ds_.view(), bmask_.get(), part_rank_.get(), gath_.get(), stride, q_.get(),
+                         qd_.get(), s_);
+}
+
 void Engine::check_err(const char* where) {
     CUDA_CHECK(cudaMemcpyAsync(pin_i_.get(), err_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
     CUDA_CHECK(cudaStreamSynchronize(s_));
@@ -1065,9 +1130,39 @@ FrameStats Engine::frame_admm(int frame) {
                 h_shared_inst_.push_back(i);
             }
         }
+        // replicas whose partner partition lives on a neighbouring rank
+        // (partition-per-GPU runs): lo side = shared with p0-1, hi side =
+        // shared with p1; both lists in instance (= body) order, which the
+        // neighbour derives identically from the same masks.
+        h_halo_inst_.clear();
+        std::vector<int> hi_list;
+        for (int i = 0; i < I; ++i) {
+            if (!anc[i]) continue;
+            const int b = h_ibody_[i];
+            const int lo = std::countr_zero(mask[b]), hi = 31 - std::countl_zero(mask[b]);
+            if (lo < p0_) h_halo_inst_.push_back(i);
+            else if (hi >= p1_) hi_list.push_back(i);
+        }
+        n_halo_lo_ = static_cast<int>(h_halo_inst_.size());
+        n_halo_hi_ = static_cast<int>(hi_list.size());
+        if ((n_halo_lo_ || n_halo_hi_) && !distributed_)
+            throw Error("ctx: the partition range needs dabd_gpu_ctx_set_comm (neighbour partitions are remote)");
+        for (int j = 0; j < n_halo_lo_; ++j) { // remote replica first (lower partition)
+            h_shared_inst_.push_back(-1 - j);
+            h_shared_inst_.push_back(h_halo_inst_[j]);
+        }
+        for (int j = 0; j < n_halo_hi_; ++j) {
+            h_shared_inst_.push_back(hi_list[j]);
+            h_shared_inst_.push_back(-1 - (n_halo_lo_ + j));
+        }
+        h_halo_inst_.insert(h_halo_inst_.end(), hi_list.begin(), hi_list.end());
         const int ns = static_cast<int>(h_shared_inst_.size() / 2);
-        if (W_ > 1 && P_ < W_ && ns * 2 != static_cast<int>(std::count(anc.begin(), anc.begin() + I, 1)))
-            throw Error("multi-GPU replica exchange is driven through the distributed runtime");
+        if (distributed_) {
+            const size_t nh = std::max<size_t>(h_halo_inst_.size(), 1);
+            halo_inst_.upload(h_halo_inst_.empty() ? std::vector<int>{0} : h_halo_inst_, s_);
+            hsend_.resize(kHaloStride * nh);
+            hrecv_.resize(kHaloStride * nh);
+        }
         iinvk_.upload(invk.data(), std::max(I, 1), s_);
         irho_.upload(rho.data(), std::max(I, 1), s_);
         irho0_.upload(rho0.data(), std::max(I, 1), s_);
@@ -1087,29 +1182,63 @@ FrameStats Engine::frame_admm(int frame) {
         const double tol = P.theta * h * P.scene_scale;
         std::vector<double> dq(P_, 0.0);
         bool ended = false, retry = false;
+        // A local failure on one rank must not leave its peers blocked in a
+        // collective: it is carried to the next agreement point instead.
+        std::string fail;
         for (int k = 1; k <= hs_.admm_max_iterations; ++k) {
             if (k > 1) {
-                rloc_.zero(s_);
-                sloc_.zero(s_);
-                launch_consensus(ns, shared_inst_.get(), ipart_.get(), p0_, iq_.get(), iu_.get(),
-                                 irho_.get(), iz_.get(), iznext_.get(), rb_.get(), sb_.get(),
-                                 rloc_.get(), sloc_.get(), err_.get(), s_);
-                // merge CCD gate per partition (consensus.cpp:66-75)
-                launch_merged(I, ianc_.get(), iq_.get(), iznext_.get(), iqtry_.get(), s_);
-                const int nc = det_gate_.build(ds_.view(), iview(iq_.get(), iqtry_.get()),
-                                               stat_.get(), static_cast<int>(h_stat_.size()), true,
-                                               0.0, ds_.max_verts, s_);
-                std::vector<double> init(P_, 2.0);
-                gate_.upload(init, s_);
-                launch_ccd(view(), det_gate_.keys(), nc, nullptr, det_gate_.fmt(), det_gate_.boxes(),
-                           iq_.get(), iqtry_.get(), 2, gate_.get(), s_);
-                std::vector<double> earliest = gate_.to_host(s_);
-                std::vector<double> rl = rloc_.to_host(s_), sl = sloc_.to_host(s_);
-                check_err("admm: consensus/gate");
+                std::vector<double> earliest(P_, 2.0), rl(P_, 0.0), sl(P_, 0.0);
+                try {
+                    if (!fail.empty()) throw Error(fail);
+                    rloc_.zero(s_);
+                    sloc_.zero(s_);
+                    if (distributed_) exchange_halo();
+                    launch_consensus(ns, shared_inst_.get(), ipart_.get(), p0_, iq_.get(),
+                                     iu_.get(), irho_.get(), iz_.get(), hrecv_.get(), iznext_.get(),
+                                     rb_.get(), sb_.get(), rloc_.get(), sloc_.get(), err_.get(), s_);
+                    // merge CCD gate per partition (consensus.cpp:66-75)
+                    launch_merged(I, ianc_.get(), iq_.get(), iznext_.get(), iqtry_.get(), s_);
+                    const int nc = det_gate_.build(ds_.view(), iview(iq_.get(), iqtry_.get()),
+                                                   stat_.get(), static_cast<int>(h_stat_.size()),
+                                                   true, 0.0, ds_.max_verts, s_);
+                    gate_.upload(earliest, s_);
+                    launch_ccd(view(), det_gate_.keys(), nc, nullptr, det_gate_.fmt(),
+                               det_gate_.boxes(), iq_.get(), iqtry_.get(), 2, gate_.get(), s_);
+                    earliest = gate_.to_host(s_);
+                    rl = rloc_.to_host(s_);
+                    sl = sloc_.to_host(s_);
+                    check_err("admm: consensus/gate");
+                } catch (const Error& e) {
+                    if (!distributed_) throw;
+                    if (fail.empty()) fail = e.what();
+                }
+                if (distributed_) {
+                    // controller fan-in (runtime.cpp:586-619): every rank
+                    // sees every partition's (dq, r, s, earliest TOI).
+                    std::vector<double> rec = {static_cast<double>(P_), fail.empty() ? 0.0 : 1.0};
+                    for (int p = 0; p < P_; ++p) rec.insert(rec.end(), {dq[p], rl[p], sl[p], earliest[p]});
+                    const std::vector<double> all = allgather_host(rec);
+                    const size_t stride = all.size() / comm_.world;
+                    dq.clear(), rl.clear(), sl.clear(), earliest.clear();
+                    bool any_fail = false;
+                    for (int r = 0; r < comm_.world; ++r) {
+                        const double* x = all.data() + stride * r;
+                        any_fail = any_fail || x[1] != 0.0;
+                        for (int p = 0; p < static_cast<int>(x[0]); ++p) {
+                            dq.push_back(x[2 + 4 * p]);
+                            rl.push_back(x[3 + 4 * p]);
+                            sl.push_back(x[4 + 4 * p]);
+                            earliest.push_back(x[5 + 4 * p]);
+                        }
+                    }
+                    if (any_fail)
+                        throw Error(fail.empty() ? std::string("admm: a peer rank failed") : fail);
+                }
                 TraceRow row{static_cast<double>(frame), static_cast<double>(attempt),
                              static_cast<double>(k), 0.0, 0.0, 0.0, 1.0, 0.0};
-                std::vector<double> tois(P_);
-                for (int p = 0; p < P_; ++p) {
+                const int np = static_cast<int>(earliest.size());
+                std::vector<double> tois(np);
+                for (int p = 0; p < np; ++p) {
                     tois[p] = earliest[p] > 1.0 ? 1.0 : std::min(1.0, 0.9 * earliest[p]);
                     row.dq = std::max(row.dq, dq[p]);
                     row.r = std::max(row.r, rl[p]);
@@ -1136,15 +1265,21 @@ FrameStats Engine::frame_admm(int frame) {
                 launch_adapt(I, ianc_.get(), irho_.get(), irho0_.get(), rb_.get(), sb_.get(),
                              hs_.adapt, iz_.get(), iznext_.get(), s_);
             }
-            if (I) CUDA_CHECK(cudaMemcpyAsync(iqbefore_.get(), iq_.get(), 6 * I * sizeof(double),
-                                              cudaMemcpyDeviceToDevice, s_));
-            const NewtonResult r = newton_batch(hs_.newton_cap, tol);
-            st.newton_iterations += r.iterations;
-            st.line_search_steps += r.ls_steps;
-            st.pcg_iterations += r.pcg_iters;
-            st.max_contacts = std::max(st.max_contacts, n_contacts_);
-            st.max_candidates = std::max(st.max_candidates, n_super_);
-            dq = n_rows_ ? delta_inf(iq_.get(), iqbefore_.get()) : std::vector<double>(P_, 0.0);
+            if (!fail.empty()) continue;
+            try {
+                if (I) CUDA_CHECK(cudaMemcpyAsync(iqbefore_.get(), iq_.get(), 6 * I * sizeof(double),
+                                                  cudaMemcpyDeviceToDevice, s_));
+                const NewtonResult r = newton_batch(hs_.newton_cap, tol);
+                st.newton_iterations += r.iterations;
+                st.line_search_steps += r.ls_steps;
+                st.pcg_iterations += r.pcg_iters;
+                st.max_contacts = std::max(st.max_contacts, n_contacts_);
+                st.max_candidates = std::max(st.max_candidates, n_super_);
+                dq = n_rows_ ? delta_inf(iq_.get(), iqbefore_.get()) : std::vector<double>(P_, 0.0);
+            } catch (const Error& e) {
+                if (!distributed_) throw;
+                fail = e.what();
+            }
         }
         if (retry) {
             ++attempt;
@@ -1154,12 +1289,13 @@ FrameStats Engine::frame_admm(int frame) {
         // rho carry + commit (runtime.cpp:481-506)
         std::vector<double> rho_now = irho_.to_host(s_);
         std::fill(rho_carry_.begin(), rho_carry_.end(), std::numeric_limits<double>::quiet_NaN());
-        for (int i = 0; i < I; ++i) {
-            const int b = h_ibody_[i];
-            if (anc[i] && std::countr_zero(mask[b]) == h_ipart_[i]) rho_carry_[b] = rho_now[i];
-        }
+        // Replicas carry equal rho (k_consensus checks it), so any local
+        // replica may stand in for the lowest holder's.
+        for (int i = 0; i < I; ++i)
+            if (anc[i]) rho_carry_[h_ibody_[i]] = rho_now[i];
         launch_commit(ds_.view(), I, ibody_.get(), ipart_.get(), ianc_.get(), bmask_.get(),
                       iq_.get(), iznext_.get(), q_start_.get(), h, q_.get(), qd_.get(), s_);
+        if (distributed_) commit_gather();
         sync();
         h_cur_ = std::min(hs_.params.h, 2.0 * h_cur_); // TimestepController::on_frame_committed
         halvings_ = 0;

@@ -33,6 +33,17 @@ struct NewtonResult {
     double final_update = 0.0;
 };
 
+// Inter-rank exchange of a partition-per-GPU run (dabd_gpu_comm in
+// include/dabd_gpu.h). Device pointers, ordered on the engine's stream.
+struct Comm {
+    void* user = nullptr;
+    int (*halo)(void*, const double*, double*, size_t, const double*, double*, size_t,
+                uintptr_t) = nullptr;
+    int (*allgather)(void*, const double*, double*, size_t, uintptr_t) = nullptr;
+    int rank = 0, world = 1;
+    std::vector<int> part_offsets; // world + 1
+};
+
 class Engine {
   public:
     Engine(const HostScene& hs, int device, int num_workers, int part_begin, int part_end);
@@ -41,6 +52,7 @@ class Engine {
     Engine& operator=(const Engine&) = delete;
 
     void set_stream(cudaStream_t s);
+    void set_comm(const Comm* c);
     void set_solver(double tol, int max_iters) {
         pcg_tol_ = tol;
         pcg_max_ = max_iters;
@@ -169,9 +181,20 @@ class Engine {
     int n_contacts_ = 0;
     KeyFmt cfmt_;
 
-    // ADMM shared bodies (single-device: both replicas local)
-    std::vector<int> h_shared_inst_; // [ns][2] instance indices (ascending partition)
+    // ADMM shared bodies: [ns][2] replica handles in ascending partition
+    // order, >= 0 a local instance, < 0 the halo packet -1 - v (remote rank).
+    std::vector<int> h_shared_inst_;
     DBuf<int> shared_inst_;
+    // partition-per-GPU exchange
+    bool distributed_ = false;
+    Comm comm_;
+    std::vector<int> h_halo_inst_;    // local instances packed: lo side then hi side
+    int n_halo_lo_ = 0, n_halo_hi_ = 0;
+    DBuf<int> halo_inst_, part_rank_;
+    DBuf<double> hsend_, hrecv_, rec_, rec_all_, gath_;
+    void exchange_halo();
+    std::vector<double> allgather_host(const std::vector<double>& mine);
+    void commit_gather();
     DBuf<double> rloc_, sloc_, rb_, sb_;
     DBuf<double> ifs_; // per-instance force split (fx, fy)
     SimParams frame_params_;

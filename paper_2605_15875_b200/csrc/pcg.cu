@@ -359,7 +359,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     const int rank = static_cast<int>(cl.block_rank());
     const int p = blockIdx.x / csize;
     const int R0 = sv.part_row_off[p], R1 = sv.part_row_off[p + 1];
-    const int chunk = (R1 - R0 + csize - 1) / csize;
+    // CTAs per partition from the partition's own row count (launch csize is
+    // the batch maximum): the reduction trees, hence the bits, do not depend
+    // on which other partitions share the launch or the GPU. Surplus CTAs
+    // get no rows and push exact zeros.
+    int cs_p = 1;
+    while (cs_p < csize && cs_p * 32 < R1 - R0) cs_p *= 2;
+    const int chunk = max(1, (R1 - R0 + cs_p - 1) / cs_p);
     const int r0 = min(R1, R0 + rank * chunk), r1 = min(R1, r0 + chunk);
     const int nr = r1 - r0;
     const PartState& st = sv.ps[p];
@@ -588,7 +594,8 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
     const int cmax = pcg_cluster_size();
     int csize = 1;
     while (csize < cmax && csize * 32 < max_rows_per_part) csize *= 2; // >= ~32 rows per CTA
-    const int cmax_rows = (max_rows_per_part + csize - 1) / csize;
+    // largest per-partition chunk under the per-partition rule of k_pcg_cluster
+    const int cmax_rows = std::max(std::min(max_rows_per_part, 32), (max_rows_per_part + csize - 1) / csize);
     PcgArgs a{pbuf, nullptr, nullptr, tol, max_iters};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csize * sv.n_parts);

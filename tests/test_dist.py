@@ -1,0 +1,161 @@
+"""Partition-per-GPU exchange.
+
+CPU: the torch.distributed hooks behind dabd_gpu_comm, world sizes 2 and 3
+over gloo. GPU: two ranks sharing cuda:0 (gloo staging) run a partitioned
+consensus-ADMM scene and must reproduce the single-process run of the same
+partitions bit for bit (the exchange carries no arithmetic).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2605_15875_b200.dist import TorchComm, partition_offsets
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _spawn(fn, world, *args):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=fn, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        rank, res = q.get()
+        out[rank] = res
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return out
+
+
+def test_partition_offsets():
+    assert partition_offsets(8, 1) == [0, 8]
+    assert partition_offsets(8, 8) == list(range(9))
+    assert partition_offsets(5, 2) == [0, 3, 5]
+    assert partition_offsets(2, 2) == [0, 1, 2]
+    with pytest.raises(ValueError):
+        partition_offsets(2, 3)
+
+
+def _allgather_worker(rank, world, port, q):
+    try:
+        _init(rank, world, port)
+        comm = TorchComm(num_workers=2 * world)
+        assert (comm.part_begin, comm.part_end) == (2 * rank, 2 * rank + 2)
+        rec = torch.arange(4, dtype=torch.float64) + 10.0 * rank
+        allr = torch.zeros(4 * world, dtype=torch.float64)
+        comm.allgather(rec, allr)
+        q.put((rank, allr.numpy()))
+        dist.destroy_process_group()
+    except BaseException as e:  # report instead of hanging the parent
+        q.put((rank, e))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_torchcomm_allgather_gloo(world):
+    out = _spawn(_allgather_worker, world)
+    exp = np.concatenate([np.arange(4) + 10.0 * k for k in range(world)])
+    for r in range(world):
+        assert not isinstance(out[r], BaseException), out[r]
+        assert np.array_equal(out[r], exp)
+
+
+def _pair_worker(rank, world, port, q):
+    try:
+        _init(rank, world, port)
+        comm = TorchComm(num_workers=world)
+        # the count between ranks r and r+1 is 2 + r on both sides
+        n_lo = 2 + (rank - 1) if rank > 0 else 0
+        n_hi = 2 + rank if rank < world - 1 else 0
+        send_lo = torch.tensor([1000.0 * rank + j for j in range(n_lo)], dtype=torch.float64)
+        send_hi = torch.tensor([1000.0 * rank + 500 + j for j in range(n_hi)], dtype=torch.float64)
+        recv_lo = torch.full((n_lo,), -1.0, dtype=torch.float64)
+        recv_hi = torch.full((n_hi,), -1.0, dtype=torch.float64)
+        comm.halo(send_lo, recv_lo, send_hi, recv_hi)
+        q.put((rank, (recv_lo.numpy(), recv_hi.numpy())))
+        dist.destroy_process_group()
+    except BaseException as e:
+        q.put((rank, e))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_torchcomm_halo_gloo(world):
+    out = _spawn(_pair_worker, world)
+    for r in range(world):
+        assert not isinstance(out[r], BaseException), out[r]
+        lo, hi = out[r]
+        if r > 0:  # sent by rank r-1 to its hi side
+            assert np.array_equal(lo, 1000.0 * (r - 1) + 500 + np.arange(2 + r - 1))
+        if r < world - 1:  # sent by rank r+1 to its lo side
+            assert np.array_equal(hi, 1000.0 * (r + 1) + np.arange(2 + r))
+
+
+# ---------------------------------------------------------------------------
+# GPU: two or three ranks sharing cuda:0 (gloo staging through the host)
+# ---------------------------------------------------------------------------
+TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000)
+
+
+def _gpu_worker(rank, world, port, q, name, workers, frames):
+    try:
+        _init(rank, world, port)
+        from paper_2605_15875_b200.dist import run_partitioned
+        from paper_2605_15875_b200.scene import make_scenario
+
+        torch.cuda.set_device(0)
+        t = run_partitioned(make_scenario(name), workers, frames, device=0, **TIGHT)
+        q.put((rank, (t.q, t.q_dot, t.trace, t.rho,
+                      [s["admm_iterations"] for s in t.stats], list(t.h))))
+        dist.destroy_process_group()
+    except BaseException as e:
+        q.put((rank, RuntimeError(repr(e))))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,workers,world,frames", [
+    ("drop-grid-2", 2, 2, 12),
+    ("cubes-64", 2, 2, 8),
+    ("drop-grid-4", 4, 2, 8),
+    ("drop-grid-4", 4, 3, 6),
+    ("blocked-merge", 2, 2, 3),
+])
+def test_partitioned_matches_single_gpu(name, workers, world, frames):
+    from paper_2605_15875_b200 import api
+    from paper_2605_15875_b200.scene import make_scenario
+
+    ref = api.run_distributed(make_scenario(name), workers, frames, **TIGHT)
+    out = _spawn(_gpu_worker, world, name, workers, frames)
+    offs = partition_offsets(workers, world)
+    rho = np.full_like(ref.rho, np.nan)
+    for r in range(world):
+        assert not isinstance(out[r], BaseException), out[r]
+        qs, qds, trace, rrho, admm, hs = out[r]
+        assert admm == [s["admm_iterations"] for s in ref.stats]
+        assert hs == list(ref.h)
+        assert np.array_equal(trace, ref.trace), (r, np.abs(trace - ref.trace).max())
+        assert np.array_equal(qs, ref.q), (r, np.abs(qs - ref.q).max())
+        assert np.array_equal(qds, ref.q_dot)
+        have = ~np.isnan(rrho)
+        assert np.array_equal(rrho[have], ref.rho[have])
+        rho[have] = rrho[have]
+    # every body shared at the end is carried by some rank
+    assert np.array_equal(np.isnan(rho), np.isnan(ref.rho)), offs
