@@ -12,8 +12,16 @@ the public C ABI with the state copied host->device and back every step.
 Untimed set-up drops the lattice for --settle frames so every timed step is
 a contact-rich pile frame. The L2 is flushed (256 MiB write) between timed
 steps, outside the per-step CUDA events. Rank 0 prints ONE JSON line.
-Under torchrun (N > 1) every rank steps its own replica of the scene
-(replicas only, scaling "weak") until the NVLink partition runtime lands.
+Under torchrun (N > 1) the run is partition-per-GPU consensus ADMM with weak
+scaling: the scene is N pile-1k slabs side by side (N x 1,000 bodies, N
+partitions separated by interface planes), rank r owns partition r, split
+bodies are exchanged with the neighbouring ranks over NCCL (dist.TorchComm).
+`value` counts pile-1k-equivalent steps: N x committed frames/s, so N=1 and
+N>1 share a unit (one partition of 1,000 bodies stepped once). At N=1 the
+single partition is the run_reference path (1-worker ADMM is bitwise the
+same algorithm, tests/test_gpu_admm.py). DABD_BENCH_SHARE_GPU=1 maps every
+rank to cuda:0 over gloo (a functional check of the N>1 path on one GPU; its
+timings are not scaling numbers).
 """
 
 from __future__ import annotations
@@ -193,19 +201,39 @@ def main() -> None:
     import torch
 
     ws, rank, local = _dist()
+    share = os.environ.get("DABD_BENCH_SHARE_GPU", "0") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2605_15875_b200 import _lib as L
     from paper_2605_15875_b200 import api
-    from paper_2605_15875_b200.scene import make_scenario
+    from paper_2605_15875_b200.scene import make_scenario, pile_slabs
 
     lib = L.load()
-    sd = make_scenario(args.config)
+    workers = 0 if ws == 1 else ws
+    sd = make_scenario(args.config) if ws == 1 else pile_slabs(ws)
     scene = api.Scene(sd)
-    ctx = api.Context(scene, device=local, num_workers=0)
+    comm = None
+    if ws > 1:
+        from paper_2605_15875_b200.dist import TorchComm
+
+        comm = TorchComm(workers, device=local)
+    def make_ctx():
+        c = api.Context(scene, device=local, num_workers=workers,
+                        part_begin=comm.part_begin if comm else 0,
+                        part_end=comm.part_end if comm else None)
+        if comm:
+            c.set_comm(comm)
+        return c
+
+    ctx = make_ctx()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
@@ -249,7 +277,7 @@ def main() -> None:
     pcg_ns, pcg_launches, pcg_bytes, pcg_iters = perf(True)
     total_ms = sum(step_ms)
     if ws > 1:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([total_ms], device="cpu" if share else "cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     value = ws * args.steps / (total_ms / 1e3)
@@ -258,7 +286,7 @@ def main() -> None:
     # e2e through the public API with pinned host buffers every step
     q_h = torch.from_numpy(q_warm.copy()).pin_memory()
     qd_h = torch.from_numpy(qd_warm.copy()).pin_memory()
-    ctx2 = api.Context(scene, device=local, num_workers=0)
+    ctx2 = make_ctx()
     ctx2.set_stream(stream.cuda_stream)
     qp = C.cast(q_h.data_ptr(), C.POINTER(C.c_double))
     qdp = C.cast(qd_h.data_ptr(), C.POINTER(C.c_double))
@@ -268,6 +296,8 @@ def main() -> None:
     q_h.copy_(torch.from_numpy(q_warm))
     qd_h.copy_(torch.from_numpy(qd_warm))
     torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -277,6 +307,11 @@ def main() -> None:
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64,
+                         device="cpu" if share else "cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
     nbytes = 2 * 6 * 8 * scene.n
 
     hbm, peak_kind = _peaks()
@@ -298,11 +333,15 @@ def main() -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.config, "bodies": scene.n, "partitions": 1,
-                   "semantics": "run_reference (sim.cpp:186-249)",
+        "config": {"workload": args.config if ws == 1 else sd.name, "bodies": scene.n,
+                   "partitions": max(workers, 1),
+                   "semantics": "run_reference (sim.cpp:186-249)" if ws == 1 else
+                                "consensus ADMM, one partition per GPU (runtime.cpp:110-694)",
+                   "unit_of_work": "one 1,000-body pile partition stepped one frame",
                    "start": f"lattice dropped for {args.settle} untimed frames (contact-rich pile)",
                    "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": f"replica x{ws}" if ws > 1 else "single"},
+                   "parallelism": "single" if ws == 1 else
+                                  f"partition-per-GPU x{ws} ({'gloo, shared GPU' if share else 'NCCL'})"},
         "admm_iters_per_sec": admm * ws / (total_ms / 1e3),
         "newton_iters_per_step": sum(s["newton_iterations"] for s in stats) / len(stats),
         "pcg_iters_per_step": sum(s["pcg_iterations"] for s in stats) / len(stats),
@@ -313,7 +352,7 @@ def main() -> None:
         "roofline": roof,
         "clocks": clk.summary(),
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(sd, q_warm, qd_warm)
     if rank == 0:
         print(json.dumps(line), flush=True)

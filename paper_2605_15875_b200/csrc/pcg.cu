@@ -275,24 +275,32 @@ __global__ void __launch_bounds__(kT) k_pcg(SolverView sv, PcgArgs a) {
 // ---------------------------------------------------------------------------
 // Cluster-resident PCG: one thread-block cluster (up to 16 SMs) per
 // partition. Every CTA stages its chunk of the partition's BSR rows (diagonal
-// + coupling blocks, column ids, block-Jacobi inverses) and all PCG vectors
-// in shared memory; neighbours' z / p come from the owning CTA's shared
-// memory through DSMEM (cluster.map_shared_rank), and the dot products meet
-// through DSMEM + cluster barriers. Nothing but the final dq leaves the SMs,
-// so an iteration costs a few microseconds for the ~1k-body partitions of
-// the N=1 workload. Rows that do not fit the shared-memory budget read their
+// + eps I and coupling blocks, the DSMEM address of every block's column,
+// block-Jacobi inverses) and all PCG vectors in shared memory; neighbours'
+// z / p come from the owning CTA's shared memory through DSMEM and the dot
+// products meet through DSMEM + cluster barriers. Nothing but the final dq
+// leaves the SMs. Rows that do not fit the shared-memory budget read their
 // blocks from global memory (L2).
+//
+// Lane layout: a warp owns 5 rows, lane = 6 * slot + comp computes component
+// `comp` of row `slot` (lanes 30, 31 idle), so a 6x6 block costs one row of
+// 6 FMAs per lane and no cross-lane reduction. Per iteration:
+//   A: Ap_i = sum_j M_ij (z_j + beta p_j)   (p_new recomputed by the reader),
+//      p_new = z + beta p_old, partial p.Ap       -> push, cluster barrier
+//   B: x += alpha p, r -= alpha Ap, z = Dinv r, partials r.z, r.r
+//                                                -> push, cluster barrier
 // ---------------------------------------------------------------------------
-constexpr int kCT = 1024;
+constexpr int kCT = 512;
 constexpr int kCW = kCT / 32;
+constexpr int kRowsPerWarp = 5;
 constexpr int kCSmemBytes = 200 * 1024;
 
-// Every CTA pushes its partials into slot [rank][k] of every peer's xch
-// table (fire-and-forget DSMEM stores), so after one cluster barrier each
-// CTA folds the table locally in rank order -- same bits everywhere.
+// Every CTA pushes its partials into slot [rank] of every peer's table
+// (fire-and-forget DSMEM stores), so after one cluster barrier each CTA folds
+// the table locally in rank order -- same bits everywhere.
 struct ClusterScalars {
-    double xch[16][3]; // [source rank][p.Ap, r.z, r.r]
-    double val[3];     // this CTA's partials staged for the push
+    double pap[16];
+    double2 rzr[16]; // (r.z, r.r)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -301,50 +309,25 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Threads 0..csize-1 each store slots [k0, k1) of this CTA's staged values
-// into one peer. Call after `val` is written and a __syncthreads.
-__device__ __forceinline__ void cluster_push(cg::cluster_group& cl, ClusterScalars* sc, int rank,
-                                             int csize, int k0, int k1) {
-    if (static_cast<int>(threadIdx.x) < csize) {
-        ClusterScalars* peer = cl.map_shared_rank(sc, static_cast<int>(threadIdx.x));
-        for (int k = k0; k < k1; ++k) peer->xch[rank][k] = sc->val[k];
-    }
-}
-
-// Every warp folds the 16-entry table with the same xor butterfly, so all
-// threads of all CTAs get identical bits without another barrier.
-__device__ __forceinline__ double cluster_fold(const ClusterScalars* sc, int csize, int k) {
-    const int lane = threadIdx.x & 31;
-    double v = lane < csize ? sc->xch[lane][k] : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    return v;
-}
-
-// Two block-wide sums at once; result valid in warp 0 (fixed shuffle trees).
-__device__ __forceinline__ double2 block_sum2(double a, double b, double2* red2) {
+// CTA-wide sums of (a, b); every thread gets the same bits.
+__device__ __forceinline__ double2 cta_sum2(double a, double b, double2* red) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, off);
-        b += __shfl_xor_sync(0xffffffffu, b, off);
-    }
-    if (lane == 0) red2[warp] = make_double2(a, b);
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) red[warp] = make_double2(a, b);
     __syncthreads();
-    double2 r = make_double2(0.0, 0.0);
-    if (warp == 0) {
-        const double2 v = lane < (static_cast<int>(blockDim.x) >> 5) ? red2[lane] : make_double2(0.0, 0.0);
-        double x = v.x, y = v.y;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            x += __shfl_xor_sync(0xffffffffu, x, off);
-            y += __shfl_xor_sync(0xffffffffu, y, off);
-        }
-        r = make_double2(x, y);
-    }
-    return r;
+    const double2 v = lane < kCW ? red[lane] : make_double2(0.0, 0.0);
+    return make_double2(warp_sum(v.x), warp_sum(v.y));
 }
 
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ double fold16(double v_lane) {
+    return warp_sum(v_lane);
+}
 
 __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, int csize, int cmax_rows) {
     cg::cluster_group cl = cg::this_cluster();
@@ -352,10 +335,9 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ ClusterScalars sc;
-    __shared__ double2 red2[kCW];
-    __shared__ double acc_sh[kCW][32];
-    __shared__ int nblk_total;
+    __shared__ double2 red[kCW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = lane / 6, comp = lane - 6 * slot;
     const int rank = static_cast<int>(cl.block_rank());
     const int p = blockIdx.x / csize;
     const int R0 = sv.part_row_off[p], R1 = sv.part_row_off[p + 1];
@@ -380,155 +362,170 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     double* vp1 = vp0 + 6 * cmax_rows;
     double* dinv = vp1 + 6 * cmax_rows;
     int* bstart = reinterpret_cast<int*>(dinv + 36 * cmax_rows); // [cmax_rows + 1]
-    int* bcol = bstart + cmax_rows + 1;                             // [cap_blocks]
-    const size_t used = 72ull * cmax_rows * 8 + 4ull * (cmax_rows + 1);
-    const int cap_blocks = static_cast<int>((kCSmemBytes - used) / (36 * 8 + 4));
-    double* blk = reinterpret_cast<double*>(
-        (reinterpret_cast<uintptr_t>(bcol + cap_blocks) + 15) & ~uintptr_t(15));
-    const int comp = lane % 6, grp = lane / 6;
+    const size_t used = (72ull * cmax_rows) * 8 + 4ull * (cmax_rows + 2);
+    const int cap_blocks = static_cast<int>((kCSmemBytes - used - 16) / (36 * 8 + 8)) & ~1; // blk 16B-aligned
+    const double** bptr = reinterpret_cast<const double**>(
+        (reinterpret_cast<uintptr_t>(bstart + cmax_rows + 1) + 15) & ~uintptr_t(15));
+    double* blk = reinterpret_cast<double*>(bptr + cap_blocks);
+    const ptrdiff_t off_p0 = vp0 - vz, off_p1 = vp1 - vz;
 
-    // ---- stage rows: block offsets (diag first), blocks, columns, Dinv
+    // ---- stage rows: block offsets (diag first), blocks, column addresses, Dinv
     for (int lr = threadIdx.x; lr < nr; lr += kCT) bstart[lr + 1] = sv.ell_cnt[r0 + lr] + 1;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        bstart[0] = 0;
-        for (int lr = 0; lr < nr; ++lr) bstart[lr + 1] += bstart[lr];
-        nblk_total = bstart[nr];
+    if (warp == 0) { // warp-wide inclusive scan in chunks of 32 rows
+        int carry = 0;
+        for (int b = 0; b < nr; b += 32) {
+            int v = b + lane < nr ? bstart[b + lane + 1] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += u;
+            }
+            if (b + lane < nr) bstart[b + lane + 1] = v + carry;
+            carry += __shfl_sync(0xffffffffu, v, 31);
+        }
+        if (lane == 0) bstart[0] = 0;
     }
     __syncthreads();
     for (int lr = warp; lr < nr; lr += kCW) {
         const int r = r0 + lr;
         const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
         for (int t = 0; t < nb; ++t) {
-            const int slot = b0 + t;
-            if (slot >= cap_blocks) break; // spills to global reads below
+            const int s = b0 + t;
+            if (s >= cap_blocks) break; // spills to global reads below
             const double* src = t == 0 ? sv.rdiag + 36 * r
                                        : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36;
-            for (int k = lane; k < 36; k += 32) blk[36 * slot + k] = src[k];
-            if (lane == 0) bcol[slot] = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+            for (int k = lane; k < 36; k += 32)
+                blk[36 * s + k] = src[k] + ((t == 0 && k % 7 == 0) ? eps : 0.0);
+            if (lane == 0) {
+                const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+                const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
+                bptr[s] = cl.map_shared_rank(vz, crank) + 6 * cl_row;
+            }
         }
         for (int k = lane; k < 36; k += 32) dinv[36 * lr + k] = sv.rdinv[36 * r + k];
     }
     __syncthreads();
 
+    const int row_step = kCW * kRowsPerWarp;
     // ---- init: r = -grad, x = 0, z = Dinv r, p_old = 0
     double s_rz = 0.0, s_rr = 0.0;
-    for (int lr = warp; lr < nr; lr += kCW) {
-        const int r = r0 + lr;
-        double g = 0.0;
-        if (lane < 6) g = act ? -sv.rgrad[6 * r + lane] : 0.0;
+    for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
+        const int lr = base + slot;
+        const bool on = lane < 30 && lr < nr;
+        const double g = on && act ? -sv.rgrad[6 * (r0 + lr) + comp] : 0.0;
         double z = 0.0;
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-            const double gc = __shfl_sync(0xffffffffu, g, c);
-            if (lane < 6) z += dinv[36 * lr + 6 * lane + c] * gc;
+            const double gc = __shfl_sync(0xffffffffu, g, (6 * slot + c) & 31);
+            if (on) z += dinv[36 * lr + 6 * comp + c] * gc;
         }
-        if (lane < 6) {
-            vr[6 * lr + lane] = g;
-            vz[6 * lr + lane] = z;
-            vx[6 * lr + lane] = 0.0;
-            vp0[6 * lr + lane] = 0.0;
+        if (on) {
+            const int i = 6 * lr + comp;
+            vr[i] = g;
+            vz[i] = z;
+            vx[i] = 0.0;
+            vp0[i] = 0.0;
             s_rz += g * z;
             s_rr += g * g;
         }
     }
-    const double2 bb = block_sum2(s_rz, s_rr, red2);
-    if (threadIdx.x == 0) {
-        sc.val[1] = bb.x;
-        sc.val[2] = bb.y;
+    double2 bb = cta_sum2(s_rz, s_rr, red);
+    if (static_cast<int>(threadIdx.x) < csize)
+        cl.map_shared_rank(&sc, static_cast<int>(threadIdx.x))->rzr[rank] = bb;
+    cluster_barrier();
+    {
+        const double2 v = lane < csize ? sc.rzr[lane] : make_double2(0.0, 0.0);
+        bb = make_double2(fold16(v.x), fold16(v.y));
     }
-    __syncthreads();
-    cluster_push(cl, &sc, rank, csize, 1, 3);
-    cl.sync();
-    double rz = cluster_fold(&sc, csize, 1);
-    const double bnorm2 = cluster_fold(&sc, csize, 2);
+    double rz = bb.x;
+    const double bnorm2 = bb.y;
     bool done = !act || bnorm2 == 0.0;
     double beta = 0.0;
     int it = 0, cur = 0;
     while (!done) {
         double* pold = cur ? vp1 : vp0;
         double* pnew = cur ? vp0 : vp1;
-        // ---- phase A: p_new = z + beta p_old ; Ap ; p.Ap
+        const ptrdiff_t poff = cur ? off_p1 : off_p0;
+        // ---- phase A: Ap over (z + beta p_old) of the columns; p_new; p.Ap
         double pap = 0.0;
-        for (int lr = warp; lr < nr; lr += kCW) {
-            const int r = r0 + lr;
-            const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
-            double acc = 0.0;
-            if (grp < 5) {
-                for (int t = grp; t < nb; t += 5) {
-                    const int slot = b0 + t;
-                    const bool in_smem = slot < cap_blocks;
-                    const int col = in_smem ? bcol[slot]
-                                            : (t == 0 ? r : sv.ell_col[r * kEll + t - 1]);
-                    const double* M = in_smem ? blk + 36 * slot
-                                              : (t == 0 ? sv.rdiag + 36 * r
-                                                        : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36);
-                    const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
-                    const double* zc = cl.map_shared_rank(vz, crank) + 6 * cl_row;
-                    const double* pc = cl.map_shared_rank(pold, crank) + 6 * cl_row;
-                    double y = 0.0;
-#pragma unroll
-                    for (int c = 0; c < 6; ++c) {
-                        const double v = zc[c] + beta * pc[c];
-                        y += M[6 * comp + c] * v;
-                        if (t == 0 && c == comp) y += eps * v;
-                    }
-                    acc += y;
-                }
-            }
-            acc_sh[warp][lane] = acc;
-            __syncwarp();
-            if (lane < 6) {
+        for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
+            const int lr = base + slot;
+            if (lane < 30 && lr < nr) {
+                const int b0 = bstart[lr], b1 = bstart[lr + 1];
                 double y = 0.0;
+                for (int s = b0; s < b1; ++s) {
+                    const double* M;
+                    const double* zc;
+                    double e = 0.0;
+                    if (s < cap_blocks) {
+                        M = blk + 36 * s + 6 * comp;
+                        zc = bptr[s];
+                    } else { // spilled block: global memory, eps added here
+                        const int r = r0 + lr, t = s - b0;
+                        const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+                        M = (t == 0 ? sv.rdiag + 36 * r
+                                    : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36) + 6 * comp;
+                        const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
+                        zc = cl.map_shared_rank(vz, crank) + 6 * cl_row;
+                        e = t == 0 ? eps : 0.0;
+                    }
+                    const double* pc = zc + poff;
+                    const double2* M2 = reinterpret_cast<const double2*>(M);
+                    const double2* z2 = reinterpret_cast<const double2*>(zc);
+                    const double2* p2 = reinterpret_cast<const double2*>(pc);
 #pragma unroll
-                for (int g = 0; g < 5; ++g) y += acc_sh[warp][g * 6 + lane];
-                const double pr = vz[6 * lr + lane] + beta * pold[6 * lr + lane];
-                pnew[6 * lr + lane] = pr;
-                vap[6 * lr + lane] = y;
+                    for (int h = 0; h < 3; ++h) {
+                        const double2 m = M2[h], zz = z2[h], pp = p2[h];
+                        y += m.x * (zz.x + beta * pp.x);
+                        y += m.y * (zz.y + beta * pp.y);
+                    }
+                    if (e != 0.0) y += e * (zc[comp] + beta * pc[comp]);
+                }
+                const int i = 6 * lr + comp;
+                const double pr = vz[i] + beta * pold[i];
+                pnew[i] = pr;
+                vap[i] = y;
                 pap += pr * y;
             }
-            __syncwarp();
         }
-        const double2 bp = block_sum2(pap, 0.0, red2);
-        if (threadIdx.x == 0) sc.val[0] = bp.x;
-        __syncthreads();
-        cluster_push(cl, &sc, rank, csize, 0, 1);
-        cl.sync();
-        const double pap_all = cluster_fold(&sc, csize, 0);
+        const double2 bp = cta_sum2(pap, 0.0, red);
+        if (static_cast<int>(threadIdx.x) < csize)
+            cl.map_shared_rank(&sc, static_cast<int>(threadIdx.x))->pap[rank] = bp.x;
+        cluster_barrier();
+        const double pap_all = fold16(lane < csize ? sc.pap[lane] : 0.0);
         if (!(pap_all > 0.0)) break; // exact solution or breakdown (uniform)
         const double alpha = rz / pap_all;
         // ---- phase B: x += alpha p ; r -= alpha Ap ; z = Dinv r
         double l_rz = 0.0, l_rr = 0.0;
-        for (int lr = warp; lr < nr; lr += kCW) {
+        for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
+            const int lr = base + slot;
+            const bool on = lane < 30 && lr < nr;
+            const int i = 6 * lr + comp;
             double rv = 0.0;
-            if (lane < 6) {
-                vx[6 * lr + lane] += alpha * pnew[6 * lr + lane];
-                rv = vr[6 * lr + lane] - alpha * vap[6 * lr + lane];
-                vr[6 * lr + lane] = rv;
+            if (on) {
+                vx[i] += alpha * pnew[i];
+                rv = vr[i] - alpha * vap[i];
+                vr[i] = rv;
             }
             double z = 0.0;
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
-                const double rc = __shfl_sync(0xffffffffu, rv, c);
-                if (lane < 6) z += dinv[36 * lr + 6 * lane + c] * rc;
+                const double rc = __shfl_sync(0xffffffffu, rv, (6 * slot + c) & 31);
+                if (on) z += dinv[36 * lr + 6 * comp + c] * rc;
             }
-            if (lane < 6) {
+            if (on) {
+                vz[i] = z;
                 l_rz += rv * z;
                 l_rr += rv * rv;
             }
-            __syncwarp();
-            if (lane < 6) vz[6 * lr + lane] = z;
         }
-        const double2 cc = block_sum2(l_rz, l_rr, red2);
-        if (threadIdx.x == 0) {
-            sc.val[1] = cc.x;
-            sc.val[2] = cc.y;
-        }
-        __syncthreads();
-        cluster_push(cl, &sc, rank, csize, 1, 3);
-        cl.sync();
-        const double rz_new = cluster_fold(&sc, csize, 1);
-        const double rr = cluster_fold(&sc, csize, 2);
+        const double2 cc = cta_sum2(l_rz, l_rr, red);
+        if (static_cast<int>(threadIdx.x) < csize)
+            cl.map_shared_rank(&sc, static_cast<int>(threadIdx.x))->rzr[rank] = cc;
+        cluster_barrier();
+        const double2 v = lane < csize ? sc.rzr[lane] : make_double2(0.0, 0.0);
+        const double rz_new = fold16(v.x), rr = fold16(v.y);
         beta = rz != 0.0 ? rz_new / rz : 0.0;
         rz = rz_new;
         ++it;
@@ -538,13 +535,15 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         // p_new writes before the peers' next phase A, the one in phase A
         // orders their reads of our z before our next phase-B writes.
     }
-    for (int lr = warp; lr < nr; lr += kCW)
-        if (lane < 6) sv.x[6 * (r0 + lr) + lane] = vx[6 * lr + lane];
+    for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
+        const int lr = base + slot;
+        if (lane < 30 && lr < nr) sv.x[6 * (r0 + lr) + comp] = vx[6 * lr + comp];
+    }
     if (rank == 0 && threadIdx.x == 0) {
         sv.ps[p].pcg_iters = it;
         sv.ps[p].pcg_done = 1;
     }
-    cl.sync(); // no CTA leaves while a peer may still read its shared memory
+    cluster_barrier(); // no CTA leaves while a peer may still read its shared memory
     if (sv.perf && threadIdx.x == 0) {
         if (rank == 0) { // algorithmic bytes of this partition's solve
             int nblk = 0;

@@ -397,6 +397,13 @@ def pile_1k(seed: int = 11) -> SceneData:
                         spacing=0.13, jitter=0.005, seed=seed, l=6.0)
 
 
+def pile_slabs(n: int, seed: int = 11) -> SceneData:
+    """Weak-scaling workload: n pile-1k slabs side by side (n x 1,000 boxes),
+    one interface plane between neighbouring slabs."""
+    return lattice_pile(f"pile-1k-x{n}", rows=25, cols_per_slab=40, slabs=n, half=0.05,
+                        spacing=0.13, jitter=0.005, seed=seed, l=6.0)
+
+
 def pour_10k(seed: int = 11) -> SceneData:
     """C3: 10,000 boxes over 8 slabs (50 rows x 25 columns each)."""
     return lattice_pile("pour-10k", rows=50, cols_per_slab=25, slabs=8, half=0.03,
@@ -446,6 +453,8 @@ def make_scenario(name: str, seed: Optional[int] = None) -> SceneData:
         return s
     if name in _BUILTINS:
         return _BUILTINS[name](seed)
+    if name.startswith("pile-1k-x"):
+        return pile_slabs(int(name[len("pile-1k-x"):]), 11 if seed is None else seed)
     prefix = "density-sweep-"
     if name.startswith(prefix):
         density = float(name[len(prefix):])
