@@ -295,12 +295,13 @@ constexpr int kCW = kCT / 32;
 constexpr int kRowsPerWarp = 5;
 constexpr int kCSmemBytes = 200 * 1024;
 
-// Every CTA pushes its partials into slot [rank] of every peer's table
-// (fire-and-forget DSMEM stores), so after one cluster barrier each CTA folds
-// the table locally in rank order -- same bits everywhere.
+// Every warp pushes its partials into slot [rank][warp] of every peer's
+// table (fire-and-forget DSMEM stores), so after one cluster barrier each
+// thread folds the whole table locally in a fixed order -- same bits in every
+// thread of every CTA, and no CTA-level barrier on the reduction path.
 struct ClusterScalars {
-    double pap[16];
-    double2 rzr[16]; // (r.z, r.r)
+    double pap[16 * kCW];
+    double2 rzr[16 * kCW]; // (r.z, r.r)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -309,24 +310,48 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// CTA-wide sums of (a, b); every thread gets the same bits.
-__device__ __forceinline__ double2 cta_sum2(double a, double b, double2* red) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    a = warp_sum(a);
-    b = warp_sum(b);
-    if (lane == 0) red[warp] = make_double2(a, b);
-    __syncthreads();
-    const double2 v = lane < kCW ? red[lane] : make_double2(0.0, 0.0);
-    return make_double2(warp_sum(v.x), warp_sum(v.y));
-}
-
 __device__ __forceinline__ void cluster_barrier() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-__device__ __forceinline__ double fold16(double v_lane) {
-    return warp_sum(v_lane);
+// Fold of the first n entries of a [rank][warp] table (n = csize * kCW).
+__device__ __forceinline__ double fold_table(const double* t, int n) {
+    const int lane = threadIdx.x & 31;
+    double v = 0.0;
+    for (int i = lane; i < n; i += 32) v += t[i];
+    return warp_sum(v);
+}
+
+__device__ __forceinline__ double2 fold_table2(const double2* t, int n) {
+    const int lane = threadIdx.x & 31;
+    double x = 0.0, y = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        x += t[i].x;
+        y += t[i].y;
+    }
+    return make_double2(warp_sum(x), warp_sum(y));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// One 6x6 block-row product term: y += M_row . (z + beta p), M/z/p 16B aligned.
+__device__ __forceinline__ void blk_row(const double* M, const double* zc, const double* pc,
+                                        double beta, double& y) {
+    const double2* M2 = reinterpret_cast<const double2*>(M);
+    const double2* z2 = reinterpret_cast<const double2*>(zc);
+    const double2* p2 = reinterpret_cast<const double2*>(pc);
+    const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2];
+    const double2 z0 = z2[0], z1 = z2[1], z2v = z2[2];
+    const double2 q0 = p2[0], q1 = p2[1], q2 = p2[2];
+    y += m0.x * (z0.x + beta * q0.x);
+    y += m0.y * (z0.y + beta * q0.y);
+    y += m1.x * (z1.x + beta * q1.x);
+    y += m1.y * (z1.y + beta * q1.y);
+    y += m2.x * (z2v.x + beta * q2.x);
+    y += m2.y * (z2v.y + beta * q2.y);
 }
 
 __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, int csize, int cmax_rows) {
@@ -335,7 +360,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ ClusterScalars sc;
-    __shared__ double2 red[kCW];
+    __shared__ __align__(8) unsigned long long mbar;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = lane / 6, comp = lane - 6 * slot;
     const int rank = static_cast<int>(cl.block_rank());
@@ -353,6 +378,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     const PartState& st = sv.ps[p];
     const bool act = st.active != 0 && R1 > R0;
     const double eps = st.eps;
+    const int ntab = csize * kCW;
     // shared-memory carve-up (cmax_rows = chunk upper bound used at launch)
     double* vx = reinterpret_cast<double*>(smem);
     double* vr = vx + 6 * cmax_rows;
@@ -369,7 +395,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     double* blk = reinterpret_cast<double*>(bptr + cap_blocks);
     const ptrdiff_t off_p0 = vp0 - vz, off_p1 = vp1 - vz;
 
-    // ---- stage rows: block offsets (diag first), blocks, column addresses, Dinv
+    // ---- stage rows with TMA bulk copies: per row the diagonal block and the
+    // contiguous run of coupling blocks, plus the chunk's Dinv in one copy.
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
     for (int lr = threadIdx.x; lr < nr; lr += kCT) bstart[lr + 1] = sv.ell_cnt[r0 + lr] + 1;
     __syncthreads();
     if (warp == 0) { // warp-wide inclusive scan in chunks of 32 rows
@@ -385,25 +417,64 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             carry += __shfl_sync(0xffffffffu, v, 31);
         }
         if (lane == 0) bstart[0] = 0;
+        __syncwarp();
+        // bytes this CTA will receive, then the copies (lanes over rows)
+        unsigned bytes = 0;
+        for (int lr = lane; lr < nr; lr += 32) {
+            const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
+            const int ncp = min(nb, cap_blocks - b0);
+            if (ncp > 0) bytes += 288u * ncp;
+        }
+        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+        if (nr > 0) bytes += 288u * nr; // Dinv
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)),
+                         "r"(bytes)
+                         : "memory");
+        __syncwarp();
+        const unsigned bar = smem_u32(&mbar);
+        for (int lr = lane; lr < nr; lr += 32) {
+            const int r = r0 + lr;
+            const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
+            const int ncp = min(nb, cap_blocks - b0);
+            if (ncp <= 0) continue;
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(smem_u32(blk + 36 * b0)), "l"(sv.rdiag + 36 * r), "r"(288u), "r"(bar)
+                         : "memory");
+            if (ncp > 1)
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(smem_u32(blk + 36 * (b0 + 1))),
+                             "l"(sv.ell_blk + static_cast<size_t>(r) * kEll * 36),
+                             "r"(288u * (ncp - 1)), "r"(bar)
+                             : "memory");
+        }
+        if (lane == 0 && nr > 0)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(smem_u32(dinv)), "l"(sv.rdinv + 36 * r0), "r"(288u * nr), "r"(bar)
+                         : "memory");
     }
     __syncthreads();
+    // DSMEM address of every staged block's column (lanes over a row's blocks)
     for (int lr = warp; lr < nr; lr += kCW) {
         const int r = r0 + lr;
         const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
-        for (int t = 0; t < nb; ++t) {
-            const int s = b0 + t;
-            if (s >= cap_blocks) break; // spills to global reads below
-            const double* src = t == 0 ? sv.rdiag + 36 * r
-                                       : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36;
-            for (int k = lane; k < 36; k += 32)
-                blk[36 * s + k] = src[k] + ((t == 0 && k % 7 == 0) ? eps : 0.0);
-            if (lane == 0) {
-                const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
-                const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
-                bptr[s] = cl.map_shared_rank(vz, crank) + 6 * cl_row;
-            }
+        for (int t = lane; t < nb && b0 + t < cap_blocks; t += 32) {
+            const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+            const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
+            bptr[b0 + t] = cl.map_shared_rank(vz, crank) + 6 * cl_row;
         }
-        for (int k = lane; k < 36; k += 32) dinv[36 * lr + k] = sv.rdinv[36 * r + k];
+    }
+    {
+        const unsigned bar = smem_u32(&mbar);
+        asm volatile("{\n.reg .pred P;\nWAIT%=:\n"
+                     "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n"
+                     "@!P bra WAIT%=;\n}" ::"r"(bar)
+                     : "memory");
+    }
+    for (int i = threadIdx.x; i < 6 * nr; i += kCT) { // (D + eps I)
+        const int lr = i / 6, k = i - 6 * lr;
+        const int b0 = bstart[lr];
+        if (b0 < cap_blocks) blk[36 * b0 + 7 * k] += eps;
     }
     __syncthreads();
 
@@ -430,14 +501,12 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             s_rr += g * g;
         }
     }
-    double2 bb = cta_sum2(s_rz, s_rr, red);
-    if (static_cast<int>(threadIdx.x) < csize)
-        cl.map_shared_rank(&sc, static_cast<int>(threadIdx.x))->rzr[rank] = bb;
-    cluster_barrier();
     {
-        const double2 v = lane < csize ? sc.rzr[lane] : make_double2(0.0, 0.0);
-        bb = make_double2(fold16(v.x), fold16(v.y));
+        const double2 w = make_double2(warp_sum(s_rz), warp_sum(s_rr));
+        if (lane < csize) cl.map_shared_rank(&sc, lane)->rzr[rank * kCW + warp] = w;
     }
+    cluster_barrier();
+    const double2 bb = fold_table2(sc.rzr, ntab);
     double rz = bb.x;
     const double bnorm2 = bb.y;
     bool done = !act || bnorm2 == 0.0;
@@ -454,33 +523,40 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             if (lane < 30 && lr < nr) {
                 const int b0 = bstart[lr], b1 = bstart[lr + 1];
                 double y = 0.0;
-                for (int s = b0; s < b1; ++s) {
-                    const double* M;
-                    const double* zc;
-                    double e = 0.0;
-                    if (s < cap_blocks) {
-                        M = blk + 36 * s + 6 * comp;
-                        zc = bptr[s];
-                    } else { // spilled block: global memory, eps added here
-                        const int r = r0 + lr, t = s - b0;
-                        const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
-                        M = (t == 0 ? sv.rdiag + 36 * r
-                                    : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36) + 6 * comp;
-                        const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
-                        zc = cl.map_shared_rank(vz, crank) + 6 * cl_row;
-                        e = t == 0 ? eps : 0.0;
+                if (b1 <= cap_blocks) { // all blocks staged: two at a time, loads first
+                    int s = b0;
+                    for (; s + 1 < b1; s += 2) {
+                        const double* za = bptr[s];
+                        const double* zb = bptr[s + 1];
+                        double ya = 0.0, yb = 0.0;
+                        blk_row(blk + 36 * s + 6 * comp, za, za + poff, beta, ya);
+                        blk_row(blk + 36 * (s + 1) + 6 * comp, zb, zb + poff, beta, yb);
+                        y += ya;
+                        y += yb;
                     }
-                    const double* pc = zc + poff;
-                    const double2* M2 = reinterpret_cast<const double2*>(M);
-                    const double2* z2 = reinterpret_cast<const double2*>(zc);
-                    const double2* p2 = reinterpret_cast<const double2*>(pc);
-#pragma unroll
-                    for (int h = 0; h < 3; ++h) {
-                        const double2 m = M2[h], zz = z2[h], pp = p2[h];
-                        y += m.x * (zz.x + beta * pp.x);
-                        y += m.y * (zz.y + beta * pp.y);
+                    if (s < b1) {
+                        const double* za = bptr[s];
+                        double ya = 0.0;
+                        blk_row(blk + 36 * s + 6 * comp, za, za + poff, beta, ya);
+                        y += ya;
                     }
-                    if (e != 0.0) y += e * (zc[comp] + beta * pc[comp]);
+                } else {
+                    for (int s = b0; s < b1; ++s) {
+                        double ya = 0.0;
+                        if (s < cap_blocks) {
+                            blk_row(blk + 36 * s + 6 * comp, bptr[s], bptr[s] + poff, beta, ya);
+                        } else { // spilled block: global memory, eps added here
+                            const int r = r0 + lr, t = s - b0;
+                            const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+                            const double* M = (t == 0 ? sv.rdiag + 36 * r
+                                                      : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36) + 6 * comp;
+                            const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
+                            const double* zc = cl.map_shared_rank(vz, crank) + 6 * cl_row;
+                            blk_row(M, zc, zc + poff, beta, ya);
+                            if (t == 0) ya += eps * (zc[comp] + beta * zc[poff + comp]);
+                        }
+                        y += ya;
+                    }
                 }
                 const int i = 6 * lr + comp;
                 const double pr = vz[i] + beta * pold[i];
@@ -489,11 +565,12 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 pap += pr * y;
             }
         }
-        const double2 bp = cta_sum2(pap, 0.0, red);
-        if (static_cast<int>(threadIdx.x) < csize)
-            cl.map_shared_rank(&sc, static_cast<int>(threadIdx.x))->pap[rank] = bp.x;
+        {
+            const double w = warp_sum(pap);
+            if (lane < csize) cl.map_shared_rank(&sc, lane)->pap[rank * kCW + warp] = w;
+        }
         cluster_barrier();
-        const double pap_all = fold16(lane < csize ? sc.pap[lane] : 0.0);
+        const double pap_all = fold_table(sc.pap, ntab);
         if (!(pap_all > 0.0)) break; // exact solution or breakdown (uniform)
         const double alpha = rz / pap_all;
         // ---- phase B: x += alpha p ; r -= alpha Ap ; z = Dinv r
@@ -520,12 +597,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 l_rr += rv * rv;
             }
         }
-        const double2 cc = cta_sum2(l_rz, l_rr, red);
-        if (static_cast<int>(threadIdx.x) < csize)
-            cl.map_shared_rank(&sc, static_cast<int>(threadIdx.x))->rzr[rank] = cc;
+        {
+            const double2 w = make_double2(warp_sum(l_rz), warp_sum(l_rr));
+            if (lane < csize) cl.map_shared_rank(&sc, lane)->rzr[rank * kCW + warp] = w;
+        }
         cluster_barrier();
-        const double2 v = lane < csize ? sc.rzr[lane] : make_double2(0.0, 0.0);
-        const double rz_new = fold16(v.x), rr = fold16(v.y);
+        const double2 v = fold_table2(sc.rzr, ntab);
+        const double rz_new = v.x, rr = v.y;
         beta = rz != 0.0 ? rz_new / rz : 0.0;
         rz = rz_new;
         ++it;
