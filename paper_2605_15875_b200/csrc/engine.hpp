@@ -56,6 +56,7 @@ class Engine {
     void set_solver(double tol, int max_iters) {
         pcg_tol_ = tol;
         pcg_max_ = max_iters;
+        graph_ok_ = false; // the captured frame bakes the PCG arguments in
     }
     cudaStream_t stream() const { return s_; }
     const HostScene& scene() const { return hs_; }

@@ -293,15 +293,16 @@ __global__ void __launch_bounds__(kT) k_pcg(SolverView sv, PcgArgs a) {
 constexpr int kCT = 512;
 constexpr int kCW = kCT / 32;
 constexpr int kRowsPerWarp = 5;
-constexpr int kCSmemBytes = 200 * 1024;
+constexpr int kCSmemBytes = 220 * 1024;
 
-// Every warp pushes its partials into slot [rank][warp] of every peer's
-// table (fire-and-forget DSMEM stores), so after one cluster barrier each
-// thread folds the whole table locally in a fixed order -- same bits in every
-// thread of every CTA, and no CTA-level barrier on the reduction path.
+// Per-iteration partials (r.u, w.u, r.r) of every CTA, pushed into slot
+// [parity][rank] of every peer (fire-and-forget DSMEM stores); after the
+// cluster barrier every thread folds the csize entries in rank order, so all
+// threads of all CTAs hold the same bits. Parity double-buffering lets a fast
+// CTA push iteration k+1 while a slow peer still folds iteration k.
 struct ClusterScalars {
-    double pap[16 * kCW];
-    double2 rzr[16 * kCW]; // (r.z, r.r)
+    double3 tab[2][16];
+    double3 red[kCW];
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -314,46 +315,64 @@ __device__ __forceinline__ void cluster_barrier() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-
-// Fold of the first n entries of a [rank][warp] table (n = csize * kCW).
-__device__ __forceinline__ double fold_table(const double* t, int n) {
-    const int lane = threadIdx.x & 31;
-    double v = 0.0;
-    for (int i = lane; i < n; i += 32) v += t[i];
-    return warp_sum(v);
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
-
-__device__ __forceinline__ double2 fold_table2(const double2* t, int n) {
-    const int lane = threadIdx.x & 31;
-    double x = 0.0, y = 0.0;
-    for (int i = lane; i < n; i += 32) {
-        x += t[i].x;
-        y += t[i].y;
-    }
-    return make_double2(warp_sum(x), warp_sum(y));
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-// One 6x6 block-row product term: y += M_row . (z + beta p), M/z/p 16B aligned.
-__device__ __forceinline__ void blk_row(const double* M, const double* zc, const double* pc,
-                                        double beta, double& y) {
-    const double2* M2 = reinterpret_cast<const double2*>(M);
-    const double2* z2 = reinterpret_cast<const double2*>(zc);
-    const double2* p2 = reinterpret_cast<const double2*>(pc);
-    const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2];
-    const double2 z0 = z2[0], z1 = z2[1], z2v = z2[2];
-    const double2 q0 = p2[0], q1 = p2[1], q2 = p2[2];
-    y += m0.x * (z0.x + beta * q0.x);
-    y += m0.y * (z0.y + beta * q0.y);
-    y += m1.x * (z1.x + beta * q1.x);
-    y += m1.y * (z1.y + beta * q1.y);
-    y += m2.x * (z2v.x + beta * q2.x);
-    y += m2.y * (z2v.y + beta * q2.y);
+// CTA-wide sums of three values, pushed to every peer's tab[par][rank].
+// Ends with the values visible only after the next cluster barrier.
+__device__ __forceinline__ void cta_push3(cg::cluster_group& cl, ClusterScalars& sc, int par,
+                                          int rank, int csize, double a, double b, double c) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, off);
+        b += __shfl_xor_sync(0xffffffffu, b, off);
+        c += __shfl_xor_sync(0xffffffffu, c, off);
+    }
+    if (lane == 0) sc.red[warp] = make_double3(a, b, c);
+    __syncthreads();
+    if (warp == 0 && lane < csize) {
+        double3 t = make_double3(0.0, 0.0, 0.0);
+#pragma unroll
+        for (int w = 0; w < kCW; ++w) { // fixed order
+            t.x += sc.red[w].x;
+            t.y += sc.red[w].y;
+            t.z += sc.red[w].z;
+        }
+        cl.map_shared_rank(&sc, lane)->tab[par][rank] = t;
+    }
 }
 
+__device__ __forceinline__ double3 fold3(const ClusterScalars& sc, int par, int csize) {
+    double3 t = make_double3(0.0, 0.0, 0.0);
+    for (int k = 0; k < csize; ++k) { // rank order; surplus CTAs pushed zeros
+        const double3 v = sc.tab[par][k];
+        t.x += v.x;
+        t.y += v.y;
+        t.z += v.z;
+    }
+    return t;
+}
+
+// Pipelined block-Jacobi PCG (Ghysels & Vanroose 2014, preconditioned
+// variant): the three dot products of an iteration travel in ONE cluster
+// reduction whose barrier also publishes m = Dinv w to the peers, and the
+// barrier latency is hidden behind the local-column half of n = A m:
+//   local:  m = Dinv w; partials (r.u, w.u, r.r)  -> push, arrive
+//           n_loc = sum_{j in CTA} A_ij m_j
+//   wait:   fold; beta, alpha; n += sum_{j in peers} A_ij m_j (DSMEM)
+//   update: z = n + b z, q = m + b q, s = w + b s, p = u + b p,
+//           x += a p, r -= a s, u -= a q, w -= a z
+// Lane layout: a warp owns 5 rows, lane = 6 * slot + comp (lanes 30, 31
+// idle), so a 6x6 block costs one row of 6 FMAs per lane.
 __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, int csize, int cmax_rows) {
     cg::cluster_group cl = cg::this_cluster();
     unsigned long long t_start = 0;
@@ -361,6 +380,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ ClusterScalars sc;
     __shared__ __align__(8) unsigned long long mbar;
+    __shared__ int n_remote;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = lane / 6, comp = lane - 6 * slot;
     const int rank = static_cast<int>(cl.block_rank());
@@ -378,22 +398,29 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     const PartState& st = sv.ps[p];
     const bool act = st.active != 0 && R1 > R0;
     const double eps = st.eps;
-    const int ntab = csize * kCW;
     // shared-memory carve-up (cmax_rows = chunk upper bound used at launch)
+    const int V = 6 * cmax_rows;
     double* vx = reinterpret_cast<double*>(smem);
-    double* vr = vx + 6 * cmax_rows;
-    double* vz = vr + 6 * cmax_rows;
-    double* vap = vz + 6 * cmax_rows;
-    double* vp0 = vap + 6 * cmax_rows;
-    double* vp1 = vp0 + 6 * cmax_rows;
-    double* dinv = vp1 + 6 * cmax_rows;
+    double* vr = vx + V;
+    double* vu = vr + V;
+    double* vw = vu + V;
+    double* vz = vw + V;
+    double* vq = vz + V;
+    double* vs = vq + V;
+    double* vp = vs + V;
+    double* vm0 = vp + V; // m ping-pong: the vector the peers read
+    double* vm1 = vm0 + V;
+    double* dinv = vm1 + V;
     int* bstart = reinterpret_cast<int*>(dinv + 36 * cmax_rows); // [cmax_rows + 1]
-    const size_t used = (72ull * cmax_rows) * 8 + 4ull * (cmax_rows + 2);
-    const int cap_blocks = static_cast<int>((kCSmemBytes - used - 16) / (36 * 8 + 8)) & ~1; // blk 16B-aligned
-    const double** bptr = reinterpret_cast<const double**>(
+    // per staged block: the block (288 B), its column code (4 B) and, for a
+    // column in a peer CTA, the DSMEM address of that row's m0 entry (8 B)
+    const size_t used = (96ull * cmax_rows) * 8 + 4ull * (cmax_rows + 2) + 16;
+    const int cap_blocks = static_cast<int>((kCSmemBytes - used - 32) / (288 + 4 + 8)) & ~1;
+    double* blk = reinterpret_cast<double*>(
         (reinterpret_cast<uintptr_t>(bstart + cmax_rows + 1) + 15) & ~uintptr_t(15));
-    double* blk = reinterpret_cast<double*>(bptr + cap_blocks);
-    const ptrdiff_t off_p0 = vp0 - vz, off_p1 = vp1 - vz;
+    const double** rptr = reinterpret_cast<const double**>(blk + 36 * cap_blocks);
+    int* bcode = reinterpret_cast<int*>(rptr + cap_blocks);
+    const ptrdiff_t m_off = vm1 - vm0;
 
     // ---- stage rows with TMA bulk copies: per row the diagonal block and the
     // contiguous run of coupling blocks, plus the chunk's Dinv in one copy.
@@ -401,6 +428,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        n_remote = 0;
     }
     for (int lr = threadIdx.x; lr < nr; lr += kCT) bstart[lr + 1] = sv.ell_cnt[r0 + lr] + 1;
     __syncthreads();
@@ -418,7 +446,6 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         }
         if (lane == 0) bstart[0] = 0;
         __syncwarp();
-        // bytes this CTA will receive, then the copies (lanes over rows)
         unsigned bytes = 0;
         for (int lr = lane; lr < nr; lr += 32) {
             const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
@@ -454,14 +481,21 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                          : "memory");
     }
     __syncthreads();
-    // DSMEM address of every staged block's column (lanes over a row's blocks)
+    // column code of every staged block: >= 0 a row of this CTA, < 0 the
+    // remote slot -1 - j (DSMEM address of the peer row's m0 entry)
     for (int lr = warp; lr < nr; lr += kCW) {
         const int r = r0 + lr;
         const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
         for (int t = lane; t < nb && b0 + t < cap_blocks; t += 32) {
             const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
             const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
-            bptr[b0 + t] = cl.map_shared_rank(vz, crank) + 6 * cl_row;
+            if (crank == rank) {
+                bcode[b0 + t] = cl_row;
+            } else {
+                const int j = atomicAdd(&n_remote, 1);
+                rptr[j] = cl.map_shared_rank(vm0, crank) + 6 * cl_row;
+                bcode[b0 + t] = -1 - j;
+            }
         }
     }
     {
@@ -479,139 +513,170 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     __syncthreads();
 
     const int row_step = kCW * kRowsPerWarp;
-    // ---- init: r = -grad, x = 0, z = Dinv r, p_old = 0
-    double s_rz = 0.0, s_rr = 0.0;
+    // y = (A v)_row comp over the blocks of one class: local columns (v in
+    // this CTA at vloc) or remote columns (peer m buffer `moff` from m0) and
+    // spilled blocks (global memory, after the barrier only).
+    auto spmv_local = [&](int lr, const double* vloc) -> double {
+        const int b0 = bstart[lr], bs = min(bstart[lr + 1], cap_blocks);
+        double y = 0.0;
+        for (int s = b0; s < bs; ++s) {
+            const int code = bcode[s];
+            if (code < 0) continue;
+            const double2* M2 = reinterpret_cast<const double2*>(blk + 36 * s + 6 * comp);
+            const double2* v2 = reinterpret_cast<const double2*>(vloc + 6 * code);
+            const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2];
+            const double2 w0 = v2[0], w1 = v2[1], w2 = v2[2];
+            double ya = m0.x * w0.x;
+            ya += m0.y * w0.y;
+            ya += m1.x * w1.x;
+            ya += m1.y * w1.y;
+            ya += m2.x * w2.x;
+            ya += m2.y * w2.y;
+            y += ya;
+        }
+        return y;
+    };
+    auto spmv_remote = [&](int lr, ptrdiff_t moff, double y) -> double {
+        const int b0 = bstart[lr], b1 = bstart[lr + 1], bs = min(b1, cap_blocks);
+        for (int s = b0; s < bs; ++s) {
+            const int code = bcode[s];
+            if (code >= 0) continue;
+            const double2* M2 = reinterpret_cast<const double2*>(blk + 36 * s + 6 * comp);
+            const double2* v2 = reinterpret_cast<const double2*>(rptr[-1 - code] + moff);
+            const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2];
+            const double2 w0 = v2[0], w1 = v2[1], w2 = v2[2];
+            double ya = m0.x * w0.x;
+            ya += m0.y * w0.y;
+            ya += m1.x * w1.x;
+            ya += m1.y * w1.y;
+            ya += m2.x * w2.x;
+            ya += m2.y * w2.y;
+            y += ya;
+        }
+        for (int s = bs; s < b1; ++s) { // spilled block: global memory + DSMEM
+            const int r = r0 + lr, t = s - b0;
+            const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+            const double* M = (t == 0 ? sv.rdiag + 36 * r
+                                      : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36) + 6 * comp;
+            const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
+            const double* v = cl.map_shared_rank(vm0, crank) + moff + 6 * cl_row;
+            double ya = 0.0;
+            for (int c = 0; c < 6; ++c) ya += M[c] * v[c];
+            if (t == 0) ya += eps * v[comp];
+            y += ya;
+        }
+        return y;
+    };
+
+    // ---- init: r = b = -grad, x = 0, u = Dinv r (published in m1), w = A u
     for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
         const int lr = base + slot;
         const bool on = lane < 30 && lr < nr;
         const double g = on && act ? -sv.rgrad[6 * (r0 + lr) + comp] : 0.0;
-        double z = 0.0;
+        double u = 0.0;
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
             const double gc = __shfl_sync(0xffffffffu, g, (6 * slot + c) & 31);
-            if (on) z += dinv[36 * lr + 6 * comp + c] * gc;
+            if (on) u += dinv[36 * lr + 6 * comp + c] * gc;
         }
         if (on) {
             const int i = 6 * lr + comp;
             vr[i] = g;
-            vz[i] = z;
+            vu[i] = u;
+            vm1[i] = u;
             vx[i] = 0.0;
-            vp0[i] = 0.0;
-            s_rz += g * z;
-            s_rr += g * g;
+            vz[i] = 0.0;
+            vq[i] = 0.0;
+            vs[i] = 0.0;
+            vp[i] = 0.0;
         }
-    }
-    {
-        const double2 w = make_double2(warp_sum(s_rz), warp_sum(s_rr));
-        if (lane < csize) cl.map_shared_rank(&sc, lane)->rzr[rank * kCW + warp] = w;
     }
     cluster_barrier();
-    const double2 bb = fold_table2(sc.rzr, ntab);
-    double rz = bb.x;
-    const double bnorm2 = bb.y;
-    bool done = !act || bnorm2 == 0.0;
-    double beta = 0.0;
-    int it = 0, cur = 0;
+    for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
+        const int lr = base + slot;
+        if (lane < 30 && lr < nr) vw[6 * lr + comp] = spmv_remote(lr, m_off, spmv_local(lr, vm1));
+    }
+    __syncthreads();
+
+    bool done = !act;
+    double gamma_old = 0.0, alpha_old = 0.0, bnorm2 = 0.0;
+    int it = 0;
     while (!done) {
-        double* pold = cur ? vp1 : vp0;
-        double* pnew = cur ? vp0 : vp1;
-        const ptrdiff_t poff = cur ? off_p1 : off_p0;
-        // ---- phase A: Ap over (z + beta p_old) of the columns; p_new; p.Ap
-        double pap = 0.0;
-        for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
-            const int lr = base + slot;
-            if (lane < 30 && lr < nr) {
-                const int b0 = bstart[lr], b1 = bstart[lr + 1];
-                double y = 0.0;
-                if (b1 <= cap_blocks) { // all blocks staged: two at a time, loads first
-                    int s = b0;
-                    for (; s + 1 < b1; s += 2) {
-                        const double* za = bptr[s];
-                        const double* zb = bptr[s + 1];
-                        double ya = 0.0, yb = 0.0;
-                        blk_row(blk + 36 * s + 6 * comp, za, za + poff, beta, ya);
-                        blk_row(blk + 36 * (s + 1) + 6 * comp, zb, zb + poff, beta, yb);
-                        y += ya;
-                        y += yb;
-                    }
-                    if (s < b1) {
-                        const double* za = bptr[s];
-                        double ya = 0.0;
-                        blk_row(blk + 36 * s + 6 * comp, za, za + poff, beta, ya);
-                        y += ya;
-                    }
-                } else {
-                    for (int s = b0; s < b1; ++s) {
-                        double ya = 0.0;
-                        if (s < cap_blocks) {
-                            blk_row(blk + 36 * s + 6 * comp, bptr[s], bptr[s] + poff, beta, ya);
-                        } else { // spilled block: global memory, eps added here
-                            const int r = r0 + lr, t = s - b0;
-                            const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
-                            const double* M = (t == 0 ? sv.rdiag + 36 * r
-                                                      : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36) + 6 * comp;
-                            const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
-                            const double* zc = cl.map_shared_rank(vz, crank) + 6 * cl_row;
-                            blk_row(M, zc, zc + poff, beta, ya);
-                            if (t == 0) ya += eps * (zc[comp] + beta * zc[poff + comp]);
-                        }
-                        y += ya;
-                    }
-                }
-                const int i = 6 * lr + comp;
-                const double pr = vz[i] + beta * pold[i];
-                pnew[i] = pr;
-                vap[i] = y;
-                pap += pr * y;
-            }
-        }
-        {
-            const double w = warp_sum(pap);
-            if (lane < csize) cl.map_shared_rank(&sc, lane)->pap[rank * kCW + warp] = w;
-        }
-        cluster_barrier();
-        const double pap_all = fold_table(sc.pap, ntab);
-        if (!(pap_all > 0.0)) break; // exact solution or breakdown (uniform)
-        const double alpha = rz / pap_all;
-        // ---- phase B: x += alpha p ; r -= alpha Ap ; z = Dinv r
-        double l_rz = 0.0, l_rr = 0.0;
+        const int par = it & 1;
+        double* mcur = par ? vm1 : vm0;
+        const ptrdiff_t moff = par ? m_off : 0;
+        // ---- local: m = Dinv w; partials (r.u, w.u, r.r)
+        double l_g = 0.0, l_d = 0.0, l_r = 0.0;
         for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
             const int lr = base + slot;
             const bool on = lane < 30 && lr < nr;
             const int i = 6 * lr + comp;
-            double rv = 0.0;
-            if (on) {
-                vx[i] += alpha * pnew[i];
-                rv = vr[i] - alpha * vap[i];
-                vr[i] = rv;
-            }
-            double z = 0.0;
+            const double wv = on ? vw[i] : 0.0;
+            double m = 0.0;
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
-                const double rc = __shfl_sync(0xffffffffu, rv, (6 * slot + c) & 31);
-                if (on) z += dinv[36 * lr + 6 * comp + c] * rc;
+                const double wc = __shfl_sync(0xffffffffu, wv, (6 * slot + c) & 31);
+                if (on) m += dinv[36 * lr + 6 * comp + c] * wc;
             }
             if (on) {
-                vz[i] = z;
-                l_rz += rv * z;
-                l_rr += rv * rv;
+                mcur[i] = m;
+                const double rv = vr[i], uv = vu[i];
+                l_g += rv * uv;
+                l_d += wv * uv;
+                l_r += rv * rv;
             }
         }
+        cta_push3(cl, sc, par, rank, csize, l_g, l_d, l_r); // includes __syncthreads
+        cluster_arrive();
+        // local-column half of n = A m while the barrier completes
+        // (the first two row groups of the warp; more only when nr > 160)
+        double nloc0 = 0.0, nloc1 = 0.0;
         {
-            const double2 w = make_double2(warp_sum(l_rz), warp_sum(l_rr));
-            if (lane < csize) cl.map_shared_rank(&sc, lane)->rzr[rank * kCW + warp] = w;
+            const int lr0 = warp * kRowsPerWarp + slot, lr1 = lr0 + row_step;
+            if (lane < 30 && lr0 < nr) nloc0 = spmv_local(lr0, mcur);
+            if (lane < 30 && lr1 < nr) nloc1 = spmv_local(lr1, mcur);
         }
-        cluster_barrier();
-        const double2 v = fold_table2(sc.rzr, ntab);
-        const double rz_new = v.x, rr = v.y;
-        beta = rz != 0.0 ? rz_new / rz : 0.0;
-        rz = rz_new;
+        cluster_wait();
+        const double3 f = fold3(sc, par, csize);
+        const double gamma = f.x, delta = f.y, rr = f.z;
+        if (it == 0) bnorm2 = rr;
+        if (bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters) break;
+        double alpha, beta;
+        if (it == 0) {
+            beta = 0.0;
+            alpha = gamma / delta;
+        } else {
+            beta = gamma / gamma_old;
+            alpha = gamma / (delta - beta * gamma / alpha_old);
+        }
+        if (!(alpha > 0.0) || !isfinite(alpha)) break; // breakdown (uniform)
+        // ---- remote half of n, then the recurrences
+        {
+            int k = 0;
+            for (int base = warp * kRowsPerWarp; base < nr; base += row_step, ++k) {
+                const int lr = base + slot;
+                if (lane < 30 && lr < nr) {
+                    const double n0 = k == 0 ? nloc0 : k == 1 ? nloc1 : spmv_local(lr, mcur);
+                    const double n = spmv_remote(lr, moff, n0);
+                    const int i = 6 * lr + comp;
+                    const double z = n + beta * vz[i];
+                    const double q = mcur[i] + beta * vq[i];
+                    const double s = vw[i] + beta * vs[i];
+                    const double pv = vu[i] + beta * vp[i];
+                    vz[i] = z;
+                    vq[i] = q;
+                    vs[i] = s;
+                    vp[i] = pv;
+                    vx[i] += alpha * pv;
+                    vr[i] -= alpha * s;
+                    vu[i] -= alpha * q;
+                    vw[i] -= alpha * z;
+                }
+            }
+        }
+        gamma_old = gamma;
+        alpha_old = alpha;
         ++it;
-        if (rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters) done = true;
-        cur ^= 1;
-        // Two barriers per iteration suffice: the one above orders our z /
-        // p_new writes before the peers' next phase A, the one in phase A
-        // orders their reads of our z before our next phase-B writes.
     }
     for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
         const int lr = base + slot;
