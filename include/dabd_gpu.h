@@ -233,6 +233,12 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_enable(const char* kernel_nam
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_pcg_perf(dabd_gpu_ctx* ctx, int reset, double* ns,
                                                    long long* launches, double* bytes,
                                                    long long* iterations);
+/* Cycles (clock64, CTA 0 / warp 0 of the cluster PCG) spent per phase of a
+ * PCG iteration since the last reset, summed over iterations: [0] local
+ * m = Dinv w + partials, [1] CTA reduction + DSMEM push, [2] arrive,
+ * [3] local-column SpMV, [4] barrier wait, [5] fold + scalars, [6] remote
+ * SpMV + recurrences, [7] iterations counted. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_pcg_phases(dabd_gpu_ctx* ctx, int reset, double* cycles);
 /* "name launches total_ms;" per timed kernel ("*" times every kernel). */
 DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_report(char* buf, int capacity);
 DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_read(double* total_ms, long long* launches,

@@ -65,7 +65,7 @@ EXPORTS = [
     "dabd_gpu_newton_solve", "dabd_gpu_run_frames", "dabd_gpu_set_state", "dabd_gpu_get_state",
     "dabd_gpu_get_rho", "dabd_gpu_take_trace", "dabd_gpu_launch_count",
     "dabd_gpu_kernel_timer_enable", "dabd_gpu_kernel_timer_read", "dabd_gpu_kernel_timer_report",
-    "dabd_gpu_ctx_pcg_perf", "dabd_gpu_ctx_set_comm",
+    "dabd_gpu_ctx_pcg_perf", "dabd_gpu_ctx_set_comm", "dabd_gpu_ctx_pcg_phases",
 ]
 
 _lib = None

@@ -398,6 +398,15 @@ dabd_gpu_status dabd_gpu_ctx_pcg_perf(dabd_gpu_ctx* ctx, int reset, double* ns,
     });
 }
 
+dabd_gpu_status dabd_gpu_ctx_pcg_phases(dabd_gpu_ctx* ctx, int reset, double* cycles) {
+    if (!ctx || !cycles) return null_arg();
+    return guarded([&] {
+        const dabd_gpu::DevPerf p = ctx->e->read_perf(reset != 0);
+        for (int k = 0; k < 8; ++k) cycles[k] = static_cast<double>(p.phase[k]);
+        return DABD_GPU_OK;
+    });
+}
+
 dabd_gpu_status dabd_gpu_kernel_timer_report(char* buf, int capacity) {
     if (!buf || capacity < 1) return null_arg();
     const std::string r = dabd_gpu::KernelTimer::get().report();

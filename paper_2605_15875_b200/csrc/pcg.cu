@@ -295,14 +295,22 @@ constexpr int kCW = kCT / 32;
 constexpr int kRowsPerWarp = 5;
 constexpr int kCSmemBytes = 220 * 1024;
 
-// Per-iteration partials (r.u, w.u, r.r) of every CTA, pushed into slot
-// [parity][rank] of every peer (fire-and-forget DSMEM stores); after the
-// cluster barrier every thread folds the csize entries in rank order, so all
-// threads of all CTAs hold the same bits. Parity double-buffering lets a fast
-// CTA push iteration k+1 while a slow peer still folds iteration k.
+// Per-iteration partials (r.u, w.u, r.r) of every CTA land in slot
+// [parity][rank] of every peer; every thread folds the csize entries in rank
+// order, so all threads of all CTAs hold the same bits. Parity
+// double-buffering lets a fast CTA send iteration k+1 while a slow peer still
+// reads iteration k.
 struct ClusterScalars {
-    double3 tab[2][16];
-    double3 red[kCW];
+    double tab[2][16][4]; // (r.u, w.u, r.r, pad): 32 B slots for v2 stores
+    double red[kCW][3];
+    unsigned long long bar[2]; // per-parity mbarriers (st.async complete_tx)
+    unsigned long long stage_bar;
+    int n_remote, n_send, fallback;
+};
+
+struct SendEntry {
+    int row;  // local row of this CTA whose m the peer needs
+    int dest; // (peer rank << 20) | peer halo slot
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -326,61 +334,54 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-// CTA-wide sums of three values, pushed to every peer's tab[par][rank].
-// Ends with the values visible only after the next cluster barrier.
-__device__ __forceinline__ void cta_push3(cg::cluster_group& cl, ClusterScalars& sc, int par,
-                                          int rank, int csize, double a, double b, double c) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, off);
-        b += __shfl_xor_sync(0xffffffffu, b, off);
-        c += __shfl_xor_sync(0xffffffffu, c, off);
-    }
-    if (lane == 0) sc.red[warp] = make_double3(a, b, c);
-    __syncthreads();
-    if (warp == 0 && lane < csize) {
-        double3 t = make_double3(0.0, 0.0, 0.0);
-#pragma unroll
-        for (int w = 0; w < kCW; ++w) { // fixed order
-            t.x += sc.red[w].x;
-            t.y += sc.red[w].y;
-            t.z += sc.red[w].z;
-        }
-        cl.map_shared_rank(&sc, lane)->tab[par][rank] = t;
-    }
+// shared::cluster address of `local_addr` (a shared::cta address) in CTA `rank`
+__device__ __forceinline__ unsigned mapa(unsigned local_addr, int rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+    return r;
 }
 
-__device__ __forceinline__ double3 fold3(const ClusterScalars& sc, int par, int csize) {
-    double3 t = make_double3(0.0, 0.0, 0.0);
-    for (int k = 0; k < csize; ++k) { // rank order; surplus CTAs pushed zeros
-        const double3 v = sc.tab[par][k];
-        t.x += v.x;
-        t.y += v.y;
-        t.z += v.z;
-    }
-    return t;
+// 16-byte remote store that completes `bytes` on the destination's mbarrier.
+__device__ __forceinline__ void st_async2(unsigned dst, double a, double b, unsigned bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                 ::"r"(dst), "d"(a), "d"(b), "r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile("{\n.reg .pred P;\nWAIT%=:\n"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+                 "@!P bra WAIT%=;\n}" ::"r"(bar), "r"(parity)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
 }
 
 // Pipelined block-Jacobi PCG (Ghysels & Vanroose 2014, preconditioned
-// variant): the three dot products of an iteration travel in ONE cluster
-// reduction whose barrier also publishes m = Dinv w to the peers, and the
-// barrier latency is hidden behind the local-column half of n = A m:
-//   local:  m = Dinv w; partials (r.u, w.u, r.r)  -> push, arrive
-//           n_loc = sum_{j in CTA} A_ij m_j
-//   wait:   fold; beta, alpha; n += sum_{j in peers} A_ij m_j (DSMEM)
+// variant) on one thread-block cluster per partition, every vector and the
+// partition's BSR rows resident in shared memory:
+//   local:  m = Dinv w; partials (r.u, w.u, r.r) -> CTA sum -> st.async to
+//           every peer; the m rows a peer's blocks need -> st.async into the
+//           peer's halo slots (push, one-way latency, no cluster barrier)
+//           n_loc = sum_{j in CTA} A_ij m_j while the messages fly
+//   wait:   this CTA's mbarrier (partials + halo bytes); fold; beta, alpha;
+//           n += sum_{j remote} A_ij halo_j
 //   update: z = n + b z, q = m + b q, s = w + b s, p = u + b p,
 //           x += a p, r -= a s, u -= a q, w -= a z
 // Lane layout: a warp owns 5 rows, lane = 6 * slot + comp (lanes 30, 31
 // idle), so a 6x6 block costs one row of 6 FMAs per lane.
+// A cluster whose rows overflow the shared-memory budget (spilled blocks or
+// send lists) takes the barrier-synchronised path that reads peers' m
+// through DSMEM and spilled blocks from global memory.
 __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, int csize, int cmax_rows) {
     cg::cluster_group cl = cg::this_cluster();
     unsigned long long t_start = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ ClusterScalars sc;
-    __shared__ __align__(8) unsigned long long mbar;
-    __shared__ int n_remote;
+    __shared__ __align__(16) ClusterScalars sc;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = lane / 6, comp = lane - 6 * slot;
     const int rank = static_cast<int>(cl.block_rank());
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     // CTAs per partition from the partition's own row count (launch csize is
     // the batch maximum): the reduction trees, hence the bits, do not depend
     // on which other partitions share the launch or the GPU. Surplus CTAs
-    // get no rows and push exact zeros.
+    // get no rows and send exact zeros.
     int cs_p = 1;
     while (cs_p < csize && cs_p * 32 < R1 - R0) cs_p *= 2;
     const int chunk = max(1, (R1 - R0 + cs_p - 1) / cs_p);
@@ -408,28 +409,36 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     double* vq = vz + V;
     double* vs = vq + V;
     double* vp = vs + V;
-    double* vm0 = vp + V; // m ping-pong: the vector the peers read
+    double* vm0 = vp + V; // m (fallback path: ping-pong read by the peers)
     double* vm1 = vm0 + V;
     double* dinv = vm1 + V;
     int* bstart = reinterpret_cast<int*>(dinv + 36 * cmax_rows); // [cmax_rows + 1]
-    // per staged block: the block (288 B), its column code (4 B) and, for a
-    // column in a peer CTA, the DSMEM address of that row's m0 entry (8 B)
-    const size_t used = (96ull * cmax_rows) * 8 + 4ull * (cmax_rows + 2) + 16;
-    const int cap_blocks = static_cast<int>((kCSmemBytes - used - 32) / (288 + 4 + 8)) & ~1;
+    // per staged block: the block (288 B), its column code (4 B); per remote
+    // block additionally two parity halo rows (96 B), the DSMEM address of the
+    // peer row (8 B) and a send entry at the producer (8 B)
+    const size_t used = (96ull * cmax_rows) * 8 + 4ull * (cmax_rows + 2) + 64;
+    const int cap_blocks = static_cast<int>((kCSmemBytes - used) / (288 + 4 + 96 + 8 + 8)) & ~1;
     double* blk = reinterpret_cast<double*>(
         (reinterpret_cast<uintptr_t>(bstart + cmax_rows + 1) + 15) & ~uintptr_t(15));
-    const double** rptr = reinterpret_cast<const double**>(blk + 36 * cap_blocks);
-    int* bcode = reinterpret_cast<int*>(rptr + cap_blocks);
+    double* halo = blk + 36 * cap_blocks; // [2][cap_blocks][6]
+    const double** rptr = reinterpret_cast<const double**>(halo + 12 * cap_blocks);
+    SendEntry* sends = reinterpret_cast<SendEntry*>(rptr + cap_blocks);
+    int* bcode = reinterpret_cast<int*>(sends + cap_blocks);
     const ptrdiff_t m_off = vm1 - vm0;
 
     // ---- stage rows with TMA bulk copies: per row the diagonal block and the
     // contiguous run of coupling blocks, plus the chunk's Dinv in one copy.
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sc.stage_bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sc.bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sc.bar[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        n_remote = 0;
+        sc.n_remote = 0;
+        sc.n_send = 0;
+        sc.fallback = 0;
     }
+    for (int i = threadIdx.x; i < 2 * 16 * 4; i += kCT) (&sc.tab[0][0][0])[i] = 0.0;
     for (int lr = threadIdx.x; lr < nr; lr += kCT) bstart[lr + 1] = sv.ell_cnt[r0 + lr] + 1;
     __syncthreads();
     if (warp == 0) { // warp-wide inclusive scan in chunks of 32 rows
@@ -454,12 +463,9 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         }
         for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
         if (nr > 0) bytes += 288u * nr; // Dinv
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)),
-                         "r"(bytes)
-                         : "memory");
+        if (lane == 0) mbar_expect(smem_u32(&sc.stage_bar), bytes);
         __syncwarp();
-        const unsigned bar = smem_u32(&mbar);
+        const unsigned bar = smem_u32(&sc.stage_bar);
         for (int lr = lane; lr < nr; lr += 32) {
             const int r = r0 + lr;
             const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
@@ -480,80 +486,92 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                          ::"r"(smem_u32(dinv)), "l"(sv.rdinv + 36 * r0), "r"(288u * nr), "r"(bar)
                          : "memory");
     }
-    __syncthreads();
+    // every CTA's counters and barriers are initialised before any peer
+    // appends to its send list
+    cluster_barrier();
     // column code of every staged block: >= 0 a row of this CTA, < 0 the
-    // remote slot -1 - j (DSMEM address of the peer row's m0 entry)
+    // remote slot -1 - j; the owning peer gets a send entry for slot j
     for (int lr = warp; lr < nr; lr += kCW) {
         const int r = r0 + lr;
         const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
+        if (b0 + nb > cap_blocks && lane == 0) atomicOr(&sc.fallback, 1); // spilled blocks
         for (int t = lane; t < nb && b0 + t < cap_blocks; t += 32) {
             const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
             const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
             if (crank == rank) {
                 bcode[b0 + t] = cl_row;
             } else {
-                const int j = atomicAdd(&n_remote, 1);
+                const int j = atomicAdd(&sc.n_remote, 1);
                 rptr[j] = cl.map_shared_rank(vm0, crank) + 6 * cl_row;
                 bcode[b0 + t] = -1 - j;
+                ClusterScalars* peer = cl.map_shared_rank(&sc, crank);
+                const int e = atomicAdd(&peer->n_send, 1);
+                if (e < cap_blocks) {
+                    SendEntry* ps = cl.map_shared_rank(sends, crank);
+                    ps[e] = SendEntry{cl_row, (rank << 20) | j};
+                } else { // send list full: the whole cluster takes the barrier path
+                    atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
+                }
             }
         }
     }
-    {
-        const unsigned bar = smem_u32(&mbar);
-        asm volatile("{\n.reg .pred P;\nWAIT%=:\n"
-                     "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n"
-                     "@!P bra WAIT%=;\n}" ::"r"(bar)
-                     : "memory");
-    }
+    mbar_wait(smem_u32(&sc.stage_bar), 0);
     for (int i = threadIdx.x; i < 6 * nr; i += kCT) { // (D + eps I)
         const int lr = i / 6, k = i - 6 * lr;
         const int b0 = bstart[lr];
         if (b0 < cap_blocks) blk[36 * b0 + 7 * k] += eps;
     }
     __syncthreads();
+    // any overflow in the cluster selects the barrier path everywhere
+    if (threadIdx.x == 0 && sc.fallback) atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
+    cluster_barrier(); // send lists and fallback flags complete
+    const bool push = cl.map_shared_rank(&sc, 0)->fallback == 0;
+    const int n_remote = sc.n_remote, n_send = sc.n_send;
 
     const int row_step = kCW * kRowsPerWarp;
-    // y = (A v)_row comp over the blocks of one class: local columns (v in
-    // this CTA at vloc) or remote columns (peer m buffer `moff` from m0) and
-    // spilled blocks (global memory, after the barrier only).
+    // (A v) row comp over the staged blocks with local columns
     auto spmv_local = [&](int lr, const double* vloc) -> double {
         const int b0 = bstart[lr], bs = min(bstart[lr + 1], cap_blocks);
-        double y = 0.0;
-        for (int s = b0; s < bs; ++s) {
-            const int code = bcode[s];
-            if (code < 0) continue;
-            const double2* M2 = reinterpret_cast<const double2*>(blk + 36 * s + 6 * comp);
-            const double2* v2 = reinterpret_cast<const double2*>(vloc + 6 * code);
-            const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2];
-            const double2 w0 = v2[0], w1 = v2[1], w2 = v2[2];
-            double ya = m0.x * w0.x;
-            ya += m0.y * w0.y;
-            ya += m1.x * w1.x;
-            ya += m1.y * w1.y;
-            ya += m2.x * w2.x;
-            ya += m2.y * w2.y;
-            y += ya;
+        double y0 = 0.0, y1 = 0.0;
+        int s = b0;
+        for (; s + 1 < bs; s += 2) {
+            const int c0 = bcode[s], c1 = bcode[s + 1];
+            if (c0 >= 0) {
+                const double2* M2 = reinterpret_cast<const double2*>(blk + 36 * s + 6 * comp);
+                const double2* v2 = reinterpret_cast<const double2*>(vloc + 6 * c0);
+                const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2], w0 = v2[0], w1 = v2[1], w2 = v2[2];
+                y0 += m0.x * w0.x + m0.y * w0.y + m1.x * w1.x + m1.y * w1.y + m2.x * w2.x + m2.y * w2.y;
+            }
+            if (c1 >= 0) {
+                const double2* M2 = reinterpret_cast<const double2*>(blk + 36 * (s + 1) + 6 * comp);
+                const double2* v2 = reinterpret_cast<const double2*>(vloc + 6 * c1);
+                const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2], w0 = v2[0], w1 = v2[1], w2 = v2[2];
+                y1 += m0.x * w0.x + m0.y * w0.y + m1.x * w1.x + m1.y * w1.y + m2.x * w2.x + m2.y * w2.y;
+            }
         }
-        return y;
+        if (s < bs && bcode[s] >= 0) {
+            const double2* M2 = reinterpret_cast<const double2*>(blk + 36 * s + 6 * comp);
+            const double2* v2 = reinterpret_cast<const double2*>(vloc + 6 * bcode[s]);
+            const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2], w0 = v2[0], w1 = v2[1], w2 = v2[2];
+            y0 += m0.x * w0.x + m0.y * w0.y + m1.x * w1.x + m1.y * w1.y + m2.x * w2.x + m2.y * w2.y;
+        }
+        return y0 + y1;
     };
-    auto spmv_remote = [&](int lr, ptrdiff_t moff, double y) -> double {
+    // staged blocks with remote columns: values from `hv` (halo rows, push
+    // path) or through DSMEM from the peer's m buffer at `moff` (fallback),
+    // then spilled blocks (global memory + DSMEM, fallback only)
+    auto spmv_remote = [&](int lr, const double* hv, ptrdiff_t moff, double y) -> double {
         const int b0 = bstart[lr], b1 = bstart[lr + 1], bs = min(b1, cap_blocks);
         for (int s = b0; s < bs; ++s) {
             const int code = bcode[s];
             if (code >= 0) continue;
             const double2* M2 = reinterpret_cast<const double2*>(blk + 36 * s + 6 * comp);
-            const double2* v2 = reinterpret_cast<const double2*>(rptr[-1 - code] + moff);
-            const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2];
-            const double2 w0 = v2[0], w1 = v2[1], w2 = v2[2];
-            double ya = m0.x * w0.x;
-            ya += m0.y * w0.y;
-            ya += m1.x * w1.x;
-            ya += m1.y * w1.y;
-            ya += m2.x * w2.x;
-            ya += m2.y * w2.y;
-            y += ya;
+            const double2* v2 = reinterpret_cast<const double2*>(
+                hv ? hv + 6 * (-1 - code) : rptr[-1 - code] + moff);
+            const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2], w0 = v2[0], w1 = v2[1], w2 = v2[2];
+            y += m0.x * w0.x + m0.y * w0.y + m1.x * w1.x + m1.y * w1.y + m2.x * w2.x + m2.y * w2.y;
         }
-        for (int s = bs; s < b1; ++s) { // spilled block: global memory + DSMEM
+        for (int s = bs; s < b1; ++s) { // spilled block
             const int r = r0 + lr, t = s - b0;
             const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
             const double* M = (t == 0 ? sv.rdiag + 36 * r
@@ -568,7 +586,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         return y;
     };
 
-    // ---- init: r = b = -grad, x = 0, u = Dinv r (published in m1), w = A u
+    // ---- init: r = b = -grad, x = 0, u = Dinv r (read by the peers from m1), w = A u
     for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
         const int lr = base + slot;
         const bool on = lane < 30 && lr < nr;
@@ -594,17 +612,34 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     cluster_barrier();
     for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
         const int lr = base + slot;
-        if (lane < 30 && lr < nr) vw[6 * lr + comp] = spmv_remote(lr, m_off, spmv_local(lr, vm1));
+        if (lane < 30 && lr < nr)
+            vw[6 * lr + comp] = spmv_remote(lr, nullptr, m_off, spmv_local(lr, vm1));
     }
+    // peers read our m1 (= u) above; the push path never reads peers' smem
+    // again, the fallback path orders its next m1 writes behind a barrier
+    if (!push) cluster_barrier();
     __syncthreads();
 
     bool done = !act;
-    double gamma_old = 0.0, alpha_old = 0.0, bnorm2 = 0.0;
+    double inv_gamma_old = 0.0, inv_alpha_old = 0.0, bnorm2 = 0.0;
     int it = 0;
+    const bool timed = sv.perf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long ph[8] = {}, tc = clock64();
+    auto mark = [&](int k) {
+        if (timed) {
+            const unsigned long long t = clock64();
+            ph[k] += t - tc;
+            tc = t;
+        }
+    };
+    const unsigned expect = static_cast<unsigned>(32 * csize + 48 * n_remote);
     while (!done) {
+        mark(7);
         const int par = it & 1;
-        double* mcur = par ? vm1 : vm0;
+        double* mcur = push ? vm0 : (par ? vm1 : vm0);
         const ptrdiff_t moff = par ? m_off : 0;
+        const unsigned bar = smem_u32(&sc.bar[par]);
+        if (push && threadIdx.x == 0) mbar_expect(bar, expect);
         // ---- local: m = Dinv w; partials (r.u, w.u, r.r)
         double l_g = 0.0, l_d = 0.0, l_r = 0.0;
         for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
@@ -612,11 +647,14 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             const bool on = lane < 30 && lr < nr;
             const int i = 6 * lr + comp;
             const double wv = on ? vw[i] : 0.0;
-            double m = 0.0;
+            double wc[6];
 #pragma unroll
-            for (int c = 0; c < 6; ++c) {
-                const double wc = __shfl_sync(0xffffffffu, wv, (6 * slot + c) & 31);
-                if (on) m += dinv[36 * lr + 6 * comp + c] * wc;
+            for (int c = 0; c < 6; ++c) wc[c] = __shfl_sync(0xffffffffu, wv, (6 * slot + c) & 31);
+            double m = 0.0;
+            if (on) {
+                const double2* d2 = reinterpret_cast<const double2*>(dinv + 36 * lr + 6 * comp);
+                const double2 d0 = d2[0], d1 = d2[1], dd = d2[2];
+                m = d0.x * wc[0] + d0.y * wc[1] + d1.x * wc[2] + d1.y * wc[3] + dd.x * wc[4] + dd.y * wc[5];
             }
             if (on) {
                 mcur[i] = m;
@@ -626,9 +664,52 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 l_r += rv * rv;
             }
         }
-        cta_push3(cl, sc, par, rank, csize, l_g, l_d, l_r); // includes __syncthreads
-        cluster_arrive();
-        // local-column half of n = A m while the barrier completes
+        mark(0);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            l_g += __shfl_xor_sync(0xffffffffu, l_g, off);
+            l_d += __shfl_xor_sync(0xffffffffu, l_d, off);
+            l_r += __shfl_xor_sync(0xffffffffu, l_r, off);
+        }
+        if (lane == 0) {
+            sc.red[warp][0] = l_g;
+            sc.red[warp][1] = l_d;
+            sc.red[warp][2] = l_r;
+        }
+        __syncthreads(); // red[] and this CTA's m complete
+        if (warp == 0 && lane < csize) {
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll
+            for (int w = 0; w < kCW; ++w) { // fixed order
+                t0 += sc.red[w][0];
+                t1 += sc.red[w][1];
+                t2 += sc.red[w][2];
+            }
+            if (push) {
+                const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), lane);
+                const unsigned pbar = mapa(bar, lane);
+                st_async2(dst, t0, t1, pbar);
+                st_async2(dst + 16, t2, 0.0, pbar);
+            } else {
+                double* d = &cl.map_shared_rank(&sc, lane)->tab[par][rank][0];
+                d[0] = t0;
+                d[1] = t1;
+                d[2] = t2;
+            }
+        }
+        if (push) { // the m rows the peers' blocks need, into their halo slots
+            for (int e = threadIdx.x; e < 3 * n_send; e += kCT) {
+                const SendEntry se = sends[e / 3];
+                const int h = e % 3, peer = se.dest >> 20, j = se.dest & 0xfffff;
+                const double2 v = reinterpret_cast<const double2*>(mcur + 6 * se.row)[h];
+                st_async2(mapa(smem_u32(halo + 6 * (par * cap_blocks + j) + 2 * h), peer), v.x, v.y,
+                          mapa(bar, peer));
+            }
+        } else {
+            cluster_arrive();
+        }
+        mark(1);
+        // local-column half of n = A m while the messages fly
         // (the first two row groups of the warp; more only when nr > 160)
         double nloc0 = 0.0, nloc1 = 0.0;
         {
@@ -636,28 +717,40 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             if (lane < 30 && lr0 < nr) nloc0 = spmv_local(lr0, mcur);
             if (lane < 30 && lr1 < nr) nloc1 = spmv_local(lr1, mcur);
         }
-        cluster_wait();
-        const double3 f = fold3(sc, par, csize);
-        const double gamma = f.x, delta = f.y, rr = f.z;
+        mark(3);
+        if (push)
+            mbar_wait(bar, (it >> 1) & 1);
+        else
+            cluster_wait();
+        mark(4);
+        double gamma = 0.0, delta = 0.0, rr = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) { // rank order; slots past csize stay zero
+            const double2 gd = *reinterpret_cast<const double2*>(&sc.tab[par][k][0]);
+            gamma += gd.x;
+            delta += gd.y;
+            rr += sc.tab[par][k][2];
+        }
         if (it == 0) bnorm2 = rr;
         if (bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters) break;
-        double alpha, beta;
-        if (it == 0) {
-            beta = 0.0;
-            alpha = gamma / delta;
-        } else {
-            beta = gamma / gamma_old;
-            alpha = gamma / (delta - beta * gamma / alpha_old);
-        }
+        // beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
+        // with the previous iteration's reciprocals: one division on the
+        // critical path
+        const double beta = gamma * inv_gamma_old;
+        const double alpha = gamma / (delta - beta * gamma * inv_alpha_old);
         if (!(alpha > 0.0) || !isfinite(alpha)) break; // breakdown (uniform)
+        mark(5);
+        inv_gamma_old = 1.0 / gamma; // not needed until the next iteration
+        inv_alpha_old = 1.0 / alpha;
         // ---- remote half of n, then the recurrences
+        const double* hv = push ? halo + 6 * par * cap_blocks : nullptr;
         {
             int k = 0;
             for (int base = warp * kRowsPerWarp; base < nr; base += row_step, ++k) {
                 const int lr = base + slot;
                 if (lane < 30 && lr < nr) {
                     const double n0 = k == 0 ? nloc0 : k == 1 ? nloc1 : spmv_local(lr, mcur);
-                    const double n = spmv_remote(lr, moff, n0);
+                    const double n = spmv_remote(lr, hv, moff, n0);
                     const int i = 6 * lr + comp;
                     const double z = n + beta * vz[i];
                     const double q = mcur[i] + beta * vq[i];
@@ -674,9 +767,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 }
             }
         }
-        gamma_old = gamma;
-        alpha_old = alpha;
+        mark(6);
         ++it;
+        if (push) __syncthreads(); // mcur is rewritten by other warps next iteration
+    }
+    if (timed) {
+        ph[7] = it;
+        for (int k = 0; k < 8; ++k) atomicAdd(&sv.perf->phase[k], ph[k]);
     }
     for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
         const int lr = base + slot;
@@ -686,7 +783,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         sv.ps[p].pcg_iters = it;
         sv.ps[p].pcg_done = 1;
     }
-    cluster_barrier(); // no CTA leaves while a peer may still read its shared memory
+    cluster_barrier(); // no CTA leaves while a peer may still touch its shared memory
     if (sv.perf && threadIdx.x == 0) {
         if (rank == 0) { // algorithmic bytes of this partition's solve
             int nblk = 0;

@@ -49,6 +49,9 @@ struct DevPerf {
     unsigned long long launches;
     double bytes;
     unsigned long long iters;
+    // clock64 cycles of CTA 0 / warp 0 per PCG phase, summed over iterations
+    // (see k_pcg_cluster; dabd_gpu_ctx_pcg_phases)
+    unsigned long long phase[8];
 };
 
 struct SolverView {

@@ -35,3 +35,17 @@ for k in (1, 2, 5, 10, 20, 40, 80):
     if n:
         print(f"max_iters {k:3d}: launches {n:4d} avg {ns / n / 1e3:8.2f} us  iters/launch {it / n:6.1f}  "
               f"us/iter {ns / max(it, 1) / 1e3:6.2f}", flush=True)
+
+# per-phase cycles of CTA 0 / warp 0 (dabd_gpu_ctx_pcg_phases)
+ctx.set_solver(1e-10, 4000)
+ctx.set_state(q, qd)
+perf(True)
+ctx.run_frames(2)
+ph = (C.c_double * 8)()
+L.check(lib.dabd_gpu_ctx_pcg_phases(ctx.h, 1, ph))
+names = ["local m,partials", "cta reduce+push", "arrive", "local spmv", "wait", "fold+scalars",
+         "remote spmv+update", "(loop top)"]
+iters = max(ph[7], 1)
+print(f"phases over {int(ph[7])} iterations (cycles/iteration):")
+for k in range(7):
+    print(f"  {names[k]:22s} {ph[k] / iters:8.1f}")
