@@ -239,6 +239,12 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_pcg_perf(dabd_gpu_ctx* ctx, int reset,
  * [3] local-column SpMV, [4] barrier wait, [5] fold + scalars, [6] remote
  * SpMV + recurrences, [7] iterations counted. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_pcg_phases(dabd_gpu_ctx* ctx, int reset, double* cycles);
+/* Skin-list counters of the local solve (no reference counterpart; the
+ * reference runs a fresh broad phase per detect, geometry.cpp:161-208):
+ * rebuilds since the context's instance set was last (re)built, the current
+ * list length (candidate superset) and the largest per-instance skin. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_list_stats(dabd_gpu_ctx* ctx, long long* rebuilds,
+                                                     int* length, double* delta);
 /* "name launches total_ms;" per timed kernel ("*" times every kernel). */
 DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_report(char* buf, int capacity);
 DABD_GPU_API dabd_gpu_status dabd_gpu_kernel_timer_read(double* total_ms, long long* launches,

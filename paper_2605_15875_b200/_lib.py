@@ -66,6 +66,7 @@ EXPORTS = [
     "dabd_gpu_get_rho", "dabd_gpu_take_trace", "dabd_gpu_launch_count",
     "dabd_gpu_kernel_timer_enable", "dabd_gpu_kernel_timer_read", "dabd_gpu_kernel_timer_report",
     "dabd_gpu_ctx_pcg_perf", "dabd_gpu_ctx_set_comm", "dabd_gpu_ctx_pcg_phases",
+    "dabd_gpu_ctx_list_stats",
 ]
 
 _lib = None

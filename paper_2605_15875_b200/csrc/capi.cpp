@@ -407,6 +407,15 @@ dabd_gpu_status dabd_gpu_ctx_pcg_phases(dabd_gpu_ctx* ctx, int reset, double* cy
     });
 }
 
+dabd_gpu_status dabd_gpu_ctx_list_stats(dabd_gpu_ctx* ctx, long long* rebuilds, int* length,
+                                       double* delta) {
+    if (!ctx || !rebuilds || !length || !delta) return null_arg();
+    return guarded([&] {
+        ctx->e->list_stats(rebuilds, length, delta);
+        return DABD_GPU_OK;
+    });
+}
+
 dabd_gpu_status dabd_gpu_kernel_timer_report(char* buf, int capacity) {
     if (!buf || capacity < 1) return null_arg();
     const std::string r = dabd_gpu::KernelTimer::get().report();

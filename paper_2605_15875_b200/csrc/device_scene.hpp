@@ -76,6 +76,9 @@ struct InstView {
     const int* part = nullptr;
     const double* q0 = nullptr;
     const double* q1 = nullptr; // == q0 for a static (non-swept) query
+    // optional per-instance skin (skin-list build): body boxes grow by
+    // skin[i], point-edge tests by skin[P] + skin[E] on top of the margin
+    const double* skin = nullptr;
 };
 
 // Sorted candidate keys: a | b | v | e with the bit widths below.

@@ -91,9 +91,14 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     ctrl_h_.resize(1);
     perf_.resize(1);
     perf_.zero(s_);
+    lstate_.resize(1);
+    lstate_h_.resize(1);
+    invalidate_list();
     trace_dev_.resize(8 * static_cast<size_t>(trace_cap_));
     qd_start_.resize(6 * std::max(hs_.nb, 1));
     if (const char* e = std::getenv("DABD_GPU_NO_GRAPH")) use_graph_ = e[0] == '0';
+    if (const char* e = std::getenv("DABD_SKIN_MIN")) skin_min_ = std::atof(e);
+    if (const char* e = std::getenv("DABD_SKIN_GROW")) skin_grow_ = std::atof(e);
     sync();
 }
 
@@ -231,6 +236,7 @@ void Engine::build_instances(const std::vector<std::vector<int>>& per_part, cons
     n_rows_ = static_cast<int>(h_rinst_.size());
     if (n_inst_ >= (1 << 22)) throw InvalidArg("too many body instances for the candidate key");
     single_domain_ = single_domain;
+    invalidate_list();
     ref_ready_ = false; // the N=1 frame graph refers to the previous instance set
     graph_ok_ = false;
     ibody_.upload(h_ibody_, s_);
@@ -242,9 +248,9 @@ void Engine::build_instances(const std::vector<std::vector<int>>& per_part, cons
     pio_.upload(h_pio_, s_);
     pro_.upload(h_pro_, s_);
     const size_t I = std::max(n_inst_, 1), R = std::max(n_rows_, 1);
-    for (DBuf<double>* b : {&iq_, &iqtry_, &iqt_, &iz_, &iu_, &iznext_, &iqbefore_})
+    for (DBuf<double>* b : {&iq_, &iqtry_, &iqt_, &iz_, &iu_, &iznext_, &iqbefore_, &qref_})
         b->resize(6 * I);
-    for (DBuf<double>* b : {&iinvk_, &irho_, &irho0_, &rb_, &sb_}) b->resize(I);
+    for (DBuf<double>* b : {&iinvk_, &irho_, &irho0_, &rb_, &sb_, &iskin_, &iskin_next_}) b->resize(I);
     ianc_.resize(I);
     ianc_.zero(s_);
     iu_.zero(s_);
@@ -321,16 +327,20 @@ SolverView Engine::view() {
 
 ContactView Engine::cview() {
     ContactView c;
-    c.n = cap_;          // grid / buffer capacity
-    c.dn = nsel_.get();  // device-side active-contact count
+    c.n = cap_;              // list capacity
+    c.dn = det_.d_count();   // device-side list length
     c.fmt = cfmt_;
-    c.key = ckey_.get();
+    c.key = det_.keys();
     c.perm_b = perm_b_.get();
     c.aoff = aoff_.get();
     c.boff = boff_.get();
+    c.flag = cflag_.get();
+    c.act = act_.get();
+    c.ls = lstate_.get();
     c.cval = cval_.get();
     c.cgrad = cgrad_.get();
     c.cmat = cmat_.get();
+    c.cgeo = cgeo_.get();
     return c;
 }
 
@@ -366,13 +376,15 @@ void Engine::prepare_solver() {
         graph_ok_ = false;
     }
     const size_t C = static_cast<size_t>(cap_);
-    const size_t before = cflag_.capacity() + ckey_.capacity() + cmat_.capacity();
+    const size_t before = cflag_.capacity() + act_.capacity() + cmat_.capacity();
     cflag_.resize(C);
     sval_.resize(C);
-    ckey_.resize(C);
+    act_.resize(C);
     cval_.resize(C);
     cgrad_.resize(12 * C);
     cmat_.resize(21 * C);
+    cgeo_.resize(6 * C);
+    invalidate_list();
     bkey_.resize(C);
     bkey_sorted_.resize(C);
     bidx_.resize(C);
@@ -383,20 +395,65 @@ void Engine::prepare_solver() {
     (void)pcg_cluster_size(); // resolve cluster attributes before any graph capture
     box_.resize(std::max(n_inst_, 1));
     size_t t1 = 0, t2 = 0;
-    CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, t1, det_.keys(), cflag_.get(), ckey_.get(),
-                                          nsel_.get(), cap_));
     CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t2, bkey_.get(), bkey_sorted_.get(),
                                                bidx_.get(), perm_b_.get(), cap_, 0,
                                                det_.fmt().total_bits()));
     temp_bytes_ = std::max(t1, t2);
     temp_.resize(temp_bytes_);
-    if (cflag_.capacity() + ckey_.capacity() + cmat_.capacity() != before) graph_ok_ = false;
+    if (cflag_.capacity() + act_.capacity() + cmat_.capacity() != before) graph_ok_ = false;
     cfmt_ = det_.fmt();
 }
 
 void Engine::enq_superset(const double* q0, const double* q1, bool swept) {
     det_.enqueue(ds_.view(), iview(q0, q1), stat_.get(), static_cast<int>(h_stat_.size()), swept,
                  frame_params_.d_hat, err_.get(), s_);
+}
+
+void Engine::invalidate_list() {
+    ListState ls{};
+    ls.valid = 0;
+    CUDA_CHECK(cudaStreamSynchronize(s_)); // lstate_h_ doubles as the read-back buffer
+    lstate_h_[0] = ls;
+    rebuilds_seen_ = 0;
+    CUDA_CHECK(cudaMemcpyAsync(lstate_.get(), lstate_h_.get(), sizeof(ListState),
+                               cudaMemcpyHostToDevice, s_));
+    CUDA_CHECK(cudaStreamSynchronize(s_));
+}
+
+// Skin list rebuild at qref = iq with the margin k_list_check wrote
+// (d_hat + 2 delta): the detector's static broad phase, the a-segment
+// offsets, and the b-sorted permutation with its segment offsets.
+void Engine::enq_list_rebuild() {
+    launch_list_commit(n_inst_, iq_.get(), qref_.get(), iskin_next_.get(), iskin_.get(), s_);
+    InstView iv = iview(iq_.get(), iq_.get());
+    iv.skin = iskin_.get();
+    det_.enqueue(ds_.view(), iv, stat_.get(), static_cast<int>(h_stat_.size()), false,
+                 frame_params_.d_hat, err_.get(), s_);
+    launch_seg_offsets(det_.keys(), cap_, det_.d_count(), cfmt_, n_inst_, aoff_.get(), 0, nullptr, s_);
+    launch_make_bkeys(det_.keys(), cap_, det_.d_count(), cfmt_, bkey_.get(), bidx_.get(), s_);
+    size_t tb = temp_bytes_;
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp_.get(), tb, bkey_.get(), bkey_sorted_.get(),
+                                               bidx_.get(), perm_b_.get(), cap_, 0,
+                                               cfmt_.total_bits(), s_));
+    launch_seg_offsets(det_.keys(), cap_, det_.d_count(), cfmt_, n_inst_, boff_.get(), 1,
+                       perm_b_.get(), s_);
+}
+
+// The list must cover iq and q1 (the CCD end point; the trials lie between).
+void Engine::enq_list_ensure(const double* q1) {
+    const bool graph = hd_.graph != 0;
+    const unsigned long long h = graph ? new_cond_handle() : 0ull;
+    launch_list_check(ds_.view(), iview(iq_.get(), q1), qref_.get(), iqt_.get(), iskin_.get(),
+                      iskin_next_.get(), skin_min_ * frame_params_.d_hat, skin_grow_,
+                      lstate_.get(), h, graph ? 1 : 0, s_);
+    if (graph) {
+        add_cond_node(h, false, cap_level_ + 1, [&] { enq_list_rebuild(); }, false);
+    } else {
+        CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState),
+                                   cudaMemcpyDeviceToHost, s_));
+        CUDA_CHECK(cudaStreamSynchronize(s_));
+        if (lstate_h_[0].rebuild) enq_list_rebuild();
+    }
 }
 
 void Engine::enq_energy(const double* q, int which, double PartState::*field) {
@@ -414,24 +471,12 @@ void Engine::enq_energy(const double* q, int which, double PartState::*field) {
 
 void Engine::enq_derivatives() {
     SolverView v = view();
+    const ContactView cv = cview();
     launch_inst_boxes(v.sc, iview(iq_.get(), iq_.get()), false, frame_params_.d_hat, box_.get(),
                       cellmax_.get(), s_);
-    launch_body_terms(v, iq_.get(), true, 0, s_);
-    launch_filter(v, det_.keys(), cap_, det_.d_count(), cfmt_, box_.get(), iq_.get(), 0, 0,
-                  cflag_.get(), nullptr, s_);
-    size_t tb = temp_bytes_;
-    CUDA_CHECK(cub::DeviceSelect::Flagged(temp_.get(), tb, det_.keys(), cflag_.get(), ckey_.get(),
-                                          nsel_.get(), cap_, s_));
-    const ContactView cv = cview();
+    launch_body_terms(v, iq_.get(), true, 0, s_, &lstate_.get()->n_act);
+    launch_contact_select(v, cv, box_.get(), s_);
     launch_contact_terms(v, cv, s_);
-    launch_make_bkeys(ckey_.get(), cap_, nsel_.get(), cfmt_, bkey_.get(), bidx_.get(), s_);
-    tb = temp_bytes_;
-    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(temp_.get(), tb, bkey_.get(), bkey_sorted_.get(),
-                                               bidx_.get(), perm_b_.get(), cap_, 0,
-                                               cfmt_.total_bits(), s_));
-    launch_seg_offsets(ckey_.get(), cap_, nsel_.get(), cfmt_, n_inst_, aoff_.get(), 0, nullptr, s_);
-    launch_seg_offsets(ckey_.get(), cap_, nsel_.get(), cfmt_, n_inst_, boff_.get(), 1,
-                       perm_b_.get(), s_);
     launch_assemble(v, cv, rowtmp_.get(), s_);
     launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
                        ps_field(ps_.get(), &PartState::trace), kPsStride, false, s_);
@@ -466,7 +511,7 @@ void Engine::enq_newton_head(int max_iters) {
 void Engine::enq_newton_ccd() {
     SolverView v = view();
     launch_make_trial(v, false, 1.0, 0, s_);
-    enq_superset(iq_.get(), iqtry_.get(), true);
+    enq_list_ensure(iqtry_.get());
     launch_inst_boxes(v.sc, iview(iq_.get(), iqtry_.get()), true, 0.0, box_.get(), cellmax_.get(),
                       s_);
     launch_ccd(v, det_.keys(), cap_, det_.d_count(), cfmt_, box_.get(), iq_.get(), iqtry_.get(), 0,
@@ -485,7 +530,7 @@ void Engine::enq_ls_trial() {
 
 void Engine::enq_solve_begin(double tol) {
     launch_scalar(ps_.get(), P_, kOpReset, ctrl_.get(), hd_, tol, 0, err_.get(), s_);
-    enq_superset(iq_.get(), iq_.get(), false);
+    enq_list_ensure(iq_.get());
     enq_energy(iq_.get(), 0, &PartState::energy);
 }
 
@@ -528,7 +573,7 @@ NewtonResult Engine::newton_batch(int max_iters, double tol, bool reset_ctrl) {
         res.final_update = std::max(res.final_update, ps_h_[p].final_update);
     }
     res.pcg_iters = c.pcg_total;
-    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, nsel_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, &lstate_.get()->n_act, sizeof(int), cudaMemcpyDeviceToHost, s_));
     CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 3, det_.d_count(), sizeof(int), cudaMemcpyDeviceToHost, s_));
     sync();
     n_contacts_ = pin_i_[2];
@@ -551,7 +596,7 @@ unsigned long long Engine::new_cond_handle() {
 }
 
 void Engine::add_cond_node(unsigned long long h, bool is_while, int level,
-                           const std::function<void()>& body) {
+                           const std::function<void()>& body, bool account) {
     cudaStreamCaptureStatus st;
     cudaGraph_t g;
     const cudaGraphNode_t* deps = nullptr;
@@ -567,15 +612,24 @@ void Engine::add_cond_node(unsigned long long h, bool is_while, int level,
     CUDA_CHECK(cudaStreamUpdateCaptureDependencies(s_, &node, 1, cudaStreamSetCaptureDependencies));
     cudaGraph_t bg = p.conditional.phGraph_out[0];
     cudaStream_t saved = s_;
+    const int saved_level = cap_level_;
     s_ = cap_stream(level);
+    cap_level_ = level;
     CUDA_CHECK(cudaStreamBeginCaptureToGraph(s_, bg, nullptr, nullptr, 0,
                                              cudaStreamCaptureModeRelaxed));
     const long long before = launch_counter().load();
     body();
-    if (level < 8) nodes_inc_[level] = launch_counter().load() - before;
+    const long long inc = launch_counter().load() - before;
+    if (account) {
+        if (level < 8) nodes_inc_[level] = inc;
+    } else { // list rebuild: counted per executed rebuild, not per enclosing body
+        rebuild_nodes_ = inc;
+        launch_counter() -= inc;
+    }
     cudaGraph_t out;
     CUDA_CHECK(cudaStreamEndCapture(s_, &out));
     s_ = saved;
+    cap_level_ = saved_level;
 }
 
 cudaStream_t Engine::cap_stream(int level) {
@@ -789,13 +843,13 @@ void Engine::objective(const ObjectiveIn& in, const double* q, int mode, double*
     hd_ = CondHandles{};
     CUDA_CHECK(cudaMemsetAsync(ctrl_.get(), 0, sizeof(FrameCtrl), s_));
     launch_scalar(ps_.get(), P_, kOpReset, ctrl_.get(), hd_, 0.0, 0, err_.get(), s_);
-    enq_superset(iq_.get(), iq_.get(), false);
+    enq_list_ensure(iq_.get());
     if (mode <= 1) {
         enq_energy(iq_.get(), 2, &PartState::energy);
         enq_derivatives(); // counts only
         CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
                                    cudaMemcpyDeviceToHost, s_));
-        CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, nsel_.get(), sizeof(int),
+        CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, &lstate_.get()->n_act, sizeof(int),
                                    cudaMemcpyDeviceToHost, s_));
         sync();
         *value = ps_h_[0].energy;
@@ -809,15 +863,16 @@ void Engine::objective(const ObjectiveIn& in, const double* q, int mode, double*
     project_ = 1;
     CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
                                cudaMemcpyDeviceToHost, s_));
-    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, nsel_.get(), sizeof(int), cudaMemcpyDeviceToHost,
-                               s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, &lstate_.get()->n_act, sizeof(int),
+                               cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 3, det_.d_count(), sizeof(int), cudaMemcpyDeviceToHost, s_));
     std::vector<double> rv = rval_.to_host(s_);
     std::vector<double> cv = cval_.to_host(s_);
     sync();
     n_contacts_ = pin_i_[2];
     double val = 0.0;
     for (int r = 0; r < n_rows_; ++r) val += rv[r];
-    for (int c = 0; c < n_contacts_; ++c) val += cv[c];
+    for (int c = 0; c < std::min(pin_i_[3], cap_); ++c) val += cv[c]; // 0 off the active set
     *value = val;
     *active = n_contacts_;
     *candidates = ps_h_[0].n_candidates;
@@ -1010,6 +1065,8 @@ FrameStats Engine::frame_reference() {
         CUDA_CHECK(cudaMemcpyAsync(ctrl_h_.get(), ctrl_.get(), sizeof(FrameCtrl),
                                    cudaMemcpyDeviceToHost, s_));
         CUDA_CHECK(cudaMemcpyAsync(pin_i_.get(), err_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+        CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState),
+                                   cudaMemcpyDeviceToHost, s_));
         CUDA_CHECK(cudaStreamSynchronize(s_));
         if (pin_i_[0] == kErrCapacity) {
             // grow the fixed capacities, restore the frame start and redo it
@@ -1030,13 +1087,15 @@ FrameStats Engine::frame_reference() {
     }
     const FrameCtrl& c = ctrl_h_[0];
     if (graph_replayed_) { // kernels the replay executed: nodes per body x body executions
-        count_launch(nodes_total_ - nodes_inc_[0] +
+        const long long rebuilds = lstate_h_[0].n_rebuilds - rebuilds_seen_;
+        count_launch(rebuilds * rebuild_nodes_ + nodes_total_ - nodes_inc_[0] +
                      static_cast<long long>(c.exec_admm) * (nodes_inc_[0] - nodes_inc_[1]) +
                      static_cast<long long>(c.exec_newton) * (nodes_inc_[1] - nodes_inc_[2]) +
                      static_cast<long long>(c.exec_step) * (nodes_inc_[2] - nodes_inc_[3]) +
                      static_cast<long long>(c.exec_ls) * nodes_inc_[3]);
         graph_replayed_ = false;
     }
+    rebuilds_seen_ = lstate_h_[0].n_rebuilds;
     if (c.failed || !c.ended) throw Error("run_reference: Newton stepping failed to settle");
     st.admm_iterations = c.admm_iterations;
     st.newton_iterations = c.newton_total;
@@ -1051,7 +1110,7 @@ FrameStats Engine::frame_reference() {
             trace_.push_back({rows[8 * i], rows[8 * i + 1], rows[8 * i + 2], rows[8 * i + 3],
                               rows[8 * i + 4], rows[8 * i + 5], rows[8 * i + 6], rows[8 * i + 7]});
     }
-    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, nsel_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, &lstate_.get()->n_act, sizeof(int), cudaMemcpyDeviceToHost, s_));
     CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 3, det_.d_count(), sizeof(int), cudaMemcpyDeviceToHost, s_));
     sync();
     st.max_contacts = pin_i_[2];
@@ -1307,6 +1366,19 @@ FrameStats Engine::frame_admm(int frame) {
 } // namespace dabd_gpu
 
 namespace dabd_gpu {
+
+void Engine::list_stats(long long* rebuilds, int* length, double* delta) {
+    CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState),
+                               cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 4, det_.d_count(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    sync();
+    *rebuilds = lstate_h_[0].n_rebuilds;
+    *length = pin_i_[4];
+    std::vector<double> sk = iskin_.to_host(s_);
+    double m = 0.0;
+    for (int i = 0; i < n_inst_; ++i) m = std::max(m, sk[i]);
+    *delta = m;
+}
 
 DevPerf Engine::read_perf(bool reset) {
     DevPerf h{};

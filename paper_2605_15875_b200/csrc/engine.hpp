@@ -93,6 +93,7 @@ class Engine {
     std::vector<TraceRow> take_trace();
     // PCG launch accounting since the last reset (device %globaltimer, SURVEY 8(d) bytes).
     DevPerf read_perf(bool reset);
+    void list_stats(long long* rebuilds, int* length, double* delta);
 
   private:
     // instance sets ----------------------------------------------------------
@@ -108,6 +109,9 @@ class Engine {
     // local solve (enqueue-only, capturable) -----------------------------------
     void prepare_solver();
     void enq_superset(const double* q0, const double* q1, bool swept);
+    void enq_list_ensure(const double* q1);
+    void enq_list_rebuild();
+    void invalidate_list();
     void enq_energy(const double* q, int which, double PartState::*field);
     void enq_derivatives();
     void enq_pcg();
@@ -122,7 +126,7 @@ class Engine {
     // CUDA graphs with conditional nodes -------------------------------------
     unsigned long long new_cond_handle();
     void add_cond_node(unsigned long long h, bool is_while, int level,
-                       const std::function<void()>& body);
+                       const std::function<void()>& body, bool account = true);
     cudaStream_t cap_stream(int level);
     void cap_newton(int max_iters, double tol, int level);
     void enq_reference_frame(bool graph);
@@ -177,7 +181,17 @@ class Engine {
     DBuf<double> sval_;
     DBuf<unsigned long long> ckey_, bkey_, bkey_sorted_;
     DBuf<int> bidx_, perm_b_, aoff_, boff_, nsel_;
-    DBuf<double> cval_, cgrad_, cmat_;
+    DBuf<double> cval_, cgrad_, cmat_, cgeo_;
+    DBuf<int> act_;
+    // skin list (ListState in solver.hpp): det_ holds the list keys
+    DBuf<double> qref_, iskin_, iskin_next_;
+    double skin_min_ = 0.5;  // x d_hat
+    double skin_grow_ = 1.5;
+    DBuf<ListState> lstate_;
+    PinnedBuf<ListState> lstate_h_;
+    long long rebuild_nodes_ = 0; // kernels in one captured rebuild body
+    long long rebuilds_seen_ = 0; // ListState::n_rebuilds at the last frame end
+    int cap_level_ = -1;          // capture level of s_ while capturing (-1: top)
     DBuf<unsigned char> temp_;
     int n_contacts_ = 0;
     KeyFmt cfmt_;

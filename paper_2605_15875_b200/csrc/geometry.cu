@@ -13,9 +13,11 @@ namespace {
 
 constexpr int kBlock = 128;
 
-__global__ void k_inst_boxes(SceneView sc, InstView iv, int swept, double margin, Box* box,
-                             double* cell_max) {
+__global__ void k_inst_boxes(SceneView sc, InstView iv, int swept, double margin,
+                             const double* dmargin, Box* box, double* cell_max) {
+    if (dmargin) margin = *dmargin;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < iv.n; i += gridDim.x * blockDim.x) {
+        const double mi = iv.skin ? margin + iv.skin[i] : margin;
         const int b = iv.body[i];
         const double* qa = iv.q0 + 6 * i;
         const double* qb = iv.q1 + 6 * i;
@@ -33,7 +35,7 @@ __global__ void k_inst_boxes(SceneView sc, InstView iv, int swept, double margin
             }
         }
         if (swept) bx = merge(bx, by);
-        bx = inflate(bx, margin);
+        bx = inflate(bx, mi);
         box[i] = bx;
         if (!sc.is_static[b]) {
             const double ext = fmax(bx.hi.x - bx.lo.x, bx.hi.y - bx.lo.y);
@@ -94,6 +96,7 @@ __device__ int emit_dir(const SceneView& sc, const InstView& iv, bool swept, dou
     const double* qb1 = iv.q1 + 6 * B;
     const int va0 = sc.vstart[ba], nva = sc.vstart[ba + 1] - va0;
     const int eb0 = sc.vstart[bb], neb = sc.vstart[bb + 1] - eb0;
+    if (iv.skin) margin = (margin + iv.skin[A]) + iv.skin[B];
     int cnt = 0;
     for (int e = 0; e < neb; ++e) {
         const Box eb = edge_box(sc, qb0, qb1, swept, eb0 + e, margin);
@@ -130,6 +133,7 @@ __device__ __forceinline__ bool combo_test(const SceneView& sc, const InstView& 
         ne = na;
     }
     const int v = c / ne, e = c - v * ne;
+    if (iv.skin) margin = (margin + iv.skin[P]) + iv.skin[E];
     const Box pb = point_box(sc, iv.q0 + 6 * P, iv.q1 + 6 * P, swept, pv0 + v);
     const Box eb = edge_box(sc, iv.q0 + 6 * E, iv.q1 + 6 * E, swept, ev0 + e, margin);
     if (!overlaps(pb, eb)) return false;
@@ -140,8 +144,9 @@ __device__ __forceinline__ bool combo_test(const SceneView& sc, const InstView& 
 __global__ void __launch_bounds__(kEmitWarps * 32)
     k_emit_warp(SceneView sc, InstView iv, const Box* box, const double* cell_max, unsigned mask,
                 const int* hstart, const int* hcount, const int* items, const int* stat,
-                int n_stat, int swept, double margin, KeyFmt fmt, unsigned long long* out, int cap,
-                int* counter, int* err) {
+                int n_stat, int swept, double margin, const double* dmargin, KeyFmt fmt,
+                unsigned long long* out, int cap, int* counter, int* err) {
+    if (dmargin) margin = *dmargin;
     __shared__ int partners[kEmitWarps][kMaxPartners];
     __shared__ int npart[kEmitWarps];
     __shared__ int wtot[kEmitWarps];
@@ -240,8 +245,10 @@ __global__ void __launch_bounds__(kEmitWarps * 32)
 }
 
 __global__ void k_emit_static_pairs(SceneView sc, InstView iv, const Box* box, const int* stat,
-                                    int n_stat, int swept, double margin, KeyFmt fmt,
-                                    unsigned long long* out, int cap, int* counter, int* err) {
+                                    int n_stat, int swept, double margin, const double* dmargin,
+                                    KeyFmt fmt, unsigned long long* out, int cap, int* counter,
+                                    int* err) {
+    if (dmargin) margin = *dmargin;
     const long long np = static_cast<long long>(n_stat) * n_stat;
     for (long long t = blockIdx.x * blockDim.x + threadIdx.x; t < np;
          t += gridDim.x * blockDim.x) {
@@ -285,10 +292,10 @@ void launch_narrow_bodies(const SceneView& sc, const double* q, const int* cand,
 }
 
 void launch_inst_boxes(const SceneView& sc, const InstView& iv, bool swept, double margin, Box* box,
-                       double* cell_max, cudaStream_t s) {
+                       double* cell_max, cudaStream_t s, const double* dmargin) {
     if (iv.n == 0) return;
-    DABD_LAUNCH("k_inst_boxes", s, k_inst_boxes<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(sc, iv, swept ? 1 : 0, margin, box,
-                                                          cell_max));
+    DABD_LAUNCH("k_inst_boxes", s, k_inst_boxes<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(sc, iv, swept ? 1 : 0, margin,
+                                                          dmargin, box, cell_max));
 }
 
 Detector::Detector() {
@@ -326,12 +333,12 @@ void Detector::prepare(int n_inst, int max_verts, int cap) {
 }
 
 void Detector::enqueue(const SceneView& sc, const InstView& iv, const int* stat, int n_stat,
-                       bool swept, double margin, int* err, cudaStream_t s) {
+                       bool swept, double margin, int* err, cudaStream_t s, const double* dmargin) {
     CUDA_CHECK(cudaMemsetAsync(counter_.get(), 0, 2 * sizeof(int), s));
     CUDA_CHECK(cudaMemsetAsync(keys_sorted_.get(), 0xFF, sizeof(unsigned long long) * cap_, s));
     if (iv.n == 0) return;
     CUDA_CHECK(cudaMemsetAsync(cell_.get(), 0, sizeof(double), s));
-    launch_inst_boxes(sc, iv, swept, margin, box_.get(), cell_.get(), s);
+    launch_inst_boxes(sc, iv, swept, margin, box_.get(), cell_.get(), s, dmargin);
     CUDA_CHECK(cudaMemsetAsync(hcount_.get(), 0, sizeof(int) * tsize_, s));
     DABD_LAUNCH("k_hash_count", s,
                 k_hash_count<<<grid_for(iv.n, kBlock), kBlock, 0, s>>>(
@@ -347,13 +354,13 @@ void Detector::enqueue(const SceneView& sc, const InstView& iv, const int* stat,
     DABD_LAUNCH("k_emit", s,
                 k_emit_warp<<<grid_for(iv.n, kEmitWarps, 148 * 64), kEmitWarps * 32, 0, s>>>(
                     sc, iv, box_.get(), cell_.get(), tsize_ - 1, hstart_.get(), hcount_.get(),
-                    hitems_.get(), stat, n_stat, swept ? 1 : 0, margin, fmt_, keys_.get(), cap_,
+                    hitems_.get(), stat, n_stat, swept ? 1 : 0, margin, dmargin, fmt_, keys_.get(), cap_,
                     counter_.get(), err));
     if (n_stat > 1) {
         const int gs = grid_for(static_cast<long long>(n_stat) * n_stat, kBlock);
         DABD_LAUNCH("k_emit_static_pairs", s,
                     k_emit_static_pairs<<<gs, kBlock, 0, s>>>(sc, iv, box_.get(), stat, n_stat,
-                                                              swept ? 1 : 0, margin, fmt_,
+                                                              swept ? 1 : 0, margin, dmargin, fmt_,
                                                               keys_.get(), cap_, counter_.get(),
                                                               err));
     }

@@ -134,8 +134,10 @@ class Detector {
     // Graph-safe variant: fixed capacity, no host reads. Keys past the count
     // are ~0ull (sorted to the end); overflow raises kErrCapacity in `err`.
     void prepare(int n_inst, int max_verts, int cap);
+    // `dmargin` (device, optional) overrides `margin` at run time, so a
+    // captured graph can rebuild with a margin computed on the device.
     void enqueue(const SceneView& sc, const InstView& iv, const int* stat, int n_stat, bool swept,
-                 double margin, int* err, cudaStream_t s);
+                 double margin, int* err, cudaStream_t s, const double* dmargin = nullptr);
     const int* d_count() const { return counter_.get(); }
     int cap() const { return cap_; }
     const unsigned long long* keys() const { return keys_sorted_.get(); }
@@ -163,6 +165,6 @@ void launch_narrow_bodies(const SceneView& sc, const double* q, const int* cand,
 
 // Per-instance boxes (body_aabb, optionally swept, inflated by margin).
 void launch_inst_boxes(const SceneView& sc, const InstView& iv, bool swept, double margin, Box* box,
-                       double* cell_max, cudaStream_t s);
+                       double* cell_max, cudaStream_t s, const double* dmargin = nullptr);
 
 } // namespace dabd_gpu

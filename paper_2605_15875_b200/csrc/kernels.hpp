@@ -14,11 +14,19 @@ namespace dabd_gpu {
 // which: 0 = partitions with an active Newton, 1 = partitions in a line
 // search, 2 = every partition.
 void launch_body_terms(const SolverView& sv, const double* q, bool derivs, int which,
-                       cudaStream_t s);
+                       cudaStream_t s, int* reset_counter = nullptr);
 void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
                    KeyFmt fmt, const Box* box, const double* q, int mode, int which,
                    unsigned char* flag, double* val, cudaStream_t s);
 void launch_contact_terms(const SolverView& sv, const ContactView& cv, cudaStream_t s);
+void launch_contact_select(const SolverView& sv, const ContactView& cv, const Box* box,
+                           cudaStream_t s);
+void launch_list_check(const SceneView& sc, const InstView& iv, const double* qref,
+                       const double* qt, const double* skin, double* skin_next, double s_min,
+                       double grow, ListState* ls, unsigned long long cond, int graph,
+                       cudaStream_t s);
+void launch_list_commit(int n, const double* iq, double* qref, const double* skin_next,
+                        double* skin, cudaStream_t s);
 void launch_seg_offsets(const unsigned long long* keys, int n, const int* dn, KeyFmt fmt,
                         int n_inst, int* off, int field, const int* perm, cudaStream_t s);
 void launch_make_bkeys(const unsigned long long* keys, int n, const int* dn, KeyFmt fmt,

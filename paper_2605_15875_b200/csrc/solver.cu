@@ -42,7 +42,9 @@ __device__ __forceinline__ bool part_flag(const SolverView& sv, int p, int which
 // Body terms: value (+ gradient + PSD-clamped 6x6 block) per dynamic row
 // (objective.cpp:117-141, 143-167).
 // ---------------------------------------------------------------------------
-__global__ void k_body_terms(SolverView sv, const double* qsrc, int with_derivs, int which) {
+__global__ void k_body_terms(SolverView sv, const double* qsrc, int with_derivs, int which,
+                             int* reset_counter) {
+    if (reset_counter && blockIdx.x == 0 && threadIdx.x == 0) *reset_counter = 0;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
         const int p = sv.rpart[r] - sv.part_base;
         if (!part_flag(sv, p, which)) continue;
@@ -185,8 +187,9 @@ __global__ void k_filter(SolverView sv, const unsigned long long* keys, int n, c
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kB)
     k_contact_terms(SolverView sv, ContactView cv) {
-    const int nc = cv.dn ? min(*cv.dn, cv.n) : cv.n;
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+    const int nc = min(cv.ls->n_act, cv.n);
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+        const int c = cv.act[k];
         int a, b, v, e;
         cv.fmt.unpack(cv.key[c], a, b, v, e);
         const int ba = sv.ibody[a], bb = sv.ibody[b];
@@ -195,6 +198,12 @@ __global__ void __launch_bounds__(kB)
         const double* qa = sv.iq + 6 * a;
         const double* qb = sv.iq + 6 * b;
         const V2 P = world_point(qa, rp), E0 = world_point(qb, r0), E1 = world_point(qb, r1);
+        {
+            double2* gg = reinterpret_cast<double2*>(cv.cgeo + 6 * c);
+            gg[0] = make_double2(rp.x, rp.y);
+            gg[1] = make_double2(r0.x, r0.y);
+            gg[2] = make_double2(r1.x, r1.y);
+        }
         double g[6], A[6][6];
         const double d = pe_distance_full(P, E0, E1, g, A);
         if (!(d > 0.0)) {
@@ -337,130 +346,168 @@ __global__ void k_make_bkeys(const unsigned long long* keys, int n, const int* d
 }
 
 // ---------------------------------------------------------------------------
-// Deterministic BSR assembly (ELL storage, kEll off-diagonal blocks / row).
+// Active-set selection over the skin list at the current iterate: the exact
+// static broad-phase predicate (margin d_hat) & not static-static & d < d_hat
+// (objective.cpp:91-106). Writes flag[t] for every list entry, appends the
+// active positions to cv.act (warp-aggregated; the order of `act` only
+// decides which thread evaluates which contact, never a result) and counts
+// candidates / active contacts per partition.
 // ---------------------------------------------------------------------------
-// M[gA[i]][gB[j]] += s * c2[al][be] * u[i] * w[j]   (J(u)^T c2 J(w))
-__device__ __forceinline__ void add_kron(double (&M)[6][6], double c00, double c01, double c10,
-                                         double c11, const double (&u)[3], const double (&w)[3],
-                                         bool transpose) {
-    const int gx[3] = {0, 2, 3}, gy[3] = {1, 4, 5};
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const double uw = u[i] * w[j];
-            if (!transpose) {
-                M[gx[i]][gx[j]] += c00 * uw;
-                M[gx[i]][gy[j]] += c01 * uw;
-                M[gy[i]][gx[j]] += c10 * uw;
-                M[gy[i]][gy[j]] += c11 * uw;
-            } else {
-                M[gx[j]][gx[i]] += c00 * uw;
-                M[gy[j]][gx[i]] += c01 * uw;
-                M[gx[j]][gy[i]] += c10 * uw;
-                M[gy[j]][gy[i]] += c11 * uw;
+__global__ void k_contact_select(SolverView sv, ContactView cv, const Box* box) {
+    const int nn = cv.dn ? min(*cv.dn, cv.n) : cv.n;
+    const int lane = threadIdx.x & 31;
+    const int span = (nn + 31) & ~31; // whole warps stay in the loop (ballots)
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < span; t += gridDim.x * blockDim.x) {
+        bool cand = false, act = false;
+        int p = -1;
+        if (t < nn) {
+            int a, b, v, e;
+            cv.fmt.unpack(cv.key[t], a, b, v, e);
+            p = sv.ipart[a] - sv.part_base;
+            if (sv.ps[p].active) {
+                const int ba = sv.ibody[a], bb = sv.ibody[b];
+                const bool ss = sv.sc.is_static[ba] && sv.sc.is_static[bb];
+                if (!ss && overlaps(box[a], box[b])) {
+                    const double* qa = sv.iq + 6 * a;
+                    const double* qb = sv.iq + 6 * b;
+                    const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
+                    const Box pb = point_box(sv.sc, qa, qa, false, vf);
+                    const Box eb = edge_box(sv.sc, qb, qb, false, ef, sv.d_hat);
+                    if (overlaps(pb, eb)) {
+                        cand = true;
+                        const V2 P = world_point(qa, rest_of(sv.sc, vf));
+                        const V2 E0 = world_point(qb, rest_of(sv.sc, ef));
+                        const V2 E1 = world_point(qb, rest_of(sv.sc, sv.sc.vnext[ef]));
+                        const double d = pe_distance(P, E0, E1);
+                        if (d < sv.d_hat) {
+                            if (d <= 0.0) raise(sv.err, d == -1.0 ? kErrDegenerateEdge : kErrBarrierDomain);
+                            act = true;
+                        }
+                    }
+                }
             }
+            cv.flag[t] = act ? 1 : 0;
+            if (!act) cv.cval[t] = 0.0;
         }
+        const unsigned ab = __ballot_sync(0xffffffffu, act);
+        const unsigned cb = __ballot_sync(0xffffffffu, cand);
+        int base = 0;
+        if (lane == 0 && ab) base = atomicAdd(&cv.ls->n_act, __popc(ab));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (act) cv.act[base + __popc(ab & ((1u << lane) - 1u))] = t;
+        // per-partition counts: one atomic per warp when the partition is warp-uniform
+        const int p0 = __shfl_sync(0xffffffffu, p, 0);
+        const bool uniform = __all_sync(0xffffffffu, p == p0 || p < 0);
+        if (uniform) {
+            if (lane == 0 && p0 >= 0) {
+                if (cb) atomicAdd(&sv.ps[p0].n_candidates, __popc(cb));
+                if (ab) atomicAdd(&sv.ps[p0].n_active_contacts, __popc(ab));
+            }
+        } else {
+            if (cand) atomicAdd(&sv.ps[p].n_candidates, 1);
+            if (act) atomicAdd(&sv.ps[p].n_active_contacts, 1);
+        }
+    }
 }
 
+// ---------------------------------------------------------------------------
+// Deterministic BSR assembly (ELL storage, kEll off-diagonal blocks / row):
+// one warp per row, lane l owns entries l and l + 32 of each 6x6 block.
+// The contact's projected world-space C (6x6 over (p, e0, e1)) is mapped to
+// DoF space on the fly: x = A xbar + p gives d(world)/d(q) = J(xbar) with
+// J = [[1, 0, x, y, 0, 0], [0, 1, 0, 0, x, y]], so
+//   TL = J(rp)^T C_pp J(rp), BR = sum_kl J(rk)^T C_kl J(rl),
+//   TR = sum_l J(rp)^T C_pl J(rl), BL = TR^T.
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ double cm_at(const double* cm, int i, int j) {
     if (i > j) {
         const int t = i;
         i = j;
         j = t;
     }
-    // upper-triangle row-major index
-    return cm[i * 6 - (i * (i - 1)) / 2 + (j - i)];
+    return cm[i * 6 - (i * (i - 1)) / 2 + (j - i)]; // upper-triangle row-major
 }
 
-struct ContactGeom {
-    double up[3], w0[3], w1[3];
-};
-
-__device__ __forceinline__ ContactGeom contact_geom(const SolverView& sv, int a, int b, int v,
-                                                    int e) {
-    const int ba = sv.ibody[a], bb = sv.ibody[b];
-    const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
-    const V2 rp = rest_of(sv.sc, vf), r0 = rest_of(sv.sc, ef), r1 = rest_of(sv.sc, sv.sc.vnext[ef]);
-    ContactGeom g;
-    g.up[0] = 1.0;
-    g.up[1] = rp.x;
-    g.up[2] = rp.y;
-    g.w0[0] = 1.0;
-    g.w0[1] = r0.x;
-    g.w0[2] = r0.y;
-    g.w1[0] = 1.0;
-    g.w1[1] = r1.x;
-    g.w1[2] = r1.y;
-    return g;
+// DoF alpha -> (world component, coefficient index into (1, x, y))
+__device__ __forceinline__ void dof_map(int alpha, int& comp, int& idx) {
+    // gx = {0, 2, 3} (x component), gy = {1, 4, 5} (y component)
+    comp = (alpha == 1 || alpha >= 4) ? 1 : 0;
+    idx = alpha <= 1 ? 0 : (alpha == 2 || alpha == 4 ? 1 : 2);
 }
 
-// point-body block (TL)
-__device__ __forceinline__ void add_tl(double (&M)[6][6], const double* cm, const ContactGeom& g) {
-    add_kron(M, cm_at(cm, 0, 0), cm_at(cm, 0, 1), cm_at(cm, 1, 0), cm_at(cm, 1, 1), g.up, g.up, false);
-}
-// edge-body block (BR)
-__device__ __forceinline__ void add_br(double (&M)[6][6], const double* cm, const ContactGeom& g) {
-    add_kron(M, cm_at(cm, 2, 2), cm_at(cm, 2, 3), cm_at(cm, 3, 2), cm_at(cm, 3, 3), g.w0, g.w0, false);
-    add_kron(M, cm_at(cm, 2, 4), cm_at(cm, 2, 5), cm_at(cm, 3, 4), cm_at(cm, 3, 5), g.w0, g.w1, false);
-    add_kron(M, cm_at(cm, 4, 2), cm_at(cm, 4, 3), cm_at(cm, 5, 2), cm_at(cm, 5, 3), g.w1, g.w0, false);
-    add_kron(M, cm_at(cm, 4, 4), cm_at(cm, 4, 5), cm_at(cm, 5, 4), cm_at(cm, 5, 5), g.w1, g.w1, false);
-}
-// coupling (point row, edge col) = TR; transpose gives BL
-__device__ __forceinline__ void add_tr(double (&M)[6][6], const double* cm, const ContactGeom& g,
-                                       bool transpose) {
-    add_kron(M, cm_at(cm, 0, 2), cm_at(cm, 0, 3), cm_at(cm, 1, 2), cm_at(cm, 1, 3), g.up, g.w0, transpose);
-    add_kron(M, cm_at(cm, 0, 4), cm_at(cm, 0, 5), cm_at(cm, 1, 4), cm_at(cm, 1, 5), g.up, g.w1, transpose);
+__device__ __forceinline__ double coef(const double* geo, int pt, int idx) {
+    return idx == 0 ? 1.0 : geo[2 * pt + idx - 1];
 }
 
-__global__ void k_assemble(SolverView sv, ContactView cv, double* row_trace) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
+// entry (alpha, beta) of the block of world points (pa -> rows, pb -> cols)
+// summed over the given point pairs; pt 0 = p, 1 = e0, 2 = e1.
+__device__ __forceinline__ double blk_entry(const double* cm, const double* geo, int ca, int ia,
+                                            int cb, int ib, int ra0, int ra1, int rb0, int rb1) {
+    double v = 0.0;
+    for (int ra = ra0; ra <= ra1; ++ra)
+        for (int rb = rb0; rb <= rb1; ++rb)
+            v += cm_at(cm, 2 * ra + ca, 2 * rb + cb) * (coef(geo, ra, ia) * coef(geo, rb, ib));
+    return v;
+}
+
+__global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv, double* row_trace) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    // the two entries of this lane
+    const int e0 = lane, e1 = lane + 32;
+    const bool has1 = e1 < 36;
+    int ca0, ia0, cb0, ib0, ca1 = 0, ia1 = 0, cb1 = 0, ib1 = 0;
+    dof_map(e0 / 6, ca0, ia0);
+    dof_map(e0 % 6, cb0, ib0);
+    if (has1) {
+        dof_map(e1 / 6, ca1, ia1);
+        dof_map(e1 % 6, cb1, ib1);
+    }
+    for (int r = gw; r < sv.n_rows; r += nw) {
         const int p = sv.rpart[r] - sv.part_base;
         if (!sv.ps[p].active) continue;
         const int i = sv.rinst[r];
-        double g[6];
-        load6(sv.rgrad + 6 * r, g);
-        double D[6][6];
-        const double* dsrc = sv.rdiag + 36 * r;
-#pragma unroll
-        for (int a = 0; a < 6; ++a)
-#pragma unroll
-            for (int c = 0; c < 6; ++c) D[a][c] = dsrc[6 * a + c];
+        double d0 = sv.rdiag[36 * r + e0];
+        double d1 = has1 ? sv.rdiag[36 * r + e1] : 0.0;
+        double g = lane < 6 ? sv.rgrad[6 * r + lane] : 0.0;
         const int a0 = cv.aoff[i], a1 = cv.aoff[i + 1];
         const int b0 = cv.boff[i], b1 = cv.boff[i + 1];
-        // diagonal + gradient
-        for (int c = a0; c < a1; ++c) {
-            int ca, cb, vv, ee;
-            cv.fmt.unpack(cv.key[c], ca, cb, vv, ee);
-            const ContactGeom geo = contact_geom(sv, ca, cb, vv, ee);
-            add_tl(D, cv.cmat + 21 * c, geo);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) g[k] += cv.cgrad[12 * c + k];
+        for (int c = a0; c < a1; ++c) { // point body: TL, gradient 0..5
+            if (!cv.flag[c]) continue;
+            const double* cm = cv.cmat + 21 * c;
+            const double* geo = cv.cgeo + 6 * c;
+            d0 += blk_entry(cm, geo, ca0, ia0, cb0, ib0, 0, 0, 0, 0);
+            if (has1) d1 += blk_entry(cm, geo, ca1, ia1, cb1, ib1, 0, 0, 0, 0);
+            if (lane < 6) g += cv.cgrad[12 * c + lane];
         }
-        for (int t = b0; t < b1; ++t) {
+        for (int t = b0; t < b1; ++t) { // edge body: BR, gradient 6..11
             const int c = cv.perm_b[t];
-            int ca, cb, vv, ee;
-            cv.fmt.unpack(cv.key[c], ca, cb, vv, ee);
-            const ContactGeom geo = contact_geom(sv, ca, cb, vv, ee);
-            add_br(D, cv.cmat + 21 * c, geo);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) g[k] += cv.cgrad[12 * c + 6 + k];
+            if (!cv.flag[c]) continue;
+            const double* cm = cv.cmat + 21 * c;
+            const double* geo = cv.cgeo + 6 * c;
+            d0 += blk_entry(cm, geo, ca0, ia0, cb0, ib0, 1, 2, 1, 2);
+            if (has1) d1 += blk_entry(cm, geo, ca1, ia1, cb1, ib1, 1, 2, 1, 2);
+            if (lane < 6) g += cv.cgrad[12 * c + 6 + lane];
         }
-        store6(sv.rgrad + 6 * r, g);
-        double tr = 0.0;
-        double* ddst = sv.rdiag + 36 * r;
+        if (lane < 6) sv.rgrad[6 * r + lane] = g;
+        sv.rdiag[36 * r + e0] = d0;
+        if (has1) sv.rdiag[36 * r + e1] = d1;
+        // trace: diagonal entries 0, 7, 14, 21, 28 (lanes) and 35 (lane 3, second entry)
+        double tr = (e0 % 7 == 0) ? d0 : 0.0;
+        if (lane == 3) tr += d1;
 #pragma unroll
-        for (int a = 0; a < 6; ++a) {
-            tr += D[a][a];
-#pragma unroll
-            for (int c = 0; c < 6; ++c) ddst[6 * a + c] = D[a][c];
-        }
-        row_trace[r] = tr;
-        // off-diagonal blocks: merge a-seg (sorted by b) and b-seg (sorted by a)
+        for (int off = 16; off > 0; off >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, off);
+        if (lane == 0) row_trace[r] = tr;
+        // off-diagonal blocks: merge the a-segment (sorted by b) and the
+        // b-segment (sorted by a) by partner instance, active contacts only
         int ia = a0, ib = b0, nblk = 0;
-        while (ia < a1 || ib < b1) {
-            int pa = 0x7fffffff, pb = 0x7fffffff;
+        while (true) {
+            while (ia < a1 && !cv.flag[ia]) ++ia;
+            while (ib < b1 && !cv.flag[cv.perm_b[ib]]) ++ib;
+            if (ia >= a1 && ib >= b1) break;
             int ca, cb, vv, ee;
+            int pa = 0x7fffffff, pb = 0x7fffffff;
             if (ia < a1) {
                 cv.fmt.unpack(cv.key[ia], ca, cb, vv, ee);
                 pa = cb;
@@ -471,38 +518,100 @@ __global__ void k_assemble(SolverView sv, ContactView cv, double* row_trace) {
             }
             const int partner = min(pa, pb);
             const int prow = sv.irow[partner];
-            double O[6][6];
-#pragma unroll
-            for (int x = 0; x < 6; ++x)
-#pragma unroll
-                for (int y = 0; y < 6; ++y) O[x][y] = 0.0;
-            while (ia < a1) {
+            double o0 = 0.0, o1 = 0.0;
+            for (; ia < a1; ++ia) { // TR: rows = point body (this), cols = edge body
                 cv.fmt.unpack(cv.key[ia], ca, cb, vv, ee);
                 if (cb != partner) break;
-                if (prow >= 0) add_tr(O, cv.cmat + 21 * ia, contact_geom(sv, ca, cb, vv, ee), false);
-                ++ia;
+                if (!cv.flag[ia] || prow < 0) continue;
+                const double* cm = cv.cmat + 21 * ia;
+                const double* geo = cv.cgeo + 6 * ia;
+                o0 += blk_entry(cm, geo, ca0, ia0, cb0, ib0, 0, 0, 1, 2);
+                if (has1) o1 += blk_entry(cm, geo, ca1, ia1, cb1, ib1, 0, 0, 1, 2);
             }
-            while (ib < b1) {
+            for (; ib < b1; ++ib) { // BL = TR^T: rows = edge body (this), cols = point body
                 const int c = cv.perm_b[ib];
                 cv.fmt.unpack(cv.key[c], ca, cb, vv, ee);
                 if (ca != partner) break;
-                if (prow >= 0) add_tr(O, cv.cmat + 21 * c, contact_geom(sv, ca, cb, vv, ee), true);
-                ++ib;
+                if (!cv.flag[c] || prow < 0) continue;
+                const double* cm = cv.cmat + 21 * c;
+                const double* geo = cv.cgeo + 6 * c;
+                o0 += blk_entry(cm, geo, cb0, ib0, ca0, ia0, 0, 0, 1, 2);
+                if (has1) o1 += blk_entry(cm, geo, cb1, ib1, ca1, ia1, 0, 0, 1, 2);
             }
             if (prow < 0) continue;
             if (nblk >= kEll) {
-                raise(sv.err, kErrCapacity);
+                if (lane == 0) raise(sv.err, kErrCapacity);
                 break;
             }
-            sv.ell_col[r * kEll + nblk] = prow;
+            if (lane == 0) sv.ell_col[r * kEll + nblk] = prow;
             double* odst = sv.ell_blk + (static_cast<size_t>(r) * kEll + nblk) * 36;
-#pragma unroll
-            for (int x = 0; x < 6; ++x)
-#pragma unroll
-                for (int y = 0; y < 6; ++y) odst[6 * x + y] = O[x][y];
+            odst[e0] = o0;
+            if (has1) odst[e1] = o1;
             ++nblk;
         }
-        sv.ell_cnt[r] = nblk;
+        if (lane == 0) sv.ell_cnt[r] = nblk;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Skin-list validity (see ListState): every dynamic vertex of q and q1 within
+// 0.99 s_i of its qref position. Every thread also proposes the skin of a
+// rebuild at qref = q: s_i = max(s_min, grow * (largest move of one of the
+// instance's vertices from q to q1 or to q_tilde)), so a rebuilt list covers
+// q1 and the predicted motion of the frame. The last block decides, sets the
+// rebuild flag and steers the conditional IF node of the rebuild.
+// ---------------------------------------------------------------------------
+__global__ void k_list_check(SceneView sc, InstView iv, const double* qref, const double* qt,
+                             const double* skin, double* skin_next, double s_min, double grow,
+                             ListState* ls, unsigned long long cond, int graph) {
+    __shared__ bool last;
+    bool bad = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < iv.n; i += gridDim.x * blockDim.x) {
+        const int b = iv.body[i];
+        if (sc.is_static[b]) {
+            skin_next[i] = 0.0;
+            continue;
+        }
+        const double* q0 = iv.q0 + 6 * i;
+        const double* q1 = iv.q1 + 6 * i;
+        const double* qr = qref + 6 * i;
+        const double* qs = qt ? qt + 6 * i : q0;
+        double dref = 0.0, dstep = 0.0;
+        for (int v = sc.vstart[b]; v < sc.vstart[b + 1]; ++v) {
+            const V2 r = rest_of(sc, v);
+            const V2 x0 = world_point(q0, r), x1 = world_point(q1, r), xr = world_point(qr, r),
+                     xs = world_point(qs, r);
+            dref = fmax(dref, fmax(fmax(fabs(x0.x - xr.x), fabs(x0.y - xr.y)),
+                                   fmax(fabs(x1.x - xr.x), fabs(x1.y - xr.y))));
+            dstep = fmax(dstep, fmax(fmax(fabs(x1.x - x0.x), fabs(x1.y - x0.y)),
+                                     fmax(fabs(xs.x - x0.x), fabs(xs.y - x0.y))));
+        }
+        if (!(dref <= 0.99 * skin[i])) bad = true; // NaN-safe
+        skin_next[i] = fmax(s_min, grow * dstep);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ls->invalid_acc, 1);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&ls->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    const bool rebuild = !ls->valid || __ldcg(&ls->invalid_acc) != 0;
+    if (rebuild) ++ls->n_rebuilds;
+    ls->valid = 1;
+    ls->rebuild = rebuild ? 1 : 0;
+    ls->invalid_acc = 0;
+    ls->ticket = 0u;
+    if (graph) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(cond), rebuild ? 1u : 0u);
+}
+
+// First node of a rebuild: qref = q, skin = the proposal of the check.
+__global__ void k_list_commit(int n, const double* iq, double* qref, const double* skin_next,
+                              double* skin) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 6 * n; i += gridDim.x * blockDim.x) {
+        qref[i] = iq[i];
+        if (i < n) skin[i] = skin_next[i];
     }
 }
 
@@ -705,9 +814,13 @@ __global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, cons
 // launch wrappers
 // ---------------------------------------------------------------------------
 void launch_body_terms(const SolverView& sv, const double* q, bool derivs, int which,
-                       cudaStream_t s) {
-    if (sv.n_rows == 0) return;
-    DABD_LAUNCH("k_body_terms", s, k_body_terms<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, q, derivs ? 1 : 0, which));
+                       cudaStream_t s, int* reset_counter) {
+    if (sv.n_rows == 0) {
+        if (reset_counter) CUDA_CHECK(cudaMemsetAsync(reset_counter, 0, sizeof(int), s));
+        return;
+    }
+    DABD_LAUNCH("k_body_terms", s, k_body_terms<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, q, derivs ? 1 : 0, which,
+                                                                                      reset_counter));
 }
 
 void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
@@ -721,7 +834,8 @@ void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, 
 
 void launch_contact_terms(const SolverView& sv, const ContactView& cv, cudaStream_t s) {
     if (cv.n == 0) return;
-    DABD_LAUNCH("k_contact_terms", s, k_contact_terms<<<grid_for(cv.n, kB), kB, 0, s>>>(sv, cv));
+    // 32-thread blocks spread the few thousand active contacts over every SM
+    DABD_LAUNCH("k_contact_terms", s, k_contact_terms<<<grid_for(cv.n, 32, 148 * 8), 32, 0, s>>>(sv, cv));
 }
 
 void launch_seg_offsets(const unsigned long long* keys, int n, const int* dn, KeyFmt fmt,
@@ -741,7 +855,30 @@ void launch_make_bkeys(const unsigned long long* keys, int n, const int* dn, Key
 void launch_assemble(const SolverView& sv, const ContactView& cv, double* row_trace,
                      cudaStream_t s) {
     if (sv.n_rows == 0) return;
-    DABD_LAUNCH("k_assemble", s, k_assemble<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, cv, row_trace));
+    DABD_LAUNCH("k_assemble", s, k_assemble<<<grid_for(32ll * sv.n_rows, 128), 128, 0, s>>>(sv, cv, row_trace));
+}
+
+void launch_contact_select(const SolverView& sv, const ContactView& cv, const Box* box,
+                           cudaStream_t s) {
+    if (cv.n == 0) return;
+    DABD_LAUNCH("k_contact_select", s,
+                k_contact_select<<<grid_for(cv.n, kB, 148 * 4), kB, 0, s>>>(sv, cv, box));
+}
+
+void launch_list_check(const SceneView& sc, const InstView& iv, const double* qref,
+                       const double* qt, const double* skin, double* skin_next, double s_min,
+                       double grow, ListState* ls, unsigned long long cond, int graph,
+                       cudaStream_t s) {
+    DABD_LAUNCH("k_list_check", s,
+                k_list_check<<<grid_for(std::max(iv.n, 1), kB, 148), kB, 0, s>>>(
+                    sc, iv, qref, qt, skin, skin_next, s_min, grow, ls, cond, graph));
+}
+
+void launch_list_commit(int n, const double* iq, double* qref, const double* skin_next,
+                        double* skin, cudaStream_t s) {
+    if (n == 0) return;
+    DABD_LAUNCH("k_list_commit", s,
+                k_list_commit<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, iq, qref, skin_next, skin));
 }
 
 void launch_precond(const SolverView& sv, cudaStream_t s) {

@@ -99,18 +99,43 @@ struct SolverView {
     int* err = nullptr;
 };
 
-// Active contacts (derivative stage) in (a,b,v,e) order plus their data.
+// Skin list ("Verlet list") of the local solve: the candidate superset
+// built at a reference configuration qref, every instance i carrying its own
+// skin s_i (body box grown by d_hat + s_i, point-edge tests by
+// d_hat + s_P + s_E). While every vertex of instance i stays within s_i of
+// its qref position (infinity norm) at the configurations a Newton iteration
+// touches (q and the CCD end q + dq; the trials lie between), every
+// candidate of the reference predicate at those configurations (static
+// margin d_hat, swept margin 0) is in the list; each use re-applies the
+// exact predicate, so detection results equal a fresh broad phase while the
+// list is rebuilt only when a body leaves its skin (k_list_check decides on
+// the device, a conditional graph node rebuilds).
+struct ListState {
+    int valid;        // 0: rebuild at the next check
+    int rebuild;      // decision of the last check
+    int n_rebuilds;
+    int n_act;        // active contacts of the current derivative pass
+    int invalid_acc;  // OR over the blocks of the running check
+    unsigned ticket;
+};
+
+// Contacts of the current derivative pass, stored at their skin-list
+// position t (list sorted by (a, b, v, e)); flag[t] marks the active ones.
 struct ContactView {
-    int n = 0;                    // capacity (grid size)
-    const int* dn = nullptr;      // device-side contact count (nullptr: n is exact)
+    int n = 0;                    // list capacity (grid size)
+    const int* dn = nullptr;      // device-side list length
     KeyFmt fmt;
-    const unsigned long long* key = nullptr; // sorted by (a, b, v, e)
-    const int* perm_b = nullptr;  // contact indices sorted by (b, a, v, e)
-    const int* aoff = nullptr;    // [I+1] contacts with a == i: [aoff[i], aoff[i+1])
+    const unsigned long long* key = nullptr; // list keys, sorted by (a, b, v, e)
+    const int* perm_b = nullptr;  // list positions sorted by (b, a, v, e)
+    const int* aoff = nullptr;    // [I+1] positions with a == i: [aoff[i], aoff[i+1])
     const int* boff = nullptr;    // [I+1] perm_b positions with b == i
-    double* cval = nullptr;       // [C] weighted barrier value
-    double* cgrad = nullptr;      // [C][12] weighted gradient
-    double* cmat = nullptr;       // [C][21] projected world-space 6x6 (upper, row-major)
+    unsigned char* flag = nullptr; // [cap] active at the current iterate
+    int* act = nullptr;           // [cap] active positions (any order)
+    ListState* ls = nullptr;      // ls->n_act = number of entries in act
+    double* cval = nullptr;       // [cap] weighted barrier value (0 when inactive)
+    double* cgrad = nullptr;      // [cap][12] weighted gradient
+    double* cmat = nullptr;       // [cap][21] projected world-space 6x6 (upper, row-major)
+    double* cgeo = nullptr;       // [cap][6] rest points (p, e0, e1) of the contact
 };
 
 } // namespace dabd_gpu

@@ -48,6 +48,7 @@ __global__ void k_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHand
             s.dq_inf = 0.0;
             s.toi_earliest = 2.0;
             s.n_candidates = 0;
+            s.n_active_contacts = 0;
             break;
         case kOpNewtonCheck: // newton.cpp:30-36
             if (ctrl) atomicAdd(&ctrl->pcg_total, s.pcg_iters);

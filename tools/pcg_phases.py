@@ -1,0 +1,37 @@
+"""Cycles per PCG iteration by phase (CTA 0 / warp 0 of the cluster kernel),
+from dabd_gpu_ctx_pcg_phases, over a few settled pile frames."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    from paper_2605_15875_b200 import _lib as L
+    from paper_2605_15875_b200 import api
+    from paper_2605_15875_b200.scene import make_scenario
+
+    lib = L.load()
+    scene = sys.argv[1] if len(sys.argv) > 1 else "pile-1k"
+    ctx = api.Context(api.Scene(make_scenario(scene)))
+    ctx.run_frames(40)
+    torch.cuda.synchronize()
+    cyc = (C.c_double * 8)()
+    L.check(lib.dabd_gpu_ctx_pcg_phases(ctx.h, 1, cyc))
+    ctx.run_frames(4)
+    torch.cuda.synchronize()
+    L.check(lib.dabd_gpu_ctx_pcg_phases(ctx.h, 1, cyc))
+    it = cyc[7]
+    names = ["m=Dinv w + partials", "CTA reduce + push", "arrive", "local SpMV", "wait", "fold+scalars",
+             "remote SpMV + recurrences", "iterations"]
+    tot = sum(cyc[k] for k in range(7))
+    print(f"iterations {it:.0f}, cycles/iteration {tot / max(it, 1):.0f}")
+    for k in range(7):
+        print(f"  [{k}] {names[k]:28s} {cyc[k] / max(it, 1):8.0f} cyc/it  {100 * cyc[k] / max(tot, 1):5.1f}%")
+
+
+if __name__ == "__main__":
+    main()
