@@ -376,6 +376,7 @@ __device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
 // A cluster whose rows overflow the shared-memory budget (spilled blocks or
 // send lists) takes the barrier-synchronised path that reads peers' m
 // through DSMEM and spilled blocks from global memory.
+template <int G>
 __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, int csize, int cmax_rows) {
     cg::cluster_group cl = cg::this_cluster();
     unsigned long long t_start = 0;
@@ -401,22 +402,14 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     const double eps = st.eps;
     // shared-memory carve-up (cmax_rows = chunk upper bound used at launch)
     const int V = 6 * cmax_rows;
-    double* vx = reinterpret_cast<double*>(smem);
-    double* vr = vx + V;
-    double* vu = vr + V;
-    double* vw = vu + V;
-    double* vz = vw + V;
-    double* vq = vz + V;
-    double* vs = vq + V;
-    double* vp = vs + V;
-    double* vm0 = vp + V; // m (fallback path: ping-pong read by the peers)
+    double* vm0 = reinterpret_cast<double*>(smem); // m = Dinv w, double-buffered by parity
     double* vm1 = vm0 + V;
     double* dinv = vm1 + V;
     int* bstart = reinterpret_cast<int*>(dinv + 36 * cmax_rows); // [cmax_rows + 1]
     // per staged block: the block (288 B), its column code (4 B); per remote
     // block additionally two parity halo rows (96 B), the DSMEM address of the
     // peer row (8 B) and a send entry at the producer (8 B)
-    const size_t used = (96ull * cmax_rows) * 8 + 4ull * (cmax_rows + 2) + 64;
+    const size_t used = (48ull * cmax_rows) * 8 + 4ull * (cmax_rows + 2) + 64;
     const int cap_blocks = static_cast<int>((kCSmemBytes - used) / (288 + 4 + 96 + 8 + 8)) & ~1;
     double* blk = reinterpret_cast<double*>(
         (reinterpret_cast<uintptr_t>(bstart + cmax_rows + 1) + 15) & ~uintptr_t(15));
@@ -586,39 +579,59 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         return y;
     };
 
-    // ---- init: r = b = -grad, x = 0, u = Dinv r (read by the peers from m1), w = A u
-    for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
-        const int lr = base + slot;
-        const bool on = lane < 30 && lr < nr;
-        const double g = on && act ? -sv.rgrad[6 * (r0 + lr) + comp] : 0.0;
-        double u = 0.0;
+    // ---- init: r = b = -grad, x = 0, u = Dinv r (read by the peers from m1), w = A u.
+    // Every lane keeps its (row, component) entries of all PCG vectors in
+    // registers (row group g of the warp: local row warp * 5 + slot + g * 80);
+    // only m = Dinv w lives in shared memory, double-buffered by parity
+    // (vm0 / vm1), because the SpMV of other lanes and CTAs reads it.
+    double x[G], r[G], u[G], w[G], z[G], qv[G], sv_[G], pv[G], mr[G];
+    bool on[G];
+    int lrg[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        lrg[g] = warp * kRowsPerWarp + slot + g * row_step;
+        on[g] = lane < 30 && lrg[g] < nr;
+        const double gr = on[g] && act ? -sv.rgrad[6 * (r0 + lrg[g]) + comp] : 0.0;
+        double uu = 0.0;
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-            const double gc = __shfl_sync(0xffffffffu, g, (6 * slot + c) & 31);
-            if (on) u += dinv[36 * lr + 6 * comp + c] * gc;
+            const double gc = __shfl_sync(0xffffffffu, gr, (6 * slot + c) & 31);
+            if (on[g]) uu += dinv[36 * lrg[g] + 6 * comp + c] * gc;
         }
-        if (on) {
-            const int i = 6 * lr + comp;
-            vr[i] = g;
-            vu[i] = u;
-            vm1[i] = u;
-            vx[i] = 0.0;
-            vz[i] = 0.0;
-            vq[i] = 0.0;
-            vs[i] = 0.0;
-            vp[i] = 0.0;
-        }
+        r[g] = gr;
+        u[g] = uu;
+        x[g] = z[g] = qv[g] = sv_[g] = pv[g] = 0.0;
+        if (on[g]) vm1[6 * lrg[g] + comp] = uu;
     }
     cluster_barrier();
-    for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
-        const int lr = base + slot;
-        if (lane < 30 && lr < nr)
-            vw[6 * lr + comp] = spmv_remote(lr, nullptr, m_off, spmv_local(lr, vm1));
-    }
-    // peers read our m1 (= u) above; the push path never reads peers' smem
-    // again, the fallback path orders its next m1 writes behind a barrier
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+        w[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, spmv_local(lrg[g], vm1)) : 0.0;
+    // m = Dinv w for iteration 0 (into vm0) and the partials (r.u, w.u, r.r)
+    double l_g = 0.0, l_d = 0.0, l_r = 0.0;
+    auto make_m = [&](double* mdst) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            double wc[6];
+#pragma unroll
+            for (int c = 0; c < 6; ++c) wc[c] = __shfl_sync(0xffffffffu, w[g], (6 * slot + c) & 31);
+            double m = 0.0;
+            if (on[g]) {
+                const double2* d2 = reinterpret_cast<const double2*>(dinv + 36 * lrg[g] + 6 * comp);
+                const double2 d0 = d2[0], d1 = d2[1], dd = d2[2];
+                m = d0.x * wc[0] + d0.y * wc[1] + d1.x * wc[2] + d1.y * wc[3] + dd.x * wc[4] + dd.y * wc[5];
+                mdst[6 * lrg[g] + comp] = m;
+                l_g += r[g] * u[g];
+                l_d += w[g] * u[g];
+                l_r += r[g] * r[g];
+            }
+            mr[g] = m;
+        }
+    };
+    make_m(vm0);
+    // the fallback path's peers may still read our vm1 (init SpMV) until
+    // this barrier; the push path only writes vm1 after a full exchange
     if (!push) cluster_barrier();
-    __syncthreads();
 
     bool done = !act;
     double inv_gamma_old = 0.0, inv_alpha_old = 0.0, bnorm2 = 0.0;
@@ -636,35 +649,12 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     while (!done) {
         mark(7);
         const int par = it & 1;
-        double* mcur = push ? vm0 : (par ? vm1 : vm0);
+        double* mcur = par ? vm1 : vm0;
+        double* mnext = par ? vm0 : vm1;
         const ptrdiff_t moff = par ? m_off : 0;
         const unsigned bar = smem_u32(&sc.bar[par]);
         if (push && threadIdx.x == 0) mbar_expect(bar, expect);
-        // ---- local: m = Dinv w; partials (r.u, w.u, r.r)
-        double l_g = 0.0, l_d = 0.0, l_r = 0.0;
-        for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
-            const int lr = base + slot;
-            const bool on = lane < 30 && lr < nr;
-            const int i = 6 * lr + comp;
-            const double wv = on ? vw[i] : 0.0;
-            double wc[6];
-#pragma unroll
-            for (int c = 0; c < 6; ++c) wc[c] = __shfl_sync(0xffffffffu, wv, (6 * slot + c) & 31);
-            double m = 0.0;
-            if (on) {
-                const double2* d2 = reinterpret_cast<const double2*>(dinv + 36 * lr + 6 * comp);
-                const double2 d0 = d2[0], d1 = d2[1], dd = d2[2];
-                m = d0.x * wc[0] + d0.y * wc[1] + d1.x * wc[2] + d1.y * wc[3] + dd.x * wc[4] + dd.y * wc[5];
-            }
-            if (on) {
-                mcur[i] = m;
-                const double rv = vr[i], uv = vu[i];
-                l_g += rv * uv;
-                l_d += wv * uv;
-                l_r += rv * rv;
-            }
-        }
-        mark(0);
+        // ---- partials of this CTA: warp trees, then one fixed 32-lane tree
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             l_g += __shfl_xor_sync(0xffffffffu, l_g, off);
@@ -676,25 +666,31 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             sc.red[warp][1] = l_d;
             sc.red[warp][2] = l_r;
         }
-        __syncthreads(); // red[] and this CTA's m complete
-        if (warp == 0 && lane < csize) {
-            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+        mark(0);
+        __syncthreads(); // red[] and this CTA's m (mcur) complete
+        mark(1);
+        if (warp == 0) {
+            double t0 = lane < kCW ? sc.red[lane][0] : 0.0;
+            double t1 = lane < kCW ? sc.red[lane][1] : 0.0;
+            double t2 = lane < kCW ? sc.red[lane][2] : 0.0;
 #pragma unroll
-            for (int w = 0; w < kCW; ++w) { // fixed order
-                t0 += sc.red[w][0];
-                t1 += sc.red[w][1];
-                t2 += sc.red[w][2];
+            for (int off = 16; off > 0; off >>= 1) {
+                t0 += __shfl_xor_sync(0xffffffffu, t0, off);
+                t1 += __shfl_xor_sync(0xffffffffu, t1, off);
+                t2 += __shfl_xor_sync(0xffffffffu, t2, off);
             }
-            if (push) {
-                const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), lane);
-                const unsigned pbar = mapa(bar, lane);
-                st_async2(dst, t0, t1, pbar);
-                st_async2(dst + 16, t2, 0.0, pbar);
-            } else {
-                double* d = &cl.map_shared_rank(&sc, lane)->tab[par][rank][0];
-                d[0] = t0;
-                d[1] = t1;
-                d[2] = t2;
+            if (lane < csize) {
+                if (push) {
+                    const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), lane);
+                    const unsigned pbar = mapa(bar, lane);
+                    st_async2(dst, t0, t1, pbar);
+                    st_async2(dst + 16, t2, 0.0, pbar);
+                } else {
+                    double* d = &cl.map_shared_rank(&sc, lane)->tab[par][rank][0];
+                    d[0] = t0;
+                    d[1] = t1;
+                    d[2] = t2;
+                }
             }
         }
         if (push) { // the m rows the peers' blocks need, into their halo slots
@@ -708,28 +704,35 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         } else {
             cluster_arrive();
         }
-        mark(1);
+        mark(2);
         // local-column half of n = A m while the messages fly
-        // (the first two row groups of the warp; more only when nr > 160)
-        double nloc0 = 0.0, nloc1 = 0.0;
-        {
-            const int lr0 = warp * kRowsPerWarp + slot, lr1 = lr0 + row_step;
-            if (lane < 30 && lr0 < nr) nloc0 = spmv_local(lr0, mcur);
-            if (lane < 30 && lr1 < nr) nloc1 = spmv_local(lr1, mcur);
-        }
+        double nloc[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) nloc[g] = on[g] ? spmv_local(lrg[g], mcur) : 0.0;
         mark(3);
         if (push)
             mbar_wait(bar, (it >> 1) & 1);
         else
             cluster_wait();
         mark(4);
+        // every warp folds the csize CTA partials with the same 32-lane tree
         double gamma = 0.0, delta = 0.0, rr = 0.0;
+        {
+            double2 gd = make_double2(0.0, 0.0);
+            double t2 = 0.0;
+            if (lane < 16) {
+                gd = *reinterpret_cast<const double2*>(&sc.tab[par][lane][0]);
+                t2 = sc.tab[par][lane][2];
+            }
+            gamma = gd.x;
+            delta = gd.y;
+            rr = t2;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) { // rank order; slots past csize stay zero
-            const double2 gd = *reinterpret_cast<const double2*>(&sc.tab[par][k][0]);
-            gamma += gd.x;
-            delta += gd.y;
-            rr += sc.tab[par][k][2];
+            for (int off = 16; off > 0; off >>= 1) {
+                gamma += __shfl_xor_sync(0xffffffffu, gamma, off);
+                delta += __shfl_xor_sync(0xffffffffu, delta, off);
+                rr += __shfl_xor_sync(0xffffffffu, rr, off);
+            }
         }
         if (it == 0) bnorm2 = rr;
         if (bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters) break;
@@ -742,43 +745,34 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         mark(5);
         inv_gamma_old = 1.0 / gamma; // not needed until the next iteration
         inv_alpha_old = 1.0 / alpha;
-        // ---- remote half of n, then the recurrences
+        // ---- remote half of n, the recurrences, then m = Dinv w and the
+        // partials of the next iteration (register-resident)
         const double* hv = push ? halo + 6 * par * cap_blocks : nullptr;
-        {
-            int k = 0;
-            for (int base = warp * kRowsPerWarp; base < nr; base += row_step, ++k) {
-                const int lr = base + slot;
-                if (lane < 30 && lr < nr) {
-                    const double n0 = k == 0 ? nloc0 : k == 1 ? nloc1 : spmv_local(lr, mcur);
-                    const double n = spmv_remote(lr, hv, moff, n0);
-                    const int i = 6 * lr + comp;
-                    const double z = n + beta * vz[i];
-                    const double q = mcur[i] + beta * vq[i];
-                    const double s = vw[i] + beta * vs[i];
-                    const double pv = vu[i] + beta * vp[i];
-                    vz[i] = z;
-                    vq[i] = q;
-                    vs[i] = s;
-                    vp[i] = pv;
-                    vx[i] += alpha * pv;
-                    vr[i] -= alpha * s;
-                    vu[i] -= alpha * q;
-                    vw[i] -= alpha * z;
-                }
-            }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (!on[g]) continue;
+            const double n = spmv_remote(lrg[g], hv, moff, nloc[g]);
+            z[g] = n + beta * z[g];
+            qv[g] = mr[g] + beta * qv[g];
+            sv_[g] = w[g] + beta * sv_[g];
+            pv[g] = u[g] + beta * pv[g];
+            x[g] += alpha * pv[g];
+            r[g] -= alpha * sv_[g];
+            u[g] -= alpha * qv[g];
+            w[g] -= alpha * z[g];
         }
+        l_g = l_d = l_r = 0.0;
+        make_m(mnext);
         mark(6);
         ++it;
-        if (push) __syncthreads(); // mcur is rewritten by other warps next iteration
     }
     if (timed) {
         ph[7] = it;
         for (int k = 0; k < 8; ++k) atomicAdd(&sv.perf->phase[k], ph[k]);
     }
-    for (int base = warp * kRowsPerWarp; base < nr; base += row_step) {
-        const int lr = base + slot;
-        if (lane < 30 && lr < nr) sv.x[6 * (r0 + lr) + comp] = vx[6 * lr + comp];
-    }
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+        if (on[g]) sv.x[6 * (r0 + lrg[g]) + comp] = x[g];
     if (rank == 0 && threadIdx.x == 0) {
         sv.ps[p].pcg_iters = it;
         sv.ps[p].pcg_done = 1;
@@ -802,12 +796,18 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
 
 } // namespace
 
+template <int G>
+static void cluster_attrs() {
+    cudaFuncSetAttribute(k_pcg_cluster<G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_pcg_cluster<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemBytes);
+}
+
 int pcg_cluster_size() {
     static int c = 0;
     if (c == 0) {
-        cudaFuncSetAttribute(k_pcg_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(k_pcg_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kCSmemBytes);
+        cluster_attrs<1>();
+        cluster_attrs<2>();
+        cluster_attrs<4>();
         c = 16;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(16);
@@ -821,7 +821,7 @@ int pcg_cluster_size() {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, k_pcg_cluster, &cfg) != cudaSuccess || n < 1) c = 8;
+        if (cudaOccupancyMaxActiveClusters(&n, k_pcg_cluster<4>, &cfg) != cudaSuccess || n < 1) c = 8;
         cudaGetLastError();
     }
     return c;
@@ -835,6 +835,9 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
     while (csize < cmax && csize * 32 < max_rows_per_part) csize *= 2; // >= ~32 rows per CTA
     // largest per-partition chunk under the per-partition rule of k_pcg_cluster
     const int cmax_rows = std::max(std::min(max_rows_per_part, 32), (max_rows_per_part + csize - 1) / csize);
+    // register-resident row groups per warp (kCW warps x kRowsPerWarp rows each)
+    const int groups = (cmax_rows + kCW * kRowsPerWarp - 1) / (kCW * kRowsPerWarp);
+    if (groups > 4) throw Error("pcg: cluster chunk exceeds 4 row groups per warp");
     PcgArgs a{pbuf, nullptr, nullptr, tol, max_iters};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csize * sv.n_parts);
@@ -848,8 +851,12 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    DABD_LAUNCH("k_pcg", s,
-                CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg_cluster, sv, a, csize, cmax_rows)));
+    if (groups <= 1)
+        DABD_LAUNCH("k_pcg", s, CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg_cluster<1>, sv, a, csize, cmax_rows)));
+    else if (groups == 2)
+        DABD_LAUNCH("k_pcg", s, CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg_cluster<2>, sv, a, csize, cmax_rows)));
+    else
+        DABD_LAUNCH("k_pcg", s, CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg_cluster<4>, sv, a, csize, cmax_rows)));
 }
 
 int pcg_grid_size(int n_rows) {
