@@ -1,0 +1,51 @@
+"""Key metrics of an `ncu --set full` report (raw page), one line each.
+
+python tools/ncu_summary.py report.ncu-rep > profiles/<round>_<kernel>_ncu_full.txt
+"""
+import csv
+import subprocess
+import sys
+
+KEYS = [
+    "Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "lts__t_bytes.sum", "l1tex__t_bytes.sum",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__cycles_active.avg", "smsp__inst_executed.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "launch__grid_size", "launch__block_size", "launch__cluster_dim_x",
+    "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
+    "launch__occupancy_limit_registers", "sm__maximum_warps_per_active_cycle_pct",
+    "smsp__average_warp_latency_issue_stalled_barrier", "smsp__pcsamp_warps_issue_stalled_barrier",
+    "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
+    "smsp__pcsamp_warps_issue_stalled_wait", "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle",
+    "smsp__pcsamp_warps_issue_stalled_membar", "smsp__pcsamp_warps_issue_stalled_selected",
+    "smsp__pcsamp_warps_issue_stalled_not_selected", "smsp__pcsamp_warps_issue_stalled_no_instructions",
+    "smsp__pcsamp_sample_count",
+]
+
+
+def main():
+    rep = sys.argv[1]
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    if len(rows) < 3:
+        print(out)
+        return
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                u = units[i] if i < len(units) else ""
+                print(f"{k} = {r[i]} {u}".rstrip())
+        print()
+
+
+if __name__ == "__main__":
+    main()

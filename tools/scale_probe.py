@@ -1,0 +1,54 @@
+"""Frames/s and solver counts of the larger BASELINE.json configs on ONE GPU
+(partitions batched on the device), plus the global minimum broad-phase
+distance after the run as a penetration sanity check.
+
+python tools/scale_probe.py scene:workers:frames [...]
+   e.g. pour-10k:8:20 sweep-100k:8:5 hetero-1000:2:20 cubes-64:2:50
+"""
+
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+
+    from paper_2605_15875_b200 import api
+    from paper_2605_15875_b200.scene import make_scenario
+
+    for spec in sys.argv[1:]:
+        name, workers, frames = spec.split(":")
+        workers, frames = int(workers), int(frames)
+        sd = make_scenario(name)
+        t0 = time.perf_counter()
+        sc = api.Scene(sd)
+        ctx = api.Context(sc, num_workers=workers)
+        ctx.run_frames(1)  # capture / first-touch outside the timing
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        st = ctx.run_frames(frames)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t1
+        q, _ = ctx.state()
+        cand = ctx.broad_phase(q, sd.params.d_hat)
+        pairs, d = ctx.narrow_phase(q, cand, sd.params.d_hat)
+        out = {
+            "scene": name, "bodies": sc.n, "workers": workers, "frames": frames,
+            "setup_s": t1 - t0, "ms_per_frame": 1e3 * dt / frames, "steps_per_s": frames / dt,
+            "admm_per_frame": sum(s["admm_iterations"] for s in st) / frames,
+            "newton_per_frame": sum(s["newton_iterations"] for s in st) / frames,
+            "pcg_per_frame": sum(s["pcg_iterations"] for s in st) / frames,
+            "attempts": sum(s["attempts"] for s in st), "committed": sum(s["committed"] for s in st),
+            "max_contacts": max(s["max_contacts"] for s in st),
+            "active_pairs_end": int(len(d)), "min_d_end": float(d.min()) if len(d) else None,
+        }
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
