@@ -183,6 +183,19 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_holder_masks(dabd_gpu_ctx* ctx, const doub
                                                    int n_planes, const double* planes, double w,
                                                    uint32_t* masks);
 
+/* Penetration audit of a configuration: intersection_test
+ * (proj/src/geometry.cpp:389-454; strict vertex / loop-centroid containment
+ * and proper edge crossings over body pairs with overlapping AABBs) and the
+ * minimum point-edge distance of proj/tests/support/oracles.cpp:153-173 over
+ * ordered pairs a != b that are not both static. q == NULL audits the
+ * context's current device state (no host copy). result = 1 iff some pair
+ * interpenetrates; n_violations (nullable) counts those pairs. min_distance
+ * (nullable) is computed when cutoff > 0 and is exact whenever it is below
+ * the cutoff (DBL_MAX when no pair comes within reach). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_audit(dabd_gpu_ctx* ctx, const double* q, const int* subset,
+                                            int n_subset, double cutoff, int* result,
+                                            int* n_violations, double* min_distance);
+
 /* LocalObjective over `local` bodies with per-local kappa and q_tilde and
  * optional anchors (body, z[6], u[6], rho). holder_mask (per body) may be
  * NULL for single-domain weights. mode 0: value; 1: value without anchors;

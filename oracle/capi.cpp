@@ -292,6 +292,15 @@ int oracle_intersection_test(void* sp, const double* q, const int* subset, int n
     });
 }
 
+int oracle_min_pair_distance(void* sp, const double* q, const int* subset, int n_subset,
+                             int skip_static_pairs, double* out) {
+    return guarded([&] {
+        Scene* s = static_cast<Scene*>(sp);
+        *out = min_pair_distance(s->bodies, to_configs(q, static_cast<int>(s->bodies.size())),
+                                 to_vec(subset, n_subset), skip_static_pairs != 0);
+    });
+}
+
 int oracle_predicted_position(void* sp, const double* q, const double* qdot, const double* f,
                               double h, double* out) {
     return guarded([&] {

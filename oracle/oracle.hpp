@@ -187,6 +187,8 @@ double ccd_toi(const std::vector<AffineBody>& bodies, const Configs& start,
                const Configs& end, const std::vector<ContactPair>& cand);
 double ccd_toi_scene(const std::vector<AffineBody>& bodies, const Configs& start,
                      const Configs& end, const std::vector<int>& subset = {});
+double min_pair_distance(const std::vector<AffineBody>& bodies, const Configs& q,
+                         const std::vector<int>& subset, bool skip_static_pairs);
 bool intersection_test(const std::vector<AffineBody>& bodies, const Configs& q,
                        const std::vector<int>& subset = {});
 

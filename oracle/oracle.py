@@ -179,6 +179,14 @@ class Scene:
                                               0 if sub is None else len(sub), C.byref(r)))
         return bool(r.value)
 
+    def min_pair_distance(self, q, subset=None, skip_static_pairs=True):
+        sub = None if subset is None else _i32(subset)
+        r = C.c_double()
+        _check(lib().oracle_min_pair_distance(self.h, _d(_f64(q, (self.n, 6))), _i(sub),
+                                              0 if sub is None else len(sub),
+                                              int(skip_static_pairs), C.byref(r)))
+        return r.value
+
     def predicted_position(self, q, qdot, f, h):
         out = np.zeros((self.n, 6))
         _check(lib().oracle_predicted_position(self.h, _d(_f64(q, (self.n, 6))),

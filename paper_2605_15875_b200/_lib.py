@@ -61,7 +61,7 @@ EXPORTS = [
     "dabd_gpu_scene_set_params", "dabd_gpu_scene_set_planes", "dabd_gpu_scene_set_force_split",
     "dabd_gpu_scene_counts", "dabd_gpu_scene_bodies", "dabd_gpu_ctx_create", "dabd_gpu_ctx_free",
     "dabd_gpu_ctx_set_solver", "dabd_gpu_ctx_set_stream", "dabd_gpu_broad_phase",
-    "dabd_gpu_narrow_phase", "dabd_gpu_ccd_toi", "dabd_gpu_holder_masks", "dabd_gpu_objective",
+    "dabd_gpu_narrow_phase", "dabd_gpu_ccd_toi", "dabd_gpu_holder_masks", "dabd_gpu_audit", "dabd_gpu_objective",
     "dabd_gpu_newton_solve", "dabd_gpu_run_frames", "dabd_gpu_set_state", "dabd_gpu_get_state",
     "dabd_gpu_get_rho", "dabd_gpu_take_trace", "dabd_gpu_launch_count",
     "dabd_gpu_kernel_timer_enable", "dabd_gpu_kernel_timer_read", "dabd_gpu_kernel_timer_report",

@@ -166,6 +166,19 @@ class Context:
                                           0 if sub is None else len(sub), C.byref(t)))
         return t.value
 
+    def intersection_test(self, q=None, subset=None) -> bool:
+        """geometry.cpp:389-454 on the device (q None: the current state)."""
+        return self.audit(q, subset)[0]
+
+    def audit(self, q=None, subset=None, cutoff: float = 0.0):
+        """(intersecting, n_violating_pairs, min_distance); see dabd_gpu_audit."""
+        res, nv, dm = C.c_int(), C.c_int(), C.c_double()
+        sub = None if subset is None else _i32(subset)
+        L.check(L.load().dabd_gpu_audit(self.h, None if q is None else _d(_f64(q, (self.n, 6))),
+                                        _i(sub), 0 if sub is None else len(sub), C.c_double(cutoff),
+                                        C.byref(res), C.byref(nv), C.byref(dm)))
+        return bool(res.value), nv.value, dm.value
+
     def holder_masks(self, q, planes, w) -> np.ndarray:
         planes = _f64(planes).reshape(-1, 4)
         out = np.zeros(self.n, dtype=np.uint32)

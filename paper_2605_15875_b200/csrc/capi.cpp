@@ -277,6 +277,18 @@ dabd_gpu_status dabd_gpu_holder_masks(dabd_gpu_ctx* ctx, const double* q, int n_
     });
 }
 
+dabd_gpu_status dabd_gpu_audit(dabd_gpu_ctx* ctx, const double* q, const int* subset, int n_subset,
+                               double cutoff, int* result, int* n_violations, double* min_distance) {
+    if (!ctx || !result || n_subset < 0 || !(cutoff >= 0.0)) return null_arg();
+    return guarded([&] {
+        const dabd_gpu::AuditResult r = ctx->e->audit(q, subset, n_subset, cutoff);
+        *result = r.violations > 0 ? 1 : 0;
+        if (n_violations) *n_violations = r.violations;
+        if (min_distance) *min_distance = r.min_distance;
+        return DABD_GPU_OK;
+    });
+}
+
 dabd_gpu_status dabd_gpu_objective(dabd_gpu_ctx* ctx, int n_local, const int* local,
                                    const double* kappa, const double* q_tilde, int n_anchor,
                                    const int* anchor_body, const double* anchor_zu,

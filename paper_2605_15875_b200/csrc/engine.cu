@@ -97,6 +97,7 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     trace_dev_.resize(8 * static_cast<size_t>(trace_cap_));
     qd_start_.resize(6 * std::max(hs_.nb, 1));
     if (const char* e = std::getenv("DABD_GPU_NO_GRAPH")) use_graph_ = e[0] == '0';
+    if (const char* e = std::getenv("DABD_GPU_PCG_PHASES")) pcg_phases_ = e[0] == '1';
     if (const char* e = std::getenv("DABD_SKIN_MIN")) skin_min_ = std::atof(e);
     if (const char* e = std::getenv("DABD_SKIN_GROW")) skin_grow_ = std::atof(e);
     sync();
@@ -321,6 +322,7 @@ SolverView Engine::view() {
     v.kappa_arap = frame_params_.arap_stiffness;
     v.project = project_;
     v.perf = perf_.get();
+    v.pcg_phases = pcg_phases_;
     v.err = err_.get();
     return v;
 }
@@ -775,6 +777,16 @@ double Engine::ccd_toi(const double* q0, const double* q1, const int* subset, in
     const double earliest = e[0];
     if (earliest > 1.0) return 1.0;
     return std::min(1.0, 0.9 * earliest);
+}
+
+AuditResult Engine::audit(const double* q, const int* subset, int n_subset, double cutoff) {
+    const std::vector<int> sub = subset_sorted(subset, n_subset, hs_.nb);
+    const double* qd = q_.get();
+    if (q) {
+        audit_q_.upload(q, 6 * static_cast<size_t>(hs_.nb), s_);
+        qd = audit_q_.get();
+    }
+    return auditor_.run(ds_.view(), qd, sub, cutoff, s_);
 }
 
 void Engine::holder_masks(const double* q, int np, const double* planes, double w, uint32_t* out) {

@@ -5,6 +5,7 @@
 // proj/src/sim.cpp:186-249 (num_workers == 0).
 #pragma once
 
+#include "audit.hpp"
 #include "geometry.cuh"
 #include "kernels.hpp"
 #include "scene.hpp"
@@ -84,6 +85,9 @@ class Engine {
     void objective(const ObjectiveIn& in, const double* q, int mode, double* value, double* grad,
                    double* hess_dense, int* active, int* candidates);
     NewtonResult newton_solve(const ObjectiveIn& in, double* q, int max_iters, double tol);
+    // intersection_test + minimum distance (audit.cu); q == nullptr audits
+    // the device-resident current state.
+    AuditResult audit(const double* q, const int* subset, int n_subset, double cutoff);
 
     // ---- stepping ----
     void run_frames(int n, FrameStats* stats);
@@ -216,6 +220,9 @@ class Engine {
     int project_ = 1;
     DBuf<double> pbuf_, pcg_part_;
     DBuf<DevPerf> perf_;
+    Auditor auditor_;
+    DBuf<double> audit_q_;
+    int pcg_phases_ = 0;
 
     // fixed capacities (graph-safe) and the captured N=1 frame
     int cap_ = 0;

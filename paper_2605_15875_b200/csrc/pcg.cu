@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     bool done = !act;
     double inv_gamma_old = 0.0, inv_alpha_old = 0.0, bnorm2 = 0.0;
     int it = 0;
-    const bool timed = sv.perf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    const bool timed = sv.pcg_phases && sv.perf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
     unsigned long long ph[8] = {}, tc = clock64();
     auto mark = [&](int k) {
         if (timed) {

@@ -56,6 +56,7 @@ struct DevPerf {
 
 struct SolverView {
     DevPerf* perf = nullptr;
+    int pcg_phases = 0; // per-phase clock64 accounting in k_pcg_cluster (DABD_GPU_PCG_PHASES=1)
     SceneView sc;
     int n_inst = 0, n_rows = 0, n_parts = 0, part_base = 0;
     // instances

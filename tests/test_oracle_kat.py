@@ -280,6 +280,18 @@ def test_intersection_cases():  # test_geometry.cpp:217-245
     assert s.intersection_test(s.q0)
 
 
+def test_min_pair_distance():  # tests/support/oracles.cpp:153-173
+    s = O.Scene(scene_of([[square(0.5)], [square(0.5, (1.5, 0))]]))
+    assert s.min_pair_distance(s.q0) == 0.5
+    s = O.Scene(scene_of([[square(0.5)], [square(0.5, (1.5, 1.5))]]))
+    assert abs(s.min_pair_distance(s.q0) - np.sqrt(0.5)) < 1e-15  # corner to corner
+    # two touching statics are skipped unless asked for
+    s = O.Scene(scene_of([[square(0.5)], [square(0.5, (1.0, 0))], [square(0.5, (0, 3))]],
+                         static=[True, True, False]))
+    assert s.min_pair_distance(s.q0, skip_static_pairs=False) == 0.0
+    assert s.min_pair_distance(s.q0) == 2.0
+
+
 # ---------------------------------------------------------------- partition (test_partition.cpp)
 
 MID = np.array([[0.0, 0.0, -1.0, 0.0]])

@@ -14,6 +14,7 @@ def main():
     from paper_2605_15875_b200 import api
     from paper_2605_15875_b200.scene import make_scenario
 
+    os.environ["DABD_GPU_PCG_PHASES"] = "1"  # read at context creation
     lib = L.load()
     scene = sys.argv[1] if len(sys.argv) > 1 else "pile-1k"
     ctx = api.Context(api.Scene(make_scenario(scene)))

@@ -1,6 +1,6 @@
 """Frames/s and solver counts of the larger BASELINE.json configs on ONE GPU
-(partitions batched on the device), plus the global minimum broad-phase
-distance after the run as a penetration sanity check.
+(partitions batched on the device), plus the device audit of the final
+state (intersection_test + minimum point-edge distance, dabd_gpu_audit).
 
 python tools/scale_probe.py scene:workers:frames [...]
    e.g. pour-10k:8:20 sweep-100k:8:5 hetero-1000:2:20 cubes-64:2:50
@@ -34,9 +34,9 @@ def main():
         st = ctx.run_frames(frames)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t1
-        q, _ = ctx.state()
-        cand = ctx.broad_phase(q, sd.params.d_hat)
-        pairs, d = ctx.narrow_phase(q, cand, sd.params.d_hat)
+        t2 = time.perf_counter()
+        hit, nviol, dmin = ctx.audit(None, cutoff=sd.params.d_hat)  # device state, no copies
+        t_audit = time.perf_counter() - t2
         out = {
             "scene": name, "bodies": sc.n, "workers": workers, "frames": frames,
             "setup_s": t1 - t0, "ms_per_frame": 1e3 * dt / frames, "steps_per_s": frames / dt,
@@ -45,7 +45,8 @@ def main():
             "pcg_per_frame": sum(s["pcg_iterations"] for s in st) / frames,
             "attempts": sum(s["attempts"] for s in st), "committed": sum(s["committed"] for s in st),
             "max_contacts": max(s["max_contacts"] for s in st),
-            "active_pairs_end": int(len(d)), "min_d_end": float(d.min()) if len(d) else None,
+            "intersecting_end": hit, "violating_pairs_end": nviol, "min_distance_end": dmin,
+            "audit_ms": 1e3 * t_audit,
         }
         print(json.dumps(out), flush=True)
 
