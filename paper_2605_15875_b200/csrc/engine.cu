@@ -341,8 +341,7 @@ ContactView Engine::cview() {
     c.ls = lstate_.get();
     c.cval = cval_.get();
     c.cgrad = cgrad_.get();
-    c.cmat = cmat_.get();
-    c.cgeo = cgeo_.get();
+    c.cblk = cblk_.get();
     return c;
 }
 
@@ -378,14 +377,13 @@ void Engine::prepare_solver() {
         graph_ok_ = false;
     }
     const size_t C = static_cast<size_t>(cap_);
-    const size_t before = cflag_.capacity() + act_.capacity() + cmat_.capacity();
+    const size_t before = cflag_.capacity() + act_.capacity() + cblk_.capacity();
     cflag_.resize(C);
     sval_.resize(C);
     act_.resize(C);
     cval_.resize(C);
     cgrad_.resize(12 * C);
-    cmat_.resize(21 * C);
-    cgeo_.resize(6 * C);
+    cblk_.resize(108 * C);
     invalidate_list();
     bkey_.resize(C);
     bkey_sorted_.resize(C);
@@ -402,7 +400,7 @@ void Engine::prepare_solver() {
                                                det_.fmt().total_bits()));
     temp_bytes_ = std::max(t1, t2);
     temp_.resize(temp_bytes_);
-    if (cflag_.capacity() + act_.capacity() + cmat_.capacity() != before) graph_ok_ = false;
+    if (cflag_.capacity() + act_.capacity() + cblk_.capacity() != before) graph_ok_ = false;
     cfmt_ = det_.fmt();
 }
 

@@ -185,7 +185,7 @@ class Engine {
     DBuf<double> sval_;
     DBuf<unsigned long long> ckey_, bkey_, bkey_sorted_;
     DBuf<int> bidx_, perm_b_, aoff_, boff_, nsel_;
-    DBuf<double> cval_, cgrad_, cmat_, cgeo_;
+    DBuf<double> cval_, cgrad_, cblk_;
     DBuf<int> act_;
     // skin list (ListState in solver.hpp): det_ holds the list keys
     DBuf<double> qref_, iskin_, iskin_next_;

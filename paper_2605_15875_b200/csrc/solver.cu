@@ -182,6 +182,53 @@ __global__ void k_filter(SolverView sv, const unsigned long long* keys, int n, c
 }
 
 // ---------------------------------------------------------------------------
+// World-space contact Hessian C (6x6 over (p, e0, e1), symmetric) -> the
+// three DoF-space 6x6 blocks the row assembly sums. x = A xbar + p gives
+// d(world)/d(q) = J(xbar) with J = [[1, 0, x, y, 0, 0], [0, 1, 0, 0, x, y]]:
+//   TL = J(rp)^T C_pp J(rp), BR = sum_kl J(rk)^T C_kl J(rl),
+//   TR = sum_l J(rp)^T C_pl J(rl)  (BL = TR^T).
+// DoF alpha -> (world component, coefficient index into (1, x, y)).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int dof_comp(int alpha) { return (alpha == 1 || alpha >= 4) ? 1 : 0; }
+__host__ __device__ constexpr int dof_idx(int alpha) { return alpha <= 1 ? 0 : (alpha == 2 || alpha == 4 ? 1 : 2); }
+
+__device__ __forceinline__ double dof_coef(V2 x, int idx) { return idx == 0 ? 1.0 : (idx == 1 ? x.x : x.y); }
+
+__device__ __forceinline__ void store_dof_blocks(double* dst, const double (&C)[6][6], V2 rp, V2 r0,
+                                                 V2 r1) {
+    const V2 pt[3] = {rp, r0, r1};
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+        const int ca = dof_comp(a), ia = dof_idx(a);
+        double tl[6], br[6], tr[6];
+#pragma unroll
+        for (int b = 0; b < 6; ++b) {
+            const int cb = dof_comp(b), ib = dof_idx(b);
+            // same term order as a (ra outer, rb inner) double loop
+            tl[b] = 0.0 + C[ca][cb] * (dof_coef(pt[0], ia) * dof_coef(pt[0], ib));
+            double v = 0.0;
+#pragma unroll
+            for (int ra = 1; ra <= 2; ++ra)
+#pragma unroll
+                for (int rb = 1; rb <= 2; ++rb)
+                    v += C[2 * ra + ca][2 * rb + cb] * (dof_coef(pt[ra], ia) * dof_coef(pt[rb], ib));
+            br[b] = v;
+            double w = 0.0;
+#pragma unroll
+            for (int rb = 1; rb <= 2; ++rb) w += C[ca][2 * rb + cb] * (dof_coef(pt[0], ia) * dof_coef(pt[rb], ib));
+            tr[b] = w;
+        }
+        double2* d2 = reinterpret_cast<double2*>(dst + 6 * a);
+#pragma unroll
+        for (int b = 0; b < 6; b += 2) {
+            d2[b / 2] = make_double2(tl[b], tl[b + 1]);
+            d2[18 + b / 2] = make_double2(br[b], br[b + 1]);
+            d2[36 + b / 2] = make_double2(tr[b], tr[b + 1]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Contact terms with the rank-6 PSD projection (energy.cpp:63-94,
 // objective.cpp:184-207).
 // ---------------------------------------------------------------------------
@@ -198,12 +245,6 @@ __global__ void __launch_bounds__(kB)
         const double* qa = sv.iq + 6 * a;
         const double* qb = sv.iq + 6 * b;
         const V2 P = world_point(qa, rp), E0 = world_point(qb, r0), E1 = world_point(qb, r1);
-        {
-            double2* gg = reinterpret_cast<double2*>(cv.cgeo + 6 * c);
-            gg[0] = make_double2(rp.x, rp.y);
-            gg[1] = make_double2(r0.x, r0.y);
-            gg[2] = make_double2(r1.x, r1.y);
-        }
         double g[6], A[6][6];
         const double d = pe_distance_full(P, E0, E1, g, A);
         if (!(d > 0.0)) {
@@ -234,79 +275,99 @@ __global__ void __launch_bounds__(kB)
 #pragma unroll
             for (int j = 0; j < 6; ++j) A[i][j] = w * (br.ddb * (g[i] * g[j]) + br.db * A[i][j]);
         if (!sv.project) {
-            double* cm = cv.cmat + 21 * c;
-            int idx = 0;
-#pragma unroll
-            for (int i = 0; i < 6; ++i)
-#pragma unroll
-                for (int j = i; j < 6; ++j) cm[idx++] = A[i][j];
+            store_dof_blocks(cv.cblk + 108 * static_cast<size_t>(c), A, rp, r0, r1);
             continue;
         }
-        // G = t t^T = L L^T (closed form), B = L^T A L
+        // G = t t^T = L L^T in closed form: L = Lp (x) I2 with the 3x3 lower
+        // Lp = [[sp, 0, 0], [0, l00, 0], [0, l10, l11]] over the points
+        // (p, e0, e1), and B = L^T A L. A annihilates the two rigid
+        // translations T = 1 (x) e_c (d is translation invariant), so B
+        // annihilates L^{-1} T = u (x) e_c with u = Lp^{-1} 1: the projection
+        // lives on the 4-dim complement Q = W (x) I2, W = an orthonormal basis
+        // of u-perp (Householder). With Kp = Lp W and Pp = Lp^{-T} W:
+        //   B4 = (Kp (x) I2)^T A (Kp (x) I2),  C = (Pp (x) I2) clamp(B4) (Pp (x) I2)^T
+        // = L^{-T} clamp(B) L^{-1}: a 4x4 Jacobi instead of 6x6.
         const double sp = sqrt(1.0 + rp.x * rp.x + rp.y * rp.y);
         const double g00 = 1.0 + r0.x * r0.x + r0.y * r0.y;
         const double g01 = 1.0 + r0.x * r1.x + r0.y * r1.y;
         const double g11 = 1.0 + r1.x * r1.x + r1.y * r1.y;
         const double l00 = sqrt(g00), l10 = g01 / l00, l11 = sqrt(fmax(g11 - l10 * l10, 1e-300));
-        // L (6x6 lower): diag(sp, sp, l00, l00, l11, l11), L[4][2]=L[5][3]=l10
-        double Bm[6][6];
-        // AL = A * L
-        double AL[6][6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            AL[i][0] = A[i][0] * sp;
-            AL[i][1] = A[i][1] * sp;
-            AL[i][2] = A[i][2] * l00 + A[i][4] * l10;
-            AL[i][3] = A[i][3] * l00 + A[i][5] * l10;
-            AL[i][4] = A[i][4] * l11;
-            AL[i][5] = A[i][5] * l11;
-        }
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-            Bm[0][j] = sp * AL[0][j];
-            Bm[1][j] = sp * AL[1][j];
-            Bm[2][j] = l00 * AL[2][j] + l10 * AL[4][j];
-            Bm[3][j] = l00 * AL[3][j] + l10 * AL[5][j];
-            Bm[4][j] = l11 * AL[4][j];
-            Bm[5][j] = l11 * AL[5][j];
-        }
-#pragma unroll
-        for (int i = 0; i < 6; ++i)
-#pragma unroll
-            for (int j = i + 1; j < 6; ++j) {
-                const double m = 0.5 * (Bm[i][j] + Bm[j][i]);
-                Bm[i][j] = m;
-                Bm[j][i] = m;
-            }
-        clamp_psd<6>(Bm);
-        // C = L^{-T} B+ L^{-1}; with Linv: diag(1/sp,1/sp,1/l00,1/l00,1/l11,1/l11),
-        // Linv[4][2] = Linv[5][3] = -l10/(l00 l11)
         const double ip = 1.0 / sp, i0 = 1.0 / l00, i1 = 1.0 / l11, m10 = -l10 / (l00 * l11);
-        double BL[6][6]; // B+ Linv
+        double W[3][2];
+        {
+            double u[3] = {ip, i0, m10 + i1};
+            const double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
 #pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            BL[i][0] = Bm[i][0] * ip;
-            BL[i][1] = Bm[i][1] * ip;
-            BL[i][2] = Bm[i][2] * i0 + Bm[i][4] * m10;
-            BL[i][3] = Bm[i][3] * i0 + Bm[i][5] * m10;
-            BL[i][4] = Bm[i][4] * i1;
-            BL[i][5] = Bm[i][5] * i1;
+            for (int k = 0; k < 3; ++k) u[k] /= un;
+            // Householder H = I - 2 v v^T / v^T v, v = u + sign(u0) e0: H u = -sign(u0) e0,
+            // so columns 1 and 2 of H span u-perp (orthonormal)
+            const double sg = u[0] >= 0.0 ? 1.0 : -1.0;
+            const double v[3] = {u[0] + sg, u[1], u[2]};
+            const double f = 2.0 / (v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) W[k][j] = (k == j + 1 ? 1.0 : 0.0) - f * v[k] * v[j + 1];
         }
-        double* cm = cv.cmat + 21 * c;
-        int idx = 0;
+        double Kp[3][2], Pp[3][2];
 #pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            // row i of Linv^T BL: Linv^T[i][k] = Linv[k][i]
+        for (int j = 0; j < 2; ++j) {
+            Kp[0][j] = sp * W[0][j];
+            Kp[1][j] = l00 * W[1][j];
+            Kp[2][j] = l10 * W[1][j] + l11 * W[2][j];
+            Pp[0][j] = ip * W[0][j];
+            Pp[1][j] = i0 * W[1][j] + m10 * W[2][j];
+            Pp[2][j] = i1 * W[2][j];
+        }
+        // AK = A (Kp (x) I2): column (b, d) -> 2b + d
+        double AK[6][4];
 #pragma unroll
-            for (int j = i; j < 6; ++j) {
-                double val;
-                if (i < 2) val = ip * BL[i][j];
-                else if (i == 2) val = i0 * BL[2][j] + m10 * BL[4][j];
-                else if (i == 3) val = i0 * BL[3][j] + m10 * BL[5][j];
-                else val = i1 * BL[i][j];
-                cm[idx++] = val;
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int d = 0; d < 2; ++d)
+                    AK[r][2 * b + d] = A[r][d] * Kp[0][b] + A[r][2 + d] * Kp[1][b] + A[r][4 + d] * Kp[2][b];
+        double B4[4][4];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+                for (int col = 0; col < 4; ++col)
+                    B4[2 * a + c2][col] = Kp[0][a] * AK[c2][col] + Kp[1][a] * AK[2 + c2][col] +
+                                          Kp[2][a] * AK[4 + c2][col];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = i + 1; j < 4; ++j) {
+                const double m = 0.5 * (B4[i][j] + B4[j][i]);
+                B4[i][j] = m;
+                B4[j][i] = m;
             }
-        }
+        clamp_psd<4>(B4);
+        // C = (Pp (x) I2) B4+ (Pp (x) I2)^T
+        double PE[6][4]; // (Pp (x) I2) B4+
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+                for (int col = 0; col < 4; ++col)
+                    PE[2 * i + c2][col] = Pp[i][0] * B4[c2][col] + Pp[i][1] * B4[2 + c2][col];
+        double Cf[6][6];
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int d = 0; d < 2; ++d) {
+                    if (2 * j + d < r) continue;
+                    const double val = PE[r][d] * Pp[j][0] + PE[r][2 + d] * Pp[j][1];
+                    Cf[r][2 * j + d] = val;
+                    Cf[2 * j + d][r] = val;
+                }
+        store_dof_blocks(cv.cblk + 108 * static_cast<size_t>(c), Cf, rp, r0, r1);
     }
 }
 
@@ -412,44 +473,11 @@ __global__ void k_contact_select(SolverView sv, ContactView cv, const Box* box) 
 
 // ---------------------------------------------------------------------------
 // Deterministic BSR assembly (ELL storage, kEll off-diagonal blocks / row):
-// one warp per row, lane l owns entries l and l + 32 of each 6x6 block.
-// The contact's projected world-space C (6x6 over (p, e0, e1)) is mapped to
-// DoF space on the fly: x = A xbar + p gives d(world)/d(q) = J(xbar) with
-// J = [[1, 0, x, y, 0, 0], [0, 1, 0, 0, x, y]], so
-//   TL = J(rp)^T C_pp J(rp), BR = sum_kl J(rk)^T C_kl J(rl),
-//   TR = sum_l J(rp)^T C_pl J(rl), BL = TR^T.
+// one warp per row, lane l owns entries l and l + 32 of each 6x6 block and
+// sums the contacts' precomputed DoF-space blocks (store_dof_blocks) in list
+// order: TL where the row's body is the point body, BR where it is the edge
+// body; off-diagonal blocks TR / BL = TR^T grouped by partner instance.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double cm_at(const double* cm, int i, int j) {
-    if (i > j) {
-        const int t = i;
-        i = j;
-        j = t;
-    }
-    return cm[i * 6 - (i * (i - 1)) / 2 + (j - i)]; // upper-triangle row-major
-}
-
-// DoF alpha -> (world component, coefficient index into (1, x, y))
-__device__ __forceinline__ void dof_map(int alpha, int& comp, int& idx) {
-    // gx = {0, 2, 3} (x component), gy = {1, 4, 5} (y component)
-    comp = (alpha == 1 || alpha >= 4) ? 1 : 0;
-    idx = alpha <= 1 ? 0 : (alpha == 2 || alpha == 4 ? 1 : 2);
-}
-
-__device__ __forceinline__ double coef(const double* geo, int pt, int idx) {
-    return idx == 0 ? 1.0 : geo[2 * pt + idx - 1];
-}
-
-// entry (alpha, beta) of the block of world points (pa -> rows, pb -> cols)
-// summed over the given point pairs; pt 0 = p, 1 = e0, 2 = e1.
-__device__ __forceinline__ double blk_entry(const double* cm, const double* geo, int ca, int ia,
-                                            int cb, int ib, int ra0, int ra1, int rb0, int rb1) {
-    double v = 0.0;
-    for (int ra = ra0; ra <= ra1; ++ra)
-        for (int rb = rb0; rb <= rb1; ++rb)
-            v += cm_at(cm, 2 * ra + ca, 2 * rb + cb) * (coef(geo, ra, ia) * coef(geo, rb, ib));
-    return v;
-}
-
 __global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv, double* row_trace) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -457,13 +485,8 @@ __global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv,
     // the two entries of this lane
     const int e0 = lane, e1 = lane + 32;
     const bool has1 = e1 < 36;
-    int ca0, ia0, cb0, ib0, ca1 = 0, ia1 = 0, cb1 = 0, ib1 = 0;
-    dof_map(e0 / 6, ca0, ia0);
-    dof_map(e0 % 6, cb0, ib0);
-    if (has1) {
-        dof_map(e1 / 6, ca1, ia1);
-        dof_map(e1 % 6, cb1, ib1);
-    }
+    // the transposed entries (BL = TR^T)
+    const int t0 = 6 * (e0 % 6) + e0 / 6, t1 = has1 ? 6 * (e1 % 6) + e1 / 6 : 0;
     for (int r = gw; r < sv.n_rows; r += nw) {
         const int p = sv.rpart[r] - sv.part_base;
         if (!sv.ps[p].active) continue;
@@ -475,19 +498,17 @@ __global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv,
         const int b0 = cv.boff[i], b1 = cv.boff[i + 1];
         for (int c = a0; c < a1; ++c) { // point body: TL, gradient 0..5
             if (!cv.flag[c]) continue;
-            const double* cm = cv.cmat + 21 * c;
-            const double* geo = cv.cgeo + 6 * c;
-            d0 += blk_entry(cm, geo, ca0, ia0, cb0, ib0, 0, 0, 0, 0);
-            if (has1) d1 += blk_entry(cm, geo, ca1, ia1, cb1, ib1, 0, 0, 0, 0);
+            const double* bk = cv.cblk + 108 * static_cast<size_t>(c);
+            d0 += bk[e0];
+            if (has1) d1 += bk[e1];
             if (lane < 6) g += cv.cgrad[12 * c + lane];
         }
         for (int t = b0; t < b1; ++t) { // edge body: BR, gradient 6..11
             const int c = cv.perm_b[t];
             if (!cv.flag[c]) continue;
-            const double* cm = cv.cmat + 21 * c;
-            const double* geo = cv.cgeo + 6 * c;
-            d0 += blk_entry(cm, geo, ca0, ia0, cb0, ib0, 1, 2, 1, 2);
-            if (has1) d1 += blk_entry(cm, geo, ca1, ia1, cb1, ib1, 1, 2, 1, 2);
+            const double* bk = cv.cblk + 108 * static_cast<size_t>(c) + 36;
+            d0 += bk[e0];
+            if (has1) d1 += bk[e1];
             if (lane < 6) g += cv.cgrad[12 * c + 6 + lane];
         }
         if (lane < 6) sv.rgrad[6 * r + lane] = g;
@@ -523,20 +544,18 @@ __global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv,
                 cv.fmt.unpack(cv.key[ia], ca, cb, vv, ee);
                 if (cb != partner) break;
                 if (!cv.flag[ia] || prow < 0) continue;
-                const double* cm = cv.cmat + 21 * ia;
-                const double* geo = cv.cgeo + 6 * ia;
-                o0 += blk_entry(cm, geo, ca0, ia0, cb0, ib0, 0, 0, 1, 2);
-                if (has1) o1 += blk_entry(cm, geo, ca1, ia1, cb1, ib1, 0, 0, 1, 2);
+                const double* bk = cv.cblk + 108 * static_cast<size_t>(ia) + 72;
+                o0 += bk[e0];
+                if (has1) o1 += bk[e1];
             }
             for (; ib < b1; ++ib) { // BL = TR^T: rows = edge body (this), cols = point body
                 const int c = cv.perm_b[ib];
                 cv.fmt.unpack(cv.key[c], ca, cb, vv, ee);
                 if (ca != partner) break;
                 if (!cv.flag[c] || prow < 0) continue;
-                const double* cm = cv.cmat + 21 * c;
-                const double* geo = cv.cgeo + 6 * c;
-                o0 += blk_entry(cm, geo, cb0, ib0, ca0, ia0, 0, 0, 1, 2);
-                if (has1) o1 += blk_entry(cm, geo, cb1, ib1, ca1, ia1, 0, 0, 1, 2);
+                const double* bk = cv.cblk + 108 * static_cast<size_t>(c) + 72;
+                o0 += bk[t0];
+                if (has1) o1 += bk[t1];
             }
             if (prow < 0) continue;
             if (nblk >= kEll) {

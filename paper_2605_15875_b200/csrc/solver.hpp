@@ -135,8 +135,10 @@ struct ContactView {
     ListState* ls = nullptr;      // ls->n_act = number of entries in act
     double* cval = nullptr;       // [cap] weighted barrier value (0 when inactive)
     double* cgrad = nullptr;      // [cap][12] weighted gradient
-    double* cmat = nullptr;       // [cap][21] projected world-space 6x6 (upper, row-major)
-    double* cgeo = nullptr;       // [cap][6] rest points (p, e0, e1) of the contact
+    // [cap][108] DoF-space blocks of the projected contact Hessian, row-major
+    // 6x6 each: TL (point body x point body), BR (edge body x edge body), TR
+    // (point body rows x edge body cols); BL = TR^T
+    double* cblk = nullptr;
 };
 
 } // namespace dabd_gpu
