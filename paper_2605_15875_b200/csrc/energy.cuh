@@ -107,6 +107,32 @@ __device__ __forceinline__ void jacobi_eig(double (&a)[N][N], double (&v)[N][N])
     }
 }
 
+// True iff the symmetric a is positive definite (every Cholesky pivot > 0):
+// then clamp_psd(a) == a up to rounding and the eigensolve can be skipped.
+template <int N>
+__device__ __forceinline__ bool is_pd(const double (&a)[N][N]) {
+    double l[N][N];
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        double d = a[j][j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) d -= l[j][k] * l[j][k];
+        ok = ok && d > 0.0;
+        const double ljj = sqrt(fmax(d, 1e-300));
+        l[j][j] = ljj;
+        const double inv = 1.0 / ljj;
+#pragma unroll
+        for (int i = j + 1; i < N; ++i) {
+            double v = a[i][j];
+#pragma unroll
+            for (int k = 0; k < j; ++k) v -= l[i][k] * l[j][k];
+            l[i][j] = v * inv;
+        }
+    }
+    return ok;
+}
+
 // In place: a <- V max(Lambda, 0) V^T.
 template <int N>
 __device__ __forceinline__ void clamp_psd(double (&a)[N][N]) {

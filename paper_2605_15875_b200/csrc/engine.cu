@@ -469,7 +469,9 @@ void Engine::enq_energy(const double* q, int which, double PartState::*field) {
                        partial_.get(), dst, kPsStride, true, s_);
 }
 
-void Engine::enq_derivatives() {
+// fused: the trace sum, kOpEps and the preconditioner factor are left to
+// the fused cluster PCG (pcg_fused()).
+void Engine::enq_derivatives(bool fused) {
     SolverView v = view();
     const ContactView cv = cview();
     launch_inst_boxes(v.sc, iview(iq_.get(), iq_.get()), false, frame_params_.d_hat, box_.get(),
@@ -478,19 +480,31 @@ void Engine::enq_derivatives() {
     launch_contact_select(v, cv, box_.get(), s_);
     launch_contact_terms(v, cv, s_);
     launch_assemble(v, cv, rowtmp_.get(), s_);
+    if (fused) return;
     launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
                        ps_field(ps_.get(), &PartState::trace), kPsStride, false, s_);
     launch_scalar(ps_.get(), P_, kOpEps, ctrl_.get(), hd_, 0.0, 0, err_.get(), s_);
     if (project_) launch_precond(v, s_); // unprojected blocks (objective mode 3) may be indefinite
 }
 
-void Engine::enq_pcg() {
-    if (n_rows_ == 0) return;
+int Engine::max_part_rows() const {
     int max_rows = 0;
     for (int p = 0; p < P_; ++p) max_rows = std::max(max_rows, h_pro_[p + 1] - h_pro_[p]);
+    return max_rows;
+}
+
+bool Engine::pcg_fused() const {
+    return n_rows_ > 0 && project_ && max_part_rows() <= kClusterPcgMaxRows &&
+           !std::getenv("DABD_GPU_NO_FUSED_PCG");
+}
+
+void Engine::enq_pcg(bool fused) {
+    if (n_rows_ == 0) return;
+    const int max_rows = max_part_rows();
     if (max_rows <= kClusterPcgMaxRows) {
         // small partitions: one thread-block cluster per partition (DSMEM dots)
-        launch_pcg_cluster(view(), max_rows, pbuf_.get(), pcg_tol_, pcg_max_, s_);
+        PcgFuse f{rowtmp_.get(), ctrl_.get(), hd_};
+        launch_pcg_cluster(view(), max_rows, pbuf_.get(), pcg_tol_, pcg_max_, s_, fused ? &f : nullptr);
     } else {
         launch_pcg_persistent(view(), pbuf_.get(), pcg_part_.get(), rowtmp_.get(), pcg_tol_,
                               pcg_max_, s_);
@@ -501,8 +515,10 @@ void Engine::enq_pcg() {
 void Engine::enq_newton_head(int max_iters) {
     SolverView v = view();
     launch_scalar(ps_.get(), P_, kOpIterBegin, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
-    enq_derivatives();
-    enq_pcg();
+    const bool fused = pcg_fused();
+    enq_derivatives(fused);
+    enq_pcg(fused);
+    if (fused) return; // ||dq||_inf and kOpNewtonCheck ran inside the PCG kernel
     launch_dq_inf(v, s_);
     launch_scalar(ps_.get(), P_, kOpNewtonCheck, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
 }

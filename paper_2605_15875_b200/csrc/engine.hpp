@@ -117,8 +117,10 @@ class Engine {
     void enq_list_rebuild();
     void invalidate_list();
     void enq_energy(const double* q, int which, double PartState::*field);
-    void enq_derivatives();
-    void enq_pcg();
+    void enq_derivatives(bool fused = false);
+    void enq_pcg(bool fused = false);
+    int max_part_rows() const;
+    bool pcg_fused() const;
     void enq_newton_head(int max_iters);
     void enq_newton_ccd();
     void enq_ls_trial();

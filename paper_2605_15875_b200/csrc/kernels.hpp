@@ -54,8 +54,11 @@ int pcg_grid_size(int n_rows);
 // used while every partition has at most kClusterPcgMaxRows rows.
 constexpr int kClusterPcgMaxRows = 4096;
 int pcg_cluster_size();
+struct PcgFuse;
+// fuse != nullptr: the fused Newton head (trace/eps/Dinv before, ||dq||_inf and
+// the kOpNewtonCheck decision after; see PcgArgs in pcg.cu).
 void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbuf, double tol,
-                        int max_iters, cudaStream_t s);
+                        int max_iters, cudaStream_t s, const PcgFuse* fuse = nullptr);
 void launch_pcg_persistent(const SolverView& sv, double* pbuf, double* partials, double* rowval,
                            double tol, int max_iters, cudaStream_t s);
 
@@ -90,6 +93,12 @@ struct FrameCtrl {
 struct CondHandles {
     unsigned long long admm = 0, newton = 0, step = 0, ls = 0; // cudaGraphConditionalHandle values
     int graph = 0;
+};
+
+struct PcgFuse {
+    const double* row_trace; // [n_rows] trace of each assembled diagonal block (k_assemble)
+    FrameCtrl* ctrl;
+    CondHandles hd;          // hd.step is set from the convergence decision
 };
 
 void launch_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHandles h, double tol,

@@ -60,6 +60,16 @@ struct PcgArgs {
     double* rowval;  // [n_rows] per-row scratch
     double tol;
     int max_iters;
+    // fused Newton head (cluster kernel): the kernel also sums the row traces,
+    // sets eps (newton.cpp:20-24, kOpEps), factors the block-Jacobi
+    // preconditioner, and after the solve computes ||dq||_inf and takes the
+    // convergence decision of newton.cpp:30-36 (kOpNewtonCheck) for every
+    // partition, steering the graph's IF node: 5 launches fewer per iteration.
+    int fused;
+    const double* row_trace; // [n_rows] trace of each assembled diagonal block
+    FrameCtrl* ctrl;
+    CondHandles hd;
+    unsigned* ticket;        // last-cluster detection, reset by the last one
 };
 
 // Block-local, partition-segmented sum of rowval over this block's chunk,
@@ -305,7 +315,13 @@ struct ClusterScalars {
     double red[kCW][3];
     unsigned long long bar[2]; // per-parity mbarriers (st.async complete_tx)
     unsigned long long stage_bar;
-    int n_remote, n_send, fallback;
+    int n_remote, n_send, fallback, nobulk;
+    int wsum[kCW];
+    int rlo[16], rcnt[16], rbase[16]; // rows this CTA needs from each peer (bulk mode)
+    int2 req[16];                     // per consumer: (first local row, count) it needs from us
+    int reqbase[16];                  // ... and where they land in its halo
+    double trc[16];                   // fused: every CTA's partial trace, by rank
+    double dqm[16];                   // fused: every CTA's max |dq|, by rank (rank 0 only)
 };
 
 struct SendEntry {
@@ -399,7 +415,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     const int nr = r1 - r0;
     const PartState& st = sv.ps[p];
     const bool act = st.active != 0 && R1 > R0;
-    const double eps = st.eps;
+    double eps = st.eps;
     // shared-memory carve-up (cmax_rows = chunk upper bound used at launch)
     const int V = 6 * cmax_rows;
     double* vm0 = reinterpret_cast<double*>(smem); // m = Dinv w, double-buffered by parity
@@ -430,8 +446,10 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         sc.n_remote = 0;
         sc.n_send = 0;
         sc.fallback = 0;
+        sc.nobulk = 0;
     }
     for (int i = threadIdx.x; i < 2 * 16 * 4; i += kCT) (&sc.tab[0][0][0])[i] = 0.0;
+    if (threadIdx.x < 16) sc.req[threadIdx.x] = make_int2(0, 0);
     for (int lr = threadIdx.x; lr < nr; lr += kCT) bstart[lr + 1] = sv.ell_cnt[r0 + lr] + 1;
     __syncthreads();
     if (warp == 0) { // warp-wide inclusive scan in chunks of 32 rows
@@ -455,7 +473,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             if (ncp > 0) bytes += 288u * ncp;
         }
         for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-        if (nr > 0) bytes += 288u * nr; // Dinv
+        if (nr > 0 && !a.fused) bytes += 288u * nr; // Dinv (the fused kernel factors it itself)
         if (lane == 0) mbar_expect(smem_u32(&sc.stage_bar), bytes);
         __syncwarp();
         const unsigned bar = smem_u32(&sc.stage_bar);
@@ -474,7 +492,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                              "r"(288u * (ncp - 1)), "r"(bar)
                              : "memory");
         }
-        if (lane == 0 && nr > 0)
+        if (lane == 0 && nr > 0 && !a.fused)
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                          ::"r"(smem_u32(dinv)), "l"(sv.rdinv + 36 * r0), "r"(288u * nr), "r"(bar)
                          : "memory");
@@ -482,21 +500,72 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     // every CTA's counters and barriers are initialised before any peer
     // appends to its send list
     cluster_barrier();
+    if (a.fused && warp == kCW - 1) { // this CTA's trace partial -> every peer's trc[rank]
+        double t = 0.0;
+        for (int lr = lane; lr < nr; lr += 32) t += a.row_trace[r0 + lr];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if (lane < csize) cl.map_shared_rank(&sc, lane)->trc[rank] = t;
+    }
     // column code of every staged block: >= 0 a row of this CTA, < 0 the
-    // remote slot -1 - j; the owning peer gets a send entry for slot j
-    for (int lr = warp; lr < nr; lr += kCW) {
-        const int r = r0 + lr;
-        const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
-        if (b0 + nb > cap_blocks && lane == 0) atomicOr(&sc.fallback, 1); // spilled blocks
-        for (int t = lane; t < nb && b0 + t < cap_blocks; t += 32) {
-            const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
-            const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
-            if (crank == rank) {
-                bcode[b0 + t] = cl_row;
-            } else {
-                const int j = atomicAdd(&sc.n_remote, 1);
+    // remote slot -1 - j. Remote columns are deduplicated: one halo slot per
+    // distinct remote row, slots numbered in partition-row order (a CTA-wide
+    // scan over marks kept in the halo buffer, which peers only write after
+    // the setup barrier), and the owning peer gets one send entry per slot.
+    {
+        const int R = R1 - R0;
+        int* mark = reinterpret_cast<int*>(halo);
+        if (4ll * R > 96ll * cap_blocks) { // marks do not fit: barrier path (never for <= 4096 rows)
+            if (threadIdx.x == 0) atomicOr(&sc.fallback, 1);
+        } else {
+            for (int i = threadIdx.x; i < R; i += kCT) mark[i] = 0;
+            __syncthreads();
+            for (int lr = warp; lr < nr; lr += kCW) {
+                const int r = r0 + lr;
+                const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
+                if (b0 + nb > cap_blocks && lane == 0) atomicOr(&sc.fallback, 1); // spilled blocks
+                for (int t = lane; t < nb && b0 + t < cap_blocks; t += 32) {
+                    const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+                    const int crank = (col - R0) / chunk;
+                    if (crank == rank) bcode[b0 + t] = (col - R0) - crank * chunk;
+                    else mark[col - R0] = 1;
+                }
+            }
+            __syncthreads();
+            // exclusive scan of the marks: thread t owns [t * per, (t + 1) * per)
+            const int per = (R + kCT - 1) / kCT;
+            const int i0 = min(R, threadIdx.x * per), i1 = min(R, i0 + per);
+            int cnt = 0;
+            for (int i = i0; i < i1; ++i) cnt += mark[i];
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (lane == 31) sc.wsum[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                const int v = lane < kCW ? sc.wsum[lane] : 0;
+                int w = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, w, o);
+                    if (lane >= o) w += u;
+                }
+                if (lane < kCW) sc.wsum[lane] = w - v;
+                if (lane == kCW - 1) sc.n_remote = w;
+            }
+            __syncthreads();
+            int j = sc.wsum[warp] + incl - cnt;
+            for (int i = i0; i < i1; ++i) {
+                if (!mark[i]) {
+                    mark[i] = -1;
+                    continue;
+                }
+                const int crank = i / chunk, cl_row = i - crank * chunk;
+                mark[i] = j;
                 rptr[j] = cl.map_shared_rank(vm0, crank) + 6 * cl_row;
-                bcode[b0 + t] = -1 - j;
                 ClusterScalars* peer = cl.map_shared_rank(&sc, crank);
                 const int e = atomicAdd(&peer->n_send, 1);
                 if (e < cap_blocks) {
@@ -505,20 +574,136 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 } else { // send list full: the whole cluster takes the barrier path
                     atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
                 }
+                ++j;
+            }
+            __syncthreads();
+            // bulk mode: per peer the contiguous range of its rows we need;
+            // the peer copies that range into our halo with one bulk DSMEM
+            // copy per iteration instead of one 16-byte st.async per value pair
+            if (warp < csize) {
+                int lo = 0x7fffffff, hi = -1;
+                for (int i = warp * chunk + lane; i < min(R, (warp + 1) * chunk); i += 32)
+                    if (mark[i] >= 0) {
+                        lo = min(lo, i);
+                        hi = max(hi, i);
+                    }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+                }
+                if (lane == 0) {
+                    sc.rlo[warp] = lo;
+                    sc.rcnt[warp] = hi >= lo ? hi - lo + 1 : 0;
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int h = 0;
+                for (int k = 0; k < csize; ++k) {
+                    sc.rbase[k] = h;
+                    h += sc.rcnt[k];
+                }
+                if (h > cap_blocks) atomicOr(&cl.map_shared_rank(&sc, 0)->nobulk, 1);
+            }
+            __syncthreads();
+            if (threadIdx.x < csize && sc.rcnt[threadIdx.x] > 0) {
+                const int k = threadIdx.x;
+                ClusterScalars* peer = cl.map_shared_rank(&sc, k);
+                peer->req[rank] = make_int2(sc.rlo[k] - k * chunk, sc.rcnt[k]);
+                peer->reqbase[rank] = sc.rbase[k];
             }
         }
     }
     mbar_wait(smem_u32(&sc.stage_bar), 0);
+    __syncthreads();
+    // any overflow in the cluster selects the barrier path everywhere
+    if (threadIdx.x == 0 && sc.fallback) atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
+    cluster_barrier(); // send lists, requests, trace partials and fallback flags complete
+    if (a.fused && act) { // kOpEps: eps = 1e-8 tr(H) / n (newton.cpp:20-24), same bits in every CTA
+        double trace = 0.0;
+        for (int k = 0; k < csize; ++k) trace += sc.trc[k];
+        eps = 1e-8 * trace / st.ndof;
+        if (rank == 0 && threadIdx.x == 0) {
+            sv.ps[p].trace = trace;
+            sv.ps[p].eps = eps;
+            ++sv.ps[p].iterations;
+        }
+    }
     for (int i = threadIdx.x; i < 6 * nr; i += kCT) { // (D + eps I)
         const int lr = i / 6, k = i - 6 * lr;
         const int b0 = bstart[lr];
         if (b0 < cap_blocks) blk[36 * b0 + 7 * k] += eps;
     }
     __syncthreads();
-    // any overflow in the cluster selects the barrier path everywhere
-    if (threadIdx.x == 0 && sc.fallback) atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
-    cluster_barrier(); // send lists and fallback flags complete
+    if (a.fused && act) { // block-Jacobi factor: Dinv = (D + eps I)^{-1} by Cholesky (k_precond)
+        for (int lr = threadIdx.x; lr < nr; lr += kCT) {
+            const int b0 = bstart[lr];
+            const double* d = b0 < cap_blocks ? blk + 36 * b0 : sv.rdiag + 36 * (r0 + lr);
+            const double ex = b0 < cap_blocks ? 0.0 : eps; // spilled diagonal: eps not staged
+            // one reciprocal square root per pivot, no divisions on the chain
+            double L[6][6], rd[6];
+            bool ok = true;
+#pragma unroll
+            for (int j = 0; j < 6; ++j) {
+                double s = d[6 * j + j] + ex;
+#pragma unroll
+                for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
+                if (!(s > 0.0)) ok = false;
+                rd[j] = rsqrt(fmax(s, 1e-300));
+#pragma unroll
+                for (int i = j + 1; i < 6; ++i) {
+                    double t = d[6 * i + j];
+#pragma unroll
+                    for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
+                    L[i][j] = t * rd[j];
+                }
+            }
+            if (!ok) atomicCAS(sv.err, 0, kErrFactor);
+            double Li[6][6];
+#pragma unroll
+            for (int c = 0; c < 6; ++c)
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    double s = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+                    for (int k = 0; k < i; ++k)
+                        if (k >= c) s -= L[i][k] * Li[k][c];
+                    Li[i][c] = (i < c) ? 0.0 : s * rd[i];
+                }
+            double* o = dinv + 36 * lr;
+#pragma unroll
+            for (int r = 0; r < 6; ++r)
+#pragma unroll
+                for (int c = r; c < 6; ++c) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 6; ++k)
+                        if (k >= r && k >= c) s += Li[k][r] * Li[k][c];
+                    o[6 * r + c] = s;
+                    o[6 * c + r] = s;
+                }
+        }
+        __syncthreads();
+    }
     const bool push = cl.map_shared_rank(&sc, 0)->fallback == 0;
+    const bool bulk = push && cl.map_shared_rank(&sc, 0)->nobulk == 0;
+    {
+        const int* mark = reinterpret_cast<const int*>(halo); // peers write halo only after the next barrier
+        for (int lr = warp; lr < nr; lr += kCW) {
+            const int r = r0 + lr;
+            const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
+            for (int t = lane; t < nb && b0 + t < cap_blocks; t += 32) {
+                const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+                const int k = (col - R0) / chunk;
+                if (k == rank) continue;
+                const int j = bulk ? sc.rbase[k] + (col - R0) - sc.rlo[k] : mark[col - R0];
+                bcode[b0 + t] = -1 - j;
+                if (bulk) rptr[j] = cl.map_shared_rank(vm0, k) + 6 * ((col - R0) - k * chunk);
+            }
+        }
+    }
+    __syncthreads();
     const int n_remote = sc.n_remote, n_send = sc.n_send;
 
     const int row_step = kCW * kRowsPerWarp;
@@ -629,6 +814,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         }
     };
     make_m(vm0);
+    if (bulk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // m feeds the bulk copies
     // the fallback path's peers may still read our vm1 (init SpMV) until
     // this barrier; the push path only writes vm1 after a full exchange
     if (!push) cluster_barrier();
@@ -645,7 +831,12 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             tc = t;
         }
     };
-    const unsigned expect = static_cast<unsigned>(32 * csize + 48 * n_remote);
+    int n_halo = n_remote;
+    if (bulk) {
+        n_halo = 0;
+        for (int k = 0; k < csize; ++k) n_halo += sc.rcnt[k];
+    }
+    const unsigned expect = static_cast<unsigned>(32 * csize + 48 * n_halo);
     while (!done) {
         mark(7);
         const int par = it & 1;
@@ -693,7 +884,18 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 }
             }
         }
-        if (push) { // the m rows the peers' blocks need, into their halo slots
+        if (bulk) { // per consumer one bulk DSMEM copy of the row range it needs
+            if (warp == 1 && lane < csize) {
+                const int2 rq = sc.req[lane];
+                if (rq.y > 0) {
+                    const unsigned dst = mapa(smem_u32(halo + 6 * (par * cap_blocks + sc.reqbase[lane])), lane);
+                    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                 ::"r"(dst), "r"(smem_u32(mcur + 6 * rq.x)), "r"(48u * rq.y),
+                                 "r"(mapa(bar, lane))
+                                 : "memory");
+                }
+            }
+        } else if (push) { // the m rows the peers' blocks need, into their halo slots
             for (int e = threadIdx.x; e < 3 * n_send; e += kCT) {
                 const SendEntry se = sends[e / 3];
                 const int h = e % 3, peer = se.dest >> 20, j = se.dest & 0xfffff;
@@ -763,6 +965,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         }
         l_g = l_d = l_r = 0.0;
         make_m(mnext);
+        if (bulk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mark(6);
         ++it;
     }
@@ -777,7 +980,53 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         sv.ps[p].pcg_iters = it;
         sv.ps[p].pcg_done = 1;
     }
+    if (a.fused) { // ||dq||_inf of this CTA's rows -> rank 0's dqm[rank]
+        double m = 0.0;
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+            if (on[g]) m = fmax(m, fabs(x[g]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+        if (lane == 0) sc.red[warp][0] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double mm = 0.0;
+            for (int w = 0; w < kCW; ++w) mm = fmax(mm, sc.red[w][0]);
+            cl.map_shared_rank(&sc, 0)->dqm[rank] = mm;
+        }
+    }
     cluster_barrier(); // no CTA leaves while a peer may still touch its shared memory
+    if (a.fused && rank == 0 && threadIdx.x == 0) {
+        if (act) {
+            double mm = 0.0;
+            for (int k = 0; k < csize; ++k) mm = fmax(mm, sc.dqm[k]);
+            sv.ps[p].dq_inf = mm;
+        }
+        // the last partition's cluster takes kOpNewtonCheck for all of them
+        __threadfence();
+        if (atomicAdd(a.ticket, 1u) == static_cast<unsigned>(sv.n_parts - 1)) {
+            *a.ticket = 0u;
+            __threadfence();
+            volatile PartState* vps = sv.ps;
+            int any_act = 0, any_srch = 0;
+            for (int q = 0; q < sv.n_parts; ++q) {
+                if (a.ctrl) a.ctrl->pcg_total += vps[q].pcg_iters;
+                if (vps[q].active && vps[q].dq_inf < vps[q].tol) {
+                    vps[q].final_update = vps[q].dq_inf;
+                    vps[q].converged = 1;
+                    vps[q].active = 0;
+                }
+                any_act |= vps[q].active != 0;
+                any_srch |= vps[q].searching != 0;
+            }
+            if (a.ctrl) {
+                a.ctrl->any_active = any_act;
+                a.ctrl->any_searching = any_srch;
+            }
+            if (a.hd.graph)
+                cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.hd.step), any_act ? 1u : 0u);
+        }
+    }
     if (sv.perf && threadIdx.x == 0) {
         if (rank == 0) { // algorithmic bytes of this partition's solve
             int nblk = 0;
@@ -796,6 +1045,18 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
 
 } // namespace
 
+// Ticket of the fused kernel's last-cluster decision; launches on one device
+// are stream ordered.
+__device__ unsigned g_pcg_ticket = 0;
+
+static unsigned* pcg_ticket() { // resolved once per device, outside any graph capture
+    static void* cache[64] = {};
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    if (!cache[dev & 63]) CUDA_CHECK(cudaGetSymbolAddress(&cache[dev & 63], g_pcg_ticket));
+    return static_cast<unsigned*>(cache[dev & 63]);
+}
+
 template <int G>
 static void cluster_attrs() {
     cudaFuncSetAttribute(k_pcg_cluster<G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -805,6 +1066,7 @@ static void cluster_attrs() {
 int pcg_cluster_size() {
     static int c = 0;
     if (c == 0) {
+        (void)pcg_ticket();
         cluster_attrs<1>();
         cluster_attrs<2>();
         cluster_attrs<4>();
@@ -828,7 +1090,7 @@ int pcg_cluster_size() {
 }
 
 void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbuf, double tol,
-                        int max_iters, cudaStream_t s) {
+                        int max_iters, cudaStream_t s, const PcgFuse* fuse) {
     if (sv.n_rows == 0) return;
     const int cmax = pcg_cluster_size();
     int csize = 1;
@@ -838,7 +1100,14 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
     // register-resident row groups per warp (kCW warps x kRowsPerWarp rows each)
     const int groups = (cmax_rows + kCW * kRowsPerWarp - 1) / (kCW * kRowsPerWarp);
     if (groups > 4) throw Error("pcg: cluster chunk exceeds 4 row groups per warp");
-    PcgArgs a{pbuf, nullptr, nullptr, tol, max_iters};
+    PcgArgs a{pbuf, nullptr, nullptr, tol, max_iters, 0, nullptr, nullptr, CondHandles{}, nullptr};
+    if (fuse) {
+        a.fused = 1;
+        a.row_trace = fuse->row_trace;
+        a.ctrl = fuse->ctrl;
+        a.hd = fuse->hd;
+        a.ticket = pcg_ticket();
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csize * sv.n_parts);
     cfg.blockDim = dim3(kCT);

@@ -109,7 +109,7 @@ __global__ void k_body_terms(SolverView sv, const double* qsrc, int with_derivs,
                 H[a][a] += rho;
             }
         }
-        if (sv.project) clamp_psd<6>(H);
+        if (sv.project && !is_pd<6>(H)) clamp_psd<6>(H); // PD (the usual case): already its own clamp
         store6(sv.rgrad + 6 * r, g);
         double* dst = sv.rdiag + 36 * r;
 #pragma unroll
