@@ -389,7 +389,8 @@ void Engine::prepare_solver() {
     bkey_sorted_.resize(C);
     bidx_.resize(C);
     perm_b_.resize(C);
-    partial_.resize(static_cast<size_t>(segsum_chunks(std::max(cap_, n_rows_))) * P_ + P_);
+    partial_.resize(static_cast<size_t>(std::max(segsum_chunks(std::max(cap_, n_rows_)),
+                                                 energy_chunks(cap_) + energy_chunks(n_rows_))) * P_ + P_);
     pbuf_.resize(12 * static_cast<size_t>(std::max(n_rows_, 1)));
     pcg_part_.resize(3 * static_cast<size_t>(pcg_grid_size(std::max(n_rows_, 1))) * P_);
     (void)pcg_cluster_size(); // resolve cluster attributes before any graph capture
@@ -456,17 +457,11 @@ void Engine::enq_list_ensure(const double* q1) {
     }
 }
 
-void Engine::enq_energy(const double* q, int which, double PartState::*field) {
-    SolverView v = view();
-    launch_inst_boxes(v.sc, iview(q, q), false, frame_params_.d_hat, box_.get(), cellmax_.get(), s_);
-    launch_body_terms(v, q, false, which, s_);
-    double* dst = ps_field(ps_.get(), field);
-    launch_segsum_rows(rval_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(), dst, kPsStride,
-                       false, s_);
-    launch_filter(v, det_.keys(), cap_, det_.d_count(), cfmt_, box_.get(), q, 1, which, nullptr,
-                  sval_.get(), s_);
-    launch_segsum_keys(sval_.get(), cap_, det_.d_count(), det_.keys(), cfmt_, ipart_.get(), P_, p0_,
-                       partial_.get(), dst, kPsStride, true, s_);
+// Objective value of every flagged partition (fused k_energy): qmode 0 at
+// iq, 1 at the line-search trial; accept = take kOpAccept afterwards.
+void Engine::enq_energy(int qmode, int which, double PartState::*field, bool accept) {
+    launch_energy(view(), det_.keys(), cap_, det_.d_count(), cfmt_, qmode, which, partial_.get(),
+                  ps_field(ps_.get(), field), kPsStride, accept, ctrl_.get(), hd_, s_);
 }
 
 // fused: the trace sum, kOpEps and the preconditioner factor are left to
@@ -538,16 +533,14 @@ void Engine::enq_newton_ccd() {
 // One backtracking trial (newton.cpp:47-59) for every partition still searching.
 void Engine::enq_ls_trial() {
     SolverView v = view();
-    launch_make_trial(v, true, 0.0, 1, s_);
-    enq_energy(iqtry_.get(), 1, &PartState::trial);
-    launch_scalar(ps_.get(), P_, kOpAccept, ctrl_.get(), hd_, 0.0, 0, err_.get(), s_);
-    launch_accept_copy(n_inst_, ipart_.get(), p0_, ps_.get(), iqtry_.get(), iq_.get(), s_);
+    enq_energy(1, 1, &PartState::trial, true); // trial value + kOpAccept
+    launch_accept_trial(v, s_);
 }
 
 void Engine::enq_solve_begin(double tol) {
     launch_scalar(ps_.get(), P_, kOpReset, ctrl_.get(), hd_, tol, 0, err_.get(), s_);
     enq_list_ensure(iq_.get());
-    enq_energy(iq_.get(), 0, &PartState::energy);
+    enq_energy(0, 0, &PartState::energy);
 }
 
 FrameCtrl Engine::read_ctrl() {
@@ -871,7 +864,7 @@ void Engine::objective(const ObjectiveIn& in, const double* q, int mode, double*
     launch_scalar(ps_.get(), P_, kOpReset, ctrl_.get(), hd_, 0.0, 0, err_.get(), s_);
     enq_list_ensure(iq_.get());
     if (mode <= 1) {
-        enq_energy(iq_.get(), 2, &PartState::energy);
+        enq_energy(0, 2, &PartState::energy);
         enq_derivatives(); // counts only
         CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
                                    cudaMemcpyDeviceToHost, s_));

@@ -116,7 +116,7 @@ class Engine {
     void enq_list_ensure(const double* q1);
     void enq_list_rebuild();
     void invalidate_list();
-    void enq_energy(const double* q, int which, double PartState::*field);
+    void enq_energy(int qmode, int which, double PartState::*field, bool accept = false);
     void enq_derivatives(bool fused = false);
     void enq_pcg(bool fused = false);
     int max_part_rows() const;

@@ -35,6 +35,7 @@ void launch_assemble(const SolverView& sv, const ContactView& cv, double* row_tr
                      cudaStream_t s);
 void launch_precond(const SolverView& sv, cudaStream_t s);
 int segsum_chunks(int n);
+int energy_chunks(int n); // k_energy blocks for n entries
 void launch_segsum_rows(const double* v, int n, const int* rpart, int P, int part_base,
                         double* partial, double* dst, int stride, bool accumulate, cudaStream_t s);
 void launch_segsum_keys(const double* v, int n, const int* dn, const unsigned long long* keys,
@@ -100,6 +101,15 @@ struct PcgFuse {
     FrameCtrl* ctrl;
     CondHandles hd;          // hd.step is set from the convergence decision
 };
+
+// Fused objective value (solver.cu k_energy): qmode 0 = iq, 1 = line-search
+// trial of searching partitions; result into dst (PartState field, stride in
+// doubles); accept = also take kOpAccept. partial: energy_chunks(n_rows) +
+// energy_chunks(cap) blocks x P doubles.
+void launch_energy(const SolverView& sv, const unsigned long long* keys, int cap, const int* dn,
+                   KeyFmt fmt, int qmode, int which, double* partial, double* dst, int stride,
+                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s);
+void launch_accept_trial(const SolverView& sv, cudaStream_t s);
 
 void launch_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHandles h, double tol,
                    int max_iters, int* err, cudaStream_t s);

@@ -4,8 +4,11 @@
 #include "geometry.cuh"
 #include "energy.cuh"
 #include "kernels.hpp"
+#include "scalar_ops.cuh"
 
 #include <cub/cub.cuh>
+
+#include <cfloat>
 
 #include "instrument.hpp"
 
@@ -14,6 +17,8 @@ namespace dabd_gpu {
 namespace {
 
 constexpr int kB = 128;
+constexpr int kCH = 1024; // segment-sum chunk (k_segsum)
+constexpr int kECH = kB;  // k_energy chunk: one entry per thread (latency-bound entries)
 
 __device__ __forceinline__ void load6(const double* src, double (&d)[6]) {
     const double2* s = reinterpret_cast<const double2*>(src);
@@ -117,6 +122,46 @@ __global__ void k_body_terms(SolverView sv, const double* qsrc, int with_derivs,
 #pragma unroll
             for (int c = 0; c < 6; ++c) dst[6 * a + c] = H[a][c];
     }
+}
+
+// Value-only body term of row r (instance i) at q: the arithmetic of
+// k_body_terms without derivatives, so values (and their sums) agree bitwise.
+__device__ __forceinline__ double body_value(const SolverView& sv, int i, const double (&q)[6]) {
+    const int b = sv.ibody[i];
+    double qt[6];
+    load6(sv.iqt + 6 * i, qt);
+    const double* k = sv.sc.mblk + 6 * b;
+    double diff[6], md[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) diff[j] = q[j] - qt[j];
+    md[0] = k[0] * diff[0] + k[1] * diff[2] + k[2] * diff[3];
+    md[2] = k[1] * diff[0] + k[3] * diff[2] + k[4] * diff[3];
+    md[3] = k[2] * diff[0] + k[4] * diff[2] + k[5] * diff[3];
+    md[1] = k[0] * diff[1] + k[1] * diff[4] + k[2] * diff[5];
+    md[4] = k[1] * diff[1] + k[3] * diff[4] + k[4] * diff[5];
+    md[5] = k[2] * diff[1] + k[4] * diff[4] + k[5] * diff[5];
+    double ein = 0.0;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) ein += diff[j] * md[j];
+    ein *= 0.5;
+    const double h2 = sv.h * sv.h;
+    const double ik = sv.iinvk[i];
+    const double w = (sv.kappa_arap * sv.sc.arap_scale[b]) * sv.sc.rest_area[b];
+    double g[6] = {0, 0, 0, 0, 0, 0};
+    double H[6][6];
+    const double ear = arap_terms(q, w, h2, g, H, false);
+    double value = ik * (ein + h2 * ear);
+    if (sv.ianc[i] != 0) {
+        const double rho = sv.irho[i];
+        double s2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            const double dz = (q[j] - sv.iz[6 * i + j]) + sv.iu[6 * i + j];
+            s2 += dz * dz;
+        }
+        value += 0.5 * rho * s2;
+    }
+    return value;
 }
 
 // ---------------------------------------------------------------------------
@@ -368,6 +413,180 @@ __global__ void __launch_bounds__(kB)
                     Cf[2 * j + d][r] = val;
                 }
         store_dof_blocks(cv.cblk + 108 * static_cast<size_t>(c), Cf, rp, r0, r1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused objective value (objective.cpp:117-141) for the Newton start and
+// every line-search trial, replacing inst_boxes + body_terms + segsum +
+// filter + segsum (+ make_trial, scalar(Accept)):
+//   q of instance i: iq (qmode 0), the trial iq + alpha dq of partitions
+//   still searching (qmode 1, k_make_trial's unfused arithmetic);
+//   blocks [0, ncr): kCH-row chunks of body values, blocks [ncr, ncr + nck):
+//   kCH-entry chunks of the candidate list with the filter's exact value
+//   predicate (body boxes recomputed from the vertices, margin d_hat).
+// Chunks of kECH entries (one per thread: every entry is a long dependent
+// load chain, so parallelism wins) sum per partition with a fixed tree, and
+// the last block folds rows then candidates into dst in block order: the same
+// bits for the Newton start and every trial (deterministic, graph == eager).
+// accept: the last block then takes kOpAccept (scalar_block).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void eval_q(const SolverView& sv, int i, int qmode, double (&q)[6]) {
+    load6(sv.iq + 6 * i, q);
+    if (qmode == 0) return;
+    const int r = sv.irow[i];
+    const int p = sv.ipart[i] - sv.part_base;
+    const PartState& st = sv.ps[p];
+    if (r >= 0 && (qmode == 1 ? st.searching != 0 : st.accepted != 0)) {
+        const double alpha = st.alpha;
+        double dq[6];
+        load6(sv.x + 6 * r, dq);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) q[k] = xadd(q[k], xmul(alpha, dq[k]));
+    }
+}
+
+__device__ __forceinline__ Box body_box_at(const SceneView& sc, int b, const double (&q)[6], double margin) {
+    Box bx{{DBL_MAX, DBL_MAX}, {-DBL_MAX, -DBL_MAX}};
+    for (int v = sc.vstart[b]; v < sc.vstart[b + 1]; ++v) {
+        const V2 x = world_point(q, rest_of(sc, v));
+        bx.lo = vmin(bx.lo, x);
+        bx.hi = vmax(bx.hi, x);
+    }
+    return inflate(bx, margin);
+}
+
+// filter value of candidate t (k_filter, mode 1)
+__device__ __forceinline__ double cand_value(const SolverView& sv, unsigned long long key, KeyFmt fmt,
+                                             int qmode, int which) {
+    int a, b, v, e;
+    fmt.unpack(key, a, b, v, e);
+    const int p = sv.ipart[a] - sv.part_base;
+    if (!part_flag(sv, p, which)) return 0.0;
+    const int ba = sv.ibody[a], bb = sv.ibody[b];
+    if (sv.sc.is_static[ba] && sv.sc.is_static[bb]) return 0.0;
+    double qa[6], qb[6];
+    eval_q(sv, a, qmode, qa);
+    eval_q(sv, b, qmode, qb);
+    if (!overlaps(body_box_at(sv.sc, ba, qa, sv.d_hat), body_box_at(sv.sc, bb, qb, sv.d_hat))) return 0.0;
+    const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
+    const Box pb = point_box(sv.sc, qa, qa, false, vf);
+    const Box eb = edge_box(sv.sc, qb, qb, false, ef, sv.d_hat);
+    if (!overlaps(pb, eb)) return 0.0;
+    const V2 P = world_point(qa, rest_of(sv.sc, vf));
+    const V2 E0 = world_point(qb, rest_of(sv.sc, ef));
+    const V2 E1 = world_point(qb, rest_of(sv.sc, sv.sc.vnext[ef]));
+    const double d = pe_distance(P, E0, E1);
+    if (!(d < sv.d_hat)) return 0.0;
+    if (d <= 0.0) {
+        raise(sv.err, d < 0.0 && d == -1.0 ? kErrDegenerateEdge : kErrBarrierDomain);
+        return 0.0;
+    }
+    const double kinv = kappa_c_inv(sv, ba, bb);
+    const Barrier br = barrier(d, sv.d_hat, sv.kappa_bar);
+    return (sv.h * sv.h * kinv) * br.b;
+}
+
+struct EnergyArgs {
+    const unsigned long long* keys;
+    int cap;         // list capacity (entries past *dn are padding, value 0)
+    const int* dn;
+    KeyFmt fmt;
+    int qmode, which;
+    int ncr;         // row chunks (the remaining blocks are candidate chunks)
+    double* partial; // [gridDim][P]
+    unsigned* ticket;
+    double* dst;     // PartState field of partition 0
+    int stride;      // PartState stride in doubles
+    int accept;      // run kOpAccept in the last block
+    FrameCtrl* ctrl;
+    CondHandles hd;
+};
+
+__global__ void __launch_bounds__(kB) k_energy(SolverView sv, EnergyArgs ea) {
+    __shared__ double sh[kB];
+    __shared__ bool last;
+    const int P = sv.n_parts;
+    const bool rows = static_cast<int>(blockIdx.x) < ea.ncr;
+    const int c = rows ? blockIdx.x : blockIdx.x - ea.ncr;
+    const int n = rows ? sv.n_rows : ea.cap;
+    const int nn = rows ? n : min(*ea.dn, n);
+    const int s0 = c * kECH, s1 = min(n, s0 + kECH);
+    auto pof = [&](int t) -> int {
+        if (rows) return sv.rpart[t] - sv.part_base;
+        if (t >= nn) return P - 1; // padding belongs to the last partition (KeyPart)
+        int a, b, v, e;
+        ea.fmt.unpack(ea.keys[t], a, b, v, e);
+        return sv.ipart[a] - sv.part_base;
+    };
+    const int plo = s0 < s1 ? pof(s0) : 0;
+    const int phi = s0 < s1 ? pof(s1 - 1) : -1;
+    double* part = ea.partial + static_cast<size_t>(blockIdx.x) * P;
+    for (int p = threadIdx.x; p < P; p += kB)
+        if (p < plo || p > phi) part[p] = 0.0;
+    for (int p = plo; p <= phi; ++p) {
+        double acc = 0.0;
+        for (int t = s0 + threadIdx.x; t < s1; t += kB) {
+            if (plo != phi && pof(t) != p) continue;
+            double v = 0.0;
+            if (rows) {
+                if (part_flag(sv, p, ea.which)) {
+                    const int i = sv.rinst[t];
+                    double q[6];
+                    eval_q(sv, i, ea.qmode, q);
+                    v = body_value(sv, i, q);
+                }
+            } else if (t < nn) {
+                v = cand_value(sv, ea.keys[t], ea.fmt, ea.qmode, ea.which);
+            }
+            acc += v;
+        }
+        sh[threadIdx.x] = acc;
+        __syncthreads();
+        for (int w = kB / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) part[p] = sh[0];
+        __syncthreads();
+    }
+    __threadfence();
+    if (threadIdx.x == 0) last = atomicAdd(ea.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int p = warp; p < P; p += kB / 32) {
+        double sr = 0.0, sk = 0.0;
+        for (int k = lane; k < ea.ncr; k += 32) sr += __ldcg(ea.partial + static_cast<size_t>(k) * P + p);
+        for (int k = ea.ncr + lane; k < static_cast<int>(gridDim.x); k += 32)
+            sk += __ldcg(ea.partial + static_cast<size_t>(k) * P + p);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            sr += __shfl_xor_sync(0xffffffffu, sr, off);
+            sk += __shfl_xor_sync(0xffffffffu, sk, off);
+        }
+        if (lane == 0) {
+            double d = sr;
+            d += sk;
+            ea.dst[p * ea.stride] = d;
+        }
+    }
+    if (threadIdx.x == 0) *ea.ticket = 0u;
+    if (!ea.accept) return;
+    __syncthreads();
+    scalar_block(sv.ps, P, kOpAccept, ea.ctrl, ea.hd, 0.0, 0, sv.err);
+}
+
+// iq += alpha dq for the instances of partitions whose trial was accepted
+// (k_make_trial + k_accept_copy: the same unfused arithmetic as the trial).
+__global__ void k_accept_trial(SolverView sv) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < sv.n_inst; i += gridDim.x * blockDim.x) {
+        const int p = sv.ipart[i] - sv.part_base;
+        if (!sv.ps[p].accepted || sv.irow[i] < 0) continue;
+        double q[6];
+        eval_q(sv, i, 2, q);
+        store6(sv.iq + 6 * i, q);
     }
 }
 
@@ -689,7 +908,6 @@ __global__ void k_precond(SolverView sv) {
 // ---------------------------------------------------------------------------
 // Two-level deterministic segment sums. Chunk c covers [c*CH, (c+1)*CH).
 // ---------------------------------------------------------------------------
-constexpr int kCH = 1024;
 
 // One launch: every block writes its chunk's per-partition partials, the
 // last block to finish (threadfence + ticket) folds them in chunk order with
@@ -906,6 +1124,7 @@ void launch_precond(const SolverView& sv, cudaStream_t s) {
 }
 
 int segsum_chunks(int n) { return std::max(1, (n + kCH - 1) / kCH); }
+int energy_chunks(int n) { return std::max(1, (n + kECH - 1) / kECH); }
 
 // Ticket for the last-block fold; launches on one device are stream ordered.
 __device__ unsigned g_segsum_ticket = 0;
@@ -935,6 +1154,20 @@ void launch_segsum_keys(const double* v, int n, const int* dn, const unsigned lo
                                            KeyPart{keys, fmt, ipart, dn, part_base + P - 1},
                                            partial, segsum_ticket(), dst, stride,
                                            accumulate ? 1 : 0));
+}
+
+void launch_energy(const SolverView& sv, const unsigned long long* keys, int cap, const int* dn,
+                   KeyFmt fmt, int qmode, int which, double* partial, double* dst, int stride,
+                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s) {
+    const int ncr = energy_chunks(sv.n_rows), nck = energy_chunks(cap);
+    EnergyArgs ea{keys, cap, dn, fmt, qmode, which, ncr, partial, segsum_ticket(), dst, stride,
+                  accept ? 1 : 0, ctrl, hd};
+    DABD_LAUNCH("k_energy", s, k_energy<<<ncr + nck, kB, 0, s>>>(sv, ea));
+}
+
+void launch_accept_trial(const SolverView& sv, cudaStream_t s) {
+    if (sv.n_inst == 0) return;
+    DABD_LAUNCH("k_accept_trial", s, k_accept_trial<<<grid_for(sv.n_inst, kB), kB, 0, s>>>(sv));
 }
 
 void launch_make_trial(const SolverView& sv, bool use_alpha, double alpha, int which,
