@@ -250,7 +250,10 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_pcg_perf(dabd_gpu_ctx* ctx, int reset,
  * PCG iteration since the last reset, summed over iterations: [0] local
  * m = Dinv w + partials, [1] CTA reduction + DSMEM push, [2] arrive,
  * [3] local-column SpMV, [4] barrier wait, [5] fold + scalars, [6] remote
- * SpMV + recurrences, [7] iterations counted. */
+ * SpMV + recurrences, [7] iterations counted, [8] setup (staging, fused
+ * preconditioner, exchange plan) and [9] epilogue cycles per launch, summed,
+ * [10..15] setup sub-phases (staging issue + first cluster barrier, exchange
+ * plan, staging wait, plan barrier, eps + factor, init). cycles: 16 doubles. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_pcg_phases(dabd_gpu_ctx* ctx, int reset, double* cycles);
 /* Skin-list counters of the local solve (no reference counterpart; the
  * reference runs a fresh broad phase per detect, geometry.cpp:161-208):

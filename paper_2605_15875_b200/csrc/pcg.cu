@@ -392,9 +392,13 @@ __device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
 // A cluster whose rows overflow the shared-memory budget (spilled blocks or
 // send lists) takes the barrier-synchronised path that reads peers' m
 // through DSMEM and spilled blocks from global memory.
-template <int G>
+// PH: per-phase clock64 accounting (DABD_GPU_PCG_PHASES); a separate
+// instantiation because the clock reads cost ~10% even when predicated off.
+template <int G, bool PH>
 __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, int csize, int cmax_rows) {
     cg::cluster_group cl = cg::this_cluster();
+    const unsigned long long c_start = PH ? clock64() : 0ull;
+    unsigned long long cs[6] = {};
     unsigned long long t_start = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     extern __shared__ __align__(16) unsigned char smem[];
@@ -500,6 +504,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     // every CTA's counters and barriers are initialised before any peer
     // appends to its send list
     cluster_barrier();
+    if constexpr (PH) cs[0] = clock64();
     if (a.fused && warp == kCW - 1) { // this CTA's trace partial -> every peer's trc[rank]
         double t = 0.0;
         for (int lr = lane; lr < nr; lr += 32) t += a.row_trace[r0 + lr];
@@ -615,11 +620,14 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             }
         }
     }
+    if constexpr (PH) cs[1] = clock64();
     mbar_wait(smem_u32(&sc.stage_bar), 0);
+    if constexpr (PH) cs[2] = clock64();
     __syncthreads();
     // any overflow in the cluster selects the barrier path everywhere
     if (threadIdx.x == 0 && sc.fallback) atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
     cluster_barrier(); // send lists, requests, trace partials and fallback flags complete
+    if constexpr (PH) cs[3] = clock64();
     if (a.fused && act) { // kOpEps: eps = 1e-8 tr(H) / n (newton.cpp:20-24), same bits in every CTA
         double trace = 0.0;
         for (int k = 0; k < csize; ++k) trace += sc.trc[k];
@@ -687,6 +695,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         __syncthreads();
     }
     const bool push = cl.map_shared_rank(&sc, 0)->fallback == 0;
+    if constexpr (PH) cs[4] = clock64();
     const bool bulk = push && cl.map_shared_rank(&sc, 0)->nobulk == 0;
     {
         const int* mark = reinterpret_cast<const int*>(halo); // peers write halo only after the next barrier
@@ -822,10 +831,12 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     bool done = !act;
     double inv_gamma_old = 0.0, inv_alpha_old = 0.0, bnorm2 = 0.0;
     int it = 0;
-    const bool timed = sv.pcg_phases && sv.perf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-    unsigned long long ph[8] = {}, tc = clock64();
+    const bool timed = PH && sv.perf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long ph[10] = {}, tc = PH ? clock64() : 0ull;
+    if constexpr (PH) ph[8] = tc - c_start;
     auto mark = [&](int k) {
-        if (timed) {
+        if constexpr (PH) {
+            if (!timed) return;
             const unsigned long long t = clock64();
             ph[k] += t - tc;
             tc = t;
@@ -969,10 +980,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         mark(6);
         ++it;
     }
-    if (timed) {
-        ph[7] = it;
-        for (int k = 0; k < 8; ++k) atomicAdd(&sv.perf->phase[k], ph[k]);
-    }
+    const unsigned long long c_loop_end = PH ? clock64() : 0ull;
 #pragma unroll
     for (int g = 0; g < G; ++g)
         if (on[g]) sv.x[6 * (r0 + lrg[g]) + comp] = x[g];
@@ -1027,6 +1035,19 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.hd.step), any_act ? 1u : 0u);
         }
     }
+    if constexpr (PH) {
+        if (timed) {
+            ph[7] = it;
+            ph[9] = clock64() - c_loop_end;
+            for (int k = 0; k < 10; ++k) atomicAdd(&sv.perf->phase[k], ph[k]);
+            unsigned long long prev = c_start;
+            for (int k = 0; k < 5; ++k) { // setup sub-phases
+                atomicAdd(&sv.perf->phase[10 + k], cs[k] - prev);
+                prev = cs[k];
+            }
+            atomicAdd(&sv.perf->phase[15], c_start + ph[8] - prev);
+        }
+    }
     if (sv.perf && threadIdx.x == 0) {
         if (rank == 0) { // algorithmic bytes of this partition's solve
             int nblk = 0;
@@ -1059,8 +1080,10 @@ static unsigned* pcg_ticket() { // resolved once per device, outside any graph c
 
 template <int G>
 static void cluster_attrs() {
-    cudaFuncSetAttribute(k_pcg_cluster<G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_pcg_cluster<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemBytes);
+    cudaFuncSetAttribute(k_pcg_cluster<G, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_pcg_cluster<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemBytes);
+    cudaFuncSetAttribute(k_pcg_cluster<G, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_pcg_cluster<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemBytes);
 }
 
 int pcg_cluster_size() {
@@ -1083,7 +1106,7 @@ int pcg_cluster_size() {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, k_pcg_cluster<4>, &cfg) != cudaSuccess || n < 1) c = 8;
+        if (cudaOccupancyMaxActiveClusters(&n, k_pcg_cluster<4, false>, &cfg) != cudaSuccess || n < 1) c = 8;
         cudaGetLastError();
     }
     return c;
@@ -1120,12 +1143,11 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (groups <= 1)
-        DABD_LAUNCH("k_pcg", s, CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg_cluster<1>, sv, a, csize, cmax_rows)));
-    else if (groups == 2)
-        DABD_LAUNCH("k_pcg", s, CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg_cluster<2>, sv, a, csize, cmax_rows)));
-    else
-        DABD_LAUNCH("k_pcg", s, CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg_cluster<4>, sv, a, csize, cmax_rows)));
+    const bool ph = sv.pcg_phases != 0;
+    auto go = [&](auto kern) { DABD_LAUNCH("k_pcg", s, CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, sv, a, csize, cmax_rows))); };
+    if (groups <= 1) ph ? go(k_pcg_cluster<1, true>) : go(k_pcg_cluster<1, false>);
+    else if (groups == 2) ph ? go(k_pcg_cluster<2, true>) : go(k_pcg_cluster<2, false>);
+    else ph ? go(k_pcg_cluster<4, true>) : go(k_pcg_cluster<4, false>);
 }
 
 int pcg_grid_size(int n_rows) {

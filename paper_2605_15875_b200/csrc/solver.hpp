@@ -50,8 +50,10 @@ struct DevPerf {
     double bytes;
     unsigned long long iters;
     // clock64 cycles of CTA 0 / warp 0 per PCG phase, summed over iterations
-    // (see k_pcg_cluster; dabd_gpu_ctx_pcg_phases)
-    unsigned long long phase[8];
+    // (see k_pcg_cluster; dabd_gpu_ctx_pcg_phases); [8] setup, [9] epilogue,
+    // [10..15] setup sub-phases: staging issue + first cluster barrier,
+    // exchange plan, staging wait, plan barrier, eps + factor, init
+    unsigned long long phase[16];
 };
 
 struct SolverView {

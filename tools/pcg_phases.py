@@ -20,10 +20,12 @@ def main():
     ctx = api.Context(api.Scene(make_scenario(scene)))
     ctx.run_frames(40)
     torch.cuda.synchronize()
-    cyc = (C.c_double * 8)()
+    cyc = (C.c_double * 16)()
     L.check(lib.dabd_gpu_ctx_pcg_phases(ctx.h, 1, cyc))
     ctx.run_frames(4)
     torch.cuda.synchronize()
+    ns, n, b, its = C.c_double(), C.c_longlong(), C.c_double(), C.c_longlong()
+    L.check(lib.dabd_gpu_ctx_pcg_perf(ctx.h, 0, C.byref(ns), C.byref(n), C.byref(b), C.byref(its)))
     L.check(lib.dabd_gpu_ctx_pcg_phases(ctx.h, 1, cyc))
     it = cyc[7]
     names = ["m=Dinv w + partials", "CTA reduce + push", "arrive", "local SpMV", "wait", "fold+scalars",
@@ -32,6 +34,13 @@ def main():
     print(f"iterations {it:.0f}, cycles/iteration {tot / max(it, 1):.0f}")
     for k in range(7):
         print(f"  [{k}] {names[k]:28s} {cyc[k] / max(it, 1):8.0f} cyc/it  {100 * cyc[k] / max(tot, 1):5.1f}%")
+    nl = max(n.value, 1)
+    print(f"launches {n.value}, avg launch {ns.value / nl / 1e3:.1f} us; per launch: setup "
+          f"{cyc[8] / nl:.0f} cycles, epilogue {cyc[9] / nl:.0f} cycles")
+    sub = ["staging issue + barrier", "exchange plan", "staging wait", "plan barrier", "eps + factor",
+           "init"]
+    for k in range(6):
+        print(f"    setup[{k}] {sub[k]:24s} {cyc[10 + k] / nl:8.0f} cycles/launch")
 
 
 if __name__ == "__main__":
