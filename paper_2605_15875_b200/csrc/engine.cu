@@ -441,12 +441,19 @@ void Engine::enq_list_rebuild() {
 }
 
 // The list must cover iq and q1 (the CCD end point; the trials lie between).
-void Engine::enq_list_ensure(const double* q1) {
+// fused_ccd: q1 = iq + dq is formed by the check itself (k_ccd_prep), which
+// also writes the swept CCD boxes.
+void Engine::enq_list_ensure(const double* q1, bool fused_ccd) {
     const bool graph = hd_.graph != 0;
     const unsigned long long h = graph ? new_cond_handle() : 0ull;
-    launch_list_check(ds_.view(), iview(iq_.get(), q1), qref_.get(), iqt_.get(), iskin_.get(),
-                      iskin_next_.get(), skin_min_ * frame_params_.d_hat, skin_grow_,
-                      lstate_.get(), h, graph ? 1 : 0, s_);
+    if (fused_ccd)
+        launch_ccd_prep(view(), qref_.get(), iskin_.get(), iskin_next_.get(),
+                        skin_min_ * frame_params_.d_hat, skin_grow_, lstate_.get(), h, graph ? 1 : 0,
+                        box_.get(), s_);
+    else
+        launch_list_check(ds_.view(), iview(iq_.get(), q1), qref_.get(), iqt_.get(), iskin_.get(),
+                          iskin_next_.get(), skin_min_ * frame_params_.d_hat, skin_grow_,
+                          lstate_.get(), h, graph ? 1 : 0, s_);
     if (graph) {
         add_cond_node(h, false, cap_level_ + 1, [&] { enq_list_rebuild(); }, false);
     } else {
@@ -466,16 +473,24 @@ void Engine::enq_energy(int qmode, int which, double PartState::*field, bool acc
 
 // fused: the trace sum, kOpEps and the preconditioner factor are left to
 // the fused cluster PCG (pcg_fused()).
+// fused (graph path of a Newton iteration): kOpIterBegin rides on the body
+// terms, the contact selection recomputes body boxes and evaluates the
+// contact terms in place: body -> select+terms -> assemble -> fused PCG.
 void Engine::enq_derivatives(bool fused) {
     SolverView v = view();
     const ContactView cv = cview();
+    if (fused) {
+        launch_body_terms(v, iq_.get(), true, 0, s_, &lstate_.get()->n_act, ctrl_.get());
+        launch_contact_select(v, cv, nullptr, s_, true);
+        launch_assemble(v, cv, rowtmp_.get(), s_);
+        return;
+    }
     launch_inst_boxes(v.sc, iview(iq_.get(), iq_.get()), false, frame_params_.d_hat, box_.get(),
                       cellmax_.get(), s_);
     launch_body_terms(v, iq_.get(), true, 0, s_, &lstate_.get()->n_act);
     launch_contact_select(v, cv, box_.get(), s_);
     launch_contact_terms(v, cv, s_);
     launch_assemble(v, cv, rowtmp_.get(), s_);
-    if (fused) return;
     launch_segsum_rows(rowtmp_.get(), n_rows_, rpart_.get(), P_, p0_, partial_.get(),
                        ps_field(ps_.get(), &PartState::trace), kPsStride, false, s_);
     launch_scalar(ps_.get(), P_, kOpEps, ctrl_.get(), hd_, 0.0, 0, err_.get(), s_);
@@ -509,8 +524,8 @@ void Engine::enq_pcg(bool fused) {
 // newton.cpp:16-69, one iteration for every partition still active.
 void Engine::enq_newton_head(int max_iters) {
     SolverView v = view();
-    launch_scalar(ps_.get(), P_, kOpIterBegin, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
     const bool fused = pcg_fused();
+    if (!fused) launch_scalar(ps_.get(), P_, kOpIterBegin, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
     enq_derivatives(fused);
     enq_pcg(fused);
     if (fused) return; // ||dq||_inf and kOpNewtonCheck ran inside the PCG kernel
@@ -521,6 +536,12 @@ void Engine::enq_newton_head(int max_iters) {
 // CCD bound over [q, q + dq] on the swept superset (newton.cpp:38-42).
 void Engine::enq_newton_ccd() {
     SolverView v = view();
+    if (pcg_fused()) { // k_ccd_prep [IF rebuild] k_ccd(+kOpAlphaMax): 2 launches
+        enq_list_ensure(iqtry_.get(), true);
+        launch_ccd(v, det_.keys(), cap_, det_.d_count(), cfmt_, box_.get(), iq_.get(), iqtry_.get(), 0,
+                   nullptr, s_, ctrl_.get(), &hd_);
+        return;
+    }
     launch_make_trial(v, false, 1.0, 0, s_);
     enq_list_ensure(iqtry_.get());
     launch_inst_boxes(v.sc, iview(iq_.get(), iqtry_.get()), true, 0.0, box_.get(), cellmax_.get(),

@@ -113,7 +113,7 @@ class Engine {
     // local solve (enqueue-only, capturable) -----------------------------------
     void prepare_solver();
     void enq_superset(const double* q0, const double* q1, bool swept);
-    void enq_list_ensure(const double* q1);
+    void enq_list_ensure(const double* q1, bool fused_ccd = false);
     void enq_list_rebuild();
     void invalidate_list();
     void enq_energy(int qmode, int which, double PartState::*field, bool accept = false);

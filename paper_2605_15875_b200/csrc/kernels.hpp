@@ -13,14 +13,15 @@ namespace dabd_gpu {
 
 // which: 0 = partitions with an active Newton, 1 = partitions in a line
 // search, 2 = every partition.
+struct FrameCtrl;
 void launch_body_terms(const SolverView& sv, const double* q, bool derivs, int which,
-                       cudaStream_t s, int* reset_counter = nullptr);
+                       cudaStream_t s, int* reset_counter = nullptr, FrameCtrl* iter_begin = nullptr);
 void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
                    KeyFmt fmt, const Box* box, const double* q, int mode, int which,
                    unsigned char* flag, double* val, cudaStream_t s);
 void launch_contact_terms(const SolverView& sv, const ContactView& cv, cudaStream_t s);
 void launch_contact_select(const SolverView& sv, const ContactView& cv, const Box* box,
-                           cudaStream_t s);
+                           cudaStream_t s, bool terms = false);
 void launch_list_check(const SceneView& sc, const InstView& iv, const double* qref,
                        const double* qt, const double* skin, double* skin_next, double s_min,
                        double grow, ListState* ls, unsigned long long cond, int graph,
@@ -44,9 +45,16 @@ void launch_segsum_keys(const double* v, int n, const int* dn, const unsigned lo
 void launch_make_trial(const SolverView& sv, bool use_alpha, double alpha, int which,
                        cudaStream_t s);
 void launch_dq_inf(const SolverView& sv, cudaStream_t s);
+struct CondHandles;
+// alpha_max_ctrl != nullptr: the last block also takes kOpAlphaMax (steering hd->ls).
 void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
                 KeyFmt fmt, const Box* box0, const double* q0, const double* q1, int which,
-                double* earliest_override, cudaStream_t s);
+                double* earliest_override, cudaStream_t s, FrameCtrl* alpha_max_ctrl = nullptr,
+                const CondHandles* hd = nullptr);
+// k_make_trial(alpha 1) + k_list_check + swept k_inst_boxes (margin 0) in one launch.
+void launch_ccd_prep(const SolverView& sv, const double* qref, const double* skin, double* skin_next,
+                     double s_min, double grow, ListState* ls, unsigned long long cond, int graph,
+                     Box* box, cudaStream_t s);
 
 // Persistent cooperative block-Jacobi PCG over all partitions (pcg.cu).
 // pbuf: 12 * n_rows doubles; partials: 3 * pcg_grid_size(n_rows) * P doubles.

@@ -43,13 +43,37 @@ __device__ __forceinline__ bool part_flag(const SolverView& sv, int p, int which
     return which == 0 ? s.active != 0 : (which == 1 ? s.searching != 0 : true);
 }
 
+// body_aabb (body.cpp:136-161) of body b at q inflated by margin: the boxes
+// k_inst_boxes stores, recomputed where a kernel needs only a few of them.
+__device__ __forceinline__ Box body_box_at(const SceneView& sc, int b, const double* q, double margin) {
+    Box bx{{DBL_MAX, DBL_MAX}, {-DBL_MAX, -DBL_MAX}};
+    for (int v = sc.vstart[b]; v < sc.vstart[b + 1]; ++v) {
+        const V2 x = world_point(q, rest_of(sc, v));
+        bx.lo = vmin(bx.lo, x);
+        bx.hi = vmax(bx.hi, x);
+    }
+    return inflate(bx, margin);
+}
+
 // ---------------------------------------------------------------------------
 // Body terms: value (+ gradient + PSD-clamped 6x6 block) per dynamic row
 // (objective.cpp:117-141, 143-167).
 // ---------------------------------------------------------------------------
+// iter_begin: block 0 also takes kOpIterBegin (resets of the per-iteration
+// partition counters, before any later kernel of the iteration reads them).
 __global__ void k_body_terms(SolverView sv, const double* qsrc, int with_derivs, int which,
-                             int* reset_counter) {
+                             int* reset_counter, FrameCtrl* iter_begin) {
     if (reset_counter && blockIdx.x == 0 && threadIdx.x == 0) *reset_counter = 0;
+    if (iter_begin && blockIdx.x == 0) {
+        for (int p = threadIdx.x; p < sv.n_parts; p += blockDim.x) {
+            PartState& st = sv.ps[p];
+            st.dq_inf = 0.0;
+            st.toi_earliest = 2.0;
+            st.n_candidates = 0;
+            st.n_active_contacts = 0;
+        }
+        if (threadIdx.x == 0) ++iter_begin->exec_newton;
+    }
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
         const int p = sv.rpart[r] - sv.part_base;
         if (!part_flag(sv, p, which)) continue;
@@ -277,143 +301,146 @@ __device__ __forceinline__ void store_dof_blocks(double* dst, const double (&C)[
 // Contact terms with the rank-6 PSD projection (energy.cpp:63-94,
 // objective.cpp:184-207).
 // ---------------------------------------------------------------------------
+// Terms of active list entry c (energy.cpp:63-94 + the rank-6 projection).
+__device__ __forceinline__ void contact_terms_one(const SolverView& sv, const ContactView& cv, int c) {
+    int a, b, v, e;
+    cv.fmt.unpack(cv.key[c], a, b, v, e);
+    const int ba = sv.ibody[a], bb = sv.ibody[b];
+    const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e, ef1 = sv.sc.vnext[ef];
+    const V2 rp = rest_of(sv.sc, vf), r0 = rest_of(sv.sc, ef), r1 = rest_of(sv.sc, ef1);
+    const double* qa = sv.iq + 6 * a;
+    const double* qb = sv.iq + 6 * b;
+    const V2 P = world_point(qa, rp), E0 = world_point(qb, r0), E1 = world_point(qb, r1);
+    double g[6], A[6][6];
+    const double d = pe_distance_full(P, E0, E1, g, A);
+    if (!(d > 0.0)) {
+        raise(sv.err, kErrBarrierDomain);
+        return;
+    }
+    const Barrier br = barrier(d, sv.d_hat, sv.kappa_bar);
+    const double w = sv.h * sv.h * kappa_c_inv(sv, ba, bb); // h^2 / kappa_c
+    cv.cval[c] = w * br.b;
+    // weighted gradient w * b' * t^T g
+    const double s = w * br.db;
+    double* cg = cv.cgrad + 12 * c;
+    cg[0] = s * g[0];
+    cg[1] = s * g[1];
+    cg[2] = s * (g[0] * rp.x);
+    cg[3] = s * (g[0] * rp.y);
+    cg[4] = s * (g[1] * rp.x);
+    cg[5] = s * (g[1] * rp.y);
+    cg[6] = s * (g[2] + g[4]);
+    cg[7] = s * (g[3] + g[5]);
+    cg[8] = s * (g[2] * r0.x + g[4] * r1.x);
+    cg[9] = s * (g[2] * r0.y + g[4] * r1.y);
+    cg[10] = s * (g[3] * r0.x + g[5] * r1.x);
+    cg[11] = s * (g[3] * r0.y + g[5] * r1.y);
+    // A = w (b'' g g^T + b' H_d)
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) A[i][j] = w * (br.ddb * (g[i] * g[j]) + br.db * A[i][j]);
+    if (!sv.project) {
+        store_dof_blocks(cv.cblk + 108 * static_cast<size_t>(c), A, rp, r0, r1);
+        return;
+    }
+    // G = t t^T = L L^T in closed form: L = Lp (x) I2 with the 3x3 lower
+    // Lp = [[sp, 0, 0], [0, l00, 0], [0, l10, l11]] over the points
+    // (p, e0, e1), and B = L^T A L. A annihilates the two rigid
+    // translations T = 1 (x) e_c (d is translation invariant), so B
+    // annihilates L^{-1} T = u (x) e_c with u = Lp^{-1} 1: the projection
+    // lives on the 4-dim complement Q = W (x) I2, W = an orthonormal basis
+    // of u-perp (Householder). With Kp = Lp W and Pp = Lp^{-T} W:
+    //   B4 = (Kp (x) I2)^T A (Kp (x) I2),  C = (Pp (x) I2) clamp(B4) (Pp (x) I2)^T
+    // = L^{-T} clamp(B) L^{-1}: a 4x4 Jacobi instead of 6x6.
+    const double sp = sqrt(1.0 + rp.x * rp.x + rp.y * rp.y);
+    const double g00 = 1.0 + r0.x * r0.x + r0.y * r0.y;
+    const double g01 = 1.0 + r0.x * r1.x + r0.y * r1.y;
+    const double g11 = 1.0 + r1.x * r1.x + r1.y * r1.y;
+    const double l00 = sqrt(g00), l10 = g01 / l00, l11 = sqrt(fmax(g11 - l10 * l10, 1e-300));
+    const double ip = 1.0 / sp, i0 = 1.0 / l00, i1 = 1.0 / l11, m10 = -l10 / (l00 * l11);
+    double W[3][2];
+    {
+        double u[3] = {ip, i0, m10 + i1};
+        const double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) u[k] /= un;
+        // Householder H = I - 2 v v^T / v^T v, v = u + sign(u0) e0: H u = -sign(u0) e0,
+        // so columns 1 and 2 of H span u-perp (orthonormal)
+        const double sg = u[0] >= 0.0 ? 1.0 : -1.0;
+        const double v[3] = {u[0] + sg, u[1], u[2]};
+        const double f = 2.0 / (v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) W[k][j] = (k == j + 1 ? 1.0 : 0.0) - f * v[k] * v[j + 1];
+    }
+    double Kp[3][2], Pp[3][2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        Kp[0][j] = sp * W[0][j];
+        Kp[1][j] = l00 * W[1][j];
+        Kp[2][j] = l10 * W[1][j] + l11 * W[2][j];
+        Pp[0][j] = ip * W[0][j];
+        Pp[1][j] = i0 * W[1][j] + m10 * W[2][j];
+        Pp[2][j] = i1 * W[2][j];
+    }
+    // AK = A (Kp (x) I2): column (b, d) -> 2b + d
+    double AK[6][4];
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int d = 0; d < 2; ++d)
+                AK[r][2 * b + d] = A[r][d] * Kp[0][b] + A[r][2 + d] * Kp[1][b] + A[r][4 + d] * Kp[2][b];
+    double B4[4][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+            for (int col = 0; col < 4; ++col)
+                B4[2 * a + c2][col] = Kp[0][a] * AK[c2][col] + Kp[1][a] * AK[2 + c2][col] +
+                                      Kp[2][a] * AK[4 + c2][col];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = i + 1; j < 4; ++j) {
+            const double m = 0.5 * (B4[i][j] + B4[j][i]);
+            B4[i][j] = m;
+            B4[j][i] = m;
+        }
+    clamp_psd<4>(B4);
+    // C = (Pp (x) I2) B4+ (Pp (x) I2)^T
+    double PE[6][4]; // (Pp (x) I2) B4+
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+            for (int col = 0; col < 4; ++col)
+                PE[2 * i + c2][col] = Pp[i][0] * B4[c2][col] + Pp[i][1] * B4[2 + c2][col];
+    double Cf[6][6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+                if (2 * j + d < r) continue;
+                const double val = PE[r][d] * Pp[j][0] + PE[r][2 + d] * Pp[j][1];
+                Cf[r][2 * j + d] = val;
+                Cf[2 * j + d][r] = val;
+            }
+    store_dof_blocks(cv.cblk + 108 * static_cast<size_t>(c), Cf, rp, r0, r1);
+}
+
 __global__ void __launch_bounds__(kB)
     k_contact_terms(SolverView sv, ContactView cv) {
     const int nc = min(cv.ls->n_act, cv.n);
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
-        const int c = cv.act[k];
-        int a, b, v, e;
-        cv.fmt.unpack(cv.key[c], a, b, v, e);
-        const int ba = sv.ibody[a], bb = sv.ibody[b];
-        const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e, ef1 = sv.sc.vnext[ef];
-        const V2 rp = rest_of(sv.sc, vf), r0 = rest_of(sv.sc, ef), r1 = rest_of(sv.sc, ef1);
-        const double* qa = sv.iq + 6 * a;
-        const double* qb = sv.iq + 6 * b;
-        const V2 P = world_point(qa, rp), E0 = world_point(qb, r0), E1 = world_point(qb, r1);
-        double g[6], A[6][6];
-        const double d = pe_distance_full(P, E0, E1, g, A);
-        if (!(d > 0.0)) {
-            raise(sv.err, kErrBarrierDomain);
-            continue;
-        }
-        const Barrier br = barrier(d, sv.d_hat, sv.kappa_bar);
-        const double w = sv.h * sv.h * kappa_c_inv(sv, ba, bb); // h^2 / kappa_c
-        cv.cval[c] = w * br.b;
-        // weighted gradient w * b' * t^T g
-        const double s = w * br.db;
-        double* cg = cv.cgrad + 12 * c;
-        cg[0] = s * g[0];
-        cg[1] = s * g[1];
-        cg[2] = s * (g[0] * rp.x);
-        cg[3] = s * (g[0] * rp.y);
-        cg[4] = s * (g[1] * rp.x);
-        cg[5] = s * (g[1] * rp.y);
-        cg[6] = s * (g[2] + g[4]);
-        cg[7] = s * (g[3] + g[5]);
-        cg[8] = s * (g[2] * r0.x + g[4] * r1.x);
-        cg[9] = s * (g[2] * r0.y + g[4] * r1.y);
-        cg[10] = s * (g[3] * r0.x + g[5] * r1.x);
-        cg[11] = s * (g[3] * r0.y + g[5] * r1.y);
-        // A = w (b'' g g^T + b' H_d)
-#pragma unroll
-        for (int i = 0; i < 6; ++i)
-#pragma unroll
-            for (int j = 0; j < 6; ++j) A[i][j] = w * (br.ddb * (g[i] * g[j]) + br.db * A[i][j]);
-        if (!sv.project) {
-            store_dof_blocks(cv.cblk + 108 * static_cast<size_t>(c), A, rp, r0, r1);
-            continue;
-        }
-        // G = t t^T = L L^T in closed form: L = Lp (x) I2 with the 3x3 lower
-        // Lp = [[sp, 0, 0], [0, l00, 0], [0, l10, l11]] over the points
-        // (p, e0, e1), and B = L^T A L. A annihilates the two rigid
-        // translations T = 1 (x) e_c (d is translation invariant), so B
-        // annihilates L^{-1} T = u (x) e_c with u = Lp^{-1} 1: the projection
-        // lives on the 4-dim complement Q = W (x) I2, W = an orthonormal basis
-        // of u-perp (Householder). With Kp = Lp W and Pp = Lp^{-T} W:
-        //   B4 = (Kp (x) I2)^T A (Kp (x) I2),  C = (Pp (x) I2) clamp(B4) (Pp (x) I2)^T
-        // = L^{-T} clamp(B) L^{-1}: a 4x4 Jacobi instead of 6x6.
-        const double sp = sqrt(1.0 + rp.x * rp.x + rp.y * rp.y);
-        const double g00 = 1.0 + r0.x * r0.x + r0.y * r0.y;
-        const double g01 = 1.0 + r0.x * r1.x + r0.y * r1.y;
-        const double g11 = 1.0 + r1.x * r1.x + r1.y * r1.y;
-        const double l00 = sqrt(g00), l10 = g01 / l00, l11 = sqrt(fmax(g11 - l10 * l10, 1e-300));
-        const double ip = 1.0 / sp, i0 = 1.0 / l00, i1 = 1.0 / l11, m10 = -l10 / (l00 * l11);
-        double W[3][2];
-        {
-            double u[3] = {ip, i0, m10 + i1};
-            const double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
-#pragma unroll
-            for (int k = 0; k < 3; ++k) u[k] /= un;
-            // Householder H = I - 2 v v^T / v^T v, v = u + sign(u0) e0: H u = -sign(u0) e0,
-            // so columns 1 and 2 of H span u-perp (orthonormal)
-            const double sg = u[0] >= 0.0 ? 1.0 : -1.0;
-            const double v[3] = {u[0] + sg, u[1], u[2]};
-            const double f = 2.0 / (v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-#pragma unroll
-                for (int j = 0; j < 2; ++j) W[k][j] = (k == j + 1 ? 1.0 : 0.0) - f * v[k] * v[j + 1];
-        }
-        double Kp[3][2], Pp[3][2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            Kp[0][j] = sp * W[0][j];
-            Kp[1][j] = l00 * W[1][j];
-            Kp[2][j] = l10 * W[1][j] + l11 * W[2][j];
-            Pp[0][j] = ip * W[0][j];
-            Pp[1][j] = i0 * W[1][j] + m10 * W[2][j];
-            Pp[2][j] = i1 * W[2][j];
-        }
-        // AK = A (Kp (x) I2): column (b, d) -> 2b + d
-        double AK[6][4];
-#pragma unroll
-        for (int r = 0; r < 6; ++r)
-#pragma unroll
-            for (int b = 0; b < 2; ++b)
-#pragma unroll
-                for (int d = 0; d < 2; ++d)
-                    AK[r][2 * b + d] = A[r][d] * Kp[0][b] + A[r][2 + d] * Kp[1][b] + A[r][4 + d] * Kp[2][b];
-        double B4[4][4];
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2)
-#pragma unroll
-                for (int col = 0; col < 4; ++col)
-                    B4[2 * a + c2][col] = Kp[0][a] * AK[c2][col] + Kp[1][a] * AK[2 + c2][col] +
-                                          Kp[2][a] * AK[4 + c2][col];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = i + 1; j < 4; ++j) {
-                const double m = 0.5 * (B4[i][j] + B4[j][i]);
-                B4[i][j] = m;
-                B4[j][i] = m;
-            }
-        clamp_psd<4>(B4);
-        // C = (Pp (x) I2) B4+ (Pp (x) I2)^T
-        double PE[6][4]; // (Pp (x) I2) B4+
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2)
-#pragma unroll
-                for (int col = 0; col < 4; ++col)
-                    PE[2 * i + c2][col] = Pp[i][0] * B4[c2][col] + Pp[i][1] * B4[2 + c2][col];
-        double Cf[6][6];
-#pragma unroll
-        for (int r = 0; r < 6; ++r)
-#pragma unroll
-            for (int j = 0; j < 3; ++j)
-#pragma unroll
-                for (int d = 0; d < 2; ++d) {
-                    if (2 * j + d < r) continue;
-                    const double val = PE[r][d] * Pp[j][0] + PE[r][2 + d] * Pp[j][1];
-                    Cf[r][2 * j + d] = val;
-                    Cf[2 * j + d][r] = val;
-                }
-        store_dof_blocks(cv.cblk + 108 * static_cast<size_t>(c), Cf, rp, r0, r1);
-    }
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x)
+        contact_terms_one(sv, cv, cv.act[k]);
 }
 
 // ---------------------------------------------------------------------------
@@ -444,16 +471,6 @@ __device__ __forceinline__ void eval_q(const SolverView& sv, int i, int qmode, d
 #pragma unroll
         for (int k = 0; k < 6; ++k) q[k] = xadd(q[k], xmul(alpha, dq[k]));
     }
-}
-
-__device__ __forceinline__ Box body_box_at(const SceneView& sc, int b, const double (&q)[6], double margin) {
-    Box bx{{DBL_MAX, DBL_MAX}, {-DBL_MAX, -DBL_MAX}};
-    for (int v = sc.vstart[b]; v < sc.vstart[b + 1]; ++v) {
-        const V2 x = world_point(q, rest_of(sc, v));
-        bx.lo = vmin(bx.lo, x);
-        bx.hi = vmax(bx.hi, x);
-    }
-    return inflate(bx, margin);
 }
 
 // filter value of candidate t (k_filter, mode 1)
@@ -633,7 +650,10 @@ __global__ void k_make_bkeys(const unsigned long long* keys, int n, const int* d
 // decides which thread evaluates which contact, never a result) and counts
 // candidates / active contacts per partition.
 // ---------------------------------------------------------------------------
-__global__ void k_contact_select(SolverView sv, ContactView cv, const Box* box) {
+// box == nullptr: body boxes recomputed on the fly (no k_inst_boxes launch);
+// terms: also evaluate the contact terms of every active entry in place (no
+// separate k_contact_terms launch over the compacted list).
+__global__ void __launch_bounds__(kB) k_contact_select(SolverView sv, ContactView cv, const Box* box, int terms) {
     const int nn = cv.dn ? min(*cv.dn, cv.n) : cv.n;
     const int lane = threadIdx.x & 31;
     const int span = (nn + 31) & ~31; // whole warps stay in the loop (ballots)
@@ -647,9 +667,11 @@ __global__ void k_contact_select(SolverView sv, ContactView cv, const Box* box) 
             if (sv.ps[p].active) {
                 const int ba = sv.ibody[a], bb = sv.ibody[b];
                 const bool ss = sv.sc.is_static[ba] && sv.sc.is_static[bb];
-                if (!ss && overlaps(box[a], box[b])) {
-                    const double* qa = sv.iq + 6 * a;
-                    const double* qb = sv.iq + 6 * b;
+                const double* qa = sv.iq + 6 * a;
+                const double* qb = sv.iq + 6 * b;
+                if (!ss && (box ? overlaps(box[a], box[b])
+                                : overlaps(body_box_at(sv.sc, ba, qa, sv.d_hat),
+                                           body_box_at(sv.sc, bb, qb, sv.d_hat)))) {
                     const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
                     const Box pb = point_box(sv.sc, qa, qa, false, vf);
                     const Box eb = edge_box(sv.sc, qb, qb, false, ef, sv.d_hat);
@@ -668,6 +690,7 @@ __global__ void k_contact_select(SolverView sv, ContactView cv, const Box* box) 
             }
             cv.flag[t] = act ? 1 : 0;
             if (!act) cv.cval[t] = 0.0;
+            else if (terms) contact_terms_one(sv, cv, t);
         }
         const unsigned ab = __ballot_sync(0xffffffffu, act);
         const unsigned cb = __ballot_sync(0xffffffffu, cand);
@@ -799,34 +822,37 @@ __global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv,
 // q1 and the predicted motion of the frame. The last block decides, sets the
 // rebuild flag and steers the conditional IF node of the rebuild.
 // ---------------------------------------------------------------------------
-__global__ void k_list_check(SceneView sc, InstView iv, const double* qref, const double* qt,
-                             const double* skin, double* skin_next, double s_min, double grow,
-                             ListState* ls, unsigned long long cond, int graph) {
-    __shared__ bool last;
-    bool bad = false;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < iv.n; i += gridDim.x * blockDim.x) {
-        const int b = iv.body[i];
-        if (sc.is_static[b]) {
-            skin_next[i] = 0.0;
-            continue;
-        }
-        const double* q0 = iv.q0 + 6 * i;
-        const double* q1 = iv.q1 + 6 * i;
-        const double* qr = qref + 6 * i;
-        const double* qs = qt ? qt + 6 * i : q0;
-        double dref = 0.0, dstep = 0.0;
-        for (int v = sc.vstart[b]; v < sc.vstart[b + 1]; ++v) {
-            const V2 r = rest_of(sc, v);
-            const V2 x0 = world_point(q0, r), x1 = world_point(q1, r), xr = world_point(qr, r),
-                     xs = world_point(qs, r);
-            dref = fmax(dref, fmax(fmax(fabs(x0.x - xr.x), fabs(x0.y - xr.y)),
-                                   fmax(fabs(x1.x - xr.x), fabs(x1.y - xr.y))));
-            dstep = fmax(dstep, fmax(fmax(fabs(x1.x - x0.x), fabs(x1.y - x0.y)),
-                                     fmax(fabs(xs.x - x0.x), fabs(xs.y - x0.y))));
-        }
-        if (!(dref <= 0.99 * skin[i])) bad = true; // NaN-safe
-        skin_next[i] = fmax(s_min, grow * dstep);
+// Skin-list test of instance i (see k_list_check): true if a vertex of q0
+// or q1 left 0.99 of its skin around qref; proposes the rebuild skin.
+__device__ __forceinline__ bool list_check_one(const SceneView& sc, int b, int i, const double* q0,
+                                               const double* q1, const double* qref, const double* qt,
+                                               const double* skin, double* skin_next, double s_min,
+                                               double grow) {
+    if (sc.is_static[b]) {
+        skin_next[i] = 0.0;
+        return false;
     }
+    const double* qr = qref + 6 * i;
+    const double* qs = qt ? qt + 6 * i : q0;
+    double dref = 0.0, dstep = 0.0;
+    for (int v = sc.vstart[b]; v < sc.vstart[b + 1]; ++v) {
+        const V2 r = rest_of(sc, v);
+        const V2 x0 = world_point(q0, r), x1 = world_point(q1, r), xr = world_point(qr, r),
+                 xs = world_point(qs, r);
+        dref = fmax(dref, fmax(fmax(fabs(x0.x - xr.x), fabs(x0.y - xr.y)),
+                               fmax(fabs(x1.x - xr.x), fabs(x1.y - xr.y))));
+        dstep = fmax(dstep, fmax(fmax(fabs(x1.x - x0.x), fabs(x1.y - x0.y)),
+                                 fmax(fabs(xs.x - x0.x), fabs(xs.y - x0.y))));
+    }
+    skin_next[i] = fmax(s_min, grow * dstep);
+    return !(dref <= 0.99 * skin[i]); // NaN-safe
+}
+
+// Block-wide vote + last-block decision of the list test (steers the IF node
+// of the conditional rebuild). All threads of every block call it.
+__device__ __forceinline__ void list_check_finish(bool bad, ListState* ls, unsigned long long cond,
+                                                  int graph) {
+    __shared__ bool last;
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ls->invalid_acc, 1);
     if (threadIdx.x == 0) {
         __threadfence();
@@ -842,6 +868,52 @@ __global__ void k_list_check(SceneView sc, InstView iv, const double* qref, cons
     ls->invalid_acc = 0;
     ls->ticket = 0u;
     if (graph) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(cond), rebuild ? 1u : 0u);
+}
+
+__global__ void k_list_check(SceneView sc, InstView iv, const double* qref, const double* qt,
+                             const double* skin, double* skin_next, double s_min, double grow,
+                             ListState* ls, unsigned long long cond, int graph) {
+    bool bad = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < iv.n; i += gridDim.x * blockDim.x)
+        bad |= list_check_one(sc, iv.body[i], i, iv.q0 + 6 * i, iv.q1 + 6 * i, qref, qt, skin,
+                              skin_next, s_min, grow);
+    list_check_finish(bad, ls, cond, graph);
+}
+
+// CCD preparation of a Newton iteration (newton.cpp:38-42) in one launch:
+// q1 = q + dq for the active partitions (k_make_trial, alpha 1, unfused),
+// the skin-list test over [q, q1] (k_list_check) and the margin-0 swept
+// instance boxes for the CCD filter (k_inst_boxes).
+__global__ void k_ccd_prep(SolverView sv, const double* qref, const double* skin, double* skin_next,
+                           double s_min, double grow, ListState* ls, unsigned long long cond,
+                           int graph, Box* box) {
+    bool bad = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < sv.n_inst; i += gridDim.x * blockDim.x) {
+        const int p = sv.ipart[i] - sv.part_base;
+        const int r = sv.irow[i];
+        double q0[6], q1[6];
+        load6(sv.iq + 6 * i, q0);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) q1[k] = q0[k];
+        if (r >= 0 && sv.ps[p].active) {
+            double dq[6];
+            load6(sv.x + 6 * r, dq);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) q1[k] = xadd(q0[k], xmul(1.0, dq[k]));
+        }
+        store6(sv.iq_try + 6 * i, q1);
+        const int b = sv.ibody[i];
+        bad |= list_check_one(sv.sc, b, i, q0, q1, qref, sv.iqt, skin, skin_next, s_min, grow);
+        Box bx{{DBL_MAX, DBL_MAX}, {-DBL_MAX, -DBL_MAX}};
+        for (int v = sv.sc.vstart[b]; v < sv.sc.vstart[b + 1]; ++v) {
+            const V2 rr = rest_of(sv.sc, v);
+            const V2 x = world_point(q0, rr), y = world_point(q1, rr);
+            bx.lo = vmin(bx.lo, vmin(x, y));
+            bx.hi = vmax(bx.hi, vmax(x, y));
+        }
+        box[i] = inflate(bx, 0.0);
+    }
+    list_check_finish(bad, ls, cond, graph);
 }
 
 // First node of a rebuild: qref = q, skin = the proposal of the check.
@@ -1010,9 +1082,17 @@ __global__ void k_dq_inf(SolverView sv) {
 
 // CCD over the candidate superset with the exact swept margin-0 predicate
 // (geometry.cpp:311-341). box0: per-instance swept boxes with margin 0.
+// fin != nullptr: the last block then takes kOpAlphaMax (scalar_block).
+struct CcdFinish {
+    FrameCtrl* ctrl;
+    CondHandles hd;
+    unsigned* ticket;
+};
+
 __global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, const int* dn,
                       KeyFmt fmt, const Box* box0, const double* q0, const double* q1, int which,
-                      double* earliest_override) {
+                      double* earliest_override, CcdFinish fin) {
+    __shared__ bool last;
     const int nn = dn ? min(*dn, n) : n;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += gridDim.x * blockDim.x) {
         int a, b, v, e;
@@ -1043,6 +1123,15 @@ __global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, cons
         if (toi <= 1.0)
             atomic_min_nonneg(earliest_override ? &earliest_override[p] : &sv.ps[p].toi_earliest, toi);
     }
+    if (!fin.ticket) return;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(fin.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x == 0) *fin.ticket = 0u;
+    scalar_block(sv.ps, sv.n_parts, kOpAlphaMax, fin.ctrl, fin.hd, 0.0, 0, sv.err);
 }
 
 } // namespace
@@ -1051,13 +1140,13 @@ __global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, cons
 // launch wrappers
 // ---------------------------------------------------------------------------
 void launch_body_terms(const SolverView& sv, const double* q, bool derivs, int which,
-                       cudaStream_t s, int* reset_counter) {
+                       cudaStream_t s, int* reset_counter, FrameCtrl* iter_begin) {
     if (sv.n_rows == 0) {
         if (reset_counter) CUDA_CHECK(cudaMemsetAsync(reset_counter, 0, sizeof(int), s));
         return;
     }
     DABD_LAUNCH("k_body_terms", s, k_body_terms<<<grid_for(sv.n_rows, 64), 64, 0, s>>>(sv, q, derivs ? 1 : 0, which,
-                                                                                      reset_counter));
+                                                                                      reset_counter, iter_begin));
 }
 
 void launch_filter(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
@@ -1096,10 +1185,10 @@ void launch_assemble(const SolverView& sv, const ContactView& cv, double* row_tr
 }
 
 void launch_contact_select(const SolverView& sv, const ContactView& cv, const Box* box,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool terms) {
     if (cv.n == 0) return;
     DABD_LAUNCH("k_contact_select", s,
-                k_contact_select<<<grid_for(cv.n, kB, 148 * 4), kB, 0, s>>>(sv, cv, box));
+                k_contact_select<<<grid_for(cv.n, kB, 148 * 4), kB, 0, s>>>(sv, cv, box, terms ? 1 : 0));
 }
 
 void launch_list_check(const SceneView& sc, const InstView& iv, const double* qref,
@@ -1183,11 +1272,22 @@ void launch_dq_inf(const SolverView& sv, cudaStream_t s) {
 
 void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, const int* dn,
                 KeyFmt fmt, const Box* box0, const double* q0, const double* q1, int which,
-                double* earliest_override, cudaStream_t s) {
-    if (n == 0) return;
+                double* earliest_override, cudaStream_t s, FrameCtrl* alpha_max_ctrl,
+                const CondHandles* hd) {
+    CcdFinish fin{nullptr, CondHandles{}, nullptr};
+    if (alpha_max_ctrl) fin = CcdFinish{alpha_max_ctrl, *hd, segsum_ticket()};
+    if (n == 0 && !alpha_max_ctrl) return;
     DABD_LAUNCH("k_ccd", s,
-                k_ccd<<<grid_for(n, kB), kB, 0, s>>>(sv, keys, n, dn, fmt, box0, q0, q1, which,
-                                                     earliest_override));
+                k_ccd<<<grid_for(std::max(n, 1), kB), kB, 0, s>>>(sv, keys, n, dn, fmt, box0, q0, q1, which,
+                                                                   earliest_override, fin));
+}
+
+void launch_ccd_prep(const SolverView& sv, const double* qref, const double* skin, double* skin_next,
+                     double s_min, double grow, ListState* ls, unsigned long long cond, int graph,
+                     Box* box, cudaStream_t s) {
+    DABD_LAUNCH("k_ccd_prep", s,
+                k_ccd_prep<<<grid_for(std::max(sv.n_inst, 1), kB, 148), kB, 0, s>>>(
+                    sv, qref, skin, skin_next, s_min, grow, ls, cond, graph, box));
 }
 
 } // namespace dabd_gpu
