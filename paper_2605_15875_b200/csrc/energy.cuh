@@ -14,18 +14,19 @@
 
 namespace dabd_gpu {
 
-// Jacobi rotation (c, s) annihilating a[p][q]; the identity (1, 0) when it
-// is already 0. Branch-free (selects only), so the N/2 independent angle
-// computations of a round can be interleaved by the scheduler.
+// Jacobi rotation (c, s, t = s / c) annihilating a[p][q]; the identity
+// (1, 0, 0) when it is already 0. With d = aqq - app and e = 2 apq the
+// classical t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)), theta = d / e,
+// is t = sgn(d) e / (|d| + sqrt(d^2 + e^2)) (t = 1 for d = 0): one division,
+// one square root and one reciprocal square root per rotation, no overflow
+// for |theta| -> inf, and branch-free (selects only), so the N/2 independent
+// angles of a round can be interleaved by the scheduler.
 __device__ __forceinline__ void jacobi_cs(double app, double aqq, double apq, double& c, double& s,
                                           double& tt) {
     const bool on = apq != 0.0;
-    const double theta = (aqq - app) / (2.0 * (on ? apq : 1.0));
-    const double at = fabs(theta);
-    const double t_big = 0.5 / theta;
-    const double t_n = copysign(1.0, theta) / (at + sqrt(theta * theta + 1.0));
-    double t = at > 1e150 ? t_big : t_n;
-    t = theta == 0.0 ? 1.0 : t;
+    const double d = aqq - app, e = 2.0 * apq;
+    double t = copysign(1.0, d) * e / (fabs(d) + sqrt(d * d + e * e));
+    t = d == 0.0 ? 1.0 : t;
     const double cc = rsqrt(t * t + 1.0);
     c = on ? cc : 1.0;
     s = on ? t * cc : 0.0;
