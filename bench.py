@@ -42,6 +42,27 @@ sys.path.insert(0, ROOT)
 CONFIG_N1 = "pile-1k"
 
 
+def _ncu_traffic(kernel: str = "k_pcg_cluster"):
+    """DRAM bytes per launch (read + write) of `kernel` from the newest committed
+    `ncu --set full` summary under profiles/ (tools/ncu_summary.py output)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel}_ncu_full.txt")))
+    if not files:
+        return None, None
+    units = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    seen = 0
+    with open(files[-1]) as f:
+        for line in f:
+            for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                if line.startswith(key + " ="):
+                    parts = line.split("=")[1].split()
+                    total += float(parts[0].replace(",", "")) * units.get(parts[1] if len(parts) > 1 else "byte", 1.0)
+                    seen += 1
+    return (total if seen == 2 else None), os.path.relpath(files[-1], ROOT)
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -319,8 +340,11 @@ def main() -> None:
     if pcg_launches > 0 and pcg_ns > 0:
         dur = pcg_ns / pcg_launches / 1e9
         achieved = (pcg_bytes / pcg_launches) / dur / 1e9
+        traffic, traffic_src = _ncu_traffic()
         roof = {"bound": "hbm", "kernel": "k_pcg_cluster", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                "traffic_source": f"dram__bytes_read.sum + dram__bytes_write.sum per launch, {traffic_src}"
+                                  if traffic is not None else None,
                 "peak_kind": peak_kind, "launches": pcg_launches,
                 "avg_launch_us": 1e6 * dur, "iterations_per_launch": pcg_iters / pcg_launches,
                 "share_of_step": (pcg_ns / 1e6) / total_ms,

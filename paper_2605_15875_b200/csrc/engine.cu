@@ -105,6 +105,7 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
 
 Engine::~Engine() {
     if (exec_) cudaGraphExecDestroy(exec_);
+    if (newton_exec_) cudaGraphExecDestroy(newton_exec_);
     for (cudaStream_t s : cap_streams_) cudaStreamDestroy(s);
     if (own_stream_ && s_) cudaStreamDestroy(s_);
 }
@@ -359,6 +360,7 @@ InstView Engine::iview(const double* q0, const double* q1) {
 // local solve: enqueue-only building blocks (no host reads, capturable)
 // ---------------------------------------------------------------------------
 void Engine::prepare_solver() {
+    ++solver_epoch_; // buffers, sizes and frame parameters may change: recapture the Newton graph
     // per-partition constants (ndof) live in PartState; kOpReset keeps them
     for (int p = 0; p < P_; ++p) {
         PartState& s = ps_h_[p];
@@ -594,6 +596,82 @@ NewtonResult Engine::newton_batch(int max_iters, double tol, bool reset_ctrl) {
     CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
                                cudaMemcpyDeviceToHost, s_));
     check_err("newton: end");
+    NewtonResult res;
+    res.converged = 1;
+    for (int p = 0; p < P_; ++p) {
+        res.iterations += ps_h_[p].iterations;
+        res.ls_steps += ps_h_[p].ls_steps;
+        res.converged &= ps_h_[p].converged;
+        res.final_update = std::max(res.final_update, ps_h_[p].final_update);
+    }
+    res.pcg_iters = c.pcg_total;
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 2, &lstate_.get()->n_act, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 3, det_.d_count(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    sync();
+    n_contacts_ = pin_i_[2];
+    n_super_ = pin_i_[3];
+    return res;
+}
+
+// Captured batched Newton solve for the multi-partition ADMM frame: the
+// same conditional-node structure as the N=1 frame (cap_newton), captured
+// once per solver epoch (instance set / capacities / h of the current
+// attempt) and replayed for every ADMM iteration: one host synchronisation
+// per local solve instead of several per Newton iteration.
+NewtonResult Engine::newton_graph(int max_iters, double tol) {
+    if (!newton_exec_ || newton_epoch_ != solver_epoch_ || newton_tol_ != tol || newton_max_ != max_iters) {
+        KernelTimer::get().suspend(true);
+        hd_ = CondHandles{};
+        hd_.graph = 1;
+        for (long long& v : nodes_inc_) v = 0;
+        const long long c0 = launch_counter().load();
+        CUDA_CHECK(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
+        try {
+            cap_newton(max_iters, tol, 0);
+        } catch (...) {
+            cudaGraph_t g;
+            cudaStreamEndCapture(s_, &g);
+            KernelTimer::get().suspend(false);
+            hd_ = CondHandles{};
+            throw;
+        }
+        cudaGraph_t g;
+        CUDA_CHECK(cudaStreamEndCapture(s_, &g));
+        KernelTimer::get().suspend(false);
+        newton_total_ = launch_counter().load() - c0;
+        launch_counter() -= newton_total_; // captured, not executed
+        for (int k = 0; k < 4; ++k) newton_inc_[k] = nodes_inc_[k];
+        // same topology as the last capture (the usual case: a new frame with
+        // new buffers or h): update the executable graph in place, which is
+        // much cheaper than instantiating it again
+        bool updated = false;
+        if (newton_exec_) {
+            cudaGraphExecUpdateResultInfo info;
+            updated = cudaGraphExecUpdate(newton_exec_, g, &info) == cudaSuccess;
+            if (!updated) {
+                cudaGetLastError();
+                cudaGraphExecDestroy(newton_exec_);
+                newton_exec_ = nullptr;
+            }
+        }
+        if (!updated) CUDA_CHECK(cudaGraphInstantiate(&newton_exec_, g, 0));
+        CUDA_CHECK(cudaGraphDestroy(g));
+        hd_ = CondHandles{};
+        newton_epoch_ = solver_epoch_;
+        newton_tol_ = tol;
+        newton_max_ = max_iters;
+    }
+    CUDA_CHECK(cudaMemsetAsync(ctrl_.get(), 0, sizeof(FrameCtrl), s_));
+    CUDA_CHECK(cudaGraphLaunch(newton_exec_, s_));
+    CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState), cudaMemcpyDeviceToHost, s_));
+    const FrameCtrl c = read_ctrl(); // synchronises, raises a device error
+    const long long rebuilds = lstate_h_[0].n_rebuilds - rebuilds_seen_;
+    rebuilds_seen_ = lstate_h_[0].n_rebuilds;
+    count_launch(rebuilds * rebuild_nodes_ + newton_total_ - newton_inc_[0] +
+                 static_cast<long long>(c.exec_newton) * (newton_inc_[0] - newton_inc_[1]) +
+                 static_cast<long long>(c.exec_step) * (newton_inc_[1] - newton_inc_[2]) +
+                 static_cast<long long>(c.exec_ls) * newton_inc_[2]);
     NewtonResult res;
     res.converged = 1;
     for (int p = 0; p < P_; ++p) {
@@ -1368,7 +1446,8 @@ FrameStats Engine::frame_admm(int frame) {
             try {
                 if (I) CUDA_CHECK(cudaMemcpyAsync(iqbefore_.get(), iq_.get(), 6 * I * sizeof(double),
                                                   cudaMemcpyDeviceToDevice, s_));
-                const NewtonResult r = newton_batch(hs_.newton_cap, tol);
+                const NewtonResult r = use_graph_ ? newton_graph(hs_.newton_cap, tol)
+                                                  : newton_batch(hs_.newton_cap, tol);
                 st.newton_iterations += r.iterations;
                 st.line_search_steps += r.ls_steps;
                 st.pcg_iterations += r.pcg_iters;

@@ -58,6 +58,7 @@ class Engine {
         pcg_tol_ = tol;
         pcg_max_ = max_iters;
         graph_ok_ = false; // the captured frame bakes the PCG arguments in
+        ++solver_epoch_;
     }
     cudaStream_t stream() const { return s_; }
     const HostScene& scene() const { return hs_; }
@@ -127,6 +128,7 @@ class Engine {
     void enq_solve_begin(double tol);
     FrameCtrl read_ctrl();
     NewtonResult newton_batch(int max_iters, double tol, bool reset_ctrl = true);
+    NewtonResult newton_graph(int max_iters, double tol);
     std::vector<double> delta_inf(const double* a, const double* b);
 
     // CUDA graphs with conditional nodes -------------------------------------
@@ -234,6 +236,12 @@ class Engine {
     PinnedBuf<FrameCtrl> ctrl_h_;
     CondHandles hd_;
     cudaGraphExec_t exec_ = nullptr;
+    // captured Newton solve of the ADMM frame (newton_graph)
+    cudaGraphExec_t newton_exec_ = nullptr;
+    long long solver_epoch_ = 0, newton_epoch_ = -1;
+    double newton_tol_ = 0.0;
+    int newton_max_ = 0;
+    long long newton_inc_[4] = {}, newton_total_ = 0;
     bool graph_ok_ = false;
     bool use_graph_ = true;
     bool ref_ready_ = false;
@@ -249,6 +257,7 @@ class Engine {
     void set_use_graph(bool on) {
         use_graph_ = on;
         graph_ok_ = false;
+        ++solver_epoch_;
     }
 };
 

@@ -720,6 +720,113 @@ __global__ void __launch_bounds__(kB) k_contact_select(SolverView sv, ContactVie
 // order: TL where the row's body is the point body, BR where it is the edge
 // body; off-diagonal blocks TR / BL = TR^T grouped by partner instance.
 // ---------------------------------------------------------------------------
+// One row whose a- and b-segments have at most 32 entries each: every lane
+// loads one entry's flag, partner and partner row up front, so the block
+// sums walk ballot masks with independent loads (unrolled by 4) instead of a
+// chain of dependent flag/key/perm loads per entry. Same entries, same order
+// of additions as the general loop below (bitwise identical results).
+__device__ __forceinline__ void add_blocks(const ContactView& cv, unsigned m, int cidx, int off,
+                                           int k0, int k1, bool has1, double& x0, double& x1,
+                                           int gofs, int lane, double* g) {
+    while (m) {
+        int c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = m ? __ffs(m) - 1 : -1;
+            if (m) m &= m - 1;
+            c[u] = __shfl_sync(0xffffffffu, cidx, j < 0 ? 0 : j);
+            if (j < 0) c[u] = -1;
+        }
+        double v0[4], v1[4], vg[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            v0[u] = v1[u] = vg[u] = 0.0;
+            if (c[u] >= 0) {
+                const double* bk = cv.cblk + 108 * static_cast<size_t>(c[u]) + off;
+                v0[u] = bk[k0];
+                if (has1) v1[u] = bk[k1];
+                if (g && lane < 6) vg[u] = cv.cgrad[12 * c[u] + gofs + lane];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (c[u] < 0) continue;
+            x0 += v0[u];
+            if (has1) x1 += v1[u];
+            if (g && lane < 6) *g += vg[u];
+        }
+    }
+}
+
+__device__ __forceinline__ void assemble_row_fast(const SolverView& sv, const ContactView& cv, int r,
+                                                  int a0, int a1, int b0, int b1, int lane, int e0,
+                                                  int e1, int t0, int t1, bool has1, double d0,
+                                                  double d1, double g, double* row_trace) {
+    int ca = -1, pa = 0x7fffffff, ra = -1;
+    bool fa = false;
+    if (a0 + lane < a1) {
+        ca = a0 + lane;
+        fa = cv.flag[ca] != 0;
+        if (fa) {
+            int x, y, v, e;
+            cv.fmt.unpack(cv.key[ca], x, y, v, e);
+            pa = y;
+            ra = sv.irow[y];
+        }
+    }
+    int cb = -1, pb = 0x7fffffff, rb = -1;
+    bool fb = false;
+    if (b0 + lane < b1) {
+        cb = cv.perm_b[b0 + lane];
+        fb = cv.flag[cb] != 0;
+        if (fb) {
+            int x, y, v, e;
+            cv.fmt.unpack(cv.key[cb], x, y, v, e);
+            pb = x;
+            rb = sv.irow[x];
+        }
+    }
+    unsigned ma = __ballot_sync(0xffffffffu, fa), mb = __ballot_sync(0xffffffffu, fb);
+    add_blocks(cv, ma, ca, 0, e0, e1, has1, d0, d1, 0, lane, &g);  // TL, gradient 0..5
+    add_blocks(cv, mb, cb, 36, e0, e1, has1, d0, d1, 6, lane, &g); // BR, gradient 6..11
+    if (lane < 6) sv.rgrad[6 * r + lane] = g;
+    sv.rdiag[36 * r + e0] = d0;
+    if (has1) sv.rdiag[36 * r + e1] = d1;
+    double tr = (e0 % 7 == 0) ? d0 : 0.0;
+    if (lane == 3) tr += d1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, off);
+    if (lane == 0) row_trace[r] = tr;
+    // off-diagonal blocks by ascending partner: the partner's run in the
+    // a-segment (TR) then in the b-segment (BL = TR^T)
+    int nblk = 0;
+    while (ma | mb) {
+        const int ja = ma ? __ffs(ma) - 1 : 0, jb = mb ? __ffs(mb) - 1 : 0;
+        const int qa = ma ? __shfl_sync(0xffffffffu, pa, ja) : 0x7fffffff;
+        const int qb = mb ? __shfl_sync(0xffffffffu, pb, jb) : 0x7fffffff;
+        const int partner = min(qa, qb);
+        const int prow = qa == partner ? __shfl_sync(0xffffffffu, ra, ja) : __shfl_sync(0xffffffffu, rb, jb);
+        const unsigned runa = __ballot_sync(0xffffffffu, ((ma >> lane) & 1u) && pa == partner);
+        const unsigned runb = __ballot_sync(0xffffffffu, ((mb >> lane) & 1u) && pb == partner);
+        ma &= ~runa;
+        mb &= ~runb;
+        if (prow < 0) continue; // static partner: no block
+        double o0 = 0.0, o1 = 0.0;
+        add_blocks(cv, runa, ca, 72, e0, e1, has1, o0, o1, 0, lane, nullptr);
+        add_blocks(cv, runb, cb, 72, t0, t1, has1, o0, o1, 0, lane, nullptr);
+        if (nblk >= kEll) {
+            if (lane == 0) raise(sv.err, kErrCapacity);
+            break;
+        }
+        if (lane == 0) sv.ell_col[r * kEll + nblk] = prow;
+        double* odst = sv.ell_blk + (static_cast<size_t>(r) * kEll + nblk) * 36;
+        odst[e0] = o0;
+        if (has1) odst[e1] = o1;
+        ++nblk;
+    }
+    if (lane == 0) sv.ell_cnt[r] = nblk;
+}
+
 __global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv, double* row_trace) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -738,6 +845,10 @@ __global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv,
         double g = lane < 6 ? sv.rgrad[6 * r + lane] : 0.0;
         const int a0 = cv.aoff[i], a1 = cv.aoff[i + 1];
         const int b0 = cv.boff[i], b1 = cv.boff[i + 1];
+        if (a1 - a0 <= 32 && b1 - b0 <= 32) { // the usual row: warp-parallel metadata
+            assemble_row_fast(sv, cv, r, a0, a1, b0, b1, lane, e0, e1, t0, t1, has1, d0, d1, g, row_trace);
+            continue;
+        }
         for (int c = a0; c < a1; ++c) { // point body: TL, gradient 0..5
             if (!cv.flag[c]) continue;
             const double* bk = cv.cblk + 108 * static_cast<size_t>(c);
