@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(kT) k_pcg(SolverView sv, PcgArgs a) {
 constexpr int kCT = 512;
 constexpr int kCW = kCT / 32;
 constexpr int kRowsPerWarp = 5;
+constexpr int kSW = kCW - 1; // scalar warp: partial push, fold, CG scalars
 constexpr int kCSmemBytes = 220 * 1024;
 
 // Per-iteration partials (r.u, w.u, r.r) of every CTA land in slot
@@ -313,6 +314,7 @@ constexpr int kCSmemBytes = 220 * 1024;
 struct ClusterScalars {
     double tab[2][16][4]; // (r.u, w.u, r.r, pad): 32 B slots for v2 stores
     double red[kCW][3];
+    double scal[3];       // (beta, alpha, stop) of the iteration, from the scalar warp
     unsigned long long bar[2]; // per-parity mbarriers (st.async complete_tx)
     unsigned long long stage_bar;
     int n_remote, n_send, fallback, nobulk;
@@ -871,7 +873,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         mark(0);
         __syncthreads(); // red[] and this CTA's m (mcur) complete
         mark(1);
-        if (warp == 0) {
+        if (warp == kSW) { // the scalar warp: CTA tree and push to every peer
             double t0 = lane < kCW ? sc.red[lane][0] : 0.0;
             double t1 = lane < kCW ? sc.red[lane][1] : 0.0;
             double t2 = lane < kCW ? sc.red[lane][2] : 0.0;
@@ -928,43 +930,60 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         else
             cluster_wait();
         mark(4);
-        // every warp folds the csize CTA partials with the same 32-lane tree
-        double gamma = 0.0, delta = 0.0, rr = 0.0;
-        {
+        // the scalar warp folds the csize CTA partials (fixed 32-lane tree)
+        // and derives the CG scalars while the other warps compute the
+        // remote half of n; they meet at named barrier 1
+        const double* hv = push ? halo + 6 * par * cap_blocks : nullptr;
+        double beta = 0.0, alpha = 0.0;
+        bool stop = false;
+        if (warp == kSW) {
             double2 gd = make_double2(0.0, 0.0);
             double t2 = 0.0;
             if (lane < 16) {
                 gd = *reinterpret_cast<const double2*>(&sc.tab[par][lane][0]);
                 t2 = sc.tab[par][lane][2];
             }
-            gamma = gd.x;
-            delta = gd.y;
-            rr = t2;
+            double gamma = gd.x, delta = gd.y, rr = t2;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
                 gamma += __shfl_xor_sync(0xffffffffu, gamma, off);
                 delta += __shfl_xor_sync(0xffffffffu, delta, off);
                 rr += __shfl_xor_sync(0xffffffffu, rr, off);
             }
+            if (it == 0) bnorm2 = rr;
+            stop = bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters;
+            // beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
+            // with the previous iteration's reciprocals: one division on the
+            // critical path
+            beta = gamma * inv_gamma_old;
+            alpha = gamma / (delta - beta * gamma * inv_alpha_old);
+            stop = stop || !(alpha > 0.0) || !isfinite(alpha); // breakdown
+            if (lane == 0) {
+                sc.scal[0] = beta;
+                sc.scal[1] = alpha;
+                sc.scal[2] = stop ? 1.0 : 0.0;
+            }
+            asm volatile("bar.arrive 1, %0;" ::"r"(kCT) : "memory");
+            inv_gamma_old = 1.0 / gamma; // off the critical path: next iteration
+            inv_alpha_old = 1.0 / alpha;
         }
-        if (it == 0) bnorm2 = rr;
-        if (bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters) break;
-        // beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
-        // with the previous iteration's reciprocals: one division on the
-        // critical path
-        const double beta = gamma * inv_gamma_old;
-        const double alpha = gamma / (delta - beta * gamma * inv_alpha_old);
-        if (!(alpha > 0.0) || !isfinite(alpha)) break; // breakdown (uniform)
+        double nrem[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) nrem[g] = on[g] ? spmv_remote(lrg[g], hv, moff, nloc[g]) : 0.0;
+        if (warp != kSW) {
+            asm volatile("bar.sync 1, %0;" ::"r"(kCT) : "memory");
+            beta = sc.scal[0];
+            alpha = sc.scal[1];
+            stop = sc.scal[2] != 0.0;
+        }
+        if (stop) break; // uniform across the CTA and the cluster
         mark(5);
-        inv_gamma_old = 1.0 / gamma; // not needed until the next iteration
-        inv_alpha_old = 1.0 / alpha;
-        // ---- remote half of n, the recurrences, then m = Dinv w and the
-        // partials of the next iteration (register-resident)
-        const double* hv = push ? halo + 6 * par * cap_blocks : nullptr;
+        // ---- the recurrences, then m = Dinv w and the partials of the next
+        // iteration (register-resident)
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             if (!on[g]) continue;
-            const double n = spmv_remote(lrg[g], hv, moff, nloc[g]);
+            const double n = nrem[g];
             z[g] = n + beta * z[g];
             qv[g] = mr[g] + beta * qv[g];
             sv_[g] = w[g] + beta * sv_[g];
