@@ -98,6 +98,14 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     qd_start_.resize(6 * std::max(hs_.nb, 1));
     if (const char* e = std::getenv("DABD_GPU_NO_GRAPH")) use_graph_ = e[0] == '0';
     if (const char* e = std::getenv("DABD_GPU_PCG_PHASES")) pcg_phases_ = e[0] == '1';
+    {
+        int carve = -1; // driver default unless asked (experiment: DABD_GPU_CARVEOUT=100)
+        if (const char* e = std::getenv("DABD_GPU_CARVEOUT")) carve = std::atoi(e);
+        if (carve >= 0) {
+            set_solver_carveout(carve);
+            set_scalar_carveout(carve);
+        }
+    }
     if (const char* e = std::getenv("DABD_SKIN_MIN")) skin_min_ = std::atof(e);
     if (const char* e = std::getenv("DABD_SKIN_GROW")) skin_grow_ = std::atof(e);
     sync();

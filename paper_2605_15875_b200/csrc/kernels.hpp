@@ -63,6 +63,9 @@ int pcg_grid_size(int n_rows);
 // used while every partition has at most kClusterPcgMaxRows rows.
 constexpr int kClusterPcgMaxRows = 4096;
 int pcg_cluster_size();
+// preferred shared-memory carveout (percent) of the Newton-loop kernels
+void set_solver_carveout(int pct);
+void set_scalar_carveout(int pct);
 struct PcgFuse;
 // fuse != nullptr: the fused Newton head (trace/eps/Dinv before, ||dq||_inf and
 // the kOpNewtonCheck decision after; see PcgArgs in pcg.cu).

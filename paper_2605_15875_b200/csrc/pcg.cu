@@ -317,19 +317,14 @@ struct ClusterScalars {
     double scal[3];       // (beta, alpha, stop) of the iteration, from the scalar warp
     unsigned long long bar[2]; // per-parity mbarriers (st.async complete_tx)
     unsigned long long stage_bar;
-    int n_remote, n_send, fallback, nobulk;
+    int n_remote, fallback, nobulk;
     int wsum[kCW];
     int rlo[16], rcnt[16], rbase[16]; // rows this CTA needs from each peer (bulk mode)
     int2 req[16];                     // per consumer: (first local row, count) it needs from us
     int reqbase[16];                  // ... and where they land in its halo
-    double trc[16];                   // fused: every CTA's partial trace, by rank
     double dqm[16];                   // fused: every CTA's max |dq|, by rank (rank 0 only)
 };
 
-struct SendEntry {
-    int row;  // local row of this CTA whose m the peer needs
-    int dest; // (peer rank << 20) | peer halo slot
-};
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -400,7 +395,7 @@ template <int G, bool PH>
 __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, int csize, int cmax_rows) {
     cg::cluster_group cl = cg::this_cluster();
     const unsigned long long c_start = PH ? clock64() : 0ull;
-    unsigned long long cs[6] = {};
+    unsigned long long cs[8] = {};
     unsigned long long t_start = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     extern __shared__ __align__(16) unsigned char smem[];
@@ -428,21 +423,22 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     double* vm1 = vm0 + V;
     double* dinv = vm1 + V;
     int* bstart = reinterpret_cast<int*>(dinv + 36 * cmax_rows); // [cmax_rows + 1]
-    // per staged block: the block (288 B), its column code (4 B); per remote
-    // block additionally two parity halo rows (96 B), the DSMEM address of the
-    // peer row (8 B) and a send entry at the producer (8 B)
+    // per staged block: the block (288 B), its column code and column (8 B);
+    // per remote block additionally two parity halo rows (96 B) and the DSMEM
+    // address of the peer row (8 B)
     const size_t used = (48ull * cmax_rows) * 8 + 4ull * (cmax_rows + 2) + 64;
-    const int cap_blocks = static_cast<int>((kCSmemBytes - used) / (288 + 4 + 96 + 8 + 8)) & ~1;
+    const int cap_blocks = static_cast<int>((kCSmemBytes - used) / (288 + 4 + 4 + 96 + 8)) & ~1;
     double* blk = reinterpret_cast<double*>(
         (reinterpret_cast<uintptr_t>(bstart + cmax_rows + 1) + 15) & ~uintptr_t(15));
     double* halo = blk + 36 * cap_blocks; // [2][cap_blocks][6]
     const double** rptr = reinterpret_cast<const double**>(halo + 12 * cap_blocks);
-    SendEntry* sends = reinterpret_cast<SendEntry*>(rptr + cap_blocks);
-    int* bcode = reinterpret_cast<int*>(sends + cap_blocks);
+    int* bcode = reinterpret_cast<int*>(rptr + cap_blocks);
+    int* bcol = bcode + cap_blocks; // column (partition row) of every staged block
     const ptrdiff_t m_off = vm1 - vm0;
 
-    // ---- stage rows with TMA bulk copies: per row the diagonal block and the
-    // contiguous run of coupling blocks, plus the chunk's Dinv in one copy.
+    // ---- stage the rows: per row the diagonal block and the contiguous run
+    // of coupling blocks (cooperative 16-byte copies), the chunk's Dinv with
+    // one bulk copy when it is not factored here.
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sc.stage_bar)));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sc.bar[0])));
@@ -450,14 +446,15 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         sc.n_remote = 0;
-        sc.n_send = 0;
         sc.fallback = 0;
         sc.nobulk = 0;
     }
     for (int i = threadIdx.x; i < 2 * 16 * 4; i += kCT) (&sc.tab[0][0][0])[i] = 0.0;
     if (threadIdx.x < 16) sc.req[threadIdx.x] = make_int2(0, 0);
+    if constexpr (PH) cs[5] = clock64(); // launch parameters and partition bounds read
     for (int lr = threadIdx.x; lr < nr; lr += kCT) bstart[lr + 1] = sv.ell_cnt[r0 + lr] + 1;
     __syncthreads();
+    if constexpr (PH) cs[6] = clock64(); // block counts staged
     if (warp == 0) { // warp-wide inclusive scan in chunks of 32 rows
         int carry = 0;
         for (int b = 0; b < nr; b += 32) {
@@ -472,185 +469,68 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         }
         if (lane == 0) bstart[0] = 0;
         __syncwarp();
+        // the blocks are copied by all threads below (one small TMA copy costs
+        // ~70 cycles to issue); only the chunk's Dinv (one contiguous run) is a
+        // bulk copy, and the fused kernel factors Dinv itself
         unsigned bytes = 0;
-        for (int lr = lane; lr < nr; lr += 32) {
-            const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
-            const int ncp = min(nb, cap_blocks - b0);
-            if (ncp > 0) bytes += 288u * ncp;
-        }
-        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-        if (nr > 0 && !a.fused) bytes += 288u * nr; // Dinv (the fused kernel factors it itself)
+        if (nr > 0 && !a.fused) bytes += 288u * nr;
         if (lane == 0) mbar_expect(smem_u32(&sc.stage_bar), bytes);
         __syncwarp();
         const unsigned bar = smem_u32(&sc.stage_bar);
-        for (int lr = lane; lr < nr; lr += 32) {
-            const int r = r0 + lr;
-            const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
-            const int ncp = min(nb, cap_blocks - b0);
-            if (ncp <= 0) continue;
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                         ::"r"(smem_u32(blk + 36 * b0)), "l"(sv.rdiag + 36 * r), "r"(288u), "r"(bar)
-                         : "memory");
-            if (ncp > 1)
-                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                             ::"r"(smem_u32(blk + 36 * (b0 + 1))),
-                             "l"(sv.ell_blk + static_cast<size_t>(r) * kEll * 36),
-                             "r"(288u * (ncp - 1)), "r"(bar)
-                             : "memory");
-        }
         if (lane == 0 && nr > 0 && !a.fused)
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                          ::"r"(smem_u32(dinv)), "l"(sv.rdinv + 36 * r0), "r"(288u * nr), "r"(bar)
                          : "memory");
     }
-    // every CTA's counters and barriers are initialised before any peer
-    // appends to its send list
-    cluster_barrier();
-    if constexpr (PH) cs[0] = clock64();
-    if (a.fused && warp == kCW - 1) { // this CTA's trace partial -> every peer's trc[rank]
+    __syncthreads(); // bstart complete
+    // stage the rows' blocks (diagonal + coupling run): warp per row, one
+    // 16-byte cp.async per lane and chunk, all in flight at once (waited for
+    // before the plan barrier); the blocks' columns with batched loads
+    for (int lr = warp; lr < nr; lr += kCW) {
+        const int r = r0 + lr;
+        const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
+        const int ncp = min(nb, cap_blocks - b0);
+        const double2* d0 = reinterpret_cast<const double2*>(sv.rdiag + 36 * r);
+        const double2* o0 = reinterpret_cast<const double2*>(sv.ell_blk + static_cast<size_t>(r) * kEll * 36);
+        const unsigned dst = smem_u32(blk + 36 * b0);
+        for (int c = lane; c < 18 * ncp; c += 32)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c),
+                         "l"(c < 18 ? d0 + c : o0 + (c - 18))
+                         : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int lr0 = warp; lr0 < nr; lr0 += 4 * kCW) {
+        int cv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int lr = lr0 + u * kCW;
+            cv[u] = -1;
+            if (lr < nr && lane < min(bstart[lr + 1] - bstart[lr], cap_blocks - bstart[lr]))
+                cv[u] = lane == 0 ? r0 + lr : sv.ell_col[(r0 + lr) * kEll + lane - 1];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (cv[u] >= 0) bcol[bstart[lr0 + u * kCW] + lane] = cv[u];
+    }
+    if constexpr (PH) cs[7] = clock64(); // staging issued
+    // fused head, part 1 (overlaps the block copies): kOpEps with the trace
+    // summed redundantly by every CTA of the partition in one fixed order
+    // (same bits everywhere, no exchange), then the block-Jacobi factor.
+    double trace_p = 0.0;
+    if (a.fused && act) {
         double t = 0.0;
-        for (int lr = lane; lr < nr; lr += 32) t += a.row_trace[r0 + lr];
+        for (int i = threadIdx.x; i < R1 - R0; i += kCT) t += a.row_trace[R0 + i];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-        if (lane < csize) cl.map_shared_rank(&sc, lane)->trc[rank] = t;
+        if (lane == 0) sc.red[warp][0] = t;
+        __syncthreads();
+        for (int w = 0; w < kCW; ++w) trace_p += sc.red[w][0];
+        eps = 1e-8 * trace_p / st.ndof;
     }
-    // column code of every staged block: >= 0 a row of this CTA, < 0 the
-    // remote slot -1 - j. Remote columns are deduplicated: one halo slot per
-    // distinct remote row, slots numbered in partition-row order (a CTA-wide
-    // scan over marks kept in the halo buffer, which peers only write after
-    // the setup barrier), and the owning peer gets one send entry per slot.
-    {
-        const int R = R1 - R0;
-        int* mark = reinterpret_cast<int*>(halo);
-        if (4ll * R > 96ll * cap_blocks) { // marks do not fit: barrier path (never for <= 4096 rows)
-            if (threadIdx.x == 0) atomicOr(&sc.fallback, 1);
-        } else {
-            for (int i = threadIdx.x; i < R; i += kCT) mark[i] = 0;
-            __syncthreads();
-            for (int lr = warp; lr < nr; lr += kCW) {
-                const int r = r0 + lr;
-                const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
-                if (b0 + nb > cap_blocks && lane == 0) atomicOr(&sc.fallback, 1); // spilled blocks
-                for (int t = lane; t < nb && b0 + t < cap_blocks; t += 32) {
-                    const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
-                    const int crank = (col - R0) / chunk;
-                    if (crank == rank) bcode[b0 + t] = (col - R0) - crank * chunk;
-                    else mark[col - R0] = 1;
-                }
-            }
-            __syncthreads();
-            // exclusive scan of the marks: thread t owns [t * per, (t + 1) * per)
-            const int per = (R + kCT - 1) / kCT;
-            const int i0 = min(R, threadIdx.x * per), i1 = min(R, i0 + per);
-            int cnt = 0;
-            for (int i = i0; i < i1; ++i) cnt += mark[i];
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            if (lane == 31) sc.wsum[warp] = incl;
-            __syncthreads();
-            if (warp == 0) {
-                const int v = lane < kCW ? sc.wsum[lane] : 0;
-                int w = v;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int u = __shfl_up_sync(0xffffffffu, w, o);
-                    if (lane >= o) w += u;
-                }
-                if (lane < kCW) sc.wsum[lane] = w - v;
-                if (lane == kCW - 1) sc.n_remote = w;
-            }
-            __syncthreads();
-            int j = sc.wsum[warp] + incl - cnt;
-            for (int i = i0; i < i1; ++i) {
-                if (!mark[i]) {
-                    mark[i] = -1;
-                    continue;
-                }
-                const int crank = i / chunk, cl_row = i - crank * chunk;
-                mark[i] = j;
-                rptr[j] = cl.map_shared_rank(vm0, crank) + 6 * cl_row;
-                ClusterScalars* peer = cl.map_shared_rank(&sc, crank);
-                const int e = atomicAdd(&peer->n_send, 1);
-                if (e < cap_blocks) {
-                    SendEntry* ps = cl.map_shared_rank(sends, crank);
-                    ps[e] = SendEntry{cl_row, (rank << 20) | j};
-                } else { // send list full: the whole cluster takes the barrier path
-                    atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
-                }
-                ++j;
-            }
-            __syncthreads();
-            // bulk mode: per peer the contiguous range of its rows we need;
-            // the peer copies that range into our halo with one bulk DSMEM
-            // copy per iteration instead of one 16-byte st.async per value pair
-            if (warp < csize) {
-                int lo = 0x7fffffff, hi = -1;
-                for (int i = warp * chunk + lane; i < min(R, (warp + 1) * chunk); i += 32)
-                    if (mark[i] >= 0) {
-                        lo = min(lo, i);
-                        hi = max(hi, i);
-                    }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-                    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-                }
-                if (lane == 0) {
-                    sc.rlo[warp] = lo;
-                    sc.rcnt[warp] = hi >= lo ? hi - lo + 1 : 0;
-                }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int h = 0;
-                for (int k = 0; k < csize; ++k) {
-                    sc.rbase[k] = h;
-                    h += sc.rcnt[k];
-                }
-                if (h > cap_blocks) atomicOr(&cl.map_shared_rank(&sc, 0)->nobulk, 1);
-            }
-            __syncthreads();
-            if (threadIdx.x < csize && sc.rcnt[threadIdx.x] > 0) {
-                const int k = threadIdx.x;
-                ClusterScalars* peer = cl.map_shared_rank(&sc, k);
-                peer->req[rank] = make_int2(sc.rlo[k] - k * chunk, sc.rcnt[k]);
-                peer->reqbase[rank] = sc.rbase[k];
-            }
-        }
-    }
-    if constexpr (PH) cs[1] = clock64();
-    mbar_wait(smem_u32(&sc.stage_bar), 0);
-    if constexpr (PH) cs[2] = clock64();
-    __syncthreads();
-    // any overflow in the cluster selects the barrier path everywhere
-    if (threadIdx.x == 0 && sc.fallback) atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
-    cluster_barrier(); // send lists, requests, trace partials and fallback flags complete
-    if constexpr (PH) cs[3] = clock64();
-    if (a.fused && act) { // kOpEps: eps = 1e-8 tr(H) / n (newton.cpp:20-24), same bits in every CTA
-        double trace = 0.0;
-        for (int k = 0; k < csize; ++k) trace += sc.trc[k];
-        eps = 1e-8 * trace / st.ndof;
-        if (rank == 0 && threadIdx.x == 0) {
-            sv.ps[p].trace = trace;
-            sv.ps[p].eps = eps;
-            ++sv.ps[p].iterations;
-        }
-    }
-    for (int i = threadIdx.x; i < 6 * nr; i += kCT) { // (D + eps I)
-        const int lr = i / 6, k = i - 6 * lr;
-        const int b0 = bstart[lr];
-        if (b0 < cap_blocks) blk[36 * b0 + 7 * k] += eps;
-    }
-    __syncthreads();
     if (a.fused && act) { // block-Jacobi factor: Dinv = (D + eps I)^{-1} by Cholesky (k_precond)
         for (int lr = threadIdx.x; lr < nr; lr += kCT) {
-            const int b0 = bstart[lr];
-            const double* d = b0 < cap_blocks ? blk + 36 * b0 : sv.rdiag + 36 * (r0 + lr);
-            const double ex = b0 < cap_blocks ? 0.0 : eps; // spilled diagonal: eps not staged
+            const double* d = sv.rdiag + 36 * (r0 + lr); // L2: the staged copy may still be in flight
+            const double ex = eps;
             // one reciprocal square root per pivot, no divisions on the chain
             double L[6][6], rd[6];
             bool ok = true;
@@ -696,16 +576,144 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         }
         __syncthreads();
     }
-    const bool push = cl.map_shared_rank(&sc, 0)->fallback == 0;
+
+    // every CTA's counters and barriers are initialised before any peer
+    // appends to its send list
+    cluster_barrier();
+    if constexpr (PH) cs[0] = clock64();
+    // column code of every staged block: >= 0 a row of this CTA, < 0 the
+    // remote slot -1 - j. Remote columns are deduplicated: one halo slot per
+    // distinct remote row, slots numbered in partition-row order (a CTA-wide
+    // scan over marks kept in the halo buffer, which peers only write after
+    // the setup barrier), and the owning peer gets one send entry per slot.
+    {
+        const int R = R1 - R0;
+        int* mark = reinterpret_cast<int*>(halo);
+        if (4ll * R > 96ll * cap_blocks) { // marks do not fit: barrier path (never for <= 4096 rows)
+            if (threadIdx.x == 0) atomicOr(&sc.fallback, 1);
+        } else {
+            for (int i = threadIdx.x; i < R; i += kCT) mark[i] = 0;
+            __syncthreads();
+            for (int lr = warp; lr < nr; lr += kCW) {
+                const int r = r0 + lr;
+                const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
+                if (b0 + nb > cap_blocks && lane == 0) atomicOr(&sc.fallback, 1); // spilled blocks
+                for (int t = lane; t < nb && b0 + t < cap_blocks; t += 32) {
+                    const int col = bcol[b0 + t];
+                    const int crank = (col - R0) / chunk;
+                    if (crank == rank) bcode[b0 + t] = (col - R0) - crank * chunk;
+                    else mark[col - R0] = 1;
+                }
+            }
+            __syncthreads();
+            // exclusive scan of the marks: thread t owns [t * per, (t + 1) * per)
+            const int per = (R + kCT - 1) / kCT;
+            const int i0 = min(R, threadIdx.x * per), i1 = min(R, i0 + per);
+            int cnt = 0;
+            for (int i = i0; i < i1; ++i) cnt += mark[i];
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (lane == 31) sc.wsum[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                const int v = lane < kCW ? sc.wsum[lane] : 0;
+                int w = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, w, o);
+                    if (lane >= o) w += u;
+                }
+                if (lane < kCW) sc.wsum[lane] = w - v;
+                if (lane == kCW - 1) sc.n_remote = w;
+            }
+            __syncthreads();
+            int j = sc.wsum[warp] + incl - cnt;
+            for (int i = i0; i < i1; ++i) {
+                if (!mark[i]) {
+                    mark[i] = -1;
+                    continue;
+                }
+                const int crank = i / chunk, cl_row = i - crank * chunk;
+                mark[i] = j;
+                rptr[j] = cl.map_shared_rank(vm0, crank) + 6 * cl_row;
+                ++j;
+            }
+            __syncthreads();
+            // bulk mode: per peer the contiguous range of its rows we need;
+            // the peer copies that range into our halo with one bulk DSMEM
+            // copy per iteration instead of one 16-byte st.async per value pair
+            if (warp < csize) {
+                int lo = 0x7fffffff, hi = -1;
+                for (int i = warp * chunk + lane; i < min(R, (warp + 1) * chunk); i += 32)
+                    if (mark[i] >= 0) {
+                        lo = min(lo, i);
+                        hi = max(hi, i);
+                    }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+                }
+                if (lane == 0) {
+                    sc.rlo[warp] = lo;
+                    sc.rcnt[warp] = hi >= lo ? hi - lo + 1 : 0;
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int h = 0;
+                for (int k = 0; k < csize; ++k) {
+                    sc.rbase[k] = h;
+                    h += sc.rcnt[k];
+                }
+                if (h > cap_blocks) atomicOr(&cl.map_shared_rank(&sc, 0)->nobulk, 1);
+            }
+            __syncthreads();
+            if (threadIdx.x < csize && sc.rcnt[threadIdx.x] > 0) {
+                const int k = threadIdx.x;
+                ClusterScalars* peer = cl.map_shared_rank(&sc, k);
+                peer->req[rank] = make_int2(sc.rlo[k] - k * chunk, sc.rcnt[k]);
+                peer->reqbase[rank] = sc.rbase[k];
+            }
+        }
+    }
+    if constexpr (PH) cs[1] = clock64();
+    mbar_wait(smem_u32(&sc.stage_bar), 0);
+    asm volatile("cp.async.wait_all;" ::: "memory"); // this thread's block copies
+    if constexpr (PH) cs[2] = clock64();
+    __syncthreads();
+    // any overflow in the cluster selects the barrier path everywhere
+    if (threadIdx.x == 0 && sc.fallback) atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
+    cluster_barrier(); // send lists, requests, trace partials and fallback flags complete
+    if constexpr (PH) cs[3] = clock64();
+    if (a.fused && act && rank == 0 && threadIdx.x == 0) { // kOpEps (newton.cpp:20-24)
+        sv.ps[p].trace = trace_p;
+        sv.ps[p].eps = eps;
+        ++sv.ps[p].iterations;
+    }
+    for (int i = threadIdx.x; i < 6 * nr; i += kCT) { // (D + eps I)
+        const int lr = i / 6, k = i - 6 * lr;
+        const int b0 = bstart[lr];
+        if (b0 < cap_blocks) blk[36 * b0 + 7 * k] += eps;
+    }
+    __syncthreads();
+    // push: every peer range arrives by bulk copy (st.async partials); the
+    // barrier path (DSMEM pulls through rptr) when blocks spill or the halo
+    // ranges do not fit
+    const bool push = cl.map_shared_rank(&sc, 0)->fallback == 0 && cl.map_shared_rank(&sc, 0)->nobulk == 0;
     if constexpr (PH) cs[4] = clock64();
-    const bool bulk = push && cl.map_shared_rank(&sc, 0)->nobulk == 0;
+    const bool bulk = push;
     {
         const int* mark = reinterpret_cast<const int*>(halo); // peers write halo only after the next barrier
         for (int lr = warp; lr < nr; lr += kCW) {
             const int r = r0 + lr;
             const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
             for (int t = lane; t < nb && b0 + t < cap_blocks; t += 32) {
-                const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+                const int col = bcol[b0 + t];
                 const int k = (col - R0) / chunk;
                 if (k == rank) continue;
                 const int j = bulk ? sc.rbase[k] + (col - R0) - sc.rlo[k] : mark[col - R0];
@@ -715,7 +723,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         }
     }
     __syncthreads();
-    const int n_remote = sc.n_remote, n_send = sc.n_send;
+    const int n_remote = sc.n_remote;
 
     const int row_step = kCW * kRowsPerWarp;
     // (A v) row comp over the staged blocks with local columns
@@ -908,14 +916,6 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                                  : "memory");
                 }
             }
-        } else if (push) { // the m rows the peers' blocks need, into their halo slots
-            for (int e = threadIdx.x; e < 3 * n_send; e += kCT) {
-                const SendEntry se = sends[e / 3];
-                const int h = e % 3, peer = se.dest >> 20, j = se.dest & 0xfffff;
-                const double2 v = reinterpret_cast<const double2*>(mcur + 6 * se.row)[h];
-                st_async2(mapa(smem_u32(halo + 6 * (par * cap_blocks + j) + 2 * h), peer), v.x, v.y,
-                          mapa(bar, peer));
-            }
         } else {
             cluster_arrive();
         }
@@ -1059,12 +1059,14 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             ph[7] = it;
             ph[9] = clock64() - c_loop_end;
             for (int k = 0; k < 10; ++k) atomicAdd(&sv.perf->phase[k], ph[k]);
+            // setup sub-phases: start -> params -> counts -> staging issued ->
+            // first cluster barrier -> exchange plan -> rest of the setup
+            const unsigned long long pts[6] = {cs[5], cs[6], cs[7], cs[0], cs[3], c_start + ph[8]};
             unsigned long long prev = c_start;
-            for (int k = 0; k < 5; ++k) { // setup sub-phases
-                atomicAdd(&sv.perf->phase[10 + k], cs[k] - prev);
-                prev = cs[k];
+            for (int k = 0; k < 6; ++k) {
+                atomicAdd(&sv.perf->phase[10 + k], pts[k] - prev);
+                prev = pts[k];
             }
-            atomicAdd(&sv.perf->phase[15], c_start + ph[8] - prev);
         }
     }
     if (sv.perf && threadIdx.x == 0) {

@@ -1329,6 +1329,22 @@ int energy_chunks(int n) { return std::max(1, (n + kECH - 1) / kECH); }
 // Ticket for the last-block fold; launches on one device are stream ordered.
 __device__ unsigned g_segsum_ticket = 0;
 
+// Shared-memory carveout of the per-iteration kernels: the same as the
+// cluster PCG's (maximum shared memory), so an SM never reconfigures its
+// L1/shared split between the PCG and its neighbours in the Newton loop.
+void set_solver_carveout(int pct) {
+    const void* fns[] = {reinterpret_cast<const void*>(k_body_terms), reinterpret_cast<const void*>(k_contact_select),
+                         reinterpret_cast<const void*>(k_assemble), reinterpret_cast<const void*>(k_energy),
+                         reinterpret_cast<const void*>(k_accept_trial), reinterpret_cast<const void*>(k_ccd_prep),
+                         reinterpret_cast<const void*>(k_ccd), reinterpret_cast<const void*>(k_list_check),
+                         reinterpret_cast<const void*>(k_list_commit), reinterpret_cast<const void*>(k_seg_offsets),
+                         reinterpret_cast<const void*>(k_make_bkeys), reinterpret_cast<const void*>(k_contact_terms),
+                         reinterpret_cast<const void*>(k_precond), reinterpret_cast<const void*>(k_dq_inf),
+                         reinterpret_cast<const void*>(k_make_trial), reinterpret_cast<const void*>(k_filter)};
+    for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaGetLastError();
+}
+
 static unsigned* segsum_ticket() { // resolved once per device, outside any graph capture
     static void* cache[64] = {};
     int dev = 0;

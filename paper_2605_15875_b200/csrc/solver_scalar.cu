@@ -72,6 +72,12 @@ __global__ void k_frame_ctrl(FrameCtrl* c, int op, const double* dq_part, int P,
 
 } // namespace
 
+void set_scalar_carveout(int pct) {
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(k_scalar), cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(k_frame_ctrl), cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaGetLastError();
+}
+
 void launch_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHandles h, double tol,
                    int max_iters, int* err, cudaStream_t s) {
     DABD_LAUNCH("k_scalar", s,

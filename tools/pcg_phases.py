@@ -37,8 +37,8 @@ def main():
     nl = max(n.value, 1)
     print(f"launches {n.value}, avg launch {ns.value / nl / 1e3:.1f} us; per launch: setup "
           f"{cyc[8] / nl:.0f} cycles, epilogue {cyc[9] / nl:.0f} cycles")
-    sub = ["staging issue + barrier", "exchange plan", "staging wait", "plan barrier", "eps + factor",
-           "init"]
+    sub = ["params (ps, row offsets)", "block counts", "staging issue", "first cluster barrier",
+           "exchange plan .. plan barrier", "eps, factor, init"]
     for k in range(6):
         print(f"    setup[{k}] {sub[k]:24s} {cyc[10 + k] / nl:8.0f} cycles/launch")
 
