@@ -967,9 +967,8 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             inv_gamma_old = 1.0 / gamma; // off the critical path: next iteration
             inv_alpha_old = 1.0 / alpha;
         }
-        double nrem[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) nrem[g] = on[g] ? spmv_remote(lrg[g], hv, moff, nloc[g]) : 0.0;
+        // the other warps keep the shared-memory pipe idle while the scalar
+        // warp's shuffle tree runs, then take the remote half of n
         if (warp != kSW) {
             asm volatile("bar.sync 1, %0;" ::"r"(kCT) : "memory");
             beta = sc.scal[0];
@@ -977,6 +976,9 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             stop = sc.scal[2] != 0.0;
         }
         if (stop) break; // uniform across the CTA and the cluster
+        double nrem[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) nrem[g] = on[g] ? spmv_remote(lrg[g], hv, moff, nloc[g]) : 0.0;
         mark(5);
         // ---- the recurrences, then m = Dinv w and the partials of the next
         // iteration (register-resident)
