@@ -96,3 +96,16 @@ def test_heterogeneous_mass_ratio():
 
 def test_drop_grid_four_workers():
     _compare("drop-grid-4", 4, 3)
+
+
+def test_captured_newton_equals_host_driven(monkeypatch):
+    """The multi-partition frame's captured Newton solve (replayed once per
+    ADMM iteration) is bitwise the host-driven solve."""
+    sd = make_scenario("drop-grid-4")
+    monkeypatch.setenv("DABD_GPU_NO_GRAPH", "1")
+    eager = api.run_distributed(sd, 4, 4, **TIGHT)
+    monkeypatch.setenv("DABD_GPU_NO_GRAPH", "0")
+    graph = api.run_distributed(sd, 4, 4, **TIGHT)
+    assert np.array_equal(eager.q, graph.q) and np.array_equal(eager.q_dot, graph.q_dot)
+    assert np.array_equal(eager.trace, graph.trace)
+    assert [s["newton_iterations"] for s in eager.stats] == [s["newton_iterations"] for s in graph.stats]
