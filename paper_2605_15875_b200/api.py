@@ -298,3 +298,55 @@ def run_distributed(scene: SceneData, workers: int, frames: Optional[int] = None
     """Consensus-ADMM runtime semantics (proj/src/runtime.cpp:110-694) with
     `workers` slab partitions, all solved on one GPU in batched kernels."""
     return _run(scene, scene.frames if frames is None else frames, workers, device, **solver)
+
+
+# ---- snapshot files (proj/src/sim.cpp:34-108, same byte layout as
+#      include/dabd_gpu.hpp): [u64 frame][u64 n_dynamic][per dynamic body:
+#      u64 id, 6 f64 q, 6 f64 q_dot], bodies ascending by id ----------------
+_SNAP_REC = np.dtype([("id", "<u8"), ("q", "<f8", 6), ("q_dot", "<f8", 6)])
+
+
+def frame_path(out_dir: str, frame: int) -> str:
+    return f"{out_dir}/frame_{frame:04d}.bin"
+
+
+def write_snapshot(path: str, frame: int, is_static, q, q_dot) -> None:
+    dyn = np.nonzero(~np.asarray(is_static, dtype=bool))[0]
+    rec = np.zeros(len(dyn), dtype=_SNAP_REC)
+    rec["id"] = dyn
+    rec["q"] = np.asarray(q, dtype=np.float64)[dyn]
+    rec["q_dot"] = np.asarray(q_dot, dtype=np.float64)[dyn]
+    with open(path, "wb") as f:
+        f.write(np.array([frame, len(dyn)], dtype="<u8").tobytes())
+        f.write(rec.tobytes())
+
+
+def read_snapshot(path: str):
+    """(frame, ids, q [n][6], q_dot [n][6]); raises on a truncated file."""
+    raw = open(path, "rb").read()
+    if len(raw) < 16:
+        raise L.DabdGpuError(1, f"snapshot: truncated file {path}")
+    frame, n = np.frombuffer(raw[:16], dtype="<u8")
+    if len(raw) < 16 + int(n) * _SNAP_REC.itemsize:
+        raise L.DabdGpuError(1, f"snapshot: truncated file {path}")
+    rec = np.frombuffer(raw[16:16 + int(n) * _SNAP_REC.itemsize], dtype=_SNAP_REC)
+    return int(frame), rec["id"].astype(np.int64), rec["q"].copy(), rec["q_dot"].copy()
+
+
+def load_trajectory(out_dir: str, initial_q) -> Trajectory:
+    """sim.cpp:53-78: frame_0000.bin, frame_0001.bin, ... until one is missing;
+    static bodies keep `initial_q`."""
+    import os
+
+    init = np.asarray(initial_q, dtype=np.float64)
+    qs, qds = [], []
+    while os.path.exists(frame_path(out_dir, len(qs))):
+        _, ids, q, qd = read_snapshot(frame_path(out_dir, len(qs)))
+        qq, qqd = init.copy(), np.zeros_like(init)
+        qq[ids], qqd[ids] = q, qd
+        qs.append(qq)
+        qds.append(qqd)
+    if not qs:
+        raise L.DabdGpuError(1, f"load_trajectory: no snapshots in {out_dir}")
+    return Trajectory(np.array(qs), np.array(qds), np.zeros(len(qs)), [], np.zeros((0, 8)),
+                      np.zeros(0))

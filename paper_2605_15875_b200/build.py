@@ -85,5 +85,25 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+ADAPTER_SRC = os.path.join(ROOT, "tests", "cpp", "adapter_main.cpp")
+ADAPTER_BIN = os.path.join(ROOT, "tests", "cpp", "adapter_main")
+
+
+def build_adapter() -> str:
+    """g++ build of the C++ adapter test driver (include/dabd_gpu.hpp over
+    libdabd_gpu.so), rpath'd to the in-tree library."""
+    lib = build()
+    hdr = os.path.join(INCLUDE, "dabd_gpu.hpp")
+    if (os.path.exists(ADAPTER_BIN) and os.path.getmtime(ADAPTER_BIN) >=
+            max(os.path.getmtime(ADAPTER_SRC), os.path.getmtime(hdr), os.path.getmtime(lib))):
+        return ADAPTER_BIN
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", INCLUDE, ADAPTER_SRC, "-L", HERE,
+           "-ldabd_gpu", "-Wl,-rpath,$ORIGIN/../../paper_2605_15875_b200", "-o", ADAPTER_BIN]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"adapter build failed:\n{r.stdout}\n{r.stderr}")
+    return ADAPTER_BIN
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
