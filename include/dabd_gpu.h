@@ -20,6 +20,8 @@
  *   dabd_gpu_holder_masks        body_holder_mask                include/dabd/partition.hpp:43-45
  *   dabd_gpu_objective           LocalObjective::value/derivatives include/dabd/objective.hpp:34-75
  *   dabd_gpu_newton_solve        newton_solve                    include/dabd/newton.hpp:25-26
+ *   dabd_gpu_balancer_*          Balancer, imbalance_metric, pd_update, balance_factor
+ *                                                                include/dabd/balance.hpp:9-56
  *   dabd_gpu_run_frames          run_reference (workers==0)      src/sim.cpp:186-249
  *                                WorkerSession/ControllerSession frame loop  src/runtime.cpp:110-694
  */
@@ -116,7 +118,15 @@ typedef struct dabd_gpu_comm {
     const int* part_offsets; /* world + 1 entries, copied */
 } dabd_gpu_comm;
 
+/* Balancer::Options + SceneData::balance_enabled (include/dabd/balance.hpp:24-29,
+ * scene.hpp:31-32). dp_max <= 0: w/2 per frame. */
+typedef struct dabd_gpu_balance_params {
+    int enabled;
+    double kp, kd, smoothing, dp_max;
+} dabd_gpu_balance_params;
+
 typedef struct dabd_gpu_scene dabd_gpu_scene;
+typedef struct dabd_gpu_balancer dabd_gpu_balancer;
 typedef struct dabd_gpu_ctx dabd_gpu_ctx;
 
 DABD_GPU_API const char* dabd_gpu_version(void);
@@ -141,6 +151,11 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_scene_set_planes(dabd_gpu_scene* scene, in
                                                        const double* planes);
 DABD_GPU_API dabd_gpu_status dabd_gpu_scene_set_force_split(dabd_gpu_scene* scene, int body,
                                                             double fx, double fy);
+/* PD load balancing of the interface planes between frames (runtime.cpp:537-552):
+ * each committed frame's per-partition compute costs drive Balancer::update,
+ * whose shifted planes partition the next frame. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_scene_set_balance(dabd_gpu_scene* scene,
+                                                        const dabd_gpu_balance_params* p);
 DABD_GPU_API dabd_gpu_status dabd_gpu_scene_counts(const dabd_gpu_scene* scene, int* n_bodies,
                                                    int* n_verts);
 /* rest_xy [n_verts][2], vert_start [n_bodies+1], q [n][6], mass [n], M [n][36]. */
@@ -228,10 +243,36 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_set_state(dabd_gpu_ctx* ctx, const double*
 DABD_GPU_API dabd_gpu_status dabd_gpu_get_state(dabd_gpu_ctx* ctx, double* q, double* qdot);
 /* Final adapted rho per body (NaN where the body is not shared), after a frame. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_get_rho(dabd_gpu_ctx* ctx, double* rho);
+/* Interface planes the next frame partitions with: (num_workers-1) x (px, py, nx, ny). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_get_planes(dabd_gpu_ctx* ctx, double* planes);
+/* Per-partition compute costs of the last committed frame (num_workers
+ * entries; 0 before the first commit or with balancing off). The reference
+ * feeds wall-clock worker times (runtime.cpp:674); batched partitions share
+ * kernels, so the cost is the deterministic row-weighted work of the
+ * partition's Newton + PCG iterations. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_partition_costs(dabd_gpu_ctx* ctx, double* costs);
 /* ADMM trace rows since the last call: (frame, attempt, k, dq, r, s, min_toi,
  * sigma) doubles; returns the number of rows written (<= capacity). */
 DABD_GPU_API dabd_gpu_status dabd_gpu_take_trace(dabd_gpu_ctx* ctx, double* rows, int capacity,
                                                  int* count);
+
+/* ---- PD load balancer (host control logic, no device) ----------------------
+ * balance.cpp:8-83: imbalance T = (eta-1)/(eta+1), eta = tau_i/tau_j (times
+ * must be > 0, else RUNTIME); dp = kp T + kd (T - T_prev) clamped to
+ * +-dp_max when dp_max > 0; balance factor = mean/max. The stateful balancer
+ * smooths the times (EMA), shifts each plane along its normal and keeps w of
+ * clearance to its neighbours; planes: n_planes x (px, py, nx, ny) in/out. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_imbalance_metric(double tau_i, double tau_j, double* out);
+DABD_GPU_API dabd_gpu_status dabd_gpu_pd_update(double t, double t_prev, double kp, double kd,
+                                                double dp_max, double* out);
+DABD_GPU_API dabd_gpu_status dabd_gpu_balance_factor(const double* times, int n, double* out);
+DABD_GPU_API dabd_gpu_status dabd_gpu_balancer_create(int num_workers,
+                                                      const dabd_gpu_balance_params* p,
+                                                      dabd_gpu_balancer** out);
+DABD_GPU_API void dabd_gpu_balancer_free(dabd_gpu_balancer* b);
+DABD_GPU_API dabd_gpu_status dabd_gpu_balancer_update(dabd_gpu_balancer* b, const double* times,
+                                                      int n_planes, double* planes, double w,
+                                                      double* applied);
 
 /* ---- instrumentation (bench.py) ---------------------------------------------
  * Total dabd_gpu kernel launches so far (CUB library kernels excluded), and

@@ -20,6 +20,7 @@
  *                            src/sim.cpp:34-108            same names, same byte layout
  *   write_metrics_csv        src/sim.cpp:110-137           same name, same header and columns
  *   mse_to_reference         src/sim.cpp:14-28             same name
+ *   SceneData::balance       scene.hpp:31-32, balance.hpp:24-29  (planes move between frames)
  *   broad_phase, ccd_toi_scene, body_holder_mask, intersection_test
  *                            include/dabd/geometry.hpp:47-74, partition.hpp:43-45, geometry.cpp:389
  *
@@ -108,6 +109,10 @@ struct SceneData {
     int admm_max_iterations = 300;
     int newton_cap = 32;
     int max_halvings = 4;
+    bool balance_enabled = false;
+    struct BalanceOptions { // balance.hpp:24-29
+        double kp = 0.0, kd = 0.0, smoothing = 0.5, dp_max = 0.0;
+    } balance;
     std::map<int, Vec2> replica_force_split;
     int force_split_frames = -1;
     uint64_t seed = 0;
@@ -218,6 +223,9 @@ class Scene {
         for (const Plane& p : s.planes) pl.insert(pl.end(), {p.point[0], p.point[1], p.normal[0], p.normal[1]});
         check(dabd_gpu_scene_set_planes(h_, static_cast<int>(s.planes.size()),
                                         pl.empty() ? nullptr : pl.data()));
+        const dabd_gpu_balance_params bal{s.balance_enabled ? 1 : 0, s.balance.kp, s.balance.kd,
+                                          s.balance.smoothing, s.balance.dp_max};
+        check(dabd_gpu_scene_set_balance(h_, &bal));
         for (const auto& [body, f] : s.replica_force_split)
             check(dabd_gpu_scene_set_force_split(h_, body, f[0], f[1]));
         int nv = 0;

@@ -37,6 +37,11 @@ class SolverParams(C.Structure):
     _fields_ = [("pcg_rel_tol", C.c_double), ("pcg_max_iters", C.c_int)]
 
 
+class BalanceParams(C.Structure):
+    _fields_ = [("enabled", C.c_int), ("kp", C.c_double), ("kd", C.c_double),
+                ("smoothing", C.c_double), ("dp_max", C.c_double)]
+
+
 class FrameStats(C.Structure):
     _fields_ = [("committed", C.c_int), ("attempts", C.c_int), ("h", C.c_double),
                 ("admm_iterations", C.c_int), ("newton_iterations", C.c_int),
@@ -66,7 +71,10 @@ EXPORTS = [
     "dabd_gpu_get_rho", "dabd_gpu_take_trace", "dabd_gpu_launch_count",
     "dabd_gpu_kernel_timer_enable", "dabd_gpu_kernel_timer_read", "dabd_gpu_kernel_timer_report",
     "dabd_gpu_ctx_pcg_perf", "dabd_gpu_ctx_set_comm", "dabd_gpu_ctx_pcg_phases",
-    "dabd_gpu_ctx_list_stats",
+    "dabd_gpu_ctx_list_stats", "dabd_gpu_scene_set_balance", "dabd_gpu_ctx_get_planes",
+    "dabd_gpu_ctx_partition_costs", "dabd_gpu_imbalance_metric", "dabd_gpu_pd_update",
+    "dabd_gpu_balance_factor", "dabd_gpu_balancer_create", "dabd_gpu_balancer_free",
+    "dabd_gpu_balancer_update",
 ]
 
 _lib = None
@@ -93,6 +101,10 @@ def load():
     lib.dabd_gpu_ctx_free.argtypes = [C.c_void_p]
     lib.dabd_gpu_ctx_free.restype = None
     lib.dabd_gpu_ctx_set_stream.argtypes = [C.c_void_p, C.c_size_t]
+    lib.dabd_gpu_balancer_free.argtypes = [C.c_void_p]
+    lib.dabd_gpu_balancer_free.restype = None
+    for fn in ("dabd_gpu_imbalance_metric", "dabd_gpu_pd_update"):
+        getattr(lib, fn).restype = C.c_int
     _lib = lib
     return lib
 

@@ -71,6 +71,10 @@ class Scene:
         planes = _f64(fl["planes"]).reshape(-1)
         L.check(lib.dabd_gpu_scene_set_planes(self.h, len(scene.planes),
                                               _d(planes) if planes.size else None))
+        bal = scene.balance
+        L.check(lib.dabd_gpu_scene_set_balance(self.h, C.byref(L.BalanceParams(
+            int(bool(bal.get("enabled", False))), float(bal.get("kp", 0.0)), float(bal.get("kd", 0.0)),
+            float(bal.get("smoothing", 0.5)), float(bal.get("dp_max", 0.0))))))
         for body, f in fl["force_split"]:
             L.check(lib.dabd_gpu_scene_set_force_split(self.h, body, C.c_double(f[0]),
                                                        C.c_double(f[1])))
@@ -109,6 +113,7 @@ class Context:
                                         C.byref(h)))
         self.h = h
         self.n = scene.n
+        self.num_workers = num_workers
         if pcg_rel_tol is not None or pcg_max_iters is not None:
             self.set_solver(pcg_rel_tol or 1e-10, pcg_max_iters or 4000)
 
@@ -253,11 +258,74 @@ class Context:
         L.check(L.load().dabd_gpu_get_rho(self.h, _d(out)))
         return out[: self.n]
 
+    def planes(self) -> np.ndarray:
+        """Interface planes the next frame partitions with ((W-1) x 4)."""
+        w = max(self.num_workers - 1, 0)
+        out = np.zeros(max(4 * w, 1))
+        L.check(L.load().dabd_gpu_ctx_get_planes(self.h, _d(out)))
+        return out[: 4 * w].reshape(w, 4)
+
+    def partition_costs(self) -> np.ndarray:
+        """Balancer input of the last committed frame (one cost per partition)."""
+        out = np.zeros(max(self.num_workers, 1))
+        L.check(L.load().dabd_gpu_ctx_partition_costs(self.h, _d(out)))
+        return out[: self.num_workers]
+
     def take_trace(self, cap: int = 1 << 16) -> np.ndarray:
         rows = np.zeros((cap, 8))
         cnt = C.c_int()
         L.check(L.load().dabd_gpu_take_trace(self.h, _d(rows), cap, C.byref(cnt)))
         return rows[: cnt.value].copy()
+
+
+# ---- PD load balancer (balance.hpp:9-56), host logic over the C ABI -------
+def imbalance_metric(tau_i: float, tau_j: float) -> float:
+    out = C.c_double()
+    L.check(L.load().dabd_gpu_imbalance_metric(C.c_double(tau_i), C.c_double(tau_j), C.byref(out)))
+    return out.value
+
+
+def pd_update(t: float, t_prev: float, kp: float, kd: float, dp_max: float) -> float:
+    out = C.c_double()
+    L.check(L.load().dabd_gpu_pd_update(C.c_double(t), C.c_double(t_prev), C.c_double(kp),
+                                        C.c_double(kd), C.c_double(dp_max), C.byref(out)))
+    return out.value
+
+
+def balance_factor(times) -> float:
+    t = _f64(times)
+    out = C.c_double()
+    L.check(L.load().dabd_gpu_balance_factor(_d(t) if t.size else None, int(t.size), C.byref(out)))
+    return out.value
+
+
+class Balancer:
+    """Balancer (balance.hpp:23-53): update(times, planes, w) shifts the
+    planes ((n-1) x (px, py, nx, ny), in place) and returns the shifts."""
+
+    def __init__(self, num_workers: int, kp=0.0, kd=0.0, smoothing=0.5, dp_max=0.0) -> None:
+        h = C.c_void_p()
+        L.check(L.load().dabd_gpu_balancer_create(
+            num_workers, C.byref(L.BalanceParams(1, kp, kd, smoothing, dp_max)), C.byref(h)))
+        self.h = h
+        self.n = num_workers
+
+    def __del__(self):
+        try:
+            L.load().dabd_gpu_balancer_free(self.h)
+        except Exception:
+            pass
+
+    def update(self, times, planes: np.ndarray, w: float) -> np.ndarray:
+        t = _f64(times)
+        if t.size != self.n:
+            raise L.DabdGpuError(4, "Balancer: worker count mismatch")
+        pl = np.ascontiguousarray(planes, dtype=np.float64).reshape(-1, 4)
+        applied = np.zeros(max(len(pl), 1))
+        L.check(L.load().dabd_gpu_balancer_update(self.h, _d(t), len(pl), _d(pl) if len(pl) else None,
+                                                  C.c_double(w), _d(applied)))
+        planes[...] = pl.reshape(planes.shape)
+        return applied[: len(pl)]
 
 
 @dataclass

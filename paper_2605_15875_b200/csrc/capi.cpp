@@ -18,11 +18,26 @@ struct dabd_gpu_scene {
     HostScene s;
 };
 
+struct dabd_gpu_balancer {
+    dabd_gpu::Balancer b;
+    int workers = 0;
+};
+
 struct dabd_gpu_ctx {
     std::unique_ptr<Engine> e;
 };
 
 namespace {
+
+dabd_gpu::BalanceOpts to_balance(const dabd_gpu_balance_params& p) {
+    dabd_gpu::BalanceOpts o;
+    o.enabled = p.enabled != 0;
+    o.kp = p.kp;
+    o.kd = p.kd;
+    o.smoothing = p.smoothing;
+    o.dp_max = p.dp_max;
+    return o;
+}
 
 thread_local std::string g_last_error;
 
@@ -152,6 +167,12 @@ dabd_gpu_status dabd_gpu_scene_set_force_split(dabd_gpu_scene* scene, int body, 
         return DABD_GPU_ERR_INVALID;
     }
     scene->s.force_split[body] = {fx, fy};
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_scene_set_balance(dabd_gpu_scene* scene, const dabd_gpu_balance_params* p) {
+    if (!scene || !p) return null_arg();
+    scene->s.balance = to_balance(*p);
     return DABD_GPU_OK;
 }
 
@@ -373,6 +394,76 @@ dabd_gpu_status dabd_gpu_get_rho(dabd_gpu_ctx* ctx, double* rho) {
     if (!ctx || !rho) return null_arg();
     ctx->e->get_rho(rho);
     return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_ctx_get_planes(dabd_gpu_ctx* ctx, double* planes) {
+    if (!ctx || !planes) return null_arg();
+    const std::vector<double> p = ctx->e->planes();
+    std::copy(p.begin(), p.end(), planes);
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_ctx_partition_costs(dabd_gpu_ctx* ctx, double* costs) {
+    if (!ctx || !costs) return null_arg();
+    const std::vector<double>& c = ctx->e->partition_costs();
+    std::copy(c.begin(), c.end(), costs);
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_imbalance_metric(double tau_i, double tau_j, double* out) {
+    if (!out) return null_arg();
+    return guarded([&] {
+        *out = dabd_gpu::imbalance_metric(tau_i, tau_j);
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_pd_update(double t, double t_prev, double kp, double kd, double dp_max,
+                                   double* out) {
+    if (!out) return null_arg();
+    *out = dabd_gpu::pd_update(t, t_prev, kp, kd, dp_max);
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_balance_factor(const double* times, int n, double* out) {
+    if (!out || n < 0 || (n > 0 && !times)) return null_arg();
+    return guarded([&] {
+        *out = dabd_gpu::balance_factor(std::vector<double>(times, times + n));
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_balancer_create(int num_workers, const dabd_gpu_balance_params* p,
+                                         dabd_gpu_balancer** out) {
+    if (!p || !out || num_workers < 1) return null_arg();
+    return guarded([&] {
+        auto b = std::make_unique<dabd_gpu_balancer>();
+        b->b = dabd_gpu::Balancer(num_workers, to_balance(*p));
+        b->workers = num_workers;
+        *out = b.release();
+        return DABD_GPU_OK;
+    });
+}
+
+void dabd_gpu_balancer_free(dabd_gpu_balancer* b) { delete b; }
+
+dabd_gpu_status dabd_gpu_balancer_update(dabd_gpu_balancer* b, const double* times, int n_planes,
+                                         double* planes, double w, double* applied) {
+    if (!b || !times || n_planes < 0 || (n_planes > 0 && !planes)) return null_arg();
+    return guarded([&] {
+        std::vector<dabd_gpu::PlaneH> pl(n_planes);
+        for (int k = 0; k < n_planes; ++k) pl[k] = {planes[4 * k], planes[4 * k + 1], planes[4 * k + 2], planes[4 * k + 3]};
+        const std::vector<double> dp =
+            b->b.update(std::vector<double>(times, times + b->workers), pl, w);
+        for (int k = 0; k < n_planes; ++k) {
+            planes[4 * k] = pl[k].px;
+            planes[4 * k + 1] = pl[k].py;
+            planes[4 * k + 2] = pl[k].nx;
+            planes[4 * k + 3] = pl[k].ny;
+            if (applied) applied[k] = dp[k];
+        }
+        return DABD_GPU_OK;
+    });
 }
 
 dabd_gpu_status dabd_gpu_take_trace(dabd_gpu_ctx* ctx, double* rows, int capacity, int* count) {

@@ -47,6 +47,17 @@ bool check_stopping(double dq, double r, double s, const std::vector<double>& to
     return end;
 }
 
+// A partition's compute cost for the balancer: the reference feeds the
+// worker's wall-clock compute time (runtime.cpp:674); partitions batched in
+// shared kernels have no separable clock, so the cost is the deterministic
+// row-weighted work of its solves: every Newton iteration touches its rows
+// and contact blocks, every PCG iteration its rows. Floored at 1 so the
+// imbalance metric's positivity holds for an empty partition.
+double partition_cost(const PartState& s) {
+    const double rows = s.ndof / 6.0;
+    return std::max(1.0, s.iterations * (rows + 2.0 * s.n_active_contacts) + s.pcg_total * rows);
+}
+
 } // namespace
 
 Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs), device_(device) {
@@ -73,6 +84,11 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     q_start_.resize(6 * std::max(hs_.nb, 1));
     rho_carry_.assign(hs_.nb, std::numeric_limits<double>::quiet_NaN());
     h_cur_ = hs_.params.h;
+    if (W_ > 0) {
+        planes_cur_.assign(hs_.planes.begin(), hs_.planes.begin() + (W_ - 1));
+        balancer_ = Balancer(W_, hs_.balance);
+        part_cost_.assign(W_, 0.0);
+    }
     ps_.resize(P_);
     ps_h_.resize(P_);
     scal_a_.resize(P_);
@@ -1057,6 +1073,12 @@ void Engine::get_state(double* q, double* qd) {
     sync();
 }
 
+std::vector<double> Engine::planes() const {
+    std::vector<double> out;
+    for (const PlaneH& p : planes_cur_) out.insert(out.end(), {p.px, p.py, p.nx, p.ny});
+    return out;
+}
+
 void Engine::get_rho(double* rho) const {
     std::copy(rho_carry_.begin(), rho_carry_.end(), rho);
 }
@@ -1249,7 +1271,11 @@ FrameStats Engine::frame_reference() {
 // this context solved in the same batched kernels.
 FrameStats Engine::frame_admm(int frame) {
     const int nb = hs_.nb;
-    const std::vector<PlaneH> planes(hs_.planes.begin(), hs_.planes.begin() + (W_ - 1));
+    // PD balancer step on the previous committed frame's partition costs;
+    // the shifted planes take effect in this frame's partitioning
+    // (runtime.cpp:543-552, applied by every worker at runtime.cpp:97-103)
+    if (hs_.balance.enabled && have_costs_ && W_ > 1) balancer_.update(part_cost_, planes_cur_, w_last_);
+    const std::vector<PlaneH>& planes = planes_cur_;
     std::vector<double> hplanes;
     for (const PlaneH& p : planes) hplanes.insert(hplanes.end(), {p.px, p.py, p.nx, p.ny});
     DBuf<double> dplanes;
@@ -1270,6 +1296,8 @@ FrameStats Engine::frame_admm(int frame) {
         launch_vmax(ds_.view(), qd_.get(), gate_.get(), s_);
         const double v_max = gate_.to_host(s_)[0];
         const double w = std::max(2.0 * v_max * h, hs_.w_min);
+        w_last_ = w;
+        std::vector<double> cost(P_, 0.0); // this attempt's per-partition compute cost
         // holder masks (partition.cpp:36-67)
         DBuf<uint32_t> dm;
         dm.resize(std::max(nb, 1));
@@ -1459,6 +1487,7 @@ FrameStats Engine::frame_admm(int frame) {
                 st.newton_iterations += r.iterations;
                 st.line_search_steps += r.ls_steps;
                 st.pcg_iterations += r.pcg_iters;
+                for (int p = 0; p < P_; ++p) cost[p] += partition_cost(ps_h_[p]);
                 st.max_contacts = std::max(st.max_contacts, n_contacts_);
                 st.max_candidates = std::max(st.max_candidates, n_super_);
                 dq = n_rows_ ? delta_inf(iq_.get(), iqbefore_.get()) : std::vector<double>(P_, 0.0);
@@ -1482,6 +1511,19 @@ FrameStats Engine::frame_admm(int frame) {
         launch_commit(ds_.view(), I, ibody_.get(), ipart_.get(), ianc_.get(), bmask_.get(),
                       iq_.get(), iznext_.get(), q_start_.get(), h, q_.get(), qd_.get(), s_);
         if (distributed_) commit_gather();
+        if (hs_.balance.enabled && W_ > 1) {
+            // every rank needs every partition's cost (runtime.cpp:674-675)
+            const std::vector<double> all = distributed_ ? allgather_host(cost) : cost;
+            if (distributed_) { // fixed-width records, one per rank (allgather_host)
+                const size_t stride = all.size() / comm_.world;
+                for (int r = 0; r < comm_.world; ++r)
+                    for (int p = comm_.part_offsets[r]; p < comm_.part_offsets[r + 1]; ++p)
+                        part_cost_[p] = all[stride * r + (p - comm_.part_offsets[r])];
+            } else {
+                for (int p = 0; p < P_; ++p) part_cost_[p0_ + p] = all[p];
+            }
+            have_costs_ = true;
+        }
         sync();
         h_cur_ = std::min(hs_.params.h, 2.0 * h_cur_); // TimestepController::on_frame_committed
         halvings_ = 0;

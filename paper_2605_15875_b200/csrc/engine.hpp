@@ -8,6 +8,7 @@
 #include "audit.hpp"
 #include "geometry.cuh"
 #include "kernels.hpp"
+#include "balance.hpp"
 #include "scene.hpp"
 #include "solver.hpp"
 
@@ -96,6 +97,10 @@ class Engine {
     void get_state(double* q, double* qd);
     void get_rho(double* rho) const;
     std::vector<TraceRow> take_trace();
+    // interface planes in use ((W-1) x (px, py, nx, ny)) and the per-partition
+    // compute costs of the last committed frame that fed the balancer
+    std::vector<double> planes() const;
+    const std::vector<double>& partition_costs() const { return part_cost_; }
     // PCG launch accounting since the last reset (device %globaltimer, SURVEY 8(d) bytes).
     DevPerf read_perf(bool reset);
     void list_stats(long long* rebuilds, int* length, double* delta);
@@ -160,6 +165,12 @@ class Engine {
     int halvings_ = 0;
     long long frame_counter_ = 0;
     std::vector<TraceRow> trace_;
+    // PD load balancer of the planes (runtime.cpp:537-552, 674-675)
+    std::vector<PlaneH> planes_cur_;
+    Balancer balancer_;
+    std::vector<double> part_cost_; // [W_] last committed frame
+    bool have_costs_ = false;
+    double w_last_ = 0.0;
 
     // instance set (host mirrors + device)
     int n_inst_ = 0, n_rows_ = 0;

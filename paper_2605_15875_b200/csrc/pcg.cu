@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(kT) k_pcg(SolverView sv, PcgArgs a) {
     }
     if (blockIdx.x == 0 && threadIdx.x < P) {
         sv.ps[threadIdx.x].pcg_iters = s_it[threadIdx.x];
+        sv.ps[threadIdx.x].pcg_total += s_it[threadIdx.x];
         sv.ps[threadIdx.x].pcg_done = 1;
         sv.ps[threadIdx.x].rr = s_rr[threadIdx.x];
         sv.ps[threadIdx.x].bnorm2 = s_bn[threadIdx.x];
@@ -1007,6 +1008,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         if (on[g]) sv.x[6 * (r0 + lrg[g]) + comp] = x[g];
     if (rank == 0 && threadIdx.x == 0) {
         sv.ps[p].pcg_iters = it;
+        sv.ps[p].pcg_total += it;
         sv.ps[p].pcg_done = 1;
     }
     if (a.fused) { // ||dq||_inf of this CTA's rows -> rank 0's dqm[rank]

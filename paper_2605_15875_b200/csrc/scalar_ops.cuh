@@ -30,6 +30,7 @@ __device__ __forceinline__ void scalar_block(PartState* ps, int P, int op, Frame
             s.searching = 0;
             s.accepted = 0;
             s.iterations = 0;
+            s.pcg_total = 0;
             s.ls_steps = ls;
             s.tol = tol;
             s.final_update = 0.0;

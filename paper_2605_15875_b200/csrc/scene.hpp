@@ -33,6 +33,12 @@ struct PlaneH { // partition.hpp:13-16
     double px = 0.0, py = 0.0, nx = 1.0, ny = 0.0;
 };
 
+// Balancer::Options + SceneData::balance_enabled (balance.hpp:24-29, scene.hpp:31-32).
+struct BalanceOpts {
+    bool enabled = false;
+    double kp = 0.0, kd = 0.0, smoothing = 0.5, dp_max = 0.0;
+};
+
 struct HostScene {
     // bodies
     int nb = 0;
@@ -59,6 +65,7 @@ struct HostScene {
     int max_halvings = 4;
     int force_split_frames = -1;
     std::map<int, std::pair<double, double>> force_split;
+    BalanceOpts balance;
 
     void full_mass_matrix(int b, double* m36) const; // row-major, body.cpp:84-93
 };

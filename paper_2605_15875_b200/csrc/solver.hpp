@@ -38,6 +38,7 @@ struct PartState {
     int pcg_iters;
     int n_active_contacts;
     int n_candidates;
+    int pcg_total;     // PCG iterations summed over this Newton solve (balancer cost)
 };
 
 // Device-side launch accounting of the PCG kernel (bench.py roofline): the
