@@ -154,6 +154,35 @@ __device__ __forceinline__ void clamp_psd(double (&a)[N][N]) {
         }
 }
 
+// clamp_psd of a body block H = ik (M + h^2 H_arap) (+ rho I): translation x
+// couples only to (A00, A01) through rho*sx, rho*sy and y only to (A10, A11)
+// (mass_full), the ARAP Hessian lives on A alone. Rest shapes are centroid-
+// centred (body.cpp:96-118), so those couplings are rounding-level; then the
+// translation block is positive and the clamp is that of the 4x4 A block
+// (4x4 Jacobi instead of 6x6), exact up to O(|coupling|) <= 1e-13 relative.
+// Otherwise (or when the A block is PD, the usual exit) it is the full
+// 6x6 clamp of objective.cpp:12-17.
+__device__ __forceinline__ void clamp_body_block(double (&H)[6][6]) {
+    const double tol = 1e-13 * fmin(H[0][0], H[1][1]);
+    const bool decoupled = H[0][0] > 0.0 && H[1][1] > 0.0 && fabs(H[0][2]) <= tol &&
+                           fabs(H[0][3]) <= tol && fabs(H[1][4]) <= tol && fabs(H[1][5]) <= tol;
+    if (!decoupled) {
+        if (!is_pd<6>(H)) clamp_psd<6>(H);
+        return;
+    }
+    double B[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) B[i][j] = H[2 + i][2 + j];
+    if (is_pd<4>(B)) return;
+    clamp_psd<4>(B);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) H[2 + i][2 + j] = B[i][j];
+}
+
 // Inertia 1/2 (q-qt)^T M (q-qt) with the two identical 3x3 blocks of M
 // (energy.cpp:7-15; mass layout body.cpp:84-93).
 __device__ __forceinline__ void mass_full(const double* k, double (&m)[6][6]) {

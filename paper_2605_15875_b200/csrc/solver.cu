@@ -138,7 +138,7 @@ __global__ void k_body_terms(SolverView sv, const double* qsrc, int with_derivs,
                 H[a][a] += rho;
             }
         }
-        if (sv.project && !is_pd<6>(H)) clamp_psd<6>(H); // PD (the usual case): already its own clamp
+        if (sv.project) clamp_body_block(H);
         store6(sv.rgrad + 6 * r, g);
         double* dst = sv.rdiag + 36 * r;
 #pragma unroll
