@@ -14,37 +14,51 @@
 
 namespace dabd_gpu {
 
-// Jacobi rotation (c, s, t = s / c) annihilating a[p][q]; the identity
-// (1, 0, 0) when it is already 0. With d = aqq - app and e = 2 apq the
-// classical t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)), theta = d / e,
-// is t = sgn(d) e / (|d| + sqrt(d^2 + e^2)) (t = 1 for d = 0): one division,
-// one square root and one reciprocal square root per rotation, no overflow
-// for |theta| -> inf, and branch-free (selects only), so the N/2 independent
-// angles of a round can be interleaved by the scheduler.
-__device__ __forceinline__ void jacobi_cs(double app, double aqq, double apq, double& c, double& s,
-                                          double& tt) {
+// Jacobi rotation (c, s) that (nearly) annihilates a[p][q]. With d = aqq - app
+// and e = 2 apq the annihilating tangent is t = sgn(d) e / (|d| + sqrt(d^2 +
+// e^2)) (t = 1 for d = 0). The angle only steers the iteration: it is taken in
+// FP32 (MUFU reciprocal / square root on d, e pre-scaled by a power of two, so
+// no FP64 divide or square-root chain), and the rotation built from it is
+// orthogonal to FP64 rounding (c = (1 + t^2)^-1/2 by two Newton steps from an
+// FP32 seed, s = t c). jacobi_rotate applies it as an exact similarity, so the
+// eigenvalues keep FP64 accuracy; an angle off by ~1e-7 leaves a residual
+// a[p][q] ~1e-7 of the old one, which the next sweep removes. Branch-free
+// (selects only), so the N/2 angles of a round interleave.
+__device__ __forceinline__ void jacobi_cs(double app, double aqq, double apq, double& c, double& s) {
     const bool on = apq != 0.0;
     const double d = aqq - app, e = 2.0 * apq;
-    double t = copysign(1.0, d) * e / (fabs(d) + sqrt(d * d + e * e));
-    t = d == 0.0 ? 1.0 : t;
-    const double cc = rsqrt(t * t + 1.0);
-    c = on ? cc : 1.0;
-    s = on ? t * cc : 0.0;
-    tt = on ? t : 0.0;
+    // 2^-k with 2^k ~ max(|d|, |e|): exponent arithmetic, no division
+    const int ex = (max(__double2hiint(fabs(d)), __double2hiint(fabs(e))) >> 20) & 0x7ff;
+    const double sc = __hiloint2double((2046 - min(ex, 2045)) << 20, 0);
+    const float df = static_cast<float>(d * sc), ef = static_cast<float>(e * sc);
+    const float r = sqrtf(fmaf(df, df, ef * ef));
+    float tf = copysignf(1.0f, df) * __fdividef(ef, fabsf(df) + r);
+    tf = df == 0.0f ? 1.0f : tf;
+    const double t = on ? static_cast<double>(tf) : 0.0;
+    const double x = fma(t, t, 1.0);
+    double y = static_cast<double>(rsqrtf(static_cast<float>(x)));
+    y = y * fma(-0.5 * x, y * y, 1.5);
+    y = y * fma(-0.5 * x, y * y, 1.5);
+    c = on ? y : 1.0;
+    s = t * c;
 }
 
-// Apply the rotation with t = s / c (Rutishauser's update: the 2x2 pivot
-// block in closed form, the other entries of rows/columns p and q rotated
-// once and mirrored, so ~half the FP64 work of rotating the full matrix
-// twice). The identity rotation (1, 0, t = 0) is an exact no-op.
+// a <- J^T a J, v <- v J for the rotation J in the (p, q) plane (column p =
+// (c, -s), column q = (s, c)): the 2x2 pivot block in closed form, rows and
+// columns p, q of the rest rotated once and mirrored. The identity rotation
+// (1, 0) is an exact no-op.
 template <int N>
 __device__ __forceinline__ void jacobi_rotate(double (&a)[N][N], double (&v)[N][N], int p, int q,
-                                              double c, double s, double t) {
-    const double apq = a[p][q];
-    a[p][p] -= t * apq;
-    a[q][q] += t * apq;
-    a[p][q] = 0.0;
-    a[q][p] = 0.0;
+                                              double c, double s) {
+    const double app = a[p][p], aqq = a[q][q], apq = a[p][q];
+    const double cc = c * c, ss = s * s, cs2 = 2.0 * c * s;
+    const double npp = (cc * app + ss * aqq) - cs2 * apq;
+    const double nqq = (ss * app + cc * aqq) + cs2 * apq;
+    const double npq = (c * s) * (app - aqq) + (cc - ss) * apq;
+    a[p][p] = npp;
+    a[q][q] = nqq;
+    a[p][q] = npq;
+    a[q][p] = npq;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         if (k == p || k == q) continue;
@@ -92,7 +106,7 @@ __device__ __forceinline__ void jacobi_eig(double (&a)[N][N], double (&v)[N][N])
             // circle method: position 0 fixed, positions 1..N-1 hold
             // players (i - 1 - round) mod (N - 1) + 1; pair position i with N-1-i
             int pp[N / 2], qq[N / 2];
-            double cc[N / 2], ss[N / 2], tt[N / 2];
+            double cc[N / 2], ss[N / 2];
 #pragma unroll
             for (int i = 0; i < N / 2; ++i) {
                 const int j = N - 1 - i;
@@ -100,10 +114,10 @@ __device__ __forceinline__ void jacobi_eig(double (&a)[N][N], double (&v)[N][N])
                 const int y = ((j - 1 + (N - 1) - round) % (N - 1)) + 1;
                 pp[i] = x < y ? x : y;
                 qq[i] = x < y ? y : x;
-                jacobi_cs(a[pp[i]][pp[i]], a[qq[i]][qq[i]], a[pp[i]][qq[i]], cc[i], ss[i], tt[i]);
+                jacobi_cs(a[pp[i]][pp[i]], a[qq[i]][qq[i]], a[pp[i]][qq[i]], cc[i], ss[i]);
             }
 #pragma unroll
-            for (int i = 0; i < N / 2; ++i) jacobi_rotate<N>(a, v, pp[i], qq[i], cc[i], ss[i], tt[i]);
+            for (int i = 0; i < N / 2; ++i) jacobi_rotate<N>(a, v, pp[i], qq[i], cc[i], ss[i]);
         }
     }
 }

@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <bit>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -1269,7 +1271,39 @@ FrameStats Engine::frame_reference() {
 
 // runtime.cpp:110-694 on replicated global state with every partition of
 // this context solved in the same batched kernels.
+// DABD_GPU_ADMM_PROFILE=1: host-side phase clock of the multi-partition
+// frame (synchronises the stream at every mark; a probe, never on in bench).
+namespace {
+struct AdmmProfile {
+    bool on = std::getenv("DABD_GPU_ADMM_PROFILE") != nullptr;
+    double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    void mark(int slot, cudaStream_t s) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        t[slot] += std::chrono::duration<double, std::milli>(now - last).count();
+        ++n[slot];
+        last = now;
+    }
+    ~AdmmProfile() {
+        if (!on) return;
+        static const char* names[8] = {"frame_setup", "consensus+gate", "decision", "newton",
+                                       "delta_inf", "commit", "other", "-"};
+        for (int i = 0; i < 7; ++i)
+            std::fprintf(stderr, "admm_profile %-15s %10.3f ms %8lld marks\n", names[i], t[i], n[i]);
+    }
+};
+AdmmProfile& admm_prof() {
+    static AdmmProfile p;
+    return p;
+}
+} // namespace
+
 FrameStats Engine::frame_admm(int frame) {
+    AdmmProfile& prof = admm_prof();
+    prof.mark(6, s_);
     const int nb = hs_.nb;
     // PD balancer step on the previous committed frame's partition costs;
     // the shifted planes take effect in this frame's partitioning
@@ -1395,6 +1429,7 @@ FrameStats Engine::frame_admm(int frame) {
         const double tol = P.theta * h * P.scene_scale;
         std::vector<double> dq(P_, 0.0);
         bool ended = false, retry = false;
+        prof.mark(0, s_);
         // A local failure on one rank must not leave its peers blocked in a
         // collective: it is carried to the next agreement point instead.
         std::string fail;
@@ -1421,6 +1456,7 @@ FrameStats Engine::frame_admm(int frame) {
                     rl = rloc_.to_host(s_);
                     sl = sloc_.to_host(s_);
                     check_err("admm: consensus/gate");
+                    prof.mark(1, s_);
                 } catch (const Error& e) {
                     if (!distributed_) throw;
                     if (fail.empty()) fail = e.what();
@@ -1477,6 +1513,7 @@ FrameStats Engine::frame_admm(int frame) {
                 }
                 launch_adapt(I, ianc_.get(), irho_.get(), irho0_.get(), rb_.get(), sb_.get(),
                              hs_.adapt, iz_.get(), iznext_.get(), s_);
+                prof.mark(2, s_);
             }
             if (!fail.empty()) continue;
             try {
@@ -1490,7 +1527,9 @@ FrameStats Engine::frame_admm(int frame) {
                 for (int p = 0; p < P_; ++p) cost[p] += partition_cost(ps_h_[p]);
                 st.max_contacts = std::max(st.max_contacts, n_contacts_);
                 st.max_candidates = std::max(st.max_candidates, n_super_);
+                prof.mark(3, s_);
                 dq = n_rows_ ? delta_inf(iq_.get(), iqbefore_.get()) : std::vector<double>(P_, 0.0);
+                prof.mark(4, s_);
             } catch (const Error& e) {
                 if (!distributed_) throw;
                 fail = e.what();
@@ -1525,6 +1564,7 @@ FrameStats Engine::frame_admm(int frame) {
             have_costs_ = true;
         }
         sync();
+        prof.mark(5, s_);
         h_cur_ = std::min(hs_.params.h, 2.0 * h_cur_); // TimestepController::on_frame_committed
         halvings_ = 0;
         st.committed = 1;
