@@ -20,6 +20,7 @@
  *   dabd_gpu_holder_masks        body_holder_mask                include/dabd/partition.hpp:43-45
  *   dabd_gpu_objective           LocalObjective::value/derivatives include/dabd/objective.hpp:34-75
  *   dabd_gpu_newton_solve        newton_solve                    include/dabd/newton.hpp:25-26
+ *   dabd_gpu_contact3d_terms     3D extension of contact_energy  src/energy.cpp:63-94 (PT / EE, no reference)
  *   dabd_gpu_balancer_*          Balancer, imbalance_metric, pd_update, balance_factor
  *                                                                include/dabd/balance.hpp:9-56
  *   dabd_gpu_run_frames          run_reference (workers==0)      src/sim.cpp:186-249
@@ -255,6 +256,26 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_partition_costs(dabd_gpu_ctx* ctx, dou
  * sigma) doubles; returns the number of rows written (<= capacity). */
 DABD_GPU_API dabd_gpu_status dabd_gpu_take_trace(dabd_gpu_ctx* ctx, double* rows, int capacity,
                                                  int* count);
+
+/* ---- 3D affine-body contact terms ----------------------
+ * The reference is 2D; this is its contact_energy (energy.cpp:63-94) for 3D
+ * affine bodies (q = [p(3), A row-major(9)], x = A xbar + p) and the two 3D
+ * primitive pairs: kind 0 point-triangle (rest: p of body a, t0 t1 t2 of body
+ * b), kind 1 edge-edge (rest: a0 a1 of body a, b0 b1 of body b). Per pair k
+ * (host arrays): qa/qb [n][12], rest [n][4][3] -> distance d [n], closest-
+ * feature type [n] (PT: 0-2 vertex, 3-5 edge t0t1/t1t2/t2t0, 6 face; EE: 0-3
+ * vertex pairs a0b0/a0b1/a1b0/a1b1, 4-5 a0/a1 vs edge b, 6-7 b0/b1 vs edge a,
+ * 8 line-line), value = weight * b(d) with the log barrier of energy.cpp:50-61
+ * (0 for d >= d_hat), grad [n][24] (body a then b) and, when hess != NULL,
+ * hess [n][24][24] (the objective.cpp:12-17 clamp when project != 0).
+ * Computed on `device`; RUNTIME when a pair has d <= 0. Parity unpinned: no
+ * reference implements 3D (oracle/geometry3d.cpp restates it independently). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_contact3d_terms(int device, int n, const int* kind,
+                                                      const double* qa, const double* qb,
+                                                      const double* rest, double d_hat,
+                                                      double kappa, double weight, int project,
+                                                      double* d, int* dtype, double* value,
+                                                      double* grad, double* hess);
 
 /* ---- PD load balancer (host control logic, no device) ----------------------
  * balance.cpp:8-83: imbalance T = (eta-1)/(eta+1), eta = tau_i/tau_j (times

@@ -297,3 +297,14 @@ def clamp_psd(M):
     out = np.zeros_like(M)
     _check(lib().oracle_clamp_psd(n, _d(M), _d(out)))
     return out
+
+
+def contact3d_value(kind, qa, qb, rest, d_hat, kappa, weight=1.0):
+    """oracle/geometry3d.cpp: (d, type, value) of one 3D PT (kind 0) / EE (kind 1) pair."""
+    d, t, v = C.c_double(), C.c_int(), C.c_double()
+    rc = lib().oracle_contact3d_value(int(kind), _d(_f64(qa)), _d(_f64(qb)), _d(_f64(rest)),
+                                      C.c_double(d_hat), C.c_double(kappa), C.c_double(weight),
+                                      C.byref(d), C.byref(t), C.byref(v))
+    if rc != 0:
+        raise OracleError("contact3d: d <= 0")
+    return d.value, t.value, v.value

@@ -418,3 +418,29 @@ def load_trajectory(out_dir: str, initial_q) -> Trajectory:
         raise L.DabdGpuError(1, f"load_trajectory: no snapshots in {out_dir}")
     return Trajectory(np.array(qs), np.array(qds), np.zeros(len(qs)), [], np.zeros((0, 8)),
                       np.zeros(0))
+
+
+# ---- 3D affine-body contact terms (no reference) ----
+def contact3d_terms(kind, qa, qb, rest, d_hat: float, kappa: float, weight: float = 1.0,
+                    project: bool = True, hessian: bool = True, device: int = 0) -> dict:
+    """Per pair: kind 0 point-triangle / 1 edge-edge, qa/qb [n][12], rest
+    [n][4][3] -> d, type, value, grad [n][24], hess [n][24][24] (see
+    dabd_gpu_contact3d_terms)."""
+    kind = _i32(kind).reshape(-1)
+    n = len(kind)
+    qa = _f64(qa, (n, 12))
+    qb = _f64(qb, (n, 12))
+    rest = _f64(rest, (n, 4, 3))
+    d = np.zeros(max(n, 1))
+    t = np.zeros(max(n, 1), dtype=np.int32)
+    v = np.zeros(max(n, 1))
+    g = np.zeros((max(n, 1), 24))
+    h = np.zeros((max(n, 1), 24, 24)) if hessian else None
+    L.check(L.load().dabd_gpu_contact3d_terms(device, n, _i(kind), _d(qa), _d(qb), _d(rest),
+                                              C.c_double(d_hat), C.c_double(kappa),
+                                              C.c_double(weight), int(project), _d(d), _i(t),
+                                              _d(v), _d(g), _d(h)))
+    out = dict(d=d[:n], type=t[:n], value=v[:n], grad=g[:n])
+    if hessian:
+        out["hess"] = h[:n]
+    return out

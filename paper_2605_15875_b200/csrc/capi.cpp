@@ -2,6 +2,7 @@
 // thread-local last error, no exceptions across the boundary, null -> INVALID.
 #include "dabd_gpu.h"
 
+#include "contact3d.hpp"
 #include "engine.hpp"
 #include "instrument.hpp"
 #include "scene.hpp"
@@ -408,6 +409,57 @@ dabd_gpu_status dabd_gpu_ctx_partition_costs(dabd_gpu_ctx* ctx, double* costs) {
     const std::vector<double>& c = ctx->e->partition_costs();
     std::copy(c.begin(), c.end(), costs);
     return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_contact3d_terms(int device, int n, const int* kind, const double* qa,
+                                         const double* qb, const double* rest, double d_hat,
+                                         double kappa, double weight, int project, double* d,
+                                         int* dtype, double* value, double* grad, double* hess) {
+    if (n < 0) return null_arg();
+    if (n > 0 && (!kind || !qa || !qb || !rest || !d || !dtype || !value || !grad)) return null_arg();
+    if (!(d_hat > 0.0)) {
+        set_error("contact3d: d_hat must be > 0");
+        return DABD_GPU_ERR_INVALID;
+    }
+    return guarded([&] {
+        for (int k = 0; k < n; ++k)
+            if (kind[k] != 0 && kind[k] != 1) throw dabd_gpu::InvalidArg("contact3d: kind must be 0 (PT) or 1 (EE)");
+        if (n == 0) return DABD_GPU_OK;
+        CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t s = nullptr;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        dabd_gpu::DBuf<int> dk, dt, derr;
+        dabd_gpu::DBuf<double> dqa, dqb, dr, dd, dv, dg, dh;
+        dk.upload(kind, n, s);
+        dqa.upload(qa, 12 * static_cast<size_t>(n), s);
+        dqb.upload(qb, 12 * static_cast<size_t>(n), s);
+        dr.upload(rest, 12 * static_cast<size_t>(n), s);
+        dd.resize(n);
+        dt.resize(n);
+        dv.resize(n);
+        dg.resize(24 * static_cast<size_t>(n));
+        if (hess) dh.resize(576 * static_cast<size_t>(n));
+        derr.resize(1);
+        derr.zero(s);
+        dabd_gpu::Contact3dArgs a{n, dk.get(), dqa.get(), dqb.get(), dr.get(), d_hat, kappa, weight,
+                                  project, dd.get(), dt.get(), dv.get(), dg.get(),
+                                  hess ? dh.get() : nullptr, derr.get()};
+        dabd_gpu::launch_contact3d(a, s);
+        CUDA_CHECK(cudaGetLastError());
+        int err = 0;
+        CUDA_CHECK(cudaMemcpyAsync(d, dd.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaMemcpyAsync(dtype, dt.get(), n * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaMemcpyAsync(value, dv.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaMemcpyAsync(grad, dg.get(), 24 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (hess)
+            CUDA_CHECK(cudaMemcpyAsync(hess, dh.get(), 576 * static_cast<size_t>(n) * sizeof(double),
+                                       cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaMemcpyAsync(&err, derr.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        CUDA_CHECK(cudaStreamDestroy(s));
+        if (err) throw dabd_gpu::Error("contact3d: a pair has d <= 0 (interpenetration)");
+        return DABD_GPU_OK;
+    });
 }
 
 dabd_gpu_status dabd_gpu_imbalance_metric(double tau_i, double tau_j, double* out) {

@@ -1,0 +1,161 @@
+// Batched 3D contact terms: per point-triangle or
+// edge-edge pair of two 12-DoF affine bodies, the closest-feature type, the
+// unsigned distance, the barrier value (energy.cpp:50-61 in 3D) and its
+// gradient and PSD-clamped Hessian over the 24 body DoF. The projection uses
+// the rank structure of the 2D kernel (solver.cu, contact_terms_one): with T
+// the 12x24 map from the bodies' DoF to the four points, G = T T^T =
+// (Gp (x) I3) with Gp = blockdiag over bodies of (1 + xbar_i . xbar_j), so
+// clamp(T^T A T) = T^T L^-T clamp(L^T A L) L^-1 T, L = Lp (x) I3: a 12x12
+// eigenproblem instead of 24x24 (energy.cuh's round-robin Jacobi). One
+// thread per pair.
+#include "geometry3d.cuh"
+
+#include "contact3d.hpp"
+#include "dbuf.hpp"
+#include "instrument.hpp"
+
+namespace dabd_gpu {
+
+namespace {
+
+__global__ void k_contact3d(Contact3dArgs ar) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ar.n) return;
+    const int kind = ar.kind[k];
+    const double* qa = ar.qa + 12 * static_cast<size_t>(k);
+    const double* qb = ar.qb + 12 * static_cast<size_t>(k);
+    V3 xb[4], x[4];
+    int body[4];
+    for (int i = 0; i < 4; ++i) {
+        xb[i] = v3(ar.rest + 12 * static_cast<size_t>(k) + 3 * i);
+        body[i] = kind == 0 ? (i == 0 ? 0 : 1) : (i < 2 ? 0 : 1);
+        x[i] = world3(body[i] == 0 ? qa : qb, xb[i]);
+    }
+    const int type = kind == 0 ? pt_type(x[0], x[1], x[2], x[3]) : ee_type(x[0], x[1], x[2], x[3]);
+    double gf[12], Hf[12][12];
+    const double f = f_pair(kind, type, x, gf, Hf);
+    const double d = sqrt(f);
+    ar.d[k] = d;
+    ar.dtype[k] = type;
+    double* gout = ar.grad + 24 * static_cast<size_t>(k);
+    double* hout = ar.hess ? ar.hess + 576 * static_cast<size_t>(k) : nullptr;
+    for (int i = 0; i < 24; ++i) gout[i] = 0.0;
+    if (hout)
+        for (int i = 0; i < 576; ++i) hout[i] = 0.0;
+    if (!(d < ar.d_hat)) {
+        ar.value[k] = 0.0;
+        return;
+    }
+    if (!(d > 0.0)) {
+        atomicCAS(ar.err, 0, 1);
+        ar.value[k] = 0.0;
+        return;
+    }
+    const Barrier br = barrier(d, ar.d_hat, ar.kappa);
+    ar.value[k] = ar.weight * br.b;
+    // grad d = grad f / 2d, hess d = hess f / 2d - grad f grad f^T / 4d^3
+    double gd[12];
+    const double i2d = 0.5 / d;
+    for (int i = 0; i < 12; ++i) gd[i] = gf[i] * i2d;
+    double A[12][12];
+    for (int i = 0; i < 12; ++i)
+        for (int j = 0; j < 12; ++j) {
+            const double hd = Hf[i][j] * i2d - gd[i] * gd[j] / d;
+            A[i][j] = ar.weight * (br.ddb * (gd[i] * gd[j]) + br.db * hd);
+        }
+    // body-space gradient: J(xbar)^T g per point (J = [I3 | I3 (x) xbar^T])
+    for (int i = 0; i < 4; ++i) {
+        double* gb = gout + 12 * body[i];
+        for (int r = 0; r < 3; ++r) {
+            const double gi = ar.weight * br.db * gd[3 * i + r];
+            gb[r] += gi;
+            gb[3 + 3 * r + 0] += gi * xb[i].x;
+            gb[3 + 3 * r + 1] += gi * xb[i].y;
+            gb[3 + 3 * r + 2] += gi * xb[i].z;
+        }
+    }
+    if (!hout) return;
+    if (ar.project) {
+        // Gp = blockdiag over bodies of (1 + xbar_i . xbar_j), Cholesky Lp,
+        // Li = Lp^-1 (both lower triangular)
+        double Gp[4][4], Lp[4][4], Li[4][4];
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j) {
+                Gp[i][j] = body[i] == body[j] ? 1.0 + dot3(xb[i], xb[j]) : 0.0;
+                Lp[i][j] = 0.0;
+                Li[i][j] = 0.0;
+            }
+        for (int j = 0; j < 4; ++j) {
+            double s = Gp[j][j];
+            for (int l = 0; l < j; ++l) s -= Lp[j][l] * Lp[j][l];
+            Lp[j][j] = sqrt(fmax(s, 1e-300));
+            for (int i = j + 1; i < 4; ++i) {
+                double t = Gp[i][j];
+                for (int l = 0; l < j; ++l) t -= Lp[i][l] * Lp[j][l];
+                Lp[i][j] = t / Lp[j][j];
+            }
+        }
+        for (int j = 0; j < 4; ++j) {
+            Li[j][j] = 1.0 / Lp[j][j];
+            for (int i = j + 1; i < 4; ++i) {
+                double t = 0.0;
+                for (int l = j; l < i; ++l) t -= Lp[i][l] * Li[l][j];
+                Li[i][j] = t / Lp[i][i];
+            }
+        }
+        // B = L^T A L, L = Lp (x) I3
+        double B[12][12];
+        for (int i = 0; i < 4; ++i)
+            for (int c = 0; c < 3; ++c)
+                for (int j = 0; j < 4; ++j)
+                    for (int e = 0; e < 3; ++e) {
+                        double s = 0.0;
+                        for (int kk = i; kk < 4; ++kk)
+                            for (int l = j; l < 4; ++l) s += Lp[kk][i] * A[3 * kk + c][3 * l + e] * Lp[l][j];
+                        B[3 * i + c][3 * j + e] = s;
+                    }
+        for (int i = 0; i < 12; ++i)
+            for (int j = i + 1; j < 12; ++j) {
+                const double m = 0.5 * (B[i][j] + B[j][i]);
+                B[i][j] = m;
+                B[j][i] = m;
+            }
+        clamp_psd<12>(B);
+        // A <- L^-T B+ L^-1
+        for (int i = 0; i < 4; ++i)
+            for (int c = 0; c < 3; ++c)
+                for (int j = 0; j < 4; ++j)
+                    for (int e = 0; e < 3; ++e) {
+                        double s = 0.0;
+                        for (int kk = i; kk < 4; ++kk)
+                            for (int l = j; l < 4; ++l) s += Li[kk][i] * B[3 * kk + c][3 * l + e] * Li[l][j];
+                        A[3 * i + c][3 * j + e] = s;
+                    }
+    }
+    // H = T^T A T: block (body[i], body[j]) += J_i^T A_ij J_j
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            const double xi[3] = {xb[i].x, xb[i].y, xb[i].z}, xj[3] = {xb[j].x, xb[j].y, xb[j].z};
+            double* H = hout + 24 * (12 * body[i]) + 12 * body[j];
+            for (int r = 0; r < 3; ++r)
+                for (int s = 0; s < 3; ++s) {
+                    const double m = A[3 * i + r][3 * j + s];
+                    // rows: translation r, A_rc (3 + 3r + c); columns likewise with s
+                    H[24 * r + s] += m;
+                    for (int c = 0; c < 3; ++c) {
+                        H[24 * r + 3 + 3 * s + c] += m * xj[c];
+                        H[24 * (3 + 3 * r + c) + s] += m * xi[c];
+                        for (int c2 = 0; c2 < 3; ++c2) H[24 * (3 + 3 * r + c) + 3 + 3 * s + c2] += m * xi[c] * xj[c2];
+                    }
+                }
+        }
+}
+
+} // namespace
+
+void launch_contact3d(const Contact3dArgs& a, cudaStream_t s) {
+    if (a.n <= 0) return;
+    DABD_LAUNCH("k_contact3d", s, k_contact3d<<<(a.n + 63) / 64, 64, 0, s>>>(a));
+}
+
+} // namespace dabd_gpu

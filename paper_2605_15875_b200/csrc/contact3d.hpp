@@ -1,0 +1,30 @@
+// Batched 3D contact terms (contact3d.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace dabd_gpu {
+
+// Device pointers. kind[k]: 0 point-triangle, 1 edge-edge; qa/qb [n][12];
+// rest [n][4][3] (PT: p of a, t0 t1 t2 of b; EE: a0 a1 of a, b0 b1 of b).
+// Outputs: d [n], dtype [n], value [n] = weight * b(d) (0 when d >= d_hat),
+// grad [n][24] (body a then b), hess [n][24][24] or nullptr.
+struct Contact3dArgs {
+    int n;
+    const int* kind;
+    const double* qa;
+    const double* qb;
+    const double* rest;
+    double d_hat, kappa, weight;
+    int project;
+    double* d;
+    int* dtype;
+    double* value;
+    double* grad;
+    double* hess;
+    int* err;
+};
+
+void launch_contact3d(const Contact3dArgs& a, cudaStream_t s);
+
+} // namespace dabd_gpu
