@@ -21,6 +21,7 @@
  *   dabd_gpu_objective           LocalObjective::value/derivatives include/dabd/objective.hpp:34-75
  *   dabd_gpu_newton_solve        newton_solve                    include/dabd/newton.hpp:25-26
  *   dabd_gpu_contact3d_terms     3D extension of contact_energy  src/energy.cpp:63-94 (PT / EE, no reference)
+ *   dabd_gpu_ccd3d               3D extension of ccd_toi          src/geometry.cpp:232-341 (no reference)
  *   dabd_gpu_balancer_*          Balancer, imbalance_metric, pd_update, balance_factor
  *                                                                include/dabd/balance.hpp:9-56
  *   dabd_gpu_run_frames          run_reference (workers==0)      src/sim.cpp:186-249
@@ -276,6 +277,16 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_contact3d_terms(int device, int n, const i
                                                       double kappa, double weight, int project,
                                                       double* d, int* dtype, double* value,
                                                       double* grad, double* hess);
+
+/* CCD of the same 3D pairs while both bodies move linearly from (qa0, qb0) to
+ * (qa1, qb1) (so every point moves linearly): additive CCD (conservative
+ * advancement on the distance), toi [n] = 1.0 when the pair stays apart over
+ * [0, 1], else a time at which it still keeps 10% of its starting gap; the
+ * line-search bound is min(toi) like ccd_toi_scene (geometry.cpp:322-341).
+ * 0.0 when a pair already touches. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ccd3d(int device, int n, const int* kind, const double* qa0,
+                                            const double* qa1, const double* qb0,
+                                            const double* qb1, const double* rest, double* toi);
 
 /* ---- PD load balancer (host control logic, no device) ----------------------
  * balance.cpp:8-83: imbalance T = (eta-1)/(eta+1), eta = tau_i/tau_j (times

@@ -144,3 +144,49 @@ int oracle_contact3d_value(int kind, const double* qa, const double* qb, const d
 }
 
 } // extern "C"
+
+extern "C" {
+
+// Additive CCD of one pair (same rule as csrc/contact3d.cu accd_pair), with
+// this file's minimum-over-features distance.
+double oracle_ccd3d(int kind, const double* qa0, const double* qa1, const double* qb0,
+                    const double* qb1, const double* rest) {
+    using namespace oracle3d;
+    V x[4], dx[4];
+    for (int i = 0; i < 4; ++i) {
+        const bool on_a = kind == 0 ? i == 0 : i < 2;
+        x[i] = world(on_a ? qa0 : qb0, rest + 3 * i);
+        const V x1 = world(on_a ? qa1 : qb1, rest + 3 * i);
+        dx[i] = sub(x1, x[i]);
+    }
+    V mean;
+    for (int c = 0; c < 3; ++c) mean[c] = 0.25 * (((dx[0][c] + dx[1][c]) + dx[2][c]) + dx[3][c]);
+    double m0 = 0.0, m1 = 0.0;
+    for (int i = 0; i < 4; ++i) {
+        dx[i] = sub(dx[i], mean);
+        const double n = std::sqrt(dot(dx[i], dx[i]));
+        if (kind == 0 ? i == 0 : i < 2) m0 = std::max(m0, n);
+        else m1 = std::max(m1, n);
+    }
+    const double lp = m0 + m1;
+    if (!(lp > 0.0)) return 1.0;
+    auto dist = [&]() {
+        int t;
+        return kind == 0 ? pt_distance(x[0], x[1], x[2], x[3], &t) : ee_distance(x[0], x[1], x[2], x[3], &t);
+    };
+    double d = dist();
+    if (!(d > 0.0)) return 0.0;
+    const double g = 0.1 * d;
+    double t = 0.0, tl = 0.9 * d / lp;
+    for (int it = 0; it < 100000; ++it) {
+        for (int i = 0; i < 4; ++i) x[i] = axpy(tl, dx[i], x[i]);
+        d = dist();
+        if (t > 0.0 && d < g) break;
+        t += tl;
+        if (t > 1.0) return 1.0;
+        tl = 0.9 * d / lp;
+    }
+    return t;
+}
+
+} // extern "C"

@@ -308,3 +308,10 @@ def contact3d_value(kind, qa, qb, rest, d_hat, kappa, weight=1.0):
     if rc != 0:
         raise OracleError("contact3d: d <= 0")
     return d.value, t.value, v.value
+
+
+def ccd3d(kind, qa0, qa1, qb0, qb1, rest):
+    """oracle/geometry3d.cpp additive CCD of one 3D pair."""
+    f = lib().oracle_ccd3d
+    f.restype = C.c_double
+    return f(int(kind), _d(_f64(qa0)), _d(_f64(qa1)), _d(_f64(qb0)), _d(_f64(qb1)), _d(_f64(rest)))

@@ -444,3 +444,14 @@ def contact3d_terms(kind, qa, qb, rest, d_hat: float, kappa: float, weight: floa
     if hessian:
         out["hess"] = h[:n]
     return out
+
+
+def ccd3d(kind, qa0, qa1, qb0, qb1, rest, device: int = 0) -> np.ndarray:
+    """Additive CCD per 3D pair (dabd_gpu_ccd3d): toi in [0, 1]."""
+    kind = _i32(kind).reshape(-1)
+    n = len(kind)
+    arrs = [_f64(a, (n, 12)) for a in (qa0, qa1, qb0, qb1)]
+    rest = _f64(rest, (n, 4, 3))
+    toi = np.zeros(max(n, 1))
+    L.check(L.load().dabd_gpu_ccd3d(device, n, _i(kind), *[_d(a) for a in arrs], _d(rest), _d(toi)))
+    return toi[:n]

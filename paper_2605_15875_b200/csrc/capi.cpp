@@ -462,6 +462,37 @@ dabd_gpu_status dabd_gpu_contact3d_terms(int device, int n, const int* kind, con
     });
 }
 
+dabd_gpu_status dabd_gpu_ccd3d(int device, int n, const int* kind, const double* qa0, const double* qa1,
+                               const double* qb0, const double* qb1, const double* rest, double* toi) {
+    if (n < 0) return null_arg();
+    if (n > 0 && (!kind || !qa0 || !qa1 || !qb0 || !qb1 || !rest || !toi)) return null_arg();
+    return guarded([&] {
+        for (int k = 0; k < n; ++k)
+            if (kind[k] != 0 && kind[k] != 1) throw dabd_gpu::InvalidArg("ccd3d: kind must be 0 (PT) or 1 (EE)");
+        if (n == 0) return DABD_GPU_OK;
+        CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t s = nullptr;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        const size_t m = 12 * static_cast<size_t>(n);
+        dabd_gpu::DBuf<int> dk;
+        dabd_gpu::DBuf<double> a0, a1, b0, b1, dr, dt;
+        dk.upload(kind, n, s);
+        a0.upload(qa0, m, s);
+        a1.upload(qa1, m, s);
+        b0.upload(qb0, m, s);
+        b1.upload(qb1, m, s);
+        dr.upload(rest, m, s);
+        dt.resize(n);
+        dabd_gpu::Ccd3dArgs a{n, dk.get(), a0.get(), a1.get(), b0.get(), b1.get(), dr.get(), dt.get()};
+        dabd_gpu::launch_ccd3d(a, s);
+        CUDA_CHECK(cudaGetLastError());
+        CUDA_CHECK(cudaMemcpyAsync(toi, dt.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        CUDA_CHECK(cudaStreamDestroy(s));
+        return DABD_GPU_OK;
+    });
+}
+
 dabd_gpu_status dabd_gpu_imbalance_metric(double tau_i, double tau_j, double* out) {
     if (!out) return null_arg();
     return guarded([&] {

@@ -27,4 +27,18 @@ struct Contact3dArgs {
 
 void launch_contact3d(const Contact3dArgs& a, cudaStream_t s);
 
+// CCD of the same pairs moving linearly from (qa0, qb0) to (qa1, qb1).
+struct Ccd3dArgs {
+    int n;
+    const int* kind;
+    const double* qa0;
+    const double* qa1;
+    const double* qb0;
+    const double* qb1;
+    const double* rest;
+    double* toi;
+};
+
+void launch_ccd3d(const Ccd3dArgs& a, cudaStream_t s);
+
 } // namespace dabd_gpu
