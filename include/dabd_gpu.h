@@ -288,6 +288,25 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ccd3d(int device, int n, const int* kind, 
                                             const double* qa1, const double* qb0,
                                             const double* qb1, const double* rest, double* toi);
 
+/* Mass moments of a 3D affine body from a closed, outward-oriented triangle
+ * surface (verts [n_verts][3], tris [n_tris][3]): moments10 = density * (V,
+ * s_x, s_y, s_z, S_xx, S_xy, S_xz, S_yy, S_yz, S_zz) about the rest centroid
+ * (s = 0 by construction), centroid [3] (the body's initial translation, as
+ * make_affine_body re-centres, body.cpp:96-118), volume. Host only. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_body3d_moments(int n_verts, const double* verts, int n_tris,
+                                                     const int* tris, double density,
+                                                     double* moments10, double* centroid,
+                                                     double* volume);
+/* Body terms of n 12-DoF bodies (energy.cpp:7-48 in 3D): value = 1/2 (q -
+ * qt)^T M (q - qt) + scale * w ||A^T A - I||_F^2 with M from moments10, w [n]
+ * (kappa * volume * arap_scale), scale (h^2 in the objective); grad [n][12],
+ * hess [n][12][12] (nullable; clamped like objective.cpp:143-167 when
+ * project != 0). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_body3d_terms(int device, int n, const double* q,
+                                                   const double* qt, const double* moments10,
+                                                   const double* w, double scale, int project,
+                                                   double* value, double* grad, double* hess);
+
 /* ---- PD load balancer (host control logic, no device) ----------------------
  * balance.cpp:8-83: imbalance T = (eta-1)/(eta+1), eta = tau_i/tau_j (times
  * must be > 0, else RUNTIME); dp = kp T + kd (T - T_prev) clamped to

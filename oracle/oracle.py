@@ -315,3 +315,41 @@ def ccd3d(kind, qa0, qa1, qb0, qb1, rest):
     f = lib().oracle_ccd3d
     f.restype = C.c_double
     return f(int(kind), _d(_f64(qa0)), _d(_f64(qa1)), _d(_f64(qb0)), _d(_f64(qb1)), _d(_f64(rest)))
+
+
+# ---- 3D affine bodies (test-only restatements, numpy; parity unpinned) ----
+def polyhedron_moments_tets(verts, tris, density):
+    """Mass moments of a closed, outward-oriented triangle surface by signed
+    tetrahedra from the origin (a different decomposition than the library's
+    divergence-theorem integrals): (moments10 about the centroid, centroid, V)."""
+    v = np.asarray(verts, dtype=np.float64).reshape(-1, 3)
+    V, first, second = 0.0, np.zeros(3), np.zeros((3, 3))
+    for t in np.asarray(tris).reshape(-1, 3):
+        a, b, c = v[t[0]], v[t[1]], v[t[2]]
+        vol = np.dot(a, np.cross(b, c)) / 6.0
+        V += vol
+        first += vol * (a + b + c) / 4.0
+        s = a + b + c
+        second += vol / 20.0 * (np.outer(a, a) + np.outer(b, b) + np.outer(c, c) + np.outer(s, s))
+    cen = first / V
+    S = second - V * np.outer(cen, cen)
+    mom = density * np.array([V, 0, 0, 0, S[0, 0], S[0, 1], S[0, 2], S[1, 1], S[1, 2], S[2, 2]])
+    mom[1:4] = 0.0
+    return mom, cen, V
+
+
+def body3d_value(q, qt, mom, w, scale):
+    """1/2 (q - qt)^T M (q - qt) + scale w ||A^T A - I||_F^2 (energy.cpp:7-48 in 3D)."""
+    q, qt = np.asarray(q, float), np.asarray(qt, float)
+    m, s = mom[0], np.asarray(mom[1:4])
+    S = np.array([[mom[4], mom[5], mom[6]], [mom[5], mom[7], mom[8]], [mom[6], mom[8], mom[9]]])
+    M = np.zeros((12, 12))
+    for r in range(3):
+        M[r, r] = m
+        M[r, 3 + 3 * r:6 + 3 * r] = s
+        M[3 + 3 * r:6 + 3 * r, r] = s
+        M[3 + 3 * r:6 + 3 * r, 3 + 3 * r:6 + 3 * r] = S
+    dq = q - qt
+    A = q[3:].reshape(3, 3)
+    G = A.T @ A - np.eye(3)
+    return 0.5 * dq @ M @ dq + scale * w * float(np.sum(G * G))

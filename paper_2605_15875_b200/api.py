@@ -455,3 +455,33 @@ def ccd3d(kind, qa0, qa1, qb0, qb1, rest, device: int = 0) -> np.ndarray:
     toi = np.zeros(max(n, 1))
     L.check(L.load().dabd_gpu_ccd3d(device, n, _i(kind), *[_d(a) for a in arrs], _d(rest), _d(toi)))
     return toi[:n]
+
+
+def body3d_moments(verts, tris, density: float = 1000.0):
+    """Mass moments of a closed triangle surface (dabd_gpu_body3d_moments):
+    (moments10, centroid, volume)."""
+    v = _f64(verts).reshape(-1, 3)
+    t = _i32(tris).reshape(-1, 3)
+    mom, cen, vol = np.zeros(10), np.zeros(3), C.c_double()
+    L.check(L.load().dabd_gpu_body3d_moments(len(v), _d(v), len(t), _i(t), C.c_double(density),
+                                             _d(mom), _d(cen), C.byref(vol)))
+    return mom, cen, vol.value
+
+
+def body3d_terms(q, qt, moments10, w, scale: float, project: bool = True, hessian: bool = True,
+                 device: int = 0) -> dict:
+    """Inertia + orthogonality terms of 12-DoF bodies (dabd_gpu_body3d_terms)."""
+    q = _f64(q).reshape(-1, 12)
+    n = len(q)
+    qt = _f64(qt, (n, 12))
+    mo = _f64(moments10, (n, 10))
+    w = _f64(w).reshape(n)
+    v = np.zeros(max(n, 1))
+    g = np.zeros((max(n, 1), 12))
+    h = np.zeros((max(n, 1), 12, 12)) if hessian else None
+    L.check(L.load().dabd_gpu_body3d_terms(device, n, _d(q), _d(qt), _d(mo), _d(w), C.c_double(scale),
+                                           int(project), _d(v), _d(g), _d(h)))
+    out = dict(value=v[:n], grad=g[:n])
+    if hessian:
+        out["hess"] = h[:n]
+    return out

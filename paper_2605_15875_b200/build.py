@@ -22,7 +22,7 @@ INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(HERE, "build", "obj")
 LIB = os.path.join(HERE, "libdabd_gpu.so")
 
-SOURCES = ["scene.cpp", "balance.cpp", "geometry.cu", "solver.cu", "solver_scalar.cu", "pcg.cu", "admm.cu", "engine.cu",
+SOURCES = ["scene.cpp", "balance.cpp", "body3d.cpp", "geometry.cu", "solver.cu", "solver_scalar.cu", "pcg.cu", "admm.cu", "engine.cu",
            "audit.cu", "contact3d.cu", "capi.cpp"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -2,11 +2,13 @@
 // thread-local last error, no exceptions across the boundary, null -> INVALID.
 #include "dabd_gpu.h"
 
+#include "body3d.hpp"
 #include "contact3d.hpp"
 #include "engine.hpp"
 #include "instrument.hpp"
 #include "scene.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -487,6 +489,53 @@ dabd_gpu_status dabd_gpu_ccd3d(int device, int n, const int* kind, const double*
         dabd_gpu::launch_ccd3d(a, s);
         CUDA_CHECK(cudaGetLastError());
         CUDA_CHECK(cudaMemcpyAsync(toi, dt.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        CUDA_CHECK(cudaStreamDestroy(s));
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_body3d_moments(int n_verts, const double* verts, int n_tris, const int* tris,
+                                        double density, double* moments10, double* centroid,
+                                        double* volume) {
+    if (!verts || !tris || !moments10 || n_verts < 4 || n_tris < 4) return null_arg();
+    return guarded([&] {
+        const dabd_gpu::Moments3 m = dabd_gpu::polyhedron_moments(n_verts, verts, n_tris, tris, density);
+        std::copy(m.mom, m.mom + 10, moments10);
+        if (centroid) std::copy(m.centroid, m.centroid + 3, centroid);
+        if (volume) *volume = m.volume;
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_body3d_terms(int device, int n, const double* q, const double* qt,
+                                      const double* moments10, const double* w, double scale,
+                                      int project, double* value, double* grad, double* hess) {
+    if (n < 0) return null_arg();
+    if (n > 0 && (!q || !qt || !moments10 || !w || !value || !grad)) return null_arg();
+    return guarded([&] {
+        if (n == 0) return DABD_GPU_OK;
+        CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t s = nullptr;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        const size_t m12 = 12 * static_cast<size_t>(n);
+        dabd_gpu::DBuf<double> dq, dqt, dm, dw, dv, dg, dh;
+        dq.upload(q, m12, s);
+        dqt.upload(qt, m12, s);
+        dm.upload(moments10, 10 * static_cast<size_t>(n), s);
+        dw.upload(w, n, s);
+        dv.resize(n);
+        dg.resize(m12);
+        if (hess) dh.resize(144 * static_cast<size_t>(n));
+        dabd_gpu::Body3dArgs a{n, dq.get(), dqt.get(), dm.get(), dw.get(), scale, project,
+                               dv.get(), dg.get(), hess ? dh.get() : nullptr};
+        dabd_gpu::launch_body3d(a, s);
+        CUDA_CHECK(cudaGetLastError());
+        CUDA_CHECK(cudaMemcpyAsync(value, dv.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaMemcpyAsync(grad, dg.get(), m12 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (hess)
+            CUDA_CHECK(cudaMemcpyAsync(hess, dh.get(), 144 * static_cast<size_t>(n) * sizeof(double),
+                                       cudaMemcpyDeviceToHost, s));
         CUDA_CHECK(cudaStreamSynchronize(s));
         CUDA_CHECK(cudaStreamDestroy(s));
         return DABD_GPU_OK;

@@ -205,7 +205,110 @@ __global__ void k_ccd3d(Ccd3dArgs ar) {
     ar.toi[k] = accd_pair(kind, x, dx);
 }
 
+// 3D body terms (the 12-DoF counterpart of energy.cpp:7-48 / objective.cpp:
+// 117-167): inertia 1/2 (q - qt)^T M (q - qt) with M = per-row 4x4 blocks
+// [[m, s^T], [s, S]] over (p_r, A_r0, A_r1, A_r2) (s, S: first / second mass
+// moments about the rest centroid), plus scale * w ||A^T A - I||_F^2, and the
+// PSD clamp of the 12x12 Hessian. With centroid-centred rest shapes the
+// translation coupling s is rounding-level: then only the 9x9 A block is
+// clamped (padded to 10 for the round-robin Jacobi), else the full 12x12.
+__global__ void k_body3d(Body3dArgs ar) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= ar.n) return;
+    const double* q = ar.q + 12 * static_cast<size_t>(b);
+    const double* qt = ar.qt + 12 * static_cast<size_t>(b);
+    const double* mo = ar.moments + 10 * static_cast<size_t>(b);
+    const double m = mo[0], s[3] = {mo[1], mo[2], mo[3]};
+    const double S[3][3] = {{mo[4], mo[5], mo[6]}, {mo[5], mo[7], mo[8]}, {mo[6], mo[8], mo[9]}};
+    double H[12][12], g[12];
+    for (int i = 0; i < 12; ++i) {
+        g[i] = 0.0;
+        for (int j = 0; j < 12; ++j) H[i][j] = 0.0;
+    }
+    // mass matrix rows: translation r -> r, A_rc -> 3 + 3r + c
+    for (int r = 0; r < 3; ++r) {
+        H[r][r] = m;
+        for (int c = 0; c < 3; ++c) {
+            H[r][3 + 3 * r + c] = s[c];
+            H[3 + 3 * r + c][r] = s[c];
+            for (int c2 = 0; c2 < 3; ++c2) H[3 + 3 * r + c][3 + 3 * r + c2] = S[c][c2];
+        }
+    }
+    double diff[12], md[12];
+    for (int i = 0; i < 12; ++i) diff[i] = q[i] - qt[i];
+    double ein = 0.0;
+    for (int i = 0; i < 12; ++i) {
+        double t = 0.0;
+        for (int j = 0; j < 12; ++j) t += H[i][j] * diff[j];
+        md[i] = t;
+        ein += diff[i] * t;
+    }
+    ein *= 0.5;
+    // ||A^T A - I||^2: grad 4 A G, hess_{(ij),(kl)} = 4 (d_ik G_lj + A_il A_kj + d_jl (A A^T)_ik)
+    double A[3][3], G[3][3], AAt[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) A[i][j] = q[3 + 3 * i + j];
+    double psi = 0.0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double t = 0.0, u = 0.0;
+            for (int k = 0; k < 3; ++k) {
+                t += A[k][i] * A[k][j];
+                u += A[i][k] * A[j][k];
+            }
+            G[i][j] = t - (i == j ? 1.0 : 0.0);
+            AAt[i][j] = u;
+            psi += G[i][j] * G[i][j];
+        }
+    const double w = ar.scale * ar.w[b];
+    ar.value[b] = ein + w * psi;
+    double* gout = ar.grad + 12 * static_cast<size_t>(b);
+    for (int i = 0; i < 12; ++i) g[i] = md[i];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double t = 0.0;
+            for (int k = 0; k < 3; ++k) t += A[i][k] * G[k][j];
+            g[3 + 3 * i + j] += 4.0 * w * t;
+        }
+    for (int i = 0; i < 12; ++i) gout[i] = g[i];
+    if (!ar.hess) return;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            for (int k = 0; k < 3; ++k)
+                for (int l = 0; l < 3; ++l) {
+                    double v = A[i][l] * A[k][j];
+                    if (i == k) v += G[l][j];
+                    if (j == l) v += AAt[i][k];
+                    H[3 + 3 * i + j][3 + 3 * k + l] += 4.0 * w * v;
+                }
+    if (ar.project) {
+        const double tol = 1e-13 * m;
+        bool decoupled = m > 0.0;
+        for (int c = 0; c < 3; ++c) decoupled = decoupled && fabs(s[c]) <= tol;
+        if (decoupled) {
+            double B[10][10];
+            for (int i = 0; i < 10; ++i)
+                for (int j = 0; j < 10; ++j) B[i][j] = i < 9 && j < 9 ? H[3 + i][3 + j] : (i == j ? 1.0 : 0.0);
+            if (!is_pd<10>(B)) {
+                clamp_psd<10>(B);
+                for (int i = 0; i < 9; ++i)
+                    for (int j = 0; j < 9; ++j) H[3 + i][3 + j] = B[i][j];
+            }
+        } else if (!is_pd<12>(H)) {
+            clamp_psd<12>(H);
+        }
+    }
+    double* hout = ar.hess + 144 * static_cast<size_t>(b);
+    for (int i = 0; i < 12; ++i)
+        for (int j = 0; j < 12; ++j) hout[12 * i + j] = H[i][j];
+}
+
 } // namespace
+
+void launch_body3d(const Body3dArgs& a, cudaStream_t s) {
+    if (a.n <= 0) return;
+    DABD_LAUNCH("k_body3d", s, k_body3d<<<(a.n + 63) / 64, 64, 0, s>>>(a));
+}
 
 void launch_ccd3d(const Ccd3dArgs& a, cudaStream_t s) {
     if (a.n <= 0) return;

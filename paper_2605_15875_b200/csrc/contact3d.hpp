@@ -41,4 +41,23 @@ struct Ccd3dArgs {
 
 void launch_ccd3d(const Ccd3dArgs& a, cudaStream_t s);
 
+// Body terms of 12-DoF bodies: moments [n][10] = (m, s_x, s_y, s_z, S_xx,
+// S_xy, S_xz, S_yy, S_yz, S_zz), w [n] = kappa * volume * arap_scale, scale
+// (h^2 in the objective). Outputs value [n], grad [n][12], hess [n][12][12]
+// (nullable).
+struct Body3dArgs {
+    int n;
+    const double* q;
+    const double* qt;
+    const double* moments;
+    const double* w;
+    double scale;
+    int project;
+    double* value;
+    double* grad;
+    double* hess;
+};
+
+void launch_body3d(const Body3dArgs& a, cudaStream_t s);
+
 } // namespace dabd_gpu
