@@ -133,6 +133,9 @@ Engine::~Engine() {
     if (exec_) cudaGraphExecDestroy(exec_);
     if (newton_exec_) cudaGraphExecDestroy(newton_exec_);
     for (cudaStream_t s : cap_streams_) cudaStreamDestroy(s);
+    for (cudaStream_t s : side_streams_) cudaStreamDestroy(s);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
     if (own_stream_ && s_) cudaStreamDestroy(s_);
 }
 
@@ -508,8 +511,15 @@ void Engine::enq_derivatives(bool fused) {
     SolverView v = view();
     const ContactView cv = cview();
     if (fused) {
-        launch_body_terms(v, iq_.get(), true, 0, s_, &lstate_.get()->n_act, ctrl_.get());
+        // body terms and contact terms as two independent branches (kOpIterBegin's
+        // resets ran in the kOpReset / kOpNewtonTail that decided this iteration)
+        const cudaStream_t side = side_stream();
+        CUDA_CHECK(cudaEventRecord(ev_fork_, s_));
+        CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork_, 0));
+        launch_body_terms(v, iq_.get(), true, 0, side);
         launch_contact_select(v, cv, nullptr, s_, true);
+        CUDA_CHECK(cudaEventRecord(ev_join_, side));
+        CUDA_CHECK(cudaStreamWaitEvent(s_, ev_join_, 0));
         launch_assemble(v, cv, rowtmp_.get(), s_);
         return;
     }
@@ -586,8 +596,26 @@ void Engine::enq_ls_trial() {
     launch_accept_trial(v, s_);
 }
 
+int* Engine::iter_reset() { return pcg_fused() ? &lstate_.get()->n_act : nullptr; }
+
+// Second stream of the current capture level (or of eager execution) for
+// independent branches inside one Newton iteration.
+cudaStream_t Engine::side_stream() {
+    const int idx = cap_level_ + 1;
+    while (static_cast<int>(side_streams_.size()) <= idx) {
+        cudaStream_t s;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        side_streams_.push_back(s);
+    }
+    if (!ev_fork_) {
+        CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    }
+    return side_streams_[idx];
+}
+
 void Engine::enq_solve_begin(double tol) {
-    launch_scalar(ps_.get(), P_, kOpReset, ctrl_.get(), hd_, tol, 0, err_.get(), s_);
+    launch_scalar(ps_.get(), P_, kOpReset, ctrl_.get(), hd_, tol, 0, err_.get(), s_, iter_reset());
     enq_list_ensure(iq_.get());
     enq_energy(0, 0, &PartState::energy);
 }
@@ -616,7 +644,8 @@ NewtonResult Engine::newton_batch(int max_iters, double tol, bool reset_ctrl) {
                 c = read_ctrl();
             }
         }
-        launch_scalar(ps_.get(), P_, kOpNewtonTail, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
+        launch_scalar(ps_.get(), P_, kOpNewtonTail, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_,
+                      iter_reset());
         c = read_ctrl();
     }
     CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState),
@@ -788,7 +817,8 @@ void Engine::cap_newton(int max_iters, double tol, int level) {
             enq_newton_ccd();
             add_cond_node(hd_.ls, true, level + 2, [&] { enq_ls_trial(); });
         });
-        launch_scalar(ps_.get(), P_, kOpNewtonTail, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_);
+        launch_scalar(ps_.get(), P_, kOpNewtonTail, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_,
+                      iter_reset());
     });
 }
 

@@ -127,6 +127,8 @@ class Engine {
     void enq_pcg(bool fused = false);
     int max_part_rows() const;
     bool pcg_fused() const;
+    int* iter_reset(); // kOpIterBegin's resets ride on kOpReset / kOpNewtonTail (fused head)
+    cudaStream_t side_stream();
     void enq_newton_head(int max_iters);
     void enq_newton_ccd();
     void enq_ls_trial();
@@ -165,6 +167,8 @@ class Engine {
     int halvings_ = 0;
     long long frame_counter_ = 0;
     std::vector<TraceRow> trace_;
+    std::vector<cudaStream_t> side_streams_; // per capture level: independent branches
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     // PD load balancer of the planes (runtime.cpp:537-552, 674-675)
     std::vector<PlaneH> planes_cur_;
     Balancer balancer_;

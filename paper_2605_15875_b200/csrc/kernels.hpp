@@ -123,7 +123,7 @@ void launch_energy(const SolverView& sv, const unsigned long long* keys, int cap
 void launch_accept_trial(const SolverView& sv, cudaStream_t s);
 
 void launch_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHandles h, double tol,
-                   int max_iters, int* err, cudaStream_t s);
+                   int max_iters, int* err, cudaStream_t s, int* iter_reset = nullptr);
 
 // ADMM controller of the N=1 frame (sim.cpp:223-238): op 0 = step head
 // (stop test for k > 1), op 1 = step tail (k++, K bound). Writes trace rows.

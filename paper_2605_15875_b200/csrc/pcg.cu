@@ -16,6 +16,8 @@
 
 #include "instrument.hpp"
 
+#include <cstdlib>
+
 #include <cooperative_groups.h>
 
 namespace cg = cooperative_groups;
@@ -70,6 +72,10 @@ struct PcgArgs {
     FrameCtrl* ctrl;
     CondHandles hd;
     unsigned* ticket;        // last-cluster detection, reset by the last one
+    // warm start (cluster kernel): x0 = beta x_prev with x_prev the previous
+    // solve's solution left in sv.x and beta = (x_prev.b) / (x_prev.A x_prev)
+    // (the A-norm-optimal multiple; 0 when that is not finite or positive)
+    int warm;
 };
 
 // Block-local, partition-segmented sum of rowval over this block's chunk,
@@ -324,6 +330,7 @@ struct ClusterScalars {
     int2 req[16];                     // per consumer: (first local row, count) it needs from us
     int reqbase[16];                  // ... and where they land in its halo
     double dqm[16];                   // fused: every CTA's max |dq|, by rank (rank 0 only)
+    double wsp[3];                    // warm start: this CTA's (p.b, p.Ap, b.b)
 };
 
 
@@ -796,16 +803,77 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     for (int g = 0; g < G; ++g) {
         lrg[g] = warp * kRowsPerWarp + slot + g * row_step;
         on[g] = lane < 30 && lrg[g] < nr;
-        const double gr = on[g] && act ? -sv.rgrad[6 * (r0 + lrg[g]) + comp] : 0.0;
+        r[g] = on[g] && act ? -sv.rgrad[6 * (r0 + lrg[g]) + comp] : 0.0;
+        x[g] = z[g] = qv[g] = sv_[g] = pv[g] = 0.0;
+    }
+    double bnorm2_ws = -1.0; // ||b||^2 when the warm start computed it
+    if (a.warm) {
+        // x0 = beta p, p = the previous solve's solution: one SpMV through
+        // DSMEM and one cluster reduction of (p.b, p.Ap, b.b), rank order
+        double pg[G], apg[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            pg[g] = on[g] && act ? sv.x[6 * (r0 + lrg[g]) + comp] : 0.0;
+            if (on[g]) vm1[6 * lrg[g] + comp] = pg[g];
+        }
+        cluster_barrier();
+        double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            apg[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, spmv_local(lrg[g], vm1)) : 0.0;
+            l0 += pg[g] * r[g];
+            l1 += pg[g] * apg[g];
+            l2 += r[g] * r[g];
+        }
+        l0 = warp_sum(l0);
+        l1 = warp_sum(l1);
+        l2 = warp_sum(l2);
+        if (lane == 0) {
+            sc.red[warp][0] = l0;
+            sc.red[warp][1] = l1;
+            sc.red[warp][2] = l2;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+            for (int k = 0; k < kCW; ++k) {
+                t0 += sc.red[k][0];
+                t1 += sc.red[k][1];
+                t2 += sc.red[k][2];
+            }
+            sc.wsp[0] = t0;
+            sc.wsp[1] = t1;
+            sc.wsp[2] = t2;
+        }
+        cluster_barrier(); // wsp of every CTA ready; every peer done reading our vm1
+        double pb = 0.0, pap = 0.0, bb = 0.0;
+        for (int k = 0; k < csize; ++k) {
+            const double* o = cl.map_shared_rank(&sc, k)->wsp;
+            pb += o[0];
+            pap += o[1];
+            bb += o[2];
+        }
+        double beta = pb / pap;
+        if (!(pap > 0.0) || !isfinite(beta)) beta = 0.0;
+        bnorm2_ws = bb;
+        if (beta != 0.0) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                x[g] = beta * pg[g];
+                r[g] -= beta * apg[g];
+            }
+        }
+        cluster_barrier(); // peers finished reading wsp before sc is reused
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
         double uu = 0.0;
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-            const double gc = __shfl_sync(0xffffffffu, gr, (6 * slot + c) & 31);
-            if (on[g]) uu += dinv[36 * lrg[g] + 6 * comp + c] * gc;
+            const double rc = __shfl_sync(0xffffffffu, r[g], (6 * slot + c) & 31);
+            if (on[g]) uu += dinv[36 * lrg[g] + 6 * comp + c] * rc;
         }
-        r[g] = gr;
         u[g] = uu;
-        x[g] = z[g] = qv[g] = sv_[g] = pv[g] = 0.0;
         if (on[g]) vm1[6 * lrg[g] + comp] = uu;
     }
     cluster_barrier();
@@ -951,7 +1019,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 delta += __shfl_xor_sync(0xffffffffu, delta, off);
                 rr += __shfl_xor_sync(0xffffffffu, rr, off);
             }
-            if (it == 0) bnorm2 = rr;
+            if (it == 0) bnorm2 = bnorm2_ws >= 0.0 ? bnorm2_ws : rr;
             stop = bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters;
             // beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
             // with the previous iteration's reciprocals: one division on the
@@ -1148,7 +1216,12 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
     // register-resident row groups per warp (kCW warps x kRowsPerWarp rows each)
     const int groups = (cmax_rows + kCW * kRowsPerWarp - 1) / (kCW * kRowsPerWarp);
     if (groups > 4) throw Error("pcg: cluster chunk exceeds 4 row groups per warp");
-    PcgArgs a{pbuf, nullptr, nullptr, tol, max_iters, 0, nullptr, nullptr, CondHandles{}, nullptr};
+    PcgArgs a{pbuf, nullptr, nullptr, tol, max_iters, 0, nullptr, nullptr, CondHandles{}, nullptr, 0};
+    static const int warm = [] {
+        const char* e = std::getenv("DABD_GPU_PCG_WARM");
+        return e ? std::atoi(e) : 1;
+    }();
+    a.warm = warm;
     if (fuse) {
         a.fused = 1;
         a.row_trace = fuse->row_trace;

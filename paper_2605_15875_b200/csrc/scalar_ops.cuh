@@ -14,8 +14,14 @@ __device__ __forceinline__ void set_cond(unsigned long long h, bool v, int graph
 // One step of the per-partition scalar control, executed by ALL threads of
 // one block (blockDim.x >= P). Shared by k_scalar and the fused kernels that
 // finish with a control step (k_energy's line-search accept).
+// iter_reset (fused Newton body, kOpReset / kOpNewtonTail only): when the
+// Newton loop is about to run another iteration, also take kOpIterBegin's
+// resets here (per-partition counters, the active-contact counter
+// *iter_reset, exec_newton), so the iteration's body and contact terms can
+// run side by side as independent graph branches.
 __device__ __forceinline__ void scalar_block(PartState* ps, int P, int op, FrameCtrl* ctrl,
-                                             CondHandles hd, double tol, int max_iters, int* err) {
+                                             CondHandles hd, double tol, int max_iters, int* err,
+                                             int* iter_reset = nullptr) {
     const int p = threadIdx.x;
     bool act = false, srch = false;
     if (p < P) {
@@ -104,6 +110,19 @@ __device__ __forceinline__ void scalar_block(PartState* ps, int P, int op, Frame
     }
     const bool any_act = __syncthreads_or(act);
     const bool any_srch = __syncthreads_or(srch);
+    if (iter_reset && any_act && (op == kOpReset || op == kOpNewtonTail)) {
+        if (p < P) {
+            PartState& s = ps[p];
+            s.dq_inf = 0.0;
+            s.toi_earliest = 2.0;
+            s.n_candidates = 0;
+            s.n_active_contacts = 0;
+        }
+        if (threadIdx.x == 0) {
+            *iter_reset = 0;
+            if (ctrl) ++ctrl->exec_newton;
+        }
+    }
     if (threadIdx.x == 0) {
         if (ctrl) {
             ctrl->any_active = any_act;

@@ -12,8 +12,8 @@ namespace dabd_gpu {
 namespace {
 
 __global__ void k_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHandles hd,
-                         double tol, int max_iters, int* err) {
-    scalar_block(ps, P, op, ctrl, hd, tol, max_iters, err);
+                         double tol, int max_iters, int* err, int* iter_reset) {
+    scalar_block(ps, P, op, ctrl, hd, tol, max_iters, err, iter_reset);
 }
 
 // N=1 ADMM frame controller (sim.cpp:221-239).
@@ -79,9 +79,9 @@ void set_scalar_carveout(int pct) {
 }
 
 void launch_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHandles h, double tol,
-                   int max_iters, int* err, cudaStream_t s) {
+                   int max_iters, int* err, cudaStream_t s, int* iter_reset) {
     DABD_LAUNCH("k_scalar", s,
-                k_scalar<<<1, 32, 0, s>>>(ps, P, op, ctrl, h, tol, max_iters, err));
+                k_scalar<<<1, 32, 0, s>>>(ps, P, op, ctrl, h, tol, max_iters, err, iter_reset));
 }
 
 void launch_frame_ctrl(FrameCtrl* ctrl, int op, const double* dq_part, int P, double h, double l,
