@@ -72,9 +72,9 @@ struct PcgArgs {
     FrameCtrl* ctrl;
     CondHandles hd;
     unsigned* ticket;        // last-cluster detection, reset by the last one
-    // warm start (cluster kernel): x0 = beta x_prev with x_prev the previous
-    // solve's solution left in sv.x and beta = (x_prev.b) / (x_prev.A x_prev)
-    // (the A-norm-optimal multiple; 0 when that is not finite or positive)
+    // warm start (cluster kernel): 1 = x0 the A-norm-optimal multiple of the
+    // previous solve's solution (sv.x); 2 = x0 the Galerkin solution over the
+    // previous two solutions (sv.x and pa, which the kernel rotates); 0 = off
     int warm;
 };
 
@@ -330,7 +330,8 @@ struct ClusterScalars {
     int2 req[16];                     // per consumer: (first local row, count) it needs from us
     int reqbase[16];                  // ... and where they land in its halo
     double dqm[16];                   // fused: every CTA's max |dq|, by rank (rank 0 only)
-    double wsp[3];                    // warm start: this CTA's (p.b, p.Ap, b.b)
+    double wsp[6];                    // warm start: this CTA's (p1.b, p2.b, p1.Ap1, p1.Ap2, p2.Ap2, b.b)
+    double wred[kCW][6];
 };
 
 
@@ -808,59 +809,68 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     }
     double bnorm2_ws = -1.0; // ||b||^2 when the warm start computed it
     if (a.warm) {
-        // x0 = beta p, p = the previous solve's solution: one SpMV through
-        // DSMEM and one cluster reduction of (p.b, p.Ap, b.b), rank order
-        double pg[G], apg[G];
+        // x0 in span{p1, p2}, the previous two solves' solutions (sv.x and
+        // a.pa), by the Galerkin condition: [p_i . A p_j] c = [p_i . b] (2x2,
+        // one-vector fallback when nearly dependent). Two SpMVs through DSMEM
+        // (p1 from vm1, p2 from vm0) and one cluster reduction, rank order.
+        double p1[G], p2[G], ap1[G], ap2[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            pg[g] = on[g] && act ? sv.x[6 * (r0 + lrg[g]) + comp] : 0.0;
-            if (on[g]) vm1[6 * lrg[g] + comp] = pg[g];
+            const size_t e = 6 * static_cast<size_t>(r0 + lrg[g]) + comp;
+            p1[g] = on[g] && act ? sv.x[e] : 0.0;
+            p2[g] = on[g] && act && a.warm > 1 ? a.pa[e] : 0.0;
+            if (on[g]) {
+                vm1[6 * lrg[g] + comp] = p1[g];
+                vm0[6 * lrg[g] + comp] = p2[g];
+                if (a.warm > 1) a.pa[e] = p1[g]; // becomes the next solve's p2
+            }
         }
         cluster_barrier();
-        double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+        double l[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            apg[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, spmv_local(lrg[g], vm1)) : 0.0;
-            l0 += pg[g] * r[g];
-            l1 += pg[g] * apg[g];
-            l2 += r[g] * r[g];
+            ap1[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, spmv_local(lrg[g], vm1)) : 0.0;
+            ap2[g] = on[g] && a.warm > 1 ? spmv_remote(lrg[g], nullptr, 0, spmv_local(lrg[g], vm0)) : 0.0;
+            l[0] += p1[g] * r[g];
+            l[1] += p2[g] * r[g];
+            l[2] += p1[g] * ap1[g];
+            l[3] += p1[g] * ap2[g];
+            l[4] += p2[g] * ap2[g];
+            l[5] += r[g] * r[g];
         }
-        l0 = warp_sum(l0);
-        l1 = warp_sum(l1);
-        l2 = warp_sum(l2);
-        if (lane == 0) {
-            sc.red[warp][0] = l0;
-            sc.red[warp][1] = l1;
-            sc.red[warp][2] = l2;
-        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) l[k] = warp_sum(l[k]);
+        if (lane == 0)
+            for (int k = 0; k < 6; ++k) sc.wred[warp][k] = l[k];
         __syncthreads();
-        if (threadIdx.x == 0) {
-            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-            for (int k = 0; k < kCW; ++k) {
-                t0 += sc.red[k][0];
-                t1 += sc.red[k][1];
-                t2 += sc.red[k][2];
-            }
-            sc.wsp[0] = t0;
-            sc.wsp[1] = t1;
-            sc.wsp[2] = t2;
+        if (threadIdx.x < 6) {
+            double t = 0.0;
+            for (int k = 0; k < kCW; ++k) t += sc.wred[k][threadIdx.x];
+            sc.wsp[threadIdx.x] = t;
         }
-        cluster_barrier(); // wsp of every CTA ready; every peer done reading our vm1
-        double pb = 0.0, pap = 0.0, bb = 0.0;
+        cluster_barrier(); // wsp of every CTA ready; every peer done reading vm0 / vm1
+        double tt[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         for (int k = 0; k < csize; ++k) {
             const double* o = cl.map_shared_rank(&sc, k)->wsp;
-            pb += o[0];
-            pap += o[1];
-            bb += o[2];
+#pragma unroll
+            for (int m = 0; m < 6; ++m) tt[m] += o[m];
         }
-        double beta = pb / pap;
-        if (!(pap > 0.0) || !isfinite(beta)) beta = 0.0;
-        bnorm2_ws = bb;
-        if (beta != 0.0) {
+        const double b1 = tt[0], b2 = tt[1], a11 = tt[2], a12 = tt[3], a22 = tt[4];
+        double c1 = 0.0, c2 = 0.0;
+        const double det = a11 * a22 - a12 * a12;
+        if (a.warm > 1 && a11 > 0.0 && a22 > 0.0 && det > 1e-8 * a11 * a22) {
+            c1 = (b1 * a22 - b2 * a12) / det;
+            c2 = (b2 * a11 - b1 * a12) / det;
+        } else if (a11 > 0.0) {
+            c1 = b1 / a11;
+        }
+        if (!isfinite(c1) || !isfinite(c2)) c1 = c2 = 0.0;
+        bnorm2_ws = tt[5];
+        if (c1 != 0.0 || c2 != 0.0) {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                x[g] = beta * pg[g];
-                r[g] -= beta * apg[g];
+                x[g] = c1 * p1[g] + c2 * p2[g];
+                r[g] -= c1 * ap1[g] + c2 * ap2[g];
             }
         }
         cluster_barrier(); // peers finished reading wsp before sc is reused
@@ -1219,7 +1229,7 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
     PcgArgs a{pbuf, nullptr, nullptr, tol, max_iters, 0, nullptr, nullptr, CondHandles{}, nullptr, 0};
     static const int warm = [] {
         const char* e = std::getenv("DABD_GPU_PCG_WARM");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 2;
     }();
     a.warm = warm;
     if (fuse) {
