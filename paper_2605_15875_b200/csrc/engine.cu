@@ -101,7 +101,7 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     err_.resize(1);
     err_.zero(s_);
     pin_i_.resize(16);
-    pin_d_.resize(64);
+    pin_d_.resize(256); // [0,32) gate, [32,64) r, [64,96) s, [96,128) dq, [128,160) 2.0 fill
     cellmax_.resize(1);
     nsel_.resize(1);
     ctrl_.resize(1);
@@ -673,7 +673,7 @@ NewtonResult Engine::newton_batch(int max_iters, double tol, bool reset_ctrl) {
 // once per solver epoch (instance set / capacities / h of the current
 // attempt) and replayed for every ADMM iteration: one host synchronisation
 // per local solve instead of several per Newton iteration.
-NewtonResult Engine::newton_graph(int max_iters, double tol) {
+NewtonResult Engine::newton_graph(int max_iters, double tol, const std::function<void()>& tail) {
     if (!newton_exec_ || newton_epoch_ != solver_epoch_ || newton_tol_ != tol || newton_max_ != max_iters) {
         KernelTimer::get().suspend(true);
         hd_ = CondHandles{};
@@ -718,6 +718,7 @@ NewtonResult Engine::newton_graph(int max_iters, double tol) {
     }
     CUDA_CHECK(cudaMemsetAsync(ctrl_.get(), 0, sizeof(FrameCtrl), s_));
     CUDA_CHECK(cudaGraphLaunch(newton_exec_, s_));
+    if (tail) tail();
     CUDA_CHECK(cudaMemcpyAsync(ps_h_.get(), ps_.get(), P_ * sizeof(PartState), cudaMemcpyDeviceToHost, s_));
     CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState), cudaMemcpyDeviceToHost, s_));
     const FrameCtrl c = read_ctrl(); // synchronises, raises a device error
@@ -1474,18 +1475,52 @@ FrameStats Engine::frame_admm(int frame) {
                     launch_consensus(ns, shared_inst_.get(), ipart_.get(), p0_, iq_.get(),
                                      iu_.get(), irho_.get(), iz_.get(), hrecv_.get(), iznext_.get(),
                                      rb_.get(), sb_.get(), rloc_.get(), sloc_.get(), err_.get(), s_);
-                    // merge CCD gate per partition (consensus.cpp:66-75)
+                    // merge CCD gate per partition (consensus.cpp:66-75): a
+                    // fixed-capacity broad phase and the CCD over its device
+                    // count, then ONE readback of (earliest TOI, r, s, error)
                     launch_merged(I, ianc_.get(), iq_.get(), iznext_.get(), iqtry_.get(), s_);
-                    const int nc = det_gate_.build(ds_.view(), iview(iq_.get(), iqtry_.get()),
-                                                   stat_.get(), static_cast<int>(h_stat_.size()),
-                                                   true, 0.0, ds_.max_verts, s_);
-                    gate_.upload(earliest, s_);
-                    launch_ccd(view(), det_gate_.keys(), nc, nullptr, det_gate_.fmt(),
-                               det_gate_.boxes(), iq_.get(), iqtry_.get(), 2, gate_.get(), s_);
-                    earliest = gate_.to_host(s_);
-                    rl = rloc_.to_host(s_);
-                    sl = sloc_.to_host(s_);
-                    check_err("admm: consensus/gate");
+                    gate_cap_ = std::max(gate_cap_, 64 * std::max(I, 1));
+                    det_gate_.ensure(I, ds_.max_verts, gate_cap_);
+                    det_gate_.enqueue(ds_.view(), iview(iq_.get(), iqtry_.get()), stat_.get(),
+                                      static_cast<int>(h_stat_.size()), true, 0.0, err_.get(), s_);
+                    for (int p = 0; p < P_; ++p) pin_d_[128 + p] = 2.0;
+                    CUDA_CHECK(cudaMemcpyAsync(gate_.get(), pin_d_.get() + 128, P_ * sizeof(double),
+                                               cudaMemcpyHostToDevice, s_));
+                    launch_ccd(view(), det_gate_.keys(), det_gate_.cap(), det_gate_.d_count(),
+                               det_gate_.fmt(), det_gate_.boxes(), iq_.get(), iqtry_.get(), 2,
+                               gate_.get(), s_);
+                    CUDA_CHECK(cudaMemcpyAsync(pin_d_.get(), gate_.get(), P_ * sizeof(double),
+                                               cudaMemcpyDeviceToHost, s_));
+                    CUDA_CHECK(cudaMemcpyAsync(pin_d_.get() + 32, rloc_.get(), P_ * sizeof(double),
+                                               cudaMemcpyDeviceToHost, s_));
+                    CUDA_CHECK(cudaMemcpyAsync(pin_d_.get() + 64, sloc_.get(), P_ * sizeof(double),
+                                               cudaMemcpyDeviceToHost, s_));
+                    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 8, err_.get(), sizeof(int),
+                                               cudaMemcpyDeviceToHost, s_));
+                    sync();
+                    if (pin_i_[8] == kErrCapacity) { // grow and redo this gate with the counted build
+                        err_.zero(s_);
+                        const int nc = det_gate_.build(ds_.view(), iview(iq_.get(), iqtry_.get()),
+                                                       stat_.get(), static_cast<int>(h_stat_.size()),
+                                                       true, 0.0, ds_.max_verts, s_);
+                        gate_cap_ = det_gate_.cap();
+                        gate_.upload(earliest, s_);
+                        launch_ccd(view(), det_gate_.keys(), nc, nullptr, det_gate_.fmt(),
+                                   det_gate_.boxes(), iq_.get(), iqtry_.get(), 2, gate_.get(), s_);
+                        earliest = gate_.to_host(s_);
+                        check_err("admm: consensus/gate");
+                    } else if (pin_i_[8] != 0) {
+                        const int code = pin_i_[8];
+                        err_.zero(s_);
+                        sync();
+                        throw Error(std::string(err_text(code)) + " [admm: consensus/gate]");
+                    } else {
+                        for (int p = 0; p < P_; ++p) earliest[p] = pin_d_[p];
+                    }
+                    for (int p = 0; p < P_; ++p) {
+                        rl[p] = pin_d_[32 + p];
+                        sl[p] = pin_d_[64 + p];
+                    }
                     prof.mark(1, s_);
                 } catch (const Error& e) {
                     if (!distributed_) throw;
@@ -1549,7 +1584,16 @@ FrameStats Engine::frame_admm(int frame) {
             try {
                 if (I) CUDA_CHECK(cudaMemcpyAsync(iqbefore_.get(), iq_.get(), 6 * I * sizeof(double),
                                                   cudaMemcpyDeviceToDevice, s_));
-                const NewtonResult r = use_graph_ ? newton_graph(hs_.newton_cap, tol)
+                // ||q - q_before||_inf per partition rides on the Newton readback
+                auto dq_tail = [&] {
+                    gate_.zero(s_);
+                    launch_delta_inf(n_rows_, rinst_.get(), rpart_.get(), p0_, iq_.get(), iqbefore_.get(),
+                                     gate_.get(), s_);
+                    CUDA_CHECK(cudaMemcpyAsync(pin_d_.get() + 96, gate_.get(), P_ * sizeof(double),
+                                               cudaMemcpyDeviceToHost, s_));
+                };
+                const bool fused_dq = use_graph_ && n_rows_ > 0;
+                const NewtonResult r = use_graph_ ? newton_graph(hs_.newton_cap, tol, fused_dq ? dq_tail : std::function<void()>{})
                                                   : newton_batch(hs_.newton_cap, tol);
                 st.newton_iterations += r.iterations;
                 st.line_search_steps += r.ls_steps;
@@ -1558,7 +1602,11 @@ FrameStats Engine::frame_admm(int frame) {
                 st.max_contacts = std::max(st.max_contacts, n_contacts_);
                 st.max_candidates = std::max(st.max_candidates, n_super_);
                 prof.mark(3, s_);
-                dq = n_rows_ ? delta_inf(iq_.get(), iqbefore_.get()) : std::vector<double>(P_, 0.0);
+                if (fused_dq) {
+                    for (int p = 0; p < P_; ++p) dq[p] = pin_d_[96 + p];
+                } else {
+                    dq = n_rows_ ? delta_inf(iq_.get(), iqbefore_.get()) : std::vector<double>(P_, 0.0);
+                }
                 prof.mark(4, s_);
             } catch (const Error& e) {
                 if (!distributed_) throw;

@@ -135,7 +135,8 @@ class Engine {
     void enq_solve_begin(double tol);
     FrameCtrl read_ctrl();
     NewtonResult newton_batch(int max_iters, double tol, bool reset_ctrl = true);
-    NewtonResult newton_graph(int max_iters, double tol);
+    // tail: enqueued after the graph launch, before the one readback sync
+    NewtonResult newton_graph(int max_iters, double tol, const std::function<void()>& tail = {});
     std::vector<double> delta_inf(const double* a, const double* b);
 
     // CUDA graphs with conditional nodes -------------------------------------
@@ -197,6 +198,7 @@ class Engine {
     // detection
     Detector det_;       // superset for the local solve
     Detector det_gate_;  // merge gate / parity
+    int gate_cap_ = 0;   // fixed merge-gate candidate capacity (grown on kErrCapacity)
     int n_super_ = 0;
     DBuf<Box> box_;
     DBuf<double> cellmax_;

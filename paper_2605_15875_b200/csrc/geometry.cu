@@ -369,6 +369,12 @@ void Detector::enqueue(const SceneView& sc, const InstView& iv, const int* stat,
                                               0, fmt_.total_bits(), s));
 }
 
+void Detector::ensure(int n_inst, int max_verts, int cap) {
+    if (cap != cap_ || tsize_ < 2u * static_cast<unsigned>(std::max(n_inst, 1)) ||
+        fmt_.ibits != bits_for(std::max(n_inst, 2)) || fmt_.vbits != bits_for(std::max(max_verts, 2)))
+        prepare(n_inst, max_verts, cap);
+}
+
 int Detector::build(const SceneView& sc, const InstView& iv, const int* stat, int n_stat,
                     bool swept, double margin, int max_verts, cudaStream_t s) {
     int cap = std::max(cap_, 64 * std::max(iv.n, 1));

@@ -134,6 +134,9 @@ class Detector {
     // Graph-safe variant: fixed capacity, no host reads. Keys past the count
     // are ~0ull (sorted to the end); overflow raises kErrCapacity in `err`.
     void prepare(int n_inst, int max_verts, int cap);
+    // prepare() only when the capacity, table size or key format must change
+    // (what build() checks before each attempt).
+    void ensure(int n_inst, int max_verts, int cap);
     // `dmargin` (device, optional) overrides `margin` at run time, so a
     // captured graph can rebuild with a margin computed on the device.
     void enqueue(const SceneView& sc, const InstView& iv, const int* stat, int n_stat, bool swept,
