@@ -115,14 +115,25 @@ def test_torchcomm_halo_gloo(world):
 TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000)
 
 
-def _gpu_worker(rank, world, port, q, name, workers, frames):
+BALANCE = {"enabled": True, "kp": 0.3, "kd": 0.05, "smoothing": 0.5, "dp_max": 0.0}
+
+
+def _scene(name, balanced):
+    from paper_2605_15875_b200.scene import make_scenario
+
+    sd = make_scenario(name)
+    if balanced:
+        sd.balance = dict(BALANCE)
+    return sd
+
+
+def _gpu_worker(rank, world, port, q, name, workers, frames, balanced=False):
     try:
         _init(rank, world, port)
         from paper_2605_15875_b200.dist import run_partitioned
-        from paper_2605_15875_b200.scene import make_scenario
 
         torch.cuda.set_device(0)
-        t = run_partitioned(make_scenario(name), workers, frames, device=0, **TIGHT)
+        t = run_partitioned(_scene(name, balanced), workers, frames, device=0, **TIGHT)
         q.put((rank, (t.q, t.q_dot, t.trace, t.rho,
                       [s["admm_iterations"] for s in t.stats], list(t.h))))
         dist.destroy_process_group()
@@ -159,3 +170,25 @@ def test_partitioned_matches_single_gpu(name, workers, world, frames):
         rho[have] = rrho[have]
     # every body shared at the end is carried by some rank
     assert np.array_equal(np.isnan(rho), np.isnan(ref.rho)), offs
+
+
+@pytest.mark.gpu
+def test_balanced_partitioned_matches_single_gpu():
+    """PD plane balancing across ranks: every rank all-gathers the partition
+    costs and shifts the planes identically, so 2 ranks x 2 partitions
+    reproduce the single-process balanced run bit for bit; the planes move."""
+    from paper_2605_15875_b200 import api
+
+    name, workers, world, frames = "cubes-64", 2, 2, 12
+    sc = api.Scene(_scene(name, True))
+    ctx = api.Context(sc, num_workers=workers, **TIGHT)
+    p0 = ctx.planes().copy()
+    qs = []
+    for _ in range(frames):
+        ctx.run_frames(1)
+        qs.append(ctx.state()[0])
+    assert not np.array_equal(ctx.planes(), p0)
+    out = _spawn(_gpu_worker, world, name, workers, frames, True)
+    for r in range(world):
+        assert not isinstance(out[r], BaseException), out[r]
+        assert np.array_equal(out[r][0], np.array(qs)), (r, np.abs(out[r][0] - np.array(qs)).max())
