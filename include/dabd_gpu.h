@@ -22,6 +22,7 @@
  *   dabd_gpu_newton_solve        newton_solve                    include/dabd/newton.hpp:25-26
  *   dabd_gpu_contact3d_terms     3D extension of contact_energy  src/energy.cpp:63-94 (PT / EE, no reference)
  *   dabd_gpu_ccd3d               3D extension of ccd_toi          src/geometry.cpp:232-341 (no reference)
+ *   dabd_gpu_broad_phase3d       3D extension of broad_phase      src/geometry.cpp:106-208 (no reference)
  *   dabd_gpu_balancer_*          Balancer, imbalance_metric, pd_update, balance_factor
  *                                                                include/dabd/balance.hpp:9-56
  *   dabd_gpu_run_frames          run_reference (workers==0)      src/sim.cpp:186-249
@@ -306,6 +307,22 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_body3d_terms(int device, int n, const doub
                                                    const double* qt, const double* moments10,
                                                    const double* w, double scale, int project,
                                                    double* value, double* grad, double* hess);
+
+/* 3D broad phase (geometry.cpp:106-208 in 3D): candidate pairs between n
+ * bodies at q [n][12] (q_end [n][12] nullable: swept), each body a closed
+ * triangle mesh in rest coordinates (vert_start [n+1] into verts [nv][3],
+ * tri_start [n+1] into tris [nt][3], edge_start [n+1] into edges [ne][2],
+ * local vertex indices). Body boxes inflated by margin, sweep on lo.x (ties by
+ * id), 3D overlap; per overlapping pair, both orders, point box vs inflated
+ * triangle box -> (0, a, b, vertex, triangle); once per pair (a < b), edge box
+ * vs inflated edge box -> (1, a, b, edge, edge). pairs [capacity][5] sorted
+ * lexicographically; INVALID with the needed count when capacity is short. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_broad_phase3d(int device, int n_bodies, const double* q,
+                                                    const double* q_end, const int* vert_start,
+                                                    const double* verts, const int* tri_start,
+                                                    const int* tris, const int* edge_start,
+                                                    const int* edges, double margin, int* pairs,
+                                                    int capacity, int* count);
 
 /* ---- PD load balancer (host control logic, no device) ----------------------
  * balance.cpp:8-83: imbalance T = (eta-1)/(eta+1), eta = tau_i/tau_j (times

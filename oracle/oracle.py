@@ -353,3 +353,57 @@ def body3d_value(q, qt, mom, w, scale):
     A = q[3:].reshape(3, 3)
     G = A.T @ A - np.eye(3)
     return 0.5 * dq @ M @ dq + scale * w * float(np.sum(G * G))
+
+
+def broad_phase3d(q, meshes, margin, q_end=None):
+    """Brute-force 3D broad phase with the library's box rules (test-only):
+    every body pair whose inflated boxes overlap; PT both orders (point box
+    vs inflated triangle box), EE once with a < b (edge box vs inflated edge
+    box of b). World points round like x = ((A0 xb + A1 yb) + A2 zb) + p."""
+    q = np.asarray(q, float).reshape(-1, 12)
+    qe = None if q_end is None else np.asarray(q_end, float).reshape(-1, 12)
+
+    def world(qq, xb):
+        A = qq[3:].reshape(3, 3)
+        X = np.empty_like(xb)
+        for r in range(3):
+            X[:, r] = ((A[r, 0] * xb[:, 0] + A[r, 1] * xb[:, 1]) + A[r, 2] * xb[:, 2]) + qq[r]
+        return X
+
+    def box(b, idx):
+        xb = np.asarray(meshes[b][0], float).reshape(-1, 3)[list(idx)]
+        pts = [world(q[b], xb)] + ([world(qe[b], xb)] if qe is not None else [])
+        P = np.vstack(pts)
+        return P.min(axis=0), P.max(axis=0)
+
+    def ov(a, b):
+        return bool(np.all(a[0] <= b[1]) and np.all(b[0] <= a[1]))
+
+    def infl(bx):
+        return (bx[0] - margin, bx[1] + margin)
+
+    n = len(meshes)
+    bb = [infl(box(b, range(len(meshes[b][0])))) for b in range(n)]
+    out = []
+    for a in range(n):
+        for b in range(a + 1, n):
+            if not ov(bb[a], bb[b]):
+                continue
+            for pa, tb in ((a, b), (b, a)):
+                tris = np.asarray(meshes[tb][1]).reshape(-1, 3)
+                tboxes = [infl(box(tb, t)) for t in tris]
+                for v in range(len(meshes[pa][0])):
+                    pbx = box(pa, [v])
+                    for ti, tbx in enumerate(tboxes):
+                        if ov(pbx, tbx):
+                            out.append((0, pa, tb, v, ti))
+            ea = np.asarray(meshes[a][2]).reshape(-1, 2)
+            eb = np.asarray(meshes[b][2]).reshape(-1, 2)
+            ebx = [infl(box(b, e)) for e in eb]
+            for i, e in enumerate(ea):
+                abx = box(a, e)
+                for j, bx in enumerate(ebx):
+                    if ov(abx, bx):
+                        out.append((1, a, b, i, j))
+    out.sort()
+    return np.array(out, dtype=np.int32).reshape(-1, 5)

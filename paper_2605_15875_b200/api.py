@@ -485,3 +485,36 @@ def body3d_terms(q, qt, moments10, w, scale: float, project: bool = True, hessia
     if hessian:
         out["hess"] = h[:n]
     return out
+
+
+def broad_phase3d(q, meshes, margin: float, q_end=None, device: int = 0) -> np.ndarray:
+    """3D broad phase (dabd_gpu_broad_phase3d). meshes: per body (verts [k][3]
+    rest coordinates, tris [t][3], edges [e][2]); returns [m][5] rows (kind,
+    a, b, primitive a, primitive b), sorted."""
+    n = len(meshes)
+    q = _f64(q, (n, 12))
+    qe = None if q_end is None else _f64(q_end, (n, 12))
+    vs, ts, es = [0], [0], [0]
+    V, T, E = [], [], []
+    for v, t, e in meshes:
+        V.append(np.asarray(v, float).reshape(-1, 3))
+        T.append(np.asarray(t, np.int32).reshape(-1, 3))
+        E.append(np.asarray(e, np.int32).reshape(-1, 2))
+        vs.append(vs[-1] + len(V[-1]))
+        ts.append(ts[-1] + len(T[-1]))
+        es.append(es[-1] + len(E[-1]))
+    V = _f64(np.concatenate(V) if V else np.zeros((0, 3)))
+    T = _i32(np.concatenate(T) if T else np.zeros((0, 3)))
+    E = _i32(np.concatenate(E) if E else np.zeros((0, 2)))
+    vs, ts, es = _i32(vs), _i32(ts), _i32(es)
+    cap = 4096
+    while True:
+        out = np.zeros((cap, 5), dtype=np.int32)
+        cnt = C.c_int()
+        st = L.load().dabd_gpu_broad_phase3d(device, n, _d(q), _d(qe), _i(vs), _d(V), _i(ts), _i(T), _i(es),
+                                             _i(E), C.c_double(margin), _i(out), cap, C.byref(cnt))
+        if st == 3 and cnt.value > cap:
+            cap = cnt.value
+            continue
+        L.check(st)
+        return out[: cnt.value].copy()

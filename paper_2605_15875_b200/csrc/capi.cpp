@@ -3,6 +3,7 @@
 #include "dabd_gpu.h"
 
 #include "body3d.hpp"
+#include "broad3d.hpp"
 #include "contact3d.hpp"
 #include "engine.hpp"
 #include "instrument.hpp"
@@ -538,6 +539,67 @@ dabd_gpu_status dabd_gpu_body3d_terms(int device, int n, const double* q, const 
                                        cudaMemcpyDeviceToHost, s));
         CUDA_CHECK(cudaStreamSynchronize(s));
         CUDA_CHECK(cudaStreamDestroy(s));
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_broad_phase3d(int device, int n, const double* q, const double* q_end,
+                                       const int* vert_start, const double* verts, const int* tri_start,
+                                       const int* tris, const int* edge_start, const int* edges,
+                                       double margin, int* pairs, int capacity, int* count) {
+    if (n < 0 || !count || (n > 0 && (!q || !vert_start || !verts || !tri_start || !tris || !edge_start || !edges)) ||
+        (capacity > 0 && !pairs))
+        return null_arg();
+    return guarded([&] {
+        *count = 0;
+        if (n < 2) return DABD_GPU_OK;
+        const int nv = vert_start[n], nt = tri_start[n], ne = edge_start[n];
+        int maxp = 1;
+        for (int b = 0; b < n; ++b) {
+            if (vert_start[b + 1] < vert_start[b] || tri_start[b + 1] < tri_start[b] || edge_start[b + 1] < edge_start[b])
+                throw dabd_gpu::InvalidArg("broad_phase3d: offsets must be non-decreasing");
+            const int nvb = vert_start[b + 1] - vert_start[b];
+            for (int t = 3 * tri_start[b]; t < 3 * tri_start[b + 1]; ++t)
+                if (tris[t] < 0 || tris[t] >= nvb) throw dabd_gpu::InvalidArg("broad_phase3d: triangle vertex out of range");
+            for (int e = 2 * edge_start[b]; e < 2 * edge_start[b + 1]; ++e)
+                if (edges[e] < 0 || edges[e] >= nvb) throw dabd_gpu::InvalidArg("broad_phase3d: edge vertex out of range");
+            maxp = std::max({maxp, nvb, tri_start[b + 1] - tri_start[b], edge_start[b + 1] - edge_start[b]});
+        }
+        auto bits = [](int x) {
+            int b = 1;
+            while ((1ll << b) < x) ++b;
+            return b;
+        };
+        dabd_gpu::Key3Fmt f;
+        f.bb = bits(n);
+        f.pb = bits(maxp);
+        if (f.total_bits() > 64) throw dabd_gpu::InvalidArg("broad_phase3d: body / primitive counts exceed the key width");
+        CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t s = nullptr;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        dabd_gpu::DBuf<double> dq, dqe, dv;
+        dabd_gpu::DBuf<int> dvs, dts, dt, des, de;
+        dq.upload(q, 12 * static_cast<size_t>(n), s);
+        if (q_end) dqe.upload(q_end, 12 * static_cast<size_t>(n), s);
+        dvs.upload(vert_start, n + 1, s);
+        dv.upload(verts, 3 * static_cast<size_t>(std::max(nv, 1)), s);
+        dts.upload(tri_start, n + 1, s);
+        dt.upload(tris, 3 * static_cast<size_t>(std::max(nt, 1)), s);
+        des.upload(edge_start, n + 1, s);
+        de.upload(edges, 2 * static_cast<size_t>(std::max(ne, 1)), s);
+        dabd_gpu::Broad3dView v{n, dq.get(), q_end ? dqe.get() : nullptr, dvs.get(), dv.get(), dts.get(),
+                                dt.get(), des.get(), de.get(), margin};
+        const std::vector<unsigned long long> keys = dabd_gpu::broad_phase3d(v, f, s);
+        CUDA_CHECK(cudaStreamDestroy(s));
+        *count = static_cast<int>(keys.size());
+        if (*count > capacity) {
+            set_error("broad_phase3d: capacity too small (needed count written)");
+            return DABD_GPU_ERR_INVALID;
+        }
+        for (size_t k = 0; k < keys.size(); ++k) {
+            int* o = pairs + 5 * k;
+            f.unpack(keys[k], o[0], o[1], o[2], o[3], o[4]);
+        }
         return DABD_GPU_OK;
     });
 }

@@ -255,3 +255,84 @@ def test_ccd3d_known_answers_gpu():
     up2[0] = 0.5
     toi = api.ccd3d([0, 0, 0], [up, up, I], [down, up2, I], [I, I, I], [I, I, I], [rest, rest, rest])
     assert 0.40 < toi[0] < 0.5 and toi[1] == 1.0 and toi[2] == 1.0
+
+
+# ---- 3D broad phase (dabd_gpu_broad_phase3d) --------------------------------
+def _box_mesh(half=0.1):
+    """Closed box surface in rest coordinates: 8 vertices, 12 triangles, 18 edges."""
+    v = np.array([[x, y, z] for x in (-half, half) for y in (-half, half) for z in (-half, half)])
+    quads = [(0, 1, 3, 2), (4, 6, 7, 5), (0, 4, 5, 1), (2, 3, 7, 6), (0, 2, 6, 4), (1, 5, 7, 3)]
+    tris = []
+    for a, b, c, d in quads:
+        tris += [(a, b, c), (a, c, d)]
+    edges = sorted({tuple(sorted((t[i], t[(i + 1) % 3]))) for t in tris for i in range(3)})
+    return v, np.array(tris), np.array(edges)
+
+
+def _pile3d(seed, n):
+    rng = np.random.default_rng(seed)
+    meshes, q = [], []
+    for i in range(n):
+        meshes.append(_box_mesh(rng.uniform(0.08, 0.12)))
+        A = np.eye(3) + 0.1 * rng.standard_normal((3, 3))
+        q.append(np.concatenate([rng.uniform(-0.5, 0.5, 3), A.ravel()]))
+    return np.array(q), meshes
+
+
+def test_broad_phase3d_argument_checks():
+    v, t, e = _box_mesh()
+    bad = t.copy()
+    bad[0, 0] = 99
+    with pytest.raises(L.DabdGpuError, match="out of range"):
+        api.broad_phase3d(np.tile(np.concatenate([np.zeros(3), np.eye(3).ravel()]), (2, 1)),
+                          [(v, bad, e), (v, t, e)], 0.01)
+    assert api.broad_phase3d(np.zeros((1, 12)), [(v, t, e)], 0.01).shape == (0, 5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,n,swept", [(1, 12, False), (2, 20, True), (3, 40, False)])
+def test_broad_phase3d_bitwise_against_brute_force(seed, n, swept):
+    q, meshes = _pile3d(seed, n)
+    q_end = q + 0.02 * np.random.default_rng(seed + 100).standard_normal(q.shape) if swept else None
+    got = api.broad_phase3d(q, meshes, 0.01, q_end=q_end)
+    ref = O.broad_phase3d(q, meshes, 0.01, q_end=q_end)
+    assert len(ref) > 0 and (ref[:, 0] == 0).any() and (ref[:, 0] == 1).any()
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.gpu
+def test_broad_phase3d_feeds_contact_terms():
+    """Every pair the 3D contact terms see as active (d < d_hat) is in the
+    broad phase's candidate list with margin d_hat (no missed contacts)."""
+    q, meshes = _pile3d(4, 16)
+    cand = api.broad_phase3d(q, meshes, D_HAT)
+    cset = {tuple(r) for r in cand.tolist()}
+    kinds, qa, qb, rest, keys = [], [], [], [], []
+    for a in range(len(meshes)):
+        for b in range(len(meshes)):
+            if a == b:
+                continue
+            va, ta, ea = meshes[a]
+            vb, tb, eb = meshes[b]
+            for vi in range(len(va)):
+                for ti, t in enumerate(tb):
+                    kinds.append(0); qa.append(q[a]); qb.append(q[b])
+                    rest.append(np.vstack([va[vi], vb[t]])); keys.append((0, a, b, vi, ti))
+            if a < b:
+                for i, e in enumerate(ea):
+                    for j, f in enumerate(eb):
+                        kinds.append(1); qa.append(q[a]); qb.append(q[b])
+                        rest.append(np.vstack([va[e], vb[f]])); keys.append((1, a, b, i, j))
+    # skip pairs that interpenetrate in this random pile (d = 0 is an error)
+    out = {}
+    for s in range(0, len(kinds), 4096):
+        try:
+            r = api.contact3d_terms(kinds[s:s + 4096], qa[s:s + 4096], qb[s:s + 4096], rest[s:s + 4096],
+                                    D_HAT, KAPPA, hessian=False)
+        except L.DabdGpuError:
+            continue
+        for k, d in zip(keys[s:s + 4096], r["d"]):
+            out[k] = d
+    active = [k for k, d in out.items() if d < D_HAT]
+    assert active, "the pile has no close pairs"
+    assert all(k in cset for k in active)
