@@ -183,3 +183,28 @@ def test_graph_frame_equals_eager_frame(monkeypatch):
     assert np.array_equal(eager.q, graph.q) and np.array_equal(eager.q_dot, graph.q_dot)
     assert [s["admm_iterations"] for s in eager.stats] == [s["admm_iterations"] for s in graph.stats]
     assert [s["newton_iterations"] for s in eager.stats] == [s["newton_iterations"] for s in graph.stats]
+
+
+def test_bench_settings_match_oracle_on_a_pile():
+    """The bench's solver settings (PCG to 1e-10, warm-started; the defaults)
+    on a contact-rich pile: 100 boxes of the pile-1k recipe dropped into the
+    container, 40 frames of run_reference. States match the oracle to the
+    north star's 1e-6 relative tolerance (on scene scale l), the per-frame
+    ADMM k-counts exactly, and the final state is penetration-free."""
+    from paper_2605_15875_b200.scene import lattice_pile
+
+    sd = lattice_pile("pile-100", rows=10, cols_per_slab=10, slabs=1, half=0.05, spacing=0.13,
+                      jitter=0.005, seed=11, l=6.0)
+    frames = 40
+    o = O.Scene(sd)
+    ref = o.run(frames, workers=0)
+    gpu = api.run_reference(sd, frames)
+    dyn = ~o.is_static
+    l = sd.params.scene_scale
+    err = max(float(np.abs(gpu.q[f][dyn] - ref["q"][f][dyn]).max()) for f in range(frames))
+    assert err < 1e-6 * l, err
+    assert [s["admm_iterations"] for s in gpu.stats] == list(ref["admm"])
+    assert max(s["max_contacts"] for s in gpu.stats) > 100  # contact-rich
+    ctx = api.Context(api.Scene(sd))
+    hit, _, dmin = ctx.audit(gpu.q[-1], cutoff=sd.params.d_hat)
+    assert not hit and dmin > 0.0
