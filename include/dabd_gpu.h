@@ -183,6 +183,11 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_stream(dabd_gpu_ctx* ctx, uintptr_
  * called from the thread that calls dabd_gpu_run_frames. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_comm(dabd_gpu_ctx* ctx, const dabd_gpu_comm* comm);
 
+/* Exchange path of a joined context: 0 single process, 1 halo callback,
+ * 2 peer-memory halo (the neighbours' published packets mapped through CUDA
+ * IPC and loaded by the consensus kernel; DABD_GPU_P2P_HALO=0 disables it). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_comm_mode(dabd_gpu_ctx* ctx, int* mode);
+
 /* ---- parity entry points (identical-input comparisons with the oracle) ---
  * subset == NULL means all bodies. q_end == NULL: static broad phase. On
  * capacity overflow the call returns INVALID and writes the needed count. */

@@ -258,6 +258,12 @@ class Context:
         L.check(L.load().dabd_gpu_get_rho(self.h, _d(out)))
         return out[: self.n]
 
+    def comm_mode(self) -> int:
+        """0 single process, 1 halo callback, 2 peer-memory halo (CUDA IPC)."""
+        m = C.c_int()
+        L.check(L.load().dabd_gpu_ctx_comm_mode(self.h, C.byref(m)))
+        return m.value
+
     def planes(self) -> np.ndarray:
         """Interface planes the next frame partitions with ((W-1) x 4)."""
         w = max(self.num_workers - 1, 0)

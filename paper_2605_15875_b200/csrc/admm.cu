@@ -144,20 +144,26 @@ struct Replica {
     int inst; // -1 when remote
 };
 
+// Remote packets j < n_lo come from rank - 1 (at remote_lo), the others from
+// rank + 1 (at remote_hi, index j - n_lo). With the peer-memory halo these
+// are the neighbours' own published buffers (CUDA IPC mappings: NVLink loads
+// on a multi-GPU box), so the exchange is fused into this kernel's reads.
 __device__ __forceinline__ Replica replica(int v, const double* iq, double* iu, const double* irho,
-                                           const double* remote) {
+                                           const double* remote_lo, const double* remote_hi, int n_lo) {
     if (v >= 0) return Replica{iq + 6 * v, iu + 6 * v, irho[v], v};
-    const double* p = remote + kHaloStride * (-1 - v);
+    const int j = -1 - v;
+    const double* p = j < n_lo ? remote_lo + kHaloStride * j : remote_hi + kHaloStride * (j - n_lo);
     return Replica{p, const_cast<double*>(p + 6), p[12], -1};
 }
 
 __global__ void k_consensus(int ns, const int* sh, const int* ipart, int part_base,
                             const double* iq, double* iu, const double* irho, const double* iz,
-                            const double* remote, double* iznext, double* rb, double* sb,
-                            double* rloc, double* sloc, int* err) {
+                            const double* remote_lo, const double* remote_hi, int n_lo,
+                            double* iznext, double* rb, double* sb, double* rloc, double* sloc,
+                            int* err) {
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
-        const Replica a = replica(sh[2 * s], iq, iu, irho, remote);
-        const Replica b = replica(sh[2 * s + 1], iq, iu, irho, remote);
+        const Replica a = replica(sh[2 * s], iq, iu, irho, remote_lo, remote_hi, n_lo);
+        const Replica b = replica(sh[2 * s + 1], iq, iu, irho, remote_lo, remote_hi, n_lo);
         if (a.rho != b.rho) raise(err, kErrReplica);
         double z[6];
         const double den = xadd(xadd(0.0, a.rho), b.rho);
@@ -307,12 +313,13 @@ void launch_vmax(const SceneView& sc, const double* qd, double* out, cudaStream_
 }
 
 void launch_consensus(int ns, const int* sh, const int* ipart, int part_base, const double* iq,
-                      double* iu, const double* irho, const double* iz, const double* remote,
-                      double* iznext, double* rb, double* sb, double* rloc, double* sloc, int* err,
-                      cudaStream_t s) {
+                      double* iu, const double* irho, const double* iz, const double* remote_lo,
+                      const double* remote_hi, int n_lo, double* iznext, double* rb, double* sb,
+                      double* rloc, double* sloc, int* err, cudaStream_t s) {
     if (ns == 0) return;
     DABD_LAUNCH("k_consensus", s, k_consensus<<<grid_for(ns, kB), kB, 0, s>>>(ns, sh, ipart, part_base, iq, iu, irho, iz,
-                                                remote, iznext, rb, sb, rloc, sloc, err));
+                                                                             remote_lo, remote_hi, n_lo, iznext, rb,
+                                                                             sb, rloc, sloc, err));
 }
 
 void launch_pack_halo(int n, const int* inst, const double* iq, const double* iu,

@@ -19,9 +19,9 @@ void launch_vmax(const SceneView& sc, const double* qd, double* out, cudaStream_
 constexpr int kHaloStride = 13;
 
 void launch_consensus(int ns, const int* sh, const int* ipart, int part_base, const double* iq,
-                      double* iu, const double* irho, const double* iz, const double* remote,
-                      double* iznext, double* rb, double* sb, double* rloc, double* sloc, int* err,
-                      cudaStream_t s);
+                      double* iu, const double* irho, const double* iz, const double* remote_lo,
+                      const double* remote_hi, int n_lo, double* iznext, double* rb, double* sb,
+                      double* rloc, double* sloc, int* err, cudaStream_t s);
 void launch_pack_halo(int n, const int* inst, const double* iq, const double* iu,
                       const double* irho, double* out, cudaStream_t s);
 void launch_select_commit(const SceneView& sc, const uint32_t* bmask, const int* part_rank,

@@ -400,6 +400,12 @@ dabd_gpu_status dabd_gpu_get_rho(dabd_gpu_ctx* ctx, double* rho) {
     return DABD_GPU_OK;
 }
 
+dabd_gpu_status dabd_gpu_ctx_comm_mode(dabd_gpu_ctx* ctx, int* mode) {
+    if (!ctx || !mode) return null_arg();
+    *mode = ctx->e->comm_mode();
+    return DABD_GPU_OK;
+}
+
 dabd_gpu_status dabd_gpu_ctx_get_planes(dabd_gpu_ctx* ctx, double* planes) {
     if (!ctx || !planes) return null_arg();
     const std::vector<double> p = ctx->e->planes();

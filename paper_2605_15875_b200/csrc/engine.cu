@@ -134,6 +134,8 @@ Engine::~Engine() {
     if (newton_exec_) cudaGraphExecDestroy(newton_exec_);
     for (cudaStream_t s : cap_streams_) cudaStreamDestroy(s);
     for (cudaStream_t s : side_streams_) cudaStreamDestroy(s);
+    if (peer_lo_) cudaIpcCloseMemHandle(const_cast<double*>(peer_lo_));
+    if (peer_hi_) cudaIpcCloseMemHandle(const_cast<double*>(peer_hi_));
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (own_stream_ && s_) cudaStreamDestroy(s_);
@@ -152,6 +154,13 @@ void Engine::set_stream(cudaStream_t s) {
 
 void Engine::set_comm(const Comm* c) {
     sync();
+    // drop a previous run's peer mappings
+    if (peer_lo_) cudaIpcCloseMemHandle(const_cast<double*>(peer_lo_));
+    if (peer_hi_) cudaIpcCloseMemHandle(const_cast<double*>(peer_hi_));
+    cudaGetLastError();
+    peer_lo_ = peer_hi_ = nullptr;
+    p2p_ = false;
+    halo_parity_ = 0;
     if (!c) {
         distributed_ = false;
         comm_ = Comm{};
@@ -172,16 +181,96 @@ void Engine::set_comm(const Comm* c) {
         for (int p = o[r]; p < o[r + 1]; ++p) pr[p] = r;
     part_rank_.upload(pr, s_);
     sync();
+    if (distributed_) setup_p2p();
+}
+
+// One all-gather of a single value: every rank's earlier work on its stream
+// is complete (gloo stages through the host) or ordered (NCCL) before any
+// rank's later work.
+void Engine::comm_barrier() {
+    rec_.resize(1);
+    rec_all_.resize(comm_.world);
+    if (comm_.allgather(comm_.user, rec_.get(), rec_all_.get(), 1, reinterpret_cast<uintptr_t>(s_)) != 0)
+        throw Error("comm: barrier failed");
+}
+
+void Engine::setup_p2p() {
+    p2p_ = false;
+    if (const char* e = std::getenv("DABD_GPU_P2P_HALO"))
+        if (e[0] == '0') return;
+    // capacity: every body could be split (packets per region)
+    pub_cap_ = static_cast<size_t>(std::max(hs_.nb, 1));
+    pub_.resize(4 * kHaloStride * pub_cap_);
+    // IPC handle (64 bytes = 8 doubles) + a success flag, all-gathered
+    std::vector<double> rec(9, 0.0);
+    cudaIpcMemHandle_t mine{};
+    bool ok = cudaIpcGetMemHandle(&mine, pub_.get()) == cudaSuccess;
+    cudaGetLastError();
+    std::memcpy(rec.data(), &mine, sizeof(mine));
+    rec[8] = ok ? 1.0 : 0.0;
+    rec_.upload(rec, s_);
+    rec_all_.resize(9 * comm_.world);
+    if (comm_.allgather(comm_.user, rec_.get(), rec_all_.get(), 9, reinterpret_cast<uintptr_t>(s_)) != 0)
+        throw Error("comm: all-gather failed");
+    std::vector<double> all = rec_all_.to_host(s_);
+    void* lo = nullptr;
+    void* hi = nullptr;
+    auto open = [&](int r, void** out) {
+        if (r < 0 || r >= comm_.world) return true;
+        if (all[9 * r + 8] == 0.0) return false;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, all.data() + 9 * r, sizeof(h));
+        const bool good = cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+        cudaGetLastError();
+        return good;
+    };
+    ok = ok && open(comm_.rank - 1, &lo) && open(comm_.rank + 1, &hi);
+    // every rank must agree, or all fall back to the halo callback
+    rec_.upload(std::vector<double>{ok ? 1.0 : 0.0}, s_);
+    rec_all_.resize(comm_.world);
+    if (comm_.allgather(comm_.user, rec_.get(), rec_all_.get(), 1, reinterpret_cast<uintptr_t>(s_)) != 0)
+        throw Error("comm: all-gather failed");
+    all = rec_all_.to_host(s_);
+    bool every = true;
+    for (int r = 0; r < comm_.world; ++r) every = every && all[r] != 0.0;
+    if (!every) {
+        if (lo) cudaIpcCloseMemHandle(lo);
+        if (hi) cudaIpcCloseMemHandle(hi);
+        cudaGetLastError();
+        return;
+    }
+    peer_lo_ = static_cast<const double*>(lo);
+    peer_hi_ = static_cast<const double*>(hi);
+    p2p_ = true;
 }
 
 void Engine::exchange_halo() {
     const int n = n_halo_lo_ + n_halo_hi_;
-    launch_pack_halo(n, halo_inst_.get(), iq_.get(), iu_.get(), irho_.get(), hsend_.get(), s_);
     const size_t lo = static_cast<size_t>(kHaloStride) * n_halo_lo_;
     const size_t hi = static_cast<size_t>(kHaloStride) * n_halo_hi_;
+    if (p2p_) {
+        if (static_cast<size_t>(std::max(n_halo_lo_, n_halo_hi_)) > pub_cap_)
+            throw Error("comm: peer halo capacity exceeded");
+        // publish into [side][parity], barrier, then k_consensus reads the
+        // neighbours' regions in place: rank-1's hi side, rank+1's lo side
+        const size_t reg = static_cast<size_t>(kHaloStride) * pub_cap_;
+        const int par = halo_parity_;
+        halo_parity_ ^= 1;
+        double* my_lo = pub_.get() + (0 * 2 + par) * reg;
+        double* my_hi = pub_.get() + (1 * 2 + par) * reg;
+        launch_pack_halo(n_halo_lo_, halo_inst_.get(), iq_.get(), iu_.get(), irho_.get(), my_lo, s_);
+        launch_pack_halo(n_halo_hi_, halo_inst_.get() + n_halo_lo_, iq_.get(), iu_.get(), irho_.get(), my_hi, s_);
+        comm_barrier();
+        remote_lo_ = peer_lo_ ? peer_lo_ + (1 * 2 + par) * reg : nullptr;
+        remote_hi_ = peer_hi_ ? peer_hi_ + (0 * 2 + par) * reg : nullptr;
+        return;
+    }
+    launch_pack_halo(n, halo_inst_.get(), iq_.get(), iu_.get(), irho_.get(), hsend_.get(), s_);
     if (comm_.halo(comm_.user, hsend_.get(), hrecv_.get(), lo, hsend_.get() + lo, hrecv_.get() + lo,
                    hi, reinterpret_cast<uintptr_t>(s_)) != 0)
         throw Error("comm: halo exchange failed");
+    remote_lo_ = hrecv_.get();
+    remote_hi_ = hrecv_.get() + lo;
 }
 
 std::vector<double> Engine::allgather_host(const std::vector<double>& mine) {
@@ -1471,9 +1560,14 @@ FrameStats Engine::frame_admm(int frame) {
                     if (!fail.empty()) throw Error(fail);
                     rloc_.zero(s_);
                     sloc_.zero(s_);
-                    if (distributed_) exchange_halo();
+                    if (distributed_) {
+                        exchange_halo();
+                    } else {
+                        remote_lo_ = remote_hi_ = nullptr;
+                    }
                     launch_consensus(ns, shared_inst_.get(), ipart_.get(), p0_, iq_.get(),
-                                     iu_.get(), irho_.get(), iz_.get(), hrecv_.get(), iznext_.get(),
+                                     iu_.get(), irho_.get(), iz_.get(), remote_lo_, remote_hi_,
+                                     n_halo_lo_, iznext_.get(),
                                      rb_.get(), sb_.get(), rloc_.get(), sloc_.get(), err_.get(), s_);
                     // merge CCD gate per partition (consensus.cpp:66-75): a
                     // fixed-capacity broad phase and the CCD over its device

@@ -62,6 +62,7 @@ class Engine {
         ++solver_epoch_;
     }
     cudaStream_t stream() const { return s_; }
+    int comm_mode() const { return !distributed_ ? 0 : (p2p_ ? 2 : 1); }
     const HostScene& scene() const { return hs_; }
 
     // ---- parity entry points (host arrays) ----
@@ -233,6 +234,20 @@ class Engine {
     DBuf<int> halo_inst_, part_rank_;
     DBuf<double> hsend_, hrecv_, rec_, rec_all_, gath_;
     void exchange_halo();
+    // Peer-memory halo (SURVEY 8(e) "direct P2P halo reads"): every rank
+    // publishes its packets in a device buffer the neighbours map through
+    // CUDA IPC; k_consensus loads the neighbours' packets directly.
+    // pub_ regions: [side lo/hi][parity] x pub_cap_ packets.
+    void setup_p2p();
+    void comm_barrier();
+    DBuf<double> pub_;
+    size_t pub_cap_ = 0;
+    const double* peer_lo_ = nullptr; // rank - 1's pub_ (mapped)
+    const double* peer_hi_ = nullptr; // rank + 1's pub_ (mapped)
+    bool p2p_ = false;
+    int halo_parity_ = 0;
+    const double* remote_lo_ = nullptr; // what k_consensus reads this iteration
+    const double* remote_hi_ = nullptr;
     std::vector<double> allgather_host(const std::vector<double>& mine);
     void commit_gather();
     DBuf<double> rloc_, sloc_, rb_, sb_;

@@ -156,6 +156,7 @@ def run_partitioned(scene, workers: int, frames: int, device: int = 0, group=Non
     ctx = api.Context(sc, device=device, num_workers=workers, part_begin=comm.part_begin,
                       part_end=comm.part_end, **solver)
     ctx.set_comm(comm)
+    run_partitioned.last_comm_mode = ctx.comm_mode()
     qs, qds, hs, stats = [], [], [], []
     for _ in range(frames):
         st = ctx.run_frames(1)[0]

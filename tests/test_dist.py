@@ -127,21 +127,24 @@ def _scene(name, balanced):
     return sd
 
 
-def _gpu_worker(rank, world, port, q, name, workers, frames, balanced=False):
+def _gpu_worker(rank, world, port, q, name, workers, frames, balanced=False, p2p=None):
     try:
+        if p2p is not None:
+            os.environ["DABD_GPU_P2P_HALO"] = p2p
         _init(rank, world, port)
         from paper_2605_15875_b200.dist import run_partitioned
 
         torch.cuda.set_device(0)
         t = run_partitioned(_scene(name, balanced), workers, frames, device=0, **TIGHT)
         q.put((rank, (t.q, t.q_dot, t.trace, t.rho,
-                      [s["admm_iterations"] for s in t.stats], list(t.h))))
+                      [s["admm_iterations"] for s in t.stats], list(t.h), run_partitioned.last_comm_mode)))
         dist.destroy_process_group()
     except BaseException as e:
         q.put((rank, RuntimeError(repr(e))))
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("p2p", ["1", "0"], ids=["peer_memory_halo", "halo_callback"])
 @pytest.mark.parametrize("name,workers,world,frames", [
     ("drop-grid-2", 2, 2, 12),
     ("cubes-64", 2, 2, 8),
@@ -149,17 +152,21 @@ def _gpu_worker(rank, world, port, q, name, workers, frames, balanced=False):
     ("drop-grid-4", 4, 3, 6),
     ("blocked-merge", 2, 2, 3),
 ])
-def test_partitioned_matches_single_gpu(name, workers, world, frames):
+def test_partitioned_matches_single_gpu(name, workers, world, frames, p2p):
+    """p2p "1": k_consensus loads the neighbours' packets through CUDA IPC
+    mappings of their published buffers (the ranks share cuda:0 here; NVLink
+    peer loads on a multi-GPU box); "0": the halo callback (NCCL / gloo)."""
     from paper_2605_15875_b200 import api
     from paper_2605_15875_b200.scene import make_scenario
 
     ref = api.run_distributed(make_scenario(name), workers, frames, **TIGHT)
-    out = _spawn(_gpu_worker, world, name, workers, frames)
+    out = _spawn(_gpu_worker, world, name, workers, frames, False, p2p)
     offs = partition_offsets(workers, world)
     rho = np.full_like(ref.rho, np.nan)
     for r in range(world):
         assert not isinstance(out[r], BaseException), out[r]
-        qs, qds, trace, rrho, admm, hs = out[r]
+        qs, qds, trace, rrho, admm, hs, mode = out[r]
+        assert mode == (2 if p2p == "1" else 1)
         assert admm == [s["admm_iterations"] for s in ref.stats]
         assert hs == list(ref.h)
         assert np.array_equal(trace, ref.trace), (r, np.abs(trace - ref.trace).max())
