@@ -62,6 +62,37 @@ double partition_cost(const PartState& s) {
 
 } // namespace
 
+// DABD_GPU_ADMM_PROFILE=1: host-side phase clock of the multi-partition
+// frame (synchronises the stream at every mark; a probe, never on in bench).
+namespace {
+struct AdmmProfile {
+    bool on = std::getenv("DABD_GPU_ADMM_PROFILE") != nullptr;
+    double t[12] = {};
+    long long n[12] = {};
+    std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    void mark(int slot, cudaStream_t s) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        t[slot] += std::chrono::duration<double, std::milli>(now - last).count();
+        ++n[slot];
+        last = now;
+    }
+    ~AdmmProfile() {
+        if (!on) return;
+        static const char* names[12] = {"frame_setup(rest)", "consensus+gate", "decision", "newton",
+                                        "delta_inf", "commit", "other", "setup:masks", "setup:instances",
+                                        "setup:prepare_solver(rest)", "prep:det_prepare", "prep:resizes"};
+        for (int i = 0; i < 12; ++i)
+            std::fprintf(stderr, "admm_profile %-15s %10.3f ms %8lld marks\n", names[i], t[i], n[i]);
+    }
+};
+AdmmProfile& admm_prof() {
+    static AdmmProfile p;
+    return p;
+}
+} // namespace
+
 Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs), device_(device) {
     if (W < 0 || W > 32) throw InvalidArg("ctx: worker count must be in [0, 32]");
     if (W == 0) {
@@ -490,12 +521,14 @@ void Engine::prepare_solver() {
     CUDA_CHECK(cudaMemcpyAsync(ps_.get(), ps_h_.get(), P_ * sizeof(PartState),
                                cudaMemcpyHostToDevice, s_));
     const int want = std::max(cap_, 48 * std::max(n_inst_, 1) + 4096);
+    admm_prof().mark(9, s_);
     if (want != cap_ || det_.cap() != want || det_fmt_n_ != n_inst_) {
         cap_ = want;
         det_.prepare(n_inst_, ds_.max_verts, cap_);
         det_fmt_n_ = n_inst_;
         graph_ok_ = false;
     }
+    admm_prof().mark(10, s_);
     const size_t C = static_cast<size_t>(cap_);
     const size_t before = cflag_.capacity() + act_.capacity() + cblk_.capacity();
     cflag_.resize(C);
@@ -515,6 +548,7 @@ void Engine::prepare_solver() {
     pcg_part_.resize(3 * static_cast<size_t>(pcg_grid_size(std::max(n_rows_, 1))) * P_);
     (void)pcg_cluster_size(); // resolve cluster attributes before any graph capture
     box_.resize(std::max(n_inst_, 1));
+    admm_prof().mark(11, s_);
     size_t t1 = 0, t2 = 0;
     CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, t2, bkey_.get(), bkey_sorted_.get(),
                                                bidx_.get(), perm_b_.get(), cap_, 0,
@@ -1391,36 +1425,6 @@ FrameStats Engine::frame_reference() {
 
 // runtime.cpp:110-694 on replicated global state with every partition of
 // this context solved in the same batched kernels.
-// DABD_GPU_ADMM_PROFILE=1: host-side phase clock of the multi-partition
-// frame (synchronises the stream at every mark; a probe, never on in bench).
-namespace {
-struct AdmmProfile {
-    bool on = std::getenv("DABD_GPU_ADMM_PROFILE") != nullptr;
-    double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
-    void mark(int slot, cudaStream_t s) {
-        if (!on) return;
-        cudaStreamSynchronize(s);
-        const auto now = std::chrono::steady_clock::now();
-        t[slot] += std::chrono::duration<double, std::milli>(now - last).count();
-        ++n[slot];
-        last = now;
-    }
-    ~AdmmProfile() {
-        if (!on) return;
-        static const char* names[8] = {"frame_setup", "consensus+gate", "decision", "newton",
-                                       "delta_inf", "commit", "other", "-"};
-        for (int i = 0; i < 7; ++i)
-            std::fprintf(stderr, "admm_profile %-15s %10.3f ms %8lld marks\n", names[i], t[i], n[i]);
-    }
-};
-AdmmProfile& admm_prof() {
-    static AdmmProfile p;
-    return p;
-}
-} // namespace
-
 FrameStats Engine::frame_admm(int frame) {
     AdmmProfile& prof = admm_prof();
     prof.mark(6, s_);
@@ -1458,14 +1462,18 @@ FrameStats Engine::frame_admm(int frame) {
         launch_masks(ds_.view(), q_.get(), dplanes.get(), W_ - 1, w, everyone, dm.get(), err_.get(), s_);
         std::vector<uint32_t> mask = dm.to_host(s_);
         check_err("frame: holder masks");
+        prof.mark(7, s_);
         mask.resize(nb);
         // local sets per partition (runtime.cpp:212-236)
         std::vector<std::vector<int>> per(P_);
         for (int b = 0; b < nb; ++b)
             for (int p = 0; p < P_; ++p)
                 if (mask[b] & (1u << (p0_ + p))) per[p].push_back(b);
+        prof.mark(0, s_);
         build_instances(per, mask.data(), false);
+        prof.mark(8, s_);
         prepare_solver();
+        prof.mark(9, s_);
         const int I = n_inst_;
         std::vector<double> invk(std::max(I, 1)), rho(std::max(I, 1), 0.0), rho0(std::max(I, 1), 0.0),
             fs(2 * std::max(I, 1), 0.0);
@@ -1573,7 +1581,7 @@ FrameStats Engine::frame_admm(int frame) {
                     // fixed-capacity broad phase and the CCD over its device
                     // count, then ONE readback of (earliest TOI, r, s, error)
                     launch_merged(I, ianc_.get(), iq_.get(), iznext_.get(), iqtry_.get(), s_);
-                    gate_cap_ = std::max(gate_cap_, 64 * std::max(I, 1));
+                    if (gate_cap_ == 0) gate_cap_ = 64 * std::max(I, 1);
                     det_gate_.ensure(I, ds_.max_verts, gate_cap_);
                     det_gate_.enqueue(ds_.view(), iview(iq_.get(), iqtry_.get()), stat_.get(),
                                       static_cast<int>(h_stat_.size()), true, 0.0, err_.get(), s_);
@@ -1591,7 +1599,13 @@ FrameStats Engine::frame_admm(int frame) {
                                                cudaMemcpyDeviceToHost, s_));
                     CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 8, err_.get(), sizeof(int),
                                                cudaMemcpyDeviceToHost, s_));
+                    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 9, det_gate_.d_count(), sizeof(int),
+                                               cudaMemcpyDeviceToHost, s_));
                     sync();
+                    // the gate's sort cost follows its capacity: shrink it (with
+                    // hysteresis) towards twice the candidates actually found
+                    if (pin_i_[8] == 0 && 4 * pin_i_[9] < gate_cap_ && gate_cap_ > 8192)
+                        gate_cap_ = std::max(8192, 2 * pin_i_[9]);
                     if (pin_i_[8] == kErrCapacity) { // grow and redo this gate with the counted build
                         err_.zero(s_);
                         const int nc = det_gate_.build(ds_.view(), iview(iq_.get(), iqtry_.get()),
