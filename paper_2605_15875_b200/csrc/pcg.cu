@@ -849,23 +849,32 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             sc.wsp[threadIdx.x] = t;
         }
         cluster_barrier(); // wsp of every CTA ready; every peer done reading vm0 / vm1
-        double tt[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        for (int k = 0; k < csize; ++k) {
-            const double* o = cl.map_shared_rank(&sc, k)->wsp;
+        // one thread per CTA folds the csize CTA records (rank order; 6 x csize
+        // DSMEM loads per CTA, not per thread) and solves the 2x2 system
+        if (threadIdx.x == 0) {
+            double tt[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int k = 0; k < csize; ++k) {
+                const double* o = cl.map_shared_rank(&sc, k)->wsp;
 #pragma unroll
-            for (int m = 0; m < 6; ++m) tt[m] += o[m];
+                for (int m = 0; m < 6; ++m) tt[m] += o[m];
+            }
+            const double b1 = tt[0], b2 = tt[1], a11 = tt[2], a12 = tt[3], a22 = tt[4];
+            double c1 = 0.0, c2 = 0.0;
+            const double det = a11 * a22 - a12 * a12;
+            if (a.warm > 1 && a11 > 0.0 && a22 > 0.0 && det > 1e-8 * a11 * a22) {
+                c1 = (b1 * a22 - b2 * a12) / det;
+                c2 = (b2 * a11 - b1 * a12) / det;
+            } else if (a11 > 0.0) {
+                c1 = b1 / a11;
+            }
+            if (!isfinite(c1) || !isfinite(c2)) c1 = c2 = 0.0;
+            sc.scal[0] = c1;
+            sc.scal[1] = c2;
+            sc.scal[2] = tt[5];
         }
-        const double b1 = tt[0], b2 = tt[1], a11 = tt[2], a12 = tt[3], a22 = tt[4];
-        double c1 = 0.0, c2 = 0.0;
-        const double det = a11 * a22 - a12 * a12;
-        if (a.warm > 1 && a11 > 0.0 && a22 > 0.0 && det > 1e-8 * a11 * a22) {
-            c1 = (b1 * a22 - b2 * a12) / det;
-            c2 = (b2 * a11 - b1 * a12) / det;
-        } else if (a11 > 0.0) {
-            c1 = b1 / a11;
-        }
-        if (!isfinite(c1) || !isfinite(c2)) c1 = c2 = 0.0;
-        bnorm2_ws = tt[5];
+        __syncthreads();
+        const double c1 = sc.scal[0], c2 = sc.scal[1];
+        bnorm2_ws = sc.scal[2];
         if (c1 != 0.0 || c2 != 0.0) {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
