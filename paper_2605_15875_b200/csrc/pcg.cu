@@ -324,7 +324,7 @@ struct ClusterScalars {
     double scal[3];       // (beta, alpha, stop) of the iteration, from the scalar warp
     unsigned long long bar[2]; // per-parity mbarriers (st.async complete_tx)
     unsigned long long stage_bar;
-    int n_remote, fallback, nobulk;
+    int n_remote, fallback, nobulk, push_ok;
     int wsum[kCW];
     int rlo[16], rcnt[16], rbase[16]; // rows this CTA needs from each peer (bulk mode)
     int2 req[16];                     // per consumer: (first local row, count) it needs from us
@@ -713,7 +713,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     // push: every peer range arrives by bulk copy (st.async partials); the
     // barrier path (DSMEM pulls through rptr) when blocks spill or the halo
     // ranges do not fit
-    const bool push = cl.map_shared_rank(&sc, 0)->fallback == 0 && cl.map_shared_rank(&sc, 0)->nobulk == 0;
+    // (one DSMEM read per CTA, broadcast through shared memory)
+    if (threadIdx.x == 0) {
+        const ClusterScalars* r0s = cl.map_shared_rank(&sc, 0);
+        sc.push_ok = r0s->fallback == 0 && r0s->nobulk == 0;
+    }
+    __syncthreads();
+    const bool push = sc.push_ok != 0;
     if constexpr (PH) cs[4] = clock64();
     const bool bulk = push;
     {
@@ -792,6 +798,52 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         return y;
     };
 
+    // (A v1, A v0) rows in one pass over the staged blocks (warm start): the
+    // matrix is read once and the two vectors' DSMEM loads overlap; v1 = vm1
+    // (peers' copies at moff = m_off), v0 = vm0 (moff = 0). Same per-block
+    // summation order as spmv_local / spmv_remote, so each result equals the
+    // single-vector SpMV.
+    auto spmv_pair = [&](int lr, double& y1, double& y0) {
+        const int b0 = bstart[lr], b1 = bstart[lr + 1], bs = min(b1, cap_blocks);
+        double l1a = 0.0, l1b = 0.0, l0a = 0.0, l0b = 0.0;
+        int s = b0;
+        auto dot6 = [&](int blkidx, const double* v) {
+            const double2* M2 = reinterpret_cast<const double2*>(blk + 36 * blkidx + 6 * comp);
+            const double2* v2 = reinterpret_cast<const double2*>(v);
+            const double2 m0 = M2[0], m1 = M2[1], m2 = M2[2], w0 = v2[0], w1 = v2[1], w2 = v2[2];
+            return m0.x * w0.x + m0.y * w0.y + m1.x * w1.x + m1.y * w1.y + m2.x * w2.x + m2.y * w2.y;
+        };
+        for (; s + 1 < bs; s += 2) {
+            const int c0 = bcode[s], c1 = bcode[s + 1];
+            if (c0 >= 0) {
+                l1a += dot6(s, vm1 + 6 * c0);
+                l0a += dot6(s, vm0 + 6 * c0);
+            }
+            if (c1 >= 0) {
+                l1b += dot6(s + 1, vm1 + 6 * c1);
+                l0b += dot6(s + 1, vm0 + 6 * c1);
+            }
+        }
+        if (s < bs && bcode[s] >= 0) {
+            l1a += dot6(s, vm1 + 6 * bcode[s]);
+            l0a += dot6(s, vm0 + 6 * bcode[s]);
+        }
+        y1 = l1a + l1b;
+        y0 = l0a + l0b;
+        for (int t = b0; t < bs; ++t) {
+            const int code = bcode[t];
+            if (code >= 0) continue;
+            const double* base = rptr[-1 - code];
+            const double d1 = dot6(t, base + m_off), d0 = dot6(t, base);
+            y1 += d1;
+            y0 += d0;
+        }
+        if (bs < b1) { // spilled blocks: the single-vector path
+            y1 = spmv_remote(lr, nullptr, m_off, spmv_local(lr, vm1));
+            y0 = spmv_remote(lr, nullptr, 0, spmv_local(lr, vm0));
+        }
+    };
+
     // ---- init: r = b = -grad, x = 0, u = Dinv r (read by the peers from m1), w = A u.
     // Every lane keeps its (row, component) entries of all PCG vectors in
     // registers (row group g of the warp: local row warp * 5 + slot + g * 80);
@@ -829,8 +881,8 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         double l[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            ap1[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, spmv_local(lrg[g], vm1)) : 0.0;
-            ap2[g] = on[g] && a.warm > 1 ? spmv_remote(lrg[g], nullptr, 0, spmv_local(lrg[g], vm0)) : 0.0;
+            ap1[g] = ap2[g] = 0.0;
+            if (on[g]) spmv_pair(lrg[g], ap1[g], ap2[g]); // ap2 = A p2 (p2 = 0 when warm == 1)
             l[0] += p1[g] * r[g];
             l[1] += p2[g] * r[g];
             l[2] += p1[g] * ap1[g];
@@ -882,7 +934,8 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 r[g] -= c1 * ap1[g] + c2 * ap2[g];
             }
         }
-        cluster_barrier(); // peers finished reading wsp before sc is reused
+        // (no trailing barrier: wsp is never rewritten in this launch, and the
+        // barrier above already ordered every peer's reads of vm0 / vm1)
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
