@@ -206,6 +206,20 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_holder_masks(dabd_gpu_ctx* ctx, const doub
                                                    int n_planes, const double* planes, double w,
                                                    uint32_t* masks);
 
+/* One consensus step for n split bodies with two replicas each (lower holder
+ * first; the k_consensus / k_adapt kernels of the ADMM frame):
+ * z = sum rho (q + u) / sum rho (consensus_update, consensus.cpp:9-21),
+ * u' = (u + q) - z per replica (dual_update, :23-25), r = max |q - z| over
+ * both replicas, s = max |z - z_prev| (:27-36), rho' = adapt_rho(rho, r, s,
+ * rho0) (:44-52; rho' = rho when adapt->adapt_enabled == 0). q, u, u_new:
+ * [n][2][6]; z_prev, z: [n][6]; rho, rho0, r, s, rho_next: [n]. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_consensus_step(int device, int n, const double* q,
+                                                     const double* u, const double* rho,
+                                                     const double* z_prev, const double* rho0,
+                                                     const dabd_gpu_adapt_params* adapt, double* z,
+                                                     double* u_new, double* r, double* s,
+                                                     double* rho_next);
+
 /* Penetration audit of a configuration: intersection_test
  * (proj/src/geometry.cpp:389-454; strict vertex / loop-centroid containment
  * and proper edge crossings over body pairs with overlapping AABBs) and the

@@ -512,3 +512,46 @@ int oracle_run(void* sp, int workers, int frames, double* q_traj, double* qdot_t
 }
 
 } // extern "C"
+
+// ---- consensus step (consensus.cpp:9-52, runtime.cpp:361-397) ----------------
+// TEST INFRASTRUCTURE: n split bodies with two replicas each (lower holder
+// first): z = consensus_update, u' = dual_update per replica, r = primal
+// residual over both replicas, s = dual residual against z_prev, rho' =
+// adapt_rho (skipped when adapt5[5] == 0).
+extern "C" int oracle_consensus_step(int n, const double* q, const double* u, const double* rho,
+                                     const double* z_prev, const double* rho0, const double* adapt6,
+                                     double* z, double* u_new, double* r, double* s, double* rho_next) {
+    using namespace oracle;
+    return guarded([&] {
+        AdaptParams ap;
+        ap.beta = adapt6[0];
+        ap.tau = adapt6[1];
+        ap.mu = adapt6[2];
+        ap.sigma_min = adapt6[3];
+        ap.sigma_max = adapt6[4];
+        ap.adapt_enabled = adapt6[5] != 0.0;
+        for (int i = 0; i < n; ++i) {
+            std::vector<Vec6> rq(2), rqu(2);
+            for (int h = 0; h < 2; ++h)
+                for (int c = 0; c < 6; ++c) {
+                    rq[h][c] = q[12 * i + 6 * h + c];
+                    rqu[h][c] = q[12 * i + 6 * h + c] + u[12 * i + 6 * h + c];
+                }
+            const Vec6 zi = consensus_update(rqu, {rho[i], rho[i]});
+            Vec6 zp;
+            for (int c = 0; c < 6; ++c) {
+                z[6 * i + c] = zi[c];
+                zp[c] = z_prev[6 * i + c];
+            }
+            for (int h = 0; h < 2; ++h) {
+                Vec6 uh;
+                for (int c = 0; c < 6; ++c) uh[c] = u[12 * i + 6 * h + c];
+                const Vec6 un = dual_update(uh, rq[h], zi);
+                for (int c = 0; c < 6; ++c) u_new[12 * i + 6 * h + c] = un[c];
+            }
+            r[i] = primal_residual_inf(rq, zi);
+            s[i] = dual_residual_inf(zi, zp);
+            rho_next[i] = ap.adapt_enabled ? adapt_rho(rho[i], r[i], s[i], ap, rho0[i]) : rho[i];
+        }
+    });
+}

@@ -407,3 +407,14 @@ def broad_phase3d(q, meshes, margin, q_end=None):
                         out.append((1, a, b, i, j))
     out.sort()
     return np.array(out, dtype=np.int32).reshape(-1, 5)
+
+
+def consensus_step(q, u, rho, z_prev, rho0, adapt6):
+    """oracle/capi.cpp oracle_consensus_step (consensus.cpp:9-52)."""
+    q = _f64(q).reshape(-1, 2, 6)
+    n = len(q)
+    z, un = np.zeros((max(n, 1), 6)), np.zeros((max(n, 1), 2, 6))
+    r, s, rn = np.zeros(max(n, 1)), np.zeros(max(n, 1)), np.zeros(max(n, 1))
+    _check(lib().oracle_consensus_step(n, _d(q), _d(_f64(u, (n, 2, 6))), _d(_f64(rho)), _d(_f64(z_prev, (n, 6))),
+                                       _d(_f64(rho0)), _d(_f64(adapt6)), _d(z), _d(un), _d(r), _d(s), _d(rn)))
+    return dict(z=z[:n], u=un[:n], r=r[:n], s=s[:n], rho=rn[:n])

@@ -76,7 +76,7 @@ EXPORTS = [
     "dabd_gpu_balance_factor", "dabd_gpu_balancer_create", "dabd_gpu_balancer_free",
     "dabd_gpu_balancer_update", "dabd_gpu_contact3d_terms", "dabd_gpu_ccd3d",
     "dabd_gpu_body3d_moments", "dabd_gpu_body3d_terms",
-    "dabd_gpu_broad_phase3d", "dabd_gpu_ctx_comm_mode",
+    "dabd_gpu_broad_phase3d", "dabd_gpu_ctx_comm_mode", "dabd_gpu_consensus_step",
 ]
 
 _lib = None

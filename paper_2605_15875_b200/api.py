@@ -524,3 +524,22 @@ def broad_phase3d(q, meshes, margin: float, q_end=None, device: int = 0) -> np.n
             continue
         L.check(st)
         return out[: cnt.value].copy()
+
+
+def consensus_step(q, u, rho, z_prev, rho0, adapt=None, device: int = 0) -> dict:
+    """One consensus / dual / residual / rho-adaptation step for split bodies
+    with two replicas (dabd_gpu_consensus_step). q, u: [n][2][6]."""
+    from .scene import AdaptParams
+
+    a = adapt or AdaptParams()
+    q = _f64(q).reshape(-1, 2, 6)
+    n = len(q)
+    u = _f64(u, (n, 2, 6))
+    rho, zp, r0 = _f64(rho).reshape(n), _f64(z_prev, (n, 6)), _f64(rho0).reshape(n)
+    z, un = np.zeros((max(n, 1), 6)), np.zeros((max(n, 1), 2, 6))
+    r, s, rn = np.zeros(max(n, 1)), np.zeros(max(n, 1)), np.zeros(max(n, 1))
+    L.check(L.load().dabd_gpu_consensus_step(
+        device, n, _d(q), _d(u), _d(rho), _d(zp), _d(r0),
+        C.byref(L.AdaptParams(a.beta, a.tau, a.mu, a.sigma_min, a.sigma_max, int(a.adapt_enabled))),
+        _d(z), _d(un), _d(r), _d(s), _d(rn)))
+    return dict(z=z[:n], u=un[:n], r=r[:n], s=s[:n], rho=rn[:n])

@@ -2,6 +2,7 @@
 // thread-local last error, no exceptions across the boundary, null -> INVALID.
 #include "dabd_gpu.h"
 
+#include "admm.hpp"
 #include "body3d.hpp"
 #include "broad3d.hpp"
 #include "contact3d.hpp"
@@ -605,6 +606,80 @@ dabd_gpu_status dabd_gpu_broad_phase3d(int device, int n, const double* q, const
         for (size_t k = 0; k < keys.size(); ++k) {
             int* o = pairs + 5 * k;
             f.unpack(keys[k], o[0], o[1], o[2], o[3], o[4]);
+        }
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_consensus_step(int device, int n, const double* q, const double* u,
+                                        const double* rho, const double* z_prev, const double* rho0,
+                                        const dabd_gpu_adapt_params* adapt, double* z, double* u_new,
+                                        double* r, double* s, double* rho_next) {
+    if (n < 0 || !adapt) return null_arg();
+    if (n > 0 && (!q || !u || !rho || !z_prev || !rho0 || !z || !u_new || !r || !s || !rho_next))
+        return null_arg();
+    return guarded([&] {
+        if (n == 0) return DABD_GPU_OK;
+        for (int i = 0; i < n; ++i)
+            if (!(rho[i] > 0.0)) throw dabd_gpu::Error("consensus_update: rho must be > 0");
+        CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t st = nullptr;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        const int I = 2 * n; // replica instances 2i (partition 0), 2i + 1 (partition 1)
+        std::vector<double> hrho(I), hrho0(I), hz(6 * static_cast<size_t>(I));
+        std::vector<int> hpart(I), hsh(I), hanc(I, 1);
+        for (int i = 0; i < n; ++i)
+            for (int h = 0; h < 2; ++h) {
+                const int k = 2 * i + h;
+                hrho[k] = rho[i];
+                hrho0[k] = rho0[i];
+                hpart[k] = h;
+                hsh[k] = k;
+                for (int c = 0; c < 6; ++c) hz[6 * k + c] = z_prev[6 * i + c];
+            }
+        dabd_gpu::DBuf<double> dq, du, drho, drho0, dz, dzn, drb, dsb, drl, dsl;
+        dabd_gpu::DBuf<int> dpart, dsh, danc, derr;
+        dq.upload(q, 6 * static_cast<size_t>(I), st);
+        du.upload(u, 6 * static_cast<size_t>(I), st);
+        drho.upload(hrho, st);
+        drho0.upload(hrho0, st);
+        dz.upload(hz, st);
+        dzn.resize(6 * static_cast<size_t>(I));
+        drb.resize(I);
+        dsb.resize(I);
+        drl.resize(2);
+        dsl.resize(2);
+        drl.zero(st);
+        dsl.zero(st);
+        dpart.upload(hpart, st);
+        dsh.upload(hsh, st);
+        danc.upload(hanc, st);
+        derr.resize(1);
+        derr.zero(st);
+        dabd_gpu::launch_consensus(n, dsh.get(), dpart.get(), 0, dq.get(), du.get(), drho.get(), dz.get(),
+                                   nullptr, nullptr, 0, dzn.get(), drb.get(), dsb.get(), drl.get(), dsl.get(),
+                                   derr.get(), st);
+        dabd_gpu::AdaptParams ap;
+        ap.beta = adapt->beta;
+        ap.tau = adapt->tau;
+        ap.mu = adapt->mu;
+        ap.sigma_min = adapt->sigma_min;
+        ap.sigma_max = adapt->sigma_max;
+        ap.adapt_enabled = adapt->adapt_enabled != 0;
+        dabd_gpu::launch_adapt(I, danc.get(), drho.get(), drho0.get(), drb.get(), dsb.get(), ap, dz.get(),
+                               dzn.get(), st);
+        CUDA_CHECK(cudaGetLastError());
+        const std::vector<double> zn = dzn.to_host(st), un = du.to_host(st), rb = drb.to_host(st),
+                                  sb = dsb.to_host(st), rn = drho.to_host(st);
+        const std::vector<int> e = derr.to_host(st);
+        CUDA_CHECK(cudaStreamDestroy(st));
+        if (e[0] != 0) throw dabd_gpu::Error("consensus: replica rho mismatch");
+        for (int i = 0; i < n; ++i) {
+            for (int c = 0; c < 6; ++c) z[6 * i + c] = zn[12 * i + c];
+            for (int c = 0; c < 12; ++c) u_new[12 * i + c] = un[12 * i + c];
+            r[i] = rb[2 * i];
+            s[i] = sb[2 * i];
+            rho_next[i] = rn[2 * i];
         }
         return DABD_GPU_OK;
     });

@@ -109,3 +109,26 @@ def test_captured_newton_equals_host_driven(monkeypatch):
     assert np.array_equal(eager.q, graph.q) and np.array_equal(eager.q_dot, graph.q_dot)
     assert np.array_equal(eager.trace, graph.trace)
     assert [s["newton_iterations"] for s in eager.stats] == [s["newton_iterations"] for s in graph.stats]
+
+
+def test_consensus_step_bitwise_against_oracle():
+    """consensus_update / dual_update / residuals / adapt_rho (consensus.cpp:
+    9-52) on identical inputs: the device step equals the oracle bitwise,
+    including rho adaptation up, down and at both clamps."""
+    from paper_2605_15875_b200.scene import AdaptParams
+
+    rng = np.random.default_rng(21)
+    n = 512
+    q = rng.standard_normal((n, 1, 6)) + rng.choice([1e-6, 1e-1], size=(n, 1, 1)) * rng.standard_normal((n, 2, 6))
+    u = 1e-3 * rng.standard_normal((n, 2, 6))
+    # spread primal vs dual residual ratios across the adaptation branches
+    zp = q.mean(axis=1) + rng.choice([1e-9, 1e-2, 1.0], size=(n, 1)) * rng.standard_normal((n, 6))
+    rho0 = rng.uniform(0.5, 2.0, n)
+    rho = rho0 * rng.choice([1e-3, 1.0, 1e3], size=n)
+    a = AdaptParams()
+    gpu = api.consensus_step(q, u, rho, zp, rho0, a)
+    ref = O.consensus_step(q, u, rho, zp, rho0, [a.beta, a.tau, a.mu, a.sigma_min, a.sigma_max, 1.0])
+    for k in ("z", "u", "r", "s", "rho"):
+        assert np.array_equal(gpu[k], ref[k]), k
+    ratio = gpu["rho"] / rho
+    assert (ratio == 2.0).any() and (ratio == 0.5).any() and (ratio == 1.0).any()
