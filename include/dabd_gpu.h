@@ -20,6 +20,8 @@
  *   dabd_gpu_holder_masks        body_holder_mask                include/dabd/partition.hpp:43-45
  *   dabd_gpu_objective           LocalObjective::value/derivatives include/dabd/objective.hpp:34-75
  *   dabd_gpu_newton_solve        newton_solve                    include/dabd/newton.hpp:25-26
+ *   dabd_gpu_consensus_step      consensus_update, dual_update, *_residual_inf, adapt_rho
+ *                                                                include/dabd/consensus.hpp:13-55
  *   dabd_gpu_contact3d_terms     3D extension of contact_energy  src/energy.cpp:63-94 (PT / EE, no reference)
  *   dabd_gpu_ccd3d               3D extension of ccd_toi          src/geometry.cpp:232-341 (no reference)
  *   dabd_gpu_broad_phase3d       3D extension of broad_phase      src/geometry.cpp:106-208 (no reference)
