@@ -545,6 +545,18 @@ void Engine::prepare_solver() {
     partial_.resize(static_cast<size_t>(std::max(segsum_chunks(std::max(cap_, n_rows_)),
                                                  energy_chunks(cap_) + energy_chunks(n_rows_))) * P_ + P_);
     pbuf_.resize(12 * static_cast<size_t>(std::max(n_rows_, 1)));
+    // the PCG warm start reads the previous solutions (x_, pbuf_): zero them
+    // whenever they are (re)allocated, so no run ever reads uninitialised
+    // device memory and every run is reproducible bit for bit, while the
+    // previous directions still carry over from frame to frame
+    if (x_.get() != x_seen_) {
+        x_.zero(s_);
+        x_seen_ = x_.get();
+    }
+    if (pbuf_.get() != pbuf_seen_) {
+        pbuf_.zero(s_);
+        pbuf_seen_ = pbuf_.get();
+    }
     pcg_part_.resize(3 * static_cast<size_t>(pcg_grid_size(std::max(n_rows_, 1))) * P_);
     (void)pcg_cluster_size(); // resolve cluster attributes before any graph capture
     box_.resize(std::max(n_inst_, 1));

