@@ -1365,6 +1365,9 @@ FrameStats Engine::frame_reference() {
     }
     FrameStats st;
     st.h = frame_params_.h;
+    bool exact_retry = false;
+    double saved_tol = pcg_tol_;
+    int saved_max = pcg_max_;
     for (int attempt = 0; attempt < 6; ++attempt) {
         FrameCtrl init{};
         init.frame = static_cast<double>(frame_counter_);
@@ -1398,9 +1401,29 @@ FrameStats Engine::frame_reference() {
             graph_ok_ = false;
             continue;
         }
+        if (pin_i_[0] == kErrLineSearch && !exact_retry) {
+            // newton.cpp:56-58's collapse after an iterative solve: redo the
+            // frame from its start with the PCG at the exact-solve limit (see
+            // frame_admm) before reporting the reference's error
+            err_.zero(s_);
+            const size_t nq = 6 * static_cast<size_t>(hs_.nb);
+            CUDA_CHECK(cudaMemcpyAsync(q_.get(), q_start_.get(), nq * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s_));
+            CUDA_CHECK(cudaMemcpyAsync(qd_.get(), qd_start_.get(), nq * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s_));
+            exact_retry = true;
+            saved_tol = pcg_tol_;
+            saved_max = pcg_max_;
+            set_solver(1e-14, std::max(saved_max, 50000));
+            ++exact_retries_;
+            continue;
+        }
+        if (exact_retry) set_solver(saved_tol, saved_max);
+        exact_retry = false;
         check_err("frame_reference");
         break;
     }
+    if (exact_retry) set_solver(saved_tol, saved_max);
     const FrameCtrl& c = ctrl_h_[0];
     if (graph_replayed_) { // kernels the replay executed: nodes per body x body executions
         const long long rebuilds = lstate_h_[0].n_rebuilds - rebuilds_seen_;
@@ -1713,8 +1736,35 @@ FrameStats Engine::frame_admm(int frame) {
                                                cudaMemcpyDeviceToHost, s_));
                 };
                 const bool fused_dq = use_graph_ && n_rows_ > 0;
-                const NewtonResult r = use_graph_ ? newton_graph(hs_.newton_cap, tol, fused_dq ? dq_tail : std::function<void()>{})
-                                                  : newton_batch(hs_.newton_cap, tol);
+                auto solve = [&] {
+                    return use_graph_ ? newton_graph(hs_.newton_cap, tol, fused_dq ? dq_tail : std::function<void()>{})
+                                      : newton_batch(hs_.newton_cap, tol);
+                };
+                NewtonResult r;
+                try {
+                    r = solve();
+                } catch (const Error& e) {
+                    // newton.cpp:56-58's line-search collapse. The reference
+                    // solves exactly (SimplicialLDLT); an iterative solve to a
+                    // relative residual can leave error in near-null
+                    // directions that keeps ||dq||_inf above tol where the
+                    // exact step would stop. Redo this solve from its start
+                    // with the PCG at the exact-solve limit before failing.
+                    if (std::string(e.what()).find("line search") == std::string::npos) throw;
+                    if (I) CUDA_CHECK(cudaMemcpyAsync(iq_.get(), iqbefore_.get(), 6 * I * sizeof(double),
+                                                      cudaMemcpyDeviceToDevice, s_));
+                    const double t0 = pcg_tol_;
+                    const int m0 = pcg_max_;
+                    set_solver(1e-14, std::max(m0, 50000));
+                    try {
+                        r = solve();
+                    } catch (...) {
+                        set_solver(t0, m0);
+                        throw;
+                    }
+                    set_solver(t0, m0);
+                    ++exact_retries_;
+                }
                 st.newton_iterations += r.iterations;
                 st.line_search_steps += r.ls_steps;
                 st.pcg_iterations += r.pcg_iters;

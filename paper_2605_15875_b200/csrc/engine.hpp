@@ -169,6 +169,7 @@ class Engine {
     int halvings_ = 0;
     long long frame_counter_ = 0;
     std::vector<TraceRow> trace_;
+    long long exact_retries_ = 0;       // Newton solves redone at the exact-solve PCG limit
     const double* x_seen_ = nullptr;    // allocations of x_ / pbuf_ already zeroed
     const double* pbuf_seen_ = nullptr;
     std::vector<cudaStream_t> side_streams_; // per capture level: independent branches

@@ -38,14 +38,11 @@ def test_criterion2_consensus_convergence():  # acceptance.cpp:72-107
 
 
 def test_criterion3_penetration_free_300_frames():  # acceptance.cpp:110-125, experiments.cpp:160-175
-    """Zero interpenetrating commits over every builtin x 300 frames. The
-    reference's newton_solve throws when its line search collapses below
-    alpha = 1e-12 (newton.cpp:56-58); the oracle restatement hits that on
-    `heterogeneous` (1e4:1 mass ratios) within 300 frames too. Which scenes
-    collapse, and when, follows the chaotic divergence of FP64 rounding (the
-    device hits it on some of the consensus scenes the oracle finishes), so a
-    run may end early with exactly that error, never with an interpenetrating
-    commit; the funnel and the single-partition grid always finish."""
+    """Zero interpenetrating commits over every builtin x 300 frames, no
+    short runs. The only tolerated early end is the reference's own
+    line-search collapse (newton.cpp:56-58) on `heterogeneous` (1e4:1 mass
+    ratios), which the oracle restatement with its direct solve hits too; the
+    device redoes a collapsed solve at the exact-solve PCG limit first."""
     short = {}
     for name in BUILTINS:
         sd = make_scenario(name)
@@ -61,9 +58,7 @@ def test_criterion3_penetration_free_300_frames():  # acceptance.cpp:110-125, ex
             assert st["committed"] == 1, (name, f)
             hit, nviol, _ = ctx.audit()
             assert not hit and nviol == 0, (name, f)
-    for name in ("funnel-analog", "drop-grid-1"):
-        assert name not in short, short
-    assert len(short) <= len(BUILTINS) // 2, short
+    assert set(short) <= {"heterogeneous"}, short
 
 
 def test_criterion4_beta_robustness():  # acceptance.cpp:128-148
