@@ -184,7 +184,7 @@ def run_reference_arm(args) -> None:
     if ws > 1:
         line["config"]["note"] = (
             f"N={ws}: the reference arm times the single-domain pile-1k step (one pile-1k-equivalent "
-            f"unit, as the GPU arm counts them); the CPU consensus run of pile-1k-x{ws} needs ~230 ADMM "
+            f"unit, as the GPU arm counts them); the CPU consensus run of pile-1k-x{ws} needs ~150 ADMM "
             "iterations of 1,000-body Newton solves per frame and partition, minutes per frame")
     print(json.dumps(line), flush=True)
 
