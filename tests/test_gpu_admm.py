@@ -90,15 +90,15 @@ def test_blocked_merge_halving():  # test_runtime.cpp:146-159
 
 
 def test_cubes_64_two_partitions():
-    _compare("cubes-64", 2, 3)
+    _compare("cubes-64", 2, 20)
 
 
 def test_heterogeneous_mass_ratio():
-    _compare("heterogeneous", 2, 3, state_tol=1e-6, trace_tol=1e-5)
+    _compare("heterogeneous", 2, 20, state_tol=1e-6, trace_tol=1e-5)
 
 
 def test_drop_grid_four_workers():
-    _compare("drop-grid-4", 4, 3)
+    _compare("drop-grid-4", 4, 20)
 
 
 def test_captured_newton_equals_host_driven(monkeypatch):
