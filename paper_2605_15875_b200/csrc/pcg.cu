@@ -903,13 +903,12 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         cluster_barrier(); // wsp of every CTA ready; every peer done reading vm0 / vm1
         // one thread per CTA folds the csize CTA records (rank order; 6 x csize
         // DSMEM loads per CTA, not per thread) and solves the 2x2 system
-        if (threadIdx.x == 0) {
-            double tt[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int k = 0; k < csize; ++k) {
-                const double* o = cl.map_shared_rank(&sc, k)->wsp;
+        if (warp == 0) { // lane k loads CTA k's record; fixed shuffle tree
+            double tt[6];
 #pragma unroll
-                for (int m = 0; m < 6; ++m) tt[m] += o[m];
-            }
+            for (int m = 0; m < 6; ++m) tt[m] = lane < csize ? cl.map_shared_rank(&sc, lane)->wsp[m] : 0.0;
+#pragma unroll
+            for (int m = 0; m < 6; ++m) tt[m] = warp_sum(tt[m]);
             const double b1 = tt[0], b2 = tt[1], a11 = tt[2], a12 = tt[3], a22 = tt[4];
             double c1 = 0.0, c2 = 0.0;
             const double det = a11 * a22 - a12 * a12;
@@ -920,9 +919,11 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 c1 = b1 / a11;
             }
             if (!isfinite(c1) || !isfinite(c2)) c1 = c2 = 0.0;
-            sc.scal[0] = c1;
-            sc.scal[1] = c2;
-            sc.scal[2] = tt[5];
+            if (lane == 0) {
+                sc.scal[0] = c1;
+                sc.scal[1] = c2;
+                sc.scal[2] = tt[5];
+            }
         }
         __syncthreads();
         const double c1 = sc.scal[0], c2 = sc.scal[1];
