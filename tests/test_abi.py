@@ -62,3 +62,29 @@ def test_invalid_scene_rejected():
     with pytest.raises(L.DabdGpuError) as e:
         api.Scene(sd)
     assert e.value.status == 3
+
+
+def test_header_is_plain_c99_and_links(tmp_path):
+    """include/dabd_gpu.h is a C header (no C++ in the signatures): a C99
+    translation unit calling through it compiles with -pedantic and links
+    against libdabd_gpu.so."""
+    import subprocess
+
+    from paper_2605_15875_b200 import build as B
+
+    lib = B.build()
+    src = tmp_path / "abi.c"
+    src.write_text('#include "dabd_gpu.h"\n'
+                   "int main(void) {\n"
+                   "    dabd_gpu_scene* s = 0;\n"
+                   "    int n = 0, nv = 0;\n"
+                   "    if (dabd_gpu_scene_counts(s, &n, &nv) != DABD_GPU_ERR_INVALID) return 1;\n"
+                   "    return dabd_gpu_last_error()[0] == 0;\n"
+                   "}\n")
+    exe = tmp_path / "abi"
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I",
+                        os.path.join(ROOT, "include"), str(src), "-L", os.path.dirname(lib),
+                        "-ldabd_gpu", "-Wl,-rpath," + os.path.dirname(lib), "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert subprocess.run([str(exe)]).returncode == 0
