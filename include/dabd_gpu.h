@@ -22,6 +22,8 @@
  *   dabd_gpu_newton_solve        newton_solve                    include/dabd/newton.hpp:25-26
  *   dabd_gpu_consensus_step      consensus_update, dual_update, *_residual_inf, adapt_rho
  *                                                                include/dabd/consensus.hpp:13-55
+ *   dabd_gpu_check_stopping      check_stopping                  src/consensus.cpp:54-64
+ *   dabd_gpu_timestep_apply      TimestepController              include/dabd/consensus.hpp:60-87
  *   dabd_gpu_contact3d_terms     3D extension of contact_energy  src/energy.cpp:63-94 (PT / EE, no reference)
  *   dabd_gpu_ccd3d               3D extension of ccd_toi          src/geometry.cpp:232-341 (no reference)
  *   dabd_gpu_broad_phase3d       3D extension of broad_phase      src/geometry.cpp:106-208 (no reference)
@@ -97,6 +99,15 @@ typedef struct dabd_gpu_frame_stats {
     int pcg_iterations;
     int max_contacts;     /* largest active set seen */
     int max_candidates;
+    int exact_retries;    /* Newton solves redone at the exact-solve PCG limit after a
+                             line-search collapse (newton.cpp:56-58); 0 on a clean frame */
+    int capacity_retries; /* work redone after a capacity grew (candidate list, BSR row width) */
+    /* Host wall-clock seconds, as the reference's worker timers
+     * (runtime.cpp:117-124, 399-402, 466-475; sim.hpp:44-47): local Newton
+     * solves, collision work of the consensus step (merge gate), waiting on
+     * peer ranks, and the whole frame (t_compute = t_frame - t_sync). For a
+     * run_reference context t_solve = t_frame. */
+    double t_solve, t_coll, t_sync, t_frame;
 } dabd_gpu_frame_stats;
 
 /* Inter-GPU exchange of a partition-per-GPU run; replaces
@@ -221,6 +232,20 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_consensus_step(int device, int n, const do
                                                      const dabd_gpu_adapt_params* adapt, double* z,
                                                      double* u_new, double* r, double* s,
                                                      double* rho_next);
+
+/* The controller's stop rule (consensus.cpp:54-64), the function the
+ * multi-partition frame evaluates: *end = 1 iff dq / (h l), r / (h l) and
+ * s / (h l) are all strictly below theta and every merge-gate toi is exactly
+ * 1.0 (n_tois may be 0). */
+DABD_GPU_API dabd_gpu_status dabd_gpu_check_stopping(double dq, double r, double s,
+                                                     const double* tois, int n_tois, double h,
+                                                     double l, double theta, int* end);
+/* TimestepController (consensus.hpp:60-87) driven by a sequence of frame
+ * outcomes: events[i] = 0 a failed frame (h /= 2; more than max_halvings
+ * failures in a row is DABD_GPU_RUNTIME), 1 a committed frame
+ * (h = min(h0, 2 h)). h_after[i] = h after event i. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_timestep_apply(double h0, int max_halvings, const int* events,
+                                                     int n_events, double* h_after);
 
 /* Penetration audit of a configuration: intersection_test
  * (proj/src/geometry.cpp:389-454; strict vertex / loop-centroid containment

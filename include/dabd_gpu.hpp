@@ -131,8 +131,10 @@ struct Trajectory {
     std::vector<double> h;
 };
 
-/* sim.hpp:25-40. The per-worker wall clocks of the reference's threads have
- * no meaning for batched kernels: t_compute / t_sync stay empty. */
+/* sim.hpp:25-40. Partitions batched in one context share one host clock, so
+ * every worker column of a commit row carries the context's frame compute /
+ * sync seconds (dabd_gpu_frame_stats t_frame - t_sync, t_sync); the
+ * iteration rows leave them empty. */
 struct MetricsRow {
     int64_t frame = 0;
     int32_t attempt = 0;
@@ -161,6 +163,9 @@ struct FrameStats {
     int pcg_iterations = 0;
     int max_contacts = 0;
     int max_candidates = 0;
+    int exact_retries = 0;
+    int capacity_retries = 0;
+    double t_solve = 0.0, t_coll = 0.0, t_sync = 0.0, t_frame = 0.0; // sim.hpp:44-47
 };
 
 /* sim.hpp:55-61. */
@@ -490,6 +495,10 @@ inline RunResult run_distributed(const SceneData& scene, const RunOptions& optio
             row.commit_row = t[7] == 1.0;
             if (row.commit_row && options.reference && f < static_cast<int64_t>(options.reference->q.size()))
                 row.mse = mse_to_reference(sc.is_static(), q, options.reference->q[f]);
+            if (row.commit_row) {
+                row.t_compute.assign(options.workers, st.t_frame - st.t_sync);
+                row.t_sync.assign(options.workers, st.t_sync);
+            }
             res.metrics.push_back(std::move(row));
         }
         FrameStats fs;
@@ -502,6 +511,12 @@ inline RunResult run_distributed(const SceneData& scene, const RunOptions& optio
         fs.pcg_iterations = st.pcg_iterations;
         fs.max_contacts = st.max_contacts;
         fs.max_candidates = st.max_candidates;
+        fs.exact_retries = st.exact_retries;
+        fs.capacity_retries = st.capacity_retries;
+        fs.t_solve = st.t_solve;
+        fs.t_coll = st.t_coll;
+        fs.t_sync = st.t_sync;
+        fs.t_frame = st.t_frame;
         res.frames.push_back(fs);
         if (options.audit && ctx.intersection_test()) ++res.intersection_violations;
         if (!options.out_dir.empty())

@@ -555,3 +555,63 @@ extern "C" int oracle_consensus_step(int n, const double* q, const double* u, co
         }
     });
 }
+
+// consensus.cpp:9-21 with arbitrary replica weights: qu [n][6], rho [n].
+extern "C" int oracle_consensus_update(int n, const double* qu, const double* rho, double* z) {
+    return guarded([&] {
+        std::vector<Vec6> v(n);
+        for (int i = 0; i < n; ++i)
+            for (int c = 0; c < 6; ++c) v[i][c] = qu[6 * i + c];
+        const Vec6 zz = consensus_update(v, rho ? std::vector<double>(rho, rho + n) : std::vector<double>());
+        for (int c = 0; c < 6; ++c) z[c] = zz[c];
+    });
+}
+
+// consensus.cpp:38-52
+extern "C" int oracle_init_rho(double mass, double beta, double* out) {
+    return guarded([&] { *out = init_rho(mass, beta); });
+}
+
+extern "C" int oracle_adapt_rho(double rho, double r, double s, const double* adapt6, double rho0,
+                                double* out) {
+    return guarded([&] {
+        AdaptParams ap;
+        ap.beta = adapt6[0];
+        ap.tau = adapt6[1];
+        ap.mu = adapt6[2];
+        ap.sigma_min = adapt6[3];
+        ap.sigma_max = adapt6[4];
+        ap.adapt_enabled = adapt6[5] != 0.0;
+        *out = adapt_rho(rho, r, s, ap, rho0);
+    });
+}
+
+// consensus.cpp:54-64
+extern "C" int oracle_check_stopping(double dq, double r, double s, const double* tois, int n, double h,
+                                     double l, double theta, int* end) {
+    return guarded([&] {
+        *end = check_stopping(dq, r, s, std::vector<double>(tois, tois + n), h, l, theta) ? 1 : 0;
+    });
+}
+
+// consensus.hpp:60-87: events 0 = failed frame, 1 = committed frame.
+extern "C" int oracle_timestep_apply(double h0, int max_halvings, const int* events, int n,
+                                     double* h_after) {
+    return guarded([&] {
+        TimestepController ts(h0, max_halvings);
+        for (int i = 0; i < n; ++i) {
+            if (events[i] == 0) ts.on_frame_failed();
+            else ts.on_frame_committed();
+            h_after[i] = ts.h();
+        }
+    });
+}
+
+// partition.cpp:131-138 on two holder masks.
+extern "C" int oracle_contact_replication(uint32_t mask_a, uint32_t mask_b, int* kc) {
+    return guarded([&] {
+        PartitionLayout L;
+        L.holder_mask = {mask_a, mask_b};
+        *kc = contact_replication(L, 0, 1);
+    });
+}

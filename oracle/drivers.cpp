@@ -9,9 +9,46 @@
 
 #include <algorithm>
 #include <bit>
+#include <cstdlib>
+#include <exception>
 #include <limits>
+#include <thread>
 
 namespace oracle {
+
+// One std::thread per worker, as the reference runs its workers
+// (sim.cpp:281-322): fn(i) for i in [0, n) on up to
+// worker_threads() threads. Each worker's work touches only its own state;
+// results are combined by the caller in worker order, so the outcome is
+// independent of the thread count. ORACLE_THREADS=1 runs sequentially.
+int worker_threads() {
+    if (const char* e = std::getenv("ORACLE_THREADS")) return std::max(1, std::atoi(e));
+    return std::max(1u, std::thread::hardware_concurrency());
+}
+
+template <typename Fn>
+void for_workers(int n, Fn&& fn) {
+    const int t = std::min(n, worker_threads());
+    if (t <= 1) {
+        for (int i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::exception_ptr> errs(n);
+    std::vector<std::thread> pool;
+    for (int k = 0; k < t; ++k)
+        pool.emplace_back([&, k] {
+            for (int i = k; i < n; i += t) {
+                try {
+                    fn(i);
+                } catch (...) {
+                    errs[i] = std::current_exception();
+                }
+            }
+        });
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e); // the lowest worker's error, like a sequential run
+}
 
 // partition.cpp:9-11
 double overlap_width(double v_max, double h, double w_min) {
@@ -399,8 +436,9 @@ Trajectory run_distributed(const Scene& scene, int nw, int frames) {
                         }
                     }
                     for (int i = 0; i < nw; ++i) W[i].u = u_new[i];
-                    for (int i = 0; i < nw; ++i)
+                    for_workers(nw, [&](int i) {
                         toi[i] = merge_ccd_gate(bodies, W[i].wq, W[i].shared, z_next[i], W[i].local_all);
+                    });
                     // controller (runtime.cpp:586-619)
                     IterTrace it;
                     it.frame = f;
@@ -443,8 +481,9 @@ Trajectory run_distributed(const Scene& scene, int nw, int frames) {
                                                         scene.adapt, W[i].rho0[s]);
                     for (int i = 0; i < nw; ++i) W[i].z = z_next[i];
                 }
-                // local solves (runtime.cpp:465-475)
-                for (int i = 0; i < nw; ++i) {
+                // local solves (runtime.cpp:465-475), one thread per worker
+                std::vector<NewtonReport> reps(nw);
+                for_workers(nw, [&](int i) {
                     Worker& wk = W[i];
                     std::vector<double> kap;
                     std::vector<Vec6> qt;
@@ -466,10 +505,12 @@ Trajectory run_distributed(const Scene& scene, int nw, int frames) {
                     const LocalObjective obj =
                         LocalObjective::assemble(bodies, wk.local_all, kap, qt, an, hm, fp);
                     const Configs before = wk.wq;
-                    const NewtonReport r = newton_solve(obj, wk.wq, no);
-                    st.newton_iterations += r.iterations;
-                    st.line_search_steps += r.line_search_steps;
+                    reps[i] = newton_solve(obj, wk.wq, no);
                     wk.dq = obj.config_delta_inf(wk.wq, before);
+                });
+                for (int i = 0; i < nw; ++i) {
+                    st.newton_iterations += reps[i].iterations;
+                    st.line_search_steps += reps[i].line_search_steps;
                 }
             }
             if (retry) {

@@ -418,3 +418,46 @@ def consensus_step(q, u, rho, z_prev, rho0, adapt6):
     _check(lib().oracle_consensus_step(n, _d(q), _d(_f64(u, (n, 2, 6))), _d(_f64(rho)), _d(_f64(z_prev, (n, 6))),
                                        _d(_f64(rho0)), _d(_f64(adapt6)), _d(z), _d(un), _d(r), _d(s), _d(rn)))
     return dict(z=z[:n], u=un[:n], r=r[:n], s=s[:n], rho=rn[:n])
+
+
+def consensus_update(qu, rho):
+    """consensus.cpp:9-21 with per-replica weights (oracle_consensus_update)."""
+    qu = _f64(qu).reshape(-1, 6)
+    z = np.zeros(6)
+    n = len(qu)
+    _check(lib().oracle_consensus_update(n, _d(qu), _d(_f64(rho)) if n else None, _d(z)))
+    return z
+
+
+def init_rho(mass, beta):
+    out = C.c_double()
+    _check(lib().oracle_init_rho(C.c_double(mass), C.c_double(beta), C.byref(out)))
+    return out.value
+
+
+def adapt_rho(rho, r, s, adapt6, rho0):
+    out = C.c_double()
+    _check(lib().oracle_adapt_rho(C.c_double(rho), C.c_double(r), C.c_double(s),
+                                  _d(_f64(adapt6)), C.c_double(rho0), C.byref(out)))
+    return out.value
+
+
+def check_stopping(dq, r, s, tois, h, l, theta):
+    t = _f64(tois).reshape(-1)
+    end = C.c_int()
+    _check(lib().oracle_check_stopping(*(C.c_double(x) for x in (dq, r, s)), _d(t), len(t),
+                                       *(C.c_double(x) for x in (h, l, theta)), C.byref(end)))
+    return bool(end.value)
+
+
+def timestep_apply(h0, max_halvings, events):
+    ev = np.asarray(events, dtype=np.int32)
+    out = np.zeros(max(len(ev), 1))
+    _check(lib().oracle_timestep_apply(C.c_double(h0), int(max_halvings), _i(ev), len(ev), _d(out)))
+    return out[: len(ev)]
+
+
+def contact_replication(mask_a, mask_b):
+    kc = C.c_int()
+    _check(lib().oracle_contact_replication(C.c_uint32(mask_a), C.c_uint32(mask_b), C.byref(kc)))
+    return kc.value

@@ -46,7 +46,10 @@ class FrameStats(C.Structure):
     _fields_ = [("committed", C.c_int), ("attempts", C.c_int), ("h", C.c_double),
                 ("admm_iterations", C.c_int), ("newton_iterations", C.c_int),
                 ("line_search_steps", C.c_int), ("pcg_iterations", C.c_int),
-                ("max_contacts", C.c_int), ("max_candidates", C.c_int)]
+                ("max_contacts", C.c_int), ("max_candidates", C.c_int),
+                ("exact_retries", C.c_int), ("capacity_retries", C.c_int),
+                ("t_solve", C.c_double), ("t_coll", C.c_double), ("t_sync", C.c_double),
+                ("t_frame", C.c_double)]
 
 
 HaloFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
@@ -77,6 +80,7 @@ EXPORTS = [
     "dabd_gpu_balancer_update", "dabd_gpu_contact3d_terms", "dabd_gpu_ccd3d",
     "dabd_gpu_body3d_moments", "dabd_gpu_body3d_terms",
     "dabd_gpu_broad_phase3d", "dabd_gpu_ctx_comm_mode", "dabd_gpu_consensus_step",
+    "dabd_gpu_check_stopping", "dabd_gpu_timestep_apply",
 ]
 
 _lib = None

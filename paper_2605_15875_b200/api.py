@@ -543,3 +543,23 @@ def consensus_step(q, u, rho, z_prev, rho0, adapt=None, device: int = 0) -> dict
         C.byref(L.AdaptParams(a.beta, a.tau, a.mu, a.sigma_min, a.sigma_max, int(a.adapt_enabled))),
         _d(z), _d(un), _d(r), _d(s), _d(rn)))
     return dict(z=z[:n], u=un[:n], r=r[:n], s=s[:n], rho=rn[:n])
+
+
+def check_stopping(dq: float, r: float, s: float, tois, h: float, l: float, theta: float) -> bool:
+    """The controller's stop rule (consensus.cpp:54-64) as the multi-partition
+    frame evaluates it (dabd_gpu_check_stopping; host code, no device)."""
+    t = _f64(tois).reshape(-1)
+    end = C.c_int()
+    L.check(L.load().dabd_gpu_check_stopping(
+        C.c_double(dq), C.c_double(r), C.c_double(s), _d(t) if len(t) else None, len(t),
+        C.c_double(h), C.c_double(l), C.c_double(theta), C.byref(end)))
+    return bool(end.value)
+
+
+def timestep_apply(h0: float, max_halvings: int, events) -> np.ndarray:
+    """TimestepController (consensus.hpp:60-87) over frame outcomes
+    (0 failed, 1 committed); h after each event (dabd_gpu_timestep_apply)."""
+    ev = np.ascontiguousarray(events, dtype=np.int32)
+    out = np.zeros(max(len(ev), 1))
+    L.check(L.load().dabd_gpu_timestep_apply(C.c_double(h0), int(max_halvings), _i(ev), len(ev), _d(out)))
+    return out[: len(ev)]

@@ -17,6 +17,19 @@ __global__ void k_gather(int n, const int* ibody, const double* q, double* iq) {
         iq[t] = q[6 * ibody[t / 6] + t % 6];
 }
 
+// PCG warm-start vectors carried to a new instance set: row r takes the
+// previous row map[r] (same (partition, body)) or starts from zero. prev holds
+// the previous x (6 R_old) followed by the previous p2 (6 R_old).
+__global__ void k_warm_remap(int n_rows, const int* map, const double* prev, int r_old, double* x,
+                             double* p2) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 6 * n_rows; t += gridDim.x * blockDim.x) {
+        const int m = map[t / 6];
+        const size_t e = 6 * static_cast<size_t>(m) + t % 6;
+        x[t] = m >= 0 ? prev[e] : 0.0;
+        p2[t] = m >= 0 ? prev[6 * static_cast<size_t>(r_old) + e] : 0.0;
+    }
+}
+
 // q_tilde = q + h qdot + h^2 M^{-1} f, f = m g (+ replica force split) on the
 // translation slots (body.cpp:120-134, runtime.cpp:252-264).
 __global__ void k_predict(SceneView sc, int n, const int* ibody, const double* iq,
@@ -286,6 +299,12 @@ __global__ void k_accept_copy(int n, const int* ipart, int part_base, const Part
 void launch_gather(int n, const int* ibody, const double* q, double* iq, cudaStream_t s) {
     if (n == 0) return;
     DABD_LAUNCH("k_gather", s, k_gather<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ibody, q, iq));
+}
+
+void launch_warm_remap(int n_rows, const int* map, const double* prev, int r_old, double* x,
+                       double* p2, cudaStream_t s) {
+    if (n_rows == 0) return;
+    DABD_LAUNCH("k_warm_remap", s, k_warm_remap<<<grid_for(6ll * n_rows, kB), kB, 0, s>>>(n_rows, map, prev, r_old, x, p2));
 }
 
 void launch_predict(const SceneView& sc, int n, const int* ibody, const double* iq,

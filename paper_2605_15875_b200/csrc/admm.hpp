@@ -7,6 +7,9 @@
 namespace dabd_gpu {
 
 void launch_gather(int n, const int* ibody, const double* q, double* iq, cudaStream_t s);
+// x[6 n_rows], p2[6 n_rows] from prev = (x_old, p2_old) through map (-1: zero).
+void launch_warm_remap(int n_rows, const int* map, const double* prev, int r_old, double* x,
+                       double* p2, cudaStream_t s);
 void launch_predict(const SceneView& sc, int n, const int* ibody, const double* iq,
                     const double* qd, double h, double gx, double gy, const double* ifs,
                     double* iqt, cudaStream_t s);

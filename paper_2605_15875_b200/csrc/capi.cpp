@@ -374,6 +374,12 @@ dabd_gpu_status dabd_gpu_run_frames(dabd_gpu_ctx* ctx, int n_frames, dabd_gpu_fr
                 o.pcg_iterations = st[f].pcg_iterations;
                 o.max_contacts = st[f].max_contacts;
                 o.max_candidates = st[f].max_candidates;
+                o.exact_retries = st[f].exact_retries;
+                o.capacity_retries = st[f].capacity_retries;
+                o.t_solve = st[f].t_solve;
+                o.t_coll = st[f].t_coll;
+                o.t_sync = st[f].t_sync;
+                o.t_frame = st[f].t_frame;
             }
         return DABD_GPU_OK;
     });
@@ -606,6 +612,29 @@ dabd_gpu_status dabd_gpu_broad_phase3d(int device, int n, const double* q, const
         for (size_t k = 0; k < keys.size(); ++k) {
             int* o = pairs + 5 * k;
             f.unpack(keys[k], o[0], o[1], o[2], o[3], o[4]);
+        }
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_check_stopping(double dq, double r, double s, const double* tois, int n_tois,
+                                        double h, double l, double theta, int* end) {
+    if (!end || n_tois < 0 || (n_tois > 0 && !tois)) return null_arg();
+    return guarded([&] {
+        *end = dabd_gpu::check_stopping(dq, r, s, tois, n_tois, h, l, theta) ? 1 : 0;
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_timestep_apply(double h0, int max_halvings, const int* events, int n_events,
+                                        double* h_after) {
+    if (n_events < 0 || (n_events > 0 && (!events || !h_after))) return null_arg();
+    return guarded([&] {
+        dabd_gpu::TimestepController ts(h0, max_halvings);
+        for (int i = 0; i < n_events; ++i) {
+            if (events[i] == 0) ts.on_frame_failed();
+            else ts.on_frame_committed();
+            h_after[i] = ts.h();
         }
         return DABD_GPU_OK;
     });

@@ -90,6 +90,7 @@ enum DevError : int {
     kErrLineSearch = 8,     // newton.cpp:60-62
     kErrReplica = 9,        // runtime.cpp:384-385 replica rho mismatch
     kErrSettle = 10,        // sim.cpp:239 Newton stepping failed to settle
+    kErrEll = 11,           // a BSR row couples more bodies than the ELL width (host regrows)
 };
 
 __device__ __forceinline__ void raise(int* err, int code) { atomicCAS(err, 0, code); }

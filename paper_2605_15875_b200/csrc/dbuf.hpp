@@ -18,6 +18,12 @@ struct Error : std::runtime_error {
     explicit Error(const std::string& w) : std::runtime_error(w) {}
 };
 
+// A device-side error code (common.cuh DevError) raised by a kernel.
+struct DeviceError : Error {
+    int code;
+    DeviceError(const std::string& w, int c) : Error(w), code(c) {}
+};
+
 struct InvalidArg : std::runtime_error {
     explicit InvalidArg(const std::string& w) : std::runtime_error(w) {}
 };

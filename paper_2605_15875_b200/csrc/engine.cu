@@ -26,7 +26,9 @@ const char* err_text(int code) {
     case kErrTouching: return "ccd_toi: start configuration already touching/intersecting";
     case kErrBarrierDomain: return "barrier_energy: d <= 0 (barrier domain violated)";
     case kErrDegenerateEdge: return "point_edge_distance: degenerate edge (e0 == e1)";
-    case kErrCapacity: return "capacity exceeded (BSR row has more than kEll coupled bodies)";
+    case kErrCapacity: return "capacity exceeded (contact candidate list)";
+    case kErrEll: return "capacity exceeded (BSR row couples more bodies than the ELL width)";
+    case kErrSettle: return "run_reference: Newton stepping failed to settle";
     case kErrNoHolder: return "LocalObjective: contact pair visible to no worker (overlap too small)";
     case kErrFactor: return "newton_solve: factorization failed (non-SPD diagonal block)";
     case kErrLineSearch: return "newton_solve: line search failed below 1e-12 (non-descent direction)";
@@ -40,21 +42,16 @@ static_assert(sizeof(PartState) % sizeof(double) == 0, "PartState must be 8-byte
 
 double* ps_field(PartState* ps, double PartState::*f) { return &(ps->*f); }
 
-bool check_stopping(double dq, double r, double s, const std::vector<double>& tois, double h,
-                    double l, double theta) { // consensus.cpp:54-64
-    const double nrm = h * l;
-    bool end = dq / nrm < theta && r / nrm < theta && s / nrm < theta;
-    for (double t : tois)
-        if (t != 1.0) end = false;
-    return end;
-}
-
 // A partition's compute cost for the balancer: the reference feeds the
 // worker's wall-clock compute time (runtime.cpp:674); partitions batched in
 // shared kernels have no separable clock, so the cost is the deterministic
 // row-weighted work of its solves: every Newton iteration touches its rows
 // and contact blocks, every PCG iteration its rows. Floored at 1 so the
 // imbalance metric's positivity holds for an empty partition.
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 double partition_cost(const PartState& s) {
     const double rows = s.ndof / 6.0;
     return std::max(1.0, s.iterations * (rows + 2.0 * s.n_active_contacts) + s.pcg_total * rows);
@@ -116,7 +113,7 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     qd_.upload(hs_.qdot0, s_);
     q_start_.resize(6 * std::max(hs_.nb, 1));
     rho_carry_.assign(hs_.nb, std::numeric_limits<double>::quiet_NaN());
-    h_cur_ = hs_.params.h;
+    tsc_ = TimestepController(hs_.params.h, hs_.max_halvings);
     if (W_ > 0) {
         planes_cur_.assign(hs_.planes.begin(), hs_.planes.begin() + (W_ - 1));
         balancer_ = Balancer(W_, hs_.balance);
@@ -342,7 +339,7 @@ void Engine::check_err(const char* where) {
     if (code != 0) {
         err_.zero(s_);
         CUDA_CHECK(cudaStreamSynchronize(s_));
-        throw Error(std::string(err_text(code)) + " [" + where + "]");
+        throw DeviceError(std::string(err_text(code)) + " [" + where + "]", code);
     }
 }
 
@@ -356,6 +353,15 @@ void Engine::sync() {
 // ---------------------------------------------------------------------------
 void Engine::build_instances(const std::vector<std::vector<int>>& per_part, const uint32_t* masks,
                              bool single_domain) {
+    // (partition, body) of every row of the outgoing set: the PCG warm start
+    // of a row that survives into the new set is carried over (per partition,
+    // so N ranks and one GPU hand a partition the same starting guess);
+    // every other row starts from zero
+    std::vector<std::pair<long long, int>> old_keys(h_rinst_.size());
+    for (size_t r = 0; r < h_rinst_.size(); ++r)
+        old_keys[r] = {(static_cast<long long>(h_rpart_[r]) << 32) | h_ibody_[h_rinst_[r]], static_cast<int>(r)};
+    std::sort(old_keys.begin(), old_keys.end());
+    const int r_old = n_rows_;
     h_ibody_.clear();
     h_ipart_.clear();
     h_irow_.clear();
@@ -405,15 +411,42 @@ void Engine::build_instances(const std::vector<std::vector<int>>& per_part, cons
     ianc_.resize(I);
     ianc_.zero(s_);
     iu_.zero(s_);
-    for (DBuf<double>* b : {&rgrad_, &x_, &r_, &z_, &p0v_, &p1v_, &ap_}) b->resize(6 * R);
+    {
+        std::vector<int> map(R, -1);
+        bool carried = false;
+        for (int r = 0; r < n_rows_; ++r) {
+            const long long key = (static_cast<long long>(h_rpart_[r]) << 32) | h_ibody_[h_rinst_[r]];
+            const auto it = std::lower_bound(old_keys.begin(), old_keys.end(), std::make_pair(key, -1));
+            if (it != old_keys.end() && it->first == key) {
+                map[r] = it->second;
+                carried = true;
+            }
+        }
+        if (carried) { // old rows (x, p2) out of the way before the buffers are reused
+            warm_prev_.resize(12 * static_cast<size_t>(r_old));
+            CUDA_CHECK(cudaMemcpyAsync(warm_prev_.get(), x_.get(), 6 * r_old * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s_));
+            CUDA_CHECK(cudaMemcpyAsync(warm_prev_.get() + 6 * r_old, pbuf_.get(), 6 * r_old * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s_));
+        }
+        for (DBuf<double>* b : {&rgrad_, &x_, &r_, &z_, &p0v_, &p1v_, &ap_}) b->resize(6 * R);
+        pbuf_.resize(12 * R);
+        if (carried) {
+            warm_map_.upload(map, s_);
+            launch_warm_remap(n_rows_, warm_map_.get(), warm_prev_.get(), r_old, x_.get(), pbuf_.get(), s_);
+        } else {
+            x_.zero(s_);
+            pbuf_.zero(s_);
+        }
+    }
     rdiag_.resize(36 * R);
     rdinv_.resize(36 * R);
     rval_.resize(R);
     rowtmp_.resize(R);
     rowtmp2_.resize(R);
     ell_cnt_.resize(R);
-    ell_col_.resize(R * kEll);
-    ell_blk_.resize(R * kEll * 36);
+    ell_col_.resize(R * ell_w_);
+    ell_blk_.resize(R * ell_w_ * 36);
     partial_.resize(static_cast<size_t>(segsum_chunks(std::max(n_inst_ * 64, 1 << 16))) * P_ + P_);
     if (masks) {
         bmask_.upload(masks, hs_.nb, s_);
@@ -457,6 +490,7 @@ SolverView Engine::view() {
     v.ell_cnt = ell_cnt_.get();
     v.ell_col = ell_col_.get();
     v.ell_blk = ell_blk_.get();
+    v.ell_w = ell_w_;
     v.x = x_.get();
     v.r = r_.get();
     v.z = z_.get();
@@ -544,19 +578,7 @@ void Engine::prepare_solver() {
     perm_b_.resize(C);
     partial_.resize(static_cast<size_t>(std::max(segsum_chunks(std::max(cap_, n_rows_)),
                                                  energy_chunks(cap_) + energy_chunks(n_rows_))) * P_ + P_);
-    pbuf_.resize(12 * static_cast<size_t>(std::max(n_rows_, 1)));
-    // the PCG warm start reads the previous solutions (x_, pbuf_): zero them
-    // whenever they are (re)allocated, so no run ever reads uninitialised
-    // device memory and every run is reproducible bit for bit, while the
-    // previous directions still carry over from frame to frame
-    if (x_.get() != x_seen_) {
-        x_.zero(s_);
-        x_seen_ = x_.get();
-    }
-    if (pbuf_.get() != pbuf_seen_) {
-        pbuf_.zero(s_);
-        pbuf_seen_ = pbuf_.get();
-    }
+    // (x_ / pbuf_, the PCG warm start, are (re)initialised by build_instances)
     pcg_part_.resize(3 * static_cast<size_t>(pcg_grid_size(std::max(n_rows_, 1))) * P_);
     (void)pcg_cluster_size(); // resolve cluster attributes before any graph capture
     box_.resize(std::max(n_inst_, 1));
@@ -1201,11 +1223,11 @@ void Engine::objective(const ObjectiveIn& in, const double* q, int mode, double*
                 for (int c = 0; c < 6; ++c)
                     hess_dense[static_cast<size_t>(6 * r + a) * nd + 6 * r + c] = dg[36 * r + 6 * a + c];
             for (int t = 0; t < cnt[r]; ++t) {
-                const int cc = col[r * kEll + t];
+                const int cc = col[r * ell_w_ + t];
                 for (int a = 0; a < 6; ++a)
                     for (int c = 0; c < 6; ++c)
                         hess_dense[static_cast<size_t>(6 * r + a) * nd + 6 * cc + c] =
-                            blk[(static_cast<size_t>(r) * kEll + t) * 36 + 6 * a + c];
+                            blk[(static_cast<size_t>(r) * ell_w_ + t) * 36 + 6 * a + c];
             }
         }
     }
@@ -1259,7 +1281,10 @@ std::vector<TraceRow> Engine::take_trace() {
 
 void Engine::run_frames(int n, FrameStats* stats) {
     for (int f = 0; f < n; ++f) {
-        const FrameStats st = W_ == 0 ? frame_reference() : frame_admm(static_cast<int>(frame_counter_));
+        const auto t0 = std::chrono::steady_clock::now();
+        FrameStats st = W_ == 0 ? frame_reference() : frame_admm(static_cast<int>(frame_counter_));
+        st.t_frame = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (W_ == 0) st.t_solve = st.t_frame; // the whole N=1 frame is one solve graph (sim.cpp:207-247)
         ++frame_counter_;
         if (stats) stats[f] = st;
     }
@@ -1349,6 +1374,26 @@ void Engine::capture_reference_graph() {
     graph_ok_ = true;
 }
 
+// kErrCapacity: the contact-candidate list; kErrEll: the BSR row width. The
+// caller has restored the state the failed work started from.
+bool Engine::grow_capacity(int code) {
+    if (code == kErrCapacity) {
+        cap_ *= 2;
+        det_fmt_n_ = -1;
+        prepare_solver();
+    } else if (code == kErrEll) {
+        ell_w_ *= 2;
+        const size_t R = std::max(n_rows_, 1);
+        ell_col_.resize(R * ell_w_);
+        ell_blk_.resize(R * ell_w_ * 36);
+        ++solver_epoch_;
+    } else {
+        return false;
+    }
+    graph_ok_ = false;
+    return true;
+}
+
 // sim.cpp:186-249
 FrameStats Engine::frame_reference() {
     frame_params_ = hs_.params;
@@ -1365,10 +1410,16 @@ FrameStats Engine::frame_reference() {
     }
     FrameStats st;
     st.h = frame_params_.h;
+    const long long exact0 = exact_retries_, cap0 = capacity_retries_;
     bool exact_retry = false;
-    double saved_tol = pcg_tol_;
-    int saved_max = pcg_max_;
-    for (int attempt = 0; attempt < 6; ++attempt) {
+    SolverRestore restore(*this); // the exact-solve retry's PCG limits never outlive the frame
+    const size_t nq = 6 * static_cast<size_t>(hs_.nb);
+    auto restart = [&] { // back to the frame start
+        err_.zero(s_);
+        CUDA_CHECK(cudaMemcpyAsync(q_.get(), q_start_.get(), nq * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+        CUDA_CHECK(cudaMemcpyAsync(qd_.get(), qd_start_.get(), nq * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+    };
+    for (int grows = 0;;) {
         FrameCtrl init{};
         init.frame = static_cast<double>(frame_counter_);
         ctrl_h_[0] = init;
@@ -1387,43 +1438,29 @@ FrameStats Engine::frame_reference() {
         CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState),
                                    cudaMemcpyDeviceToHost, s_));
         CUDA_CHECK(cudaStreamSynchronize(s_));
-        if (pin_i_[0] == kErrCapacity) {
-            // grow the fixed capacities, restore the frame start and redo it
-            err_.zero(s_);
-            const size_t nq = 6 * static_cast<size_t>(hs_.nb);
-            CUDA_CHECK(cudaMemcpyAsync(q_.get(), q_start_.get(), nq * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, s_));
-            CUDA_CHECK(cudaMemcpyAsync(qd_.get(), qd_start_.get(), nq * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, s_));
-            cap_ *= 2;
-            det_fmt_n_ = -1;
-            prepare_solver();
-            graph_ok_ = false;
+        const int code = pin_i_[0];
+        if ((code == kErrCapacity || code == kErrEll) && grows < kMaxGrows) {
+            // grow the capacity that overflowed, restore the frame start and
+            // redo it; past the budget check_err below reports the overflow
+            restart();
+            grow_capacity(code);
+            ++grows;
+            ++capacity_retries_;
             continue;
         }
-        if (pin_i_[0] == kErrLineSearch && !exact_retry) {
+        if (code == kErrLineSearch && !exact_retry) {
             // newton.cpp:56-58's collapse after an iterative solve: redo the
             // frame from its start with the PCG at the exact-solve limit (see
             // frame_admm) before reporting the reference's error
-            err_.zero(s_);
-            const size_t nq = 6 * static_cast<size_t>(hs_.nb);
-            CUDA_CHECK(cudaMemcpyAsync(q_.get(), q_start_.get(), nq * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, s_));
-            CUDA_CHECK(cudaMemcpyAsync(qd_.get(), qd_start_.get(), nq * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, s_));
+            restart();
             exact_retry = true;
-            saved_tol = pcg_tol_;
-            saved_max = pcg_max_;
-            set_solver(1e-14, std::max(saved_max, 50000));
+            set_solver(1e-14, std::max(pcg_max_, 50000));
             ++exact_retries_;
             continue;
         }
-        if (exact_retry) set_solver(saved_tol, saved_max);
-        exact_retry = false;
-        check_err("frame_reference");
+        check_err("frame_reference"); // any other device error, or an overflow past the budget
         break;
     }
-    if (exact_retry) set_solver(saved_tol, saved_max);
     const FrameCtrl& c = ctrl_h_[0];
     if (graph_replayed_) { // kernels the replay executed: nodes per body x body executions
         const long long rebuilds = lstate_h_[0].n_rebuilds - rebuilds_seen_;
@@ -1436,6 +1473,8 @@ FrameStats Engine::frame_reference() {
     }
     rebuilds_seen_ = lstate_h_[0].n_rebuilds;
     if (c.failed || !c.ended) throw Error("run_reference: Newton stepping failed to settle");
+    st.exact_retries = static_cast<int>(exact_retries_ - exact0);
+    st.capacity_retries = static_cast<int>(capacity_retries_ - cap0);
     st.admm_iterations = c.admm_iterations;
     st.newton_iterations = c.newton_total;
     st.line_search_steps = c.ls_total;
@@ -1477,9 +1516,10 @@ FrameStats Engine::frame_admm(int frame) {
     const uint32_t everyone = W_ == 32 ? 0xffffffffu : ((1u << W_) - 1u);
     int attempt = 0;
     FrameStats st;
+    const long long exact0 = exact_retries_, cap0 = capacity_retries_;
     while (true) {
         st.attempts = attempt + 1;
-        const double h = h_cur_;
+        const double h = tsc_.h();
         st.h = h;
         frame_params_ = hs_.params;
         frame_params_.h = h;
@@ -1601,10 +1641,13 @@ FrameStats Engine::frame_admm(int frame) {
                 std::vector<double> earliest(P_, 2.0), rl(P_, 0.0), sl(P_, 0.0);
                 try {
                     if (!fail.empty()) throw Error(fail);
+                    const auto tc = std::chrono::steady_clock::now();
                     rloc_.zero(s_);
                     sloc_.zero(s_);
                     if (distributed_) {
+                        const auto ts = std::chrono::steady_clock::now();
                         exchange_halo();
+                        st.t_sync += seconds_since(ts);
                     } else {
                         remote_lo_ = remote_hi_ = nullptr;
                     }
@@ -1664,6 +1707,7 @@ FrameStats Engine::frame_admm(int frame) {
                         rl[p] = pin_d_[32 + p];
                         sl[p] = pin_d_[64 + p];
                     }
+                    st.t_coll += seconds_since(tc); // consensus + merge gate (runtime.cpp:399-402)
                     prof.mark(1, s_);
                 } catch (const Error& e) {
                     if (!distributed_) throw;
@@ -1674,7 +1718,9 @@ FrameStats Engine::frame_admm(int frame) {
                     // sees every partition's (dq, r, s, earliest TOI).
                     std::vector<double> rec = {static_cast<double>(P_), fail.empty() ? 0.0 : 1.0};
                     for (int p = 0; p < P_; ++p) rec.insert(rec.end(), {dq[p], rl[p], sl[p], earliest[p]});
+                    const auto ts = std::chrono::steady_clock::now();
                     const std::vector<double> all = allgather_host(rec);
+                    st.t_sync += seconds_since(ts); // controller fan-in (runtime.cpp:586-601)
                     const size_t stride = all.size() / comm_.world;
                     dq.clear(), rl.clear(), sl.clear(), earliest.clear();
                     bool any_fail = false;
@@ -1705,7 +1751,7 @@ FrameStats Engine::frame_admm(int frame) {
                 const bool end =
                     check_stopping(row.dq, row.r, row.s, tois, h, P.scene_scale, P.theta);
                 if (end) row.sigma = 1;
-                else if (k == hs_.admm_max_iterations) row.sigma = halvings_ < hs_.max_halvings ? 2 : 3;
+                else if (k == hs_.admm_max_iterations) row.sigma = tsc_.can_halve() ? 2 : 3;
                 trace_.push_back(row);
                 if (row.sigma == 1) {
                     st.admm_iterations = k;
@@ -1714,8 +1760,7 @@ FrameStats Engine::frame_admm(int frame) {
                 }
                 if (row.sigma == 3) throw Error("frame failed: halving budget exhausted with a blocked merge");
                 if (row.sigma == 2) {
-                    h_cur_ /= 2.0;
-                    ++halvings_;
+                    tsc_.on_frame_failed();
                     retry = true;
                     break;
                 }
@@ -1740,30 +1785,38 @@ FrameStats Engine::frame_admm(int frame) {
                     return use_graph_ ? newton_graph(hs_.newton_cap, tol, fused_dq ? dq_tail : std::function<void()>{})
                                       : newton_batch(hs_.newton_cap, tol);
                 };
+                // Capacity overflow inside the solve (contact list, BSR row
+                // width): grow and redo the solve from its start. newton.cpp:
+                // 56-58's line-search collapse: the reference solves exactly
+                // (SimplicialLDLT); an iterative solve to a relative residual
+                // can leave error in near-null directions that keeps
+                // ||dq||_inf above tol where the exact step would stop, so the
+                // solve is redone once with the PCG at the exact-solve limit
+                // before the error is reported.
                 NewtonResult r;
-                try {
-                    r = solve();
-                } catch (const Error& e) {
-                    // newton.cpp:56-58's line-search collapse. The reference
-                    // solves exactly (SimplicialLDLT); an iterative solve to a
-                    // relative residual can leave error in near-null
-                    // directions that keeps ||dq||_inf above tol where the
-                    // exact step would stop. Redo this solve from its start
-                    // with the PCG at the exact-solve limit before failing.
-                    if (std::string(e.what()).find("line search") == std::string::npos) throw;
-                    if (I) CUDA_CHECK(cudaMemcpyAsync(iq_.get(), iqbefore_.get(), 6 * I * sizeof(double),
-                                                      cudaMemcpyDeviceToDevice, s_));
-                    const double t0 = pcg_tol_;
-                    const int m0 = pcg_max_;
-                    set_solver(1e-14, std::max(m0, 50000));
+                SolverRestore restore(*this);
+                for (int grows = 0, exact = 0;;) {
                     try {
+                        const auto tn = std::chrono::steady_clock::now();
                         r = solve();
-                    } catch (...) {
-                        set_solver(t0, m0);
-                        throw;
+                        st.t_solve += seconds_since(tn); // runtime.cpp:466-468
+                        break;
+                    } catch (const DeviceError& e) {
+                        const bool cap = (e.code == kErrCapacity || e.code == kErrEll) && grows < kMaxGrows;
+                        const bool ls = e.code == kErrLineSearch && !exact;
+                        if (!cap && !ls) throw;
+                        if (I) CUDA_CHECK(cudaMemcpyAsync(iq_.get(), iqbefore_.get(), 6 * I * sizeof(double),
+                                                          cudaMemcpyDeviceToDevice, s_));
+                        if (cap) {
+                            grow_capacity(e.code);
+                            ++grows;
+                            ++capacity_retries_;
+                        } else {
+                            set_solver(1e-14, std::max(pcg_max_, 50000));
+                            exact = 1;
+                            ++exact_retries_;
+                        }
                     }
-                    set_solver(t0, m0);
-                    ++exact_retries_;
                 }
                 st.newton_iterations += r.iterations;
                 st.line_search_steps += r.ls_steps;
@@ -1797,7 +1850,12 @@ FrameStats Engine::frame_admm(int frame) {
             if (anc[i]) rho_carry_[h_ibody_[i]] = rho_now[i];
         launch_commit(ds_.view(), I, ibody_.get(), ipart_.get(), ianc_.get(), bmask_.get(),
                       iq_.get(), iznext_.get(), q_start_.get(), h, q_.get(), qd_.get(), s_);
-        if (distributed_) commit_gather();
+        if (distributed_) {
+            const auto ts = std::chrono::steady_clock::now();
+            commit_gather();
+            sync();
+            st.t_sync += seconds_since(ts);
+        }
         if (hs_.balance.enabled && W_ > 1) {
             // every rank needs every partition's cost (runtime.cpp:674-675)
             const std::vector<double> all = distributed_ ? allgather_host(cost) : cost;
@@ -1813,8 +1871,9 @@ FrameStats Engine::frame_admm(int frame) {
         }
         sync();
         prof.mark(5, s_);
-        h_cur_ = std::min(hs_.params.h, 2.0 * h_cur_); // TimestepController::on_frame_committed
-        halvings_ = 0;
+        tsc_.on_frame_committed();
+        st.exact_retries = static_cast<int>(exact_retries_ - exact0);
+        st.capacity_retries = static_cast<int>(capacity_retries_ - cap0);
         st.committed = 1;
         return st;
     }

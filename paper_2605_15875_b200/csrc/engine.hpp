@@ -9,6 +9,7 @@
 #include "geometry.cuh"
 #include "kernels.hpp"
 #include "balance.hpp"
+#include "controller.hpp"
 #include "scene.hpp"
 #include "solver.hpp"
 
@@ -24,6 +25,12 @@ struct FrameStats {
     double h = 0.0;
     int admm_iterations = 0, newton_iterations = 0, line_search_steps = 0, pcg_iterations = 0;
     int max_contacts = 0, max_candidates = 0;
+    int exact_retries = 0;    // solves redone at the exact-solve PCG limit (line-search collapse)
+    int capacity_retries = 0; // work redone after a capacity grew (list / ELL width)
+    // host wall-clock seconds (runtime.cpp:117-124, 399-402, 466-475): local
+    // Newton solves, consensus + merge-gate collision work, waiting on
+    // exchanges with peer ranks, the whole frame (compute = frame - sync)
+    double t_solve = 0.0, t_coll = 0.0, t_sync = 0.0, t_frame = 0.0;
 };
 
 struct TraceRow {
@@ -165,13 +172,24 @@ class Engine {
     // global replicated state
     DBuf<double> q_, qd_, q_start_;
     std::vector<double> rho_carry_; // host, NaN = none
-    double h_cur_ = 0.0;
-    int halvings_ = 0;
+    TimestepController tsc_; // h of the next attempt (consensus.hpp:60-87)
     long long frame_counter_ = 0;
     std::vector<TraceRow> trace_;
     long long exact_retries_ = 0;       // Newton solves redone at the exact-solve PCG limit
-    const double* x_seen_ = nullptr;    // allocations of x_ / pbuf_ already zeroed
-    const double* pbuf_seen_ = nullptr;
+    long long capacity_retries_ = 0;    // frames / solves redone after a capacity grew
+    static constexpr int kMaxGrows = 8; // capacity doublings per frame before the overflow is an error
+    // restores the PCG limits a retry changed, on every exit path
+    struct SolverRestore {
+        Engine& e;
+        double tol;
+        int max;
+        explicit SolverRestore(Engine& en) : e(en), tol(en.pcg_tol_), max(en.pcg_max_) {}
+        ~SolverRestore() {
+            if (e.pcg_tol_ != tol || e.pcg_max_ != max) e.set_solver(tol, max);
+        }
+    };
+    DBuf<double> warm_prev_;            // previous instance set's (x, p2) while remapping
+    DBuf<int> warm_map_;
     std::vector<cudaStream_t> side_streams_; // per capture level: independent branches
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     // PD load balancer of the planes (runtime.cpp:537-552, 674-675)
@@ -191,6 +209,8 @@ class Engine {
     DBuf<uint32_t> bmask_;
     DBuf<double> rgrad_, rdiag_, rdinv_, rval_, x_, r_, z_, p0v_, p1v_, ap_, rowtmp_, rowtmp2_;
     DBuf<int> ell_cnt_, ell_col_;
+    int ell_w_ = kEll; // ELL width, doubled on kErrEll (a row coupling more bodies)
+    bool grow_capacity(int code); // kErrCapacity / kErrEll: grow, true if grown
     DBuf<double> ell_blk_;
     DBuf<PartState> ps_;
     PinnedBuf<PartState> ps_h_;

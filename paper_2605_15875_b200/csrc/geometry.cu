@@ -193,12 +193,51 @@ __global__ void __launch_bounds__(kEmitWarps * 32)
         }
         __syncwarp();
         const int np_raw = npart[warp];
-        if (np_raw > kMaxPartners && lane == 0 && err) raise(err, kErrCapacity);
+        // Partners of instance i: the shared-memory list, or (more than
+        // kMaxPartners, e.g. a large body resting on many small ones) the
+        // same hash cells and statics walked again warp-uniformly. Either way
+        // every partner is visited once; the keys are sorted afterwards, so
+        // the visiting order does not matter.
+        const bool spill = np_raw > kMaxPartners;
         const int np = min(np_raw, kMaxPartners);
+        auto for_each_partner = [&](auto&& fn) {
+            if (!valid) return;
+            if (!spill) {
+                for (int q = 0; q < np; ++q) fn(partners[warp][q]);
+                return;
+            }
+            const Box bi = box[i];
+            const int p = iv.part[i];
+            const long long cx0 = static_cast<long long>(floor(bi.lo.x * inv)) - 1;
+            const long long cy0 = static_cast<long long>(floor(bi.lo.y * inv)) - 1;
+            const long long cx1 = static_cast<long long>(floor(bi.hi.x * inv));
+            const long long cy1 = static_cast<long long>(floor(bi.hi.y * inv));
+            unsigned seen[9];
+            int nseen = 0;
+            for (int m = 0; m < 9; ++m) {
+                const long long cx = cx0 + m / 3, cy = cy0 + m % 3;
+                if (cx > cx1 || cy > cy1) continue;
+                const unsigned h = cell_hash(p, cx, cy, mask);
+                bool dup = false;
+                for (int u = 0; u < nseen; ++u) dup = dup || seen[u] == h;
+                if (dup) continue;
+                seen[nseen++] = h;
+                const int s0 = hstart[h], s1 = s0 + hcount[h];
+                for (int t = s0; t < s1; ++t) {
+                    const int j = items[t];
+                    if (j <= i || iv.part[j] != p || !overlaps(bi, box[j])) continue;
+                    fn(j);
+                }
+            }
+            for (int k = 0; k < n_stat; ++k) {
+                const int st = stat[k];
+                if (iv.part[st] != p || !overlaps(bi, box[st])) continue;
+                fn(st);
+            }
+        };
         // count pass
         int cnt = 0;
-        for (int q = 0; q < np; ++q) {
-            const int j = partners[warp][q];
+        for_each_partner([&](int j) {
             const int na = sc.vstart[iv.body[i] + 1] - sc.vstart[iv.body[i]];
             const int nb = sc.vstart[iv.body[j] + 1] - sc.vstart[iv.body[j]];
             const int combos = 2 * na * nb;
@@ -206,7 +245,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32)
                 unsigned long long k;
                 cnt += combo_test(sc, iv, sw, margin, i, j, c, fmt, k) ? 1 : 0;
             }
-        }
+        });
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
         if (lane == 0) wtot[warp] = cnt;
@@ -225,8 +264,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32)
         if (base >= 0) {
             int pos = base;
             for (int w = 0; w < warp; ++w) pos += wtot[w];
-            for (int q = 0; q < np; ++q) {
-                const int j = partners[warp][q];
+            for_each_partner([&](int j) {
                 const int na = sc.vstart[iv.body[i] + 1] - sc.vstart[iv.body[i]];
                 const int nb = sc.vstart[iv.body[j] + 1] - sc.vstart[iv.body[j]];
                 const int combos = 2 * na * nb;
@@ -238,7 +276,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32)
                     if (hit) out[pos + __popc(bal & ((1u << lane) - 1u))] = k;
                     pos += __popc(bal);
                 }
-            }
+            });
         }
         __syncthreads();
     }

@@ -201,13 +201,13 @@ __global__ void __launch_bounds__(kT) k_pcg(SolverView sv, PcgArgs a) {
             for (int k = 0; k < 6; ++k) y[k] += eps * pr[k];
             const int nb = sv.ell_cnt[r];
             for (int t = 0; t < nb; ++t) {
-                const int c = sv.ell_col[r * kEll + t];
+                const int c = sv.ell_col[r * sv.ell_w + t];
                 double pc[6], zc[6], yc[6];
                 ld6(pold + 6 * c, pc);
                 ld6(sv.z + 6 * c, zc);
 #pragma unroll
                 for (int k = 0; k < 6; ++k) pc[k] = zc[k] + beta * pc[k];
-                mv36(sv.ell_blk + (static_cast<size_t>(r) * kEll + t) * 36, pc, yc);
+                mv36(sv.ell_blk + (static_cast<size_t>(r) * sv.ell_w + t) * 36, pc, yc);
 #pragma unroll
                 for (int k = 0; k < 6; ++k) y[k] += yc[k];
             }
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         const int b0 = bstart[lr], nb = bstart[lr + 1] - b0;
         const int ncp = min(nb, cap_blocks - b0);
         const double2* d0 = reinterpret_cast<const double2*>(sv.rdiag + 36 * r);
-        const double2* o0 = reinterpret_cast<const double2*>(sv.ell_blk + static_cast<size_t>(r) * kEll * 36);
+        const double2* o0 = reinterpret_cast<const double2*>(sv.ell_blk + static_cast<size_t>(r) * sv.ell_w * 36);
         const unsigned dst = smem_u32(blk + 36 * b0);
         for (int c = lane; c < 18 * ncp; c += 32)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c),
@@ -515,12 +515,17 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             const int lr = lr0 + u * kCW;
             cv[u] = -1;
             if (lr < nr && lane < min(bstart[lr + 1] - bstart[lr], cap_blocks - bstart[lr]))
-                cv[u] = lane == 0 ? r0 + lr : sv.ell_col[(r0 + lr) * kEll + lane - 1];
+                cv[u] = lane == 0 ? r0 + lr : sv.ell_col[(r0 + lr) * sv.ell_w + lane - 1];
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (cv[u] >= 0) bcol[bstart[lr0 + u * kCW] + lane] = cv[u];
     }
+    if (sv.ell_w >= 32) // rows wider than a warp (grown ELL): the remaining columns
+        for (int lr = warp; lr < nr; lr += kCW) {
+            const int nb = min(bstart[lr + 1] - bstart[lr], cap_blocks - bstart[lr]);
+            for (int t = 32 + lane; t < nb; t += 32) bcol[bstart[lr] + t] = sv.ell_col[(r0 + lr) * sv.ell_w + t - 1];
+        }
     if constexpr (PH) cs[7] = clock64(); // staging issued
     // fused head, part 1 (overlaps the block copies): kOpEps with the trace
     // summed redundantly by every CTA of the partition in one fixed order
@@ -785,9 +790,9 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         }
         for (int s = bs; s < b1; ++s) { // spilled block
             const int r = r0 + lr, t = s - b0;
-            const int col = t == 0 ? r : sv.ell_col[r * kEll + t - 1];
+            const int col = t == 0 ? r : sv.ell_col[r * sv.ell_w + t - 1];
             const double* M = (t == 0 ? sv.rdiag + 36 * r
-                                      : sv.ell_blk + (static_cast<size_t>(r) * kEll + t - 1) * 36) + 6 * comp;
+                                      : sv.ell_blk + (static_cast<size_t>(r) * sv.ell_w + t - 1) * 36) + 6 * comp;
             const int crank = (col - R0) / chunk, cl_row = (col - R0) - crank * chunk;
             const double* v = cl.map_shared_rank(vm0, crank) + moff + 6 * cl_row;
             double ya = 0.0;
@@ -901,8 +906,9 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             sc.wsp[threadIdx.x] = t;
         }
         cluster_barrier(); // wsp of every CTA ready; every peer done reading vm0 / vm1
-        // one thread per CTA folds the csize CTA records (rank order; 6 x csize
-        // DSMEM loads per CTA, not per thread) and solves the 2x2 system
+        // one warp per CTA folds the csize CTA records: lane k loads CTA k's
+        // record (6 x csize DSMEM loads per CTA, not per thread), a fixed
+        // shuffle tree sums them, and lane 0 solves the 2x2 system
         if (warp == 0) { // lane k loads CTA k's record; fixed shuffle tree
             double tt[6];
 #pragma unroll
@@ -912,13 +918,17 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             const double b1 = tt[0], b2 = tt[1], a11 = tt[2], a12 = tt[3], a22 = tt[4];
             double c1 = 0.0, c2 = 0.0;
             const double det = a11 * a22 - a12 * a12;
+            bool two = false; // 2x2 Galerkin solution usable
             if (a.warm > 1 && a11 > 0.0 && a22 > 0.0 && det > 1e-8 * a11 * a22) {
                 c1 = (b1 * a22 - b2 * a12) / det;
                 c2 = (b2 * a11 - b1 * a12) / det;
-            } else if (a11 > 0.0) {
-                c1 = b1 / a11;
+                two = isfinite(c1) && isfinite(c2);
             }
-            if (!isfinite(c1) || !isfinite(c2)) c1 = c2 = 0.0;
+            if (!two) { // one-vector fallback; a non-finite p2 never enters it
+                c2 = 0.0;
+                c1 = a11 > 0.0 ? b1 / a11 : 0.0;
+                if (!isfinite(c1)) c1 = 0.0;
+            }
             if (lane == 0) {
                 sc.scal[0] = c1;
                 sc.scal[1] = c2;
@@ -928,11 +938,17 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         __syncthreads();
         const double c1 = sc.scal[0], c2 = sc.scal[1];
         bnorm2_ws = sc.scal[2];
-        if (c1 != 0.0 || c2 != 0.0) {
+        if (c2 != 0.0) {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 x[g] = c1 * p1[g] + c2 * p2[g];
                 r[g] -= c1 * ap1[g] + c2 * ap2[g];
+            }
+        } else if (c1 != 0.0) { // p2 / A p2 untouched: 0 * NaN never reaches x or r
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                x[g] = c1 * p1[g];
+                r[g] -= c1 * ap1[g];
             }
         }
         // (no trailing barrier: wsp is never rewritten in this launch, and the

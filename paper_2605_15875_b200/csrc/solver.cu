@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(kB) k_contact_select(SolverView sv, ContactVie
 }
 
 // ---------------------------------------------------------------------------
-// Deterministic BSR assembly (ELL storage, kEll off-diagonal blocks / row):
+// Deterministic BSR assembly (ELL storage, sv.ell_w off-diagonal blocks / row):
 // one warp per row, lane l owns entries l and l + 32 of each 6x6 block and
 // sums the contacts' precomputed DoF-space blocks (store_dof_blocks) in list
 // order: TL where the row's body is the point body, BR where it is the edge
@@ -818,12 +818,12 @@ __device__ __forceinline__ void assemble_row_fast(const SolverView& sv, const Co
         double o0 = 0.0, o1 = 0.0;
         add_blocks(cv, runa, ca, 72, e0, e1, has1, o0, o1, 0, lane, nullptr);
         add_blocks(cv, runb, cb, 72, t0, t1, has1, o0, o1, 0, lane, nullptr);
-        if (nblk >= kEll) {
-            if (lane == 0) raise(sv.err, kErrCapacity);
+        if (nblk >= sv.ell_w) {
+            if (lane == 0) raise(sv.err, kErrEll);
             break;
         }
-        if (lane == 0) sv.ell_col[r * kEll + nblk] = prow;
-        double* odst = sv.ell_blk + (static_cast<size_t>(r) * kEll + nblk) * 36;
+        if (lane == 0) sv.ell_col[r * sv.ell_w + nblk] = prow;
+        double* odst = sv.ell_blk + (static_cast<size_t>(r) * sv.ell_w + nblk) * 36;
         odst[e0] = o0;
         if (has1) odst[e1] = o1;
         ++nblk;
@@ -915,12 +915,12 @@ __global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv,
                 if (has1) o1 += bk[t1];
             }
             if (prow < 0) continue;
-            if (nblk >= kEll) {
-                if (lane == 0) raise(sv.err, kErrCapacity);
+            if (nblk >= sv.ell_w) {
+                if (lane == 0) raise(sv.err, kErrEll);
                 break;
             }
-            if (lane == 0) sv.ell_col[r * kEll + nblk] = prow;
-            double* odst = sv.ell_blk + (static_cast<size_t>(r) * kEll + nblk) * 36;
+            if (lane == 0) sv.ell_col[r * sv.ell_w + nblk] = prow;
+            double* odst = sv.ell_blk + (static_cast<size_t>(r) * sv.ell_w + nblk) * 36;
             odst[e0] = o0;
             if (has1) odst[e1] = o1;
             ++nblk;

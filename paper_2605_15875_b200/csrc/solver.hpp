@@ -12,7 +12,7 @@
 
 namespace dabd_gpu {
 
-constexpr int kEll = 24;   // max off-diagonal 6x6 blocks per BSR row
+constexpr int kEll = 24;   // initial off-diagonal 6x6 blocks per BSR row (SolverView::ell_w grows on kErrEll)
 constexpr int kMaxParts = 32;
 
 struct PartState {
@@ -85,8 +85,9 @@ struct SolverView {
     double* rdinv = nullptr;  // [R][36]
     double* rval = nullptr;   // [R]
     int* ell_cnt = nullptr;   // [R]
-    int* ell_col = nullptr;   // [R][kEll]
-    double* ell_blk = nullptr; // [R][kEll][36]
+    int* ell_col = nullptr;   // [R][ell_w]
+    double* ell_blk = nullptr; // [R][ell_w][36]
+    int ell_w = kEll;          // ELL width: coupling blocks a row can hold
     double* x = nullptr;      // dq [R][6]
     double* r = nullptr;
     double* z = nullptr;

@@ -422,6 +422,58 @@ def hetero_1000(seed: int = 13) -> SceneData:
                          name="hetero-1000")
 
 
+def hooks_c4(seed: int = 17) -> SceneData:
+    """C4: contact-rich non-convex bodies with 1000:1 mass
+    ratios across a two-partition interface. The reference has no 2D
+    "interlocking chains"; this uses its multi-loop / non-convex polygon
+    bodies (scene.cpp:212-217) instead (parity-unpinned geometry):
+      - a heavy U-shaped tray (non-convex, 8 vertices) spanning the x = 0
+        interface, so it is split, and whose bounding box holds every box in
+        it (> 96 broad-phase partners, > 24 coupled bodies in its BSR row);
+      - 200 small boxes in the tray whose densities alternate 1000 and 1
+        (1000:1 masses between neighbours), arap_scale proportional to mass
+        (1 for the light bodies, as the heterogeneous builtin);
+      - six U-hooks (density 1000) carrying one light peg each (density 1)
+        dropped onto the pile.
+    The U floors are thick enough that every loop centroid lies inside its
+    own loop: intersection_test's centroid probe (geometry.cpp:412-427)
+    assumes that, and would flag a cup holding a body otherwise.
+    """
+    s = SceneData(name="hooks-c4", frames=100, seed=seed)
+    s.params = SimParams(h=0.01, gravity=(0.0, -10.0), arap_stiffness=1e6,
+                         barrier_stiffness=1e4, d_hat=0.01, theta=1e-3, scene_scale=4.0)
+    s.planes = [Plane((0.0, 0.0), (-1.0, 0.0))]
+    s.w_min = 0.4
+    s.bodies.append(_container(4.4, 1.6))
+
+    def u_loop(cx, y0, hw, height, tf, tw):  # counter-clockwise U (cup opening up)
+        return [(cx - hw, y0), (cx + hw, y0), (cx + hw, y0 + height), (cx + hw - tw, y0 + height),
+                (cx + hw - tw, y0 + tf), (cx - hw + tw, y0 + tf), (cx - hw + tw, y0 + height),
+                (cx - hw, y0 + height)]
+
+    tray_y0, tray_tf = 0.015, 0.1
+    s.bodies.append(BodySpec(loops=[u_loop(0.0, tray_y0, 1.6, 0.5, tray_tf, 0.06)], density=100.0,
+                             arap_scale=1000.0))
+    rng = JitterRng(seed)
+    half, spacing, cols, rows = 0.03, 0.075, 40, 5
+    y_row0 = tray_y0 + tray_tf + 0.015 + half
+    for r in range(rows):
+        for c in range(cols):
+            heavy = (r + c) % 2 == 0
+            cx = -0.5 * (cols - 1) * spacing + spacing * c + rng.uniform(-0.002, 0.002)
+            cy = y_row0 + spacing * r + rng.uniform(-0.002, 0.002)
+            dens = 1000.0 if heavy else 1.0
+            s.bodies.append(BodySpec(loops=[box_loop((cx, cy), (half, half))], density=dens,
+                                     arap_scale=dens))
+    for k in range(6):
+        cx = -1.25 + 0.5 * k
+        s.bodies.append(BodySpec(loops=[u_loop(cx, 0.7, 0.2, 0.25, 0.09, 0.04)], density=1000.0,
+                                 arap_scale=1000.0))
+        s.bodies.append(BodySpec(loops=[box_loop((cx, 0.7 + 0.09 + 0.015 + 0.05), (0.05, 0.05))],
+                                 density=1.0, arap_scale=1.0))
+    return s
+
+
 _BUILTINS = {
     "funnel-analog": lambda seed: funnel_analog(1000.0, 7 if seed is None else seed),
     "drop-grid-1": lambda seed: drop_grid(1, 11 if seed is None else seed),
@@ -433,6 +485,7 @@ _BUILTINS = {
     "pour-10k": lambda seed: pour_10k(11 if seed is None else seed),
     "sweep-100k": lambda seed: sweep_100k(11 if seed is None else seed),
     "hetero-1000": lambda seed: hetero_1000(13 if seed is None else seed),
+    "hooks-c4": lambda seed: hooks_c4(17 if seed is None else seed),
 }
 
 
@@ -441,7 +494,7 @@ def scenario_names() -> List[str]:
     return ["funnel-analog", "drop-grid-1", "drop-grid-2", "drop-grid-4", "density-sweep-10",
             "density-sweep-100", "density-sweep-1000", "density-sweep-10000",
             "density-sweep-100000", "blocked-merge", "heterogeneous", "cubes-64", "pile-1k",
-            "pour-10k", "sweep-100k", "hetero-1000"]
+            "pour-10k", "sweep-100k", "hetero-1000", "hooks-c4"]
 
 
 def make_scenario(name: str, seed: Optional[int] = None) -> SceneData:

@@ -1,0 +1,151 @@
+"""Oracle parity at the configurations the bench and the north star run
+(BASELINE.json configs C2-C5), from states the GPU reached itself:
+
+- C2 pile-1k, run_reference semantics (sim.cpp:186-249) at the bench's own
+  solver settings (PCG to 1e-10 relative, warm-started): GPU and oracle start
+  from the same settled pile and step 5 frames side by side;
+- C3 pour-10k with 8 partitions, consensus-ADMM semantics
+  (runtime.cpp:110-694): ADMM traces (dq, r, s), merge-gate TOIs, iteration
+  counts and the final rho of two frames from a settled pour;
+- C5 sweep-100k: broad phase (plain and swept), holder masks and CCD
+  accept/reject bitwise at a settled state;
+- C4 hooks-c4: non-convex bodies, 1000:1 mass ratios across the interface, a
+  tray whose BSR row outgrows the initial ELL width.
+
+Tolerances are the north star's: states within 1e-6 (relative to the scene
+scale l), residual traces within 1e-6 h l, integer decisions exact.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_15875_b200 import api
+from paper_2605_15875_b200.scene import make_scenario
+
+pytestmark = pytest.mark.gpu
+
+TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000)
+
+
+def _settled(name, frames, **solver):
+    """The scene after `frames` run_reference frames on the GPU."""
+    sd = make_scenario(name)
+    ctx = api.Context(api.Scene(sd), **solver)
+    if frames:
+        ctx.run_frames(frames)
+    q, qd = ctx.state()
+    return sd, q, qd
+
+
+def test_pile_1k_bench_settings():
+    """C2 at the bench's settings: identical ADMM (k-loop) counts, no exact
+    retries, states within 1e-6 l of the oracle for 5 consecutive frames."""
+    sd, q, qd = _settled("pile-1k", 40)
+    ctx = api.Context(api.Scene(sd))  # defaults = bench.py (1e-10, warm start)
+    ctx.set_state(q, qd)
+    o = O.Scene(sd)
+    o.set_state(q, qd)
+    frames = 5
+    ref = o.run(frames, workers=0)
+    l = sd.params.scene_scale
+    for f in range(frames):
+        st = ctx.run_frames(1)[0]
+        qg, _ = ctx.state()
+        assert st["admm_iterations"] == ref["admm"][f], (f, st["admm_iterations"], ref["admm"][f])
+        assert st["exact_retries"] == 0 and st["capacity_retries"] == 0, (f, st)
+        err = np.abs(qg - ref["q"][f]).max()
+        assert err < 1e-6 * l, (f, err)
+
+
+@pytest.mark.slow
+def test_pour_10k_eight_partitions():
+    """C3: two consensus-ADMM frames of the 8-partition pour from a settled
+    state (rho carry empty on both sides): identical ADMM counts, sigma and
+    merge-gate TOIs, dq / r / s within 1e-6 h l, states within 1e-6 l, final
+    rho to 1e-12."""
+    sd, q, qd = _settled("pour-10k", 30)
+    frames = 2
+    ctx = api.Context(api.Scene(sd), num_workers=8, **TIGHT)
+    ctx.set_state(q, qd)
+    stats = [ctx.run_frames(1)[0] for _ in range(frames)]
+    qg, _ = ctx.state()
+    tr_g = ctx.take_trace()
+    o = O.Scene(sd)
+    o.set_state(q, qd)
+    ref = o.run(frames, workers=8)  # one oracle thread per worker (sim.cpp:281-322)
+    tr_o = ref["trace"]
+    norm = sd.params.h * sd.params.scene_scale
+    for f in range(frames):
+        assert stats[f]["admm_iterations"] == ref["admm"][f], (f, stats[f]["admm_iterations"], ref["admm"][f])
+        assert stats[f]["attempts"] == ref["attempts"][f]
+    assert tr_g.shape == tr_o.shape
+    assert np.array_equal(tr_g[:, [1, 2, 7]], tr_o[:, [1, 2, 7]])
+    assert np.array_equal(tr_g[:, 6], tr_o[:, 6])  # merge-gate TOIs, exact
+    for col in (3, 4, 5):
+        assert np.abs(tr_g[:, col] - tr_o[:, col]).max() < 1e-6 * norm, col
+    assert np.abs(qg - ref["q"][-1]).max() < 1e-6 * sd.params.scene_scale
+    rho_g = ctx.rho()
+    shared = ~np.isnan(ref["rho"])
+    assert shared.sum() > 100  # the interfaces of a settled pour carry many split bodies
+    assert np.array_equal(shared, ~np.isnan(rho_g))
+    assert np.allclose(rho_g[shared], ref["rho"][shared], rtol=1e-12)
+
+
+@pytest.mark.slow
+def test_sweep_100k_broad_phase_and_masks():
+    """C5 at a settled state: candidate lists (static and swept), holder masks
+    of the 8-slab partition and the CCD accept/reject decision are bitwise the
+    oracle's."""
+    sd, q, qd = _settled("sweep-100k", 8)
+    ctx = api.Context(api.Scene(sd))
+    o = O.Scene(sd)
+    d_hat = sd.params.d_hat
+    a = ctx.broad_phase(q, d_hat)
+    b = o.broad_phase(q, d_hat)
+    assert len(a) > 100000 and np.array_equal(a, b)
+    q1 = q + sd.params.h * qd
+    a = ctx.broad_phase(q, 0.0, q_end=q1)
+    b = o.broad_phase(q, 0.0, q_end=q1)
+    assert np.array_equal(a, b)
+    planes = np.array([[p.point[0], p.point[1], p.normal[0], p.normal[1]] for p in sd.planes])
+    w = max(2.0 * sd.params.h * float(np.abs(qd).max()) * 2.0, sd.w_min)
+    mg, mo = ctx.holder_masks(q, planes, w), o.holder_masks(q, planes, w)
+    assert np.array_equal(mg, mo)
+    assert (np.array([bin(int(m)).count("1") for m in mg[1:]]) == 2).sum() > 100
+    tg, to = ctx.ccd_toi(q, q1), o.ccd_toi(q, q1)
+    assert tg == to
+
+
+def test_hooks_c4_two_partitions():
+    """C4: consensus-ADMM parity over the first 8 frames (exact counts,
+    decisions and gate TOIs), then 30 GPU frames stay penetration-free; the
+    tray's BSR row outgrows the initial ELL width (24 coupled bodies) and
+    the engine grows it instead of failing."""
+    from test_gpu_admm import _compare
+
+    gpu, ref = _compare("hooks-c4", 2, 8, state_tol=1e-6, trace_tol=1e-5)
+    sd = make_scenario("hooks-c4")
+    ctx = api.Context(api.Scene(sd), num_workers=2)
+    st = ctx.run_frames(30)
+    assert all(s["committed"] for s in st)
+    assert sum(s["capacity_retries"] for s in st) >= 1
+    intersecting, violating, dmin = ctx.audit()
+    assert not intersecting and violating == 0 and dmin > 0.0
+
+
+def test_large_body_partner_spill():
+    """k_emit_warp keeps at most 96 broad-phase partners per body in shared
+    memory; the tray of hooks-c4 has ~200 boxes inside its bounding box, so
+    its candidates come from the spill path. Candidate lists stay bitwise
+    the oracle's."""
+    sd, q, _ = _settled("hooks-c4", 20)
+    ctx = api.Context(api.Scene(sd))
+    o = O.Scene(sd)
+    for margin in (sd.params.d_hat, 0.05):
+        a = ctx.broad_phase(q, margin)
+        b = o.broad_phase(q, margin)
+        assert np.array_equal(a, b)
+        assert len(np.unique(a[a[:, 0] == 1, 1])) + len(np.unique(a[a[:, 1] == 1, 0])) > 30

@@ -509,3 +509,78 @@ def test_two_worker_mse_and_blocked_merge():  # test_runtime.cpp:98-115, 146-159
     assert t["h"][0] < 0.02
     for f in range(3):
         assert not bm.intersection_test(t["q"][f])
+
+
+# ---------------------------------------------------------------- consensus (test_consensus.cpp)
+
+ADAPT6 = [1.0, 2.0, 5.0, 1e-3, 1e3, 1.0]  # params.hpp:26-41 defaults
+
+
+def test_consensus_update_closed_form():  # test_consensus.cpp:30-50
+    a, b = np.zeros(6), np.full(6, 4.0)
+    assert O.consensus_update([a, b], [2.0, 2.0])[0] == pytest.approx(2.0)
+    assert np.allclose(O.consensus_update([a, b], [1.0, 3.0]), 3.0)
+    r = np.random.default_rng(31).uniform(-2, 2, 6)
+    assert np.abs(O.consensus_update([r], [7.5]) - r).max() == pytest.approx(0.0, abs=1e-15)
+    with pytest.raises(O.OracleError):
+        O.consensus_update(np.zeros((0, 6)), [])
+    with pytest.raises(O.OracleError):
+        O.consensus_update([np.zeros(6)], [0.0])
+
+
+def test_stopping_rule():  # test_consensus.cpp:131-161
+    h, l, th = 0.01, 2.0, 1e-3
+    assert O.check_stopping(0, 0, 0, [1.0, 1.0], h, l, th)
+    assert not O.check_stopping(0, 0, 0, [1.0, 0.7], h, l, th)
+    at = th * h * l
+    assert not O.check_stopping(0, at, 0, [1.0], h, l, th)
+    assert O.check_stopping(0, np.nextafter(at, 0.0), 0, [1.0], h, l, th)
+    rng = np.random.default_rng(39)
+    for _ in range(200):
+        dq, r, s = rng.uniform(0, 2 * at, 3)
+        if not O.check_stopping(dq, r, s, [1.0], h, l, th):
+            continue
+        for m in range(3):
+            v = [dq, r, s]
+            v[m] *= rng.uniform()
+            assert O.check_stopping(*v, [1.0], h, l, th)
+
+
+def test_penalty_policy():  # test_consensus.cpp:163-187
+    assert O.init_rho(100.0, 1.0) == pytest.approx(100.0)
+    assert O.init_rho(100.0, 0.01) == pytest.approx(1.0)
+    prev = None
+    for beta in (0.01, 0.1, 1.0, 10.0, 100.0):
+        rho = O.init_rho(50.0, beta)
+        if prev:
+            assert rho / prev == pytest.approx(10.0)
+        prev = rho
+    with pytest.raises(O.OracleError):
+        O.init_rho(0.0, 1.0)
+    assert O.adapt_rho(1.0, 10.0, 1.0, ADAPT6, 1.0) == pytest.approx(2.0)
+    assert O.adapt_rho(1.0, 1.0, 10.0, ADAPT6, 1.0) == pytest.approx(0.5)
+    assert O.adapt_rho(1.0, 3.0, 3.0, ADAPT6, 1.0) == pytest.approx(1.0)
+    top, bottom = ADAPT6[4], ADAPT6[3]
+    assert O.adapt_rho(top, 100.0, 0.001, ADAPT6, 1.0) == pytest.approx(top)
+    assert O.adapt_rho(bottom, 0.001, 100.0, ADAPT6, 1.0) == pytest.approx(bottom)
+
+
+def test_adaptive_timestep_controller():  # test_consensus.cpp:246-261
+    h = O.timestep_apply(0.02, 4, [0, 0, 1, 1, 1])
+    assert list(h) == pytest.approx([0.01, 0.005, 0.01, 0.02, 0.02])
+    assert O.timestep_apply(0.02, 4, [0, 0, 0, 0])[-1] == pytest.approx(0.02 / 16)
+    with pytest.raises(O.OracleError):
+        O.timestep_apply(0.02, 4, [0, 0, 0, 0, 0])
+
+
+def test_contact_replication_counts():  # test_partition.cpp:107-123
+    s = O.Scene(scene_of([[square(0.2, (-2.0, 0.0))], [square(0.2, (-1.8, 0.5))], [square(0.2)],
+                          [square(0.2, (0.05, 0.5))], [square(0.2, (2.0, 0.0))]], density=1000.0))
+    m = s.holder_masks(s.q0, MID, 0.4)
+    assert list(m) == [1, 1, 3, 3, 2]
+    assert O.contact_replication(m[0], m[1]) == 1  # both internal to worker 0
+    assert O.contact_replication(m[2], m[3]) == 2  # both shared
+    assert O.contact_replication(m[0], m[2]) == 1  # internal vs shared
+    assert O.contact_replication(m[2], m[4]) == 1  # shared vs internal(1)
+    with pytest.raises(O.OracleError):
+        O.contact_replication(m[0], m[4])  # disjoint holders
