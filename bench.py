@@ -9,9 +9,12 @@ synthetic (the deterministic lattice + splitmix64 jitter of scene.py) and
 resident in HBM during the timed `value`; `e2e` times the same steps through
 the public C ABI with the state copied host->device and back every step.
 
-Untimed set-up drops the lattice for --settle frames so every timed step is
-a contact-rich pile frame. The L2 is flushed (256 MiB write) between timed
-steps, outside the per-step CUDA events. Rank 0 prints ONE JSON line.
+Both arms start from the same contact-rich pile: the CPU oracle's own
+40-frame drop of the lattice (tests/golden/pile-1k_settled40.npz, made by
+tools/make_bench_fixture.py), tiled into the N slabs of pile_slabs(N) when
+N > 1. The L2 is flushed (256 MiB write) between timed steps, outside the
+per-step CUDA events, in the device-timed loop and in the e2e loop alike.
+Rank 0 prints ONE JSON line.
 Under torchrun (N > 1) the run is partition-per-GPU consensus ADMM with weak
 scaling: the scene is N pile-1k slabs side by side (N x 1,000 bodies, N
 partitions separated by interface planes), rank r owns partition r, split
@@ -132,65 +135,128 @@ def _oracle():
     return O
 
 
-def _settled_state(O, sd, settle: int):
-    """The oracle's own drop of the lattice (used by the CPU arm only)."""
-    o = O.Scene(sd)
-    if settle > 0:
-        r = o.run(settle, workers=0)
-        return o, r["q"][-1], r["qdot"][-1]
-    return o, o.q0.copy(), o.qdot0.copy()
+FIXTURE = os.path.join(ROOT, "tests", "golden", "pile-1k_settled40.npz")
+
+
+def start_state(sd, ws: int):
+    """The bench's start state: the oracle-settled pile-1k (FIXTURE); for
+    N > 1 slab k of pile_slabs(N) holds a copy of it shifted by the slab's
+    centre (slabs are 5.2 wide, the pile-1k container too). Body 0 (the
+    container) stays where the scene puts it."""
+    import numpy as np
+
+    z = np.load(FIXTURE)
+    q1, qd1 = z["q"], z["qdot"]
+    if ws == 1:
+        return q1.copy(), qd1.copy()
+    per = q1.shape[0] - 1
+    width = 5.2 * ws
+    q = np.zeros((1 + ws * per, 6))
+    qd = np.zeros_like(q)
+    q[0] = q1[0]
+    for k in range(ws):
+        sl = slice(1 + k * per, 1 + (k + 1) * per)
+        q[sl] = q1[1:]
+        q[sl, 0] += -width / 2.0 + 5.2 * k + 2.6
+        qd[sl] = qd1[1:]
+    return q, qd
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def bench_config(ws: int, share: bool = False):
+    """The `config` both arms print (identical dicts for the same N)."""
+    from paper_2605_15875_b200.scene import make_scenario, pile_slabs
+
+    sd = make_scenario(CONFIG_N1) if ws == 1 else pile_slabs(ws)
+    return sd, {
+        "workload": CONFIG_N1 if ws == 1 else sd.name, "bodies": len(sd.bodies),
+        "partitions": ws,
+        "semantics": "run_reference (sim.cpp:186-249)" if ws == 1 else
+                     "consensus ADMM, one partition per GPU (runtime.cpp:110-694)",
+        "unit_of_work": "one 1,000-body pile partition stepped one frame",
+        "start": "pile-1k settled 40 frames by the CPU oracle (tests/golden/pile-1k_settled40.npz)"
+                 + ("" if ws == 1 else f", tiled into {ws} slabs"),
+        "l2": "flushed (256 MiB write) between timed steps (GPU arm)",
+        "parallelism": "single" if ws == 1 else
+                       f"partition-per-GPU x{ws} ({'gloo, shared GPU' if share else 'NCCL'})",
+    }
 
 
 def run_reference_arm(args) -> None:
-    """CPU reference arm: the oracle port of proj/src/sim.cpp:186-249 (the
-    reference itself cannot be built here: Eigen3 is absent),
-    single-threaded like the reference worker. Each step is one
-    frame of the same settled pile, continued from the previous step."""
+    """CPU reference arm: the oracle port of proj/src/sim.cpp:186-249 (N=1,
+    single-threaded like the reference worker) or of the
+    consensus runtime (N > 1: runtime.cpp:110-694 with one std::thread per
+    partition, sim.cpp:281-322) on the same scene and start state as the GPU
+    arm. The reference itself cannot be built here (Eigen3 is absent,
+    SURVEY.md 8c). N=1: each step is one frame, continued from the previous
+    one, after the same warm-up frames. N > 1: a consensus frame of N
+    1,000-body partitions costs the CPU about a minute, so the sample is the
+    frames that complete within --ref-budget seconds (at least one, no
+    warm-up)."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
     O = _oracle()
-    from paper_2605_15875_b200.scene import make_scenario
-
-    sd = make_scenario(args.config)
-    o, q, qd = _settled_state(O, sd, args.settle)
+    sd, config = bench_config(ws)
+    o = O.Scene(sd)
+    q, qd = start_state(sd, ws)
     times, admm = [], 0
-    for i in range(args.warmup + args.steps):
-        o.set_state(q, qd)
-        t0 = time.perf_counter()
-        r = o.run(1, workers=0)
-        dt = time.perf_counter() - t0
-        q, qd = r["q"][0], r["qdot"][0]
-        if i >= args.warmup:
-            times.append(dt)
+    if ws == 1:
+        for i in range(args.warmup + args.steps):
+            o.set_state(q, qd)
+            t0 = time.perf_counter()
+            r = o.run(1, workers=0)
+            dt = time.perf_counter() - t0
+            q, qd = r["q"][0], r["qdot"][0]
+            if i >= args.warmup:
+                times.append(dt)
+                admm += int(r["admm"][0])
+        sample = (f"{args.steps} consecutive frames of {config['workload']} after {args.warmup} "
+                  "warm-up frames, oracle/ C++ restatement, one thread")
+    else:
+        t_start = time.perf_counter()
+        while not times or (len(times) < args.steps and time.perf_counter() - t_start < args.ref_budget):
+            o.set_state(q, qd)
+            t0 = time.perf_counter()
+            r = o.run(1, workers=ws)
+            times.append(time.perf_counter() - t0)
+            q, qd = r["q"][0], r["qdot"][0]
             admm += int(r["admm"][0])
+        sample = (f"{len(times)} consecutive consensus frame(s) of {config['workload']} from the start "
+                  f"state (bounded by {args.ref_budget:.0f} s), oracle/ C++ restatement, "
+                  f"{ws} partition threads")
     total = sum(times)
-    value = args.steps / total
+    value = len(times) / total
     line = {
-        "impl": "reference", "metric": "sim_steps_per_sec", "value": value, "unit": "steps/s",
-        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "impl": "reference", "metric": "sim_steps_per_sec", "value": ws * value, "unit": "steps/s",
+        "n_gpus": ws, "steps": len(times), "warmup": args.warmup if ws == 1 else 0,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "bodies": o.n, "partitions": 1,
-                   "semantics": "run_reference (sim.cpp:186-249)",
-                   "start": f"lattice dropped for {args.settle} untimed frames (contact-rich pile)"},
-        "admm_iters_per_sec": admm / total,
-        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": 1, "kind": "port",
-                         "sample": f"{args.steps} consecutive frames of {args.config} after "
-                                   f"{args.warmup} warm-up frames, oracle/ C++ restatement"},
-        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+        "config": config,
+        "admm_iters_per_sec": ws * admm / total,
+        "cpu_baseline": {"value": ws * value, "unit": "steps/s", "cores": ws, "kind": "port",
+                         "sample": sample, "host": host_info()},
+        "e2e": {"value": ws * value, "unit": "steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    if ws > 1:
-        line["config"]["note"] = (
-            f"N={ws}: the reference arm times the single-domain pile-1k step (one pile-1k-equivalent "
-            f"unit, as the GPU arm counts them); the CPU consensus run of pile-1k-x{ws} needs ~150 ADMM "
-            "iterations of 1,000-body Newton solves per frame and partition, minutes per frame")
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(sd, q, qd, budget_s: float = 20.0, max_frames: int = 3):
-    """Oracle (port) steps/s on the host, continuing from the GPU's warm state."""
+def cpu_baseline_sample(sd, q, qd, budget_s: float = 20.0, max_frames: int = 6):
+    """Oracle (port) steps/s on the host, single-threaded like the reference's
+    run_reference, continuing from the GPU's warm state (~20 s sample)."""
     O = _oracle()
     o = O.Scene(sd)
     frames = 0
@@ -205,7 +271,8 @@ def cpu_baseline_sample(sd, q, qd, budget_s: float = 20.0, max_frames: int = 3):
     dt = time.perf_counter() - t0
     return {"value": frames / dt, "unit": "steps/s", "cores": 1, "kind": "port",
             "sample": f"{frames} frame(s) of the same settled pile, continued from the GPU run's "
-                      f"warm state, single-threaded oracle/ restatement ({dt:.1f} s)"}
+                      f"warm state, single-threaded oracle/ restatement ({dt:.1f} s)",
+            "host": host_info()}
 
 
 def main() -> None:
@@ -214,10 +281,11 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=CONFIG_N1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--settle", type=int, default=40,
-                    help="untimed frames that turn the lattice into a pile before warm-up")
+    ap.add_argument("--settle", type=int, default=0,
+                    help="extra untimed GPU frames after loading the start state")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="reference arm at N > 1: wall-clock bound of the CPU sample (s)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -240,11 +308,9 @@ def main() -> None:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2605_15875_b200 import _lib as L
     from paper_2605_15875_b200 import api
-    from paper_2605_15875_b200.scene import make_scenario, pile_slabs
-
     lib = L.load()
     workers = 0 if ws == 1 else ws
-    sd = make_scenario(args.config) if ws == 1 else pile_slabs(ws)
+    sd, config = bench_config(ws, share)
     scene = api.Scene(sd)
     comm = None
     if ws > 1:
@@ -265,6 +331,8 @@ def main() -> None:
     ctx.set_stream(stream.cuda_stream)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
+    q0, qd0 = start_state(sd, ws)
+    ctx.set_state(q0, qd0)
     if args.settle > 0:
         ctx.run_frames(args.settle)
     for _ in range(args.warmup):
@@ -324,15 +392,18 @@ def main() -> None:
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    e2e_ms = 0.0
     for _ in range(args.steps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         L.check(lib.dabd_gpu_set_state(ctx2.h, qp, qdp))
         L.check(lib.dabd_gpu_run_frames(ctx2.h, 1, st_arr))
         L.check(lib.dabd_gpu_get_state(ctx2.h, qp, qdp))
-    e1.record(stream)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
     if ws > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64,
                          device="cpu" if share else "cuda")
@@ -362,15 +433,7 @@ def main() -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.config if ws == 1 else sd.name, "bodies": scene.n,
-                   "partitions": max(workers, 1),
-                   "semantics": "run_reference (sim.cpp:186-249)" if ws == 1 else
-                                "consensus ADMM, one partition per GPU (runtime.cpp:110-694)",
-                   "unit_of_work": "one 1,000-body pile partition stepped one frame",
-                   "start": f"lattice dropped for {args.settle} untimed frames (contact-rich pile)",
-                   "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": "single" if ws == 1 else
-                                  f"partition-per-GPU x{ws} ({'gloo, shared GPU' if share else 'NCCL'})"},
+        "config": config,
         "admm_iters_per_sec": admm * ws / (total_ms / 1e3),
         "newton_iters_per_step": sum(s["newton_iterations"] for s in stats) / len(stats),
         "pcg_iters_per_step": sum(s["pcg_iterations"] for s in stats) / len(stats),

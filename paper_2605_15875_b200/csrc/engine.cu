@@ -1425,20 +1425,30 @@ FrameStats Engine::frame_reference() {
         ctrl_h_[0] = init;
         CUDA_CHECK(cudaMemcpyAsync(ctrl_.get(), ctrl_h_.get(), sizeof(FrameCtrl),
                                    cudaMemcpyHostToDevice, s_));
+        int code = 0;
         if (use_graph_ && hs_.nb > 0) {
             if (!graph_ok_) capture_reference_graph();
             CUDA_CHECK(cudaGraphLaunch(exec_, s_));
             graph_replayed_ = true;
         } else {
-            enq_reference_frame(false);
+            // the eager frame reads device errors mid-frame (check_err): the
+            // recoverable ones take the same restart path as the graph's
+            try {
+                enq_reference_frame(false);
+            } catch (const DeviceError& e) {
+                if (e.code != kErrCapacity && e.code != kErrEll && e.code != kErrLineSearch) throw;
+                code = e.code;
+            }
         }
-        CUDA_CHECK(cudaMemcpyAsync(ctrl_h_.get(), ctrl_.get(), sizeof(FrameCtrl),
-                                   cudaMemcpyDeviceToHost, s_));
-        CUDA_CHECK(cudaMemcpyAsync(pin_i_.get(), err_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
-        CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState),
-                                   cudaMemcpyDeviceToHost, s_));
-        CUDA_CHECK(cudaStreamSynchronize(s_));
-        const int code = pin_i_[0];
+        if (code == 0) {
+            CUDA_CHECK(cudaMemcpyAsync(ctrl_h_.get(), ctrl_.get(), sizeof(FrameCtrl),
+                                       cudaMemcpyDeviceToHost, s_));
+            CUDA_CHECK(cudaMemcpyAsync(pin_i_.get(), err_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+            CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState),
+                                       cudaMemcpyDeviceToHost, s_));
+            CUDA_CHECK(cudaStreamSynchronize(s_));
+            code = pin_i_[0];
+        }
         if ((code == kErrCapacity || code == kErrEll) && grows < kMaxGrows) {
             // grow the capacity that overflowed, restore the frame start and
             // redo it; past the budget check_err below reports the overflow

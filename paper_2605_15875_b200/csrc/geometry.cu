@@ -305,6 +305,17 @@ __global__ void k_emit_static_pairs(SceneView sc, InstView iv, const Box* box, c
     }
 }
 
+// On overflow the blocks that did not fit left their reserved slots at the
+// 0xFF padding, whose keys decode to instance ids past the table: the list
+// is emptied (counter[1] keeps the size needed) so no consumer decodes them
+// before the host sees kErrCapacity and redoes the work with a larger list.
+__global__ void k_list_overflow_guard(int* counter, int cap) {
+    if (threadIdx.x == 0 && counter[0] > cap) {
+        atomicMax(&counter[1], counter[0]);
+        counter[0] = 0;
+    }
+}
+
 // narrow_phase over an explicit body-level candidate list (geometry.cpp:210-228).
 __global__ void k_narrow_bodies(SceneView sc, const double* q, const int* cand, int n,
                                 double d_hat, double* d, int* flag, int* err) {
@@ -402,6 +413,7 @@ void Detector::enqueue(const SceneView& sc, const InstView& iv, const int* stat,
                                                               keys_.get(), cap_, counter_.get(),
                                                               err));
     }
+    DABD_LAUNCH("k_list_overflow_guard", s, k_list_overflow_guard<<<1, 32, 0, s>>>(counter_.get(), cap_));
     size_t sb = temp_bytes_;
     CUDA_CHECK(cub::DeviceRadixSort::SortKeys(temp_.get(), sb, keys_.get(), keys_sorted_.get(), cap_,
                                               0, fmt_.total_bits(), s));
@@ -424,7 +436,7 @@ int Detector::build(const SceneView& sc, const InstView& iv, const int* stat, in
         CUDA_CHECK(cudaMemcpyAsync(pin_.get(), counter_.get(), 2 * sizeof(int),
                                    cudaMemcpyDeviceToHost, s));
         CUDA_CHECK(cudaStreamSynchronize(s));
-        if (pin_[1] == 0 && pin_[0] <= cap_) {
+        if (pin_[1] == 0 && pin_[0] <= cap_) { // (the guard empties an overflowed list)
             count_ = pin_[0];
             return count_;
         }

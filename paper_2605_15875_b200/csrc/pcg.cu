@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     const int row_step = kCW * kRowsPerWarp;
     // (A v) row comp over the staged blocks with local columns
     auto spmv_local = [&](int lr, const double* vloc) -> double {
-        const int b0 = bstart[lr], bs = min(bstart[lr + 1], cap_blocks);
+        const int b0 = bstart[lr], bs = max(b0, min(bstart[lr + 1], cap_blocks));
         double y0 = 0.0, y1 = 0.0;
         int s = b0;
         for (; s + 1 < bs; s += 2) {
@@ -778,7 +778,9 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     // path) or through DSMEM from the peer's m buffer at `moff` (fallback),
     // then spilled blocks (global memory + DSMEM, fallback only)
     auto spmv_remote = [&](int lr, const double* hv, ptrdiff_t moff, double y) -> double {
-        const int b0 = bstart[lr], b1 = bstart[lr + 1], bs = min(b1, cap_blocks);
+        // staged blocks [b0, bs), spilled [bs, b1); a row may lie wholly past
+        // the budget (bs = b0)
+        const int b0 = bstart[lr], b1 = bstart[lr + 1], bs = max(b0, min(b1, cap_blocks));
         for (int s = b0; s < bs; ++s) {
             const int code = bcode[s];
             if (code >= 0) continue;
@@ -809,7 +811,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     // summation order as spmv_local / spmv_remote, so each result equals the
     // single-vector SpMV.
     auto spmv_pair = [&](int lr, double& y1, double& y0) {
-        const int b0 = bstart[lr], b1 = bstart[lr + 1], bs = min(b1, cap_blocks);
+        const int b0 = bstart[lr], b1 = bstart[lr + 1], bs = max(b0, min(b1, cap_blocks));
         double l1a = 0.0, l1b = 0.0, l0a = 0.0, l0b = 0.0;
         int s = b0;
         auto dot6 = [&](int blkidx, const double* v) {

@@ -30,10 +30,11 @@ pytestmark = pytest.mark.gpu
 TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000)
 
 
-def _settled(name, frames, **solver):
-    """The scene after `frames` run_reference frames on the GPU."""
+def _settled(name, frames, workers=0, **solver):
+    """The scene after `frames` GPU frames (run_reference, or consensus ADMM
+    over `workers` partitions)."""
     sd = make_scenario(name)
-    ctx = api.Context(api.Scene(sd), **solver)
+    ctx = api.Context(api.Scene(sd), num_workers=workers, **solver)
     if frames:
         ctx.run_frames(frames)
     q, qd = ctx.state()
@@ -62,12 +63,25 @@ def test_pile_1k_bench_settings():
 
 @pytest.mark.slow
 def test_pour_10k_eight_partitions():
-    """C3: two consensus-ADMM frames of the 8-partition pour from a settled
-    state (rho carry empty on both sides): identical ADMM counts, sigma and
-    merge-gate TOIs, dq / r / s within 1e-6 h l, states within 1e-6 l, final
-    rho to 1e-12."""
+    """C3: one consensus-ADMM frame of the 8-partition pour from a state the
+    8-partition GPU run reached (rho carry empty on both sides, as at the
+    start of a run): identical ADMM counts, attempts and sigma decisions,
+    identical merge-gate accept/reject decisions with the TOI values within
+    1e-9 relative, dq / r / s within 1e-6 h l, states within 1e-6 l, final
+    rho to 1e-12.
+
+    The gate TOIs are bit-exact on identical inputs (test_gpu_geometry); here
+    they are evaluated at ADMM iterates that agree with the oracle's to the
+    PCG's rounding, not bitwise, so their values carry that rounding."""
+    # the lattice lands after ~20 frames; 30 single-domain frames make a
+    # contact-rich pile, then 2 consensus frames on 8 partitions (the first
+    # split of a settled pile halves h four times) reach an 8-partition state
     sd, q, qd = _settled("pour-10k", 30)
-    frames = 2
+    ctx = api.Context(api.Scene(sd), num_workers=8)
+    ctx.set_state(q, qd)
+    ctx.run_frames(2)
+    q, qd = ctx.state()
+    frames = 1
     ctx = api.Context(api.Scene(sd), num_workers=8, **TIGHT)
     ctx.set_state(q, qd)
     stats = [ctx.run_frames(1)[0] for _ in range(frames)]
@@ -83,13 +97,17 @@ def test_pour_10k_eight_partitions():
         assert stats[f]["attempts"] == ref["attempts"][f]
     assert tr_g.shape == tr_o.shape
     assert np.array_equal(tr_g[:, [1, 2, 7]], tr_o[:, [1, 2, 7]])
-    assert np.array_equal(tr_g[:, 6], tr_o[:, 6])  # merge-gate TOIs, exact
+    assert np.array_equal(tr_g[:, 6] == 1.0, tr_o[:, 6] == 1.0)  # merge-gate accept/reject
+    toi_rel = np.abs(tr_g[:, 6] - tr_o[:, 6]) / tr_o[:, 6]
+    assert toi_rel.max() < 1e-9, toi_rel.max()
     for col in (3, 4, 5):
-        assert np.abs(tr_g[:, col] - tr_o[:, col]).max() < 1e-6 * norm, col
+        err = np.abs(tr_g[:, col] - tr_o[:, col]).max()
+        assert err < 1e-6 * norm, (col, err)
     assert np.abs(qg - ref["q"][-1]).max() < 1e-6 * sd.params.scene_scale
     rho_g = ctx.rho()
     shared = ~np.isnan(ref["rho"])
     assert shared.sum() > 100  # the interfaces of a settled pour carry many split bodies
+    assert stats[0]["admm_iterations"] > 3 and stats[0]["max_contacts"] > 10000
     assert np.array_equal(shared, ~np.isnan(rho_g))
     assert np.allclose(rho_g[shared], ref["rho"][shared], rtol=1e-12)
 
@@ -126,7 +144,11 @@ def test_hooks_c4_two_partitions():
     the engine grows it instead of failing."""
     from test_gpu_admm import _compare
 
-    gpu, ref = _compare("hooks-c4", 2, 8, state_tol=1e-6, trace_tol=1e-5)
+    # 1000:1 mass ratios: the Newton systems are ill-conditioned enough that
+    # a 1e-12 relative PCG residual leaves ~1e-5 h l of difference to the
+    # reference's exact LDL^T step, so the PCG runs at the exact-solve limit
+    gpu, ref = _compare("hooks-c4", 2, 8, state_tol=1e-6, trace_tol=1e-5,
+                        pcg_rel_tol=1e-14, pcg_max_iters=50000)
     sd = make_scenario("hooks-c4")
     ctx = api.Context(api.Scene(sd), num_workers=2)
     st = ctx.run_frames(30)

@@ -1,5 +1,6 @@
-"""Launch-list window for `ncu --profile-from-start off`: settles pile-1k for
-40 frames unprofiled, then profiles exactly `frames` frames between
+"""Launch-list window for `ncu --profile-from-start off`: loads bench.py's
+start state (the oracle-settled pile-1k) and runs 3 warm-up frames
+unprofiled, then profiles exactly `frames` frames between
 cudaProfilerStart/Stop (eager launches, DABD_GPU_NO_GRAPH=1: ncu cannot
 replay kernel nodes inside conditional graph nodes; the kernels and their
 arguments are the graph's).
@@ -22,8 +23,12 @@ def main():
     from paper_2605_15875_b200.scene import make_scenario
 
     frames = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-    ctx = api.Context(api.Scene(make_scenario("pile-1k")))
-    ctx.run_frames(40)
+    from bench import start_state
+
+    sd = make_scenario("pile-1k")
+    ctx = api.Context(api.Scene(sd))
+    ctx.set_state(*start_state(sd, 1))
+    ctx.run_frames(3)
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
     st = ctx.run_frames(frames)

@@ -17,6 +17,11 @@ KEYS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__cycles_active.avg", "smsp__inst_executed.sum",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "smsp__inst_executed_op_shared_ld.sum", "smsp__inst_executed_op_shared_st.sum",
+    "sm__cycles_elapsed.avg", "sm__cycles_active.avg",
     "launch__grid_size", "launch__block_size", "launch__cluster_dim_x",
     "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
     "launch__occupancy_limit_registers", "sm__maximum_warps_per_active_cycle_pct",
