@@ -408,7 +408,9 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_pcg_perf(dabd_gpu_ctx* ctx, int reset,
  * SpMV + recurrences, [7] iterations counted, [8] setup (staging, fused
  * preconditioner, exchange plan) and [9] epilogue cycles per launch, summed,
  * [10..15] setup sub-phases (staging issue + first cluster barrier, exchange
- * plan, staging wait, plan barrier, eps + factor, init). cycles: 16 doubles. */
+ * plan, staging wait, plan barrier, eps + factor, init), [16..19] init
+ * sub-phases (eps + send plan, warm start, u = Dinv r + cluster barrier,
+ * initial SpMV + m). cycles: 24 doubles. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_pcg_phases(dabd_gpu_ctx* ctx, int reset, double* cycles);
 /* Skin-list counters of the local solve (no reference counterpart; the
  * reference runs a fresh broad phase per detect, geometry.cpp:161-208):

@@ -809,7 +809,7 @@ dabd_gpu_status dabd_gpu_ctx_pcg_phases(dabd_gpu_ctx* ctx, int reset, double* cy
     if (!ctx || !cycles) return null_arg();
     return guarded([&] {
         const dabd_gpu::DevPerf p = ctx->e->read_perf(reset != 0);
-        for (int k = 0; k < 16; ++k) cycles[k] = static_cast<double>(p.phase[k]);
+        for (int k = 0; k < 24; ++k) cycles[k] = static_cast<double>(p.phase[k]);
         return DABD_GPU_OK;
     });
 }

@@ -143,7 +143,15 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     trace_dev_.resize(8 * static_cast<size_t>(trace_cap_));
     qd_start_.resize(6 * std::max(hs_.nb, 1));
     if (const char* e = std::getenv("DABD_GPU_NO_GRAPH")) use_graph_ = e[0] == '0';
-    if (const char* e = std::getenv("DABD_GPU_PCG_PHASES")) pcg_phases_ = e[0] == '1';
+    if (const char* e = std::getenv("DABD_GPU_PCG_PHASES")) {
+        // "1": CTA 0 / warp 0; "1:<cta>:<warp>": the timed thread is lane 0
+        // of that warp of that CTA (per-CTA timelines, tools/pcg_phases.py)
+        int cta = 0, w = 0;
+        if (e[0] == '1') {
+            std::sscanf(e, "1:%d:%d", &cta, &w);
+            pcg_phases_ = 1 + 256 * cta + 16 * w;
+        }
+    }
     {
         int carve = -1; // driver default unless asked (experiment: DABD_GPU_CARVEOUT=100)
         if (const char* e = std::getenv("DABD_GPU_CARVEOUT")) carve = std::atoi(e);

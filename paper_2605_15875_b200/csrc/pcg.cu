@@ -76,6 +76,9 @@ struct PcgArgs {
     // previous solve's solution (sv.x); 2 = x0 the Galerkin solution over the
     // previous two solutions (sv.x and pa, which the kernel rotates); 0 = off
     int warm;
+    int min_rows; // rows per CTA the cluster size aims for (>= min_rows per CTA)
+    int spread;   // 1: every warp sends to one peer (partials + halo), 0: one warp sends to all
+    int fold_all; // 1: every warp folds the cluster partials itself, 0: the scalar warp folds
 };
 
 // Block-local, partition-segmented sum of rowval over this block's chunk,
@@ -404,7 +407,7 @@ template <int G, bool PH>
 __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, int csize, int cmax_rows) {
     cg::cluster_group cl = cg::this_cluster();
     const unsigned long long c_start = PH ? clock64() : 0ull;
-    unsigned long long cs[8] = {};
+    unsigned long long cs[8] = {}, ci[4] = {};
     unsigned long long t_start = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     extern __shared__ __align__(16) unsigned char smem[];
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     // on which other partitions share the launch or the GPU. Surplus CTAs
     // get no rows and send exact zeros.
     int cs_p = 1;
-    while (cs_p < csize && cs_p * 32 < R1 - R0) cs_p *= 2;
+    while (cs_p < csize && cs_p * a.min_rows < R1 - R0) cs_p *= 2;
     const int chunk = max(1, (R1 - R0 + cs_p - 1) / cs_p);
     const int r0 = min(R1, R0 + rank * chunk), r1 = min(R1, r0 + chunk);
     const int nr = r1 - r0;
@@ -867,6 +870,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         x[g] = z[g] = qv[g] = sv_[g] = pv[g] = 0.0;
     }
     double bnorm2_ws = -1.0; // ||b||^2 when the warm start computed it
+    if constexpr (PH) ci[0] = clock64();
     if (a.warm) {
         // x0 in span{p1, p2}, the previous two solves' solutions (sv.x and
         // a.pa), by the Galerkin condition: [p_i . A p_j] c = [p_i . b] (2x2,
@@ -956,6 +960,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         // (no trailing barrier: wsp is never rewritten in this launch, and the
         // barrier above already ordered every peer's reads of vm0 / vm1)
     }
+    if constexpr (PH) ci[1] = clock64();
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         double uu = 0.0;
@@ -968,6 +973,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         if (on[g]) vm1[6 * lrg[g] + comp] = uu;
     }
     cluster_barrier();
+    if constexpr (PH) ci[2] = clock64();
 #pragma unroll
     for (int g = 0; g < G; ++g)
         w[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, spmv_local(lrg[g], vm1)) : 0.0;
@@ -1001,7 +1007,9 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     bool done = !act;
     double inv_gamma_old = 0.0, inv_alpha_old = 0.0, bnorm2 = 0.0;
     int it = 0;
-    const bool timed = PH && sv.perf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    const int ph_at = sv.pcg_phases - 1; // 256 * CTA + 16 * warp of the timed thread
+    const bool timed = PH && sv.perf != nullptr && static_cast<int>(blockIdx.x) == (ph_at >> 8) &&
+                       static_cast<int>(threadIdx.x) == 32 * ((ph_at >> 4) & 15);
     unsigned long long ph[10] = {}, tc = PH ? clock64() : 0ull;
     if constexpr (PH) ph[8] = tc - c_start;
     auto mark = [&](int k) {
@@ -1041,7 +1049,11 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         mark(0);
         __syncthreads(); // red[] and this CTA's m (mcur) complete
         mark(1);
-        if (warp == kSW) { // the scalar warp: CTA tree and push to every peer
+        if (a.spread) {
+            // every warp folds the CTA's partials (same fixed tree in every
+            // warp) and warp k sends them, plus the halo rows consumer k
+            // needs, to peer k: one remote store pair and one bulk copy per
+            // warp instead of csize of each serialised in one warp
             double t0 = lane < kCW ? sc.red[lane][0] : 0.0;
             double t1 = lane < kCW ? sc.red[lane][1] : 0.0;
             double t2 = lane < kCW ? sc.red[lane][2] : 0.0;
@@ -1051,33 +1063,70 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 t1 += __shfl_xor_sync(0xffffffffu, t1, off);
                 t2 += __shfl_xor_sync(0xffffffffu, t2, off);
             }
-            if (lane < csize) {
-                if (push) {
-                    const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), lane);
-                    const unsigned pbar = mapa(bar, lane);
-                    st_async2(dst, t0, t1, pbar);
-                    st_async2(dst + 16, t2, 0.0, pbar);
-                } else {
-                    double* d = &cl.map_shared_rank(&sc, lane)->tab[par][rank][0];
-                    d[0] = t0;
-                    d[1] = t1;
-                    d[2] = t2;
+            if (warp < csize) {
+                if (lane == 0) {
+                    if (push) {
+                        const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), warp);
+                        const unsigned pbar = mapa(bar, warp);
+                        st_async2(dst, t0, t1, pbar);
+                        st_async2(dst + 16, t2, 0.0, pbar);
+                    } else {
+                        double* d = &cl.map_shared_rank(&sc, warp)->tab[par][rank][0];
+                        d[0] = t0;
+                        d[1] = t1;
+                        d[2] = t2;
+                    }
+                } else if (lane == 1 && bulk) {
+                    const int2 rq = sc.req[warp];
+                    if (rq.y > 0) {
+                        const unsigned dst = mapa(smem_u32(halo + 6 * (par * cap_blocks + sc.reqbase[warp])), warp);
+                        asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                     ::"r"(dst), "r"(smem_u32(mcur + 6 * rq.x)), "r"(48u * rq.y),
+                                     "r"(mapa(bar, warp))
+                                     : "memory");
+                    }
                 }
             }
-        }
-        if (bulk) { // per consumer one bulk DSMEM copy of the row range it needs
-            if (warp == 1 && lane < csize) {
-                const int2 rq = sc.req[lane];
-                if (rq.y > 0) {
-                    const unsigned dst = mapa(smem_u32(halo + 6 * (par * cap_blocks + sc.reqbase[lane])), lane);
-                    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                                 ::"r"(dst), "r"(smem_u32(mcur + 6 * rq.x)), "r"(48u * rq.y),
-                                 "r"(mapa(bar, lane))
-                                 : "memory");
-                }
-            }
+            if (!bulk) cluster_arrive();
         } else {
-            cluster_arrive();
+            if (warp == kSW) { // the scalar warp: CTA tree and push to every peer
+                double t0 = lane < kCW ? sc.red[lane][0] : 0.0;
+                double t1 = lane < kCW ? sc.red[lane][1] : 0.0;
+                double t2 = lane < kCW ? sc.red[lane][2] : 0.0;
+    #pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    t0 += __shfl_xor_sync(0xffffffffu, t0, off);
+                    t1 += __shfl_xor_sync(0xffffffffu, t1, off);
+                    t2 += __shfl_xor_sync(0xffffffffu, t2, off);
+                }
+                if (lane < csize) {
+                    if (push) {
+                        const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), lane);
+                        const unsigned pbar = mapa(bar, lane);
+                        st_async2(dst, t0, t1, pbar);
+                        st_async2(dst + 16, t2, 0.0, pbar);
+                    } else {
+                        double* d = &cl.map_shared_rank(&sc, lane)->tab[par][rank][0];
+                        d[0] = t0;
+                        d[1] = t1;
+                        d[2] = t2;
+                    }
+                }
+            }
+            if (bulk) { // per consumer one bulk DSMEM copy of the row range it needs
+                if (warp == 1 && lane < csize) {
+                    const int2 rq = sc.req[lane];
+                    if (rq.y > 0) {
+                        const unsigned dst = mapa(smem_u32(halo + 6 * (par * cap_blocks + sc.reqbase[lane])), lane);
+                        asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                     ::"r"(dst), "r"(smem_u32(mcur + 6 * rq.x)), "r"(48u * rq.y),
+                                     "r"(mapa(bar, lane))
+                                     : "memory");
+                    }
+                }
+            } else {
+                cluster_arrive();
+            }
         }
         mark(2);
         // local-column half of n = A m while the messages fly
@@ -1096,7 +1145,8 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         const double* hv = push ? halo + 6 * par * cap_blocks : nullptr;
         double beta = 0.0, alpha = 0.0;
         bool stop = false;
-        if (warp == kSW) {
+        const bool folder = a.fold_all || warp == kSW; // fold_all: every warp, no hand-off
+        if (folder) {
             double2 gd = make_double2(0.0, 0.0);
             double t2 = 0.0;
             if (lane < 16) {
@@ -1118,18 +1168,20 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             beta = gamma * inv_gamma_old;
             alpha = gamma / (delta - beta * gamma * inv_alpha_old);
             stop = stop || !(alpha > 0.0) || !isfinite(alpha); // breakdown
-            if (lane == 0) {
-                sc.scal[0] = beta;
-                sc.scal[1] = alpha;
-                sc.scal[2] = stop ? 1.0 : 0.0;
+            if (!a.fold_all) {
+                if (lane == 0) {
+                    sc.scal[0] = beta;
+                    sc.scal[1] = alpha;
+                    sc.scal[2] = stop ? 1.0 : 0.0;
+                }
+                asm volatile("bar.arrive 1, %0;" ::"r"(kCT) : "memory");
             }
-            asm volatile("bar.arrive 1, %0;" ::"r"(kCT) : "memory");
             inv_gamma_old = 1.0 / gamma; // off the critical path: next iteration
             inv_alpha_old = 1.0 / alpha;
         }
         // the other warps keep the shared-memory pipe idle while the scalar
         // warp's shuffle tree runs, then take the remote half of n
-        if (warp != kSW) {
+        if (!folder) {
             asm volatile("bar.sync 1, %0;" ::"r"(kCT) : "memory");
             beta = sc.scal[0];
             alpha = sc.scal[1];
@@ -1230,6 +1282,10 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 atomicAdd(&sv.perf->phase[10 + k], pts[k] - prev);
                 prev = pts[k];
             }
+            // init sub-phases: [cs[3], ci0) eps + send plan, [ci0, ci1) warm
+            // start, [ci1, ci2) u + barrier, [ci2, loop) initial SpMV + m
+            const unsigned long long qi[5] = {cs[3], ci[0], ci[1], ci[2], c_start + ph[8]};
+            for (int k = 0; k < 4; ++k) atomicAdd(&sv.perf->phase[16 + k], qi[k + 1] - qi[k]);
         }
     }
     if (sv.perf && threadIdx.x == 0) {
@@ -1300,10 +1356,14 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
                         int max_iters, cudaStream_t s, const PcgFuse* fuse) {
     if (sv.n_rows == 0) return;
     const int cmax = pcg_cluster_size();
+    static const int min_rows = [] {
+        const char* e = std::getenv("DABD_GPU_PCG_MIN_ROWS");
+        return e ? std::max(8, std::atoi(e)) : 32;
+    }();
     int csize = 1;
-    while (csize < cmax && csize * 32 < max_rows_per_part) csize *= 2; // >= ~32 rows per CTA
+    while (csize < cmax && csize * min_rows < max_rows_per_part) csize *= 2; // >= ~min_rows rows per CTA
     // largest per-partition chunk under the per-partition rule of k_pcg_cluster
-    const int cmax_rows = std::max(std::min(max_rows_per_part, 32), (max_rows_per_part + csize - 1) / csize);
+    const int cmax_rows = std::max(std::min(max_rows_per_part, min_rows), (max_rows_per_part + csize - 1) / csize);
     // register-resident row groups per warp (kCW warps x kRowsPerWarp rows each)
     const int groups = (cmax_rows + kCW * kRowsPerWarp - 1) / (kCW * kRowsPerWarp);
     if (groups > 4) throw Error("pcg: cluster chunk exceeds 4 row groups per warp");
@@ -1313,6 +1373,17 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
         return e ? std::atoi(e) : 2;
     }();
     a.warm = warm;
+    a.min_rows = min_rows;
+    static const int spread = [] {
+        const char* e = std::getenv("DABD_GPU_PCG_SPREAD");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.spread = spread;
+    static const int fold_all = [] {
+        const char* e = std::getenv("DABD_GPU_PCG_FOLD_ALL");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.fold_all = fold_all;
     if (fuse) {
         a.fused = 1;
         a.row_trace = fuse->row_trace;

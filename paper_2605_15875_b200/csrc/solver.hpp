@@ -54,7 +54,9 @@ struct DevPerf {
     // (see k_pcg_cluster; dabd_gpu_ctx_pcg_phases); [8] setup, [9] epilogue,
     // [10..15] setup sub-phases: staging issue + first cluster barrier,
     // exchange plan, staging wait, plan barrier, eps + factor, init
-    unsigned long long phase[16];
+    // [16..19] init sub-phases: eps + send plan, warm start, u = Dinv r +
+    // barrier, initial SpMV + m
+    unsigned long long phase[24];
 };
 
 struct SolverView {

@@ -14,13 +14,26 @@ def main():
     from paper_2605_15875_b200 import api
     from paper_2605_15875_b200.scene import make_scenario
 
-    os.environ["DABD_GPU_PCG_PHASES"] = "1"  # read at context creation
     lib = L.load()
     scene = sys.argv[1] if len(sys.argv) > 1 else "pile-1k"
-    ctx = api.Context(api.Scene(make_scenario(scene)))
-    ctx.run_frames(40)
+    specs = sys.argv[2:] or ["0:0"]
+    for spec in specs:
+        os.environ["DABD_GPU_PCG_PHASES"] = "1:" + spec  # read at context creation
+        print(f"== timed thread: CTA:warp {spec}")
+        one(lib, L, api, make_scenario, scene, torch)
+
+
+def one(lib, L, api, make_scenario, scene, torch):
+    sd = make_scenario(scene)
+    ctx = api.Context(api.Scene(sd))
+    if scene == "pile-1k":
+        from bench import start_state
+        ctx.set_state(*start_state(sd, 1))
+        ctx.run_frames(3)
+    else:
+        ctx.run_frames(40)
     torch.cuda.synchronize()
-    cyc = (C.c_double * 16)()
+    cyc = (C.c_double * 24)()
     L.check(lib.dabd_gpu_ctx_pcg_phases(ctx.h, 1, cyc))
     ctx.run_frames(4)
     torch.cuda.synchronize()
@@ -41,6 +54,8 @@ def main():
            "exchange plan .. plan barrier", "eps, factor, init"]
     for k in range(6):
         print(f"    setup[{k}] {sub[k]:24s} {cyc[10 + k] / nl:8.0f} cycles/launch")
+    for k, nm in enumerate(["eps + send plan", "warm start", "u = Dinv r + barrier", "initial SpMV + m"]):
+        print(f"      init[{k}] {nm:22s} {cyc[16 + k] / nl:8.0f} cycles/launch")
 
 
 if __name__ == "__main__":
