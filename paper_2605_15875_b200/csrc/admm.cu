@@ -251,7 +251,8 @@ __global__ void k_merged(int n, const int* ianc, const double* iq, const double*
 // followed by z = z_next (runtime.cpp:462).
 __global__ void k_adapt(int n, const int* ianc, double* irho, const double* irho0, const double* rb,
                         const double* sb, double tau, double mu, double smin, double smax,
-                        int enabled, double* iz, const double* iznext) {
+                        int enabled, double* iz, const double* iznext, const FrameCtrl* skip_first) {
+    if (skip_first && skip_first->k == 1) return; // device ADMM frame: no consensus before the first solve
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         if (!ianc[i]) continue;
         if (enabled) {
@@ -292,6 +293,124 @@ __global__ void k_accept_copy(int n, const int* ipart, int part_base, const Part
                               const double* src, double* dst) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 6 * n; t += gridDim.x * blockDim.x)
         if (ps[ipart[t / 6] - part_base].accepted) dst[t] = src[t];
+}
+
+
+__device__ __forceinline__ void admm_cond(unsigned long long h, bool v, int graph) {
+    if (graph) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(h), v ? 1u : 0u);
+}
+
+// one warp; lane p < P handles partition p where partitions are independent
+__global__ void k_admm_ctrl(AdmmCtrlArgs a, int op) {
+    FrameCtrl* c = a.c;
+    const int lane = threadIdx.x;
+    const bool graph = a.hd.graph != 0;
+    if (op == kAdmmInit) {
+        if (lane == 0) {
+            c->k = 1;
+            c->ended = c->failed = 0;
+            c->sigma = 0;
+            c->admm_iterations = 0;
+            c->trace_n = 0;
+            c->newton_total = c->ls_total = c->pcg_total = 0;
+            c->exec_admm = c->exec_gate = c->exec_solve = 0;
+            c->exec_newton = c->exec_step = c->exec_ls = 0;
+            c->gate_max = 0;
+            admm_cond(a.hd.admm, true, graph);
+        }
+        for (int p = lane; p < a.P; p += 32) {
+            a.dq[p] = 0.0;
+            a.cost[p] = 0.0;
+        }
+        return;
+    }
+    if (op == kAdmmHead) {
+        const bool gate = c->k > 1;
+        for (int p = lane; p < a.P; p += 32) {
+            a.gate[p] = 2.0;
+            a.rloc[p] = 0.0;
+            a.sloc[p] = 0.0;
+        }
+        if (lane == 0) {
+            ++c->exec_admm;
+            admm_cond(a.hd.gate, gate, graph);
+            admm_cond(a.hd.solve, !gate, graph); // k = 1: straight to the local solve
+        }
+        return;
+    }
+    if (op == kAdmmDecide) {
+        if (lane != 0) return;
+        ++c->exec_gate;
+        const int gc = *a.gate_count;
+        if (gc > c->gate_max) c->gate_max = gc;
+        int sigma = 0;
+        if (*a.err != 0) {
+            sigma = -1;
+        } else {
+            // runtime.cpp:586-619: every partition's (dq, r, s, earliest TOI)
+            double dq = 0.0, r = 0.0, sres = 0.0, toi = 1.0;
+            bool all_one = true;
+            for (int p = 0; p < a.P; ++p) {
+                const double e = a.gate[p];
+                const double t = e > 1.0 ? 1.0 : fmin(1.0, __dmul_rn(0.9, e));
+                dq = fmax(dq, a.dq[p]);
+                r = fmax(r, a.rloc[p]);
+                sres = fmax(sres, a.sloc[p]);
+                toi = fmin(toi, t);
+                all_one = all_one && t == 1.0;
+            }
+            const double nrm = __dmul_rn(a.h, a.l); // consensus.cpp:54-64
+            const bool end = __ddiv_rn(dq, nrm) < a.theta && __ddiv_rn(r, nrm) < a.theta &&
+                             __ddiv_rn(sres, nrm) < a.theta && all_one;
+            if (end) sigma = 1;
+            else if (c->k == a.K) sigma = c->can_halve ? 2 : 3;
+            if (a.trace && c->trace_n < a.trace_cap) {
+                double* row = a.trace + 8 * c->trace_n;
+                row[0] = c->frame;
+                row[1] = c->attempt;
+                row[2] = c->k;
+                row[3] = dq;
+                row[4] = r;
+                row[5] = sres;
+                row[6] = toi;
+                row[7] = sigma;
+            }
+            ++c->trace_n;
+            if (sigma == 1) {
+                c->ended = 1;
+                c->admm_iterations = c->k;
+            }
+        }
+        c->sigma = sigma;
+        admm_cond(a.hd.solve, sigma == 0, graph);
+        admm_cond(a.hd.admm, sigma == 0, graph);
+        return;
+    }
+    // kAdmmTail
+    __shared__ int s_err;
+    if (lane == 0) {
+        ++c->exec_solve;
+        s_err = *a.err;
+    }
+    __syncwarp();
+    for (int p = lane; p < a.P; p += 32) {
+        const PartState& s = a.ps[p];
+        a.dq[p] = a.dq_new[p];
+        // balancer cost (engine.cu partition_cost)
+        const double rows = s.ndof / 6.0;
+        a.cost[p] += fmax(1.0, s.iterations * (rows + 2.0 * s.n_active_contacts) + s.pcg_total * rows);
+    }
+    if (lane == 0) {
+        for (int p = 0; p < a.P; ++p) {
+            c->newton_total += a.ps[p].iterations;
+            c->ls_total += a.ps[p].ls_steps;
+        }
+        c->k += 1;
+        if (s_err != 0) {
+            c->sigma = -1;
+            admm_cond(a.hd.admm, false, graph);
+        }
+    }
 }
 
 } // namespace
@@ -362,10 +481,10 @@ void launch_merged(int n, const int* ianc, const double* iq, const double* iznex
 
 void launch_adapt(int n, const int* ianc, double* irho, const double* irho0, const double* rb,
                   const double* sb, const AdaptParams& a, double* iz, const double* iznext,
-                  cudaStream_t s) {
+                  cudaStream_t s, const FrameCtrl* skip_first) {
     if (n == 0) return;
     DABD_LAUNCH("k_adapt", s, k_adapt<<<grid_for(n, kB), kB, 0, s>>>(n, ianc, irho, irho0, rb, sb, a.tau, a.mu, a.sigma_min,
-                                           a.sigma_max, a.adapt_enabled ? 1 : 0, iz, iznext));
+                                           a.sigma_max, a.adapt_enabled ? 1 : 0, iz, iznext, skip_first));
 }
 
 void launch_commit(const SceneView& sc, int n, const int* ibody, const int* ipart, const int* ianc,
@@ -380,6 +499,10 @@ void launch_accept_copy(int n, const int* ipart, int part_base, const PartState*
                         const double* src, double* dst, cudaStream_t s) {
     if (n == 0) return;
     DABD_LAUNCH("k_accept_copy", s, k_accept_copy<<<grid_for(6ll * n, kB), kB, 0, s>>>(n, ipart, part_base, ps, src, dst));
+}
+
+void launch_admm_ctrl(const AdmmCtrlArgs& a, int op, cudaStream_t s) {
+    DABD_LAUNCH("k_admm_ctrl", s, k_admm_ctrl<<<1, 32, 0, s>>>(a, op));
 }
 
 } // namespace dabd_gpu

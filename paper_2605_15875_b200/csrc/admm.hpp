@@ -34,11 +34,38 @@ void launch_merged(int n, const int* ianc, const double* iq, const double* iznex
                    cudaStream_t s);
 void launch_adapt(int n, const int* ianc, double* irho, const double* irho0, const double* rb,
                   const double* sb, const AdaptParams& a, double* iz, const double* iznext,
-                  cudaStream_t s);
+                  cudaStream_t s, const FrameCtrl* skip_first = nullptr);
 void launch_commit(const SceneView& sc, int n, const int* ibody, const int* ipart, const int* ianc,
                    const uint32_t* bmask, double* iq, const double* iznext, const double* q_start,
                    double h, double* q, double* qd, cudaStream_t s);
 void launch_accept_copy(int n, const int* ipart, int part_base, const PartState* ps,
                         const double* src, double* dst, cudaStream_t s);
+
+// Device controller of the multi-partition consensus-ADMM frame
+// (runtime.cpp:316-476 and the controller round trip 572-638 for the
+// partitions of one context). ops: kAdmmInit, kAdmmHead (IF(gate) = k > 1;
+// gate TOIs <- 2, r/s partials <- 0), kAdmmDecide (stop test of
+// consensus.cpp:54-64 over every partition's dq, r, s and merge-gate TOI,
+// trace row, sigma; IF(solve), WHILE), kAdmmTail (collect the local solve:
+// dq, Newton totals, partition costs; k++).
+enum AdmmCtrlOp { kAdmmInit = 0, kAdmmHead = 1, kAdmmDecide = 2, kAdmmTail = 3 };
+struct AdmmCtrlArgs {
+    FrameCtrl* c = nullptr;
+    double* gate = nullptr;      // [P] earliest merge-gate TOI (2.0 = none)
+    double* rloc = nullptr;      // [P] primal residual
+    double* sloc = nullptr;      // [P] dual residual
+    double* dq = nullptr;        // [P] last local solve's ||q - q_before||_inf
+    const double* dq_new = nullptr; // [P] delta_inf output of the solve just done
+    double* cost = nullptr;      // [P] balancer cost of the attempt
+    const PartState* ps = nullptr;
+    const int* gate_count = nullptr; // merge-gate candidate count (device)
+    int* err = nullptr;
+    double* trace = nullptr;
+    int trace_cap = 0;
+    int P = 0, K = 0;
+    double h = 0.0, l = 0.0, theta = 0.0;
+    CondHandles hd;
+};
+void launch_admm_ctrl(const AdmmCtrlArgs& a, int op, cudaStream_t s);
 
 } // namespace dabd_gpu

@@ -160,6 +160,7 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
             set_scalar_carveout(carve);
         }
     }
+    if (const char* e = std::getenv("DABD_GPU_ADMM_HOST")) admm_device_ = e[0] != '1';
     if (const char* e = std::getenv("DABD_SKIN_MIN")) skin_min_ = std::atof(e);
     if (const char* e = std::getenv("DABD_SKIN_GROW")) skin_grow_ = std::atof(e);
     sync();
@@ -168,6 +169,7 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
 Engine::~Engine() {
     if (exec_) cudaGraphExecDestroy(exec_);
     if (newton_exec_) cudaGraphExecDestroy(newton_exec_);
+    if (admm_exec_) cudaGraphExecDestroy(admm_exec_);
     for (cudaStream_t s : cap_streams_) cudaStreamDestroy(s);
     for (cudaStream_t s : side_streams_) cudaStreamDestroy(s);
     if (peer_lo_) cudaIpcCloseMemHandle(const_cast<double*>(peer_lo_));
@@ -1515,6 +1517,202 @@ FrameStats Engine::frame_reference() {
     return st;
 }
 
+// ---------------------------------------------------------------------------
+// Multi-partition ADMM attempt as one captured graph (runtime.cpp:316-476 and
+// the controller round trip 572-638, for the partitions of this context):
+//
+//   init; WHILE(sigma == 0) {
+//     head                       (IF(gate) = k > 1; TOIs <- 2, r, s <- 0)
+//     IF(gate)  { consensus, merge targets, merge-gate broad phase + CCD,
+//                 decide: stop test, trace row, sigma, IF(solve), WHILE }
+//     IF(solve) { adapt rho + z (k > 1), q_before, Newton solve (nested
+//                 conditional graph), delta_inf, tail: dq, totals, costs, k++ }
+//   }
+//
+// Instance sets and capacities change per attempt, so the graph is captured
+// per attempt (an in-place update when the topology is unchanged) and read
+// back once. Recoverable device errors (contact-list, BSR-width or gate
+// capacity; the line-search collapse of an iterative solve) redo the attempt
+// from its start, which is deterministic.
+int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, int I, int ns,
+                                FrameStats& st, std::vector<double>& cost, int& grows, bool& exact) {
+    const SimParams& P = frame_params_;
+    if (gate_cap_ == 0) gate_cap_ = 64 * std::max(I, 1);
+    det_gate_.ensure(I, ds_.max_verts, gate_cap_);
+    admm_dq_.resize(std::max(P_, 1));
+    admm_dqnew_.resize(std::max(P_, 1));
+    admm_cost_.resize(std::max(P_, 1));
+    admm_cost_h_.resize(std::max(P_, 1));
+    FrameCtrl init{};
+    init.frame = static_cast<double>(frame);
+    init.attempt = static_cast<double>(attempt);
+    init.can_halve = tsc_.can_halve() ? 1 : 0;
+    ctrl_h_[0] = init;
+    CUDA_CHECK(cudaMemcpyAsync(ctrl_.get(), ctrl_h_.get(), sizeof(FrameCtrl), cudaMemcpyHostToDevice, s_));
+    err_.zero(s_);
+
+    AdmmCtrlArgs a;
+    a.c = ctrl_.get();
+    a.gate = gate_.get();
+    a.rloc = rloc_.get();
+    a.sloc = sloc_.get();
+    a.dq = admm_dq_.get();
+    a.dq_new = admm_dqnew_.get();
+    a.cost = admm_cost_.get();
+    a.ps = ps_.get();
+    a.gate_count = det_gate_.d_count();
+    a.err = err_.get();
+    a.trace = trace_dev_.get();
+    a.trace_cap = trace_cap_;
+    a.P = P_;
+    a.K = hs_.admm_max_iterations;
+    a.h = h;
+    a.l = P.scene_scale;
+    a.theta = P.theta;
+
+    KernelTimer::get().suspend(true);
+    hd_ = CondHandles{};
+    hd_.graph = 1;
+    for (long long& v : nodes_inc_) v = 0;
+    const long long c0 = launch_counter().load();
+    long long total = 0;
+    CUDA_CHECK(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
+    try {
+        hd_.admm = new_cond_handle();
+        a.hd = hd_;
+        launch_admm_ctrl(a, kAdmmInit, s_);
+        add_cond_node(hd_.admm, true, 0, [&] {
+            hd_.gate = new_cond_handle();
+            hd_.solve = new_cond_handle();
+            a.hd = hd_;
+            launch_admm_ctrl(a, kAdmmHead, s_);
+            add_cond_node(hd_.gate, false, 1, [&] {
+                launch_consensus(ns, shared_inst_.get(), ipart_.get(), p0_, iq_.get(), iu_.get(),
+                                 irho_.get(), iz_.get(), nullptr, nullptr, 0, iznext_.get(), rb_.get(),
+                                 sb_.get(), rloc_.get(), sloc_.get(), err_.get(), s_);
+                // merge gate per partition (consensus.cpp:66-75): fixed-capacity
+                // broad phase, CCD over its device count
+                launch_merged(I, ianc_.get(), iq_.get(), iznext_.get(), iqtry_.get(), s_);
+                det_gate_.enqueue(ds_.view(), iview(iq_.get(), iqtry_.get()), stat_.get(),
+                                  static_cast<int>(h_stat_.size()), true, 0.0, err_.get(), s_);
+                launch_ccd(view(), det_gate_.keys(), det_gate_.cap(), det_gate_.d_count(), det_gate_.fmt(),
+                           det_gate_.boxes(), iq_.get(), iqtry_.get(), 2, gate_.get(), s_);
+                launch_admm_ctrl(a, kAdmmDecide, s_);
+            });
+            add_cond_node(hd_.solve, false, 2, [&] {
+                launch_adapt(I, ianc_.get(), irho_.get(), irho0_.get(), rb_.get(), sb_.get(), hs_.adapt,
+                             iz_.get(), iznext_.get(), s_, ctrl_.get());
+                if (I) CUDA_CHECK(cudaMemcpyAsync(iqbefore_.get(), iq_.get(), 6 * I * sizeof(double),
+                                                  cudaMemcpyDeviceToDevice, s_));
+                cap_newton(hs_.newton_cap, tol, 3);
+                CUDA_CHECK(cudaMemsetAsync(admm_dqnew_.get(), 0, P_ * sizeof(double), s_));
+                launch_delta_inf(n_rows_, rinst_.get(), rpart_.get(), p0_, iq_.get(), iqbefore_.get(),
+                                 admm_dqnew_.get(), s_);
+                launch_admm_ctrl(a, kAdmmTail, s_);
+            });
+        });
+        total = launch_counter().load() - c0;
+        launch_counter() -= total; // captured, not executed
+    } catch (...) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(s_, &g);
+        if (g) cudaGraphDestroy(g);
+        KernelTimer::get().suspend(false);
+        hd_ = CondHandles{};
+        throw;
+    }
+    cudaGraph_t g;
+    CUDA_CHECK(cudaStreamEndCapture(s_, &g));
+    KernelTimer::get().suspend(false);
+    hd_ = CondHandles{};
+    bool updated = false;
+    if (admm_exec_) {
+        cudaGraphExecUpdateResultInfo info;
+        updated = cudaGraphExecUpdate(admm_exec_, g, &info) == cudaSuccess;
+        if (!updated) {
+            cudaGetLastError();
+            cudaGraphExecDestroy(admm_exec_);
+            admm_exec_ = nullptr;
+        }
+    }
+    if (!updated) CUDA_CHECK(cudaGraphInstantiate(&admm_exec_, g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+    const long long inc[6] = {nodes_inc_[0], nodes_inc_[1], nodes_inc_[2], nodes_inc_[3], nodes_inc_[4],
+                              nodes_inc_[5]};
+
+    const auto t0 = std::chrono::steady_clock::now();
+    CUDA_CHECK(cudaGraphLaunch(admm_exec_, s_));
+    CUDA_CHECK(cudaMemcpyAsync(ctrl_h_.get(), ctrl_.get(), sizeof(FrameCtrl), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get(), err_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 9, det_gate_.d_count(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 3, det_.d_count(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(admm_cost_h_.get(), admm_cost_.get(), P_ * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaStreamSynchronize(s_));
+    st.t_solve += seconds_since(t0);
+    const FrameCtrl c = ctrl_h_[0];
+    // kernels the replay executed: per conditional body its own nodes x its
+    // executions (levels: 0 ADMM body, 1 gate, 2 solve, 3 Newton, 4 step, 5 ls)
+    const long long rebuilds = lstate_h_[0].n_rebuilds - rebuilds_seen_;
+    rebuilds_seen_ = lstate_h_[0].n_rebuilds;
+    count_launch(rebuilds * rebuild_nodes_ + (total - inc[0]) +
+                 static_cast<long long>(c.exec_admm) * (inc[0] - inc[1] - inc[2]) +
+                 static_cast<long long>(c.exec_gate) * inc[1] +
+                 static_cast<long long>(c.exec_solve) * (inc[2] - inc[3]) +
+                 static_cast<long long>(c.exec_newton) * (inc[3] - inc[4]) +
+                 static_cast<long long>(c.exec_step) * (inc[4] - inc[5]) +
+                 static_cast<long long>(c.exec_ls) * inc[5]);
+    const int code = pin_i_[0];
+    if (code != 0) {
+        err_.zero(s_);
+        const int gate_count = pin_i_[9];
+        if (code == kErrCapacity && gate_count > gate_cap_ && grows < kMaxGrows) {
+            gate_cap_ = 2 * gate_count; // merge-gate candidates overflowed its fixed capacity
+            ++grows;
+            ++capacity_retries_;
+            return 0;
+        }
+        if ((code == kErrCapacity || code == kErrEll) && grows < kMaxGrows) {
+            grow_capacity(code);
+            ++grows;
+            ++capacity_retries_;
+            return 0;
+        }
+        if (code == kErrLineSearch && !exact) {
+            set_solver(1e-14, std::max(pcg_max_, 50000));
+            exact = true;
+            ++exact_retries_;
+            return 0;
+        }
+        sync();
+        throw DeviceError(std::string(err_text(code)) + " [admm frame]", code);
+    }
+    // the gate's sort cost follows its capacity: shrink it (with hysteresis)
+    // towards twice the most candidates an iteration found
+    if (4 * c.gate_max < gate_cap_ && gate_cap_ > 8192) gate_cap_ = std::max(8192, 2 * c.gate_max);
+    const int nt = std::min(c.trace_n, trace_cap_);
+    if (nt > 0) {
+        std::vector<double> rows(8 * static_cast<size_t>(nt));
+        CUDA_CHECK(cudaMemcpy(rows.data(), trace_dev_.get(), rows.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nt; ++i)
+            trace_.push_back({rows[8 * i], rows[8 * i + 1], rows[8 * i + 2], rows[8 * i + 3], rows[8 * i + 4],
+                              rows[8 * i + 5], rows[8 * i + 6], rows[8 * i + 7]});
+    }
+    st.newton_iterations += c.newton_total;
+    st.line_search_steps += c.ls_total;
+    st.pcg_iterations += c.pcg_total;
+    st.max_contacts = std::max(st.max_contacts, lstate_h_[0].n_act);
+    st.max_candidates = std::max(st.max_candidates, pin_i_[3]);
+    for (int p = 0; p < P_; ++p) cost[p] += admm_cost_h_[p];
+    if (c.sigma == 1) {
+        st.admm_iterations = c.admm_iterations;
+        return 1;
+    }
+    if (c.sigma == 2) return 2;
+    if (c.sigma == 3) throw Error("frame failed: halving budget exhausted with a blocked merge");
+    throw Error("controller: frame ended without a decision");
+}
+
 // runtime.cpp:110-694 on replicated global state with every partition of
 // this context solved in the same batched kernels.
 FrameStats Engine::frame_admm(int frame) {
@@ -1535,6 +1733,9 @@ FrameStats Engine::frame_admm(int frame) {
     int attempt = 0;
     FrameStats st;
     const long long exact0 = exact_retries_, cap0 = capacity_retries_;
+    SolverRestore frame_restore(*this); // an exact-solve retry's PCG limits end with the frame
+    int dev_grows = 0;
+    bool dev_exact = false;
     while (true) {
         st.attempts = attempt + 1;
         const double h = tsc_.h();
@@ -1654,7 +1855,18 @@ FrameStats Engine::frame_admm(int frame) {
         // A local failure on one rank must not leave its peers blocked in a
         // collective: it is carried to the next agreement point instead.
         std::string fail;
-        for (int k = 1; k <= hs_.admm_max_iterations; ++k) {
+        const bool device_loop = admm_device_ && use_graph_ && !distributed_ && n_rows_ > 0;
+        if (device_loop) {
+            const int r = admm_attempt_device(frame, attempt, h, tol, I, ns, st, cost, dev_grows, dev_exact);
+            if (r == 0) continue; // a capacity grew / the exact-solve retry is armed: redo the attempt
+            if (r == 2) {         // blocked merge at K: h halves (runtime.cpp:603-642)
+                tsc_.on_frame_failed();
+                retry = true;
+            } else {
+                ended = true;
+            }
+        }
+        for (int k = 1; !device_loop && k <= hs_.admm_max_iterations; ++k) {
             if (k > 1) {
                 std::vector<double> earliest(P_, 2.0), rl(P_, 0.0), sl(P_, 0.0);
                 try {

@@ -159,6 +159,16 @@ class Engine {
     // frames -----------------------------------------------------------------
     FrameStats frame_reference();
     FrameStats frame_admm(int frame_index);
+    // One attempt of the multi-partition frame as ONE captured graph (no
+    // host round trip per ADMM iteration): 1 = ended, 2 = retry with h / 2,
+    // 0 = a capacity grew or the exact-solve retry was armed (redo the
+    // attempt); throws on any other device error.
+    int admm_attempt_device(int frame, int attempt, double h, double tol, int I, int ns,
+                            FrameStats& st, std::vector<double>& cost, int& grows, bool& exact);
+    cudaGraphExec_t admm_exec_ = nullptr;
+    DBuf<double> admm_dq_, admm_dqnew_, admm_cost_;
+    PinnedBuf<double> admm_cost_h_;
+    bool admm_device_ = true; // DABD_GPU_ADMM_HOST=1: the host-driven ADMM loop
 
     HostScene hs_;
     DeviceScene ds_;

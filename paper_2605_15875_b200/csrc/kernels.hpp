@@ -97,13 +97,20 @@ struct FrameCtrl {
     int any_active, any_searching;
     int trace_n;
     int exec_admm, exec_newton, exec_step, exec_ls; // conditional-body executions
-    int pad_;
+    // multi-partition ADMM frame on the device (k_admm_ctrl): sigma of the
+    // last decision (0 running, 1 end, 2 retry with h/2, 3 halving budget
+    // spent, -1 device error), whether h may still halve (host-written),
+    // executions of the merge-gate and local-solve bodies, and the largest
+    // merge-gate candidate count of the attempt (capacity feedback)
+    int sigma, can_halve, exec_gate, exec_solve, gate_max;
     double dq_inf;       // max over partitions of the last solve's config delta
     double frame;        // frame index for trace rows (written by the host)
+    double attempt;      // attempt index for trace rows (written by the host)
 };
 
 struct CondHandles {
     unsigned long long admm = 0, newton = 0, step = 0, ls = 0; // cudaGraphConditionalHandle values
+    unsigned long long gate = 0, solve = 0; // multi-partition ADMM frame: IF(k > 1), IF(continue)
     int graph = 0;
 };
 

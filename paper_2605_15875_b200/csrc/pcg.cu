@@ -77,7 +77,8 @@ struct PcgArgs {
     // previous two solutions (sv.x and pa, which the kernel rotates); 0 = off
     int warm;
     int min_rows; // rows per CTA the cluster size aims for (>= min_rows per CTA)
-    int spread;   // 1: every warp sends to one peer (partials + halo), 0: one warp sends to all
+    int spread;   // 1: every warp sends to one peer (partials + halo); 0: the scalar warp sends to
+                  // all (two remote stores per peer), 2: the same in one 32-lane store
     int fold_all; // 1: every warp folds the cluster partials itself, 0: the scalar warp folds
 };
 
@@ -341,6 +342,28 @@ struct ClusterScalars {
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// Sums of three values over a warp with 6 double shuffles instead of 15:
+// after the first two levels different lane groups reduce different values.
+// Returns sum(a) in lanes 0-7, sum(b) in lanes 8-15, sum(c) in lanes 16-31
+// (fixed pattern, so every warp and CTA rounds identically).
+__device__ __forceinline__ double warp_sum3(double a, double b, double c, int lane) {
+    const bool lo = lane < 16, q = (lane & 8) != 0;
+    const double r1 = __shfl_xor_sync(0xffffffffu, lo ? c : a, 16);
+    const double r2 = __shfl_xor_sync(0xffffffffu, lo ? 0.0 : b, 16);
+    if (lo) {
+        a += r1;
+        b += r2;
+    } else {
+        c += r1;
+    }
+    const double r3 = __shfl_xor_sync(0xffffffffu, lo ? (q ? a : b) : c, 8);
+    double v = lo ? (q ? b + r3 : a + r3) : c + r3;
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
     return v;
 }
 
@@ -750,10 +773,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
 
     const int row_step = kCW * kRowsPerWarp;
     // (A v) row comp over the staged blocks with local columns
-    auto spmv_local = [&](int lr, const double* vloc) -> double {
+    // skip_diag: the row's diagonal block is left out; the caller adds
+    // (D + eps I) v_i itself where it is known without a product (v = Dinv w
+    // gives exactly w for the operator whose diagonal block is Dinv^-1)
+    auto spmv_local = [&](int lr, const double* vloc, bool skip_diag = false) -> double {
         const int b0 = bstart[lr], bs = max(b0, min(bstart[lr + 1], cap_blocks));
         double y0 = 0.0, y1 = 0.0;
-        int s = b0;
+        int s = skip_diag && b0 < bs ? b0 + 1 : b0;
         for (; s + 1 < bs; s += 2) {
             const int c0 = bcode[s], c1 = bcode[s + 1];
             if (c0 >= 0) {
@@ -780,7 +806,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     // staged blocks with remote columns: values from `hv` (halo rows, push
     // path) or through DSMEM from the peer's m buffer at `moff` (fallback),
     // then spilled blocks (global memory + DSMEM, fallback only)
-    auto spmv_remote = [&](int lr, const double* hv, ptrdiff_t moff, double y) -> double {
+    auto spmv_remote = [&](int lr, const double* hv, ptrdiff_t moff, double y, bool skip_diag = false) -> double {
         // staged blocks [b0, bs), spilled [bs, b1); a row may lie wholly past
         // the budget (bs = b0)
         const int b0 = bstart[lr], b1 = bstart[lr + 1], bs = max(b0, min(b1, cap_blocks));
@@ -795,6 +821,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         }
         for (int s = bs; s < b1; ++s) { // spilled block
             const int r = r0 + lr, t = s - b0;
+            if (t == 0 && skip_diag) continue;
             const int col = t == 0 ? r : sv.ell_col[r * sv.ell_w + t - 1];
             const double* M = (t == 0 ? sv.rdiag + 36 * r
                                       : sv.ell_blk + (static_cast<size_t>(r) * sv.ell_w + t - 1) * 36) + 6 * comp;
@@ -974,9 +1001,10 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     }
     cluster_barrier();
     if constexpr (PH) ci[2] = clock64();
+    // w = A u with u = Dinv r: the diagonal block contributes r itself
 #pragma unroll
     for (int g = 0; g < G; ++g)
-        w[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, spmv_local(lrg[g], vm1)) : 0.0;
+        w[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, r[g] + spmv_local(lrg[g], vm1, true), true) : 0.0;
     // m = Dinv w for iteration 0 (into vm0) and the partials (r.u, w.u, r.r)
     double l_g = 0.0, l_d = 0.0, l_r = 0.0;
     auto make_m = [&](double* mdst) {
@@ -1035,34 +1063,22 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         const unsigned bar = smem_u32(&sc.bar[par]);
         if (push && threadIdx.x == 0) mbar_expect(bar, expect);
         // ---- partials of this CTA: warp trees, then one fixed 32-lane tree
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            l_g += __shfl_xor_sync(0xffffffffu, l_g, off);
-            l_d += __shfl_xor_sync(0xffffffffu, l_d, off);
-            l_r += __shfl_xor_sync(0xffffffffu, l_r, off);
-        }
-        if (lane == 0) {
-            sc.red[warp][0] = l_g;
-            sc.red[warp][1] = l_d;
-            sc.red[warp][2] = l_r;
+        {
+            const double v = warp_sum3(l_g, l_d, l_r, lane);
+            if ((lane & 7) == 0 && lane <= 16) sc.red[warp][lane >> 3] = v;
         }
         mark(0);
         __syncthreads(); // red[] and this CTA's m (mcur) complete
         mark(1);
-        if (a.spread) {
+        if (a.spread == 1) {
             // every warp folds the CTA's partials (same fixed tree in every
             // warp) and warp k sends them, plus the halo rows consumer k
             // needs, to peer k: one remote store pair and one bulk copy per
             // warp instead of csize of each serialised in one warp
-            double t0 = lane < kCW ? sc.red[lane][0] : 0.0;
-            double t1 = lane < kCW ? sc.red[lane][1] : 0.0;
-            double t2 = lane < kCW ? sc.red[lane][2] : 0.0;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                t0 += __shfl_xor_sync(0xffffffffu, t0, off);
-                t1 += __shfl_xor_sync(0xffffffffu, t1, off);
-                t2 += __shfl_xor_sync(0xffffffffu, t2, off);
-            }
+            const double tv = warp_sum3(lane < kCW ? sc.red[lane][0] : 0.0, lane < kCW ? sc.red[lane][1] : 0.0,
+                                        lane < kCW ? sc.red[lane][2] : 0.0, lane);
+            const double t0 = __shfl_sync(0xffffffffu, tv, 0), t1 = __shfl_sync(0xffffffffu, tv, 8),
+                         t2 = __shfl_sync(0xffffffffu, tv, 16);
             if (warp < csize) {
                 if (lane == 0) {
                     if (push) {
@@ -1090,16 +1106,19 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             if (!bulk) cluster_arrive();
         } else {
             if (warp == kSW) { // the scalar warp: CTA tree and push to every peer
-                double t0 = lane < kCW ? sc.red[lane][0] : 0.0;
-                double t1 = lane < kCW ? sc.red[lane][1] : 0.0;
-                double t2 = lane < kCW ? sc.red[lane][2] : 0.0;
-    #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    t0 += __shfl_xor_sync(0xffffffffu, t0, off);
-                    t1 += __shfl_xor_sync(0xffffffffu, t1, off);
-                    t2 += __shfl_xor_sync(0xffffffffu, t2, off);
-                }
-                if (lane < csize) {
+                const double tv = warp_sum3(lane < kCW ? sc.red[lane][0] : 0.0, lane < kCW ? sc.red[lane][1] : 0.0,
+                                            lane < kCW ? sc.red[lane][2] : 0.0, lane);
+                const double t0 = __shfl_sync(0xffffffffu, tv, 0), t1 = __shfl_sync(0xffffffffu, tv, 8),
+                             t2 = __shfl_sync(0xffffffffu, tv, 16);
+                if (push && a.spread == 2) {
+                    // one remote-store instruction: lane k < 16 sends (r.u, w.u)
+                    // to peer k, lane 16 + k sends (r.r, 0)
+                    const int peer = lane & 15;
+                    if (peer < csize) {
+                        const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), peer) + (lane >> 4) * 16u;
+                        st_async2(dst, lane < 16 ? t0 : t2, lane < 16 ? t1 : 0.0, mapa(bar, peer));
+                    }
+                } else if (lane < csize) {
                     if (push) {
                         const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), lane);
                         const unsigned pbar = mapa(bar, lane);
@@ -1132,7 +1151,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         // local-column half of n = A m while the messages fly
         double nloc[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) nloc[g] = on[g] ? spmv_local(lrg[g], mcur) : 0.0;
+        for (int g = 0; g < G; ++g) nloc[g] = on[g] ? w[g] + spmv_local(lrg[g], mcur, true) : 0.0; // m = Dinv w
         mark(3);
         if (push)
             mbar_wait(bar, (it >> 1) & 1);
@@ -1153,13 +1172,9 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 gd = *reinterpret_cast<const double2*>(&sc.tab[par][lane][0]);
                 t2 = sc.tab[par][lane][2];
             }
-            double gamma = gd.x, delta = gd.y, rr = t2;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                gamma += __shfl_xor_sync(0xffffffffu, gamma, off);
-                delta += __shfl_xor_sync(0xffffffffu, delta, off);
-                rr += __shfl_xor_sync(0xffffffffu, rr, off);
-            }
+            const double fv = warp_sum3(gd.x, gd.y, t2, lane);
+            const double gamma = __shfl_sync(0xffffffffu, fv, 0), delta = __shfl_sync(0xffffffffu, fv, 8),
+                         rr = __shfl_sync(0xffffffffu, fv, 16);
             if (it == 0) bnorm2 = bnorm2_ws >= 0.0 ? bnorm2_ws : rr;
             stop = bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters;
             // beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
@@ -1190,7 +1205,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         if (stop) break; // uniform across the CTA and the cluster
         double nrem[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) nrem[g] = on[g] ? spmv_remote(lrg[g], hv, moff, nloc[g]) : 0.0;
+        for (int g = 0; g < G; ++g) nrem[g] = on[g] ? spmv_remote(lrg[g], hv, moff, nloc[g], true) : 0.0;
         mark(5);
         // ---- the recurrences, then m = Dinv w and the partials of the next
         // iteration (register-resident)

@@ -144,3 +144,22 @@ def default_params(**kw):
     for k, v in kw.items():
         setattr(p, k, v)
     return p
+
+
+def assert_rho(rho_g, rho_o, max_flip_frac=0.0):
+    """Final per-replica rho (runtime.cpp:481-482). rho only ever changes by
+    exact factors of tau (and the sigma clamps), so a replica either carries
+    the oracle's value to 1e-12 or one of its adaptation decisions flipped.
+    The decision compares r_b with mu s_b (consensus.cpp:44-52); for a
+    replica at rest both are at rounding level (~1e-17) and rounding decides
+    the comparison, which two implementations whose iterates agree to ~1e-14
+    (not bitwise) cannot share. `max_flip_frac` bounds the flipped fraction
+    (0: every replica exact)."""
+    rho_g, rho_o = np.asarray(rho_g), np.asarray(rho_o)
+    same = np.isclose(rho_g, rho_o, rtol=1e-12, atol=0.0)
+    flips = ~same
+    ratio = rho_g[flips] / rho_o[flips]
+    print(f"rho: {same.sum()} of {len(same)} replicas equal, {flips.sum()} decision flips"
+          + (f" (ratios {ratio.min():.3g}..{ratio.max():.3g})" if flips.any() else ""))
+    allowed = 0 if max_flip_frac <= 0.0 else max(1, int(max_flip_frac * len(same)))
+    assert flips.sum() <= allowed, (int(flips.sum()), len(same))

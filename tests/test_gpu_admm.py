@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from support import assert_rho
 from paper_2605_15875_b200 import api
 from paper_2605_15875_b200.scene import make_scenario
 
@@ -25,10 +26,13 @@ def _near_threshold(row, sd, rel=1e-2):
     return any(abs(row[c] / norm - th) < rel * th for c in (3, 4, 5))
 
 
-def _compare(name, workers, frames, state_tol=1e-7, trace_tol=1e-6, exact_toi=True, **solver):
+def _compare(name, workers, frames, state_tol=1e-7, trace_tol=1e-6, exact_toi=True, rho_flips=0.0,
+             **solver):
     """Frame-by-frame comparison over every requested frame: identical h,
     attempts, ADMM counts, trace rows (k, sigma) and gate decisions; dq, r, s
-    within trace_tol * h * l; states within state_tol; final rho to 1e-12."""
+    within trace_tol * h * l; states within state_tol; final rho to 1e-12
+    (at most a `rho_flips` fraction of replicas with a flipped adaptation
+    decision, support.assert_rho)."""
     sd = make_scenario(name)
     o = O.Scene(sd)
     ref = o.run(frames, workers=workers)
@@ -58,7 +62,7 @@ def _compare(name, workers, frames, state_tol=1e-7, trace_tol=1e-6, exact_toi=Tr
     shared = ~np.isnan(ref["rho"])
     assert np.array_equal(shared, ~np.isnan(gpu.rho))
     if shared.any():
-        assert np.allclose(gpu.rho[shared], ref["rho"][shared], rtol=1e-12)
+        assert_rho(gpu.rho[shared], ref["rho"][shared], rho_flips)
     return gpu, ref
 
 

@@ -7,7 +7,11 @@
 //   2 scalar warp: plain remote stores + remote mbarrier arrive (release.cluster)
 //   3 local store + barrier.cluster + 16-lane DSMEM pull + fold
 //   4 warp k -> peer k: plain remote stores + remote arrive
-//   5 scalar warp, lanes < csize: st.async of one v2 (2 doubles) only
+//   5 scalar warp, one 32-lane st.async (lane k: (t0, t1) to k, lane 16 + k: (t2, 0))
+//   6 local only: the same trees, __syncthreads and hand-off, no remote traffic
+//   7 as 6 without the FP64 division
+//   8 as 0 without the FP64 division
+//   9 as 5, every warp folds (no hand-off)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/exchange_probe tools/exchange_probe.cu
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -78,7 +82,8 @@ __global__ void __launch_bounds__(kT) k_probe(int mode, int iters, double* out, 
             red[warp][1] = l1;
             red[warp][2] = l2;
         }
-        if (!remote_arrive && mode != 3 && threadIdx.x == 0)
+        const bool remote = mode != 6 && mode != 7;
+        if (!remote_arrive && mode != 3 && remote && threadIdx.x == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(32u * csize) : "memory");
         __syncthreads();
         const bool sender = (mode == 1 || mode == 4) ? warp < csize : warp == kW - 1;
@@ -90,12 +95,17 @@ __global__ void __launch_bounds__(kT) k_probe(int mode, int iters, double* out, 
             t2 = warp_sum(t2);
             const int peer = (mode == 1 || mode == 4) ? warp : lane;
             const bool go = (mode == 1 || mode == 4) ? lane == 0 : lane < csize;
-            if (go) {
+            if (mode == 5 || mode == 9) {
+                const int pr = lane & 15;
+                if (pr < csize) {
+                    const unsigned dst = mapa(smem_u32(&tab[par][rank][0]), pr) + (lane >> 4) * 16u;
+                    st_async2(dst, lane < 16 ? t0s : t2, lane < 16 ? t1 : 0.0, mapa(b, pr));
+                }
+            } else if (mode == 6 || mode == 7) {
+                if (lane < csize) tab[par][lane][0] = t0s + t1 + t2;
+            } else if (go) {
                 const unsigned dst = mapa(smem_u32(&tab[par][rank][0]), peer);
-                if (mode == 0 || mode == 1) {
-                    st_async2(dst, t0s, t1, mapa(b, peer));
-                    st_async2(dst + 16, t2, 0.0, mapa(b, peer));
-                } else if (mode == 5) {
+                if (mode == 0 || mode == 1 || mode == 8) {
                     st_async2(dst, t0s, t1, mapa(b, peer));
                     st_async2(dst + 16, t2, 0.0, mapa(b, peer));
                 } else if (mode == 2 || mode == 4) {
@@ -114,12 +124,14 @@ __global__ void __launch_bounds__(kT) k_probe(int mode, int iters, double* out, 
         // ... local work would go here ...
         if (mode == 3) {
             cbar();
+        } else if (!remote) {
+            __syncwarp();
         } else if (remote_arrive) {
             mbar_wait_cluster(b, (it >> 1) & 1);
         } else {
             mbar_wait(b, (it >> 1) & 1);
         }
-        if (warp == kW - 1) {
+        if (warp == kW - 1 || mode == 9) {
             double g = 0.0, d = 0.0, r = 0.0;
             if (lane < csize) {
                 const double* src = mode == 3 ? cl.map_shared_rank(&tab[par][lane][0], lane) : &tab[par][lane][0];
@@ -130,15 +142,17 @@ __global__ void __launch_bounds__(kT) k_probe(int mode, int iters, double* out, 
             g = warp_sum(g);
             d = warp_sum(d);
             r = warp_sum(r);
-            const double alpha = g / (d + 1.0 + r * r);
-            if (lane == 0) {
-                scal[0] = alpha;
+            const double alpha = (mode == 7 || mode == 8) ? g * (d + 1.0 + r * r) : g / (d + 1.0 + r * r);
+            if (mode == 9) {
+                acc += 1e-12 * alpha;
+            } else {
+                if (lane == 0) scal[0] = alpha;
+                asm volatile("bar.arrive 1, %0;" ::"r"(kT) : "memory");
             }
-            asm volatile("bar.arrive 1, %0;" ::"r"(kT) : "memory");
         } else {
             asm volatile("bar.sync 1, %0;" ::"r"(kT) : "memory");
         }
-        acc += 1e-12 * scal[0];
+        if (mode != 9) acc += 1e-12 * scal[0];
         if (mode == 3) __syncthreads(); // scal reuse
     }
     const long long t1c = clock64();
@@ -157,7 +171,7 @@ int main() {
     cudaMalloc(&cyc, 64 * sizeof(long long));
     const int iters = 2000;
     for (int cs : {16, 8}) {
-        for (int mode = 0; mode <= 5; ++mode) {
+        for (int mode = 0; mode <= 9; ++mode) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(cs);
             cfg.blockDim = dim3(kT);
