@@ -25,6 +25,17 @@ single partition is the run_reference path (1-worker ADMM is bitwise the
 same algorithm, tests/test_gpu_admm.py). DABD_BENCH_SHARE_GPU=1 maps every
 rank to cuda:0 over gloo (a functional check of the N>1 path on one GPU; its
 timings are not scaling numbers).
+
+`--mode strong` (a second, opt-in mode for the C3/C5 story): the same
+pour-10k scene with 8 consensus partitions at every N, rank r owning
+partitions [8r/N, 8(r+1)/N); N=1 runs all 8 partitions batched on one GPU
+(the device-side ADMM frame), so N=1,2,4,8 run the same algorithm and
+`value` is whole-scene frames/s ("scaling": "strong"). Both modes start
+from a state the GPU reached itself in strong mode (30 single-domain frames
+of the pour, then 2 consensus frames), and the N=1 strong line also reports
+the undivided single-domain frame rate of the same state. The reference arm
+has no strong mode (an 8-partition pour frame costs the CPU oracle tens of
+minutes) and says so.
 """
 
 from __future__ import annotations
@@ -43,6 +54,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIG_N1 = "pile-1k"
+STRONG_SCENE, STRONG_PARTS, STRONG_SETTLE, STRONG_SPLIT = "pour-10k", 8, 30, 2
 
 
 def _ncu_traffic(kernel: str = "k_pcg_cluster"):
@@ -194,6 +206,34 @@ def bench_config(ws: int, share: bool = False):
     }
 
 
+def strong_config(ws: int, share: bool = False):
+    """Strong-scaling workload: pour-10k, 8 partitions over ws GPUs."""
+    from paper_2605_15875_b200.scene import make_scenario
+
+    sd = make_scenario(STRONG_SCENE)
+    return sd, {
+        "workload": STRONG_SCENE, "bodies": len(sd.bodies), "partitions": STRONG_PARTS,
+        "semantics": "consensus ADMM (runtime.cpp:110-694), the same 8 partitions at every N",
+        "unit_of_work": "one 10,000-body frame of the whole scene",
+        "start": f"pour-10k: {STRONG_SETTLE} single-domain + {STRONG_SPLIT} 8-partition frames on the GPU",
+        "l2": "flushed (256 MiB write) between timed steps (GPU arm)",
+        "parallelism": f"{STRONG_PARTS // ws} partition(s) per GPU x{ws}"
+                       + (" (gloo, shared GPU)" if share else (" (NCCL)" if ws > 1 else " (batched)")),
+    }
+
+
+def strong_start_state(api, sd):
+    """The strong mode's start state: every rank computes it itself (the
+    frames are deterministic, so all ranks hold the same bits)."""
+    ctx = api.Context(api.Scene(sd))
+    ctx.run_frames(STRONG_SETTLE)
+    q, qd = ctx.state()
+    c8 = api.Context(api.Scene(sd), num_workers=STRONG_PARTS)
+    c8.set_state(q, qd)
+    c8.run_frames(STRONG_SPLIT)
+    return c8.state()
+
+
 def run_reference_arm(args) -> None:
     """CPU reference arm: the oracle port of proj/src/sim.cpp:186-249 (N=1,
     single-threaded like the reference worker) or of the
@@ -207,6 +247,10 @@ def run_reference_arm(args) -> None:
     warm-up)."""
     ws, rank, _ = _dist()
     if rank != 0:
+        return
+    if args.mode == "strong":
+        print(json.dumps({"impl": "reference", "unavailable": "strong mode: one 8-partition pour-10k frame "
+                          "costs the CPU oracle tens of minutes; the reference arm runs the default mode"}))
         return
     O = _oracle()
     sd, config = bench_config(ws)
@@ -286,6 +330,8 @@ def main() -> None:
                     help="extra untimed GPU frames after loading the start state")
     ap.add_argument("--ref-budget", type=float, default=150.0,
                     help="reference arm at N > 1: wall-clock bound of the CPU sample (s)")
+    ap.add_argument("--mode", default="weak", choices=["weak", "strong"],
+                    help="weak: pile-1k slabs (default); strong: pour-10k, 8 partitions at every N")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -309,8 +355,13 @@ def main() -> None:
     from paper_2605_15875_b200 import _lib as L
     from paper_2605_15875_b200 import api
     lib = L.load()
-    workers = 0 if ws == 1 else ws
-    sd, config = bench_config(ws, share)
+    strong = args.mode == "strong"
+    if strong:
+        workers = STRONG_PARTS
+        sd, config = strong_config(ws, share)
+    else:
+        workers = 0 if ws == 1 else ws
+        sd, config = bench_config(ws, share)
     scene = api.Scene(sd)
     comm = None
     if ws > 1:
@@ -331,7 +382,7 @@ def main() -> None:
     ctx.set_stream(stream.cuda_stream)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    q0, qd0 = start_state(sd, ws)
+    q0, qd0 = strong_start_state(api, sd) if strong else start_state(sd, ws)
     ctx.set_state(q0, qd0)
     if args.settle > 0:
         ctx.run_frames(args.settle)
@@ -374,7 +425,7 @@ def main() -> None:
         t = torch.tensor([total_ms], device="cpu" if share else "cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = ws * args.steps / (total_ms / 1e3)
+    value = (1 if strong else ws) * args.steps / (total_ms / 1e3)
     admm = sum(s["admm_iterations"] for s in stats)
 
     # e2e through the public API with pinned host buffers every step
@@ -431,20 +482,38 @@ def main() -> None:
     line = {
         "metric": "sim_steps_per_sec", "value": value, "unit": "steps/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
         "config": config,
-        "admm_iters_per_sec": admm * ws / (total_ms / 1e3),
+        "admm_iters_per_sec": admm * (1 if strong else ws) / (total_ms / 1e3),
         "newton_iters_per_step": sum(s["newton_iterations"] for s in stats) / len(stats),
         "pcg_iters_per_step": sum(s["pcg_iterations"] for s in stats) / len(stats),
         "max_contacts": max(s["max_contacts"] for s in stats),
-        "e2e": {"value": ws * args.steps / (e2e_ms / 1e3), "unit": "steps/s",
+        "e2e": {"value": (1 if strong else ws) * args.steps / (e2e_ms / 1e3), "unit": "steps/s",
                 "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
         "gpu_launches": int(n1.value - n0.value),
         "roofline": roof,
         "clocks": clk.summary(),
     }
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if strong:
+        line["t_frame_split_ms"] = {  # host wall split of the timed frames (FrameStats)
+            "frame": 1e3 * sum(s["t_frame"] for s in stats) / len(stats),
+            "solve": 1e3 * sum(s["t_solve"] for s in stats) / len(stats),
+            "sync": 1e3 * sum(s["t_sync"] for s in stats) / len(stats)}
+        if ws == 1:  # the undivided single-domain frame rate of the same start state
+            c1 = api.Context(scene, device=local)
+            c1.set_stream(stream.cuda_stream)
+            c1.set_state(q_warm, qd_warm)
+            c1.run_frames(1)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            c1.run_frames(args.steps)
+            e1.record(stream)
+            e1.synchronize()
+            line["single_domain_steps_per_s"] = args.steps / (e0.elapsed_time(e1) / 1e3)
+        line["cpu_baseline"] = None  # see the reference arm
+    elif rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(sd, q_warm, qd_warm)
     if rank == 0:
         print(json.dumps(line), flush=True)

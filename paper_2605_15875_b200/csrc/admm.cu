@@ -74,7 +74,13 @@ __global__ void k_delta_inf(int n_rows, const int* rinst, const int* rpart, int 
 
 // body_holder_mask (partition.cpp:36-67), bit-exact.
 __global__ void k_masks(SceneView sc, const double* q, const double* planes, int np, double w,
-                        uint32_t all, uint32_t* masks, int* err) {
+                        uint32_t all, uint32_t* masks, int* err, const double* vmax_dev = nullptr,
+                        double h = 0.0, double w_min = 0.0, double* w_out = nullptr) {
+    if (vmax_dev) { // overlap width on the device: max(2 v_max h, w_min), host rounding (runtime.cpp:556-560)
+        const double x = xmul(xmul(2.0, *vmax_dev), h);
+        w = x < w_min ? w_min : x;
+        if (w_out && blockIdx.x == 0 && threadIdx.x == 0) *w_out = w;
+    }
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < sc.nb; b += gridDim.x * blockDim.x) {
         if (sc.is_static[b]) {
             masks[b] = all;
@@ -296,6 +302,92 @@ __global__ void k_accept_copy(int n, const int* ipart, int part_base, const Part
 }
 
 
+// ---- device-side instance sets (runtime.cpp:126-236) ----------------------
+__global__ void k_inst_flags(SceneView sc, const uint32_t* masks, int P, int p0, int* f_all, int* f_dyn,
+                             int* f_sh) {
+    const long long n = static_cast<long long>(P) * sc.nb;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int p = static_cast<int>(t / sc.nb), b = static_cast<int>(t - static_cast<long long>(p) * sc.nb);
+        const uint32_t m = masks[b];
+        const int in = static_cast<int>((m >> (p0 + p)) & 1u);
+        const int dyn = in && !sc.is_static[b];
+        f_all[t] = in;
+        f_dyn[t] = dyn;
+        f_sh[t] = dyn && __popc(m) >= 2 && (p0 + p) != __ffs(m) - 1;
+    }
+}
+
+__global__ void k_inst_counts(int P, int nb, const int* f_all, const int* f_dyn, const int* f_sh,
+                              const int* s_all, const int* s_dyn, const int* s_sh, int* counts) {
+    const long long n = static_cast<long long>(P) * nb;
+    const long long last = n - 1;
+    if (threadIdx.x == 0) {
+        counts[0] = n ? s_all[last] + f_all[last] : 0;
+        counts[1] = n ? s_dyn[last] + f_dyn[last] : 0;
+        counts[2] = n ? s_sh[last] + f_sh[last] : 0;
+    }
+    for (int p = threadIdx.x; p <= P; p += blockDim.x) {
+        const long long t = static_cast<long long>(p) * nb;
+        counts[3 + p] = p < P ? (n ? s_all[t] : 0) : (n ? s_all[last] + f_all[last] : 0);
+        counts[4 + P + p] = p < P ? (n ? s_dyn[t] : 0) : (n ? s_dyn[last] + f_dyn[last] : 0);
+    }
+}
+
+__global__ void k_inst_scatter(SceneView sc, const uint32_t* masks, int P, int p0, const int* f_all,
+                               const int* f_dyn, const int* f_sh, const int* s_all, const int* s_dyn,
+                               const int* s_sh, double beta, const double* rho_carry,
+                               const int* rowtab_prev, InstOut o) {
+    const int nb = sc.nb;
+    const long long n = static_cast<long long>(P) * nb;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int dyn = f_dyn[t];
+        o.rowtab[t] = dyn ? s_dyn[t] : -1;
+        if (!f_all[t]) continue;
+        const int p = static_cast<int>(t / nb), b = static_cast<int>(t - static_cast<long long>(p) * nb);
+        const uint32_t m = masks[b];
+        const int i = s_all[t];
+        const int kb = __popc(m);
+        o.ibody[i] = b;
+        o.ipart[i] = p0 + p;
+        o.invk[i] = 1.0 / kb;
+        const int anc = dyn && kb >= 2;
+        o.ianc[i] = anc;
+        const double r0 = anc ? xmul(beta, sc.mass[b]) : 0.0; // init_rho (consensus.cpp:38-42)
+        o.rho0[i] = r0;
+        o.rho[i] = anc ? (isnan(rho_carry[b]) ? r0 : rho_carry[b]) : 0.0;
+        if (dyn) {
+            const int row = s_dyn[t];
+            o.irow[i] = row;
+            o.rinst[row] = i;
+            o.rpart[row] = p0 + p;
+            o.wmap[row] = rowtab_prev ? rowtab_prev[t] : -1;
+        } else {
+            o.irow[i] = -1;
+            o.stat[i - s_dyn[t]] = i;
+        }
+        if (f_sh[t]) { // (first replica, this replica) in instance order
+            const int j = s_sh[t];
+            const int lowp = __ffs(m) - 1 - p0;
+            o.shared[2 * j] = s_all[static_cast<long long>(lowp) * nb + b];
+            o.shared[2 * j + 1] = i;
+        }
+    }
+}
+
+__global__ void k_rho_carry(int n_inst, int nb, const int* ibody, const int* ianc, const double* irho,
+                            double* carry) {
+    const int t0 = blockIdx.x * blockDim.x + threadIdx.x, st = gridDim.x * blockDim.x;
+    for (int b = t0; b < nb; b += st) carry[b] = __longlong_as_double(0x7ff8000000000000ll);
+    __syncthreads();
+    // replicas carry equal rho (k_consensus checks it): any one may stand in;
+    // a grid-stride pass after a grid-wide NaN fill needs the fill first, so
+    // the fill and the writes run in one block
+    for (int i = t0; i < n_inst; i += st)
+        if (ianc[i]) carry[ibody[i]] = irho[i];
+}
+
 __device__ __forceinline__ void admm_cond(unsigned long long h, bool v, int graph) {
     if (graph) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(h), v ? 1u : 0u);
 }
@@ -503,6 +595,42 @@ void launch_accept_copy(int n, const int* ipart, int part_base, const PartState*
 
 void launch_admm_ctrl(const AdmmCtrlArgs& a, int op, cudaStream_t s) {
     DABD_LAUNCH("k_admm_ctrl", s, k_admm_ctrl<<<1, 32, 0, s>>>(a, op));
+}
+
+void launch_inst_flags(const SceneView& sc, const uint32_t* masks, int P, int p0, int* f_all, int* f_dyn,
+                       int* f_sh, cudaStream_t s) {
+    const long long n = static_cast<long long>(P) * sc.nb;
+    if (n == 0) return;
+    DABD_LAUNCH("k_inst_flags", s, k_inst_flags<<<grid_for(n, 256), 256, 0, s>>>(sc, masks, P, p0, f_all, f_dyn, f_sh));
+}
+
+void launch_inst_counts(int P, int nb, const int* f_all, const int* f_dyn, const int* f_sh, const int* s_all,
+                        const int* s_dyn, const int* s_sh, int* counts, cudaStream_t s) {
+    DABD_LAUNCH("k_inst_counts", s, k_inst_counts<<<1, 64, 0, s>>>(P, nb, f_all, f_dyn, f_sh, s_all, s_dyn, s_sh, counts));
+}
+
+void launch_inst_scatter(const SceneView& sc, const uint32_t* masks, int P, int p0, const int* f_all,
+                         const int* f_dyn, const int* f_sh, const int* s_all, const int* s_dyn,
+                         const int* s_sh, double beta, const double* rho_carry, const int* rowtab_prev,
+                         InstOut o, cudaStream_t s) {
+    const long long n = static_cast<long long>(P) * sc.nb;
+    if (n == 0) return;
+    DABD_LAUNCH("k_inst_scatter", s, k_inst_scatter<<<grid_for(n, 256), 256, 0, s>>>(sc, masks, P, p0, f_all, f_dyn, f_sh, s_all,
+                                                                        s_dyn, s_sh, beta, rho_carry, rowtab_prev, o));
+}
+
+void launch_rho_carry(int n_inst, int nb, const int* ibody, const int* ianc, const double* irho,
+                      double* carry, cudaStream_t s) {
+    if (nb == 0) return;
+    DABD_LAUNCH("k_rho_carry", s, k_rho_carry<<<1, 1024, 0, s>>>(n_inst, nb, ibody, ianc, irho, carry));
+}
+
+void launch_masks_w(const SceneView& sc, const double* q, const double* planes, int np, const double* vmax,
+                    double h, double w_min, double* w_out, uint32_t all, uint32_t* masks, int* err,
+                    cudaStream_t s) {
+    if (sc.nb == 0) return;
+    DABD_LAUNCH("k_masks", s, k_masks<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, q, planes, np, 0.0, all, masks, err, vmax, h,
+                                                                   w_min, w_out));
 }
 
 } // namespace dabd_gpu

@@ -41,6 +41,32 @@ void launch_commit(const SceneView& sc, int n, const int* ibody, const int* ipar
 void launch_accept_copy(int n, const int* ipart, int part_base, const PartState* ps,
                         const double* src, double* dst, cudaStream_t s);
 
+// Device-side instance sets (runtime.cpp:126-236): flags of every
+// (partition, body) pair in partition-major order t = p * nb + b: in the
+// partition, dynamic in it, a replica past the body's lowest holder (a
+// shared-pair second). w: when vmax is given, the overlap width
+// max(2 v_max h, w_min) (runtime.cpp:556-560) is formed on the device.
+void launch_inst_flags(const SceneView& sc, const uint32_t* masks, int P, int p0, int* f_all, int* f_dyn,
+                       int* f_sh, cudaStream_t s);
+// counts: [0] instances, [1] rows, [2] shared pairs, [3, 3 + P] instance
+// offsets per partition, [4 + P, 5 + 2P] row offsets
+void launch_inst_counts(int P, int nb, const int* f_all, const int* f_dyn, const int* f_sh, const int* s_all,
+                        const int* s_dyn, const int* s_sh, int* counts, cudaStream_t s);
+struct InstOut {
+    int *ibody, *ipart, *irow, *rinst, *rpart, *stat, *ianc, *shared, *wmap, *rowtab, *pio, *pro;
+    double *invk, *rho, *rho0;
+};
+void launch_inst_scatter(const SceneView& sc, const uint32_t* masks, int P, int p0, const int* f_all,
+                         const int* f_dyn, const int* f_sh, const int* s_all, const int* s_dyn,
+                         const int* s_sh, double beta, const double* rho_carry, const int* rowtab_prev,
+                         InstOut o, cudaStream_t s);
+// rho carry (runtime.cpp:481-482): NaN everywhere, then each replica's rho
+void launch_rho_carry(int n_inst, int nb, const int* ibody, const int* ianc, const double* irho,
+                      double* carry, cudaStream_t s);
+void launch_masks_w(const SceneView& sc, const double* q, const double* planes, int np, const double* vmax,
+                    double h, double w_min, double* w_out, uint32_t all, uint32_t* masks, int* err,
+                    cudaStream_t s);
+
 // Device controller of the multi-partition consensus-ADMM frame
 // (runtime.cpp:316-476 and the controller round trip 572-638 for the
 // partitions of one context). ops: kAdmmInit, kAdmmHead (IF(gate) = k > 1;

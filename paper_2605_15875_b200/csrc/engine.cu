@@ -77,7 +77,7 @@ struct AdmmProfile {
     }
     ~AdmmProfile() {
         if (!on) return;
-        static const char* names[12] = {"frame_setup(rest)", "consensus+gate", "decision", "newton",
+        static const char* names[12] = {"frame_setup(rest)", "consensus+gate|capture", "decision", "newton|graph",
                                         "delta_inf", "commit", "other", "setup:masks", "setup:instances",
                                         "setup:prepare_solver(rest)", "prep:det_prepare", "prep:resizes"};
         for (int i = 0; i < 12; ++i)
@@ -370,6 +370,17 @@ void Engine::build_instances(const std::vector<std::vector<int>>& per_part, cons
     std::vector<std::pair<long long, int>> old_keys(h_rinst_.size());
     for (size_t r = 0; r < h_rinst_.size(); ++r)
         old_keys[r] = {(static_cast<long long>(h_rpart_[r]) << 32) | h_ibody_[h_rinst_[r]], static_cast<int>(r)};
+    if (h_rinst_.empty() && rowtab_valid_ && n_rows_ > 0) {
+        // the outgoing set came from the device builder: its (partition,
+        // body) -> row table stands in for the host lists
+        const std::vector<int> tab = rowtab_.to_host(s_);
+        const int nb = std::max(hs_.nb, 1);
+        for (size_t t = 0; t < tab.size(); ++t)
+            if (tab[t] >= 0)
+                old_keys.push_back({(static_cast<long long>(p0_ + static_cast<int>(t / nb)) << 32) |
+                                        static_cast<long long>(t % nb),
+                                    tab[t]});
+    }
     std::sort(old_keys.begin(), old_keys.end());
     const int r_old = n_rows_;
     h_ibody_.clear();
@@ -401,6 +412,16 @@ void Engine::build_instances(const std::vector<std::vector<int>>& per_part, cons
     h_pro_[P_] = static_cast<int>(h_rinst_.size());
     n_inst_ = static_cast<int>(h_ibody_.size());
     n_rows_ = static_cast<int>(h_rinst_.size());
+    n_stat_ = static_cast<int>(h_stat_.size());
+    {
+        // (partition, body) -> row table of this set, so a device-built set
+        // that follows carries the PCG warm start exactly as a host one would
+        const int nb = std::max(hs_.nb, 1);
+        std::vector<int> tab(static_cast<size_t>(P_) * nb, -1);
+        for (int r = 0; r < n_rows_; ++r) tab[static_cast<size_t>(h_rpart_[r] - p0_) * nb + h_ibody_[h_rinst_[r]]] = r;
+        rowtab_.upload(tab, s_);
+        rowtab_valid_ = true;
+    }
     if (n_inst_ >= (1 << 22)) throw InvalidArg("too many body instances for the candidate key");
     single_domain_ = single_domain;
     invalidate_list();
@@ -465,6 +486,113 @@ void Engine::build_instances(const std::vector<std::vector<int>>& per_part, cons
     }
     aoff_.resize(I + 1);
     boff_.resize(I + 1);
+}
+
+// Device-side instance set of a multi-partition attempt (runtime.cpp:126-236,
+// partition.cpp:69-129): the same sets, order and per-instance constants as
+// build_instances + frame_admm's host loops (instances sorted by (partition,
+// body), rows = dynamic instances, static list, 1/kappa_b, anchor flags,
+// rho0 = beta m_b and the carried rho, the shared-replica pairs, the PCG
+// warm-start map by (partition, body)), from flags of every (partition, body)
+// pair and three exclusive scans. One read-back: the counts (and w).
+int Engine::build_instances_device(const uint32_t* masks_dev, double* w_out) {
+    const int nb = hs_.nb;
+    const size_t n = static_cast<size_t>(P_) * std::max(nb, 1);
+    for (DBuf<int>* b : {&fl_all_, &fl_dyn_, &fl_sh_, &sc_all_, &sc_dyn_, &sc_sh_}) b->resize(n);
+    if (rowtab_.size() != n) rowtab_valid_ = false;
+    rowtab_.resize(n);
+    rowtab_prev_.resize(n);
+    inst_cnt_.resize(5 + 2 * static_cast<size_t>(P_));
+    inst_cnt_h_.resize(8 + 2 * static_cast<size_t>(P_));
+    launch_inst_flags(ds_.view(), masks_dev, P_, p0_, fl_all_.get(), fl_dyn_.get(), fl_sh_.get(), s_);
+    size_t tb = 0;
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, fl_all_.get(), sc_all_.get(), static_cast<int>(n)));
+    scan_temp_.resize(std::max<size_t>(tb, 1));
+    for (int k = 0; k < 3; ++k) {
+        const int* in = k == 0 ? fl_all_.get() : k == 1 ? fl_dyn_.get() : fl_sh_.get();
+        int* out = k == 0 ? sc_all_.get() : k == 1 ? sc_dyn_.get() : sc_sh_.get();
+        size_t t2 = tb;
+        CUDA_CHECK(cub::DeviceScan::ExclusiveSum(scan_temp_.get(), t2, in, out, static_cast<int>(n), s_));
+    }
+    launch_inst_counts(P_, nb, fl_all_.get(), fl_dyn_.get(), fl_sh_.get(), sc_all_.get(), sc_dyn_.get(),
+                       sc_sh_.get(), inst_cnt_.get(), s_);
+    CUDA_CHECK(cudaMemcpyAsync(inst_cnt_h_.get(), inst_cnt_.get(), (5 + 2 * P_) * sizeof(int),
+                               cudaMemcpyDeviceToHost, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pin_d_.get() + 160, gate_.get() + 1, sizeof(double), cudaMemcpyDeviceToHost, s_));
+    sync(); // the only host read of the instance build
+    if (w_out) *w_out = pin_d_[160];
+    const int I = inst_cnt_h_[0], R = inst_cnt_h_[1], ns = inst_cnt_h_[2];
+    if (I >= (1 << 22)) throw InvalidArg("too many body instances for the candidate key");
+    h_pio_.assign(inst_cnt_h_.get() + 3, inst_cnt_h_.get() + 4 + P_);
+    h_pro_.assign(inst_cnt_h_.get() + 4 + P_, inst_cnt_h_.get() + 5 + 2 * P_);
+    // host mirrors of the per-instance lists are not built on this path
+    h_ibody_.clear();
+    h_ipart_.clear();
+    h_irow_.clear();
+    h_rinst_.clear();
+    h_rpart_.clear();
+    h_stat_.clear();
+    const int r_old = n_rows_;
+    n_inst_ = I;
+    n_rows_ = R;
+    n_stat_ = I - R;
+    single_domain_ = false;
+    invalidate_list();
+    ref_ready_ = false;
+    graph_ok_ = false;
+    const size_t Ic = std::max(I, 1), Rc = std::max(R, 1);
+    for (DBuf<int>* b : {&ibody_, &ipart_, &irow_, &ianc_}) b->resize(Ic);
+    rinst_.resize(Rc);
+    rpart_.resize(Rc);
+    stat_.resize(std::max(I - R, 1));
+    pio_.resize(P_ + 1);
+    pro_.resize(P_ + 1);
+    shared_inst_.resize(2 * static_cast<size_t>(std::max(ns, 1)));
+    warm_map_.resize(Rc);
+    for (DBuf<double>* b : {&iq_, &iqtry_, &iqt_, &iz_, &iu_, &iznext_, &iqbefore_, &qref_}) b->resize(6 * Ic);
+    for (DBuf<double>* b : {&iinvk_, &irho_, &irho0_, &rb_, &sb_, &iskin_, &iskin_next_}) b->resize(Ic);
+    iu_.zero(s_);
+    // the previous rows' (x, p2) out of the way before the buffers are reused
+    const bool carry = rowtab_valid_ && r_old > 0;
+    if (carry) {
+        warm_prev_.resize(12 * static_cast<size_t>(r_old));
+        CUDA_CHECK(cudaMemcpyAsync(warm_prev_.get(), x_.get(), 6 * r_old * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+        CUDA_CHECK(cudaMemcpyAsync(warm_prev_.get() + 6 * r_old, pbuf_.get(), 6 * r_old * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, s_));
+        std::swap(rowtab_, rowtab_prev_);
+    }
+    InstOut o{ibody_.get(), ipart_.get(), irow_.get(), rinst_.get(), rpart_.get(), stat_.get(), ianc_.get(),
+              shared_inst_.get(), warm_map_.get(), rowtab_.get(), pio_.get(), pro_.get(),
+              iinvk_.get(), irho_.get(), irho0_.get()};
+    launch_inst_scatter(ds_.view(), masks_dev, P_, p0_, fl_all_.get(), fl_dyn_.get(), fl_sh_.get(), sc_all_.get(),
+                        sc_dyn_.get(), sc_sh_.get(), hs_.adapt.beta, rho_carry_d_.get(),
+                        carry ? rowtab_prev_.get() : nullptr, o, s_);
+    rowtab_valid_ = true;
+    CUDA_CHECK(cudaMemcpyAsync(pio_.get(), inst_cnt_.get() + 3, (P_ + 1) * sizeof(int), cudaMemcpyDeviceToDevice, s_));
+    CUDA_CHECK(cudaMemcpyAsync(pro_.get(), inst_cnt_.get() + 4 + P_, (P_ + 1) * sizeof(int),
+                               cudaMemcpyDeviceToDevice, s_));
+    for (DBuf<double>* b : {&rgrad_, &x_, &r_, &z_, &p0v_, &p1v_, &ap_}) b->resize(6 * Rc);
+    pbuf_.resize(12 * Rc);
+    if (carry) {
+        launch_warm_remap(R, warm_map_.get(), warm_prev_.get(), r_old, x_.get(), pbuf_.get(), s_);
+    } else {
+        x_.zero(s_);
+        pbuf_.zero(s_);
+    }
+    rdiag_.resize(36 * Rc);
+    rdinv_.resize(36 * Rc);
+    rval_.resize(Rc);
+    rowtmp_.resize(Rc);
+    rowtmp2_.resize(Rc);
+    ell_cnt_.resize(Rc);
+    ell_col_.resize(Rc * ell_w_);
+    ell_blk_.resize(Rc * ell_w_ * 36);
+    partial_.resize(static_cast<size_t>(segsum_chunks(std::max(I * 64, 1 << 16))) * P_ + P_);
+    bmask_.resize(std::max(nb, 1));
+    if (nb) CUDA_CHECK(cudaMemcpyAsync(bmask_.get(), masks_dev, nb * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s_));
+    aoff_.resize(Ic + 1);
+    boff_.resize(Ic + 1);
+    return ns;
 }
 
 void Engine::gather_iq(const double* q_dev) {
@@ -604,7 +732,7 @@ void Engine::prepare_solver() {
 }
 
 void Engine::enq_superset(const double* q0, const double* q1, bool swept) {
-    det_.enqueue(ds_.view(), iview(q0, q1), stat_.get(), static_cast<int>(h_stat_.size()), swept,
+    det_.enqueue(ds_.view(), iview(q0, q1), stat_.get(), n_stat_, swept,
                  frame_params_.d_hat, err_.get(), s_);
 }
 
@@ -626,7 +754,7 @@ void Engine::enq_list_rebuild() {
     launch_list_commit(n_inst_, iq_.get(), qref_.get(), iskin_next_.get(), iskin_.get(), s_);
     InstView iv = iview(iq_.get(), iq_.get());
     iv.skin = iskin_.get();
-    det_.enqueue(ds_.view(), iv, stat_.get(), static_cast<int>(h_stat_.size()), false,
+    det_.enqueue(ds_.view(), iv, stat_.get(), n_stat_, false,
                  frame_params_.d_hat, err_.get(), s_);
     launch_seg_offsets(det_.keys(), cap_, det_.d_count(), cfmt_, n_inst_, aoff_.get(), 0, nullptr, s_);
     launch_make_bkeys(det_.keys(), cap_, det_.d_count(), cfmt_, bkey_.get(), bidx_.get(), s_);
@@ -1034,7 +1162,7 @@ std::vector<int> Engine::broad_phase(const double* q, const double* q_end, doubl
         q1 = iqtry_.get();
     }
     const int n = det_gate_.build(ds_.view(), iview(iq_.get(), q1), stat_.get(),
-                                  static_cast<int>(h_stat_.size()), q_end != nullptr, margin,
+                                  n_stat_, q_end != nullptr, margin,
                                   ds_.max_verts, s_);
     std::vector<unsigned long long> keys(n);
     if (n) {
@@ -1095,7 +1223,7 @@ double Engine::ccd_toi(const double* q0, const double* q1, const int* subset, in
     gather_iq(g0.get());
     launch_gather(n_inst_, ibody_.get(), g1.get(), iqtry_.get(), s_);
     const int n = det_gate_.build(ds_.view(), iview(iq_.get(), iqtry_.get()), stat_.get(),
-                                  static_cast<int>(h_stat_.size()), true, 0.0, ds_.max_verts, s_);
+                                  n_stat_, true, 0.0, ds_.max_verts, s_);
     std::vector<double> init(P_, 2.0);
     gate_.upload(init, s_);
     // margin-0 swept candidates are exactly the reference set; the filter
@@ -1280,6 +1408,11 @@ std::vector<double> Engine::planes() const {
 }
 
 void Engine::get_rho(double* rho) const {
+    if (carry_on_device_) {
+        const std::vector<double> c = rho_carry_d_.to_host(s_);
+        std::copy(c.begin(), c.begin() + hs_.nb, rho);
+        return;
+    }
     std::copy(rho_carry_.begin(), rho_carry_.end(), rho);
 }
 
@@ -1537,6 +1670,8 @@ FrameStats Engine::frame_reference() {
 int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, int I, int ns,
                                 FrameStats& st, std::vector<double>& cost, int& grows, bool& exact) {
     const SimParams& P = frame_params_;
+    AdmmProfile& prof = admm_prof();
+    prof.mark(0, s_);
     if (gate_cap_ == 0) gate_cap_ = 64 * std::max(I, 1);
     det_gate_.ensure(I, ds_.max_verts, gate_cap_);
     admm_dq_.resize(std::max(P_, 1));
@@ -1594,7 +1729,7 @@ int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, in
                 // broad phase, CCD over its device count
                 launch_merged(I, ianc_.get(), iq_.get(), iznext_.get(), iqtry_.get(), s_);
                 det_gate_.enqueue(ds_.view(), iview(iq_.get(), iqtry_.get()), stat_.get(),
-                                  static_cast<int>(h_stat_.size()), true, 0.0, err_.get(), s_);
+                                  n_stat_, true, 0.0, err_.get(), s_);
                 launch_ccd(view(), det_gate_.keys(), det_gate_.cap(), det_gate_.d_count(), det_gate_.fmt(),
                            det_gate_.boxes(), iq_.get(), iqtry_.get(), 2, gate_.get(), s_);
                 launch_admm_ctrl(a, kAdmmDecide, s_);
@@ -1639,6 +1774,7 @@ int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, in
     CUDA_CHECK(cudaGraphDestroy(g));
     const long long inc[6] = {nodes_inc_[0], nodes_inc_[1], nodes_inc_[2], nodes_inc_[3], nodes_inc_[4],
                               nodes_inc_[5]};
+    prof.mark(1, s_);
 
     const auto t0 = std::chrono::steady_clock::now();
     CUDA_CHECK(cudaGraphLaunch(admm_exec_, s_));
@@ -1650,6 +1786,7 @@ int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, in
     CUDA_CHECK(cudaMemcpyAsync(admm_cost_h_.get(), admm_cost_.get(), P_ * sizeof(double), cudaMemcpyDeviceToHost, s_));
     CUDA_CHECK(cudaStreamSynchronize(s_));
     st.t_solve += seconds_since(t0);
+    prof.mark(3, s_);
     const FrameCtrl c = ctrl_h_[0];
     // kernels the replay executed: per conditional body its own nodes x its
     // executions (levels: 0 ADMM body, 1 gate, 2 solve, 3 Newton, 4 step, 5 ls)
@@ -1743,13 +1880,78 @@ FrameStats Engine::frame_admm(int frame) {
         frame_params_ = hs_.params;
         frame_params_.h = h;
         const SimParams& P = frame_params_;
+        std::vector<double> cost(P_, 0.0); // this attempt's per-partition compute cost
+        // the whole attempt on the device: instance sets, constants and the
+        // ADMM loop (no force split: its per-frame host table stays host-side)
+        const bool split_active =
+            !hs_.force_split.empty() && (hs_.force_split_frames < 0 || frame < hs_.force_split_frames);
+        const bool device_attempt = admm_device_ && use_graph_ && !distributed_ && !split_active;
+        if (device_attempt) {
+            if (!carry_on_device_) {
+                rho_carry_d_.resize(std::max(nb, 1));
+                rho_carry_d_.upload(rho_carry_, s_);
+                carry_on_device_ = true;
+            }
+            gate_.resize(std::max(P_, 2));
+            gate_.zero(s_);
+            launch_vmax(ds_.view(), qd_.get(), gate_.get(), s_);
+            masks_d_.resize(std::max(nb, 1));
+            launch_masks_w(ds_.view(), q_.get(), dplanes.get(), W_ - 1, gate_.get(), h, hs_.w_min, gate_.get() + 1,
+                           everyone, masks_d_.get(), err_.get(), s_);
+            prof.mark(7, s_);
+            double w = 0.0;
+            const int ns = build_instances_device(masks_d_.get(), &w); // synchronises once
+            w_last_ = w;
+            check_err("frame: holder masks");
+            prof.mark(8, s_);
+            prepare_solver();
+            prof.mark(9, s_);
+            const int I = n_inst_;
+            const size_t nq = 6 * static_cast<size_t>(nb);
+            if (nq) CUDA_CHECK(cudaMemcpyAsync(q_start_.get(), q_.get(), nq * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+            gather_iq(q_.get());
+            launch_predict(ds_.view(), I, ibody_.get(), iq_.get(), qd_.get(), h, P.gravity[0], P.gravity[1], nullptr,
+                           iqt_.get(), s_);
+            if (I) CUDA_CHECK(cudaMemcpyAsync(iz_.get(), iqt_.get(), 6 * I * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+            const double tol = P.theta * h * P.scene_scale;
+            const int r = n_rows_ > 0 ? admm_attempt_device(frame, attempt, h, tol, I, ns, st, cost, dev_grows, dev_exact)
+                                      : -1;
+            if (r == 0) continue; // a capacity grew / the exact-solve retry is armed: redo the attempt
+            if (r == 2) {         // blocked merge at K: h halves (runtime.cpp:603-642)
+                tsc_.on_frame_failed();
+                ++attempt;
+                continue;
+            }
+            if (r == 1) {
+                // rho carry + commit (runtime.cpp:481-506), on the device
+                launch_rho_carry(I, nb, ibody_.get(), ianc_.get(), irho_.get(), rho_carry_d_.get(), s_);
+                launch_commit(ds_.view(), I, ibody_.get(), ipart_.get(), ianc_.get(), bmask_.get(), iq_.get(),
+                              iznext_.get(), q_start_.get(), h, q_.get(), qd_.get(), s_);
+                if (hs_.balance.enabled && W_ > 1) {
+                    for (int p = 0; p < P_; ++p) part_cost_[p0_ + p] = cost[p];
+                    have_costs_ = true;
+                }
+                sync();
+                prof.mark(5, s_);
+                tsc_.on_frame_committed();
+                st.exact_retries = static_cast<int>(exact_retries_ - exact0);
+                st.capacity_retries = static_cast<int>(capacity_retries_ - cap0);
+                st.committed = 1;
+                return st;
+            }
+            // no dynamic instance: nothing to solve; fall through to the host path
+        }
+        if (carry_on_device_) { // the host path owns the carry from here
+            rho_carry_ = rho_carry_d_.to_host(s_);
+            rho_carry_.resize(nb);
+            carry_on_device_ = false;
+        }
         // overlap width from the current velocities (runtime.cpp:556-560)
         gate_.zero(s_);
         launch_vmax(ds_.view(), qd_.get(), gate_.get(), s_);
         const double v_max = gate_.to_host(s_)[0];
         const double w = std::max(2.0 * v_max * h, hs_.w_min);
         w_last_ = w;
-        std::vector<double> cost(P_, 0.0); // this attempt's per-partition compute cost
         // holder masks (partition.cpp:36-67)
         DBuf<uint32_t> dm;
         dm.resize(std::max(nb, 1));
@@ -1855,18 +2057,7 @@ FrameStats Engine::frame_admm(int frame) {
         // A local failure on one rank must not leave its peers blocked in a
         // collective: it is carried to the next agreement point instead.
         std::string fail;
-        const bool device_loop = admm_device_ && use_graph_ && !distributed_ && n_rows_ > 0;
-        if (device_loop) {
-            const int r = admm_attempt_device(frame, attempt, h, tol, I, ns, st, cost, dev_grows, dev_exact);
-            if (r == 0) continue; // a capacity grew / the exact-solve retry is armed: redo the attempt
-            if (r == 2) {         // blocked merge at K: h halves (runtime.cpp:603-642)
-                tsc_.on_frame_failed();
-                retry = true;
-            } else {
-                ended = true;
-            }
-        }
-        for (int k = 1; !device_loop && k <= hs_.admm_max_iterations; ++k) {
+        for (int k = 1; k <= hs_.admm_max_iterations; ++k) {
             if (k > 1) {
                 std::vector<double> earliest(P_, 2.0), rl(P_, 0.0), sl(P_, 0.0);
                 try {
@@ -1892,7 +2083,7 @@ FrameStats Engine::frame_admm(int frame) {
                     if (gate_cap_ == 0) gate_cap_ = 64 * std::max(I, 1);
                     det_gate_.ensure(I, ds_.max_verts, gate_cap_);
                     det_gate_.enqueue(ds_.view(), iview(iq_.get(), iqtry_.get()), stat_.get(),
-                                      static_cast<int>(h_stat_.size()), true, 0.0, err_.get(), s_);
+                                      n_stat_, true, 0.0, err_.get(), s_);
                     for (int p = 0; p < P_; ++p) pin_d_[128 + p] = 2.0;
                     CUDA_CHECK(cudaMemcpyAsync(gate_.get(), pin_d_.get() + 128, P_ * sizeof(double),
                                                cudaMemcpyHostToDevice, s_));
@@ -1917,7 +2108,7 @@ FrameStats Engine::frame_admm(int frame) {
                     if (pin_i_[8] == kErrCapacity) { // grow and redo this gate with the counted build
                         err_.zero(s_);
                         const int nc = det_gate_.build(ds_.view(), iview(iq_.get(), iqtry_.get()),
-                                                       stat_.get(), static_cast<int>(h_stat_.size()),
+                                                       stat_.get(), n_stat_,
                                                        true, 0.0, ds_.max_verts, s_);
                         gate_cap_ = det_gate_.cap();
                         gate_.upload(earliest, s_);

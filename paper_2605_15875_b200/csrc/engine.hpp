@@ -210,7 +210,19 @@ class Engine {
     double w_last_ = 0.0;
 
     // instance set (host mirrors + device)
-    int n_inst_ = 0, n_rows_ = 0;
+    int n_inst_ = 0, n_rows_ = 0, n_stat_ = 0;
+    // Device-side instance sets (runtime.cpp:126-236, partition.cpp:69-129):
+    // holder masks -> (partition, body) flags -> scans -> scatter, with one
+    // read-back of the counts. Returns the number of shared-replica pairs;
+    // host mirrors h_ibody_ ... are not filled (only h_pio_ / h_pro_).
+    int build_instances_device(const uint32_t* masks_dev, double* w_out);
+    DBuf<int> fl_all_, fl_dyn_, fl_sh_, sc_all_, sc_dyn_, sc_sh_, rowtab_, rowtab_prev_, inst_cnt_;
+    PinnedBuf<int> inst_cnt_h_;
+    DBuf<unsigned char> scan_temp_;
+    bool rowtab_valid_ = false;
+    DBuf<double> rho_carry_d_;   // device rho carry (NaN = none), authoritative when carry_on_device_
+    bool carry_on_device_ = false;
+    DBuf<uint32_t> masks_d_;
     bool single_domain_ = true;
     std::vector<int> h_ibody_, h_ipart_, h_irow_, h_rinst_, h_rpart_, h_stat_;
     std::vector<int> h_pio_, h_pro_;

@@ -80,6 +80,13 @@ struct PcgArgs {
     int spread;   // 1: every warp sends to one peer (partials + halo); 0: the scalar warp sends to
                   // all (two remote stores per peer), 2: the same in one 32-lane store
     int fold_all; // 1: every warp folds the cluster partials itself, 0: the scalar warp folds
+    int remote_first; // 1: remote-column SpMV before the scalar hand-off
+    int fast_rcp;     // 1: alpha from a MUFU reciprocal + 2 Newton steps, 0: IEEE division
+    // inexact Newton (fused cluster kernel): a partition whose previous
+    // Newton direction had ||dq||_inf > eta_factor * tol solves to the
+    // relative residual eta_loose instead of tol (0: always tol)
+    double eta_loose;
+    double eta_factor;
 };
 
 // Block-local, partition-segmented sum of rowval over this block's chunk,
@@ -367,6 +374,17 @@ __device__ __forceinline__ double warp_sum3(double a, double b, double c, int la
     return v;
 }
 
+// 1/x from the MUFU approximation and two Newton steps (a few ulp; the CG
+// scalars need not be correctly rounded, only identical in every CTA)
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 __device__ __forceinline__ void cluster_barrier() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -452,6 +470,10 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     const PartState& st = sv.ps[p];
     const bool act = st.active != 0 && R1 > R0;
     double eps = st.eps;
+    // inexact Newton: loose while the previous direction of this solve was
+    // far above the Newton tolerance (uniform across the cluster)
+    const bool loose = a.fused && a.eta_loose > 0.0 && st.dq_last > a.eta_factor * st.tol;
+    const double tol_p = loose ? fmax(a.tol, a.eta_loose) : a.tol;
     // shared-memory carve-up (cmax_rows = chunk upper bound used at launch)
     const int V = 6 * cmax_rows;
     double* vm0 = reinterpret_cast<double*>(smem); // m = Dinv w, double-buffered by parity
@@ -1176,12 +1198,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             const double gamma = __shfl_sync(0xffffffffu, fv, 0), delta = __shfl_sync(0xffffffffu, fv, 8),
                          rr = __shfl_sync(0xffffffffu, fv, 16);
             if (it == 0) bnorm2 = bnorm2_ws >= 0.0 ? bnorm2_ws : rr;
-            stop = bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters;
+            stop = bnorm2 == 0.0 || rr <= tol_p * tol_p * bnorm2 || it >= a.max_iters;
             // beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
             // with the previous iteration's reciprocals: one division on the
             // critical path
             beta = gamma * inv_gamma_old;
-            alpha = gamma / (delta - beta * gamma * inv_alpha_old);
+            alpha = a.fast_rcp ? gamma * fast_rcp(delta - beta * gamma * inv_alpha_old)
+                               : gamma / (delta - beta * gamma * inv_alpha_old);
             stop = stop || !(alpha > 0.0) || !isfinite(alpha); // breakdown
             if (!a.fold_all) {
                 if (lane == 0) {
@@ -1191,11 +1214,18 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 }
                 asm volatile("bar.arrive 1, %0;" ::"r"(kCT) : "memory");
             }
-            inv_gamma_old = 1.0 / gamma; // off the critical path: next iteration
-            inv_alpha_old = 1.0 / alpha;
+            inv_gamma_old = fast_rcp(gamma); // off the critical path: next iteration
+            inv_alpha_old = fast_rcp(alpha);
         }
-        // the other warps keep the shared-memory pipe idle while the scalar
-        // warp's shuffle tree runs, then take the remote half of n
+        // remote_first: the other warps take the remote half of n while the
+        // scalar warp folds (it needs no scalar); else they keep the shared-
+        // memory pipe idle for the scalar warp's shuffle tree and take it after
+        double nrem[G];
+        const bool early = a.remote_first && !folder;
+        if (early) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) nrem[g] = on[g] ? spmv_remote(lrg[g], hv, moff, nloc[g], true) : 0.0;
+        }
         if (!folder) {
             asm volatile("bar.sync 1, %0;" ::"r"(kCT) : "memory");
             beta = sc.scal[0];
@@ -1203,9 +1233,10 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             stop = sc.scal[2] != 0.0;
         }
         if (stop) break; // uniform across the CTA and the cluster
-        double nrem[G];
+        if (!early) {
 #pragma unroll
-        for (int g = 0; g < G; ++g) nrem[g] = on[g] ? spmv_remote(lrg[g], hv, moff, nloc[g], true) : 0.0;
+            for (int g = 0; g < G; ++g) nrem[g] = on[g] ? spmv_remote(lrg[g], hv, moff, nloc[g], true) : 0.0;
+        }
         mark(5);
         // ---- the recurrences, then m = Dinv w and the partials of the next
         // iteration (register-resident)
@@ -1258,6 +1289,8 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             double mm = 0.0;
             for (int k = 0; k < csize; ++k) mm = fmax(mm, sc.dqm[k]);
             sv.ps[p].dq_inf = mm;
+            sv.ps[p].dq_last = mm;
+            sv.ps[p].loose = loose ? 1 : 0;
         }
         // the last partition's cluster takes kOpNewtonCheck for all of them
         __threadfence();
@@ -1268,7 +1301,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             int any_act = 0, any_srch = 0;
             for (int q = 0; q < sv.n_parts; ++q) {
                 if (a.ctrl) a.ctrl->pcg_total += vps[q].pcg_iters;
-                if (vps[q].active && vps[q].dq_inf < vps[q].tol) {
+                if (vps[q].active && vps[q].dq_inf < vps[q].tol && !vps[q].loose) {
                     vps[q].final_update = vps[q].dq_inf;
                     vps[q].converged = 1;
                     vps[q].active = 0;
@@ -1399,6 +1432,21 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
         return e ? std::atoi(e) : 0;
     }();
     a.fold_all = fold_all;
+    static const int remote_first = [] {
+        const char* e = std::getenv("DABD_GPU_PCG_REMOTE_FIRST");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.remote_first = remote_first;
+    static const int frcp = [] {
+        const char* e = std::getenv("DABD_GPU_PCG_FAST_RCP");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.fast_rcp = frcp;
+    static const double eta[2] = {
+        [] { const char* e = std::getenv("DABD_GPU_PCG_ETA"); return e ? std::atof(e) : 0.0; }(),
+        [] { const char* e = std::getenv("DABD_GPU_PCG_ETA_FACTOR"); return e ? std::atof(e) : 100.0; }()};
+    a.eta_loose = eta[0];
+    a.eta_factor = eta[1];
     if (fuse) {
         a.fused = 1;
         a.row_trace = fuse->row_trace;

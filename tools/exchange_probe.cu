@@ -17,7 +17,6 @@
 #include <cstdio>
 
 namespace cg = cooperative_groups;
-constexpr int kT = 512, kW = kT / 32;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -51,7 +50,9 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+template <int kT>
 __global__ void __launch_bounds__(kT) k_probe(int mode, int iters, double* out, long long* cycles) {
+    constexpr int kW = kT / 32;
     cg::cluster_group cl = cg::this_cluster();
     __shared__ __align__(16) double tab[2][16][4];
     __shared__ double red[kW][3];
@@ -163,15 +164,27 @@ __global__ void __launch_bounds__(kT) k_probe(int mode, int iters, double* out, 
     }
 }
 
+template <int kT>
+void run_all(double* out, long long* cyc);
+
 int main() {
-    cudaFuncSetAttribute(k_probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     double* out;
     long long* cyc;
     cudaMalloc(&out, 64 * sizeof(double));
     cudaMalloc(&cyc, 64 * sizeof(long long));
+    run_all<512>(out, cyc);
+    run_all<256>(out, cyc);
+    run_all<128>(out, cyc);
+    return 0;
+}
+
+template <int kT>
+void run_all(double* out, long long* cyc) {
+    cudaFuncSetAttribute(k_probe<kT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     const int iters = 2000;
     for (int cs : {16, 8}) {
         for (int mode = 0; mode <= 9; ++mode) {
+            if ((mode == 1 || mode == 4) && kT / 32 < cs) continue; // warp k -> peer k needs csize warps
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(cs);
             cfg.blockDim = dim3(kT);
@@ -182,15 +195,14 @@ int main() {
             at[0].val.clusterDim.z = 1;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&cfg, k_probe, mode, iters, out, cyc);
+            for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&cfg, k_probe<kT>, mode, iters, out, cyc);
             cudaError_t e = cudaDeviceSynchronize();
             long long h[64];
             cudaMemcpy(h, cyc, cs * sizeof(long long), cudaMemcpyDeviceToHost);
             long long mx = 0;
             for (int i = 0; i < cs; ++i) mx = h[i] > mx ? h[i] : mx;
-            printf("{\"csize\": %d, \"mode\": %d, \"cycles_per_round\": %.1f, \"err\": \"%s\"}\n", cs, mode,
+            printf("{\"threads\": %d, \"csize\": %d, \"mode\": %d, \"cycles_per_round\": %.1f, \"err\": \"%s\"}\n", kT, cs, mode,
                    double(mx) / iters, cudaGetErrorString(e));
         }
     }
-    return 0;
 }

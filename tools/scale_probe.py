@@ -47,6 +47,10 @@ def main():
             "max_contacts": max(s["max_contacts"] for s in st),
             "intersecting_end": hit, "violating_pairs_end": nviol, "min_distance_end": dmin,
             "audit_ms": 1e3 * t_audit,
+            # per-frame wall split (FrameStats): the solve graph vs host setup + commit
+            "t_frame_ms": 1e3 * sum(s["t_frame"] for s in st) / frames,
+            "t_solve_ms": 1e3 * sum(s["t_solve"] for s in st) / frames,
+            "host_setup_frac": 1.0 - sum(s["t_solve"] for s in st) / max(sum(s["t_frame"] for s in st), 1e-12),
         }
         print(json.dumps(out), flush=True)
 
