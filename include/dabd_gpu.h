@@ -27,6 +27,7 @@
  *   dabd_gpu_contact3d_terms     3D extension of contact_energy  src/energy.cpp:63-94 (PT / EE, no reference)
  *   dabd_gpu_ccd3d               3D extension of ccd_toi          src/geometry.cpp:232-341 (no reference)
  *   dabd_gpu_broad_phase3d       3D extension of broad_phase      src/geometry.cpp:106-208 (no reference)
+ *   dabd_gpu_sim3d_*             3D extension of run_reference    src/sim.cpp:186-249 + newton.cpp:7-71 (no reference)
  *   dabd_gpu_balancer_*          Balancer, imbalance_metric, pd_update, balance_factor
  *                                                                include/dabd/balance.hpp:9-56
  *   dabd_gpu_run_frames          run_reference (workers==0)      src/sim.cpp:186-249
@@ -189,6 +190,15 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_create(const dabd_gpu_scene* scene, in
 DABD_GPU_API void dabd_gpu_ctx_free(dabd_gpu_ctx* ctx);
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_solver(dabd_gpu_ctx* ctx,
                                                      const dabd_gpu_solver_params* p);
+/* Inexact Newton inside frames (the cluster PCG of partitions up to 4096
+ * rows): a Newton direction may stop at the relative residual `eta` (instead
+ * of pcg_rel_tol) while its ||dq||_inf exceeds `factor` x the Newton
+ * tolerance theta h l, so every direction that can decide convergence
+ * (newton.cpp:30-36) or end a line search (newton.cpp:56-62) is still solved
+ * to pcg_rel_tol. eta <= pcg_rel_tol (e.g. 0) turns it off. Default 1e-4,
+ * factor 10; dabd_gpu_newton_solve always solves every direction to
+ * pcg_rel_tol. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_inexact(dabd_gpu_ctx* ctx, double eta, double factor);
 /* Stream (cudaStream_t as uintptr_t) the context launches on; 0 = own stream. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_stream(dabd_gpu_ctx* ctx, uintptr_t stream);
 /* Join a partition-per-GPU run (comm == NULL leaves it). Required when the
@@ -369,6 +379,47 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_broad_phase3d(int device, int n_bodies, co
                                                     const int* tris, const int* edge_start,
                                                     const int* edges, double margin, int* pairs,
                                                     int capacity, int* count);
+
+/* ---- 3D affine-body scene stepping -------------------
+ * run_reference (sim.cpp:186-249) with newton.cpp:7-71 for 12-DoF bodies on
+ * the 3D primitives above: predict q~ = q + h qdot + h^2 g, then Newton on
+ * 1/2 (q - q~)^T M (q - q~) + h^2 kappa_arap vol ||A^T A - I||^2 + h^2 sum b(d)
+ * (PSD-projected terms, eps I of newton.cpp:20-24, a block-Jacobi PCG on
+ * 12x12 blocks, the CCD bound 0.9 toi and halving line search). Bodies as in
+ * dabd_gpu_broad_phase3d (rest vertices about each body's centroid),
+ * moments10 / volume from dabd_gpu_body3d_moments, q0 / qd0 [n][12]. No
+ * reference frame exists to compare with (the reference is 2D). */
+typedef struct dabd_gpu_sim3d dabd_gpu_sim3d;
+typedef struct {
+    double h;
+    double gravity[3];
+    double d_hat, kappa, kappa_arap;
+    double theta, scene_scale; /* Newton tolerance theta h l on ||dq||_inf */
+    int newton_cap;
+    double pcg_rel_tol;
+    int pcg_max_iters;
+} dabd_gpu_sim3d_params;
+typedef struct {
+    int newton_iterations, line_search_steps, pcg_iterations, max_candidates, converged;
+    double min_distance; /* over the pairs within d_hat at the committed state (0: none) */
+} dabd_gpu_sim3d_stats;
+DABD_GPU_API dabd_gpu_status dabd_gpu_sim3d_create(int device, int n_bodies, const int* vert_start,
+                                                   const double* verts, const int* tri_start,
+                                                   const int* tris, const int* edge_start,
+                                                   const int* edges, const int* is_static,
+                                                   const double* moments10, const double* volume,
+                                                   const double* q0, const double* qd0,
+                                                   const dabd_gpu_sim3d_params* params,
+                                                   dabd_gpu_sim3d** out);
+DABD_GPU_API void dabd_gpu_sim3d_free(dabd_gpu_sim3d* sim);
+DABD_GPU_API dabd_gpu_status dabd_gpu_sim3d_run(dabd_gpu_sim3d* sim, int frames, dabd_gpu_sim3d_stats* stats);
+DABD_GPU_API dabd_gpu_status dabd_gpu_sim3d_get_state(dabd_gpu_sim3d* sim, double* q, double* qd);
+DABD_GPU_API dabd_gpu_status dabd_gpu_sim3d_set_state(dabd_gpu_sim3d* sim, const double* q, const double* qd);
+/* The Newton system of the next frame's first iteration at the current state:
+ * H [12R][12R] (dense, + eps I), g [12R] and the PCG direction dq [12R] for
+ * the R dynamic bodies in body order; *rows = R. Buffers sized for 12 n. */
+DABD_GPU_API dabd_gpu_status dabd_gpu_sim3d_system(dabd_gpu_sim3d* sim, double* H, double* g, double* dq,
+                                                   int* rows);
 
 /* ---- PD load balancer (host control logic, no device) ----------------------
  * balance.cpp:8-83: imbalance T = (eta-1)/(eta+1), eta = tau_i/tau_j (times

@@ -63,12 +63,27 @@ class Comm(C.Structure):
                 ("rank", C.c_int), ("world", C.c_int), ("part_offsets", _ip)]
 
 
+class Sim3dParams(C.Structure):
+    """dabd_gpu_sim3d_params (include/dabd_gpu.h)."""
+    _fields_ = [("h", C.c_double), ("gravity", C.c_double * 3), ("d_hat", C.c_double),
+                ("kappa", C.c_double), ("kappa_arap", C.c_double), ("theta", C.c_double),
+                ("scene_scale", C.c_double), ("newton_cap", C.c_int), ("pcg_rel_tol", C.c_double),
+                ("pcg_max_iters", C.c_int)]
+
+
+class Sim3dStats(C.Structure):
+    """dabd_gpu_sim3d_stats (include/dabd_gpu.h)."""
+    _fields_ = [("newton_iterations", C.c_int), ("line_search_steps", C.c_int),
+                ("pcg_iterations", C.c_int), ("max_candidates", C.c_int), ("converged", C.c_int),
+                ("min_distance", C.c_double)]
+
+
 # Every symbol include/dabd_gpu.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "dabd_gpu_version", "dabd_gpu_last_error", "dabd_gpu_scene_create", "dabd_gpu_scene_free",
     "dabd_gpu_scene_set_params", "dabd_gpu_scene_set_planes", "dabd_gpu_scene_set_force_split",
     "dabd_gpu_scene_counts", "dabd_gpu_scene_bodies", "dabd_gpu_ctx_create", "dabd_gpu_ctx_free",
-    "dabd_gpu_ctx_set_solver", "dabd_gpu_ctx_set_stream", "dabd_gpu_broad_phase",
+    "dabd_gpu_ctx_set_solver", "dabd_gpu_ctx_set_inexact", "dabd_gpu_ctx_set_stream", "dabd_gpu_broad_phase",
     "dabd_gpu_narrow_phase", "dabd_gpu_ccd_toi", "dabd_gpu_holder_masks", "dabd_gpu_audit", "dabd_gpu_objective",
     "dabd_gpu_newton_solve", "dabd_gpu_run_frames", "dabd_gpu_set_state", "dabd_gpu_get_state",
     "dabd_gpu_get_rho", "dabd_gpu_take_trace", "dabd_gpu_launch_count",
@@ -81,6 +96,8 @@ EXPORTS = [
     "dabd_gpu_body3d_moments", "dabd_gpu_body3d_terms",
     "dabd_gpu_broad_phase3d", "dabd_gpu_ctx_comm_mode", "dabd_gpu_consensus_step",
     "dabd_gpu_check_stopping", "dabd_gpu_timestep_apply",
+    "dabd_gpu_sim3d_create", "dabd_gpu_sim3d_free", "dabd_gpu_sim3d_run", "dabd_gpu_sim3d_get_state",
+    "dabd_gpu_sim3d_set_state", "dabd_gpu_sim3d_system",
 ]
 
 _lib = None
@@ -105,8 +122,11 @@ def load():
     lib.dabd_gpu_scene_free.argtypes = [C.c_void_p]
     lib.dabd_gpu_scene_free.restype = None
     lib.dabd_gpu_ctx_free.argtypes = [C.c_void_p]
+    lib.dabd_gpu_sim3d_free.argtypes = [C.c_void_p]
+    lib.dabd_gpu_sim3d_free.restype = None
     lib.dabd_gpu_ctx_free.restype = None
     lib.dabd_gpu_ctx_set_stream.argtypes = [C.c_void_p, C.c_size_t]
+    lib.dabd_gpu_ctx_set_inexact.argtypes = [C.c_void_p, C.c_double, C.c_double]
     lib.dabd_gpu_balancer_free.argtypes = [C.c_void_p]
     lib.dabd_gpu_balancer_free.restype = None
     for fn in ("dabd_gpu_imbalance_metric", "dabd_gpu_pd_update"):

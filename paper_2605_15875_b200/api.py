@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from typing import List, Optional, Sequence
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -103,7 +103,8 @@ class Context:
 
     def __init__(self, scene: Scene, device: int = 0, num_workers: int = 0,
                  part_begin: int = 0, part_end: Optional[int] = None,
-                 pcg_rel_tol: Optional[float] = None, pcg_max_iters: Optional[int] = None) -> None:
+                 pcg_rel_tol: Optional[float] = None, pcg_max_iters: Optional[int] = None,
+                 inexact: Optional[Tuple[float, float]] = None) -> None:
         lib = L.load()
         self.scene = scene
         if part_end is None:
@@ -116,6 +117,8 @@ class Context:
         self.num_workers = num_workers
         if pcg_rel_tol is not None or pcg_max_iters is not None:
             self.set_solver(pcg_rel_tol or 1e-10, pcg_max_iters or 4000)
+        if inexact is not None:
+            self.set_inexact(*inexact)
 
     def __del__(self):
         try:
@@ -125,6 +128,10 @@ class Context:
 
     def set_solver(self, rel_tol: float, max_iters: int) -> None:
         L.check(L.load().dabd_gpu_ctx_set_solver(self.h, C.byref(L.SolverParams(rel_tol, max_iters))))
+
+    def set_inexact(self, eta: float, factor: float = 10.0) -> None:
+        """Inexact Newton inside frames (dabd_gpu_ctx_set_inexact); eta=0: off."""
+        L.check(L.load().dabd_gpu_ctx_set_inexact(self.h, C.c_double(eta), C.c_double(factor)))
 
     def set_stream(self, stream_handle: int) -> None:
         L.check(L.load().dabd_gpu_ctx_set_stream(self.h, int(stream_handle)))
@@ -524,6 +531,89 @@ def broad_phase3d(q, meshes, margin: float, q_end=None, device: int = 0) -> np.n
             continue
         L.check(st)
         return out[: cnt.value].copy()
+
+
+def cube_mesh(half):
+    """Closed, outward-oriented box surface about its centroid: verts [8][3],
+    tris [12][3], edges [12][2] (half = scalar or (hx, hy, hz))."""
+    hx, hy, hz = (half, half, half) if np.isscalar(half) else half
+    v = np.array([[x, y, z] for x in (-hx, hx) for y in (-hy, hy) for z in (-hz, hz)], float)
+    # vertex index = 4 ix + 2 iy + iz; two triangles per face, outward normals
+    quads = [(0, 1, 3, 2), (4, 6, 7, 5), (0, 4, 5, 1), (2, 3, 7, 6), (0, 2, 6, 4), (1, 5, 7, 3)]
+    tris = []
+    for a, b, c, d in quads:
+        tris += [(a, b, c), (a, c, d)]
+    edges = sorted({tuple(sorted(e)) for a, b, c, d in quads for e in ((a, b), (b, c), (c, d), (d, a))})
+    return v, np.array(tris, np.int32), np.array(edges, np.int32)
+
+
+class Sim3D:
+    """3D affine-body scene stepping on the device (dabd_gpu_sim3d_*; the
+    reference's run_reference + newton_solve in 3D). bodies: list of
+    (verts [k][3] about the centroid, tris, edges, centre (3,), static)."""
+
+    def __init__(self, bodies, h=1.0 / 60.0, gravity=(0.0, -9.81, 0.0), d_hat=1e-2, kappa=1e3,
+                 kappa_arap=1e4, theta=1e-3, scene_scale=1.0, newton_cap=64, pcg_rel_tol=1e-10,
+                 pcg_max_iters=4000, density=1000.0, qd0=None, device: int = 0) -> None:
+        lib = L.load()
+        n = len(bodies)
+        vs, ts, es, V, T, E, mom, vol, stat = [0], [0], [0], [], [], [], [], [], []
+        q0 = np.zeros((n, 12))
+        for i, (v, t, e, centre, static) in enumerate(bodies):
+            v = np.asarray(v, float).reshape(-1, 3)
+            V.append(v)
+            T.append(np.asarray(t, np.int32).reshape(-1, 3))
+            E.append(np.asarray(e, np.int32).reshape(-1, 2))
+            vs.append(vs[-1] + len(v))
+            ts.append(ts[-1] + len(T[-1]))
+            es.append(es[-1] + len(E[-1]))
+            m, _, vl = body3d_moments(v, T[-1], density)
+            mom.append(m)
+            vol.append(vl)
+            stat.append(1 if static else 0)
+            q0[i, :3] = centre
+            q0[i, 3:] = np.eye(3).reshape(-1)
+        self.n = n
+        self.is_static = np.array(stat, bool)
+        self._arrays = (_i32(vs), _f64(np.concatenate(V)), _i32(ts), _i32(np.concatenate(T)), _i32(es),
+                        _i32(np.concatenate(E)), _i32(stat), _f64(np.array(mom)), _f64(vol))
+        qd = np.zeros((n, 12)) if qd0 is None else _f64(qd0, (n, 12))
+        p = L.Sim3dParams(h, (C.c_double * 3)(*gravity), d_hat, kappa, kappa_arap, theta, scene_scale,
+                          newton_cap, pcg_rel_tol, pcg_max_iters)
+        a = self._arrays
+        h_ = C.c_void_p()
+        L.check(lib.dabd_gpu_sim3d_create(device, n, _i(a[0]), _d(a[1]), _i(a[2]), _i(a[3]), _i(a[4]),
+                                          _i(a[5]), _i(a[6]), _d(a[7]), _d(a[8]), _d(_f64(q0)), _d(qd),
+                                          C.byref(p), C.byref(h_)))
+        self.h = h_
+        self.params = p
+
+    def __del__(self):
+        try:
+            L.load().dabd_gpu_sim3d_free(self.h)
+        except Exception:
+            pass
+
+    def run(self, frames: int) -> List[dict]:
+        st = (L.Sim3dStats * max(frames, 1))()
+        L.check(L.load().dabd_gpu_sim3d_run(self.h, frames, st))
+        return [{k: getattr(st[i], k) for k, _ in L.Sim3dStats._fields_} for i in range(frames)]
+
+    def state(self):
+        q, qd = np.zeros((self.n, 12)), np.zeros((self.n, 12))
+        L.check(L.load().dabd_gpu_sim3d_get_state(self.h, _d(q), _d(qd)))
+        return q, qd
+
+    def set_state(self, q, qd) -> None:
+        L.check(L.load().dabd_gpu_sim3d_set_state(self.h, _d(_f64(q, (self.n, 12))), _d(_f64(qd, (self.n, 12)))))
+
+    def system(self):
+        """(H, g, dq) of the next frame's first Newton iteration (dynamic bodies)."""
+        N = 12 * self.n
+        H, g, dq, rows = np.zeros((N, N)), np.zeros(N), np.zeros(N), C.c_int()
+        L.check(L.load().dabd_gpu_sim3d_system(self.h, _d(H), _d(g), _d(dq), C.byref(rows)))
+        m = 12 * rows.value
+        return H[:m, :m] if m == N else H.reshape(-1)[: m * m].reshape(m, m), g[:m], dq[:m]
 
 
 def consensus_step(q, u, rho, z_prev, rho0, adapt=None, device: int = 0) -> dict:

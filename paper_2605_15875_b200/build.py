@@ -23,7 +23,7 @@ OBJ = os.path.join(HERE, "build", "obj")
 LIB = os.path.join(HERE, "libdabd_gpu.so")
 
 SOURCES = ["scene.cpp", "balance.cpp", "body3d.cpp", "geometry.cu", "solver.cu", "solver_scalar.cu", "pcg.cu", "admm.cu", "engine.cu",
-           "audit.cu", "contact3d.cu", "broad3d.cu", "capi.cpp"]
+           "audit.cu", "contact3d.cu", "broad3d.cu", "sim3d.cu", "capi.cpp"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

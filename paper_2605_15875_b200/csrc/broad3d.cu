@@ -150,9 +150,8 @@ __global__ void k_prims3(Broad3dView v, const int2* pairs, const int* n_pairs, i
 
 } // namespace
 
-std::vector<unsigned long long> broad_phase3d(const Broad3dView& v, Key3Fmt f, cudaStream_t s) {
-    std::vector<unsigned long long> out;
-    if (v.n < 2) return out;
+int broad_phase3d_device(const Broad3dView& v, Key3Fmt f, DBuf<unsigned long long>& sorted, cudaStream_t s) {
+    if (v.n < 2) return 0;
     DBuf<Box3> box;
     DBuf<double> kx, kx2;
     DBuf<int> idx, idx2, cnt;
@@ -185,9 +184,9 @@ std::vector<unsigned long long> broad_phase3d(const Broad3dView& v, Key3Fmt f, c
             continue;
         }
         const int n_pairs = pin[0];
-        if (n_pairs == 0) return out;
+        if (n_pairs == 0) return 0;
         for (int a2 = 0; a2 < 3; ++a2) {
-            DBuf<unsigned long long> keys, sorted;
+            DBuf<unsigned long long> keys;
             keys.resize(cap);
             sorted.resize(cap);
             CUDA_CHECK(cudaMemsetAsync(cnt.get() + 1, 0, sizeof(int), s));
@@ -205,16 +204,23 @@ std::vector<unsigned long long> broad_phase3d(const Broad3dView& v, Key3Fmt f, c
                 CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys.get(), sorted.get(), nk, 0, f.total_bits(), s));
                 tmp.resize(std::max(sb, tmp.size()));
                 CUDA_CHECK(cub::DeviceRadixSort::SortKeys(tmp.get(), sb, keys.get(), sorted.get(), nk, 0, f.total_bits(), s));
-                out.resize(nk);
-                CUDA_CHECK(cudaMemcpyAsync(out.data(), sorted.get(), nk * sizeof(unsigned long long),
-                                           cudaMemcpyDeviceToHost, s));
-                CUDA_CHECK(cudaStreamSynchronize(s));
             }
-            return out;
+            return nk;
         }
         throw Error("broad phase 3d: candidate buffer growth failed");
     }
     throw Error("broad phase 3d: body-pair buffer growth failed");
+}
+
+std::vector<unsigned long long> broad_phase3d(const Broad3dView& v, Key3Fmt f, cudaStream_t s) {
+    DBuf<unsigned long long> sorted;
+    const int nk = broad_phase3d_device(v, f, sorted, s);
+    std::vector<unsigned long long> out(nk);
+    if (nk > 0) {
+        CUDA_CHECK(cudaMemcpyAsync(out.data(), sorted.get(), nk * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    return out;
 }
 
 } // namespace dabd_gpu

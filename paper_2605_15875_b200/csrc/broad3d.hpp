@@ -52,5 +52,9 @@ struct Key3Fmt {
 // Sorted candidate keys (host vector); the sort order is the lexicographic
 // (kind, a, b, prim a, prim b) order.
 std::vector<unsigned long long> broad_phase3d(const Broad3dView& v, Key3Fmt f, cudaStream_t s);
+// The same, device-resident: the sorted keys stay in `sorted`; returns their count.
+template <typename T>
+class DBuf;
+int broad_phase3d_device(const Broad3dView& v, Key3Fmt f, DBuf<unsigned long long>& sorted, cudaStream_t s);
 
 } // namespace dabd_gpu

@@ -7,6 +7,7 @@
 #include "broad3d.hpp"
 #include "contact3d.hpp"
 #include "engine.hpp"
+#include "sim3d.hpp"
 #include "instrument.hpp"
 #include "scene.hpp"
 
@@ -30,6 +31,10 @@ struct dabd_gpu_balancer {
 
 struct dabd_gpu_ctx {
     std::unique_ptr<Engine> e;
+};
+
+struct dabd_gpu_sim3d {
+    std::unique_ptr<dabd_gpu::Sim3d> s;
 };
 
 namespace {
@@ -221,6 +226,16 @@ dabd_gpu_status dabd_gpu_ctx_set_solver(dabd_gpu_ctx* ctx, const dabd_gpu_solver
         return DABD_GPU_ERR_INVALID;
     }
     ctx->e->set_solver(p->pcg_rel_tol, p->pcg_max_iters);
+    return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_ctx_set_inexact(dabd_gpu_ctx* ctx, double eta, double factor) {
+    if (!ctx) return null_arg();
+    if (!(eta >= 0.0) || !(factor >= 1.0)) {
+        set_error("invalid inexact-Newton parameters (eta >= 0, factor >= 1)");
+        return DABD_GPU_ERR_INVALID;
+    }
+    ctx->e->set_inexact(eta, factor);
     return DABD_GPU_OK;
 }
 
@@ -838,6 +853,85 @@ dabd_gpu_status dabd_gpu_kernel_timer_read(double* total_ms, long long* launches
     *total_ms = dabd_gpu::KernelTimer::get().total_ms();
     *launches = dabd_gpu::KernelTimer::get().count();
     return DABD_GPU_OK;
+}
+
+dabd_gpu_status dabd_gpu_sim3d_create(int device, int n, const int* vert_start, const double* verts,
+                                      const int* tri_start, const int* tris, const int* edge_start, const int* edges,
+                                      const int* is_static, const double* moments10, const double* volume,
+                                      const double* q0, const double* qd0, const dabd_gpu_sim3d_params* p,
+                                      dabd_gpu_sim3d** out) {
+    if (!out || !p || n < 1 || !vert_start || !verts || !tri_start || !tris || !edge_start || !edges || !is_static ||
+        !moments10 || !volume || !q0 || !qd0)
+        return null_arg();
+    *out = nullptr;
+    return guarded([&] {
+        if (!(p->h > 0.0) || !(p->d_hat > 0.0) || !(p->kappa > 0.0) || !(p->theta > 0.0) || p->newton_cap < 1 ||
+            !(p->pcg_rel_tol > 0.0) || p->pcg_max_iters < 1)
+            throw dabd_gpu::InvalidArg("sim3d: invalid parameters");
+        for (int b = 0; b < n; ++b) {
+            const int nvb = vert_start[b + 1] - vert_start[b];
+            if (nvb < 1 || tri_start[b + 1] < tri_start[b] || edge_start[b + 1] < edge_start[b])
+                throw dabd_gpu::InvalidArg("sim3d: offsets must be non-decreasing, every body needs vertices");
+            for (int t = 3 * tri_start[b]; t < 3 * tri_start[b + 1]; ++t)
+                if (tris[t] < 0 || tris[t] >= nvb) throw dabd_gpu::InvalidArg("sim3d: triangle vertex out of range");
+            for (int e = 2 * edge_start[b]; e < 2 * edge_start[b + 1]; ++e)
+                if (edges[e] < 0 || edges[e] >= nvb) throw dabd_gpu::InvalidArg("sim3d: edge vertex out of range");
+        }
+        dabd_gpu::Sim3dParams sp;
+        sp.h = p->h;
+        for (int k = 0; k < 3; ++k) sp.gravity[k] = p->gravity[k];
+        sp.d_hat = p->d_hat;
+        sp.kappa = p->kappa;
+        sp.kappa_arap = p->kappa_arap;
+        sp.theta = p->theta;
+        sp.scene_scale = p->scene_scale;
+        sp.newton_cap = p->newton_cap;
+        sp.pcg_rel_tol = p->pcg_rel_tol;
+        sp.pcg_max_iters = p->pcg_max_iters;
+        auto h = std::make_unique<dabd_gpu_sim3d>();
+        h->s = std::make_unique<dabd_gpu::Sim3d>(device, n, vert_start, verts, tri_start, tris, edge_start, edges,
+                                                 is_static, moments10, volume, q0, qd0, sp);
+        *out = h.release();
+        return DABD_GPU_OK;
+    });
+}
+
+void dabd_gpu_sim3d_free(dabd_gpu_sim3d* sim) { delete sim; }
+
+dabd_gpu_status dabd_gpu_sim3d_run(dabd_gpu_sim3d* sim, int frames, dabd_gpu_sim3d_stats* stats) {
+    if (!sim || frames < 0 || (frames > 0 && !stats)) return null_arg();
+    return guarded([&] {
+        for (int f = 0; f < frames; ++f) {
+            const dabd_gpu::Sim3dStats s = sim->s->frame();
+            stats[f] = dabd_gpu_sim3d_stats{s.newton_iterations, s.line_search_steps, s.pcg_iterations,
+                                            s.max_candidates, s.converged, s.min_distance};
+        }
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_sim3d_get_state(dabd_gpu_sim3d* sim, double* q, double* qd) {
+    if (!sim || !q || !qd) return null_arg();
+    return guarded([&] {
+        sim->s->state(q, qd);
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_sim3d_set_state(dabd_gpu_sim3d* sim, const double* q, const double* qd) {
+    if (!sim || !q || !qd) return null_arg();
+    return guarded([&] {
+        sim->s->set_state(q, qd);
+        return DABD_GPU_OK;
+    });
+}
+
+dabd_gpu_status dabd_gpu_sim3d_system(dabd_gpu_sim3d* sim, double* H, double* g, double* dq, int* rows) {
+    if (!sim || !H || !g || !dq || !rows) return null_arg();
+    return guarded([&] {
+        *rows = sim->s->system(H, g, dq);
+        return DABD_GPU_OK;
+    });
 }
 
 } // extern "C"

@@ -161,6 +161,8 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
         }
     }
     if (const char* e = std::getenv("DABD_GPU_ADMM_HOST")) admm_device_ = e[0] != '1';
+    if (const char* e = std::getenv("DABD_GPU_PCG_ETA")) eta_loose_ = std::atof(e);
+    if (const char* e = std::getenv("DABD_GPU_PCG_ETA_FACTOR")) eta_factor_ = std::atof(e);
     if (const char* e = std::getenv("DABD_SKIN_MIN")) skin_min_ = std::atof(e);
     if (const char* e = std::getenv("DABD_SKIN_GROW")) skin_grow_ = std::atof(e);
     sync();
@@ -846,7 +848,7 @@ void Engine::enq_pcg(bool fused) {
     const int max_rows = max_part_rows();
     if (max_rows <= kClusterPcgMaxRows) {
         // small partitions: one thread-block cluster per partition (DSMEM dots)
-        PcgFuse f{rowtmp_.get(), ctrl_.get(), hd_};
+        PcgFuse f{rowtmp_.get(), ctrl_.get(), hd_, inexact_ ? eta_loose_ : 0.0, eta_factor_};
         launch_pcg_cluster(view(), max_rows, pbuf_.get(), pcg_tol_, pcg_max_, s_, fused ? &f : nullptr);
     } else {
         launch_pcg_persistent(view(), pbuf_.get(), pcg_part_.get(), rowtmp_.get(), pcg_tol_,
@@ -1376,7 +1378,15 @@ NewtonResult Engine::newton_solve(const ObjectiveIn& in, double* q, int max_iter
     int da, dc;
     // Reuse objective() for the instance/anchor setup (mode 0 evaluates once).
     objective(in, q, 0, &dummy_v, nullptr, nullptr, &da, &dc);
-    const NewtonResult r = newton_batch(max_iters, tol);
+    inexact_ = false; // newton.cpp:7-71 as the reference solves it: every direction to pcg_tol_
+    NewtonResult r;
+    try {
+        r = newton_batch(max_iters, tol);
+    } catch (...) {
+        inexact_ = true;
+        throw;
+    }
+    inexact_ = true;
     std::vector<double> iq = iq_.to_host(s_);
     for (int i = 0; i < n_inst_; ++i) {
         const int b = h_ibody_[i];
@@ -1802,7 +1812,7 @@ int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, in
     const int code = pin_i_[0];
     if (code != 0) {
         err_.zero(s_);
-        const int gate_count = pin_i_[9];
+        const int gate_count = std::max(pin_i_[9], c.gate_max); // the largest gate of the attempt
         if (code == kErrCapacity && gate_count > gate_cap_ && grows < kMaxGrows) {
             gate_cap_ = 2 * gate_count; // merge-gate candidates overflowed its fixed capacity
             ++grows;

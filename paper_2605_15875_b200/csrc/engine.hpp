@@ -178,6 +178,13 @@ class Engine {
     bool own_stream_ = false;
     double pcg_tol_ = 1e-10;
     int pcg_max_ = 4000;
+    // Inexact Newton inside frames (cluster PCG): a Newton direction may stop
+    // at the relative residual eta_loose_ while its ||dq||_inf exceeds
+    // eta_factor_ x the Newton tolerance; the directions that decide
+    // convergence are solved to pcg_tol_. 0 = off. The standalone
+    // newton_solve parity entry point always solves to pcg_tol_.
+    double eta_loose_ = 1e-4, eta_factor_ = 10.0;
+    bool inexact_ = true;
 
     // global replicated state
     DBuf<double> q_, qd_, q_start_;
@@ -331,6 +338,12 @@ class Engine {
     DBuf<double> qd_start_;
 
   public:
+    void set_inexact(double eta, double factor) {
+        eta_loose_ = eta;
+        eta_factor_ = factor;
+        graph_ok_ = false;
+        ++solver_epoch_;
+    }
     void set_use_graph(bool on) {
         use_graph_ = on;
         graph_ok_ = false;

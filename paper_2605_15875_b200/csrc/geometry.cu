@@ -364,6 +364,7 @@ void Detector::prepare(int n_inst, int max_verts, int cap) {
     tsize_ = tsize;
     cap = std::max(cap, 64);
     box_.resize(std::max(n_inst, 1));
+    n_cap_ = std::max(n_inst, 1);
     hcount_.resize(tsize);
     hstart_.resize(tsize);
     hfill_.resize(tsize);
@@ -420,7 +421,9 @@ void Detector::enqueue(const SceneView& sc, const InstView& iv, const int* stat,
 }
 
 void Detector::ensure(int n_inst, int max_verts, int cap) {
-    if (cap != cap_ || tsize_ < 2u * static_cast<unsigned>(std::max(n_inst, 1)) ||
+    // per-instance buffers too: a set that grew within the hash table's slack
+    // would otherwise write boxes / hash items past their allocation
+    if (cap != cap_ || n_inst > n_cap_ || tsize_ < 2u * static_cast<unsigned>(std::max(n_inst, 1)) ||
         fmt_.ibits != bits_for(std::max(n_inst, 2)) || fmt_.vbits != bits_for(std::max(max_verts, 2)))
         prepare(n_inst, max_verts, cap);
 }
@@ -429,7 +432,7 @@ int Detector::build(const SceneView& sc, const InstView& iv, const int* stat, in
                     bool swept, double margin, int max_verts, cudaStream_t s) {
     int cap = std::max(cap_, 64 * std::max(iv.n, 1));
     for (int attempt = 0; attempt < 4; ++attempt) {
-        if (cap != cap_ || tsize_ < 2u * static_cast<unsigned>(std::max(iv.n, 1)) ||
+        if (cap != cap_ || iv.n > n_cap_ || tsize_ < 2u * static_cast<unsigned>(std::max(iv.n, 1)) ||
             fmt_.ibits != bits_for(std::max(iv.n, 2)) || fmt_.vbits != bits_for(std::max(max_verts, 2)))
             prepare(iv.n, max_verts, cap);
         enqueue(sc, iv, stat, n_stat, swept, margin, nullptr, s);

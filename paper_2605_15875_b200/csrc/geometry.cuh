@@ -159,6 +159,7 @@ class Detector {
     KeyFmt fmt_;
     int count_ = 0;
     int cap_ = 0;
+    int n_cap_ = 0; // instances the per-instance buffers (boxes, hash items) hold
     unsigned tsize_ = 0;
     size_t temp_bytes_ = 0;
 };

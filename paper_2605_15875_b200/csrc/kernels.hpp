@@ -118,6 +118,8 @@ struct PcgFuse {
     const double* row_trace; // [n_rows] trace of each assembled diagonal block (k_assemble)
     FrameCtrl* ctrl;
     CondHandles hd;          // hd.step is set from the convergence decision
+    double eta_loose = 0.0;  // inexact Newton: loose relative residual (0: off)
+    double eta_factor = 0.0; // ... allowed while ||x||_inf > eta_factor x Newton tol
 };
 
 // Fused objective value (solver.cu k_energy): qmode 0 = iq, 1 = line-search

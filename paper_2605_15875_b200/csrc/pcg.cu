@@ -82,9 +82,8 @@ struct PcgArgs {
     int fold_all; // 1: every warp folds the cluster partials itself, 0: the scalar warp folds
     int remote_first; // 1: remote-column SpMV before the scalar hand-off
     int fast_rcp;     // 1: alpha from a MUFU reciprocal + 2 Newton steps, 0: IEEE division
-    // inexact Newton (fused cluster kernel): a partition whose previous
-    // Newton direction had ||dq||_inf > eta_factor * tol solves to the
-    // relative residual eta_loose instead of tol (0: always tol)
+    // inexact Newton (fused cluster kernel, 0: off): stop at the relative
+    // residual eta_loose while ||x||_inf > eta_factor x the Newton tolerance
     double eta_loose;
     double eta_factor;
 };
@@ -331,7 +330,7 @@ constexpr int kCSmemBytes = 220 * 1024;
 // reads iteration k.
 struct ClusterScalars {
     double tab[2][16][4]; // (r.u, w.u, r.r, pad): 32 B slots for v2 stores
-    double red[kCW][3];
+    double red[kCW][4];
     double scal[3];       // (beta, alpha, stop) of the iteration, from the scalar warp
     unsigned long long bar[2]; // per-parity mbarriers (st.async complete_tx)
     unsigned long long stage_bar;
@@ -470,10 +469,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     const PartState& st = sv.ps[p];
     const bool act = st.active != 0 && R1 > R0;
     double eps = st.eps;
-    // inexact Newton: loose while the previous direction of this solve was
-    // far above the Newton tolerance (uniform across the cluster)
-    const bool loose = a.fused && a.eta_loose > 0.0 && st.dq_last > a.eta_factor * st.tol;
-    const double tol_p = loose ? fmax(a.tol, a.eta_loose) : a.tol;
+    // inexact Newton (a.eta_loose > 0): the solve may stop at the relative
+    // residual eta_loose instead of tol, but only while the iterate's
+    // ||x||_inf (reduced with the CG dots) exceeds eta_factor x the Newton
+    // tolerance, so a direction that can decide convergence (newton.cpp:
+    // 30-36) or end the line search (56-62) is always solved to tol
+    const bool inexact = a.fused && a.eta_loose > a.tol;
+    const double xcut = a.eta_factor * st.tol;
     // shared-memory carve-up (cmax_rows = chunk upper bound used at launch)
     const int V = 6 * cmax_rows;
     double* vm0 = reinterpret_cast<double*>(smem); // m = Dinv w, double-buffered by parity
@@ -1028,7 +1030,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     for (int g = 0; g < G; ++g)
         w[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, r[g] + spmv_local(lrg[g], vm1, true), true) : 0.0;
     // m = Dinv w for iteration 0 (into vm0) and the partials (r.u, w.u, r.r)
-    double l_g = 0.0, l_d = 0.0, l_r = 0.0;
+    double l_g = 0.0, l_d = 0.0, l_r = 0.0, l_x = 0.0; // l_x: max |x| (inexact Newton)
     auto make_m = [&](double* mdst) {
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -1044,6 +1046,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 l_g += r[g] * u[g];
                 l_d += w[g] * u[g];
                 l_r += r[g] * r[g];
+                l_x = fmax(l_x, fabs(x[g]));
             }
             mr[g] = m;
         }
@@ -1088,6 +1091,12 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         {
             const double v = warp_sum3(l_g, l_d, l_r, lane);
             if ((lane & 7) == 0 && lane <= 16) sc.red[warp][lane >> 3] = v;
+            if (inexact) { // max is exact in any order
+                double xm = l_x;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) xm = fmax(xm, __shfl_xor_sync(0xffffffffu, xm, off));
+                if (lane == 0) sc.red[warp][3] = xm;
+            }
         }
         mark(0);
         __syncthreads(); // red[] and this CTA's m (mcur) complete
@@ -1101,18 +1110,24 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                                         lane < kCW ? sc.red[lane][2] : 0.0, lane);
             const double t0 = __shfl_sync(0xffffffffu, tv, 0), t1 = __shfl_sync(0xffffffffu, tv, 8),
                          t2 = __shfl_sync(0xffffffffu, tv, 16);
+            double t3 = inexact && lane < kCW ? sc.red[lane][3] : 0.0;
+            if (inexact)
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) t3 = fmax(t3, __shfl_xor_sync(0xffffffffu, t3, off));
             if (warp < csize) {
                 if (lane == 0) {
                     if (push) {
                         const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), warp);
                         const unsigned pbar = mapa(bar, warp);
                         st_async2(dst, t0, t1, pbar);
-                        st_async2(dst + 16, t2, 0.0, pbar);
+                        st_async2(dst + 16, t2, t3, pbar);
                     } else {
                         double* d = &cl.map_shared_rank(&sc, warp)->tab[par][rank][0];
                         d[0] = t0;
                         d[1] = t1;
                         d[2] = t2;
+                    d[3] = t3;
+                        d[3] = t3;
                     }
                 } else if (lane == 1 && bulk) {
                     const int2 rq = sc.req[warp];
@@ -1132,25 +1147,31 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                                             lane < kCW ? sc.red[lane][2] : 0.0, lane);
                 const double t0 = __shfl_sync(0xffffffffu, tv, 0), t1 = __shfl_sync(0xffffffffu, tv, 8),
                              t2 = __shfl_sync(0xffffffffu, tv, 16);
+                double t3 = inexact && lane < kCW ? sc.red[lane][3] : 0.0;
+                if (inexact)
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) t3 = fmax(t3, __shfl_xor_sync(0xffffffffu, t3, off));
                 if (push && a.spread == 2) {
                     // one remote-store instruction: lane k < 16 sends (r.u, w.u)
                     // to peer k, lane 16 + k sends (r.r, 0)
                     const int peer = lane & 15;
                     if (peer < csize) {
                         const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), peer) + (lane >> 4) * 16u;
-                        st_async2(dst, lane < 16 ? t0 : t2, lane < 16 ? t1 : 0.0, mapa(bar, peer));
+                        st_async2(dst, lane < 16 ? t0 : t2, lane < 16 ? t1 : t3, mapa(bar, peer));
                     }
                 } else if (lane < csize) {
                     if (push) {
                         const unsigned dst = mapa(smem_u32(&sc.tab[par][rank][0]), lane);
                         const unsigned pbar = mapa(bar, lane);
                         st_async2(dst, t0, t1, pbar);
-                        st_async2(dst + 16, t2, 0.0, pbar);
+                        st_async2(dst + 16, t2, t3, pbar);
                     } else {
                         double* d = &cl.map_shared_rank(&sc, lane)->tab[par][rank][0];
                         d[0] = t0;
                         d[1] = t1;
                         d[2] = t2;
+                    d[3] = t3;
+                        d[3] = t3;
                     }
                 }
             }
@@ -1188,17 +1209,22 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         bool stop = false;
         const bool folder = a.fold_all || warp == kSW; // fold_all: every warp, no hand-off
         if (folder) {
-            double2 gd = make_double2(0.0, 0.0);
-            double t2 = 0.0;
+            double2 gd = make_double2(0.0, 0.0), rx = make_double2(0.0, 0.0);
             if (lane < 16) {
                 gd = *reinterpret_cast<const double2*>(&sc.tab[par][lane][0]);
-                t2 = sc.tab[par][lane][2];
+                rx = *reinterpret_cast<const double2*>(&sc.tab[par][lane][2]);
             }
+            const double t2 = rx.x;
+            double xmax = rx.y;
+            if (inexact)
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, off));
             const double fv = warp_sum3(gd.x, gd.y, t2, lane);
             const double gamma = __shfl_sync(0xffffffffu, fv, 0), delta = __shfl_sync(0xffffffffu, fv, 8),
                          rr = __shfl_sync(0xffffffffu, fv, 16);
             if (it == 0) bnorm2 = bnorm2_ws >= 0.0 ? bnorm2_ws : rr;
-            stop = bnorm2 == 0.0 || rr <= tol_p * tol_p * bnorm2 || it >= a.max_iters;
+            stop = bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters ||
+                   (inexact && rr <= a.eta_loose * a.eta_loose * bnorm2 && xmax > xcut);
             // beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
             // with the previous iteration's reciprocals: one division on the
             // critical path
@@ -1253,7 +1279,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             u[g] -= alpha * qv[g];
             w[g] -= alpha * z[g];
         }
-        l_g = l_d = l_r = 0.0;
+        l_g = l_d = l_r = l_x = 0.0;
         make_m(mnext);
         if (bulk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mark(6);
@@ -1289,8 +1315,6 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             double mm = 0.0;
             for (int k = 0; k < csize; ++k) mm = fmax(mm, sc.dqm[k]);
             sv.ps[p].dq_inf = mm;
-            sv.ps[p].dq_last = mm;
-            sv.ps[p].loose = loose ? 1 : 0;
         }
         // the last partition's cluster takes kOpNewtonCheck for all of them
         __threadfence();
@@ -1301,7 +1325,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             int any_act = 0, any_srch = 0;
             for (int q = 0; q < sv.n_parts; ++q) {
                 if (a.ctrl) a.ctrl->pcg_total += vps[q].pcg_iters;
-                if (vps[q].active && vps[q].dq_inf < vps[q].tol && !vps[q].loose) {
+                if (vps[q].active && vps[q].dq_inf < vps[q].tol) {
                     vps[q].final_update = vps[q].dq_inf;
                     vps[q].converged = 1;
                     vps[q].active = 0;
@@ -1408,8 +1432,10 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
         const char* e = std::getenv("DABD_GPU_PCG_MIN_ROWS");
         return e ? std::max(8, std::atoi(e)) : 32;
     }();
-    int csize = 1;
-    while (csize < cmax && csize * min_rows < max_rows_per_part) csize *= 2; // >= ~min_rows rows per CTA
+    // >= ~min_rows rows per CTA; at least 2 CTAs: st.async / bulk DSMEM
+    // copies need a cluster of two or more (a surplus CTA gets no rows)
+    int csize = 2;
+    while (csize < cmax && csize * min_rows < max_rows_per_part) csize *= 2;
     // largest per-partition chunk under the per-partition rule of k_pcg_cluster
     const int cmax_rows = std::max(std::min(max_rows_per_part, min_rows), (max_rows_per_part + csize - 1) / csize);
     // register-resident row groups per warp (kCW warps x kRowsPerWarp rows each)
@@ -1442,17 +1468,16 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
         return e ? std::atoi(e) : 0;
     }();
     a.fast_rcp = frcp;
-    static const double eta[2] = {
-        [] { const char* e = std::getenv("DABD_GPU_PCG_ETA"); return e ? std::atof(e) : 0.0; }(),
-        [] { const char* e = std::getenv("DABD_GPU_PCG_ETA_FACTOR"); return e ? std::atof(e) : 100.0; }()};
-    a.eta_loose = eta[0];
-    a.eta_factor = eta[1];
+    a.eta_loose = 0.0;
+    a.eta_factor = 0.0;
     if (fuse) {
         a.fused = 1;
         a.row_trace = fuse->row_trace;
         a.ctrl = fuse->ctrl;
         a.hd = fuse->hd;
         a.ticket = pcg_ticket();
+        a.eta_loose = fuse->eta_loose;
+        a.eta_factor = fuse->eta_factor;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csize * sv.n_parts);

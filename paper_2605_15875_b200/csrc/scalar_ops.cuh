@@ -41,8 +41,6 @@ __device__ __forceinline__ void scalar_block(PartState* ps, int P, int op, Frame
             s.tol = tol;
             s.final_update = 0.0;
             s.dq_inf = 0.0;
-            s.dq_last = -1.0;
-            s.loose = 0;
             s.toi_earliest = 2.0;
             s.alpha = 1.0;
             break;
@@ -86,7 +84,7 @@ __device__ __forceinline__ void scalar_block(PartState* ps, int P, int op, Frame
                     s.accepted = 1;
                     s.searching = 0;
                     s.final_update = s.alpha * s.dq_inf;
-                    if (s.final_update < s.tol && !s.loose) {
+                    if (s.final_update < s.tol) {
                         s.converged = 1;
                         s.active = 0;
                     }

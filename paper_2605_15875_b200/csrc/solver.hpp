@@ -39,13 +39,6 @@ struct PartState {
     int n_active_contacts;
     int n_candidates;
     int pcg_total;     // PCG iterations summed over this Newton solve (balancer cost)
-    // inexact Newton (cluster PCG, PcgArgs::eta_loose): ||dq||_inf of the
-    // previous Newton direction of this solve (-1: none yet) and whether the
-    // current direction was solved to the loose tolerance (its norm then
-    // never decides convergence, newton.cpp:30-36, 56-62)
-    double dq_last;
-    int loose;
-    int pad_;
 };
 
 // Device-side launch accounting of the PCG kernel (bench.py roofline): the

@@ -112,7 +112,9 @@ def test_torchcomm_halo_gloo(world):
 # ---------------------------------------------------------------------------
 # GPU: two or three ranks sharing cuda:0 (gloo staging through the host)
 # ---------------------------------------------------------------------------
-TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000)
+# the oracle-parity settings emulate the reference's exact solves: PCG to
+# 1e-12 and every Newton direction to it (inexact Newton off)
+TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000, inexact=(0.0, 10.0))
 
 
 BALANCE = {"enabled": True, "kp": 0.3, "kd": 0.05, "smoothing": 0.5, "dp_max": 0.0}

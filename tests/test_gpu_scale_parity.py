@@ -29,7 +29,9 @@ from paper_2605_15875_b200.scene import make_scenario
 
 pytestmark = pytest.mark.gpu
 
-TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000)
+# the oracle-parity settings emulate the reference's exact solves: PCG to
+# 1e-12 and every Newton direction to it (inexact Newton off)
+TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000, inexact=(0.0, 10.0))
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
@@ -141,7 +143,7 @@ def test_hooks_c4_two_partitions():
     # a 1e-12 relative PCG residual leaves ~1e-5 h l of difference to the
     # reference's exact LDL^T step, so the PCG runs at the exact-solve limit
     gpu, ref = _compare("hooks-c4", 2, 8, state_tol=1e-6, trace_tol=1e-5, rho_flips=0.05,
-                        pcg_rel_tol=1e-14, pcg_max_iters=50000)
+                        pcg_rel_tol=1e-14, pcg_max_iters=50000, inexact=(0.0, 10.0))
     sd = make_scenario("hooks-c4")
     ctx = api.Context(api.Scene(sd), num_workers=2)
     st = ctx.run_frames(30)

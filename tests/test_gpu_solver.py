@@ -16,7 +16,9 @@ from paper_2605_15875_b200.scene import BodySpec, SceneData, SimParams, make_sce
 
 pytestmark = pytest.mark.gpu
 
-TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000)
+# the oracle-parity settings emulate the reference's exact solves: PCG to
+# 1e-12 and every Newton direction to it (inexact Newton off)
+TIGHT = dict(pcg_rel_tol=1e-12, pcg_max_iters=20000, inexact=(0.0, 10.0))
 
 
 def _single(o, p):
