@@ -195,9 +195,10 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_solver(dabd_gpu_ctx* ctx,
  * of pcg_rel_tol) while its ||dq||_inf exceeds `factor` x the Newton
  * tolerance theta h l, so every direction that can decide convergence
  * (newton.cpp:30-36) or end a line search (newton.cpp:56-62) is still solved
- * to pcg_rel_tol. eta <= pcg_rel_tol (e.g. 0) turns it off. Default 1e-4,
- * factor 10; dabd_gpu_newton_solve always solves every direction to
- * pcg_rel_tol. */
+ * to pcg_rel_tol. eta <= pcg_rel_tol (e.g. 0) turns it off. Default: 1e-4,
+ * factor 10 for single-domain contexts (num_workers == 0), off for consensus
+ * contexts (their stop test reads residuals of the local solutions);
+ * dabd_gpu_newton_solve always solves every direction to pcg_rel_tol. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_inexact(dabd_gpu_ctx* ctx, double eta, double factor);
 /* Stream (cudaStream_t as uintptr_t) the context launches on; 0 = own stream. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_stream(dabd_gpu_ctx* ctx, uintptr_t stream);

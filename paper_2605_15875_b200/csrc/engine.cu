@@ -161,6 +161,11 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
         }
     }
     if (const char* e = std::getenv("DABD_GPU_ADMM_HOST")) admm_device_ = e[0] != '1';
+    // inexact Newton: on by default for single-domain frames only (a
+    // consensus frame's stop test reads residuals built from the local
+    // solutions, which the loose directions would perturb at the scale it
+    // tests); dabd_gpu_ctx_set_inexact overrides
+    eta_loose_ = W_ == 0 ? 1e-4 : 0.0;
     if (const char* e = std::getenv("DABD_GPU_PCG_ETA")) eta_loose_ = std::atof(e);
     if (const char* e = std::getenv("DABD_GPU_PCG_ETA_FACTOR")) eta_factor_ = std::atof(e);
     if (const char* e = std::getenv("DABD_SKIN_MIN")) skin_min_ = std::atof(e);
