@@ -179,12 +179,12 @@ class Engine {
     double pcg_tol_ = 1e-10;
     int pcg_max_ = 4000;
     // Inexact Newton inside frames (cluster PCG): a Newton direction may stop
-    // at the relative residual eta_loose_ while its ||dq||_inf exceeds
+    // at the relative residual eta_loose_ while its rms entry exceeds
     // eta_factor_ x the Newton tolerance; the directions that decide
     // convergence are solved to pcg_tol_. 0 = off (default for consensus
     // contexts; 1e-4 for single-domain ones, set in the constructor). The
     // standalone newton_solve parity entry point always solves to pcg_tol_.
-    double eta_loose_ = 0.0, eta_factor_ = 10.0;
+    double eta_loose_ = 0.0, eta_factor_ = 2.0;
     bool inexact_ = true;
 
     // global replicated state

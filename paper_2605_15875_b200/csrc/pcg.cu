@@ -83,7 +83,7 @@ struct PcgArgs {
     int remote_first; // 1: remote-column SpMV before the scalar hand-off
     int fast_rcp;     // 1: alpha from a MUFU reciprocal + 2 Newton steps, 0: IEEE division
     // inexact Newton (fused cluster kernel, 0: off): stop at the relative
-    // residual eta_loose while ||x||_inf > eta_factor x the Newton tolerance
+    // residual eta_loose while rms(x) > eta_factor x the Newton tolerance
     double eta_loose;
     double eta_factor;
 };
@@ -351,28 +351,6 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Sums of three values over a warp with 6 double shuffles instead of 15:
-// after the first two levels different lane groups reduce different values.
-// Returns sum(a) in lanes 0-7, sum(b) in lanes 8-15, sum(c) in lanes 16-31
-// (fixed pattern, so every warp and CTA rounds identically).
-__device__ __forceinline__ double warp_sum3(double a, double b, double c, int lane) {
-    const bool lo = lane < 16, q = (lane & 8) != 0;
-    const double r1 = __shfl_xor_sync(0xffffffffu, lo ? c : a, 16);
-    const double r2 = __shfl_xor_sync(0xffffffffu, lo ? 0.0 : b, 16);
-    if (lo) {
-        a += r1;
-        b += r2;
-    } else {
-        c += r1;
-    }
-    const double r3 = __shfl_xor_sync(0xffffffffu, lo ? (q ? a : b) : c, 8);
-    double v = lo ? (q ? b + r3 : a + r3) : c + r3;
-    v += __shfl_xor_sync(0xffffffffu, v, 4);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    return v;
-}
-
 // 1/x from the MUFU approximation and two Newton steps (a few ulp; the CG
 // scalars need not be correctly rounded, only identical in every CTA)
 __device__ __forceinline__ double fast_rcp(double x) {
@@ -382,6 +360,29 @@ __device__ __forceinline__ double fast_rcp(double x) {
     r = fma(r, e, r);
     e = fma(-x, r, 1.0);
     return fma(r, e, r);
+}
+
+// Sums of four values over a warp with 6 double shuffles instead of 20:
+// after the first two levels different lane groups reduce different values.
+// sum(a) in lanes 0-7, sum(b) in 8-15, sum(c) in 16-23, sum(d) in 24-31
+// (fixed pattern, so every warp and CTA rounds identically).
+__device__ __forceinline__ double warp_sum4(double a, double b, double c, double d, int lane) {
+    const bool lo = lane < 16, q = (lane & 8) != 0;
+    const double r1 = __shfl_xor_sync(0xffffffffu, lo ? c : a, 16);
+    const double r2 = __shfl_xor_sync(0xffffffffu, lo ? d : b, 16);
+    if (lo) {
+        a += r1;
+        b += r2;
+    } else {
+        c += r1;
+        d += r2;
+    }
+    const double r3 = __shfl_xor_sync(0xffffffffu, lo ? (q ? a : b) : (q ? c : d), 8);
+    double v = (lo ? (q ? b : a) : (q ? d : c)) + r3;
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v;
 }
 
 __device__ __forceinline__ void cluster_barrier() {
@@ -471,11 +472,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     double eps = st.eps;
     // inexact Newton (a.eta_loose > 0): the solve may stop at the relative
     // residual eta_loose instead of tol, but only while the iterate's
-    // ||x||_inf (reduced with the CG dots) exceeds eta_factor x the Newton
-    // tolerance, so a direction that can decide convergence (newton.cpp:
-    // 30-36) or end the line search (56-62) is always solved to tol
+    // ||x||_2^2 (a fourth sum next to the CG dots, same shuffles) exceeds
+    // ndof (eta_factor tol)^2, i.e. rms(x) > eta_factor x the Newton
+    // tolerance, so ||x||_inf does too: a direction that can decide
+    // convergence (newton.cpp:30-36) is always solved to tol, one that can
+    // end the line search (56-62) only after the step halved below 1/factor
     const bool inexact = a.fused && a.eta_loose > a.tol;
-    const double xcut = a.eta_factor * st.tol;
+    const double xcut2 = static_cast<double>(st.ndof) * (a.eta_factor * st.tol) * (a.eta_factor * st.tol);
     // shared-memory carve-up (cmax_rows = chunk upper bound used at launch)
     const int V = 6 * cmax_rows;
     double* vm0 = reinterpret_cast<double*>(smem); // m = Dinv w, double-buffered by parity
@@ -1030,7 +1033,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     for (int g = 0; g < G; ++g)
         w[g] = on[g] ? spmv_remote(lrg[g], nullptr, m_off, r[g] + spmv_local(lrg[g], vm1, true), true) : 0.0;
     // m = Dinv w for iteration 0 (into vm0) and the partials (r.u, w.u, r.r)
-    double l_g = 0.0, l_d = 0.0, l_r = 0.0, l_x = 0.0; // l_x: max |x| (inexact Newton)
+    double l_g = 0.0, l_d = 0.0, l_r = 0.0, l_x = 0.0; // l_x: x.x (inexact Newton)
     auto make_m = [&](double* mdst) {
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -1046,7 +1049,7 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 l_g += r[g] * u[g];
                 l_d += w[g] * u[g];
                 l_r += r[g] * r[g];
-                l_x = fmax(l_x, fabs(x[g]));
+                l_x += x[g] * x[g];
             }
             mr[g] = m;
         }
@@ -1089,14 +1092,8 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         if (push && threadIdx.x == 0) mbar_expect(bar, expect);
         // ---- partials of this CTA: warp trees, then one fixed 32-lane tree
         {
-            const double v = warp_sum3(l_g, l_d, l_r, lane);
-            if ((lane & 7) == 0 && lane <= 16) sc.red[warp][lane >> 3] = v;
-            if (inexact) { // max is exact in any order
-                double xm = l_x;
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) xm = fmax(xm, __shfl_xor_sync(0xffffffffu, xm, off));
-                if (lane == 0) sc.red[warp][3] = xm;
-            }
+            const double v = warp_sum4(l_g, l_d, l_r, l_x, lane);
+            if ((lane & 7) == 0) sc.red[warp][lane >> 3] = v;
         }
         mark(0);
         __syncthreads(); // red[] and this CTA's m (mcur) complete
@@ -1106,14 +1103,11 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             // warp) and warp k sends them, plus the halo rows consumer k
             // needs, to peer k: one remote store pair and one bulk copy per
             // warp instead of csize of each serialised in one warp
-            const double tv = warp_sum3(lane < kCW ? sc.red[lane][0] : 0.0, lane < kCW ? sc.red[lane][1] : 0.0,
-                                        lane < kCW ? sc.red[lane][2] : 0.0, lane);
+            const double tv = warp_sum4(lane < kCW ? sc.red[lane][0] : 0.0, lane < kCW ? sc.red[lane][1] : 0.0,
+                                        lane < kCW ? sc.red[lane][2] : 0.0, lane < kCW ? sc.red[lane][3] : 0.0,
+                                        lane);
             const double t0 = __shfl_sync(0xffffffffu, tv, 0), t1 = __shfl_sync(0xffffffffu, tv, 8),
-                         t2 = __shfl_sync(0xffffffffu, tv, 16);
-            double t3 = inexact && lane < kCW ? sc.red[lane][3] : 0.0;
-            if (inexact)
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) t3 = fmax(t3, __shfl_xor_sync(0xffffffffu, t3, off));
+                         t2 = __shfl_sync(0xffffffffu, tv, 16), t3 = __shfl_sync(0xffffffffu, tv, 24);
             if (warp < csize) {
                 if (lane == 0) {
                     if (push) {
@@ -1143,14 +1137,11 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             if (!bulk) cluster_arrive();
         } else {
             if (warp == kSW) { // the scalar warp: CTA tree and push to every peer
-                const double tv = warp_sum3(lane < kCW ? sc.red[lane][0] : 0.0, lane < kCW ? sc.red[lane][1] : 0.0,
-                                            lane < kCW ? sc.red[lane][2] : 0.0, lane);
+                const double tv = warp_sum4(lane < kCW ? sc.red[lane][0] : 0.0, lane < kCW ? sc.red[lane][1] : 0.0,
+                                            lane < kCW ? sc.red[lane][2] : 0.0, lane < kCW ? sc.red[lane][3] : 0.0,
+                                            lane);
                 const double t0 = __shfl_sync(0xffffffffu, tv, 0), t1 = __shfl_sync(0xffffffffu, tv, 8),
-                             t2 = __shfl_sync(0xffffffffu, tv, 16);
-                double t3 = inexact && lane < kCW ? sc.red[lane][3] : 0.0;
-                if (inexact)
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) t3 = fmax(t3, __shfl_xor_sync(0xffffffffu, t3, off));
+                             t2 = __shfl_sync(0xffffffffu, tv, 16), t3 = __shfl_sync(0xffffffffu, tv, 24);
                 if (push && a.spread == 2) {
                     // one remote-store instruction: lane k < 16 sends (r.u, w.u)
                     // to peer k, lane 16 + k sends (r.r, 0)
@@ -1214,17 +1205,12 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 gd = *reinterpret_cast<const double2*>(&sc.tab[par][lane][0]);
                 rx = *reinterpret_cast<const double2*>(&sc.tab[par][lane][2]);
             }
-            const double t2 = rx.x;
-            double xmax = rx.y;
-            if (inexact)
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, off));
-            const double fv = warp_sum3(gd.x, gd.y, t2, lane);
+            const double fv = warp_sum4(gd.x, gd.y, rx.x, rx.y, lane);
             const double gamma = __shfl_sync(0xffffffffu, fv, 0), delta = __shfl_sync(0xffffffffu, fv, 8),
-                         rr = __shfl_sync(0xffffffffu, fv, 16);
+                         rr = __shfl_sync(0xffffffffu, fv, 16), xx = __shfl_sync(0xffffffffu, fv, 24);
             if (it == 0) bnorm2 = bnorm2_ws >= 0.0 ? bnorm2_ws : rr;
             stop = bnorm2 == 0.0 || rr <= a.tol * a.tol * bnorm2 || it >= a.max_iters ||
-                   (inexact && rr <= a.eta_loose * a.eta_loose * bnorm2 && xmax > xcut);
+                   (inexact && rr <= a.eta_loose * a.eta_loose * bnorm2 && xx > xcut2);
             // beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old),
             // with the previous iteration's reciprocals: one division on the
             // critical path
