@@ -388,6 +388,36 @@ __global__ void k_rho_carry(int n_inst, int nb, const int* ibody, const int* ian
         if (ianc[i]) carry[ibody[i]] = irho[i];
 }
 
+__global__ void k_pack_owned(SceneView sc, const uint32_t* bmask, int p0, int p1, const double* q,
+                             const double* qd, double* rec, int* count) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < sc.nb; b += gridDim.x * blockDim.x) {
+        if (sc.is_static[b]) continue;
+        const int owner = __ffs(bmask[b]) - 1;
+        if (owner < p0 || owner >= p1) continue;
+        double* o = rec + 13 * static_cast<size_t>(atomicAdd(count, 1)); // slot order is irrelevant: keyed by id
+        o[0] = b;
+        for (int k = 0; k < 6; ++k) {
+            o[1 + k] = q[6 * b + k];
+            o[7 + k] = qd[6 * b + k];
+        }
+    }
+}
+
+__global__ void k_unpack_owned(int world, const int* counts, const double* gath, size_t stride, double* q,
+                               double* qd) {
+    for (int r = 0; r < world; ++r) {
+        const double* g = gath + stride * r;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < counts[r]; i += gridDim.x * blockDim.x) {
+            const double* rc = g + 13 * static_cast<size_t>(i);
+            const int b = static_cast<int>(rc[0]);
+            for (int k = 0; k < 6; ++k) {
+                q[6 * b + k] = rc[1 + k];
+                qd[6 * b + k] = rc[7 + k];
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void admm_cond(unsigned long long h, bool v, int graph) {
     if (graph) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(h), v ? 1u : 0u);
 }
@@ -631,6 +661,17 @@ void launch_masks_w(const SceneView& sc, const double* q, const double* planes, 
     if (sc.nb == 0) return;
     DABD_LAUNCH("k_masks", s, k_masks<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, q, planes, np, 0.0, all, masks, err, vmax, h,
                                                                    w_min, w_out));
+}
+
+void launch_pack_owned(const SceneView& sc, const uint32_t* bmask, int p0, int p1, const double* q,
+                       const double* qd, double* rec, int* count, cudaStream_t s) {
+    if (sc.nb == 0) return;
+    DABD_LAUNCH("k_pack_owned", s, k_pack_owned<<<grid_for(sc.nb, kB), kB, 0, s>>>(sc, bmask, p0, p1, q, qd, rec, count));
+}
+
+void launch_unpack_owned(int world, const int* counts, const double* gath, size_t stride, double* q,
+                         double* qd, cudaStream_t s) {
+    DABD_LAUNCH("k_unpack_owned", s, k_unpack_owned<<<64, kB, 0, s>>>(world, counts, gath, stride, q, qd));
 }
 
 } // namespace dabd_gpu

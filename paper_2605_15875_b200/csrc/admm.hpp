@@ -30,6 +30,13 @@ void launch_pack_halo(int n, const int* inst, const double* iq, const double* iu
 void launch_select_commit(const SceneView& sc, const uint32_t* bmask, const int* part_rank,
                           const double* gath, size_t stride, double* q, double* qd,
                           cudaStream_t s);
+// Owned-body commit records (runtime.cpp:484-506 across ranks): bodies whose
+// lowest holder partition lies in [p0, p1) -> (id, q[6], qdot[6]); and the
+// inverse over every rank's records.
+void launch_pack_owned(const SceneView& sc, const uint32_t* bmask, int p0, int p1, const double* q,
+                       const double* qd, double* rec, int* count, cudaStream_t s);
+void launch_unpack_owned(int world, const int* counts, const double* gath, size_t stride, double* q,
+                         double* qd, cudaStream_t s);
 void launch_merged(int n, const int* ianc, const double* iq, const double* iznext, double* out,
                    cudaStream_t s);
 void launch_adapt(int n, const int* ianc, double* irho, const double* irho0, const double* rb,

@@ -335,18 +335,32 @@ std::vector<double> Engine::allgather_host(const std::vector<double>& mine) {
 }
 
 void Engine::commit_gather() {
-    // Each rank wrote the bodies it holds; the lowest holder's copy wins.
-    const size_t n6 = 6 * static_cast<size_t>(hs_.nb), stride = 2 * n6;
-    rec_.resize(stride);
-    CUDA_CHECK(cudaMemcpyAsync(rec_.get(), q_.get(), n6 * sizeof(double), cudaMemcpyDeviceToDevice, s_));
-    CUDA_CHECK(cudaMemcpyAsync(rec_.get() + n6, qd_.get(), n6 * sizeof(double),
-                               cudaMemcpyDeviceToDevice, s_));
+    // Each rank publishes only the bodies it owns (its partitions hold the
+    // body's lowest holder, the replica whose copy wins): a count all-gather,
+    // then records (id, q, qdot) at the largest rank's count
+    const int nb = hs_.nb;
+    own_cnt_.resize(1);
+    own_cnt_.zero(s_);
+    own_rec_.resize(13 * static_cast<size_t>(std::max(nb, 1)));
+    launch_pack_owned(ds_.view(), bmask_.get(), p0_, p1_, q_.get(), qd_.get(), own_rec_.get(), own_cnt_.get(), s_);
+    CUDA_CHECK(cudaMemcpyAsync(pin_i_.get() + 12, own_cnt_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+    sync();
+    const std::vector<double> counts = allgather_host({static_cast<double>(pin_i_[12])});
+    const size_t cstride = counts.size() / comm_.world;
+    int cmax = 0;
+    std::vector<int> cnt(comm_.world);
+    for (int r = 0; r < comm_.world; ++r) {
+        cnt[r] = static_cast<int>(counts[cstride * r]);
+        cmax = std::max(cmax, cnt[r]);
+    }
+    if (cmax == 0) return;
+    const size_t stride = 13 * static_cast<size_t>(cmax);
+    own_rec_.resize(std::max(own_rec_.size(), stride));
     gath_.resize(stride * comm_.world);
-    if (comm_.allgather(comm_.user, rec_.get(), gath_.get(), stride,
-                        reinterpret_cast<uintptr_t>(s_)) != 0)
+    if (comm_.allgather(comm_.user, own_rec_.get(), gath_.get(), stride, reinterpret_cast<uintptr_t>(s_)) != 0)
         throw Error("comm: commit all-gather failed");
-    launch_select_commit(ds_.view(), bmask_.get(), part_rank_.get(), gath_.get(), stride, q_.get(),
-                         qd_.get(), s_);
+    own_cnts_.upload(cnt, s_);
+    launch_unpack_owned(comm_.world, own_cnts_.get(), gath_.get(), stride, q_.get(), qd_.get(), s_);
 }
 
 void Engine::check_err(const char* where) {
@@ -724,7 +738,9 @@ void Engine::prepare_solver() {
     partial_.resize(static_cast<size_t>(std::max(segsum_chunks(std::max(cap_, n_rows_)),
                                                  energy_chunks(cap_) + energy_chunks(n_rows_))) * P_ + P_);
     // (x_ / pbuf_, the PCG warm start, are (re)initialised by build_instances)
-    pcg_part_.resize(3 * static_cast<size_t>(pcg_grid_size(std::max(n_rows_, 1))) * P_);
+    pcg_part_.resize(std::max(3 * static_cast<size_t>(pcg_grid_size(std::max(n_rows_, 1))),
+                              8 * static_cast<size_t>(pcg_grid_blocks())) * P_);
+    if (max_part_rows() > kClusterPcgMaxRows) pcg_vec_.resize(60 * static_cast<size_t>(std::max(n_rows_, 1)));
     (void)pcg_cluster_size(); // resolve cluster attributes before any graph capture
     box_.resize(std::max(n_inst_, 1));
     admm_prof().mark(11, s_);
@@ -856,8 +872,17 @@ void Engine::enq_pcg(bool fused) {
         PcgFuse f{rowtmp_.get(), ctrl_.get(), hd_, inexact_ ? eta_loose_ : 0.0, eta_factor_};
         launch_pcg_cluster(view(), max_rows, pbuf_.get(), pcg_tol_, pcg_max_, s_, fused ? &f : nullptr);
     } else {
-        launch_pcg_persistent(view(), pbuf_.get(), pcg_part_.get(), rowtmp_.get(), pcg_tol_,
+        static const bool grid_kernel = [] {
+            const char* e = std::getenv("DABD_GPU_PCG_GRID");
+            return !e || e[0] != '0';
+        }();
+        if (grid_kernel) { // one grid barrier per iteration (pipelined CG); vectors sized in prepare_solver
+            launch_pcg_grid(view(), pcg_vec_.get(), pcg_part_.get(), pcg_tol_, pcg_max_, s_,
+                            inexact_ ? eta_loose_ : 0.0, eta_factor_);
+        } else {
+            launch_pcg_persistent(view(), pbuf_.get(), pcg_part_.get(), rowtmp_.get(), pcg_tol_,
                               pcg_max_, s_);
+        }
     }
 }
 

@@ -303,11 +303,13 @@ class Engine {
     const double* remote_hi_ = nullptr;
     std::vector<double> allgather_host(const std::vector<double>& mine);
     void commit_gather();
+    DBuf<int> own_cnt_, own_cnts_;
+    DBuf<double> own_rec_;
     DBuf<double> rloc_, sloc_, rb_, sb_;
     DBuf<double> ifs_; // per-instance force split (fx, fy)
     SimParams frame_params_;
     int project_ = 1;
-    DBuf<double> pbuf_, pcg_part_;
+    DBuf<double> pbuf_, pcg_part_, pcg_vec_;
     DBuf<DevPerf> perf_;
     Auditor auditor_;
     DBuf<double> audit_q_;

@@ -73,6 +73,11 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
                         int max_iters, cudaStream_t s, const PcgFuse* fuse = nullptr);
 void launch_pcg_persistent(const SolverView& sv, double* pbuf, double* partials, double* rowval,
                            double tol, int max_iters, cudaStream_t s);
+// Grid-wide pipelined PCG (one grid barrier per iteration) for partitions
+// beyond the cluster kernel: vecs [10][6 n_rows], partials [2][blocks][P][4].
+int pcg_grid_blocks();
+void launch_pcg_grid(const SolverView& sv, double* vecs, double* partials, double tol, int max_iters,
+                     cudaStream_t s, double eta_loose = 0.0, double eta_factor = 0.0);
 
 // Per-partition scalar steps (solver_scalar.cu). `op` selects the update.
 enum ScalarOp : int {

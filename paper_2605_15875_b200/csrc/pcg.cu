@@ -16,6 +16,7 @@
 
 #include "instrument.hpp"
 
+#include <algorithm>
 #include <cstdlib>
 
 #include <cooperative_groups.h>
@@ -54,6 +55,29 @@ __device__ __forceinline__ void mv36(const double* m, const double (&x)[6], doub
         const double2 r0 = row[0], r1 = row[1], r2 = row[2];
         y[a] = r0.x * x[0] + r0.y * x[1] + r1.x * x[2] + r1.y * x[3] + r2.x * x[4] + r2.y * x[5];
     }
+}
+
+// Sums of four values over a warp with 6 double shuffles instead of 20:
+// after the first two levels different lane groups reduce different values.
+// sum(a) in lanes 0-7, sum(b) in 8-15, sum(c) in 16-23, sum(d) in 24-31
+// (fixed pattern, so every warp and CTA rounds identically).
+__device__ __forceinline__ double warp_sum4(double a, double b, double c, double d, int lane) {
+    const bool lo = lane < 16, q = (lane & 8) != 0;
+    const double r1 = __shfl_xor_sync(0xffffffffu, lo ? c : a, 16);
+    const double r2 = __shfl_xor_sync(0xffffffffu, lo ? d : b, 16);
+    if (lo) {
+        a += r1;
+        b += r2;
+    } else {
+        c += r1;
+        d += r2;
+    }
+    const double r3 = __shfl_xor_sync(0xffffffffu, lo ? (q ? a : b) : (q ? c : d), 8);
+    double v = (lo ? (q ? b : a) : (q ? d : c)) + r3;
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v;
 }
 
 struct PcgArgs {
@@ -300,6 +324,309 @@ __global__ void __launch_bounds__(kT) k_pcg(SolverView sv, PcgArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Grid-wide pipelined block-Jacobi PCG for partitions too large for one
+// cluster (> 4096 rows: undivided C3, C5 partitions). Ghysels & Vanroose's
+// pipelined recurrences as in k_pcg_cluster, so ONE grid-wide exchange per
+// iteration: every block folds its warps' partials per partition, writes
+// them to a parity-double-buffered table, and after the grid barrier every
+// block folds the table in the same fixed order (same scalars everywhere).
+// One block of 512 threads per SM; lane = 6 * slot + comp, a warp owns row
+// groups of 5 rows of one partition (groups aligned to partitions), strided
+// over all warps of the grid. Vectors live in global memory (L2-resident,
+// read with ld.global.cg across blocks), m = Dinv w double-buffered.
+constexpr int kGT = 512, kGW = kGT / 32;
+
+struct GridVecs {
+    double *x, *r, *u, *w, *z, *q, *s, *p, *m0, *m1; // [6 R] each
+};
+
+__global__ void __launch_bounds__(kGT) k_pcg_grid(SolverView sv, PcgArgs a, GridVecs v) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int s_goff[kMaxParts + 1];
+    __shared__ double s_acc[kGW][kMaxParts][4];
+    __shared__ double s_beta[kMaxParts], s_alpha[kMaxParts], s_igo[kMaxParts], s_iao[kMaxParts], s_bn[kMaxParts];
+    __shared__ int s_done[kMaxParts], s_it[kMaxParts], s_all;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = lane / 6, comp = lane - 6 * slot;
+    const int P = sv.n_parts, G = gridDim.x;
+    const int gw = blockIdx.x * kGW + warp, NW = G * kGW;
+    if (threadIdx.x == 0) {
+        int g = 0;
+        for (int p = 0; p < P; ++p) {
+            s_goff[p] = g;
+            g += (sv.part_row_off[p + 1] - sv.part_row_off[p] + 4) / 5;
+        }
+        s_goff[P] = g;
+    }
+    if (threadIdx.x < P) {
+        const int p = threadIdx.x;
+        s_done[p] = sv.ps[p].active ? 0 : 1;
+        s_it[p] = 0;
+        s_igo[p] = s_iao[p] = 0.0;
+    }
+    __syncthreads();
+    const int n_groups = s_goff[P];
+    // row of this lane in group rg (-1: past the partition's end / idle lane)
+    auto row_of = [&](int rg, int& part) {
+        int p = 0;
+        while (rg >= s_goff[p + 1]) ++p;
+        part = p;
+        const int row = sv.part_row_off[p] + 5 * (rg - s_goff[p]) + slot;
+        return (lane < 30 && row < sv.part_row_off[p + 1]) ? row : -1;
+    };
+    auto spmv = [&](int row, int p, const double* vec) -> double {
+        // (D + eps I) v_row + sum_t B_t v_col, row `comp` of every block
+        const double2* d2 = reinterpret_cast<const double2*>(sv.rdiag + 36 * static_cast<size_t>(row) + 6 * comp);
+        const double2* o2 = reinterpret_cast<const double2*>(vec + 6 * static_cast<size_t>(row));
+        double2 m0 = d2[0], m1 = d2[1], m2 = d2[2];
+        double2 w0 = __ldcg(o2), w1 = __ldcg(o2 + 1), w2 = __ldcg(o2 + 2);
+        double y = m0.x * w0.x + m0.y * w0.y + m1.x * w1.x + m1.y * w1.y + m2.x * w2.x + m2.y * w2.y;
+        y += sv.ps[p].eps * __ldcg(vec + 6 * static_cast<size_t>(row) + comp);
+        const int nb = sv.ell_cnt[row];
+        for (int t = 0; t < nb; ++t) {
+            const int c = sv.ell_col[static_cast<size_t>(row) * sv.ell_w + t];
+            const double2* b2 = reinterpret_cast<const double2*>(
+                sv.ell_blk + (static_cast<size_t>(row) * sv.ell_w + t) * 36 + 6 * comp);
+            const double2* c2 = reinterpret_cast<const double2*>(vec + 6 * static_cast<size_t>(c));
+            m0 = b2[0], m1 = b2[1], m2 = b2[2];
+            w0 = __ldcg(c2), w1 = __ldcg(c2 + 1), w2 = __ldcg(c2 + 2);
+            y += m0.x * w0.x + m0.y * w0.y + m1.x * w1.x + m1.y * w1.y + m2.x * w2.x + m2.y * w2.y;
+        }
+        return y;
+    };
+    // Dinv (6x6 row `comp`) times the 6 lane values of this slot
+    auto dinv_apply = [&](int row, double val) -> double {
+        double vc[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) vc[c] = __shfl_sync(0xffffffffu, val, (6 * slot + c) & 31);
+        if (row < 0) return 0.0;
+        const double2* d2 = reinterpret_cast<const double2*>(sv.rdinv + 36 * static_cast<size_t>(row) + 6 * comp);
+        const double2 d0 = d2[0], d1 = d2[1], dd = d2[2];
+        return d0.x * vc[0] + d0.y * vc[1] + d1.x * vc[2] + d1.y * vc[3] + dd.x * vc[4] + dd.y * vc[5];
+    };
+    // per-warp partials per partition in s_acc (fixed order), then the block
+    // fold into the parity table part[par][block][P][4]
+    auto zero_acc = [&] {
+        for (int i = threadIdx.x; i < kGW * kMaxParts * 4; i += kGT) (&s_acc[0][0][0])[i] = 0.0;
+        __syncthreads();
+    };
+    auto flush = [&](int p, double l0, double l1, double l2, double l3) {
+        const double v = warp_sum4(l0, l1, l2, l3, lane);
+        if ((lane & 7) == 0) s_acc[warp][p][lane >> 3] += v;
+    };
+    auto block_fold = [&](int par) {
+        __syncthreads();
+        double* out = a.part + static_cast<size_t>(par) * G * P * 4 + static_cast<size_t>(blockIdx.x) * P * 4;
+        for (int i = threadIdx.x; i < P * 4; i += kGT) {
+            const int p = i >> 2, k = i & 3;
+            double t = 0.0;
+            for (int w = 0; w < kGW; ++w) t += s_acc[w][p][k];
+            out[i] = t;
+        }
+    };
+
+    // ---- warm start (a.warm): x0 = c x_prev, the A-optimal multiple of the
+    // previous solve's solution (sv.x, carried across instance sets), with
+    // ||b||^2 from the same reduction for the stopping test
+    __shared__ double s_c[kMaxParts];
+    if (a.warm) {
+        zero_acc();
+        for (int rg = gw; rg < n_groups; rg += NW) {
+            int p;
+            const int row = row_of(rg, p);
+            const bool on = row >= 0 && !s_done[p];
+            const size_t e = 6 * static_cast<size_t>(row) + comp;
+            double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+            if (on) {
+                const double ap = spmv(row, p, sv.x);
+                const double pv = sv.x[e], bv = -sv.rgrad[e];
+                v.z[e] = ap; // A x_prev, consumed below
+                l0 = pv * bv;
+                l1 = pv * ap;
+                l2 = bv * bv;
+            }
+            flush(p, l0, l1, l2, 0.0);
+        }
+        block_fold(1);
+        grid.sync();
+        if (warp < P) {
+            const int p = warp;
+            const double* tb = a.part + static_cast<size_t>(G) * P * 4;
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+            for (int b = lane; b < G; b += 32) {
+                const double2* q2 = reinterpret_cast<const double2*>(tb + (static_cast<size_t>(b) * P + p) * 4);
+                const double2 ab = __ldcg(q2), cd = __ldcg(q2 + 1);
+                t0 += ab.x;
+                t1 += ab.y;
+                t2 += cd.x;
+            }
+            const double fv = warp_sum4(t0, t1, t2, 0.0, lane);
+            const double pb = __shfl_sync(0xffffffffu, fv, 0), pap = __shfl_sync(0xffffffffu, fv, 8),
+                         bb = __shfl_sync(0xffffffffu, fv, 16);
+            if (lane == 0) {
+                double c = pap > 0.0 ? pb / pap : 0.0;
+                if (!isfinite(c)) c = 0.0;
+                s_c[p] = c;
+                s_bn[p] = bb;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- init: r = b - A x0, u = Dinv r; then w = A u, m = Dinv w
+    for (int rg = gw; rg < n_groups; rg += NW) {
+        int p;
+        const int row = row_of(rg, p);
+        const bool on = row >= 0 && !s_done[p];
+        const size_t e = 6 * static_cast<size_t>(row) + comp;
+        const double c = a.warm ? s_c[p] : 0.0;
+        double rv = on ? -sv.rgrad[e] : 0.0, xv = 0.0;
+        if (on && c != 0.0) { // (c == 0: A x_prev / x_prev never touch x, r)
+            xv = c * sv.x[e];
+            rv -= c * __ldcg(v.z + e);
+        }
+        const double uv = dinv_apply(on ? row : -1, rv);
+        if (row >= 0) {
+            v.r[e] = rv;
+            v.u[e] = uv;
+            v.x[e] = xv;
+        }
+    }
+    grid.sync(); // (v.z is reset only after every block consumed A x_prev)
+    for (int rg = gw; rg < n_groups; rg += NW) {
+        int p;
+        const int row = row_of(rg, p);
+        if (row < 0) continue;
+        const size_t e = 6 * static_cast<size_t>(row) + comp;
+        v.z[e] = v.q[e] = v.s[e] = v.p[e] = 0.0;
+    }
+    zero_acc();
+    for (int rg = gw; rg < n_groups; rg += NW) {
+        int p;
+        const int row = row_of(rg, p);
+        const bool on = row >= 0 && !s_done[p];
+        const size_t e = 6 * static_cast<size_t>(row) + comp;
+        const double wv = on ? spmv(row, p, v.u) : 0.0;
+        const double mv = dinv_apply(on ? row : -1, wv);
+        double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+        if (on) {
+            const double rv = __ldcg(v.r + e), uv = __ldcg(v.u + e);
+            v.w[e] = wv;
+            v.m0[e] = mv;
+            l0 = rv * uv;
+            l1 = wv * uv;
+            l2 = rv * rv;
+        }
+        flush(p, l0, l1, l2, 0.0); // x = 0
+    }
+    block_fold(0);
+    grid.sync();
+
+    for (int it = 0;; ++it) {
+        const int par = it & 1;
+        const double* mcur = par ? v.m1 : v.m0;
+        double* mnext = par ? v.m0 : v.m1;
+        // every block folds the table in the same order -> identical scalars
+        if (warp < P) {
+            const int p = warp;
+            const double* tb = a.part + static_cast<size_t>(par) * G * P * 4;
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+            for (int b = lane; b < G; b += 32) {
+                const double2* q2 = reinterpret_cast<const double2*>(tb + (static_cast<size_t>(b) * P + p) * 4);
+                const double2 ab = __ldcg(q2), cd = __ldcg(q2 + 1);
+                t0 += ab.x;
+                t1 += ab.y;
+                t2 += cd.x;
+                t3 += cd.y;
+            }
+            const double fv = warp_sum4(t0, t1, t2, t3, lane);
+            const double gamma = __shfl_sync(0xffffffffu, fv, 0), delta = __shfl_sync(0xffffffffu, fv, 8),
+                         rr = __shfl_sync(0xffffffffu, fv, 16), xx = __shfl_sync(0xffffffffu, fv, 24);
+            if (lane == 0 && !s_done[p]) {
+                if (it == 0 && !a.warm) s_bn[p] = rr;
+                const double bn = s_bn[p];
+                // inexact Newton as in k_pcg_cluster: loose only while rms(x) > eta_factor tol
+                const double xcut = a.eta_factor * sv.ps[p].tol;
+                const bool loose = a.eta_loose > a.tol && rr <= a.eta_loose * a.eta_loose * bn &&
+                                   xx > static_cast<double>(sv.ps[p].ndof) * xcut * xcut;
+                bool stop = bn == 0.0 || rr <= a.tol * a.tol * bn || it >= a.max_iters || loose;
+                const double beta = gamma * s_igo[p];
+                const double alpha = gamma / (delta - beta * gamma * s_iao[p]);
+                stop = stop || !(alpha > 0.0) || !isfinite(alpha);
+                s_beta[p] = beta;
+                s_alpha[p] = alpha;
+                s_igo[p] = 1.0 / gamma;
+                s_iao[p] = 1.0 / alpha;
+                if (stop) {
+                    s_done[p] = 1;
+                    s_it[p] = it;
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int all = 1;
+            for (int p = 0; p < P; ++p) all &= s_done[p];
+            s_all = all;
+        }
+        zero_acc(); // (its __syncthreads also publishes s_all)
+        if (s_all) break; // uniform across blocks
+        for (int rg = gw; rg < n_groups; rg += NW) {
+            int p;
+            const int row = row_of(rg, p);
+            if (s_done[p]) continue; // uniform per group: the whole warp skips
+            const bool on = row >= 0;
+            const size_t e = 6 * static_cast<size_t>(row) + comp;
+            const double beta = s_beta[p], alpha = s_alpha[p];
+            double wv = 0.0, l0 = 0.0, l1 = 0.0, l2 = 0.0, l3 = 0.0;
+            if (on) {
+                const double n = spmv(row, p, mcur);
+                const double mv = __ldcg(mcur + e);
+                const double zv = n + beta * __ldcg(v.z + e);
+                const double qv = mv + beta * __ldcg(v.q + e);
+                const double sv_ = __ldcg(v.w + e) + beta * __ldcg(v.s + e);
+                const double pv = __ldcg(v.u + e) + beta * __ldcg(v.p + e);
+                const double xv = __ldcg(v.x + e) + alpha * pv;
+                const double rv = __ldcg(v.r + e) - alpha * sv_;
+                const double uv = __ldcg(v.u + e) - alpha * qv;
+                wv = __ldcg(v.w + e) - alpha * zv;
+                v.z[e] = zv;
+                v.q[e] = qv;
+                v.s[e] = sv_;
+                v.p[e] = pv;
+                v.x[e] = xv;
+                v.r[e] = rv;
+                v.u[e] = uv;
+                v.w[e] = wv;
+                l0 = rv * uv;
+                l1 = wv * uv;
+                l2 = rv * rv;
+                l3 = xv * xv;
+            }
+            const double mn = dinv_apply(on ? row : -1, wv);
+            if (on) mnext[e] = mn;
+            flush(p, l0, l1, l2, l3);
+        }
+        block_fold(par ^ 1);
+        grid.sync();
+    }
+    // solution to sv.x (the Newton direction)
+    for (int rg = gw; rg < n_groups; rg += NW) {
+        int p;
+        const int row = row_of(rg, p);
+        if (row < 0) continue;
+        const size_t e = 6 * static_cast<size_t>(row) + comp;
+        sv.x[e] = sv.ps[p].active ? __ldcg(v.x + e) : 0.0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < P) {
+        const int p = threadIdx.x;
+        sv.ps[p].pcg_iters = s_it[p];
+        sv.ps[p].pcg_total += s_it[p];
+        sv.ps[p].pcg_done = 1;
+        sv.ps[p].bnorm2 = s_bn[p];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Cluster-resident PCG: one thread-block cluster (up to 16 SMs) per
 // partition. Every CTA stages its chunk of the partition's BSR rows (diagonal
 // + eps I and coupling blocks, the DSMEM address of every block's column,
@@ -360,29 +687,6 @@ __device__ __forceinline__ double fast_rcp(double x) {
     r = fma(r, e, r);
     e = fma(-x, r, 1.0);
     return fma(r, e, r);
-}
-
-// Sums of four values over a warp with 6 double shuffles instead of 20:
-// after the first two levels different lane groups reduce different values.
-// sum(a) in lanes 0-7, sum(b) in 8-15, sum(c) in 16-23, sum(d) in 24-31
-// (fixed pattern, so every warp and CTA rounds identically).
-__device__ __forceinline__ double warp_sum4(double a, double b, double c, double d, int lane) {
-    const bool lo = lane < 16, q = (lane & 8) != 0;
-    const double r1 = __shfl_xor_sync(0xffffffffu, lo ? c : a, 16);
-    const double r2 = __shfl_xor_sync(0xffffffffu, lo ? d : b, 16);
-    if (lo) {
-        a += r1;
-        b += r2;
-    } else {
-        c += r1;
-        d += r2;
-    }
-    const double r3 = __shfl_xor_sync(0xffffffffu, lo ? (q ? a : b) : (q ? c : d), 8);
-    double v = (lo ? (q ? b : a) : (q ? d : c)) + r3;
-    v += __shfl_xor_sync(0xffffffffu, v, 4);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    return v;
 }
 
 __device__ __forceinline__ void cluster_barrier() {
@@ -1496,6 +1800,46 @@ int pcg_grid_size(int n_rows) {
     // ~2 rows per thread keeps each block's chunk busy; never exceed residency.
     const int want = (n_rows + 2 * kT - 1) / (2 * kT);
     return std::max(1, std::min(want, max_blocks));
+}
+
+int pcg_grid_blocks() {
+    static int g = 0;
+    if (g == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_grid, kGT, 0);
+        g = std::max(1, sms * std::min(std::max(per_sm, 1), 1));
+    }
+    return g;
+}
+
+void launch_pcg_grid(const SolverView& sv, double* vecs, double* partials, double tol, int max_iters,
+                     cudaStream_t s, double eta_loose, double eta_factor) {
+    if (sv.n_rows == 0) return;
+    if (sv.n_parts > kGW) throw Error("pcg: grid kernel folds at most 16 partitions per launch");
+    const size_t n = 6 * static_cast<size_t>(sv.n_rows);
+    GridVecs v{vecs, vecs + n, vecs + 2 * n, vecs + 3 * n, vecs + 4 * n, vecs + 5 * n, vecs + 6 * n,
+               vecs + 7 * n, vecs + 8 * n, vecs + 9 * n};
+    PcgArgs a{nullptr, partials, nullptr, tol, max_iters};
+    a.eta_loose = eta_loose;
+    a.eta_factor = eta_factor;
+    static const int warm = [] {
+        const char* e = std::getenv("DABD_GPU_PCG_WARM");
+        return e ? std::min(std::atoi(e), 1) : 1;
+    }();
+    a.warm = warm;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pcg_grid_blocks());
+    cfg.blockDim = dim3(kGT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DABD_LAUNCH("k_pcg_grid", s, CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_pcg_grid, sv, a, v)));
 }
 
 void launch_pcg_persistent(const SolverView& sv, double* pbuf, double* partials, double* rowval,

@@ -168,3 +168,17 @@ def test_large_body_partner_spill():
         b = o.broad_phase(q, margin)
         assert np.array_equal(a, b)
         assert len(np.unique(a[a[:, 0] == 1, 1])) + len(np.unique(a[a[:, 1] == 1, 0])) > 30
+
+
+def test_pour_10k_single_domain_grid_pcg():
+    """The undivided pour (one partition of 10,000 rows) goes past the
+    cluster kernel's 4,096-row limit to the grid-wide pipelined PCG
+    (k_pcg_grid): two run_reference frames against the oracle's, identical
+    ADMM counts and states within 1e-6 l (exact-solve settings)."""
+    sd = make_scenario("pour-10k")
+    ref = O.Scene(sd).run(2, workers=0)
+    gpu = api.run_reference(sd, 2, **TIGHT)
+    for f in range(2):
+        assert gpu.stats[f]["admm_iterations"] == ref["admm"][f]
+        assert np.abs(gpu.q[f] - ref["q"][f]).max() < 1e-6 * sd.params.scene_scale
+    assert sum(s["pcg_iterations"] for s in gpu.stats) > 0
