@@ -210,7 +210,10 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_comm(dabd_gpu_ctx* ctx, const dabd
 
 /* Exchange path of a joined context: 0 single process, 1 halo callback,
  * 2 peer-memory halo (the neighbours' published packets mapped through CUDA
- * IPC and loaded by the consensus kernel; DABD_GPU_P2P_HALO=0 disables it). */
+ * IPC and loaded by the consensus kernel; DABD_GPU_P2P_HALO=0 disables it),
+ * 3 the same plus the device ADMM loop: every rank's controller fan-in record
+ * and the ordering barriers through IPC-mapped peer slots and device flags,
+ * the attempt one captured graph per rank (DABD_GPU_FANIN=0 disables it). */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_comm_mode(dabd_gpu_ctx* ctx, int* mode);
 
 /* ---- parity entry points (identical-input comparisons with the oracle) ---

@@ -179,7 +179,12 @@ __global__ void k_consensus(int ns, const int* sh, const int* ipart, int part_ba
                             const double* iq, double* iu, const double* irho, const double* iz,
                             const double* remote_lo, const double* remote_hi, int n_lo,
                             double* iznext, double* rb, double* sb, double* rloc, double* sloc,
-                            int* err) {
+                            int* err, const FrameCtrl* pc = nullptr, size_t reg = 0) {
+    if (pc) { // device ADMM loop: the neighbours' publish regions of this iteration's parity
+        const int par = pc->k & 1;
+        if (remote_lo) remote_lo += (1 * 2 + par) * reg;
+        if (remote_hi) remote_hi += (0 * 2 + par) * reg;
+    }
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
         const Replica a = replica(sh[2 * s], iq, iu, irho, remote_lo, remote_hi, n_lo);
         const Replica b = replica(sh[2 * s + 1], iq, iu, irho, remote_lo, remote_hi, n_lo);
@@ -218,7 +223,9 @@ __global__ void k_consensus(int ns, const int* sh, const int* ipart, int part_ba
 
 // Halo packets of the local replicas a neighbouring rank pairs with.
 __global__ void k_pack_halo(int n, const int* inst, const double* iq, const double* iu,
-                            const double* irho, double* out) {
+                            const double* irho, double* out, const FrameCtrl* pc = nullptr, int side = 0,
+                            size_t reg = 0) {
+    if (pc) out += (side * 2 + (pc->k & 1)) * reg; // [side][parity] publish region
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const int i = inst[j];
         double* o = out + kHaloStride * j;
@@ -418,6 +425,52 @@ __global__ void k_unpack_owned(int world, const int* counts, const double* gath,
     }
 }
 
+// ---- device fan-in across ranks (partition-per-GPU device ADMM loop) ------
+// Every rank owns a fan-in buffer [world][rec_len] records + [world] flags,
+// mapped into every peer (CUDA IPC). post: this rank's record (if any) into
+// slot `rank` of every peer's buffer, a system fence, then the flag = the
+// next sequence number; wait: until every flag of the local buffer reached
+// the local sequence number. Every rank posts the same sequence of rounds.
+__global__ void k_fan_post(FanView f, const double* rec, int rec_len) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long seq = ++(*f.seq);
+    for (int r = 0; r < f.world; ++r) {
+        double* dst = f.peer_rec[r] + static_cast<size_t>(f.rank) * f.rec_stride;
+        for (int k = 0; k < rec_len; ++k) dst[k] = rec[k];
+    }
+    __threadfence_system();
+    for (int r = 0; r < f.world; ++r)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f.peer_flag[r] + f.rank), "l"(seq) : "memory");
+}
+
+__global__ void k_fan_wait(FanView f) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long seq = *f.seq;
+    for (int r = 0; r < f.world; ++r) {
+        while (true) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f.local_flag + r) : "memory");
+            if (v >= seq) break;
+            __nanosleep(200);
+        }
+    }
+    __threadfence_system();
+}
+
+// this rank's fan-in record: (n_parts, fail, then per partition dq, r, s, earliest TOI)
+__global__ void k_fan_record(int P, const double* dq, const double* rloc, const double* sloc,
+                             const double* gate, const int* err, double* rec) {
+    if (threadIdx.x != 0) return;
+    rec[0] = P;
+    rec[1] = *err != 0 ? 1.0 : 0.0;
+    for (int p = 0; p < P; ++p) {
+        rec[2 + 4 * p] = dq[p];
+        rec[3 + 4 * p] = rloc[p];
+        rec[4 + 4 * p] = sloc[p];
+        rec[5 + 4 * p] = gate[p];
+    }
+}
+
 __device__ __forceinline__ void admm_cond(unsigned long long h, bool v, int graph) {
     if (graph) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(h), v ? 1u : 0u);
 }
@@ -466,20 +519,32 @@ __global__ void k_admm_ctrl(AdmmCtrlArgs a, int op) {
         const int gc = *a.gate_count;
         if (gc > c->gate_max) c->gate_max = gc;
         int sigma = 0;
-        if (*a.err != 0) {
+        bool fail = *a.err != 0;
+        if (a.fan_rec)
+            for (int rk = 0; rk < a.fan_world; ++rk) fail = fail || a.fan_rec[static_cast<size_t>(rk) * a.fan_stride + 1] != 0.0;
+        if (fail) {
             sigma = -1;
         } else {
-            // runtime.cpp:586-619: every partition's (dq, r, s, earliest TOI)
+            // runtime.cpp:586-619: every partition's (dq, r, s, earliest TOI),
+            // of every rank in partition order when the frame is distributed
             double dq = 0.0, r = 0.0, sres = 0.0, toi = 1.0;
             bool all_one = true;
-            for (int p = 0; p < a.P; ++p) {
-                const double e = a.gate[p];
+            auto take = [&](double dqp, double rp, double sp, double e) {
                 const double t = e > 1.0 ? 1.0 : fmin(1.0, __dmul_rn(0.9, e));
-                dq = fmax(dq, a.dq[p]);
-                r = fmax(r, a.rloc[p]);
-                sres = fmax(sres, a.sloc[p]);
+                dq = fmax(dq, dqp);
+                r = fmax(r, rp);
+                sres = fmax(sres, sp);
                 toi = fmin(toi, t);
                 all_one = all_one && t == 1.0;
+            };
+            if (a.fan_rec) {
+                for (int rk = 0; rk < a.fan_world; ++rk) {
+                    const double* rc = a.fan_rec + static_cast<size_t>(rk) * a.fan_stride;
+                    for (int p = 0; p < static_cast<int>(rc[0]); ++p)
+                        take(rc[2 + 4 * p], rc[3 + 4 * p], rc[4 + 4 * p], rc[5 + 4 * p]);
+                }
+            } else {
+                for (int p = 0; p < a.P; ++p) take(a.dq[p], a.rloc[p], a.sloc[p], a.gate[p]);
             }
             const double nrm = __dmul_rn(a.h, a.l); // consensus.cpp:54-64
             const bool end = __ddiv_rn(dq, nrm) < a.theta && __ddiv_rn(r, nrm) < a.theta &&
@@ -528,7 +593,7 @@ __global__ void k_admm_ctrl(AdmmCtrlArgs a, int op) {
             c->ls_total += a.ps[p].ls_steps;
         }
         c->k += 1;
-        if (s_err != 0) {
+        if (s_err != 0 && !a.fan_rec) { // distributed: the next fan-in carries the failure to every rank
             c->sigma = -1;
             admm_cond(a.hd.admm, false, graph);
         }
@@ -672,6 +737,35 @@ void launch_pack_owned(const SceneView& sc, const uint32_t* bmask, int p0, int p
 void launch_unpack_owned(int world, const int* counts, const double* gath, size_t stride, double* q,
                          double* qd, cudaStream_t s) {
     DABD_LAUNCH("k_unpack_owned", s, k_unpack_owned<<<64, kB, 0, s>>>(world, counts, gath, stride, q, qd));
+}
+
+void launch_fan_post(const FanView& f, const double* rec, int rec_len, cudaStream_t s) {
+    DABD_LAUNCH("k_fan_post", s, k_fan_post<<<1, 32, 0, s>>>(f, rec, rec_len));
+}
+
+void launch_fan_wait(const FanView& f, cudaStream_t s) {
+    DABD_LAUNCH("k_fan_wait", s, k_fan_wait<<<1, 32, 0, s>>>(f));
+}
+
+void launch_fan_record(int P, const double* dq, const double* rloc, const double* sloc, const double* gate,
+                       const int* err, double* rec, cudaStream_t s) {
+    DABD_LAUNCH("k_fan_record", s, k_fan_record<<<1, 32, 0, s>>>(P, dq, rloc, sloc, gate, err, rec));
+}
+
+void launch_pack_halo_par(int n, const int* inst, const double* iq, const double* iu, const double* irho,
+                          double* pub, const FrameCtrl* pc, int side, size_t reg, cudaStream_t s) {
+    if (n == 0) return;
+    DABD_LAUNCH("k_pack_halo", s, k_pack_halo<<<grid_for(n, kB), kB, 0, s>>>(n, inst, iq, iu, irho, pub, pc, side, reg));
+}
+
+void launch_consensus_par(int ns, const int* sh, const int* ipart, int part_base, const double* iq, double* iu,
+                          const double* irho, const double* iz, const double* peer_lo, const double* peer_hi,
+                          int n_lo, double* iznext, double* rb, double* sb, double* rloc, double* sloc, int* err,
+                          const FrameCtrl* pc, size_t reg, cudaStream_t s) {
+    if (ns == 0) return;
+    DABD_LAUNCH("k_consensus", s, k_consensus<<<grid_for(ns, kB), kB, 0, s>>>(ns, sh, ipart, part_base, iq, iu, irho, iz,
+                                                                          peer_lo, peer_hi, n_lo, iznext, rb, sb,
+                                                                          rloc, sloc, err, pc, reg));
 }
 
 } // namespace dabd_gpu

@@ -74,6 +74,27 @@ void launch_masks_w(const SceneView& sc, const double* q, const double* planes, 
                     double h, double w_min, double* w_out, uint32_t all, uint32_t* masks, int* err,
                     cudaStream_t s);
 
+// Device fan-in across ranks (admm.cu k_fan_*): records [world][rec_stride]
+// and flags [world] in every rank's buffer, peers' buffers mapped by IPC.
+struct FanView {
+    int rank = 0, world = 1, rec_stride = 0;
+    double* peer_rec[32] = {};              // slot array of every rank's buffer (own included)
+    unsigned long long* peer_flag[32] = {}; // flags of every rank's buffer
+    const unsigned long long* local_flag = nullptr;
+    const double* local_rec = nullptr;
+    unsigned long long* seq = nullptr; // local round counter (device)
+};
+void launch_fan_post(const FanView& f, const double* rec, int rec_len, cudaStream_t s);
+void launch_fan_wait(const FanView& f, cudaStream_t s);
+void launch_fan_record(int P, const double* dq, const double* rloc, const double* sloc, const double* gate,
+                       const int* err, double* rec, cudaStream_t s);
+void launch_pack_halo_par(int n, const int* inst, const double* iq, const double* iu, const double* irho,
+                          double* pub, const FrameCtrl* pc, int side, size_t reg, cudaStream_t s);
+void launch_consensus_par(int ns, const int* sh, const int* ipart, int part_base, const double* iq, double* iu,
+                          const double* irho, const double* iz, const double* peer_lo, const double* peer_hi,
+                          int n_lo, double* iznext, double* rb, double* sb, double* rloc, double* sloc, int* err,
+                          const FrameCtrl* pc, size_t reg, cudaStream_t s);
+
 // Device controller of the multi-partition consensus-ADMM frame
 // (runtime.cpp:316-476 and the controller round trip 572-638 for the
 // partitions of one context). ops: kAdmmInit, kAdmmHead (IF(gate) = k > 1;
@@ -98,6 +119,10 @@ struct AdmmCtrlArgs {
     int P = 0, K = 0;
     double h = 0.0, l = 0.0, theta = 0.0;
     CondHandles hd;
+    // partition-per-GPU runs: every rank's fan-in record [world][stride]
+    // (n_parts, fail, then dq, r, s, earliest TOI per partition) decides
+    const double* fan_rec = nullptr;
+    int fan_world = 0, fan_stride = 0;
 };
 void launch_admm_ctrl(const AdmmCtrlArgs& a, int op, cudaStream_t s);
 

@@ -181,6 +181,7 @@ Engine::~Engine() {
     for (cudaStream_t s : side_streams_) cudaStreamDestroy(s);
     if (peer_lo_) cudaIpcCloseMemHandle(const_cast<double*>(peer_lo_));
     if (peer_hi_) cudaIpcCloseMemHandle(const_cast<double*>(peer_hi_));
+    for (void* ptr : fan_opened_) cudaIpcCloseMemHandle(ptr);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (own_stream_ && s_) cudaStreamDestroy(s_);
@@ -205,6 +206,7 @@ void Engine::set_comm(const Comm* c) {
     cudaGetLastError();
     peer_lo_ = peer_hi_ = nullptr;
     p2p_ = false;
+    close_fanin();
     halo_parity_ = 0;
     if (!c) {
         distributed_ = false;
@@ -227,6 +229,7 @@ void Engine::set_comm(const Comm* c) {
     part_rank_.upload(pr, s_);
     sync();
     if (distributed_) setup_p2p();
+    if (distributed_ && p2p_) setup_fanin();
 }
 
 // One all-gather of a single value: every rank's earlier work on its stream
@@ -287,6 +290,83 @@ void Engine::setup_p2p() {
     peer_lo_ = static_cast<const double*>(lo);
     peer_hi_ = static_cast<const double*>(hi);
     p2p_ = true;
+}
+
+void Engine::close_fanin() {
+    for (void* ptr : fan_opened_) cudaIpcCloseMemHandle(ptr);
+    fan_opened_.clear();
+    cudaGetLastError();
+    fan_ok_ = false;
+}
+
+// Every rank's fan-in buffer mapped into every peer (the partition-per-GPU
+// device ADMM loop's controller fan-in and ordering barriers; runtime.cpp:
+// 586-619 without a host round trip). All ranks agree or none uses it.
+void Engine::setup_fanin() {
+    close_fanin();
+    if (const char* e = std::getenv("DABD_GPU_FANIN"))
+        if (e[0] == '0') return;
+    const int world = comm_.world;
+    if (world > 32) return;
+    const size_t rec_bytes = sizeof(double) * kFanStride * static_cast<size_t>(world);
+    fan_buf_.resize(rec_bytes + sizeof(unsigned long long) * world);
+    fan_buf_.zero(s_);
+    fan_rec_local_.resize(kFanStride);
+    fan_seq_.resize(1);
+    fan_seq_.zero(s_);
+    sync();
+    std::vector<double> rec(9, 0.0);
+    cudaIpcMemHandle_t mine{};
+    bool ok = cudaIpcGetMemHandle(&mine, fan_buf_.get()) == cudaSuccess;
+    cudaGetLastError();
+    std::memcpy(rec.data(), &mine, sizeof(mine));
+    rec[8] = ok ? 1.0 : 0.0;
+    rec_.upload(rec, s_);
+    rec_all_.resize(9 * world);
+    if (comm_.allgather(comm_.user, rec_.get(), rec_all_.get(), 9, reinterpret_cast<uintptr_t>(s_)) != 0)
+        throw Error("comm: all-gather failed");
+    std::vector<double> all = rec_all_.to_host(s_);
+    FanView f;
+    f.rank = comm_.rank;
+    f.world = world;
+    f.rec_stride = kFanStride;
+    for (int r = 0; r < world && ok; ++r) {
+        unsigned char* base = nullptr;
+        if (r == comm_.rank) {
+            base = fan_buf_.get();
+        } else {
+            if (all[9 * r + 8] == 0.0) {
+                ok = false;
+                break;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, all.data() + 9 * r, sizeof(h));
+            void* ptr = nullptr;
+            ok = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+            cudaGetLastError();
+            if (!ok) break;
+            fan_opened_.push_back(ptr);
+            base = static_cast<unsigned char*>(ptr);
+        }
+        f.peer_rec[r] = reinterpret_cast<double*>(base);
+        f.peer_flag[r] = reinterpret_cast<unsigned long long*>(base + rec_bytes);
+    }
+    f.local_rec = reinterpret_cast<const double*>(fan_buf_.get());
+    f.local_flag = reinterpret_cast<const unsigned long long*>(fan_buf_.get() + rec_bytes);
+    f.seq = fan_seq_.get();
+    rec_.upload(std::vector<double>{ok ? 1.0 : 0.0}, s_);
+    rec_all_.resize(world);
+    if (comm_.allgather(comm_.user, rec_.get(), rec_all_.get(), 1, reinterpret_cast<uintptr_t>(s_)) != 0)
+        throw Error("comm: all-gather failed");
+    all = rec_all_.to_host(s_);
+    bool every = true;
+    for (int r = 0; r < world; ++r) every = every && all[r] != 0.0;
+    if (!every) {
+        close_fanin();
+        return;
+    }
+    fan_view_ = f;
+    fan_ok_ = true;
 }
 
 void Engine::exchange_halo() {
@@ -1744,6 +1824,15 @@ int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, in
     a.h = h;
     a.l = P.scene_scale;
     a.theta = P.theta;
+    const bool dist = distributed_;
+    if (dist) {
+        if (!p2p_ || !fan_ok_) throw Error("admm: the device loop of a distributed frame needs the peer-memory paths");
+        if (static_cast<size_t>(std::max(n_halo_lo_, n_halo_hi_)) > pub_cap_)
+            throw Error("comm: peer halo capacity exceeded");
+        a.fan_rec = fan_view_.local_rec;
+        a.fan_world = comm_.world;
+        a.fan_stride = kFanStride;
+    }
 
     KernelTimer::get().suspend(true);
     hd_ = CondHandles{};
@@ -1762,9 +1851,25 @@ int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, in
             a.hd = hd_;
             launch_admm_ctrl(a, kAdmmHead, s_);
             add_cond_node(hd_.gate, false, 1, [&] {
-                launch_consensus(ns, shared_inst_.get(), ipart_.get(), p0_, iq_.get(), iu_.get(),
-                                 irho_.get(), iz_.get(), nullptr, nullptr, 0, iznext_.get(), rb_.get(),
-                                 sb_.get(), rloc_.get(), sloc_.get(), err_.get(), s_);
+                if (dist) {
+                    // split-body packets into this iteration's [side][parity]
+                    // publish regions, the ordering barrier, then k_consensus
+                    // reads the neighbours' packets in place over peer memory
+                    const size_t reg = static_cast<size_t>(kHaloStride) * pub_cap_;
+                    launch_pack_halo_par(n_halo_lo_, halo_inst_.get(), iq_.get(), iu_.get(), irho_.get(), pub_.get(),
+                                         ctrl_.get(), 0, reg, s_);
+                    launch_pack_halo_par(n_halo_hi_, halo_inst_.get() + n_halo_lo_, iq_.get(), iu_.get(), irho_.get(),
+                                         pub_.get(), ctrl_.get(), 1, reg, s_);
+                    launch_fan_post(fan_view_, nullptr, 0, s_);
+                    launch_fan_wait(fan_view_, s_);
+                    launch_consensus_par(ns, shared_inst_.get(), ipart_.get(), p0_, iq_.get(), iu_.get(), irho_.get(),
+                                         iz_.get(), peer_lo_, peer_hi_, n_halo_lo_, iznext_.get(), rb_.get(),
+                                         sb_.get(), rloc_.get(), sloc_.get(), err_.get(), ctrl_.get(), reg, s_);
+                } else {
+                    launch_consensus(ns, shared_inst_.get(), ipart_.get(), p0_, iq_.get(), iu_.get(),
+                                     irho_.get(), iz_.get(), nullptr, nullptr, 0, iznext_.get(), rb_.get(),
+                                     sb_.get(), rloc_.get(), sloc_.get(), err_.get(), s_);
+                }
                 // merge gate per partition (consensus.cpp:66-75): fixed-capacity
                 // broad phase, CCD over its device count
                 launch_merged(I, ianc_.get(), iq_.get(), iznext_.get(), iqtry_.get(), s_);
@@ -1772,6 +1877,12 @@ int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, in
                                   n_stat_, true, 0.0, err_.get(), s_);
                 launch_ccd(view(), det_gate_.keys(), det_gate_.cap(), det_gate_.d_count(), det_gate_.fmt(),
                            det_gate_.boxes(), iq_.get(), iqtry_.get(), 2, gate_.get(), s_);
+                if (dist) { // controller fan-in (runtime.cpp:586-601) through peer memory
+                    launch_fan_record(P_, admm_dq_.get(), rloc_.get(), sloc_.get(), gate_.get(), err_.get(),
+                                      fan_rec_local_.get(), s_);
+                    launch_fan_post(fan_view_, fan_rec_local_.get(), 2 + 4 * P_, s_);
+                    launch_fan_wait(fan_view_, s_);
+                }
                 launch_admm_ctrl(a, kAdmmDecide, s_);
             });
             add_cond_node(hd_.solve, false, 2, [&] {
@@ -1839,7 +1950,41 @@ int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, in
                  static_cast<long long>(c.exec_newton) * (inc[3] - inc[4]) +
                  static_cast<long long>(c.exec_step) * (inc[4] - inc[5]) +
                  static_cast<long long>(c.exec_ls) * inc[5]);
-    const int code = pin_i_[0];
+    int code = pin_i_[0];
+    if (dist) {
+        // every rank ran the same rounds; agree on the outcome: a recoverable
+        // error anywhere redoes the attempt everywhere (each rank grows what
+        // overflowed locally; a line-search collapse anywhere arms the exact
+        // solve everywhere, as one context would), anything else fails all
+        const std::vector<double> all = allgather_host({static_cast<double>(code)});
+        const size_t stride = all.size() / comm_.world;
+        bool any = false, fatal = false, ls = false;
+        for (int r = 0; r < comm_.world; ++r) {
+            const int cr = static_cast<int>(all[stride * r]);
+            any = any || cr != 0;
+            ls = ls || cr == kErrLineSearch;
+            fatal = fatal || (cr != 0 && cr != kErrCapacity && cr != kErrEll && cr != kErrLineSearch);
+        }
+        if (any) {
+            err_.zero(s_);
+            if (fatal || grows >= kMaxGrows || (ls && exact)) {
+                sync();
+                if (code != 0) throw DeviceError(std::string(err_text(code)) + " [admm frame]", code);
+                throw Error("admm: a peer rank failed");
+            }
+            const int gate_count = std::max(pin_i_[9], c.gate_max);
+            if (code == kErrCapacity && gate_count > gate_cap_) gate_cap_ = 2 * gate_count;
+            else if (code == kErrCapacity || code == kErrEll) grow_capacity(code);
+            if (ls && !exact) {
+                set_solver(1e-14, std::max(pcg_max_, 50000));
+                exact = true;
+                ++exact_retries_;
+            }
+            ++grows;
+            ++capacity_retries_;
+            return 0;
+        }
+    }
     if (code != 0) {
         err_.zero(s_);
         const int gate_count = std::max(pin_i_[9], c.gate_max); // the largest gate of the attempt
@@ -2097,7 +2242,21 @@ FrameStats Engine::frame_admm(int frame) {
         // A local failure on one rank must not leave its peers blocked in a
         // collective: it is carried to the next agreement point instead.
         std::string fail;
-        for (int k = 1; k <= hs_.admm_max_iterations; ++k) {
+        // partition-per-GPU: the host built the sets (remote replicas, halo
+        // lists); the k-loop itself runs on the device when every rank mapped
+        // the peer-memory paths (the same decision on every rank)
+        const bool device_loop = distributed_ && p2p_ && fan_ok_ && admm_device_ && use_graph_;
+        if (device_loop) {
+            const int r = admm_attempt_device(frame, attempt, h, tol, I, ns, st, cost, dev_grows, dev_exact);
+            if (r == 0) continue; // recoverable error somewhere: redo the attempt on every rank
+            if (r == 2) {
+                tsc_.on_frame_failed();
+                retry = true;
+            } else {
+                ended = true;
+            }
+        }
+        for (int k = 1; !device_loop && k <= hs_.admm_max_iterations; ++k) {
             if (k > 1) {
                 std::vector<double> earliest(P_, 2.0), rl(P_, 0.0), sl(P_, 0.0);
                 try {

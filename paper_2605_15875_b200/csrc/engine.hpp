@@ -8,6 +8,7 @@
 #include "audit.hpp"
 #include "geometry.cuh"
 #include "kernels.hpp"
+#include "admm.hpp"
 #include "balance.hpp"
 #include "controller.hpp"
 #include "scene.hpp"
@@ -69,7 +70,11 @@ class Engine {
         ++solver_epoch_;
     }
     cudaStream_t stream() const { return s_; }
-    int comm_mode() const { return !distributed_ ? 0 : (p2p_ ? 2 : 1); }
+    int comm_mode() const {
+        if (!distributed_) return 0;
+        if (!p2p_) return 1;
+        return fan_ok_ && admm_device_ && use_graph_ ? 3 : 2;
+    }
     const HostScene& scene() const { return hs_; }
 
     // ---- parity entry points (host arrays) ----
@@ -293,6 +298,17 @@ class Engine {
     // pub_ regions: [side lo/hi][parity] x pub_cap_ packets.
     void setup_p2p();
     void comm_barrier();
+    // Device fan-in (partition-per-GPU device ADMM loop): every rank's buffer
+    // [world][kFanStride] records + [world] flags, mapped into every peer.
+    static constexpr int kFanStride = 2 + 4 * kMaxParts;
+    void setup_fanin();
+    void close_fanin();
+    DBuf<unsigned char> fan_buf_;
+    DBuf<double> fan_rec_local_;
+    DBuf<unsigned long long> fan_seq_;
+    FanView fan_view_;
+    std::vector<void*> fan_opened_;
+    bool fan_ok_ = false;
     DBuf<double> pub_;
     size_t pub_cap_ = 0;
     const double* peer_lo_ = nullptr; // rank - 1's pub_ (mapped)

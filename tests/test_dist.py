@@ -156,8 +156,11 @@ def _gpu_worker(rank, world, port, q, name, workers, frames, balanced=False, p2p
 ])
 def test_partitioned_matches_single_gpu(name, workers, world, frames, p2p):
     """p2p "1": k_consensus loads the neighbours' packets through CUDA IPC
-    mappings of their published buffers (the ranks share cuda:0 here; NVLink
-    peer loads on a multi-GPU box); "0": the halo callback (NCCL / gloo)."""
+    mappings of their published buffers and the whole ADMM attempt runs as a
+    device graph per rank, the controller fan-in and the ordering barriers
+    through IPC-mapped peer slots (the ranks share cuda:0 here; NVLink peer
+    stores on a multi-GPU box); "0": the halo callback (NCCL / gloo) and the
+    host-driven loop."""
     from paper_2605_15875_b200 import api
     from paper_2605_15875_b200.scene import make_scenario
 
@@ -168,7 +171,7 @@ def test_partitioned_matches_single_gpu(name, workers, world, frames, p2p):
     for r in range(world):
         assert not isinstance(out[r], BaseException), out[r]
         qs, qds, trace, rrho, admm, hs, mode = out[r]
-        assert mode == (2 if p2p == "1" else 1)
+        assert mode == (3 if p2p == "1" else 1)  # 3: peer-memory halo + device ADMM loop
         assert admm == [s["admm_iterations"] for s in ref.stats]
         assert hs == list(ref.h)
         assert np.array_equal(trace, ref.trace), (r, np.abs(trace - ref.trace).max())
