@@ -195,9 +195,9 @@ DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_solver(dabd_gpu_ctx* ctx,
  * of pcg_rel_tol) while its root-mean-square entry exceeds `factor` x the
  * Newton tolerance theta h l (so ||dq||_inf does too): a direction that can
  * decide convergence (newton.cpp:30-36) is always solved to pcg_rel_tol, and
- * one that ends a line search (newton.cpp:56-62) only after the step was
- * halved below 1 / factor. eta <= pcg_rel_tol (e.g. 0) turns it off. Default: 1e-4,
- * factor 2 for single-domain contexts (num_workers == 0), off for consensus
+ * a loose one ends a line search (newton.cpp:56-62) only on a step shortened
+ * below 1 / factor. eta <= pcg_rel_tol (e.g. 0) turns it off. Default: 1e-3,
+ * factor 1 for single-domain contexts (num_workers == 0), off for consensus
  * contexts (their stop test reads residuals of the local solutions);
  * dabd_gpu_newton_solve always solves every direction to pcg_rel_tol. */
 DABD_GPU_API dabd_gpu_status dabd_gpu_ctx_set_inexact(dabd_gpu_ctx* ctx, double eta, double factor);

@@ -165,7 +165,7 @@ Engine::Engine(const HostScene& hs, int device, int W, int pb, int pe) : hs_(hs)
     // consensus frame's stop test reads residuals built from the local
     // solutions, which the loose directions would perturb at the scale it
     // tests); dabd_gpu_ctx_set_inexact overrides
-    eta_loose_ = W_ == 0 ? 1e-4 : 0.0;
+    eta_loose_ = W_ == 0 ? 1e-3 : 0.0;
     if (const char* e = std::getenv("DABD_GPU_PCG_ETA")) eta_loose_ = std::atof(e);
     if (const char* e = std::getenv("DABD_GPU_PCG_ETA_FACTOR")) eta_factor_ = std::atof(e);
     if (const char* e = std::getenv("DABD_SKIN_MIN")) skin_min_ = std::atof(e);
@@ -999,8 +999,12 @@ void Engine::enq_newton_ccd() {
 // One backtracking trial (newton.cpp:47-59) for every partition still searching.
 void Engine::enq_ls_trial() {
     SolverView v = view();
-    enq_energy(1, 1, &PartState::trial, true); // trial value + kOpAccept
-    launch_accept_trial(v, s_);
+    // small instance sets: the energy kernel's last block also applies the
+    // accepted step (one launch per trial instead of two)
+    const bool fuse = n_inst_ <= kFuseAcceptMaxInst;
+    launch_energy(v, det_.keys(), cap_, det_.d_count(), cfmt_, 1, 1, partial_.get(),
+                  ps_field(ps_.get(), &PartState::trial), kPsStride, true, ctrl_.get(), hd_, s_, fuse);
+    if (!fuse) launch_accept_trial(v, s_);
 }
 
 int* Engine::iter_reset() { return pcg_fused() ? &lstate_.get()->n_act : nullptr; }

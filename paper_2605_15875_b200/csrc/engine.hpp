@@ -189,7 +189,7 @@ class Engine {
     // convergence are solved to pcg_tol_. 0 = off (default for consensus
     // contexts; 1e-4 for single-domain ones, set in the constructor). The
     // standalone newton_solve parity entry point always solves to pcg_tol_.
-    double eta_loose_ = 0.0, eta_factor_ = 2.0;
+    double eta_loose_ = 0.0, eta_factor_ = 1.0;
     bool inexact_ = true;
 
     // global replicated state
@@ -301,6 +301,7 @@ class Engine {
     // Device fan-in (partition-per-GPU device ADMM loop): every rank's buffer
     // [world][kFanStride] records + [world] flags, mapped into every peer.
     static constexpr int kFanStride = 2 + 4 * kMaxParts;
+    static constexpr int kFuseAcceptMaxInst = 4096; // k_energy's last block applies accepted steps up to this
     void setup_fanin();
     void close_fanin();
     DBuf<unsigned char> fan_buf_;

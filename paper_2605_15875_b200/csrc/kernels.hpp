@@ -133,7 +133,7 @@ struct PcgFuse {
 // energy_chunks(cap) blocks x P doubles.
 void launch_energy(const SolverView& sv, const unsigned long long* keys, int cap, const int* dn,
                    KeyFmt fmt, int qmode, int which, double* partial, double* dst, int stride,
-                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s);
+                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s, bool apply = false);
 void launch_accept_trial(const SolverView& sv, cudaStream_t s);
 
 void launch_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHandles h, double tol,

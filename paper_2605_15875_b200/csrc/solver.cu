@@ -522,7 +522,18 @@ struct EnergyArgs {
     int accept;      // run kOpAccept in the last block
     FrameCtrl* ctrl;
     CondHandles hd;
+    int apply;       // accept: the last block also applies iq += alpha dq (k_accept_trial's work)
 };
+
+__device__ __forceinline__ void accept_trial_range(const SolverView& sv, int i0, int step) {
+    for (int i = i0; i < sv.n_inst; i += step) {
+        const int p = sv.ipart[i] - sv.part_base;
+        if (!sv.ps[p].accepted || sv.irow[i] < 0) continue;
+        double q[6];
+        eval_q(sv, i, 2, q);
+        store6(sv.iq + 6 * i, q);
+    }
+}
 
 __global__ void __launch_bounds__(kB) k_energy(SolverView sv, EnergyArgs ea) {
     __shared__ double sh[kB];
@@ -597,18 +608,15 @@ __global__ void __launch_bounds__(kB) k_energy(SolverView sv, EnergyArgs ea) {
     if (!ea.accept) return;
     __syncthreads();
     scalar_block(sv.ps, P, kOpAccept, ea.ctrl, ea.hd, 0.0, 0, sv.err);
+    if (!ea.apply) return;
+    __syncthreads(); // the accept decisions of this block are visible to it
+    accept_trial_range(sv, threadIdx.x, blockDim.x);
 }
 
 // iq += alpha dq for the instances of partitions whose trial was accepted
 // (k_make_trial + k_accept_copy: the same unfused arithmetic as the trial).
 __global__ void k_accept_trial(SolverView sv) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < sv.n_inst; i += gridDim.x * blockDim.x) {
-        const int p = sv.ipart[i] - sv.part_base;
-        if (!sv.ps[p].accepted || sv.irow[i] < 0) continue;
-        double q[6];
-        eval_q(sv, i, 2, q);
-        store6(sv.iq + 6 * i, q);
-    }
+    accept_trial_range(sv, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -1378,10 +1386,10 @@ void launch_segsum_keys(const double* v, int n, const int* dn, const unsigned lo
 
 void launch_energy(const SolverView& sv, const unsigned long long* keys, int cap, const int* dn,
                    KeyFmt fmt, int qmode, int which, double* partial, double* dst, int stride,
-                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s) {
+                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s, bool apply) {
     const int ncr = energy_chunks(sv.n_rows), nck = energy_chunks(cap);
     EnergyArgs ea{keys, cap, dn, fmt, qmode, which, ncr, partial, segsum_ticket(), dst, stride,
-                  accept ? 1 : 0, ctrl, hd};
+                  accept ? 1 : 0, ctrl, hd, apply && accept ? 1 : 0};
     DABD_LAUNCH("k_energy", s, k_energy<<<ncr + nck, kB, 0, s>>>(sv, ea));
 }
 
