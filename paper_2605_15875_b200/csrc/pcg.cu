@@ -774,6 +774,17 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     const PartState& st = sv.ps[p];
     const bool act = st.active != 0 && R1 > R0;
     double eps = st.eps;
+    // the warm start's previous solutions, loaded now so their L2 latency
+    // hides behind the staging and the exchange plan
+    double wp1[G], wp2[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int lrw = warp * kRowsPerWarp + slot + g * kCW * kRowsPerWarp;
+        const bool onw = lane < 30 && lrw < nr;
+        const size_t e = 6 * static_cast<size_t>(r0 + lrw) + comp;
+        wp1[g] = a.warm && onw && act ? sv.x[e] : 0.0;
+        wp2[g] = a.warm > 1 && onw && act ? a.pa[e] : 0.0;
+    }
     // inexact Newton (a.eta_loose > 0): the solve may stop at the relative
     // residual eta_loose instead of tol, but only while the iterate's
     // ||x||_2^2 (a fourth sum next to the CG dots, same shuffles) exceeds
@@ -1238,8 +1249,8 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             const size_t e = 6 * static_cast<size_t>(r0 + lrg[g]) + comp;
-            p1[g] = on[g] && act ? sv.x[e] : 0.0;
-            p2[g] = on[g] && act && a.warm > 1 ? a.pa[e] : 0.0;
+            p1[g] = wp1[g];
+            p2[g] = wp2[g];
             if (on[g]) {
                 vm1[6 * lrg[g] + comp] = p1[g];
                 vm0[6 * lrg[g] + comp] = p2[g];
@@ -1259,10 +1270,11 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             l[4] += p2[g] * ap2[g];
             l[5] += r[g] * r[g];
         }
-#pragma unroll
-        for (int k = 0; k < 6; ++k) l[k] = warp_sum(l[k]);
-        if (lane == 0)
-            for (int k = 0; k < 6; ++k) sc.wred[warp][k] = l[k];
+        {
+            const double va = warp_sum4(l[0], l[1], l[2], l[3], lane), vb = warp_sum4(l[4], l[5], 0.0, 0.0, lane);
+            if ((lane & 7) == 0) sc.wred[warp][lane >> 3] = va;
+            if ((lane & 7) == 0 && lane < 16) sc.wred[warp][4 + (lane >> 3)] = vb;
+        }
         __syncthreads();
         if (threadIdx.x < 6) {
             double t = 0.0;
@@ -1277,8 +1289,13 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             double tt[6];
 #pragma unroll
             for (int m = 0; m < 6; ++m) tt[m] = lane < csize ? cl.map_shared_rank(&sc, lane)->wsp[m] : 0.0;
+            {
+                const double va = warp_sum4(tt[0], tt[1], tt[2], tt[3], lane), vb = warp_sum4(tt[4], tt[5], 0.0, 0.0, lane);
 #pragma unroll
-            for (int m = 0; m < 6; ++m) tt[m] = warp_sum(tt[m]);
+                for (int m = 0; m < 4; ++m) tt[m] = __shfl_sync(0xffffffffu, va, 8 * m);
+                tt[4] = __shfl_sync(0xffffffffu, vb, 0);
+                tt[5] = __shfl_sync(0xffffffffu, vb, 8);
+            }
             const double b1 = tt[0], b2 = tt[1], a11 = tt[2], a12 = tt[3], a22 = tt[4];
             double c1 = 0.0, c2 = 0.0;
             const double det = a11 * a22 - a12 * a12;
