@@ -949,7 +949,7 @@ void Engine::enq_pcg(bool fused) {
     const int max_rows = max_part_rows();
     if (max_rows <= kClusterPcgMaxRows) {
         // small partitions: one thread-block cluster per partition (DSMEM dots)
-        PcgFuse f{rowtmp_.get(), ctrl_.get(), hd_, inexact_ ? eta_loose_ : 0.0, eta_factor_};
+        PcgFuse f{rowtmp_.get(), ctrl_.get(), hd_, inexact_ ? eta_loose_ : 0.0, eta_factor_, tail_max_iters_ > 0};
         launch_pcg_cluster(view(), max_rows, pbuf_.get(), pcg_tol_, pcg_max_, s_, fused ? &f : nullptr);
     } else {
         static const bool grid_kernel = [] {
@@ -1002,8 +1002,12 @@ void Engine::enq_ls_trial() {
     // small instance sets: the energy kernel's last block also applies the
     // accepted step (one launch per trial instead of two)
     const bool fuse = n_inst_ <= kFuseAcceptMaxInst;
+    // captured fused body (cap_newton): the last trial also takes the Newton
+    // tail when the accepted step is applied in the same kernel
+    const int tail = hd_.graph && pcg_fused() && fuse ? tail_max_iters_ : 0;
     launch_energy(v, det_.keys(), cap_, det_.d_count(), cfmt_, 1, 1, partial_.get(),
-                  ps_field(ps_.get(), &PartState::trial), kPsStride, true, ctrl_.get(), hd_, s_, fuse);
+                  ps_field(ps_.get(), &PartState::trial), kPsStride, true, ctrl_.get(), hd_, s_, fuse, tail,
+                  tail ? iter_reset() : nullptr);
     if (!fuse) launch_accept_trial(v, s_);
 }
 
@@ -1221,6 +1225,11 @@ cudaStream_t Engine::cap_stream(int level) {
 void Engine::cap_newton(int max_iters, double tol, int level) {
     hd_.newton = new_cond_handle();
     enq_solve_begin(tol);
+    // fused body, small sets: the tail (newton.cpp:16's loop bound, the WHILE
+    // condition, the next iteration's resets) rides on the last line-search
+    // trial, and the PCG epilogue closes the loop when nothing stays active
+    const bool folded_tail = pcg_fused() && n_inst_ <= kFuseAcceptMaxInst;
+    tail_max_iters_ = folded_tail ? max_iters : 0;
     add_cond_node(hd_.newton, true, level, [&] {
         hd_.step = new_cond_handle(); // set by kOpNewtonCheck inside the head
         enq_newton_head(max_iters);
@@ -1229,9 +1238,11 @@ void Engine::cap_newton(int max_iters, double tol, int level) {
             enq_newton_ccd();
             add_cond_node(hd_.ls, true, level + 2, [&] { enq_ls_trial(); });
         });
-        launch_scalar(ps_.get(), P_, kOpNewtonTail, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_,
-                      iter_reset());
+        if (!folded_tail)
+            launch_scalar(ps_.get(), P_, kOpNewtonTail, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_,
+                          iter_reset());
     });
+    tail_max_iters_ = 0;
 }
 
 

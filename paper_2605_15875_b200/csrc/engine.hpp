@@ -302,6 +302,7 @@ class Engine {
     // [world][kFanStride] records + [world] flags, mapped into every peer.
     static constexpr int kFanStride = 2 + 4 * kMaxParts;
     static constexpr int kFuseAcceptMaxInst = 4096; // k_energy's last block applies accepted steps up to this
+    int tail_max_iters_ = 0; // while capturing a folded-tail Newton body: its iteration cap
     void setup_fanin();
     void close_fanin();
     DBuf<unsigned char> fan_buf_;

@@ -124,7 +124,8 @@ struct PcgFuse {
     FrameCtrl* ctrl;
     CondHandles hd;          // hd.step is set from the convergence decision
     double eta_loose = 0.0;  // inexact Newton: loose relative residual (0: off)
-    double eta_factor = 0.0; // ... allowed while ||x||_inf > eta_factor x Newton tol
+    double eta_factor = 0.0; // ... allowed while rms(x) > eta_factor x Newton tol
+    bool close_loop = false; // folded Newton tail: end the Newton WHILE when no partition stays active
 };
 
 // Fused objective value (solver.cu k_energy): qmode 0 = iq, 1 = line-search
@@ -133,7 +134,8 @@ struct PcgFuse {
 // energy_chunks(cap) blocks x P doubles.
 void launch_energy(const SolverView& sv, const unsigned long long* keys, int cap, const int* dn,
                    KeyFmt fmt, int qmode, int which, double* partial, double* dst, int stride,
-                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s, bool apply = false);
+                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s, bool apply = false,
+                   int tail_max_iters = 0, int* iter_reset = nullptr);
 void launch_accept_trial(const SolverView& sv, cudaStream_t s);
 
 void launch_scalar(PartState* ps, int P, int op, FrameCtrl* ctrl, CondHandles h, double tol,

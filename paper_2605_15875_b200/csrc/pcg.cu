@@ -106,6 +106,7 @@ struct PcgArgs {
     int fold_all; // 1: every warp folds the cluster partials itself, 0: the scalar warp folds
     int remote_first; // 1: remote-column SpMV before the scalar hand-off
     int fast_rcp;     // 1: alpha from a MUFU reciprocal + 2 Newton steps, 0: IEEE division
+    int close_loop;   // folded Newton tail (PcgFuse::close_loop)
     // inexact Newton (fused cluster kernel, 0: off): stop at the relative
     // residual eta_loose while rms(x) > eta_factor x the Newton tolerance
     double eta_loose;
@@ -1644,8 +1645,11 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 a.ctrl->any_active = any_act;
                 a.ctrl->any_searching = any_srch;
             }
-            if (a.hd.graph)
+            if (a.hd.graph) {
                 cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.hd.step), any_act ? 1u : 0u);
+                if (a.close_loop && !any_act) // the folded tail never runs: close the Newton loop here
+                    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.hd.newton), 0u);
+            }
         }
     }
     if constexpr (PH) {
@@ -1785,6 +1789,7 @@ void launch_pcg_cluster(const SolverView& sv, int max_rows_per_part, double* pbu
         a.ticket = pcg_ticket();
         a.eta_loose = fuse->eta_loose;
         a.eta_factor = fuse->eta_factor;
+        a.close_loop = fuse->close_loop ? 1 : 0;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csize * sv.n_parts);

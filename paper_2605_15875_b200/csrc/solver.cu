@@ -523,6 +523,9 @@ struct EnergyArgs {
     FrameCtrl* ctrl;
     CondHandles hd;
     int apply;       // accept: the last block also applies iq += alpha dq (k_accept_trial's work)
+    int tail;        // captured fused Newton body: when no partition searches any more, the last
+    int max_iters;   // block also takes kOpNewtonTail (the loop bound, the Newton WHILE
+    int* iter_reset; // condition, the next iteration's resets): one node fewer per iteration
 };
 
 __device__ __forceinline__ void accept_trial_range(const SolverView& sv, int i0, int step) {
@@ -608,9 +611,15 @@ __global__ void __launch_bounds__(kB) k_energy(SolverView sv, EnergyArgs ea) {
     if (!ea.accept) return;
     __syncthreads();
     scalar_block(sv.ps, P, kOpAccept, ea.ctrl, ea.hd, 0.0, 0, sv.err);
-    if (!ea.apply) return;
-    __syncthreads(); // the accept decisions of this block are visible to it
-    accept_trial_range(sv, threadIdx.x, blockDim.x);
+    if (ea.apply) {
+        __syncthreads(); // the accept decisions of this block are visible to it
+        accept_trial_range(sv, threadIdx.x, blockDim.x);
+    }
+    if (!ea.tail) return;
+    __syncthreads();
+    const bool srch = threadIdx.x < P && sv.ps[threadIdx.x].searching != 0;
+    if (__syncthreads_or(srch)) return; // the line search goes on: the tail comes later
+    scalar_block(sv.ps, P, kOpNewtonTail, ea.ctrl, ea.hd, 0.0, ea.max_iters, sv.err, ea.iter_reset);
 }
 
 // iq += alpha dq for the instances of partitions whose trial was accepted
@@ -1386,10 +1395,12 @@ void launch_segsum_keys(const double* v, int n, const int* dn, const unsigned lo
 
 void launch_energy(const SolverView& sv, const unsigned long long* keys, int cap, const int* dn,
                    KeyFmt fmt, int qmode, int which, double* partial, double* dst, int stride,
-                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s, bool apply) {
+                   bool accept, FrameCtrl* ctrl, CondHandles hd, cudaStream_t s, bool apply, int tail_max_iters,
+                   int* iter_reset) {
     const int ncr = energy_chunks(sv.n_rows), nck = energy_chunks(cap);
     EnergyArgs ea{keys, cap, dn, fmt, qmode, which, ncr, partial, segsum_ticket(), dst, stride,
-                  accept ? 1 : 0, ctrl, hd, apply && accept ? 1 : 0};
+                  accept ? 1 : 0, ctrl, hd, apply && accept ? 1 : 0, accept && tail_max_iters > 0 ? 1 : 0,
+                  tail_max_iters, iter_reset};
     DABD_LAUNCH("k_energy", s, k_energy<<<ncr + nck, kB, 0, s>>>(sv, ea));
 }
 
