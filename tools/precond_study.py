@@ -147,13 +147,97 @@ def main():
 
     for size in (2, 4, 8, 16):
         print(f"aggregate block-Jacobi, clusters <= {size} bodies (iterations, clusters):", agg_jacobi(size))
-    # contiguous index chunks as blocks (what a CTA-local exact solve would give)
-    for chunk in (8, 63):
+
+    # the same greedy aggregates restricted to CTA chunks of `chunk` rows in a
+    # given row order (body order = the kernel's today; Morton order of the
+    # centroids = a spatial reordering), to 1e-10 and 1e-3
+    def chunked(size, chunk, order):
+        pos = np.empty(nb, dtype=int)
+        pos[order] = np.arange(nb)
+        parent = list(range(nb))
+        members = {i: [i] for i in range(nb)}
+
+        def find(x):
+            while parent[x] != x:
+                parent[x] = parent[parent[x]]
+                x = parent[x]
+            return x
+
+        for w, i, j in edges:
+            if pos[i] // chunk != pos[j] // chunk:
+                continue
+            a, c = find(i), find(j)
+            if a == c or len(members[a]) + len(members[c]) > size:
+                continue
+            parent[c] = a
+            members[a] += members.pop(c)
+        Minv = np.zeros_like(A)
+        for gr in members.values():
+            idx = np.concatenate([np.arange(6 * i, 6 * i + 6) for i in gr])
+            Minv[np.ix_(idx, idx)] = np.linalg.inv(A[np.ix_(idx, idx)])
+        return pcg(A, b, lambda r: Minv @ r), pcg(A, b, lambda r: Minv @ r, tol=1e-3), len(members)
+
+    def morton(xy):
+        lo, hi = xy.min(0), xy.max(0)
+        g = np.minimum(((xy - lo) / np.maximum(hi - lo, 1e-30) * 1023).astype(np.int64), 1023)
+        code = np.zeros(len(xy), dtype=np.int64)
+        for bit in range(10):
+            code |= ((g[:, 0] >> bit) & 1) << (2 * bit)
+            code |= ((g[:, 1] >> bit) & 1) << (2 * bit + 1)
+        return np.argsort(code, kind="stable")
+
+    body_order = np.arange(nb)
+    m_order = morton(cent)
+    for name, order in (("body", body_order), ("morton", m_order)):
+        for size in (2, 4, 5, 8):
+            print(f"aggregates <= {size} in 63-row chunks, {name} order (1e-10, 1e-3, aggregates):",
+                  chunked(size, 63, order))
+    # handshake pairing as a kernel would do it: every row picks its most
+    # strongly coupled partner among the rows of its own CTA chunk (63 rows)
+    # that are still unpaired; mutual picks pair up; `passes` rounds
+    def handshake(chunk, passes):
+        mate = -np.ones(nb, dtype=int)
+        S = np.zeros((nb, nb))
+        for w, i, j in edges:
+            S[i, j] = S[j, i] = w
+        for _ in range(passes):
+            pick = -np.ones(nb, dtype=int)
+            for i in range(nb):
+                if mate[i] >= 0:
+                    continue
+                c0 = (i // chunk) * chunk
+                cand = [j for j in range(c0, min(nb, c0 + chunk)) if j != i and mate[j] < 0 and S[i, j] > 0]
+                if cand:
+                    pick[i] = max(cand, key=lambda j: (S[i, j], -j))
+            for i in range(nb):
+                j = pick[i]
+                if j >= 0 and pick[j] == i:
+                    mate[i] = j
+        Minv = np.zeros_like(A)
+        for i in range(nb):
+            if mate[i] < 0:
+                Minv[6 * i:6 * i + 6, 6 * i:6 * i + 6] = blocks[i]
+            elif i < mate[i]:
+                idx = np.r_[6 * i:6 * i + 6, 6 * mate[i]:6 * mate[i] + 6]
+                Minv[np.ix_(idx, idx)] = np.linalg.inv(A[np.ix_(idx, idx)])
+        return (pcg(A, b, lambda r: Minv @ r), pcg(A, b, lambda r: Minv @ r, tol=1e-3),
+                int((mate >= 0).sum()))
+
+    for chunk in (63, nb):
+        for passes in (1, 3):
+            print(f"handshake pairs in {chunk}-row chunks, {passes} passes (1e-10, 1e-3, paired rows):",
+                  handshake(chunk, passes))
+    # contiguous index chunks as blocks (what a warp- or CTA-local exact solve
+    # would give: the kernel's rows are the dynamic bodies in body order, a
+    # warp owns 5 consecutive rows), to a tight and to the inexact-Newton
+    # relative residual
+    for chunk in (1, 2, 5, 10, 63):
         Minv = np.zeros_like(A)
         for s0 in range(0, nb, chunk):
             idx = np.arange(6 * s0, 6 * min(nb, s0 + chunk))
             Minv[np.ix_(idx, idx)] = np.linalg.inv(A[np.ix_(idx, idx)])
-        print(f"block-Jacobi on contiguous {chunk}-body chunks:", pcg(A, b, lambda r: Minv @ r))
+        print(f"block-Jacobi on contiguous {chunk}-body chunks (1e-10, 1e-3):",
+              pcg(A, b, lambda r: Minv @ r), pcg(A, b, lambda r: Minv @ r, tol=1e-3))
 
 
 if __name__ == "__main__":
