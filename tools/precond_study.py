@@ -188,6 +188,17 @@ def main():
 
     body_order = np.arange(nb)
     m_order = morton(cent)
+    # the simplest warp-block preconditioner: rows in Morton order, the exact
+    # inverse of every warp's 5 consecutive rows (30x30), no aggregation pass
+    for name, order in (("body", body_order), ("morton", m_order)):
+        for w in (5, 10):
+            Minv = np.zeros_like(A)
+            for s0 in range(0, nb, w):
+                rows = order[s0:s0 + w]
+                idx = np.concatenate([np.arange(6 * i, 6 * i + 6) for i in rows])
+                Minv[np.ix_(idx, idx)] = np.linalg.inv(A[np.ix_(idx, idx)])
+            print(f"exact {w}-row blocks of consecutive rows, {name} order (1e-10, 1e-3):",
+                  pcg(A, b, lambda r: Minv @ r), pcg(A, b, lambda r: Minv @ r, tol=1e-3))
     for name, order in (("body", body_order), ("morton", m_order)):
         for size in (2, 4, 5, 8):
             print(f"aggregates <= {size} in 63-row chunks, {name} order (1e-10, 1e-3, aggregates):",
