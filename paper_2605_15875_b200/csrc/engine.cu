@@ -1559,6 +1559,7 @@ std::vector<TraceRow> Engine::take_trace() {
 
 void Engine::run_frames(int n, FrameStats* stats) {
     for (int f = 0; f < n; ++f) {
+        const NvtxRange range(W_ == 0 ? "dabd.frame_reference" : "dabd.frame_admm");
         const auto t0 = std::chrono::steady_clock::now();
         FrameStats st = W_ == 0 ? frame_reference() : frame_admm(static_cast<int>(frame_counter_));
         st.t_frame = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1942,6 +1943,7 @@ int Engine::admm_attempt_device(int frame, int attempt, double h, double tol, in
                               nodes_inc_[5]};
     prof.mark(1, s_);
 
+    const NvtxRange range("dabd.solve.admm_attempt");
     const auto t0 = std::chrono::steady_clock::now();
     CUDA_CHECK(cudaGraphLaunch(admm_exec_, s_));
     CUDA_CHECK(cudaMemcpyAsync(ctrl_h_.get(), ctrl_.get(), sizeof(FrameCtrl), cudaMemcpyDeviceToHost, s_));
@@ -2276,6 +2278,7 @@ FrameStats Engine::frame_admm(int frame) {
                 std::vector<double> earliest(P_, 2.0), rl(P_, 0.0), sl(P_, 0.0);
                 try {
                     if (!fail.empty()) throw Error(fail);
+                    const NvtxRange range("dabd.coll");
                     const auto tc = std::chrono::steady_clock::now();
                     rloc_.zero(s_);
                     sloc_.zero(s_);
@@ -2353,6 +2356,7 @@ FrameStats Engine::frame_admm(int frame) {
                     // sees every partition's (dq, r, s, earliest TOI).
                     std::vector<double> rec = {static_cast<double>(P_), fail.empty() ? 0.0 : 1.0};
                     for (int p = 0; p < P_; ++p) rec.insert(rec.end(), {dq[p], rl[p], sl[p], earliest[p]});
+                    const NvtxRange range("dabd.sync.fanin");
                     const auto ts = std::chrono::steady_clock::now();
                     const std::vector<double> all = allgather_host(rec);
                     st.t_sync += seconds_since(ts); // controller fan-in (runtime.cpp:586-601)
@@ -2432,6 +2436,7 @@ FrameStats Engine::frame_admm(int frame) {
                 SolverRestore restore(*this);
                 for (int grows = 0, exact = 0;;) {
                     try {
+                        const NvtxRange range("dabd.solve");
                         const auto tn = std::chrono::steady_clock::now();
                         r = solve();
                         st.t_solve += seconds_since(tn); // runtime.cpp:466-468
@@ -2486,6 +2491,7 @@ FrameStats Engine::frame_admm(int frame) {
         launch_commit(ds_.view(), I, ibody_.get(), ipart_.get(), ianc_.get(), bmask_.get(),
                       iq_.get(), iznext_.get(), q_start_.get(), h, q_.get(), qd_.get(), s_);
         if (distributed_) {
+            const NvtxRange range("dabd.sync.commit");
             const auto ts = std::chrono::steady_clock::now();
             commit_gather();
             sync();

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <map>
@@ -98,6 +99,18 @@ class KernelTimer {
     std::vector<Pair> pending_;
     std::map<std::string, Stat> stats_;
     double bytes_ = 0.0;
+};
+
+// NVTX range over a host scope (header-only NVTX v3: a no-op unless a tool
+// such as ncu --nvtx or Nsight Systems is attached). The frame phases carry
+// the names of the reference's timers: frame, solve (runtime.cpp:466-468),
+// coll (consensus + merge gate, 399-402), sync (fan-in / commit, 586-601).
+class NvtxRange {
+  public:
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 } // namespace dabd_gpu
