@@ -538,6 +538,71 @@ __device__ __forceinline__ void accept_trial_range(const SolverView& sv, int i0,
     }
 }
 
+// accept_trial_range run by the last block alone: the partitions' accept
+// decisions staged in shared memory (alpha, or -1 when rejected), then
+// kApplyU instances per thread in flight (index loads, then state loads,
+// then stores), so the L2 round trips of a thread's instances overlap
+// instead of chaining through the stores (~8 x 3 dependent trips per thread
+// on pile-1k otherwise). Same predicate and arithmetic as eval_q(qmode 2).
+constexpr int kApplyU = 2;
+__device__ __forceinline__ void accept_trial_block(const SolverView& sv, double* s_alpha) {
+    const int P = sv.n_parts;
+    for (int p = threadIdx.x; p < P; p += blockDim.x)
+        s_alpha[p] = sv.ps[p].accepted ? sv.ps[p].alpha : -1.0;
+    __syncthreads();
+    for (int base = threadIdx.x; base < sv.n_inst; base += kApplyU * blockDim.x) {
+        int row[kApplyU];
+        double alpha[kApplyU];
+#pragma unroll
+        for (int u = 0; u < kApplyU; ++u) {
+            const int i = base + u * blockDim.x;
+            row[u] = -1;
+            alpha[u] = 0.0;
+            if (i < sv.n_inst) {
+                const int r = sv.irow[i];
+                const double a = s_alpha[sv.ipart[i] - sv.part_base];
+                if (a >= 0.0 && r >= 0) {
+                    row[u] = r;
+                    alpha[u] = a;
+                }
+            }
+        }
+        double q[kApplyU][6], dq[kApplyU][6];
+#pragma unroll
+        for (int u = 0; u < kApplyU; ++u) {
+            if (row[u] < 0) continue;
+            load6(sv.iq + 6 * (base + u * blockDim.x), q[u]);
+            load6(sv.x + 6 * row[u], dq[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kApplyU; ++u) {
+            if (row[u] < 0) continue;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) q[u][k] = xadd(q[u][k], xmul(alpha[u], dq[u][k]));
+            store6(sv.iq + 6 * (base + u * blockDim.x), q[u]);
+        }
+    }
+}
+
+// sum_{k in [k0, k1), k = k0 + lane mod 32} part[k * P + p] in ascending k
+// (the order of the plain strided loop, so the same bits), loads issued
+// eight at a time ahead of the dependent adds.
+__device__ __forceinline__ double fold_partials(const double* part, int P, int p, int k0, int k1, int lane) {
+    double s = 0.0;
+    for (int k = k0 + lane; k < k1; k += 8 * 32) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int kk = k + 32 * u;
+            v[u] = kk < k1 ? __ldcg(part + static_cast<size_t>(kk) * P + p) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (k + 32 * u < k1) s += v[u];
+    }
+    return s;
+}
+
 __global__ void __launch_bounds__(kB) k_energy(SolverView sv, EnergyArgs ea) {
     __shared__ double sh[kB];
     __shared__ bool last;
@@ -592,10 +657,8 @@ __global__ void __launch_bounds__(kB) k_energy(SolverView sv, EnergyArgs ea) {
     __threadfence();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int p = warp; p < P; p += kB / 32) {
-        double sr = 0.0, sk = 0.0;
-        for (int k = lane; k < ea.ncr; k += 32) sr += __ldcg(ea.partial + static_cast<size_t>(k) * P + p);
-        for (int k = ea.ncr + lane; k < static_cast<int>(gridDim.x); k += 32)
-            sk += __ldcg(ea.partial + static_cast<size_t>(k) * P + p);
+        double sr = fold_partials(ea.partial, P, p, 0, ea.ncr, lane);
+        double sk = fold_partials(ea.partial, P, p, ea.ncr, static_cast<int>(gridDim.x), lane);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             sr += __shfl_xor_sync(0xffffffffu, sr, off);
@@ -613,7 +676,7 @@ __global__ void __launch_bounds__(kB) k_energy(SolverView sv, EnergyArgs ea) {
     scalar_block(sv.ps, P, kOpAccept, ea.ctrl, ea.hd, 0.0, 0, sv.err);
     if (ea.apply) {
         __syncthreads(); // the accept decisions of this block are visible to it
-        accept_trial_range(sv, threadIdx.x, blockDim.x);
+        accept_trial_block(sv, sh);
     }
     if (!ea.tail) return;
     __syncthreads();
