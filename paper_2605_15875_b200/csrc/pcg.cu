@@ -1671,13 +1671,22 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
             for (int k = 0; k < 4; ++k) atomicAdd(&sv.perf->phase[16 + k], qi[k + 1] - qi[k]);
         }
     }
+    if (sv.perf && it > 0) {
+        // algorithmic bytes of this partition's solve: every CTA counts the
+        // blocks of its own rows (one row per thread, warp sums; integer-valued
+        // doubles, so the atomic order does not matter) instead of one thread
+        // walking all the partition's rows after the solve
+        const int r = r0 + static_cast<int>(threadIdx.x);
+        const int nb = r < r1 ? sv.ell_cnt[r] + 1 : 0;
+        const int nw = __reduce_add_sync(0xffffffffu, nb);
+        const int rw = __reduce_add_sync(0xffffffffu, r < r1 ? 1 : 0);
+        if ((threadIdx.x & 31) == 0 && rw > 0)
+            atomicAdd(&sv.perf->bytes, static_cast<double>(it) * (288.0 * nw + 504.0 * rw));
+        for (int rr = r + kCT; rr < r1; rr += kCT) // chunks wider than the CTA (not on the fused path)
+            atomicAdd(&sv.perf->bytes, static_cast<double>(it) * (288.0 * (sv.ell_cnt[rr] + 1) + 504.0));
+    }
     if (sv.perf && threadIdx.x == 0) {
-        if (rank == 0) { // algorithmic bytes of this partition's solve
-            int nblk = 0;
-            for (int r = R0; r < R1; ++r) nblk += sv.ell_cnt[r] + 1;
-            atomicAdd(&sv.perf->bytes, static_cast<double>(it) * (288.0 * nblk + 504.0 * (R1 - R0)));
-            atomicAdd(&sv.perf->iters, static_cast<unsigned long long>(it));
-        }
+        if (rank == 0) atomicAdd(&sv.perf->iters, static_cast<unsigned long long>(it));
         if (blockIdx.x == 0) {
             unsigned long long t1;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
