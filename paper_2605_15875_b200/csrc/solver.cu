@@ -43,18 +43,6 @@ __device__ __forceinline__ bool part_flag(const SolverView& sv, int p, int which
     return which == 0 ? s.active != 0 : (which == 1 ? s.searching != 0 : true);
 }
 
-// body_aabb (body.cpp:136-161) of body b at q inflated by margin: the boxes
-// k_inst_boxes stores, recomputed where a kernel needs only a few of them.
-__device__ __forceinline__ Box body_box_at(const SceneView& sc, int b, const double* q, double margin) {
-    Box bx{{DBL_MAX, DBL_MAX}, {-DBL_MAX, -DBL_MAX}};
-    for (int v = sc.vstart[b]; v < sc.vstart[b + 1]; ++v) {
-        const V2 x = world_point(q, rest_of(sc, v));
-        bx.lo = vmin(bx.lo, x);
-        bx.hi = vmax(bx.hi, x);
-    }
-    return inflate(bx, margin);
-}
-
 // ---------------------------------------------------------------------------
 // Body terms: value (+ gradient + PSD-clamped 6x6 block) per dynamic row
 // (objective.cpp:117-141, 143-167).
@@ -482,14 +470,15 @@ __device__ __forceinline__ double cand_value(const SolverView& sv, unsigned long
                                              int qmode, int which) {
     int a, b, v, e;
     fmt.unpack(key, a, b, v, e);
+    const int ba = sv.ibody[a], bb = sv.ibody[b]; // beside the partition index, not after its flag
     const int p = sv.ipart[a] - sv.part_base;
     if (!part_flag(sv, p, which)) return 0.0;
-    const int ba = sv.ibody[a], bb = sv.ibody[b];
     if (sv.sc.is_static[ba] && sv.sc.is_static[bb]) return 0.0;
     double qa[6], qb[6];
     eval_q(sv, a, qmode, qa);
     eval_q(sv, b, qmode, qb);
-    if (!overlaps(body_box_at(sv.sc, ba, qa, sv.d_hat), body_box_at(sv.sc, bb, qb, sv.d_hat))) return 0.0;
+    // (the body-box test of the broad phase is implied by the point / edge box
+    // test below, see k_contact_select, and is not repeated)
     const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
     const Box pb = point_box(sv.sc, qa, qa, false, vf);
     const Box eb = edge_box(sv.sc, qb, qb, false, ef, sv.d_hat);
@@ -747,15 +736,21 @@ __global__ void __launch_bounds__(kB) k_contact_select(SolverView sv, ContactVie
         if (t < nn) {
             int a, b, v, e;
             cv.fmt.unpack(cv.key[t], a, b, v, e);
+            // the instances' bodies load beside the partition index instead of
+            // after the partition's flag (two L2 trips off every thread's chain)
+            const int ba = sv.ibody[a], bb = sv.ibody[b];
             p = sv.ipart[a] - sv.part_base;
             if (sv.ps[p].active) {
-                const int ba = sv.ibody[a], bb = sv.ibody[b];
                 const bool ss = sv.sc.is_static[ba] && sv.sc.is_static[bb];
                 const double* qa = sv.iq + 6 * a;
                 const double* qb = sv.iq + 6 * b;
-                if (!ss && (box ? overlaps(box[a], box[b])
-                                : overlaps(body_box_at(sv.sc, ba, qa, sv.d_hat),
-                                           body_box_at(sv.sc, bb, qb, sv.d_hat)))) {
+                // box == nullptr: no body-box test. It is implied by the point /
+                // edge box test: pb = {P} lies in a's d_hat-inflated body box and
+                // eb in b's (the same world points, the min / max over a superset
+                // of vertices, and the inflation rounds monotonically), so pb and
+                // eb overlapping makes the body boxes overlap; dropping it only
+                // removes the two 4-vertex box chains from every thread.
+                if (!ss && (!box || overlaps(box[a], box[b]))) {
                     const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
                     const Box pb = point_box(sv.sc, qa, qa, false, vf);
                     const Box eb = edge_box(sv.sc, qb, qb, false, ef, sv.d_hat);
@@ -921,14 +916,16 @@ __global__ void __launch_bounds__(128) k_assemble(SolverView sv, ContactView cv,
     // the transposed entries (BL = TR^T)
     const int t0 = 6 * (e0 % 6) + e0 / 6, t1 = has1 ? 6 * (e1 % 6) + e1 / 6 : 0;
     for (int r = gw; r < sv.n_rows; r += nw) {
-        const int p = sv.rpart[r] - sv.part_base;
-        if (!sv.ps[p].active) continue;
+        // the row's instance, segment bounds and body terms load beside the
+        // partition flag, not after it (the flag only decides whether to store)
         const int i = sv.rinst[r];
+        const int p = sv.rpart[r] - sv.part_base;
+        const int a0 = cv.aoff[i], a1 = cv.aoff[i + 1];
+        const int b0 = cv.boff[i], b1 = cv.boff[i + 1];
         double d0 = sv.rdiag[36 * r + e0];
         double d1 = has1 ? sv.rdiag[36 * r + e1] : 0.0;
         double g = lane < 6 ? sv.rgrad[6 * r + lane] : 0.0;
-        const int a0 = cv.aoff[i], a1 = cv.aoff[i + 1];
-        const int b0 = cv.boff[i], b1 = cv.boff[i + 1];
+        if (!sv.ps[p].active) continue;
         if (a1 - a0 <= 32 && b1 - b0 <= 32) { // the usual row: warp-parallel metadata
             assemble_row_fast(sv, cv, r, a0, a1, b0, b1, lane, e0, e1, t0, t1, has1, d0, d1, g, row_trace);
             continue;
@@ -1292,10 +1289,12 @@ __global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, cons
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += gridDim.x * blockDim.x) {
         int a, b, v, e;
         fmt.unpack(keys[t], a, b, v, e);
+        // boxes and bodies load beside the partition index, not after its flag
+        const Box ba0 = box0[a], bb0 = box0[b];
+        const int ba = sv.ibody[a], bb = sv.ibody[b];
         const int p = sv.ipart[a] - sv.part_base;
         if (!part_flag(sv, p, which)) continue;
-        if (!overlaps(box0[a], box0[b])) continue;
-        const int ba = sv.ibody[a], bb = sv.ibody[b];
+        if (!overlaps(ba0, bb0)) continue;
         const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
         const double* qa0 = q0 + 6 * a;
         const double* qa1 = q1 + 6 * a;
