@@ -878,7 +878,7 @@ void Engine::enq_list_ensure(const double* q1, bool fused_ccd) {
     if (fused_ccd)
         launch_ccd_prep(view(), qref_.get(), iskin_.get(), iskin_next_.get(),
                         skin_min_ * frame_params_.d_hat, skin_grow_, lstate_.get(), h, graph ? 1 : 0,
-                        box_.get(), s_);
+                        nullptr, s_); // k_ccd runs without body boxes (the swept point/edge test implies them)
     else
         launch_list_check(ds_.view(), iview(iq_.get(), q1), qref_.get(), iqt_.get(), iskin_.get(),
                           iskin_next_.get(), skin_min_ * frame_params_.d_hat, skin_grow_,
@@ -981,10 +981,43 @@ void Engine::enq_newton_head(int max_iters) {
 // CCD bound over [q, q + dq] on the swept superset (newton.cpp:38-42).
 void Engine::enq_newton_ccd() {
     SolverView v = view();
-    if (pcg_fused()) { // k_ccd_prep [IF rebuild] k_ccd(+kOpAlphaMax): 2 launches
-        enq_list_ensure(iqtry_.get(), true);
-        launch_ccd(v, det_.keys(), cap_, det_.d_count(), cfmt_, box_.get(), iq_.get(), iqtry_.get(), 0,
-                   nullptr, s_, ctrl_.get(), &hd_);
+    if (pcg_fused()) {
+        // k_ccd forms q + dq itself (q1 == nullptr) and needs no body boxes, so
+        // it runs beside k_ccd_prep (skin check of the list) as a second branch:
+        // [k_ccd(+kOpAlphaMax) || k_ccd_prep] IF(rebuild) { rebuild, toi reset,
+        // k_ccd(+kOpAlphaMax) over the new list }. The first k_ccd's result is
+        // discarded when the list was stale (rare); decisions are the same.
+        const bool graph = hd_.graph != 0;
+        const unsigned long long h = graph ? new_cond_handle() : 0ull;
+        auto ccd = [&](cudaStream_t st) {
+            launch_ccd(view(), det_.keys(), cap_, det_.d_count(), cfmt_, nullptr, iq_.get(), nullptr, 0,
+                       nullptr, st, ctrl_.get(), &hd_);
+        };
+        const cudaStream_t side = side_stream();
+        CUDA_CHECK(cudaEventRecord(ev_fork_, s_));
+        CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork_, 0));
+        ccd(side);
+        launch_ccd_prep(v, qref_.get(), iskin_.get(), iskin_next_.get(), skin_min_ * frame_params_.d_hat,
+                        skin_grow_, lstate_.get(), h, graph ? 1 : 0, nullptr, s_);
+        CUDA_CHECK(cudaEventRecord(ev_join_, side));
+        CUDA_CHECK(cudaStreamWaitEvent(s_, ev_join_, 0));
+        auto rerun = [&] {
+            enq_list_rebuild();
+            launch_toi_reset(ps_.get(), P_, ctrl_.get(), s_);
+            ccd(s_);
+        };
+        if (graph) {
+            // launch accounting: executed rebuilds count the plain rebuild's
+            // nodes (the toi reset and the second k_ccd go uncounted)
+            const long long keep = rebuild_nodes_;
+            add_cond_node(h, false, cap_level_ + 1, rerun, false);
+            if (keep > 0) rebuild_nodes_ = keep;
+        } else {
+            CUDA_CHECK(cudaMemcpyAsync(lstate_h_.get(), lstate_.get(), sizeof(ListState),
+                                       cudaMemcpyDeviceToHost, s_));
+            CUDA_CHECK(cudaStreamSynchronize(s_));
+            if (lstate_h_[0].rebuild) rerun();
+        }
         return;
     }
     launch_make_trial(v, false, 1.0, 0, s_);

@@ -52,6 +52,7 @@ void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, con
                 double* earliest_override, cudaStream_t s, FrameCtrl* alpha_max_ctrl = nullptr,
                 const CondHandles* hd = nullptr);
 // k_make_trial(alpha 1) + k_list_check + swept k_inst_boxes (margin 0) in one launch.
+void launch_toi_reset(PartState* ps, int P, FrameCtrl* ctrl, cudaStream_t s);
 void launch_ccd_prep(const SolverView& sv, const double* qref, const double* skin, double* skin_next,
                      double s_min, double grow, ListState* ls, unsigned long long cond, int graph,
                      Box* box, cudaStream_t s);

@@ -1096,6 +1096,7 @@ __global__ void k_ccd_prep(SolverView sv, const double* qref, const double* skin
         store6(sv.iq_try + 6 * i, q1);
         const int b = sv.ibody[i];
         bad |= list_check_one(sv.sc, b, i, q0, q1, qref, sv.iqt, skin, skin_next, s_min, grow);
+        if (!box) continue; // k_ccd without body boxes (see there)
         Box bx{{DBL_MAX, DBL_MAX}, {-DBL_MAX, -DBL_MAX}};
         for (int v = sv.sc.vstart[b]; v < sv.sc.vstart[b + 1]; ++v) {
             const V2 rr = rest_of(sv.sc, v);
@@ -1261,6 +1262,14 @@ __global__ void k_make_trial(SolverView sv, int use_alpha_field, double fixed_al
     }
 }
 
+// toi_earliest of every partition back to "no impact" (kOpIterBegin's reset)
+// before k_ccd re-runs over a rebuilt candidate list; the discarded first
+// k_ccd's kOpAlphaMax is taken out of the step-body execution count.
+__global__ void k_toi_reset(PartState* ps, int P, FrameCtrl* ctrl) {
+    for (int p = threadIdx.x; p < P; p += blockDim.x) ps[p].toi_earliest = 2.0;
+    if (ctrl && threadIdx.x == 0) --ctrl->exec_step;
+}
+
 __global__ void k_dq_inf(SolverView sv) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < sv.n_rows; r += gridDim.x * blockDim.x) {
         const int p = sv.rpart[r] - sv.part_base;
@@ -1281,6 +1290,23 @@ struct CcdFinish {
     unsigned* ticket;
 };
 
+// The CCD end point of instance i, q0 + 1.0 dq for a row of an active
+// partition (else q0): k_ccd_prep's arithmetic, so k_ccd can form it itself
+// (q1 == nullptr) and run beside k_ccd_prep instead of after it.
+__device__ __forceinline__ void ccd_end_point(const SolverView& sv, int i, const double (&q0)[6],
+                                              double (&q1)[6]) {
+    const int r = sv.irow[i];
+    const int p = sv.ipart[i] - sv.part_base;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) q1[k] = q0[k];
+    if (r >= 0 && sv.ps[p].active) {
+        double dq[6];
+        load6(sv.x + 6 * r, dq);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) q1[k] = xadd(q1[k], xmul(1.0, dq[k]));
+    }
+}
+
 __global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, const int* dn,
                       KeyFmt fmt, const Box* box0, const double* q0, const double* q1, int which,
                       double* earliest_override, CcdFinish fin) {
@@ -1289,17 +1315,28 @@ __global__ void k_ccd(SolverView sv, const unsigned long long* keys, int n, cons
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += gridDim.x * blockDim.x) {
         int a, b, v, e;
         fmt.unpack(keys[t], a, b, v, e);
-        // boxes and bodies load beside the partition index, not after its flag
-        const Box ba0 = box0[a], bb0 = box0[b];
+        // bodies load beside the partition index, not after its flag.
+        // box0 == nullptr: no swept body-box test. It is implied by the swept
+        // point / edge box test below (the same world points at q0 and q1, the
+        // min / max over a superset of the body's vertices, margin 0), so it
+        // only filters early; k_ccd_prep then writes no boxes.
         const int ba = sv.ibody[a], bb = sv.ibody[b];
         const int p = sv.ipart[a] - sv.part_base;
         if (!part_flag(sv, p, which)) continue;
-        if (!overlaps(ba0, bb0)) continue;
+        if (box0 && !overlaps(box0[a], box0[b])) continue;
         const int vf = sv.sc.vstart[ba] + v, ef = sv.sc.vstart[bb] + e;
-        const double* qa0 = q0 + 6 * a;
-        const double* qa1 = q1 + 6 * a;
-        const double* qb0 = q0 + 6 * b;
-        const double* qb1 = q1 + 6 * b;
+        // both configurations in registers; the end points formed here when
+        // q1 == nullptr
+        double qa0[6], qa1[6], qb0[6], qb1[6];
+        load6(q0 + 6 * a, qa0);
+        load6(q0 + 6 * b, qb0);
+        if (q1) {
+            load6(q1 + 6 * a, qa1);
+            load6(q1 + 6 * b, qb1);
+        } else {
+            ccd_end_point(sv, a, qa0, qa1);
+            ccd_end_point(sv, b, qb0, qb1);
+        }
         const Box pb = point_box(sv.sc, qa0, qa1, true, vf);
         const Box eb = edge_box(sv.sc, qb0, qb1, true, ef, 0.0);
         if (!overlaps(pb, eb)) continue;
@@ -1492,6 +1529,10 @@ void launch_ccd(const SolverView& sv, const unsigned long long* keys, int n, con
     DABD_LAUNCH("k_ccd", s,
                 k_ccd<<<grid_for(std::max(n, 1), kB), kB, 0, s>>>(sv, keys, n, dn, fmt, box0, q0, q1, which,
                                                                    earliest_override, fin));
+}
+
+void launch_toi_reset(PartState* ps, int P, FrameCtrl* ctrl, cudaStream_t s) {
+    DABD_LAUNCH("k_toi_reset", s, k_toi_reset<<<1, 64, 0, s>>>(ps, P, ctrl));
 }
 
 void launch_ccd_prep(const SolverView& sv, const double* qref, const double* skin, double* skin_next,
