@@ -1071,7 +1071,18 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
     __syncthreads();
     // any overflow in the cluster selects the barrier path everywhere
     if (threadIdx.x == 0 && sc.fallback) atomicOr(&cl.map_shared_rank(&sc, 0)->fallback, 1);
-    cluster_barrier(); // send lists, requests, trace partials and fallback flags complete
+    if (a.warm) { // the warm start's p1 (vm1) and p2 (vm0): published by the barrier below
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int lrw = warp * kRowsPerWarp + slot + g * kCW * kRowsPerWarp;
+            if (lane < 30 && lrw < nr) {
+                vm1[6 * lrw + comp] = wp1[g];
+                vm0[6 * lrw + comp] = wp2[g];
+                if (a.warm > 1) a.pa[6 * static_cast<size_t>(r0 + lrw) + comp] = wp1[g]; // the next solve's p2
+            }
+        }
+    }
+    cluster_barrier(); // send lists, requests, trace partials, fallback flags (and p1 / p2) complete
     if constexpr (PH) cs[3] = clock64();
     if (a.fused && act && rank == 0 && threadIdx.x == 0) { // kOpEps (newton.cpp:20-24)
         sv.ps[p].trace = trace_p;
@@ -1248,17 +1259,10 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         // (p1 from vm1, p2 from vm0) and one cluster reduction, rank order.
         double p1[G], p2[G], ap1[G], ap2[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const size_t e = 6 * static_cast<size_t>(r0 + lrg[g]) + comp;
+        for (int g = 0; g < G; ++g) { // in vm1 / vm0 since the plan barrier
             p1[g] = wp1[g];
             p2[g] = wp2[g];
-            if (on[g]) {
-                vm1[6 * lrg[g] + comp] = p1[g];
-                vm0[6 * lrg[g] + comp] = p2[g];
-                if (a.warm > 1) a.pa[e] = p1[g]; // becomes the next solve's p2
-            }
         }
-        cluster_barrier();
         double l[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -1629,19 +1633,28 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
         if (atomicAdd(a.ticket, 1u) == static_cast<unsigned>(sv.n_parts - 1)) {
             *a.ticket = 0u;
             __threadfence();
-            volatile PartState* vps = sv.ps;
-            int any_act = 0, any_srch = 0;
+            // every partition's fields read from L2 (ld.global.cg, after the
+            // fence that follows the ticket) in one batch per partition, not
+            // as a chain of volatile loads and read-modify-writes
+            PartState* ps = sv.ps;
+            int any_act = 0, any_srch = 0, tot = 0;
             for (int q = 0; q < sv.n_parts; ++q) {
-                if (a.ctrl) a.ctrl->pcg_total += vps[q].pcg_iters;
-                if (vps[q].active && vps[q].dq_inf < vps[q].tol) {
-                    vps[q].final_update = vps[q].dq_inf;
-                    vps[q].converged = 1;
-                    vps[q].active = 0;
+                const int itq = __ldcg(&ps[q].pcg_iters), actq = __ldcg(&ps[q].active),
+                          srchq = __ldcg(&ps[q].searching);
+                const double dqq = __ldcg(&ps[q].dq_inf), tolq = __ldcg(&ps[q].tol);
+                tot += itq;
+                bool still = actq != 0;
+                if (still && dqq < tolq) {
+                    ps[q].final_update = dqq;
+                    ps[q].converged = 1;
+                    ps[q].active = 0;
+                    still = false;
                 }
-                any_act |= vps[q].active != 0;
-                any_srch |= vps[q].searching != 0;
+                any_act |= still;
+                any_srch |= srchq != 0;
             }
             if (a.ctrl) {
+                a.ctrl->pcg_total += tot;
                 a.ctrl->any_active = any_act;
                 a.ctrl->any_searching = any_srch;
             }
