@@ -1263,14 +1263,36 @@ void Engine::cap_newton(int max_iters, double tol, int level) {
     // trial, and the PCG epilogue closes the loop when nothing stays active
     const bool folded_tail = pcg_fused() && n_inst_ <= kFuseAcceptMaxInst;
     tail_max_iters_ = folded_tail ? max_iters : 0;
+    // flat fused body: no IF(step) node around the CCD and the line search.
+    // After a converged PCG the CCD finds no active partition, its
+    // kOpAlphaMax clears `searching` and the WHILE(ls) body never runs, so the
+    // node only saved two short launches once per solve while costing its own
+    // evaluation on every iteration. Launch accounting keeps the step level
+    // (kOpAlphaMax counts exec_step once per executed CCD).
+    static const bool flat_env = [] {
+        const char* e = std::getenv("DABD_GPU_STEP_IF");
+        return !(e && e[0] == '1');
+    }();
+    const bool flat = flat_env && pcg_fused();
     add_cond_node(hd_.newton, true, level, [&] {
-        hd_.step = new_cond_handle(); // set by kOpNewtonCheck inside the head
-        enq_newton_head(max_iters);
-        add_cond_node(hd_.step, false, level + 1, [&] {
+        auto step_body = [&] {
             hd_.ls = new_cond_handle();
             enq_newton_ccd();
             add_cond_node(hd_.ls, true, level + 2, [&] { enq_ls_trial(); });
-        });
+        };
+        if (flat) {
+            hd_.step = 0;
+            hd_.has_step = 0;
+            enq_newton_head(max_iters);
+            const long long before = launch_counter().load();
+            step_body();
+            if (level + 1 < 8) nodes_inc_[level + 1] = launch_counter().load() - before;
+        } else {
+            hd_.step = new_cond_handle(); // set by kOpNewtonCheck inside the head
+            hd_.has_step = 1;
+            enq_newton_head(max_iters);
+            add_cond_node(hd_.step, false, level + 1, step_body);
+        }
         if (!folded_tail)
             launch_scalar(ps_.get(), P_, kOpNewtonTail, ctrl_.get(), hd_, 0.0, max_iters, err_.get(), s_,
                           iter_reset());

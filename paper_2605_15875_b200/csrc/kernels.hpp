@@ -118,6 +118,7 @@ struct CondHandles {
     unsigned long long admm = 0, newton = 0, step = 0, ls = 0; // cudaGraphConditionalHandle values
     unsigned long long gate = 0, solve = 0; // multi-partition ADMM frame: IF(k > 1), IF(continue)
     int graph = 0;
+    int has_step = 0; // an IF(step) node exists for `step` (not in the flat fused Newton body)
 };
 
 struct PcgFuse {

@@ -1659,7 +1659,8 @@ __global__ void __launch_bounds__(kCT) k_pcg_cluster(SolverView sv, PcgArgs a, i
                 a.ctrl->any_searching = any_srch;
             }
             if (a.hd.graph) {
-                cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.hd.step), any_act ? 1u : 0u);
+                if (a.hd.has_step)
+                    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.hd.step), any_act ? 1u : 0u);
                 if (a.close_loop && !any_act) // the folded tail never runs: close the Newton loop here
                     cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.hd.newton), 0u);
             }

@@ -132,7 +132,7 @@ __device__ __forceinline__ void scalar_block(PartState* ps, int P, int op, Frame
             if (op == kOpAccept) ++ctrl->exec_ls;
         }
         if (op == kOpReset || op == kOpNewtonTail) set_cond(hd.newton, any_act, hd.graph);
-        if (op == kOpNewtonCheck) set_cond(hd.step, any_act, hd.graph);
+        if (op == kOpNewtonCheck && hd.has_step) set_cond(hd.step, any_act, hd.graph);
         if (op == kOpAlphaMax || op == kOpAccept) set_cond(hd.ls, any_srch, hd.graph);
     }
 }
