@@ -1274,6 +1274,10 @@ void Engine::cap_newton(int max_iters, double tol, int level) {
         return !(e && e[0] == '1');
     }();
     const bool flat = flat_env && pcg_fused();
+    static const bool flat_ls = [] { // DABD_GPU_LS_FIRST_FLAT=0: the first trial inside WHILE(ls) too
+        const char* e = std::getenv("DABD_GPU_LS_FIRST_FLAT");
+        return !(e && e[0] == '0');
+    }();
     add_cond_node(hd_.newton, true, level, [&] {
         auto step_body = [&] {
             hd_.ls = new_cond_handle();
@@ -1285,7 +1289,22 @@ void Engine::cap_newton(int max_iters, double tol, int level) {
             hd_.has_step = 0;
             enq_newton_head(max_iters);
             const long long before = launch_counter().load();
-            step_body();
+            if (flat_ls) {
+                // the first line-search trial unconditionally (every iteration
+                // tries alpha_max; with nothing searching it evaluates nothing
+                // and its kOpAccept leaves every partition as it was), then
+                // WHILE(ls) only for the halvings: the loop node is entered by
+                // ~13% of the iterations
+                hd_.ls = new_cond_handle();
+                enq_newton_ccd();
+                const long long b1 = launch_counter().load();
+                enq_ls_trial();
+                const long long first = launch_counter().load() - b1;
+                launch_counter() -= first; // counted per executed trial through exec_ls x the ls body
+                add_cond_node(hd_.ls, true, level + 2, [&] { enq_ls_trial(); });
+            } else {
+                step_body();
+            }
             if (level + 1 < 8) nodes_inc_[level + 1] = launch_counter().load() - before;
         } else {
             hd_.step = new_cond_handle(); // set by kOpNewtonCheck inside the head
