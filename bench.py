@@ -62,7 +62,12 @@ def _ncu_traffic(kernel: str = "k_pcg_cluster"):
     `ncu --set full` summary under profiles/ (tools/ncu_summary.py output)."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel}_ncu_full.txt")))
+    def tag_key(path):  # r01 < r01b < r02a < r02z < r02aa < r02bk (spreadsheet-column order)
+        tag = os.path.basename(path).split("_")[0]
+        rnd, suf = tag[:3], tag[3:]
+        return (rnd, len(suf), suf)
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_{kernel}_ncu_full.txt")), key=tag_key)
     if not files:
         return None, None
     units = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
